@@ -1,0 +1,100 @@
+"""ctypes binding of the in-tree C-ABI library ``libbrk_sm100.so`` (include/brk.h).
+
+The product path has no CPU fallback: if the shared library is missing or no
+CUDA device is present, every compute entry point raises ``BrkNativeError``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+LIB_NAME = "libbrk_sm100.so"
+LIB_PATH = Path(__file__).resolve().parent / LIB_NAME
+
+BRK_OK = 0
+BRK_ERR_CONTRACT = 1
+BRK_ERR_CUDA = 2
+
+BRK_F32 = 0
+BRK_BF16 = 1
+BRK_COMPUTE_TF32 = 0
+BRK_COMPUTE_BF16 = 1
+
+_c_int = ctypes.c_int
+_c_i64 = ctypes.c_int64
+_c_f = ctypes.c_float
+_vp = ctypes.c_void_p
+
+# name -> (restype, argtypes); the single source of truth for the exports
+# tests/test_capi_symbols.py checks against include/brk.h.
+SIGNATURES: dict[str, tuple] = {
+    "brk_last_error": (ctypes.c_char_p, []),
+    "brk_version": (_c_int, []),
+    "brk_launch_count": (ctypes.c_uint64, []),
+    "brk_brgemm_addr": (
+        _c_int,
+        [_vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_i64, _c_i64, _c_i64,
+         _c_f, _c_f, _c_int, _c_int, _c_int, _vp],
+    ),
+    "brk_brgemm_offs": (
+        _c_int,
+        [_vp, _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_i64, _c_i64, _c_i64,
+         _c_f, _c_f, _c_int, _c_int, _c_int, _vp],
+    ),
+    "brk_brgemm_stride": (
+        _c_int,
+        [_vp, _vp, _c_i64, _c_i64, _vp, _c_int, _c_i64, _c_i64, _c_i64, _c_int, _c_int, _c_int,
+         _c_int, _c_i64, _c_i64, _c_i64, _c_f, _c_f, _c_int, _c_int, _c_int, _vp],
+    ),
+}
+
+
+class BrkNativeError(RuntimeError):
+    """The native library is missing, failed to load, or returned a CUDA error."""
+
+
+_lib = None
+
+
+def load(path: os.PathLike | None = None) -> ctypes.CDLL:
+    """Load (once) and return the C-ABI library; raise loudly if it is missing."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = Path(path) if path is not None else LIB_PATH
+    if not p.exists():
+        raise BrkNativeError(
+            f"{p} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(or `make -C paper_1906_06440_b200/csrc`). There is no CPU fallback."
+        )
+    try:
+        lib = ctypes.CDLL(str(p))
+    except OSError as exc:  # pragma: no cover - depends on the box
+        raise BrkNativeError(f"failed to load {p}: {exc}") from exc
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if path is None:
+        _lib = lib
+    return lib
+
+
+def last_error() -> str:
+    return load().brk_last_error().decode("utf-8", "replace")
+
+
+def check(rc: int, contract_exc=ValueError) -> None:
+    """Map a C-ABI return code to the reference's exception classes."""
+    if rc == BRK_OK:
+        return
+    msg = last_error()
+    if rc == BRK_ERR_CONTRACT:
+        raise contract_exc(msg)
+    raise BrkNativeError(msg)
+
+
+def launch_count() -> int:
+    return int(load().brk_launch_count())

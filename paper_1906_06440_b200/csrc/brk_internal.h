@@ -1,0 +1,44 @@
+// brk_internal.h — shared host/device declarations behind the C-ABI (include/brk.h).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/brk.h"
+
+namespace brk {
+
+enum EntryMode : int { kModeAddr = 0, kModeOffs = 1, kModeStride = 2 };
+
+// Parameters of one generic BRGEMM launch (see brk_brgemm_generic.cu).
+struct GenericParams {
+  int mode;    // EntryMode
+  int n_jobs;  // number of independent output blocks C_j
+  int m, n, k, batch;
+  int64_t lda, ldb, ldc;
+  float alpha, beta;
+  int in_bf16;   // A/B storage: 0 = fp32, 1 = bf16
+  int out_bf16;  // C storage:   0 = fp32, 1 = bf16
+  // mode == kModeAddr: device tables of n_jobs*batch block addresses
+  const void* const* a_ptrs;
+  const void* const* b_ptrs;
+  // mode == kModeOffs / kModeStride: base pointers
+  const void* a_base;
+  const void* b_base;
+  // mode == kModeOffs: device tables of n_jobs*batch element offsets
+  const int64_t* a_offs;
+  const int64_t* b_offs;
+  // mode == kModeStride: block i of job j at base + j*jstride + i*stride (elements)
+  int64_t stride_a, stride_b;
+  int64_t jstride_a, jstride_b, jstride_c;
+  // outputs: mode Addr/Offs use c_ptrs[n_jobs]; mode Stride uses c_base + j*jstride_c
+  void* const* c_ptrs;
+  void* c_base;
+};
+
+int launch_brgemm_generic(const GenericParams& p, int compute_tf32, cudaStream_t stream);
+
+// error reporting (thread-local message, returned by brk_last_error())
+int set_error(int code, const char* msg);
+int set_cuda_error(cudaError_t err, const char* where);
+
+}  // namespace brk
