@@ -21,6 +21,7 @@
 #ifndef BRK_H_
 #define BRK_H_
 
+#include <stddef.h>
 #include <stdint.h>
 
 #if defined(__GNUC__)
@@ -82,6 +83,30 @@ BRK_API int brk_brgemm_stride(const void* a_base, const void* b_base, int64_t st
                       int64_t jstride_c, int m, int n, int k, int batch, int64_t lda, int64_t ldb,
                       int64_t ldc, float alpha, float beta, int in_dtype, int out_dtype,
                       int compute, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Fully-connected layer passes on the reference's blocked layouts
+ * (fc.py:99-163; tensor.py:143-158, 237-247):
+ *   x, dx, mask : [N/b_n][C/b_c][b_n][b_c]      w : [K/b_k][C/b_c][b_c][b_k]
+ *   y, dz       : [N/b_n][K/b_k][b_n][b_k]      dw: like w, fp32
+ * Engine path: bf16 storage, b_n=b_c=b_k=64, N, C, K multiples of 128.
+ * ------------------------------------------------------------------------- */
+/* Replaces brkernels.fc.fc_forward (fc.py:99-163): y = act(W x + bias);
+ * act: 0 identity, 1 relu, 2 sigmoid (fc.py:29-40); bias (fp32, K) may be NULL. */
+BRK_API int brk_fc_fwd(const void* x, const void* w, const float* bias, void* y, int N, int C, int K,
+                       int b_n, int b_c, int b_k, int act, int dtype, void* stream);
+/* Backward-data (north star): dx = (W^T dz) * (mask > 0); mask may be NULL. */
+BRK_API int brk_fc_bwd_data(const void* dz, const void* w, const void* mask, void* dx, int N, int C,
+                            int K, int b_n, int b_c, int b_k, int dtype, void* stream);
+/* Weight update (north star): dw = dz x^T (fp32); if w_sgd != NULL also
+ * w_sgd -= lr * dw (bf16 weights, fused in the epilogue). */
+BRK_API int brk_fc_upd(const void* x, const void* dz, float* dw, void* w_sgd, float lr, int N, int C,
+                       int K, int b_n, int b_c, int b_k, int dtype, void* stream);
+/* Bias gradient (north star): dz_out = dy * (y > 0) if y != NULL; db[K] = sum over N of dz.
+ * Deterministic.  workspace: brk_fc_bias_grad_workspace(K) bytes, zeroed once before first use. */
+BRK_API int brk_fc_bias_grad(const void* dy, const void* y, void* dz_out, float* db, void* workspace,
+                             int N, int K, int b_n, int b_k, void* stream);
+BRK_API size_t brk_fc_bias_grad_workspace(int K);
 
 #ifdef __cplusplus
 }

@@ -1,5 +1,6 @@
 // brk_internal.h — shared host/device declarations behind the C-ABI (include/brk.h).
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -34,6 +35,8 @@ struct GenericParams {
   void* const* c_ptrs;
   void* c_base;
 };
+
+extern std::atomic<uint64_t> g_launches;
 
 int launch_brgemm_generic(const GenericParams& p, int compute_tf32, cudaStream_t stream);
 

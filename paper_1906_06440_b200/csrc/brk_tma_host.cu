@@ -1,0 +1,51 @@
+// brk_tma_host.cu — host-side TMA tensor-map encoding without linking libcuda:
+// cuTensorMapEncodeTiled is fetched once through cudaGetDriverEntryPoint.
+#include <cstdio>
+#include <mutex>
+
+#include "brk_internal.h"
+#include "brk_tma_host.h"
+
+namespace brk {
+
+namespace {
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                              CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                              CUtensorMapFloatOOBfill);
+EncodeFn g_encode = nullptr;
+std::once_flag g_once;
+}  // namespace
+
+int encode_tmap(CUtensorMap* out, const void* ptr, bool bf16, int ndims, const uint64_t* dims,
+                const uint64_t* strides_elems, const uint32_t* box) {
+  std::call_once(g_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<EncodeFn>(fn);
+  });
+  if (g_encode == nullptr) return set_error(BRK_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const size_t esz = bf16 ? 2 : 4;
+  cuuint64_t gdim[5], gstride[4];
+  cuuint32_t bdim[5], estride[5];
+  for (int d = 0; d < ndims; ++d) {
+    gdim[d] = dims[d];
+    bdim[d] = box[d];
+    estride[d] = 1;
+    if (d > 0) gstride[d - 1] = strides_elems[d] * esz;
+  }
+  CUresult r = g_encode(out, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                        ndims, const_cast<void*>(ptr), gdim, gstride, bdim, estride,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    char buf[256];
+    std::snprintf(buf, sizeof(buf), "cuTensorMapEncodeTiled failed (CUresult %d, ndims %d)", (int)r, ndims);
+    return set_error(BRK_ERR_CONTRACT, buf);
+  }
+  return BRK_OK;
+}
+
+}  // namespace brk
