@@ -1,0 +1,375 @@
+"""Benchmark: MLP 4 x FC(1024 -> 1024) + bias + ReLU, minibatch 2048 per GPU,
+fwd / bwd-data / weight-update (+ bias grad + SGD) — BASELINE.json config 2.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+Prints ONE JSON line (rank 0).  `value` is whole-job TFLOP/s (GEMM flops
+3 * 2NCK per layer, the reference's flops_fc accounting, bench.py:112-113)
+over device-timed steps with inputs resident in HBM; `e2e` repeats it through
+the public MLP.train_step call with host->device copies of the step's input
+and gradient from pinned memory and a device->host read of the result.
+L2 is flushed (256 MiB write) between timed steps.  Multi-GPU: one process
+per GPU (torchrun), data parallel, weak scaling (N=2048 per GPU), NCCL
+all-reduce of dW/db per layer; time = max over ranks of device time.
+
+`--impl reference` times the reference algorithm's CPU implementation (the
+oracle port of the blocked FC BRGEMM loops, oracle/brk_oracle.py, all host
+threads) on one FC layer's fwd+bwd+upd at the full size, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+LAYERS, WIDTH, BATCH = 4, 1024, 2048
+METRIC = "TFLOP/s & % of B200 dense peak: ResNet-50 conv, LSTM cell, MLP fwd/bwd/upd"
+UNIT = "TFLOP/s"
+WORKLOAD = "mlp4x_fc1024_n2048_fwd_bwd_upd_bias_relu_sgd"
+
+
+def peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text()), "measured"
+    except (OSError, ValueError):
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def base_config(n_gpus):
+    return {"workload": WORKLOAD, "layers": LAYERS, "C": WIDTH, "K": WIDTH, "N_per_gpu": BATCH,
+            "global_batch": BATCH * n_gpus, "blocking": "b_n=b_c=b_k=64 (reference blocked FC layouts)",
+            "bias": True, "activation": "relu", "sgd": "fused (upd epilogue / bias-grad kernel)",
+            "parallelism": f"dp{n_gpus}", "l2": "flushed between timed steps (256 MiB write)"}
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler
+# ---------------------------------------------------------------------------
+_REASON_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+                0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+                0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+
+class ClockSampler:
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 3:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+                bits = int(parts[2], 16)
+            except ValueError:
+                continue
+            for bit, name in _REASON_BITS.items():
+                if bits & bit:
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        loaded = [v for v in sm if v > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# reference arm (CPU)
+# ---------------------------------------------------------------------------
+def run_reference(args, n_gpus, rank):
+    if rank != 0:
+        return
+    import numpy as np
+
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import brk_oracle as orc
+
+    threads = orc.cpu_threads()
+    rng = np.random.default_rng([0, 202])
+    b = 64
+    w = (rng.uniform(-1, 1, (WIDTH, WIDTH)) / 32).astype(np.float32)
+    x = rng.uniform(-1, 1, (BATCH, WIDTH)).astype(np.float32)
+    dy = rng.uniform(-1, 1, (BATCH, WIDTH)).astype(np.float32)
+    bias = rng.uniform(-0.1, 0.1, WIDTH).astype(np.float32)
+    wb = w.reshape(WIDTH // b, b, WIDTH // b, b).transpose(0, 2, 3, 1).copy()
+    xb = x.reshape(BATCH // b, b, WIDTH // b, b).transpose(0, 2, 1, 3).copy()
+    dyb = dy.reshape(BATCH // b, b, WIDTH // b, b).transpose(0, 2, 1, 3).copy()
+
+    def step():
+        yb = orc.fc_forward_blocked(wb, xb, "relu", bias, workers=threads)
+        orc.fc_backward_blocked(wb, xb, yb, dyb, "relu", workers=threads)
+
+    flops = 3 * 2 * BATCH * WIDTH * WIDTH
+    for _ in range(args.warmup):
+        step()
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        step()
+        times.append(time.perf_counter() - t0)
+    sec = statistics.fmean(times)
+    value = flops / sec / 1e12
+    sample = (f"one FC layer (C=K={WIDTH}, N={BATCH}, bias+ReLU) fwd + bwd-data + weight-update + "
+              f"bias-grad per step, reference blocked BRGEMM algorithm (oracle port, float64 block "
+              f"accumulation), {threads} threads")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n_gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64-accumulate/f32-storage", "data": "synthetic",
+            "config": base_config(n_gpus),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_sample():
+    """Bounded CPU sample for the GPU arm's cpu_baseline key (~10-30 s)."""
+    import numpy as np
+
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import brk_oracle as orc
+
+    threads = orc.cpu_threads()
+    rng = np.random.default_rng([0, 202])
+    b = 64
+    w = (rng.uniform(-1, 1, (WIDTH, WIDTH)) / 32).astype(np.float32)
+    x = rng.uniform(-1, 1, (BATCH, WIDTH)).astype(np.float32)
+    dy = rng.uniform(-1, 1, (BATCH, WIDTH)).astype(np.float32)
+    wb = w.reshape(WIDTH // b, b, WIDTH // b, b).transpose(0, 2, 3, 1).copy()
+    xb = x.reshape(BATCH // b, b, WIDTH // b, b).transpose(0, 2, 1, 3).copy()
+    dyb = dy.reshape(BATCH // b, b, WIDTH // b, b).transpose(0, 2, 1, 3).copy()
+    reps, t_total = 0, 0.0
+    while t_total < 10.0 and reps < 20:
+        t0 = time.perf_counter()
+        yb = orc.fc_forward_blocked(wb, xb, "relu", None, workers=threads)
+        orc.fc_backward_blocked(wb, xb, yb, dyb, "relu", workers=threads)
+        t_total += time.perf_counter() - t0
+        reps += 1
+    value = reps * 3 * 2 * BATCH * WIDTH * WIDTH / t_total / 1e12
+    return {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{reps} x one FC layer fwd+bwd+upd (C=K={WIDTH}, N={BATCH}) with the reference's blocked "
+                      f"BRGEMM algorithm (oracle port, f64 block accumulation), {t_total:.1f} s, {threads} threads"}
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def kernel_roofline(mlp, torch, peak_tflops):
+    """Average device duration of each engine GEMM launch (graph of 10 launches, CUDA events on
+    the launching stream) -> achieved TFLOP/s for the dominant kernel."""
+    from paper_1906_06440_b200 import _lib
+
+    lib, n, c = mlp.lib, mlp.N, mlp.C
+    B = 64
+    stream = torch.cuda.Stream()
+    calls = {
+        "fwd": lambda s: lib.brk_fc_fwd(mlp.y[0].data_ptr(), mlp.w[0].data_ptr(), mlp.bias[0].data_ptr(),
+                                        mlp.y[1].data_ptr(), n, c, c, B, B, B, 1, _lib.BRK_BF16, s),
+        "bwd": lambda s: lib.brk_fc_bwd_data(mlp.dz[2].data_ptr(), mlp.w[1].data_ptr(), mlp.y[1].data_ptr(),
+                                             mlp.dz[1].data_ptr(), n, c, c, B, B, B, _lib.BRK_BF16, s),
+        "upd": lambda s: lib.brk_fc_upd(mlp.y[0].data_ptr(), mlp.dz[1].data_ptr(), mlp.dw[0].data_ptr(), None,
+                                        0.0, n, c, c, B, B, B, _lib.BRK_BF16, s),
+    }
+    out = {}
+    reps = 10
+    for name, fn in calls.items():
+        with torch.cuda.stream(stream):
+            fn(stream.cuda_stream)
+        stream.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            for _ in range(reps):
+                fn(stream.cuda_stream)
+        with torch.cuda.stream(stream):
+            for _ in range(3):
+                g.replay()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(5):
+                g.replay()
+            e1.record(stream)
+        e1.synchronize()
+        out[name] = e0.elapsed_time(e1) / (5 * reps) * 1e-3
+    flops = 2.0 * n * c * c
+    avg = statistics.fmean(out.values())
+    achieved = flops / avg / 1e12
+    traffic = None
+    tf = ROOT / "profiles" / "engine_traffic.json"
+    if tf.exists():
+        try:
+            traffic = json.loads(tf.read_text()).get("bytes_per_launch")
+        except ValueError:
+            traffic = None
+    return {"bound": "tensor", "achieved": achieved, "peak": peak_tflops, "unit": "TFLOP/s",
+            "frac": achieved / peak_tflops, "traffic": traffic,
+            "kernel": "brk engine_kernel (TMA->tcgen05.mma->TMEM, bf16, fp32 acc)",
+            "flops_per_launch": flops,
+            "us_per_launch": {k: v * 1e6 for k, v in out.items()}}
+
+
+def run_gpu(args, n_gpus, rank, local_rank, pg):
+    import torch
+
+    from paper_1906_06440_b200 import _lib
+    from paper_1906_06440_b200.mlp import MLP, flops_per_step
+
+    torch.cuda.set_device(local_rank)
+    pk, pk_kind = peaks()
+    mlp = MLP(layers=LAYERS, width=WIDTH, batch=BATCH, lr=1e-4, seed=rank, process_group=pg)
+    g = torch.Generator(device="cpu").manual_seed(100 + rank)
+    blk = lambda t: t.reshape(BATCH // 64, 64, WIDTH // 64, 64).permute(0, 2, 1, 3).contiguous()  # noqa: E731
+    x_host = blk((torch.rand(BATCH, WIDTH, generator=g) * 2 - 1).bfloat16()).pin_memory()
+    dy_host = blk(((torch.rand(BATCH, WIDTH, generator=g) * 2 - 1) * 1e-2).bfloat16()).pin_memory()
+    mlp.load_input(x_host.cuda(), dy_host.cuda())
+    torch.cuda.synchronize()
+    single = pg is None
+    if single:
+        mlp.capture()
+        run = mlp.replay
+    else:
+        run = mlp.step
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    flops = flops_per_step(LAYERS, BATCH, WIDTH, WIDTH)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if pg is not None:
+            import torch.distributed as dist
+            dist.barrier(group=pg)
+
+    def timed(step_fn, steps):
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        barrier()
+        torch.cuda.synchronize()
+        for i in range(steps):
+            flush.fill_(float(i))                     # L2 flush, outside the timed events
+            evs[i][0].record(stream)
+            step_fn()
+            evs[i][1].record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        return sum(a.elapsed_time(b) for a, b in evs) * 1e-3 / steps
+
+    def max_over_ranks(v):
+        if pg is None:
+            return v
+        import torch.distributed as dist
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=pg)
+        return float(t.item())
+
+    with ClockSampler(local_rank) as clk:
+        # clock ramp + warm-up (at least W steps, and ~1 s of device work)
+        t_end = time.time() + 1.0
+        w = 0
+        while w < args.warmup or time.time() < t_end:
+            run()
+            w += 1
+        torch.cuda.synchronize()
+        sec = max_over_ranks(timed(run, args.steps))
+        # end-to-end through the public API: H2D inputs + step + D2H result, per step
+        out_host = torch.empty(WIDTH, dtype=torch.float32, pin_memory=True)
+        e2e_sec = max_over_ranks(timed(lambda: mlp.train_step(x_host, dy_host, out_host), args.steps))
+    clocks = clk.summary()
+    launches = mlp.launches_per_step
+    value = n_gpus * flops / sec / 1e12
+    e2e_value = n_gpus * flops / e2e_sec / 1e12
+    if rank != 0:
+        return
+    roof = kernel_roofline(mlp, torch, pk["bf16_tflops"])
+    roof["peak_source"] = f"{pk_kind} bf16 dense (burst, kernel timed alone)"
+    cpu = cpu_baseline_sample()
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n_gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (uniform, seeded; random-init weights)",
+        "config": base_config(n_gpus),
+        "pct_of_peak": value / n_gpus / pk["bf16_tflops_sustained"],
+        "peak_note": f"{pk_kind} bf16 sustained {pk['bf16_tflops_sustained']} TFLOP/s per GPU",
+        "flops_per_step_per_gpu": flops,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 2 * BATCH * WIDTH * 2,
+                "d2h_bytes_per_step": WIDTH * 4, "ms_per_step": e2e_sec * 1e3},
+        "gpu_launches": launches * args.steps,
+        "launches_per_step": launches,
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "clocks": clocks,
+        "lib_launch_counter": _lib.launch_count(),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["brk", "reference"], default="brk")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    n_gpus = world if world > 1 else args.gpus
+    if args.impl == "reference":
+        run_reference(args, n_gpus, rank)
+        return
+    pg = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        pg = dist.group.WORLD
+    try:
+        run_gpu(args, n_gpus, rank, local_rank, pg)
+    finally:
+        if pg is not None:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -68,6 +68,33 @@ BRK_API int brk_brgemm_addr(const void* const* a_ptrs, const void* const* b_ptrs
                     int64_t ldc, float alpha, float beta, int in_dtype, int out_dtype,
                     int compute, void* stream);
 
+/* Grouped address-variant BRGEMM with general block strides and a fused
+ * epilogue — the batch-list interface the FC/LSTM/conv drivers use for block
+ * factors the TMA engine does not serve (reference drivers fc.py:139-160,
+ * lstm.py:268-317, cnn.py:290-320 issue one brgemm per output block; here all
+ * output blocks of a pass go in one launch).
+ *   A_ji element (kk, col) at a_ptrs[j*batch+i][kk*a_sk + col*a_sm]
+ *   B_ji element (row, kk) at b_ptrs[j*batch+i][row*b_sn + kk*b_sk]
+ *   C_j  element (row, col) at c_ptrs[j][row*ldc + col]
+ *   C_j = act(alpha*sum_i B_ji@A_ji + beta*C_j + bias[bias_offs[j]+col]) * (mask_j > 0)
+ * act: 0 identity, 1 relu, 2 sigmoid.  bias / mask_ptrs may be NULL; mask_j
+ * has the layout and dtype of C_j.  All tables are device arrays. */
+typedef struct brk_grouped_desc {
+  int n_jobs, m, n, k, batch;
+  int64_t a_sk, a_sm, b_sn, b_sk, ldc;
+  float alpha, beta;
+  int in_dtype, out_dtype, compute;
+  const void* const* a_ptrs;
+  const void* const* b_ptrs;
+  void* const* c_ptrs;
+  const float* bias;
+  const int64_t* bias_offs;
+  int act;
+  const void* const* mask_ptrs;
+} brk_grouped_desc;
+
+BRK_API int brk_brgemm_grouped(const brk_grouped_desc* desc, void* stream);
+
 /* BRGEMM, offset variant (north star; no reference function — equivalent to
  * the address variant with A_ji = a_base + a_offs[j*batch+i] elements). */
 BRK_API int brk_brgemm_offs(const void* a_base, const void* b_base, const int64_t* a_offs,
@@ -102,11 +129,19 @@ BRK_API int brk_fc_bwd_data(const void* dz, const void* w, const void* mask, voi
  * w_sgd -= lr * dw (bf16 weights, fused in the epilogue). */
 BRK_API int brk_fc_upd(const void* x, const void* dz, float* dw, void* w_sgd, float lr, int N, int C,
                        int K, int b_n, int b_c, int b_k, int dtype, void* stream);
-/* Bias gradient (north star): dz_out = dy * (y > 0) if y != NULL; db[K] = sum over N of dz.
- * Deterministic.  workspace: brk_fc_bias_grad_workspace(K) bytes, zeroed once before first use. */
+/* Bias gradient (north star): dz_out = dy * (y > 0) if y != NULL; db[K] = sum over N of dz;
+ * if bias_sgd != NULL also bias_sgd -= lr * db (fused SGD).  Deterministic.
+ * workspace: brk_fc_bias_grad_workspace(K) bytes, zeroed once before first use. */
 BRK_API int brk_fc_bias_grad(const void* dy, const void* y, void* dz_out, float* db, void* workspace,
-                             int N, int K, int b_n, int b_k, void* stream);
+                             int N, int K, int b_n, int b_k, float* bias_sgd, float lr, void* stream);
 BRK_API size_t brk_fc_bias_grad_workspace(int K);
+/* Bias gradient for any block factors / dtype (dy, y, dz_out in the
+ * [N/b_n][K/b_k][b_n][b_k] layout): dz_out = dy*(y>0) if y != NULL; db = sum_n dz. */
+BRK_API int brk_colsum_blocked(const void* dy, const void* y, void* dz_out, float* db, int N, int K,
+                               int b_n, int b_k, int dtype, void* stream);
+/* SGD apply (north-star training step after the dW allreduce): w -= lr * dw, n elements,
+ * w in BRK_F32 or BRK_BF16 storage, dw fp32 in the same layout. */
+BRK_API int brk_sgd_apply(void* w, const float* dw, float lr, int64_t n, int w_dtype, void* stream);
 
 #ifdef __cplusplus
 }

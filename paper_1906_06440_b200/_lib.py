@@ -38,6 +38,17 @@ SIGNATURES: dict[str, tuple] = {
         [_vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_i64, _c_i64, _c_i64,
          _c_f, _c_f, _c_int, _c_int, _c_int, _vp],
     ),
+    "brk_brgemm_grouped": (_c_int, [_vp, _vp]),
+    "brk_fc_fwd": (_c_int, [_vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int,
+                            _c_int, _c_int, _vp]),
+    "brk_fc_bwd_data": (_c_int, [_vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int,
+                                 _c_int, _vp]),
+    "brk_fc_upd": (_c_int, [_vp, _vp, _vp, _vp, _c_f, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int,
+                            _c_int, _vp]),
+    "brk_fc_bias_grad": (_c_int, [_vp, _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _c_f, _vp]),
+    "brk_fc_bias_grad_workspace": (ctypes.c_size_t, [_c_int]),
+    "brk_colsum_blocked": (_c_int, [_vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp]),
+    "brk_sgd_apply": (_c_int, [_vp, _vp, _c_f, _c_i64, _c_int, _vp]),
     "brk_brgemm_offs": (
         _c_int,
         [_vp, _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_i64, _c_i64, _c_i64,
@@ -49,6 +60,19 @@ SIGNATURES: dict[str, tuple] = {
          _c_int, _c_i64, _c_i64, _c_i64, _c_f, _c_f, _c_int, _c_int, _c_int, _vp],
     ),
 }
+
+
+class GroupedDesc(ctypes.Structure):
+    """Mirror of ``brk_grouped_desc`` (include/brk.h)."""
+
+    _fields_ = [
+        ("n_jobs", _c_int), ("m", _c_int), ("n", _c_int), ("k", _c_int), ("batch", _c_int),
+        ("a_sk", _c_i64), ("a_sm", _c_i64), ("b_sn", _c_i64), ("b_sk", _c_i64), ("ldc", _c_i64),
+        ("alpha", _c_f), ("beta", _c_f),
+        ("in_dtype", _c_int), ("out_dtype", _c_int), ("compute", _c_int),
+        ("a_ptrs", _vp), ("b_ptrs", _vp), ("c_ptrs", _vp),
+        ("bias", _vp), ("bias_offs", _vp), ("act", _c_int), ("mask_ptrs", _vp),
+    ]
 
 
 class BrkNativeError(RuntimeError):

@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const Gener
 #pragma unroll
       for (int t = 0; t < kElems; ++t) {
         const int kk = k0 + c * kElems + t;
-        v[t] = (row < p.n && kk < p.k) ? load_in(e.b, static_cast<int64_t>(row) * p.ldb + kk, bf16_in)
+        v[t] = (row < p.n && kk < p.k) ? load_in(e.b, static_cast<int64_t>(row) * p.b_sn + static_cast<int64_t>(kk) * p.b_sk, bf16_in)
                                        : 0.0f;
       }
       *reinterpret_cast<uint4*>(a_op + canon_off(r, c)) = pack16<kTF32>(v);
@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const Gener
 #pragma unroll
       for (int t = 0; t < kElems; ++t) {
         const int kk = k0 + c * kElems + t;
-        v[t] = (col < p.m && kk < p.k) ? load_in(e.a, static_cast<int64_t>(kk) * p.lda + col, bf16_in)
+        v[t] = (col < p.m && kk < p.k) ? load_in(e.a, static_cast<int64_t>(kk) * p.a_sk + static_cast<int64_t>(col) * p.a_sm, bf16_in)
                                        : 0.0f;
       }
       *reinterpret_cast<uint4*>(b_op + canon_off(i, c)) = pack16<kTF32>(v);
@@ -189,6 +189,8 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const Gener
     c_ptr = static_cast<char*>(p.c_ptrs[job]);
   }
   const double alpha = p.alpha, beta = p.beta;
+  const float* bias_row = p.bias != nullptr ? p.bias + p.bias_offs[job] : nullptr;
+  const char* mask_ptr = p.mask_ptrs != nullptr ? static_cast<const char*>(p.mask_ptrs[job]) : nullptr;
   for (int c0 = 0; c0 < n_cols; c0 += 32) {
     uint32_t acc[32];
     if (steps > 0) {
@@ -210,6 +212,18 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const Gener
             const double old = p.out_bf16 ? __bfloat162float(reinterpret_cast<__nv_bfloat16*>(c_ptr)[off])
                                           : reinterpret_cast<float*>(c_ptr)[off];
             out += beta * old;
+          }
+          if (bias_row != nullptr) out += static_cast<double>(bias_row[col]);
+          if (p.act == 1) {
+            out = out > 0.0 ? out : 0.0;
+          } else if (p.act == 2) {
+            const double e = exp(-fabs(out));
+            out = out >= 0.0 ? 1.0 / (1.0 + e) : e / (1.0 + e);
+          }
+          if (mask_ptr != nullptr) {
+            const float mv = p.out_bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(mask_ptr)[off])
+                                        : reinterpret_cast<const float*>(mask_ptr)[off];
+            if (!(mv > 0.0f)) out = 0.0;
           }
           if (p.out_bf16) {
             reinterpret_cast<__nv_bfloat16*>(c_ptr)[off] = __float2bfloat16_rn(static_cast<float>(out));

@@ -57,6 +57,31 @@ using namespace brk;
 
 extern "C" {
 
+BRK_API int brk_brgemm_grouped(const brk_grouped_desc* d, void* stream) {
+  if (d == nullptr) return set_error(BRK_ERR_CONTRACT, "null descriptor");
+  int rc = check_common(d->m, d->n, d->k, d->batch, d->m, d->k, d->ldc, d->in_dtype, d->out_dtype,
+                        d->compute, d->n_jobs);
+  if (rc) return rc;
+  if (d->act < 0 || d->act > 2) return set_error(BRK_ERR_CONTRACT, "unknown activation");
+  if (d->n_jobs == 0 || d->m == 0 || d->n == 0) return BRK_OK;
+  if (d->c_ptrs == nullptr || (d->batch > 0 && (d->a_ptrs == nullptr || d->b_ptrs == nullptr)))
+    return set_error(BRK_ERR_CONTRACT, "null pointer table");
+  if (d->bias != nullptr && d->bias_offs == nullptr) return set_error(BRK_ERR_CONTRACT, "bias needs bias_offs");
+  GenericParams p{};
+  p.mode = kModeAddr;
+  p.n_jobs = d->n_jobs;
+  p.m = d->m; p.n = d->n; p.k = d->k; p.batch = d->batch;
+  p.lda = d->a_sk; p.ldb = d->b_sn; p.ldc = d->ldc;
+  p.a_sk = d->a_sk; p.a_sm = d->a_sm; p.b_sn = d->b_sn; p.b_sk = d->b_sk;
+  p.alpha = d->alpha; p.beta = d->beta;
+  p.in_bf16 = d->in_dtype == BRK_BF16;
+  p.out_bf16 = d->out_dtype == BRK_BF16;
+  p.a_ptrs = d->a_ptrs; p.b_ptrs = d->b_ptrs; p.c_ptrs = d->c_ptrs;
+  p.bias = d->bias; p.bias_offs = d->bias_offs; p.act = d->act;
+  p.mask_ptrs = d->mask_ptrs;
+  return run_generic(p, d->compute, stream);
+}
+
 const char* brk_last_error(void) { return g_last_error.c_str(); }
 
 int brk_version(void) { return 1; }
@@ -77,6 +102,7 @@ int brk_brgemm_addr(const void* const* a_ptrs, const void* const* b_ptrs, void* 
   p.n_jobs = n_jobs;
   p.m = m; p.n = n; p.k = k; p.batch = batch;
   p.lda = lda; p.ldb = ldb; p.ldc = ldc;
+  p.a_sk = lda; p.a_sm = 1; p.b_sn = ldb; p.b_sk = 1;
   p.alpha = alpha; p.beta = beta;
   p.in_bf16 = in_dtype == BRK_BF16;
   p.out_bf16 = out_dtype == BRK_BF16;
@@ -99,6 +125,7 @@ int brk_brgemm_offs(const void* a_base, const void* b_base, const int64_t* a_off
   p.n_jobs = n_jobs;
   p.m = m; p.n = n; p.k = k; p.batch = batch;
   p.lda = lda; p.ldb = ldb; p.ldc = ldc;
+  p.a_sk = lda; p.a_sm = 1; p.b_sn = ldb; p.b_sk = 1;
   p.alpha = alpha; p.beta = beta;
   p.in_bf16 = in_dtype == BRK_BF16;
   p.out_bf16 = out_dtype == BRK_BF16;
@@ -125,6 +152,7 @@ int brk_brgemm_stride(const void* a_base, const void* b_base, int64_t stride_a, 
   p.n_jobs = n_jobs;
   p.m = m; p.n = n; p.k = k; p.batch = batch;
   p.lda = lda; p.ldb = ldb; p.ldc = ldc;
+  p.a_sk = lda; p.a_sm = 1; p.b_sn = ldb; p.b_sk = 1;
   p.alpha = alpha; p.beta = beta;
   p.in_bf16 = in_dtype == BRK_BF16;
   p.out_bf16 = out_dtype == BRK_BF16;

@@ -275,8 +275,13 @@ template <int BN, bool kTF32>
 int launch_engine_t(const EngineParams& p, int grid, cudaStream_t stream) {
   using Cfg = EngineCfg<BN>;
   auto kern = engine_kernel<BN, kTF32>;
-  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
-  if (err != cudaSuccess) return set_cuda_error(err, "engine smem attribute");
+  static int attr_set = 0;  // per instantiation; the attribute is per-context state
+  cudaError_t err;
+  if (!attr_set) {
+    err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
+    if (err != cudaSuccess) return set_cuda_error(err, "engine smem attribute");
+    attr_set = 1;
+  }
   kern<<<grid, kThreads, Cfg::kSmem, stream>>>(p);
   err = cudaGetLastError();
   if (err != cudaSuccess) return set_cuda_error(err, "engine launch");

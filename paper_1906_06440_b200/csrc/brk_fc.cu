@@ -114,7 +114,8 @@ __global__ void __launch_bounds__(256) bias_grad_kernel(const __nv_bfloat16* dy,
                                                         const __nv_bfloat16* __restrict__ y,
                                                         __nv_bfloat16* dz_out,
                                                         float* __restrict__ db, float* __restrict__ partial,
-                                                        unsigned* __restrict__ counters, int N, int K) {
+                                                        unsigned* __restrict__ counters, int N, int K,
+                                                        float* __restrict__ bias, float lr) {
   const int kb = blockIdx.x, split = blockIdx.y;
   const int Kb = K / kB;
   const int tid = threadIdx.x;
@@ -161,6 +162,7 @@ __global__ void __launch_bounds__(256) bias_grad_kernel(const __nv_bfloat16* dy,
     float s = 0.0f;
     for (int sp = 0; sp < kSplit; ++sp) s += __ldcg(&partial[(static_cast<int64_t>(sp) * Kb + kb) * kB + tid]);
     db[kb * kB + tid] = s;
+    if (bias != nullptr) bias[kb * kB + tid] -= lr * s;
     if (tid == 0) counters[kb] = 0;  // self-reset for the next launch / graph replay
   }
 }
@@ -264,7 +266,7 @@ BRK_API int brk_fc_upd(const void* x, const void* dz, float* dw, void* w_sgd, fl
 // dz_out = dy * (y > 0) when y != NULL (dz_out may alias dy), db = column sums.
 // workspace: >= kSplit*K floats + K/64 unsigned counters (zero-initialised once).
 BRK_API int brk_fc_bias_grad(const void* dy, const void* y, void* dz_out, float* db, void* workspace,
-                             int N, int K, int b_n, int b_k, void* stream) {
+                             int N, int K, int b_n, int b_k, float* bias_sgd, float lr, void* stream) {
   if (b_n != kB || b_k != kB || N % (kSplit * 1) || N % kB || K % kB)
     return set_error(BRK_ERR_CONTRACT, "bias_grad needs b_n=b_k=64 and N, K multiples of 64");
   if (N % kSplit) return set_error(BRK_ERR_CONTRACT, "bias_grad needs N % 16 == 0");
@@ -274,7 +276,7 @@ BRK_API int brk_fc_bias_grad(const void* dy, const void* y, void* dz_out, float*
   g_launches.fetch_add(1);
   bias_grad_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(y),
-      static_cast<__nv_bfloat16*>(dz_out), db, partial, counters, N, K);
+      static_cast<__nv_bfloat16*>(dz_out), db, partial, counters, N, K, bias_sgd, lr);
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) return set_cuda_error(err, "bias_grad launch");
   return BRK_OK;

@@ -16,6 +16,9 @@ struct GenericParams {
   int n_jobs;  // number of independent output blocks C_j
   int m, n, k, batch;
   int64_t lda, ldb, ldc;
+  // element strides of one block: A element (kk, col) at a[kk*a_sk + col*a_sm],
+  // B element (row, kk) at b[row*b_sn + kk*b_sk]  (a_sk = lda, a_sm = 1 by default)
+  int64_t a_sk, a_sm, b_sn, b_sk;
   float alpha, beta;
   int in_bf16;   // A/B storage: 0 = fp32, 1 = bf16
   int out_bf16;  // C storage:   0 = fp32, 1 = bf16
@@ -34,6 +37,11 @@ struct GenericParams {
   // outputs: mode Addr/Offs use c_ptrs[n_jobs]; mode Stride uses c_base + j*jstride_c
   void* const* c_ptrs;
   void* c_base;
+  // fused epilogue: out = act(alpha*acc + beta*c + bias[bias_offs[j] + col])
+  int act;                  // 0 none, 1 relu, 2 sigmoid
+  const float* bias;        // may be null
+  const int64_t* bias_offs; // per job (device), used when bias != null
+  const void* const* mask_ptrs;  // per job, layout of C (ldc), dtype of C; out *= (mask > 0)
 };
 
 extern std::atomic<uint64_t> g_launches;

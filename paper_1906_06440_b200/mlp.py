@@ -1,0 +1,191 @@
+"""Multi-layer perceptron training step built from the FC passes (BASELINE config 2).
+
+One step = for every layer the paper's three passes (fwd, bwd-data, weight
+update) plus bias gradient and SGD, all on the BRGEMM engine:
+
+    fwd   y_l  = relu(W_l y_{l-1} + b_l)                       (brk_fc_fwd)
+    bwd   dz_L = dy * (y_L > 0), db_L, b_L -= lr db_L           (brk_fc_bias_grad)
+          dz_{l-1} = (W_l^T dz_l) * (y_{l-1} > 0)               (brk_fc_bwd_data, mask fused)
+          db_{l-1}, b_{l-1} -= lr db_{l-1}                      (brk_fc_bias_grad)
+          dx = W_1^T dz_1                                       (brk_fc_bwd_data)
+    upd   dW_l = dz_l y_{l-1}^T,  W_l -= lr dW_l                (brk_fc_upd, SGD fused)
+
+Layouts are the reference's blocked FC layouts with b_n = b_c = b_k = 64
+(activations [N_b][C_b][64][64], weights [K_b][C_b][64][64]); storage bf16,
+accumulation fp32 in TMEM, weight/bias gradients fp32.  The whole step is a
+fixed sequence of native launches on one stream, so it is captured once into
+a CUDA graph and replayed.
+
+Data parallel (``dist.py``): with a process group the per-layer dW/db are
+all-reduced (NCCL) before the SGD apply, bucketed per layer in reverse order.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+from ._device import require_cuda
+from .fc import Activation, FcParams
+from .tensor import BlockedTensor
+
+B = 64
+
+
+def flops_per_step(layers: int, n: int, c: int, k: int) -> int:
+    """GEMM flops of fwd + bwd-data + upd over all layers: 3 * 2NCK per layer."""
+    return layers * 3 * 2 * n * c * k
+
+
+class MLP:
+    """``layers`` x FC(width -> width) + ReLU on a minibatch of ``batch`` rows."""
+
+    def __init__(self, layers: int = 4, width: int = 1024, batch: int = 2048, lr: float = 1e-3,
+                 seed: int = 0, process_group=None, device: str = "cuda"):
+        torch = require_cuda()
+        if width % 128 or batch % 128:
+            raise ValueError("MLP engine path needs width and batch multiples of 128")
+        self.torch = torch
+        self.L, self.C, self.N, self.lr = layers, width, batch, lr
+        self.pg = process_group
+        g = torch.Generator(device="cpu").manual_seed(seed)
+        bf = torch.bfloat16
+        cb = width // B
+        nb = batch // B
+        self.w = []      # bf16 [Kb][Cb][64][64]
+        self.bias = []   # fp32 [K]
+        for _ in range(layers):
+            w = (torch.rand(width, width, generator=g) * 2 - 1) / np.sqrt(width)
+            self.w.append(w.reshape(cb, B, cb, B).permute(0, 2, 3, 1).contiguous().to(device, bf))
+            self.bias.append(((torch.rand(width, generator=g) * 2 - 1) * 0.1).to(device))
+        # activations: y[0] is the input, y[l] the output of layer l
+        self.y = [torch.empty(nb, cb, B, B, dtype=bf, device=device) for _ in range(layers + 1)]
+        self.dz = [torch.empty(nb, cb, B, B, dtype=bf, device=device) for _ in range(layers + 1)]
+        self.dy = torch.empty(nb, cb, B, B, dtype=bf, device=device)
+        self.dw = [torch.empty(cb, cb, B, B, dtype=torch.float32, device=device) for _ in range(layers)]
+        self.db = [torch.empty(width, dtype=torch.float32, device=device) for _ in range(layers)]
+        lib = _lib.load()
+        self.lib = lib
+        self.ws = [torch.zeros(lib.brk_fc_bias_grad_workspace(width), dtype=torch.uint8, device=device)
+                   for _ in range(layers)]
+        self.graph = None
+        self.launches_per_step = 0
+
+    # ------------------------------------------------------------------ params
+    def params(self, l: int) -> FcParams:
+        """Reference-API view of layer ``l`` (device bf16 weights)."""
+        w = BlockedTensor(self.w[l], n_outer=2, logical_dims={"k": (0, 3), "c": (1, 2)})
+        return FcParams(w=w, n=self.N, c=self.C, k=self.C, b_n=B, b_c=B, b_k=B,
+                        activation=Activation.RELU, bias=self.bias[l])
+
+    def load_input(self, x, dy) -> None:
+        """Copy a step's input and output-gradient (blocked, bf16) into the static buffers."""
+        self.y[0].copy_(x, non_blocking=True)
+        self.dy.copy_(dy, non_blocking=True)
+
+    # ------------------------------------------------------------------ passes
+    def _check(self, rc):
+        _lib.check(rc, RuntimeError)
+
+    def forward(self, stream: int) -> int:
+        lib, n, c = self.lib, self.N, self.C
+        for l in range(self.L):
+            self._check(lib.brk_fc_fwd(self.y[l].data_ptr(), self.w[l].data_ptr(), self.bias[l].data_ptr(),
+                                       self.y[l + 1].data_ptr(), n, c, c, B, B, B, 1, _lib.BRK_BF16, stream))
+        return self.L
+
+    def backward_update(self, stream: int, apply_sgd: bool = True) -> int:
+        """bwd-data + bias grad + weight update for all layers; returns launches issued."""
+        lib, n, c, L = self.lib, self.N, self.C, self.L
+        lr = self.lr if apply_sgd else 0.0
+        launches = 0
+        # top layer: dz_L = dy * (y_L > 0); db_L (+ bias SGD)
+        self._check(lib.brk_fc_bias_grad(self.dy.data_ptr(), self.y[L].data_ptr(), self.dz[L].data_ptr(),
+                                         self.db[L - 1].data_ptr(), self.ws[L - 1].data_ptr(), n, c, B, B,
+                                         self.bias[L - 1].data_ptr() if apply_sgd else None, lr, stream))
+        launches += 1
+        for l in range(L, 0, -1):
+            # bwd-data first (it reads W_l before the fused SGD rewrites it)
+            mask = self.y[l - 1].data_ptr() if l > 1 else None
+            self._check(lib.brk_fc_bwd_data(self.dz[l].data_ptr(), self.w[l - 1].data_ptr(), mask,
+                                            self.dz[l - 1].data_ptr(), n, c, c, B, B, B, _lib.BRK_BF16, stream))
+            launches += 1
+            self._check(lib.brk_fc_upd(self.y[l - 1].data_ptr(), self.dz[l].data_ptr(), self.dw[l - 1].data_ptr(),
+                                       self.w[l - 1].data_ptr() if apply_sgd else None, lr, n, c, c, B, B, B,
+                                       _lib.BRK_BF16, stream))
+            launches += 1
+            if l > 1:
+                self._check(lib.brk_fc_bias_grad(self.dz[l - 1].data_ptr(), None, None, self.db[l - 2].data_ptr(),
+                                                 self.ws[l - 2].data_ptr(), n, c, B, B,
+                                                 self.bias[l - 2].data_ptr() if apply_sgd else None, lr, stream))
+                launches += 1
+        return launches
+
+    def step(self, stream: int | None = None) -> int:
+        """One fwd/bwd/upd step on the current buffers (single GPU: SGD fused)."""
+        torch = self.torch
+        s = torch.cuda.current_stream().cuda_stream if stream is None else stream
+        if self.pg is None:
+            n = self.forward(s) + self.backward_update(s, apply_sgd=True)
+        else:
+            n = self.forward(s) + self.backward_update(s, apply_sgd=False)
+            n += self._allreduce_apply(s)
+        self.launches_per_step = n
+        return n
+
+    def _allreduce_apply(self, stream: int) -> int:
+        """DP exchange: allreduce(sum) dW/db per layer, then SGD with lr / world."""
+        import torch.distributed as dist
+
+        torch = self.torch
+        world = dist.get_world_size(self.pg)
+        launches = 0
+        for l in range(self.L - 1, -1, -1):
+            dist.all_reduce(self.dw[l], group=self.pg)
+            dist.all_reduce(self.db[l], group=self.pg)
+            scale = self.lr / world
+            self._check(self.lib.brk_sgd_apply(self.w[l].data_ptr(), self.dw[l].data_ptr(), scale,
+                                               self.dw[l].numel(), _lib.BRK_BF16, stream))
+            self._check(self.lib.brk_sgd_apply(self.bias[l].data_ptr(), self.db[l].data_ptr(), scale,
+                                               self.db[l].numel(), _lib.BRK_F32, stream))
+            launches += 2
+        del torch
+        return launches
+
+    # ------------------------------------------------------------------ graphs
+    def capture(self):
+        """Capture one single-GPU step into a CUDA graph (replay with ``replay``)."""
+        torch = self.torch
+        if self.pg is not None:
+            raise RuntimeError("graph capture is for the single-GPU step; DP steps call step()")
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            self.step(side.cuda_stream)  # warm: encodes tensor maps, sets smem attributes
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=side):
+            self.step(side.cuda_stream)
+        self.graph = g
+        return g
+
+    def replay(self):
+        self.graph.replay()
+
+    def train_step(self, x_host, dy_host, out_host=None):
+        """Public end-to-end step: H2D of the step's input and output gradient
+        (pinned host, blocked bf16), the fwd/bwd/upd step (graph replay when
+        captured), and a D2H read of the step's result (the last layer's bias
+        gradient) into ``out_host``.  Returns ``out_host``."""
+        torch = self.torch
+        self.y[0].copy_(x_host, non_blocking=True)
+        self.dy.copy_(dy_host, non_blocking=True)
+        if self.graph is not None:
+            self.graph.replay()
+        else:
+            self.step()
+        if out_host is None:
+            out_host = torch.empty(self.C, dtype=torch.float32, pin_memory=True)
+        out_host.copy_(self.db[self.L - 1], non_blocking=True)
+        return out_host
