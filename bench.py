@@ -205,9 +205,12 @@ def kernel_roofline(mlp, torch, peak_tflops):
         "fwd": lambda s: lib.brk_fc_fwd(mlp.y[0].data_ptr(), mlp.w[0].data_ptr(), mlp.bias[0].data_ptr(),
                                         mlp.y[1].data_ptr(), n, c, c, B, B, B, 1, _lib.BRK_BF16, s),
         "bwd": lambda s: lib.brk_fc_bwd_data(mlp.dz[2].data_ptr(), mlp.w[1].data_ptr(), mlp.y[1].data_ptr(),
-                                             mlp.dz[1].data_ptr(), n, c, c, B, B, B, _lib.BRK_BF16, s),
+                                             mlp.dz[1].data_ptr(), mlp.colsum[1].data_ptr(), n, c, c, B, B, B,
+                                             _lib.BRK_BF16, s),
         "upd": lambda s: lib.brk_fc_upd(mlp.y[0].data_ptr(), mlp.dz[1].data_ptr(), mlp.dw[0].data_ptr(), None,
-                                        0.0, n, c, c, B, B, B, _lib.BRK_BF16, s),
+                                        0.0, mlp.colsum[1].data_ptr(), n // 32, mlp.db[0].data_ptr(), None, 0.0,
+                                        mlp.upd_ws[0].data_ptr(), mlp.upd_ws[0].numel(),
+                                        n, c, c, B, B, B, _lib.BRK_BF16, s),
     }
     out = {}
     reps = 10

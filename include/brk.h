@@ -122,13 +122,22 @@ BRK_API int brk_brgemm_stride(const void* a_base, const void* b_base, int64_t st
  * act: 0 identity, 1 relu, 2 sigmoid (fc.py:29-40); bias (fp32, K) may be NULL. */
 BRK_API int brk_fc_fwd(const void* x, const void* w, const float* bias, void* y, int N, int C, int K,
                        int b_n, int b_c, int b_k, int act, int dtype, void* stream);
-/* Backward-data (north star): dx = (W^T dz) * (mask > 0); mask may be NULL. */
-BRK_API int brk_fc_bwd_data(const void* dz, const void* w, const void* mask, void* dx, int N, int C,
-                            int K, int b_n, int b_c, int b_k, int dtype, void* stream);
+/* Backward-data (north star): dx = (W^T dz) * (mask > 0); mask may be NULL.
+ * colsum_ws (may be NULL): fp32 [N/32][C] column-sum partials of the stored dx
+ * (the next weight update reduces them into that layer's bias gradient). */
+BRK_API int brk_fc_bwd_data(const void* dz, const void* w, const void* mask, void* dx, float* colsum_ws,
+                            int N, int C, int K, int b_n, int b_c, int b_k, int dtype, void* stream);
 /* Weight update (north star): dw = dz x^T (fp32); if w_sgd != NULL also
- * w_sgd -= lr * dw (bf16 weights, fused in the epilogue). */
-BRK_API int brk_fc_upd(const void* x, const void* dz, float* dw, void* w_sgd, float lr, int N, int C,
-                       int K, int b_n, int b_c, int b_k, int dtype, void* stream);
+ * w_sgd -= lr * dw (bf16 weights, fused in the epilogue).  If db_partials !=
+ * NULL (db_parts rows of K column sums, e.g. from brk_fc_bwd_data's colsum_ws)
+ * also db_out[K] = their ordered sum and bias_sgd -= bias_lr * db_out.
+ * workspace (may be NULL = no split-K): brk_fc_upd_workspace(N, C, K) bytes,
+ * zeroed once before first use (its counters self-reset). */
+BRK_API int brk_fc_upd(const void* x, const void* dz, float* dw, void* w_sgd, float lr,
+                       const float* db_partials, int db_parts, float* db_out, float* bias_sgd, float bias_lr,
+                       void* workspace, size_t ws_bytes, int N, int C, int K, int b_n, int b_c, int b_k,
+                       int dtype, void* stream);
+BRK_API size_t brk_fc_upd_workspace(int N, int C, int K);
 /* Bias gradient (north star): dz_out = dy * (y > 0) if y != NULL; db[K] = sum over N of dz;
  * if bias_sgd != NULL also bias_sgd -= lr * db (fused SGD).  Deterministic.
  * workspace: brk_fc_bias_grad_workspace(K) bytes, zeroed once before first use. */
@@ -142,6 +151,19 @@ BRK_API int brk_colsum_blocked(const void* dy, const void* y, void* dz_out, floa
 /* SGD apply (north-star training step after the dW allreduce): w -= lr * dw, n elements,
  * w in BRK_F32 or BRK_BF16 storage, dw fp32 in the same layout. */
 BRK_API int brk_sgd_apply(void* w, const float* dw, float lr, int64_t n, int w_dtype, void* stream);
+
+/* Diagnostic (not on the product path): TMA global->shared streaming
+ * throughput of `ctas` CTAs, each moving `iters` slots of loads_per_slot
+ * boxes (64 bf16 x box_rows) of a rows x cols bf16 matrix through a ring of
+ * `stages`; `spin` > 1 uses that many issuing warps.  Synchronous; returns
+ * device microseconds and bytes moved. */
+BRK_API int brk_diag_tma_bw(const void* buf, int rows, int cols, int box_rows, int loads_per_slot, int stages,
+                            int ctas, int iters, int spin, float* us, double* bytes);
+/* Diagnostic: subsequent engine launches record per-CTA %globaltimer phase
+ * stamps into ts[8 * blockIdx.x + phase] (device buffer); NULL disables. */
+BRK_API void brk_diag_set_timestamps(unsigned long long* ts);
+/* Diagnostic: per-warp clock64 cycles of iters x (tcgen05.ld.32x32b.x32 + wait); synchronous. */
+BRK_API int brk_diag_tmem_ld(int ctas, int iters, long long* cycles_dev, float* sink_dev);
 
 #ifdef __cplusplus
 }

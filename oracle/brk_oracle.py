@@ -230,19 +230,25 @@ def fc_backward_blocked(w_blk, x_blk, y_blk, dy_blk, activation="identity", work
     return dx, dw, db
 
 
-def mlp_step_reference(ws, bs, x, dy, lr=0.0, store=None):
+def mlp_step_reference(ws, bs, x, dy, lr=0.0, store=None, activations=None):
     """One MLP step (forward, backward-data, weight update, SGD) in float64.
 
     ws[l] (K, C), bs[l] (K,), x (N, C), dy (N, K_last) — ReLU after every layer.
     Stored tensors (activations y_l and back-propagated dz_l) are rounded to
     float32, then by ``store`` (e.g. ``round_bf16`` to mirror a bf16-storage
     implementation) at the same points an implementation stores them.
+    ``activations`` (optional list y_1..y_L) replaces the forward pass so the
+    backward pass uses exactly the implementation's ReLU masks (activations
+    within rounding of 0 otherwise flip masks between implementations).
     Returns dict(y=[...], dx, dw=[...], db=[...], w_new, b_new).
     """
     rnd = (lambda a: np.asarray(a, F32)) if store is None else (lambda a: store(np.asarray(a, F32)))
     ys = [rnd(x)]
-    for w, b in zip(ws, bs):
-        ys.append(rnd(fc_forward_reference(w, ys[-1].T, "relu", b).T.copy()))
+    if activations is not None:
+        ys.extend(np.asarray(a, F32) for a in activations)
+    else:
+        for w, b in zip(ws, bs):
+            ys.append(rnd(fc_forward_reference(w, ys[-1].T, "relu", b).T.copy()))
     dz = np.asarray(dy, F64) * (ys[-1] > 0)
     dws, dbs = [None] * len(ws), [None] * len(ws)
     dx = None

@@ -41,10 +41,15 @@ SIGNATURES: dict[str, tuple] = {
     "brk_brgemm_grouped": (_c_int, [_vp, _vp]),
     "brk_fc_fwd": (_c_int, [_vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int,
                             _c_int, _c_int, _vp]),
-    "brk_fc_bwd_data": (_c_int, [_vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int,
+    "brk_fc_bwd_data": (_c_int, [_vp, _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int,
                                  _c_int, _vp]),
-    "brk_fc_upd": (_c_int, [_vp, _vp, _vp, _vp, _c_f, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int,
-                            _c_int, _vp]),
+    "brk_fc_upd": (_c_int, [_vp, _vp, _vp, _vp, _c_f, _vp, _c_int, _vp, _vp, _c_f, _vp, ctypes.c_size_t,
+                            _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _vp]),
+    "brk_fc_upd_workspace": (ctypes.c_size_t, [_c_int, _c_int, _c_int]),
+    "brk_diag_set_timestamps": (None, [_vp]),
+    "brk_diag_tmem_ld": (_c_int, [_c_int, _c_int, _vp, _vp]),
+    "brk_diag_tma_bw": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int,
+                                 ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_double)]),
     "brk_fc_bias_grad": (_c_int, [_vp, _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _c_f, _vp]),
     "brk_fc_bias_grad_workspace": (ctypes.c_size_t, [_c_int]),
     "brk_colsum_blocked": (_c_int, [_vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp]),

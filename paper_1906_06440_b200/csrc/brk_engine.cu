@@ -1,15 +1,38 @@
 // brk_engine.cu — persistent, warp-specialised tcgen05 BRGEMM engine (see brk_engine.h).
 //
-// Roles (192 threads):
-//   warp 0      TMA producer: walks the batch list (k-steps) of every tile
-//               and streams (A_s, B_s) boxes into a kStages smem ring.
-//   warp 1      MMA issuer: one elected thread issues tcgen05.mma into a TMEM
+// Roles:
+//   warps 0..7  epilogue: tcgen05.ld the accumulator (TMEM lane = output row),
+//               fuse alpha/beta, bias, activation, ReLU-mask, the SGD update
+//               and bias-gradient column sums, and store.  Warp e drains TMEM
+//               lane quarter e%4, column half e/4 (two warps per SM
+//               sub-partition: the epilogue is issue-bound, not TMEM-bound).
+//               Two TMEM accumulators let the epilogue of one tile overlap the
+//               MMAs of the next.
+//   warp 8      MMA issuer: one elected thread issues tcgen05.mma into a TMEM
 //               accumulator that stays resident for the whole batch reduce;
-//               tcgen05.commit frees smem stages and publishes finished tiles.
-//   warps 2..5  epilogue: tcgen05.ld the accumulator (TMEM lane = output row),
-//               fuse alpha/beta, bias, activation, ReLU-mask and the SGD
-//               update, and store.  Two TMEM accumulators let the epilogue of
-//               tile t overlap the MMAs of tile t+1.
+//               tcgen05.commit frees ring stages and publishes finished tiles.
+//   warps 9..   kProducers TMA producers: producer j streams the (A_s, B_s)
+//               boxes of every k-step g = j (mod kProducers) of the batch list
+//               into the kStages ring.  Several issuing warps are required:
+//               one warp keeps only ~one box in flight (measured with
+//               brk_diag_tma_bw: 1 warp 12 B/clk/SM, 4 warps 44 B/clk/SM).
+//               kStages % kProducers == 0, so a slot is always refilled by the
+//               warp that filled it last and the parity waits cannot alias.
+//
+// kPair = true runs a CTA pair (cluster of 2, tcgen05 cta_group::2): the tile
+// is 256 x BN, each CTA stages its own 128 rows of A and BN/2 rows of B, the
+// leader CTA issues M=256 MMAs that read both CTAs' shared memory, and each
+// CTA drains its own 128-lane half of the accumulator.  Per-SM shared-memory
+// operand traffic per MMA halves versus the single-CTA 128 x BN tile, which is
+// what lets the tensor pipe run at full rate in SS mode.
+//
+// Split-K (k_splits > 1) cuts each tile's batch list into contiguous chunks
+// run by different CTAs; partial accumulators go through an fp32 workspace
+// and the last-arriving chunk sums them in chunk order (deterministic).
+//
+// Launched with programmatic stream serialisation (PDL): the prologue
+// (barrier init, TMEM alloc, tensor-map prefetch) overlaps the previous
+// kernel; griddepcontrol.wait precedes every global-memory access.
 #include <cstdio>
 
 #include "brk_engine.h"
@@ -19,18 +42,25 @@
 namespace brk {
 namespace {
 
-constexpr int kThreads = 192;
-constexpr int kTileABytes = kEngineBM * 128;
+constexpr int kTileABytes = kEngineBM * 128;  // 128 rows x 128 B per CTA
+constexpr int kEpiWarps = 8;
+constexpr int kEpiThreads = kEpiWarps * 32;
 
-template <int BN>
+template <int BN, bool kPair>
 struct EngineCfg {
-  static constexpr int kTileBBytes = BN * 128;
+  static constexpr int kBRows = kPair ? BN / 2 : BN;  // B rows staged per CTA
+  static constexpr int kTileBBytes = kBRows * 128;
   static constexpr int kStageBytes = kTileABytes + kTileBBytes;
-  static constexpr int kStages = (BN >= 256) ? 4 : 6;
+  static constexpr int kStages = (200 * 1024) / kStageBytes > 8 ? 8 : (200 * 1024) / kStageBytes;
   static constexpr int kTmemCols = 2 * BN;
   static constexpr int kSmem = kStages * kStageBytes + 1024 + 256;
+  static constexpr int kProducers = kStages % 4 == 0 ? 4 : (kStages % 3 == 0 ? 3 : (kStages % 2 == 0 ? 2 : 1));
+  static constexpr int kMmaWarp = kEpiWarps;
+  static constexpr int kThreads = (kEpiWarps + 1 + kProducers) * 32;
+  static constexpr int kColsPerWarp = BN >= 64 ? BN / 2 : BN;  // column half per epilogue warp
 };
 
+template <bool kPair>
 __device__ __forceinline__ void issue_operand(const CUtensorMap* map, const OperandCoords& oc,
                                               int rowblk, int s, uint8_t* dst, uint64_t* bar) {
   const int q = s / oc.kdiv, r = s - q * oc.kdiv;
@@ -39,11 +69,20 @@ __device__ __forceinline__ void issue_operand(const CUtensorMap* map, const Oper
 #pragma unroll
     for (int d = 0; d < 5; ++d) c[d] = oc.rc[d] * rowblk + oc.kq[d] * q + oc.kr[d] * r + oc.lc[d] * l;
     uint8_t* p = dst + l * oc.load_bytes;
-    switch (oc.ndims) {
-      case 2: { const int32_t cc[2] = {c[0], c[1]}; tma_load<2>(p, map, bar, cc); break; }
-      case 3: { const int32_t cc[3] = {c[0], c[1], c[2]}; tma_load<3>(p, map, bar, cc); break; }
-      case 4: { const int32_t cc[4] = {c[0], c[1], c[2], c[3]}; tma_load<4>(p, map, bar, cc); break; }
-      default: { const int32_t cc[5] = {c[0], c[1], c[2], c[3], c[4]}; tma_load<5>(p, map, bar, cc); break; }
+    if constexpr (kPair) {
+      switch (oc.ndims) {
+        case 2: { const int32_t cc[2] = {c[0], c[1]}; tma_load_pair<2>(p, map, bar, cc); break; }
+        case 3: { const int32_t cc[3] = {c[0], c[1], c[2]}; tma_load_pair<3>(p, map, bar, cc); break; }
+        case 4: { const int32_t cc[4] = {c[0], c[1], c[2], c[3]}; tma_load_pair<4>(p, map, bar, cc); break; }
+        default: { const int32_t cc[5] = {c[0], c[1], c[2], c[3], c[4]}; tma_load_pair<5>(p, map, bar, cc); break; }
+      }
+    } else {
+      switch (oc.ndims) {
+        case 2: { const int32_t cc[2] = {c[0], c[1]}; tma_load<2>(p, map, bar, cc); break; }
+        case 3: { const int32_t cc[3] = {c[0], c[1], c[2]}; tma_load<3>(p, map, bar, cc); break; }
+        case 4: { const int32_t cc[4] = {c[0], c[1], c[2], c[3]}; tma_load<4>(p, map, bar, cc); break; }
+        default: { const int32_t cc[5] = {c[0], c[1], c[2], c[3], c[4]}; tma_load<5>(p, map, bar, cc); break; }
+      }
     }
   }
 }
@@ -55,16 +94,145 @@ __device__ __forceinline__ uint64_t operand_desc(uint32_t base, int mn_major, in
     // K-major, 128B swizzle: 8-row groups 1024 B apart; K advance = 32 B.
     return make_smem_desc(base + kk * 32, 16, 1024, kSwizzle128B);
   }
-  // MN-major, 128B swizzle: atom = 64 B-elements(128 B) x BK rows; 8 K-rows = 1024 B.
+  // MN-major, 128B swizzle: atom = 128 B of MN x BK rows; 8 K-rows = 1024 B.
   constexpr uint32_t kRowsPerMma = kTF32 ? 8 : 16;
   constexpr uint32_t kAtomBytes = (kTF32 ? 32 : 64) * 128;  // BK rows x 128 B
   return make_smem_desc(base + kk * kRowsPerMma * 128, kAtomBytes, 1024, kSwizzle128B);
 }
 
-template <int BN, bool kTF32>
-__global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_constant__ EngineParams p) {
-  using Cfg = EngineCfg<BN>;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define BRK_TS(slot)                                                              \
+  do {                                                                            \
+    if (p.debug_ts != nullptr) p.debug_ts[blockIdx.x * 16 + (slot)] = gtimer();   \
+  } while (0)
+
+__device__ __forceinline__ void named_bar_sync(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+// Warp reduce-scatter: lane l ends with f[0] = sum over the 32 lanes of column l.
+__device__ __forceinline__ float warp_column_sum(float (&f)[32], int lane) {
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    const bool upper = (lane & off) != 0;
+#pragma unroll
+    for (int j = 0; j < off; ++j) {
+      const float send = upper ? f[j] : f[j + off];
+      const float keep = upper ? f[j + off] : f[j];
+      f[j] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+  return f[0];
+}
+
+// Fused epilogue of one 32-column chunk of one row.  `f` holds alpha*acc;
+// `bias_lane` is bias[col0 + lane] (broadcast by shuffle).  All 32 lanes of
+// the warp must call it (shuffles).
+__device__ __forceinline__ void epilogue_finish(const EngineParams& p, float (&f)[32], bool valid, int64_t off,
+                                                int col0, int warp_row0, int lane, float bias_lane) {
+  if (p.bias != nullptr && !(p.debug_flags & 16)) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) f[j] += __shfl_sync(0xffffffffu, bias_lane, j);
+  }
+  if (valid) {
+    if (p.beta != 0.0f) {
+      if (p.out_bf16) {
+        const __nv_bfloat16* src = static_cast<const __nv_bfloat16*>(p.out) + off;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) f[j] += p.beta * __bfloat162float(src[j]);
+      } else {
+        const float* src = static_cast<const float*>(p.out) + off;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) f[j] += p.beta * src[j];
+      }
+    }
+    if (p.act == kActRelu) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) f[j] = fmaxf(f[j], 0.0f);
+    } else if (p.act == kActSigmoid) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float e = __expf(-fabsf(f[j]));
+        const float r = __fdividef(1.0f, 1.0f + e);
+        f[j] = f[j] >= 0.0f ? r : e * r;
+      }
+    }
+    if (p.mask != nullptr) {
+      const uint4* mk = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.mask) + off);
+      uint4 w[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) w[q] = mk[q];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w[q]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 m2 = __bfloat1622float2(h[j]);
+          f[q * 8 + 2 * j] = m2.x > 0.0f ? f[q * 8 + 2 * j] : 0.0f;
+          f[q * 8 + 2 * j + 1] = m2.y > 0.0f ? f[q * 8 + 2 * j + 1] : 0.0f;
+        }
+      }
+    }
+    if (p.debug_flags & 8) {
+      // diagnostic: skip the output stores (keep the values live)
+      float acc = 0.0f;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) acc += f[j];
+      if (acc == 1234.5f) static_cast<float*>(p.out)[off] = acc;
+    } else if (p.out_bf16) {
+      uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out) + off);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 w;
+        w.x = pack_bf16x2(f[q * 8 + 0], f[q * 8 + 1]);
+        w.y = pack_bf16x2(f[q * 8 + 2], f[q * 8 + 3]);
+        w.z = pack_bf16x2(f[q * 8 + 4], f[q * 8 + 5]);
+        w.w = pack_bf16x2(f[q * 8 + 6], f[q * 8 + 7]);
+        dst[q] = w;
+      }
+      if (p.colsum_ws != nullptr) {  // column sums see the stored (rounded) values
+#pragma unroll
+        for (int j = 0; j < 32; ++j) f[j] = __bfloat162float(__float2bfloat16_rn(f[j]));
+      }
+    } else {
+      float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.out) + off);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) dst[q] = make_float4(f[q * 4], f[q * 4 + 1], f[q * 4 + 2], f[q * 4 + 3]);
+    }
+    if (p.sgd_w != nullptr) {
+      uint4* wp = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.sgd_w) + off);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 w = wp[q];
+        __nv_bfloat16* h = reinterpret_cast<__nv_bfloat16*>(&w);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) h[j] = __float2bfloat16_rn(__bfloat162float(h[j]) - p.sgd_lr * f[q * 8 + j]);
+        wp[q] = w;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) f[j] = 0.0f;
+  }
+  if (p.colsum_ws != nullptr) {
+    const float s = warp_column_sum(f, lane);
+    if (col0 < p.cols && warp_row0 < p.rows)
+      p.colsum_ws[static_cast<int64_t>(warp_row0 / 32) * p.cols + col0 + lane] = s;
+  }
+}
+
+template <int BN, bool kTF32, bool kPair>
+__global__ void __launch_bounds__(EngineCfg<BN, kPair>::kThreads, 1)
+    engine_kernel(const __grid_constant__ EngineParams p) {
+  using Cfg = EngineCfg<BN, kPair>;
   constexpr int kStages = Cfg::kStages;
+  constexpr int kMmaWarp = Cfg::kMmaWarp;
+  constexpr int kProducers = Cfg::kProducers;
+  constexpr int kCW = Cfg::kColsPerWarp;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -73,12 +241,20 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
   uint64_t* tfull = empty + kStages;  // [2]
   uint64_t* tempty = tfull + 2;       // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint32_t* split_flag = tmem_slot + 1;
 
   const int warp = warp_id();
   const int lane = threadIdx.x & 31;
-  const int num_tiles = p.m_tiles * p.n_tiles;
+  const uint32_t rank = kPair ? cluster_ctarank() : 0u;
+  const bool leader = rank == 0;
+  const int unit0 = kPair ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
+  const int n_units = kPair ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x);
+  const int splits = p.k_splits > 1 ? p.k_splits : 1;
+  const int ks_per = (p.k_steps + splits - 1) / splits;
+  const int num_work = p.m_tiles * p.n_tiles * splits;
+  if (threadIdx.x == 0) BRK_TS(0);
 
-  if (warp == 0 && lane == 0) {
+  if (warp == kMmaWarp + 1 && lane == 0) {
     tma_prefetch_desc(&p.map_a);
     tma_prefetch_desc(&p.map_b);
     for (int s = 0; s < kStages; ++s) {
@@ -87,194 +263,268 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
+      mbar_init(&tempty[a], kPair ? 2 * kEpiWarps : kEpiWarps);
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, Cfg::kTmemCols);
+  if (warp == kMmaWarp) {
+    if constexpr (kPair) tmem_alloc_pair(tmem_slot, Cfg::kTmemCols);
+    else tmem_alloc(tmem_slot, Cfg::kTmemCols);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kPair) cluster_sync_all(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) BRK_TS(1);
+  pdl_launch_dependents();  // let the next kernel's prologue start early
 
-  if (warp == 0) {
-    // ------------------------------------------------------------ producer
+  if (warp > kMmaWarp) {
+    // ------------------------------------------------------------ producers
+    const int pid = warp - kMmaWarp - 1;
     if (elect_one()) {
-      int stage = 0;
-      uint32_t phase = 0;
-      const uint32_t bytes = p.ca.n_loads * p.ca.load_bytes + p.cb.n_loads * p.cb.load_bytes;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      pdl_wait();  // inputs are produced by the previous kernel
+      const uint32_t bytes = (p.ca.n_loads * p.ca.load_bytes + p.cb.n_loads * p.cb.load_bytes) * (kPair ? 2 : 1);
+      int g = 0;  // global k-step counter of this CTA (same sequence as the MMA issuer)
+      for (int u = unit0; u < num_work; u += n_units) {
+        const int t = u / splits, sp = u - t * splits;
         const int mb = t % p.m_tiles, nb = t / p.m_tiles;
-        for (int s = 0; s < p.k_steps; ++s) {
+        const int arow = kPair ? mb * 2 + static_cast<int>(rank) : mb;
+        const int brow = kPair ? nb * 2 + static_cast<int>(rank) : nb;
+        const int s_begin = sp * ks_per;
+        const int n_steps = min(p.k_steps, s_begin + ks_per) - s_begin;
+        // Rotate the batch-list start per tile so concurrently running tiles read
+        // different blocks; the order is fixed per tile (deterministic results).
+        const int rot = (p.debug_flags & 4) ? 0 : (mb * 7 + nb * 3) % n_steps;
+        int s0 = (pid - g % kProducers + kProducers) % kProducers;  // first step owned by pid
+        for (; s0 < n_steps; s0 += kProducers) {
+          const int gg = g + s0;
+          const int stage = gg % kStages;
+          const uint32_t phase = (gg / kStages) & 1;
+          const int s = s_begin + (s0 + rot < n_steps ? s0 + rot : s0 + rot - n_steps);
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * Cfg::kStageBytes;
           uint8_t* sb = sa + kTileABytes;
           if (p.debug_flags & 2) {
-            mbar_arrive(&full[stage]);
+            if (leader) mbar_arrive(&full[stage]);
           } else {
-            mbar_arrive_expect_tx(&full[stage], bytes);
-            issue_operand(&p.map_a, p.ca, mb, s, sa, &full[stage]);
-            issue_operand(&p.map_b, p.cb, nb, s, sb, &full[stage]);
+            if (leader) mbar_arrive_expect_tx(&full[stage], bytes);
+            issue_operand<kPair>(&p.map_a, p.ca, arow, s, sa, &full[stage]);
+            issue_operand<kPair>(&p.map_b, p.cb, brow, s, sb, &full[stage]);
           }
-          if (++stage == kStages) { stage = 0; phase ^= 1; }
+          if (gg == 0 && pid == 0) BRK_TS(2);
         }
+        g += n_steps;
       }
     }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    const uint32_t idesc = make_idesc(kTF32 ? kFmtTF32 : kFmtBF16, kEngineBM, BN, p.ca.mn_major,
-                                      p.cb.mn_major);
-    int stage = 0;
-    uint32_t phase = 0;
-    int local = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
-      const int acc = local & 1;
-      const uint32_t acc_phase = (local >> 1) & 1;
-      mbar_wait(&tempty[acc], acc_phase ^ 1);
-      tc_fence_after();
-      const uint32_t d_tmem = tmem_base + acc * BN;
-      for (int s = 0; s < p.k_steps; ++s) {
-        mbar_wait(&full[stage], phase);
+  } else if (warp == kMmaWarp) {
+    // ------------------------------------------------------------ MMA issuer (leader CTA)
+    if (leader) {
+      const uint32_t idesc = make_idesc(kTF32 ? kFmtTF32 : kFmtBF16, kPair ? 256 : kEngineBM, BN,
+                                        p.ca.mn_major, p.cb.mn_major);
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      for (int u = unit0; u < num_work; u += n_units, ++local) {
+        const int sp = u % splits;
+        const int s_begin = sp * ks_per;
+        const int n_steps = min(p.k_steps, s_begin + ks_per) - s_begin;
+        const int acc = local & 1;
+        mbar_wait(&tempty[acc], ((local >> 1) & 1) ^ 1);
         tc_fence_after();
-        if (p.debug_flags & 1) {
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int s = 0; s < n_steps; ++s) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          if (local == 0 && s == 0 && lane == 0) BRK_TS(3);
           if (elect_one()) {
-            mbar_arrive(&empty[stage]);
-            if (s == p.k_steps - 1) mbar_arrive(&tfull[acc]);
-          }
-        } else if (elect_one()) {
-          const uint32_t sa = smem_u32(smem + stage * Cfg::kStageBytes);
-          const uint32_t sb = sa + kTileABytes;
+            if (p.debug_flags & 1) {
+              if constexpr (kPair) {
+                mma_commit_pair(&empty[stage]);
+                if (s == n_steps - 1) mma_commit_pair(&tfull[acc]);
+              } else {
+                mbar_arrive(&empty[stage]);
+                if (s == n_steps - 1) mbar_arrive(&tfull[acc]);
+              }
+            } else {
+              const uint32_t sa = smem_u32(smem + stage * Cfg::kStageBytes);
+              const uint32_t sb = sa + kTileABytes;
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            mma_ss<kTF32>(d_tmem, operand_desc<kTF32>(sa, p.ca.mn_major, kk),
-                          operand_desc<kTF32>(sb, p.cb.mn_major, kk), idesc,
-                          (s > 0 || kk > 0) ? 1u : 0u);
+              for (int kk = 0; kk < 4; ++kk) {
+                const uint64_t ad = operand_desc<kTF32>(sa, p.ca.mn_major, kk);
+                const uint64_t bd = operand_desc<kTF32>(sb, p.cb.mn_major, kk);
+                const uint32_t accum = (s > 0 || kk > 0) ? 1u : 0u;
+                if constexpr (kPair) mma_ss_pair<kTF32>(d_tmem, ad, bd, idesc, accum);
+                else mma_ss<kTF32>(d_tmem, ad, bd, idesc, accum);
+              }
+              if constexpr (kPair) {
+                mma_commit_pair(&empty[stage]);
+                if (s == n_steps - 1) mma_commit_pair(&tfull[acc]);
+              } else {
+                mma_commit(&empty[stage]);
+                if (s == n_steps - 1) mma_commit(&tfull[acc]);
+              }
+            }
           }
-          mma_commit(&empty[stage]);
-          if (s == p.k_steps - 1) mma_commit(&tfull[acc]);
+          __syncwarp();
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
-        __syncwarp();
-        if (++stage == kStages) { stage = 0; phase ^= 1; }
+        if (lane == 0) BRK_TS(4);
       }
     }
   } else {
-    // ------------------------------------------------------------ epilogue
+    // ------------------------------------------------------------ epilogue (warps 0..7)
+    pdl_wait();  // outputs may be read by the previous kernel (WAR) — wait before writing
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+    const int chalf = warp >> 2;   // column half this warp drains
+    const int cbeg = chalf * kCW;
     const int row_in_tile = quarter * 32 + lane;
+    const uint32_t tempty_leader = kPair ? mapa_shared(smem_u32(&tempty[0]), 0) : 0u;
+    const int halves = kPair ? 2 : 1;
     int local = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
+    for (int u = unit0; u < num_work; u += n_units, ++local) {
+      const int t = u / splits, sp = u - t * splits;
       const int mb = t % p.m_tiles, nb = t / p.m_tiles;
       const int acc = local & 1;
+      // bias for this warp's columns, one value per lane per 32-column chunk
+      float bias_r[kCW / 32];
+#pragma unroll
+      for (int c = 0; c < kCW / 32; ++c) {
+        const int col = nb * BN + cbeg + c * 32 + lane;
+        bias_r[c] = (p.bias != nullptr && col < p.cols) ? __ldg(p.bias + col) : 0.0f;
+      }
       mbar_wait(&tfull[acc], (local >> 1) & 1);
       tc_fence_after();
-      const int row = mb * kEngineBM + row_in_tile;
+      if (threadIdx.x == 0) BRK_TS(5);
+      const int tile_row0 = kPair ? mb * 256 + static_cast<int>(rank) * 128 : mb * kEngineBM;
+      const int row = tile_row0 + row_in_tile;
+      const int warp_row0 = tile_row0 + quarter * 32;
       const bool row_ok = row < p.rows;
       const int64_t roff = (row / p.om.rb) * p.om.rh + (row % p.om.rb) * p.om.rl;
-#pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
+      const uint32_t tbase = tmem_base + acc * BN + (static_cast<uint32_t>(quarter * 32) << 16) + cbeg;
+      if (splits == 1) {
+        // column offset maintained incrementally (32 columns never straddle an
+        // output block: cb % 32 == 0, host guarantees); TMEM loads are software-
+        // pipelined one chunk ahead so the ld latency overlaps the epilogue math.
+        int64_t cq = (static_cast<int64_t>(nb) * BN + cbeg) / p.om.cb;
+        int64_t cr = (static_cast<int64_t>(nb) * BN + cbeg) % p.om.cb;
         uint32_t v[32];
-        tmem_ld32(tmem_base + acc * BN + (static_cast<uint32_t>(quarter * 32) << 16) + c0, v);
-        tmem_ld_wait();
-        const int col0 = nb * BN + c0;
-        if (!row_ok || col0 >= p.cols) continue;
-        // 32 columns never straddle an output block when cb % 32 == 0 (host guarantees)
-        const int64_t off = roff + (col0 / p.om.cb) * p.om.ch + (col0 % p.om.cb) * p.om.cl;
-        float f[32];
-        if (p.alpha == 1.0f) {
+        tmem_ld32(tbase, v);
 #pragma unroll
-          for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
-        } else {
+        for (int c = 0; c < kCW / 32; ++c) {
+          tmem_ld_wait();
+          float f[32];
+          if (p.alpha == 1.0f) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]) * p.alpha;
-        }
-        if (p.out == nullptr) continue;  // diagnostic: mainloop-only timing
-        if (p.beta != 0.0f) {
-          if (p.out_bf16) {
-            const __nv_bfloat16* src = static_cast<const __nv_bfloat16*>(p.out) + off;
-#pragma unroll
-            for (int j = 0; j < 32; ++j) f[j] += p.beta * __bfloat162float(src[j]);
+            for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
           } else {
-            const float* src = static_cast<const float*>(p.out) + off;
 #pragma unroll
-            for (int j = 0; j < 32; ++j) f[j] += p.beta * src[j];
+            for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]) * p.alpha;
           }
+          if (c + 1 < kCW / 32) tmem_ld32(tbase + (c + 1) * 32, v);
+          const int col0 = nb * BN + cbeg + c * 32;
+          const int64_t off = roff + cq * p.om.ch + cr * p.om.cl;
+          cr += 32;
+          if (cr == p.om.cb) { cr = 0; ++cq; }
+          if (p.out == nullptr) continue;  // diagnostic: mainloop-only timing
+          if (threadIdx.x == 0 && c < 2) BRK_TS(8 + 2 * c);
+          epilogue_finish(p, f, row_ok && col0 < p.cols, off, col0, warp_row0, lane, bias_r[c]);
+          if (threadIdx.x == 0 && c < 2) BRK_TS(9 + 2 * c);
         }
-        if (p.bias != nullptr) {
-          const float4* b4 = reinterpret_cast<const float4*>(p.bias + col0);
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const float4 b = __ldg(b4 + q);
-            f[q * 4 + 0] += b.x; f[q * 4 + 1] += b.y; f[q * 4 + 2] += b.z; f[q * 4 + 3] += b.w;
-          }
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (threadIdx.x == 0) BRK_TS(12);
+        if (lane == 0) {
+          if constexpr (kPair) mbar_arrive_cluster(tempty_leader + acc * 8);
+          else mbar_arrive(&tempty[acc]);
         }
-        if (p.act == kActRelu) {
+        if (threadIdx.x == 0) BRK_TS(13);
+      } else {
+        // split-K: park the partial accumulator, last chunk reduces in chunk order
+        float* ws_tile = p.split_ws + (static_cast<int64_t>(t) * halves + rank) * splits * (kEngineBM * BN);
+        float* mine = ws_tile + static_cast<int64_t>(sp) * (kEngineBM * BN) + row_in_tile * BN + cbeg;
 #pragma unroll
-          for (int j = 0; j < 32; ++j) f[j] = fmaxf(f[j], 0.0f);
-        } else if (p.act == kActSigmoid) {
+        for (int c = 0; c < kCW / 32; ++c) {
+          uint32_t v[32];
+          tmem_ld32(tbase + c * 32, v);
+          tmem_ld_wait();
+          float4* d4 = reinterpret_cast<float4*>(mine + c * 32);
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const float e = __expf(-fabsf(f[j]));
-            const float r = __fdividef(1.0f, 1.0f + e);
-            f[j] = f[j] >= 0.0f ? r : e * r;
-          }
+          for (int q = 0; q < 8; ++q)
+            d4[q] = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                                __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
         }
-        if (p.mask != nullptr) {
-          const uint4* mk = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.mask) + off);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (kPair) mbar_arrive_cluster(tempty_leader + acc * 8);
+          else mbar_arrive(&tempty[acc]);
+        }
+        __threadfence();
+        named_bar_sync(1, kEpiThreads);
+        if (threadIdx.x == 0) {
+          const unsigned prev = atomicAdd(&p.split_counters[t * halves + rank], 1u);
+          *split_flag = (prev == static_cast<unsigned>(splits - 1)) ? 1u : 0u;
+        }
+        named_bar_sync(1, kEpiThreads);
+        if (*split_flag) {
+          __threadfence();
+          int64_t cq = (static_cast<int64_t>(nb) * BN + cbeg) / p.om.cb;
+          int64_t cr = (static_cast<int64_t>(nb) * BN + cbeg) % p.om.cb;
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            uint4 w = mk[q];
-            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
+          for (int c = 0; c < kCW / 32; ++c) {
+            float f[32];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const float2 m2 = __bfloat1622float2(h[j]);
-              f[q * 8 + 2 * j] = m2.x > 0.0f ? f[q * 8 + 2 * j] : 0.0f;
-              f[q * 8 + 2 * j + 1] = m2.y > 0.0f ? f[q * 8 + 2 * j + 1] : 0.0f;
+            for (int j = 0; j < 32; ++j) f[j] = 0.0f;
+            for (int q = 0; q < splits; ++q) {
+              const float4* s4 = reinterpret_cast<const float4*>(ws_tile + static_cast<int64_t>(q) * (kEngineBM * BN) +
+                                                                 row_in_tile * BN + cbeg + c * 32);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const float4 x = __ldcg(s4 + j);
+                f[4 * j] += x.x; f[4 * j + 1] += x.y; f[4 * j + 2] += x.z; f[4 * j + 3] += x.w;
+              }
             }
+#pragma unroll
+            for (int j = 0; j < 32; ++j) f[j] *= p.alpha;
+            const int col0 = nb * BN + cbeg + c * 32;
+            const int64_t off = roff + cq * p.om.ch + cr * p.om.cl;
+            cr += 32;
+            if (cr == p.om.cb) { cr = 0; ++cq; }
+            if (p.out == nullptr) continue;
+            epilogue_finish(p, f, row_ok && col0 < p.cols, off, col0, warp_row0, lane, bias_r[c]);
           }
-        }
-        if (p.out_bf16) {
-          uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out) + off);
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            uint4 w;
-            w.x = pack_bf16x2(f[q * 8 + 0], f[q * 8 + 1]);
-            w.y = pack_bf16x2(f[q * 8 + 2], f[q * 8 + 3]);
-            w.z = pack_bf16x2(f[q * 8 + 4], f[q * 8 + 5]);
-            w.w = pack_bf16x2(f[q * 8 + 6], f[q * 8 + 7]);
-            dst[q] = w;
-          }
-        } else {
-          float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.out) + off);
-#pragma unroll
-          for (int q = 0; q < 8; ++q) dst[q] = make_float4(f[q * 4], f[q * 4 + 1], f[q * 4 + 2], f[q * 4 + 3]);
-        }
-        if (p.sgd_w != nullptr) {
-          uint4* wp = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.sgd_w) + off);
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            uint4 w = wp[q];
-            __nv_bfloat16* h = reinterpret_cast<__nv_bfloat16*>(&w);
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-              h[j] = __float2bfloat16_rn(__bfloat162float(h[j]) - p.sgd_lr * f[q * 8 + j]);
-            wp[q] = w;
-          }
+          if (threadIdx.x == 0) p.split_counters[t * halves + rank] = 0u;  // self-reset
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      // bias gradient from column-sum partials of a previous pass (+ fused bias SGD)
+      if (p.db_partials != nullptr && mb == 0 && rank == 0 && sp == 0) {
+        for (int c = threadIdx.x; c < BN; c += kEpiThreads) {
+          const int col = nb * BN + c;
+          if (col >= p.cols) continue;
+          float s = 0.0f;
+          for (int q = 0; q < p.db_parts; ++q) s += p.db_partials[static_cast<int64_t>(q) * p.cols + col];
+          p.db_out[col] = s;
+          if (p.bias_sgd != nullptr) p.bias_sgd[col] -= p.bias_lr * s;
+        }
+      }
+      if (threadIdx.x == 0) BRK_TS(6);
     }
   }
   tc_fence_before();
-  __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem_base, Cfg::kTmemCols);
+  if constexpr (kPair) cluster_sync_all(); else __syncthreads();
+  if (warp == kMmaWarp) {
+    tc_fence_after();
+    if constexpr (kPair) tmem_dealloc_pair(tmem_base, Cfg::kTmemCols);
+    else tmem_dealloc(tmem_base, Cfg::kTmemCols);
+  }
+  if (threadIdx.x == 0) BRK_TS(7);
 }
 
-template <int BN, bool kTF32>
-int launch_engine_t(const EngineParams& p, int grid, cudaStream_t stream) {
-  using Cfg = EngineCfg<BN>;
-  auto kern = engine_kernel<BN, kTF32>;
+template <int BN, bool kTF32, bool kPair>
+int launch_engine_t(const EngineParams& p, int grid, cudaStream_t stream, bool pdl) {
+  using Cfg = EngineCfg<BN, kPair>;
+  auto kern = engine_kernel<BN, kTF32, kPair>;
   static int attr_set = 0;  // per instantiation; the attribute is per-context state
   cudaError_t err;
   if (!attr_set) {
@@ -282,8 +532,28 @@ int launch_engine_t(const EngineParams& p, int grid, cudaStream_t stream) {
     if (err != cudaSuccess) return set_cuda_error(err, "engine smem attribute");
     attr_set = 1;
   }
-  kern<<<grid, kThreads, Cfg::kSmem, stream>>>(p);
-  err = cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(Cfg::kThreads);
+  cfg.dynamicSmemBytes = Cfg::kSmem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attrs[2];
+  int na = 0;
+  if (kPair) {
+    attrs[na].id = cudaLaunchAttributeClusterDimension;
+    attrs[na].val.clusterDim.x = 2;
+    attrs[na].val.clusterDim.y = 1;
+    attrs[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  if (pdl) {
+    attrs[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attrs[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = attrs;
+  cfg.numAttrs = na;
+  err = cudaLaunchKernelEx(&cfg, kern, p);
   if (err != cudaSuccess) return set_cuda_error(err, "engine launch");
   return BRK_OK;
 }
@@ -301,15 +571,39 @@ int engine_sm_count() {
   return sms;
 }
 
-int launch_engine(const EngineParams& p, int bn, int tf32, int max_ctas, cudaStream_t stream) {
-  const int tiles = p.m_tiles * p.n_tiles;
-  if (tiles <= 0) return BRK_OK;
-  int grid = tiles < engine_sm_count() ? tiles : engine_sm_count();
-  if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
-  if (bn == 256) return tf32 ? launch_engine_t<256, true>(p, grid, stream) : launch_engine_t<256, false>(p, grid, stream);
-  if (bn == 128) return tf32 ? launch_engine_t<128, true>(p, grid, stream) : launch_engine_t<128, false>(p, grid, stream);
-  if (bn == 64) return tf32 ? launch_engine_t<64, true>(p, grid, stream) : launch_engine_t<64, false>(p, grid, stream);
-  return set_error(BRK_ERR_CONTRACT, "engine: BN must be 64, 128 or 256");
+// bn: 64 / 128 / 256; pair: CTA-pair (tile rows 256) — p.m_tiles is in units of
+// 128 (single) or 256 (pair) rows and the B operand coordinates in units of
+// BN (single) or BN/2 (pair) rows, as set up by the caller.
+int launch_engine(const EngineParams& p, int bn, int tf32, int pair, int max_units, cudaStream_t stream) {
+  const int splits = p.k_splits > 1 ? p.k_splits : 1;
+  const int work = p.m_tiles * p.n_tiles * splits;
+  if (work <= 0) return BRK_OK;
+  if (splits > 1 && (p.split_ws == nullptr || p.split_counters == nullptr))
+    return set_error(BRK_ERR_CONTRACT, "engine: split-K needs a workspace");
+  const int sms = engine_sm_count();
+  int units = pair ? sms / 2 : sms;
+  if (work < units) units = work;
+  if (max_units > 0 && units > max_units) units = max_units;
+  const int grid = pair ? units * 2 : units;
+  const bool pdl = true;
+#define BRK_ENGINE_CASE(BN_)                                                                  \
+  if (bn == BN_) {                                                                            \
+    if (pair) return tf32 ? launch_engine_t<BN_, true, true>(p, grid, stream, pdl)            \
+                          : launch_engine_t<BN_, false, true>(p, grid, stream, pdl);          \
+    return tf32 ? launch_engine_t<BN_, true, false>(p, grid, stream, pdl)                     \
+                : launch_engine_t<BN_, false, false>(p, grid, stream, pdl);                   \
+  }
+  BRK_ENGINE_CASE(256)
+  BRK_ENGINE_CASE(128)
+#undef BRK_ENGINE_CASE
+  if (bn == 64 && !pair)
+    return tf32 ? launch_engine_t<64, true, false>(p, grid, stream, pdl)
+                : launch_engine_t<64, false, false>(p, grid, stream, pdl);
+  return set_error(BRK_ERR_CONTRACT, "engine: BN must be 128 or 256 (pair) / 64, 128, 256 (single)");
+}
+
+size_t engine_split_ws_bytes(int tiles, int splits, int bn, int pair) {
+  return static_cast<size_t>(tiles) * (pair ? 2 : 1) * splits * kEngineBM * bn * sizeof(float);
 }
 
 }  // namespace brk

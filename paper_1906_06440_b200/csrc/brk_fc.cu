@@ -10,73 +10,107 @@
 // TMA engine path: bf16 storage with all block factors = 64 (one 128 B
 // swizzle row per block row).  Tensor-map coordinates per k-step are the
 // blocked-tensor coordinates of the batch entry.
+#include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
-#include <atomic>
 #include <cuda_bf16.h>
 
 #include "brk_engine.h"
 #include "brk_internal.h"
+#include "brk_ptx.cuh"
 #include "brk_tma_host.h"
 
 namespace brk {
 
-int launch_engine(const EngineParams& p, int bn, int tf32, int max_ctas, cudaStream_t stream);
+int launch_engine(const EngineParams& p, int bn, int tf32, int pair, int max_units, cudaStream_t stream);
 int engine_sm_count();
-
+size_t engine_split_ws_bytes(int tiles, int splits, int bn, int pair);
 
 namespace {
 
 constexpr int kB = 64;  // block factor served by the TMA path (bf16)
 
-int pick_bn(int m_tiles, int n_extent) {
-  if (const char* env = std::getenv("BRK_BN")) {
-    int v = std::atoi(env);
-    if ((v == 64 || v == 128 || v == 256) && n_extent % v == 0) return v;
+struct Plan {
+  int pair;    // 1: CTA pair, 256-row tiles
+  int bn;      // tile columns
+  int splits;  // split-K factor (1 = none)
+  int tiles;
+};
+
+// Pick (pair, BN, split-K) for a rows x cols output with k_steps batch
+// entries: minimise waves x per-work-unit time.  Per-SM tensor-pipe
+// efficiency in SS mode (measured): 1-CTA N=128 ~1/2, N=256 ~2/3, CTA pair
+// N=128 ~2/3 (L2-fed), N=256 ~1.  Split-K only when tiles cannot fill the
+// machine; each chunk keeps >= 4 k-steps.
+Plan choose_plan(int rows, int cols, int k_steps, bool allow_split) {
+  Plan forced{-1, 0, 0, 0};
+  if (const char* env = std::getenv("BRK_TILE")) {  // "pair,bn" e.g. "1,256"
+    int a = 0, b = 0;
+    if (std::sscanf(env, "%d,%d", &a, &b) == 2) forced = Plan{a, b, 0, 0};
   }
+  int forced_splits = 0;
+  if (const char* env = std::getenv("BRK_SPLITS")) forced_splits = std::atoi(env);
+  // Split-K is opt-in: measured slower than the unsplit tile for the MLP shapes
+  // (profiles/r01_engine_notes.md); kept for deep-K / few-tile problems.
+  if (forced_splits <= 0) allow_split = false;
   const int sms = engine_sm_count();
-  int best = 0;
-  long best_cost = 0;
-  for (int bn : {256, 128, 64}) {
-    if (n_extent % bn) continue;
-    const long tiles = static_cast<long>(m_tiles) * (n_extent / bn);
-    const long waves = (tiles + sms - 1) / sms;
-    const long cost = waves * (bn + 64);
-    if (best == 0 || cost < best_cost) { best = bn; best_cost = cost; }
+  struct Opt { int pair, bn; double eff; };
+  const Opt opts[] = {{1, 256, 1.0}, {1, 128, 0.67}, {0, 256, 0.67}, {0, 128, 0.5}, {0, 64, 0.33}};
+  Plan best{0, 0, 1, 0};
+  double best_cost = 0;
+  for (const Opt& o : opts) {
+    const int tile_rows = o.pair ? 256 : 128;
+    if (rows % tile_rows || cols % o.bn) continue;
+    if (forced.pair >= 0 && (forced.pair != o.pair || forced.bn != o.bn)) continue;
+    const long tiles = static_cast<long>(rows / tile_rows) * (cols / o.bn);
+    const long units = o.pair ? sms / 2 : sms;
+    const double per_tile = static_cast<double>(tile_rows) * o.bn * k_steps / ((o.pair ? 2.0 : 1.0) * o.eff);
+    int max_split = allow_split ? (int)std::max(1L, std::min<long>(k_steps / 4, units / std::max(1L, tiles))) : 1;
+    if (forced_splits > 0) max_split = allow_split ? std::min(forced_splits, k_steps) : 1;
+    for (int sp = (forced_splits > 0 ? max_split : 1); sp <= max_split; ++sp) {
+      const long work = tiles * sp;
+      const long waves = (work + units - 1) / units;
+      const double cost = waves * per_tile / sp * (sp > 1 ? 1.1 : 1.0) + 2.0e5;  // + fixed launch cost
+      if (best.bn == 0 || cost < best_cost) {
+        best = Plan{o.pair, o.bn, sp, static_cast<int>(tiles)};
+        best_cost = cost;
+      }
+    }
   }
   return best;
 }
 
 // Blocked 2-D activation [Rb][Xb][64][64] (row-major blocks, x innermost):
-// X (rows n, x = c), dZ/Y (rows n, x = k).
-struct Act4 {
+// X (rows n, x = c), dZ/Y (rows n, x = k).  dims (x_in, r_in, xb, rb)
+struct Map4 {
   uint64_t dims[4];
   uint64_t strides[4];
 };
-Act4 act_layout(int64_t rows, int64_t xs) {
-  Act4 a;
+Map4 act_layout(int64_t rows, int64_t xs) {
+  Map4 a;
   a.dims[0] = kB; a.dims[1] = kB; a.dims[2] = xs / kB; a.dims[3] = rows / kB;
   a.strides[0] = 1; a.strides[1] = kB; a.strides[2] = kB * kB; a.strides[3] = (xs / kB) * kB * kB;
   return a;
 }
 // Weights [Kb][Cb][64 c][64 k] (k innermost): dims (k_in, c_in, cb, kb)
-Act4 w_layout(int64_t K, int64_t C) {
-  Act4 a;
+Map4 w_layout(int64_t K, int64_t C) {
+  Map4 a;
   a.dims[0] = kB; a.dims[1] = kB; a.dims[2] = C / kB; a.dims[3] = K / kB;
   a.strides[0] = 1; a.strides[1] = kB; a.strides[2] = kB * kB; a.strides[3] = (C / kB) * kB * kB;
   return a;
 }
 
 void set_coords(OperandCoords& oc, std::initializer_list<int> rc, std::initializer_list<int> kq,
-                int n_loads, uint32_t load_bytes, int mn_major) {
+                uint32_t load_bytes, int mn_major) {
   std::memset(&oc, 0, sizeof(oc));
   int d = 0;
   for (int v : rc) oc.rc[d++] = v;
   d = 0;
   for (int v : kq) oc.kq[d++] = v;
   oc.kdiv = 1;
-  oc.n_loads = n_loads;
+  oc.n_loads = 1;
   oc.load_bytes = load_bytes;
   oc.mn_major = mn_major;
   oc.ndims = 4;
@@ -97,11 +131,18 @@ int check_fc(int N, int C, int K, int b_n, int b_c, int b_k, int dtype) {
   return BRK_OK;
 }
 
-int enc(CUtensorMap* map, const void* ptr, const Act4& l, uint32_t b0, uint32_t b1, uint32_t b2,
+int enc(CUtensorMap* map, const void* ptr, const Map4& l, uint32_t b0, uint32_t b1, uint32_t b2,
         uint32_t b3) {
   const uint32_t box[4] = {b0, b1, b2, b3};
   return encode_tmap(map, ptr, true, 4, l.dims, l.strides, box);
 }
+
+int debug_flags() {
+  const char* dbg = std::getenv("BRK_DEBUG_FLAGS");
+  return dbg ? std::atoi(dbg) : 0;
+}
+
+unsigned long long* g_debug_ts = nullptr;  // set by brk_diag_set_timestamps
 
 // ---------------------------------------------------------------------------
 // dZ = dY * (Y > 0) (optional) and db[k] = sum_n dZ[n][k]  — deterministic:
@@ -116,10 +157,12 @@ __global__ void __launch_bounds__(256) bias_grad_kernel(const __nv_bfloat16* dy,
                                                         float* __restrict__ db, float* __restrict__ partial,
                                                         unsigned* __restrict__ counters, int N, int K,
                                                         float* __restrict__ bias, float lr) {
+  pdl_launch_dependents();
+  pdl_wait();
   const int kb = blockIdx.x, split = blockIdx.y;
   const int Kb = K / kB;
   const int tid = threadIdx.x;
-  const int cgrp = tid & 7;   // 8 column groups of 8 (16 B)
+  const int cgrp = tid & 7;    // 8 column groups of 8 (16 B)
   const int rlane = tid >> 3;  // 32 row lanes
   const int rows_per = N / kSplit;
   const int r0 = split * rows_per;
@@ -181,16 +224,16 @@ BRK_API int brk_fc_fwd(const void* x, const void* w, const float* bias, void* y,
   if (act < kActNone || act > kActSigmoid) return set_error(BRK_ERR_CONTRACT, "unknown activation");
   EngineParams p;
   std::memset(&p, 0, sizeof(p));
-  const int m_tiles = N / 128;
-  const int bn = pick_bn(m_tiles, K);
-  // A = X (rows n, red c) K-major: box (c 64, n 64, cb 1, nb 2)
+  const Plan pl = choose_plan(N, K, C / kB, false);
+  const int brows = pl.pair ? pl.bn / 2 : pl.bn;
+  // A = X (rows n, red c) K-major: box (c 64, n 64, cb 1, nb 2) = 128 rows
   if ((rc = enc(&p.map_a, x, act_layout(N, C), 64, 64, 1, 2))) return rc;
-  set_coords(p.ca, {0, 0, 0, 2}, {0, 0, 1, 0}, 1, 128 * 128, 0);
-  // B = W (rows k, red c) MN-major: box (k 64, c 64, cb 1, kb bn/64)
-  if ((rc = enc(&p.map_b, w, w_layout(K, C), 64, 64, 1, bn / 64))) return rc;
-  set_coords(p.cb, {0, 0, 0, bn / 64}, {0, 0, 1, 0}, 1, bn * 128, 1);
-  p.m_tiles = m_tiles;
-  p.n_tiles = K / bn;
+  set_coords(p.ca, {0, 0, 0, 2}, {0, 0, 1, 0}, 128 * 128, 0);
+  // B = W (rows k, red c) MN-major: box (k 64, c 64, cb 1, kb brows/64)
+  if ((rc = enc(&p.map_b, w, w_layout(K, C), 64, 64, 1, brows / 64))) return rc;
+  set_coords(p.cb, {0, 0, 0, brows / 64}, {0, 0, 1, 0}, brows * 128, 1);
+  p.m_tiles = N / (pl.pair ? 256 : 128);
+  p.n_tiles = K / pl.bn;
   p.k_steps = C / kB;
   p.rows = N;
   p.cols = K;
@@ -200,27 +243,29 @@ BRK_API int brk_fc_fwd(const void* x, const void* w, const float* bias, void* y,
   p.alpha = 1.0f;
   p.bias = bias;
   p.act = act;
-  if (const char* dbg = std::getenv("BRK_DEBUG_FLAGS")) p.debug_flags = std::atoi(dbg);
+  p.debug_flags = debug_flags();
+  p.debug_ts = g_debug_ts;
   g_launches.fetch_add(1);
-  return launch_engine(p, bn, 0, 0, static_cast<cudaStream_t>(stream));
+  return launch_engine(p, pl.bn, 0, pl.pair, 0, static_cast<cudaStream_t>(stream));
 }
 
-BRK_API int brk_fc_bwd_data(const void* dz, const void* w, const void* mask, void* dx, int N, int C,
-                            int K, int b_n, int b_c, int b_k, int dtype, void* stream) {
+BRK_API int brk_fc_bwd_data(const void* dz, const void* w, const void* mask, void* dx, float* colsum_ws,
+                            int N, int C, int K, int b_n, int b_c, int b_k, int dtype, void* stream) {
   int rc = check_fc(N, C, K, b_n, b_c, b_k, dtype);
   if (rc) return rc;
   EngineParams p;
   std::memset(&p, 0, sizeof(p));
-  const int m_tiles = N / 128;
-  const int bn = pick_bn(m_tiles, C);
+  p.colsum_ws = colsum_ws;
+  const Plan pl = choose_plan(N, C, K / kB, false);
+  const int brows = pl.pair ? pl.bn / 2 : pl.bn;
   // A = dZ (rows n, red k) K-major
   if ((rc = enc(&p.map_a, dz, act_layout(N, K), 64, 64, 1, 2))) return rc;
-  set_coords(p.ca, {0, 0, 0, 2}, {0, 0, 1, 0}, 1, 128 * 128, 0);
-  // B = W (rows c, red k) K-major: dims (k_in, c_in, cb, kb), box (64, 64, bn/64, 1)
-  if ((rc = enc(&p.map_b, w, w_layout(K, C), 64, 64, bn / 64, 1))) return rc;
-  set_coords(p.cb, {0, 0, bn / 64, 0}, {0, 0, 0, 1}, 1, bn * 128, 0);
-  p.m_tiles = m_tiles;
-  p.n_tiles = C / bn;
+  set_coords(p.ca, {0, 0, 0, 2}, {0, 0, 1, 0}, 128 * 128, 0);
+  // B = W (rows c, red k) K-major: dims (k_in, c_in, cb, kb), box (64, 64, brows/64, 1)
+  if ((rc = enc(&p.map_b, w, w_layout(K, C), 64, 64, brows / 64, 1))) return rc;
+  set_coords(p.cb, {0, 0, brows / 64, 0}, {0, 0, 0, 1}, brows * 128, 0);
+  p.m_tiles = N / (pl.pair ? 256 : 128);
+  p.n_tiles = C / pl.bn;
   p.k_steps = K / kB;
   p.rows = N;
   p.cols = C;
@@ -229,26 +274,56 @@ BRK_API int brk_fc_bwd_data(const void* dz, const void* w, const void* mask, voi
   p.om = OutMap{kB, (int64_t)(C / kB) * kB * kB, kB, kB, kB * kB, 1};
   p.alpha = 1.0f;
   p.mask = mask;
+  p.debug_flags = debug_flags();
+  p.debug_ts = g_debug_ts;
   g_launches.fetch_add(1);
-  return launch_engine(p, bn, 0, 0, static_cast<cudaStream_t>(stream));
+  return launch_engine(p, pl.bn, 0, pl.pair, 0, static_cast<cudaStream_t>(stream));
 }
 
-BRK_API int brk_fc_upd(const void* x, const void* dz, float* dw, void* w_sgd, float lr, int N, int C,
-                       int K, int b_n, int b_c, int b_k, int dtype, void* stream) {
+// Split-K workspace of brk_fc_upd: [counters: 4 KiB][fp32 partial tiles].
+static constexpr size_t kCounterBytes = 4096;
+
+BRK_API size_t brk_fc_upd_workspace(int N, int C, int K) {
+  if (N <= 0 || C <= 0 || K <= 0 || N % 128 || C % 128 || K % 128) return 0;
+  const Plan pl = choose_plan(C, K, N / kB, true);
+  if (pl.splits <= 1) return kCounterBytes;
+  return kCounterBytes + engine_split_ws_bytes(pl.tiles, pl.splits, pl.bn, pl.pair);
+}
+
+BRK_API int brk_fc_upd(const void* x, const void* dz, float* dw, void* w_sgd, float lr,
+                       const float* db_partials, int db_parts, float* db_out, float* bias_sgd, float bias_lr,
+                       void* workspace, size_t ws_bytes, int N, int C, int K, int b_n, int b_c, int b_k,
+                       int dtype, void* stream) {
   int rc = check_fc(N, C, K, b_n, b_c, b_k, dtype);
   if (rc) return rc;
   EngineParams p;
   std::memset(&p, 0, sizeof(p));
-  const int m_tiles = C / 128;
-  const int bn = pick_bn(m_tiles, K);
-  // A = X^T (rows c, red n) MN-major: box (c 64, n 64, cb 2, nb 1) -> 2 atoms
+  const Plan pl = choose_plan(C, K, N / kB, workspace != nullptr);
+  if (pl.splits > 1) {
+    if (ws_bytes < kCounterBytes + engine_split_ws_bytes(pl.tiles, pl.splits, pl.bn, pl.pair) ||
+        static_cast<size_t>(pl.tiles) * 2 * sizeof(unsigned) > kCounterBytes)
+      return set_error(BRK_ERR_CONTRACT, "fc_upd: workspace too small (see brk_fc_upd_workspace)");
+    p.k_splits = pl.splits;
+    p.split_counters = static_cast<unsigned*>(workspace);
+    p.split_ws = reinterpret_cast<float*>(static_cast<char*>(workspace) + kCounterBytes);
+  }
+  if (db_partials != nullptr) {
+    if (db_out == nullptr || db_parts <= 0) return set_error(BRK_ERR_CONTRACT, "fc_upd: db_partials needs db_out");
+    p.db_partials = db_partials;
+    p.db_parts = db_parts;
+    p.db_out = db_out;
+    p.bias_sgd = bias_sgd;
+    p.bias_lr = bias_lr;
+  }
+  const int brows = pl.pair ? pl.bn / 2 : pl.bn;
+  // A = X^T (rows c, red n) MN-major: box (c 64, n 64, cb 2, nb 1) -> 2 atoms of 64 rows
   if ((rc = enc(&p.map_a, x, act_layout(N, C), 64, 64, 2, 1))) return rc;
-  set_coords(p.ca, {0, 0, 2, 0}, {0, 0, 0, 1}, 1, 128 * 128, 1);
-  // B = dZ^T (rows k, red n) MN-major: box (k 64, n 64, kb bn/64, nb 1)
-  if ((rc = enc(&p.map_b, dz, act_layout(N, K), 64, 64, bn / 64, 1))) return rc;
-  set_coords(p.cb, {0, 0, bn / 64, 0}, {0, 0, 0, 1}, 1, bn * 128, 1);
-  p.m_tiles = m_tiles;
-  p.n_tiles = K / bn;
+  set_coords(p.ca, {0, 0, 2, 0}, {0, 0, 0, 1}, 128 * 128, 1);
+  // B = dZ^T (rows k, red n) MN-major: box (k 64, n 64, kb brows/64, nb 1)
+  if ((rc = enc(&p.map_b, dz, act_layout(N, K), 64, 64, brows / 64, 1))) return rc;
+  set_coords(p.cb, {0, 0, brows / 64, 0}, {0, 0, 0, 1}, brows * 128, 1);
+  p.m_tiles = C / (pl.pair ? 256 : 128);
+  p.n_tiles = K / pl.bn;
   p.k_steps = N / kB;
   p.rows = C;
   p.cols = K;
@@ -259,28 +334,42 @@ BRK_API int brk_fc_upd(const void* x, const void* dz, float* dw, void* w_sgd, fl
   p.alpha = 1.0f;
   p.sgd_w = w_sgd;
   p.sgd_lr = lr;
+  p.debug_flags = debug_flags();
+  p.debug_ts = g_debug_ts;
   g_launches.fetch_add(1);
-  return launch_engine(p, bn, 0, 0, static_cast<cudaStream_t>(stream));
+  return launch_engine(p, pl.bn, 0, pl.pair, 0, static_cast<cudaStream_t>(stream));
 }
 
-// dz_out = dy * (y > 0) when y != NULL (dz_out may alias dy), db = column sums.
-// workspace: >= kSplit*K floats + K/64 unsigned counters (zero-initialised once).
+// dz_out = dy * (y > 0) when y != NULL (dz_out may alias dy), db = column sums,
+// bias_sgd -= lr * db when bias_sgd != NULL.
+// workspace: brk_fc_bias_grad_workspace(K) bytes (zero-initialised once).
 BRK_API int brk_fc_bias_grad(const void* dy, const void* y, void* dz_out, float* db, void* workspace,
                              int N, int K, int b_n, int b_k, float* bias_sgd, float lr, void* stream) {
-  if (b_n != kB || b_k != kB || N % (kSplit * 1) || N % kB || K % kB)
-    return set_error(BRK_ERR_CONTRACT, "bias_grad needs b_n=b_k=64 and N, K multiples of 64");
-  if (N % kSplit) return set_error(BRK_ERR_CONTRACT, "bias_grad needs N % 16 == 0");
+  if (b_n != kB || b_k != kB || N % kB || K % kB || N % kSplit)
+    return set_error(BRK_ERR_CONTRACT, "bias_grad needs b_n=b_k=64, N and K multiples of 64");
   float* partial = static_cast<float*>(workspace);
   unsigned* counters = reinterpret_cast<unsigned*>(partial + static_cast<size_t>(kSplit) * K);
   dim3 grid(K / kB, kSplit);
   g_launches.fetch_add(1);
-  bias_grad_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(y),
-      static_cast<__nv_bfloat16*>(dz_out), db, partial, counters, N, K, bias_sgd, lr);
-  cudaError_t err = cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(256);
+  cfg.stream = static_cast<cudaStream_t>(stream);
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr.val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  cudaError_t err = cudaLaunchKernelEx(&cfg, bias_grad_kernel, static_cast<const __nv_bfloat16*>(dy),
+                                       static_cast<const __nv_bfloat16*>(y), static_cast<__nv_bfloat16*>(dz_out),
+                                       db, partial, counters, N, K, bias_sgd, lr);
   if (err != cudaSuccess) return set_cuda_error(err, "bias_grad launch");
   return BRK_OK;
 }
+
+// Diagnostic: subsequent engine launches record per-CTA phase timestamps into
+// ts (device, >= 8 * grid entries); NULL disables.
+BRK_API void brk_diag_set_timestamps(unsigned long long* ts) { g_debug_ts = ts; }
 
 BRK_API size_t brk_fc_bias_grad_workspace(int K) {
   return static_cast<size_t>(kSplit) * K * sizeof(float) + static_cast<size_t>(K / kB + 1) * sizeof(unsigned);

@@ -250,7 +250,7 @@ def fc_backward_data(params: FcParams, dz: BlockedTensor, mask: BlockedTensor | 
     dx = torch.empty((nb, cb, params.b_n, params.b_c), dtype=dt, device="cuda")
     if _engine_ok(params, dt):
         rc = _lib.load().brk_fc_bwd_data(dzd.data_ptr(), wd.data_ptr(), md.data_ptr() if md is not None else None,
-                                         dx.data_ptr(), params.n, params.c, params.k, 64, 64, 64,
+                                         dx.data_ptr(), None, params.n, params.c, params.k, 64, 64, 64,
                                          _lib.BRK_BF16, stream_ptr())
         _lib.check(rc, LayoutError)
     else:
@@ -296,10 +296,12 @@ def fc_weight_update(params: FcParams, x: BlockedTensor, dz: BlockedTensor, lr: 
             raise LayoutError("the fused SGD update needs device-resident weights (FcParams.to)")
         sgd_w = params.w.data
     if _engine_ok(params, dt) and (sgd_w is None or sgd_w.dtype == torch.bfloat16):
-        rc = _lib.load().brk_fc_upd(xd.data_ptr(), dzd.data_ptr(), dw.data_ptr(),
-                                    sgd_w.data_ptr() if sgd_w is not None else None,
-                                    float(lr or 0.0), params.n, params.c, params.k, 64, 64, 64,
-                                    _lib.BRK_BF16, stream_ptr())
+        lib = _lib.load()
+        ws = upd_workspace(params.n, params.c, params.k)
+        rc = lib.brk_fc_upd(xd.data_ptr(), dzd.data_ptr(), dw.data_ptr(),
+                            sgd_w.data_ptr() if sgd_w is not None else None, float(lr or 0.0),
+                            None, 0, None, None, 0.0, ws.data_ptr(), ws.numel(),
+                            params.n, params.c, params.k, 64, 64, 64, _lib.BRK_BF16, stream_ptr())
         _lib.check(rc, LayoutError)
     else:
         b_n, b_c, b_k = params.b_n, params.b_c, params.b_k
@@ -324,6 +326,19 @@ def fc_weight_update(params: FcParams, x: BlockedTensor, dz: BlockedTensor, lr: 
 
 
 _BIAS_WS: dict = {}
+_UPD_WS: dict = {}
+
+
+def upd_workspace(n: int, c: int, k: int):
+    """Cached, zero-initialised split-K workspace of the weight-update engine pass."""
+    torch = require_cuda()
+    key = (torch.cuda.current_device(), n, c, k)
+    ws = _UPD_WS.get(key)
+    if ws is None:
+        nbytes = max(int(_lib.load().brk_fc_upd_workspace(n, c, k)), 16)
+        ws = torch.zeros(nbytes, dtype=torch.uint8, device="cuda")
+        _UPD_WS[key] = ws
+    return ws
 
 
 def fc_bias_grad(dy: BlockedTensor, y: BlockedTensor | None = None):
@@ -333,7 +348,7 @@ def fc_bias_grad(dy: BlockedTensor, y: BlockedTensor | None = None):
     Deterministic (fixed summation order).
     """
     names = dy.logical_dims
-    if set(names) != {"n", "k"} or dy.n_outer != 2:
+    if len(names) != 2 or "n" not in names or dy.n_outer != 2 or len(dy.shape) != 4:
         raise LayoutError("dy must be an [N_b][K_b][b_n][b_k] blocked tensor")
     if y is not None and (y.shape != dy.shape):
         raise LayoutError("y must match dy's layout")
@@ -361,7 +376,9 @@ def fc_bias_grad(dy: BlockedTensor, y: BlockedTensor | None = None):
                                     dz.data_ptr() if yd is not None else None, db.data_ptr(), N, K, b_n, b_k,
                                     _lib.BRK_BF16 if dt == torch.bfloat16 else _lib.BRK_F32, stream_ptr())
     _lib.check(rc, LayoutError)
-    dz_bt = BlockedTensor(dz, n_outer=2, logical_dims=dict(dy.logical_dims))
+    # dz is the gradient of a layer OUTPUT: label its feature dim "k" (the
+    # layout bwd-data / weight-update expect), whatever dy was called
+    dz_bt = BlockedTensor(dz, n_outer=2, logical_dims={"n": (0, 2), "k": (1, 3)})
     if host:
         return db.cpu().numpy(), dz_bt.to("cpu")
     return db, dz_bt

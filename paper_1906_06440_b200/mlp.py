@@ -68,6 +68,11 @@ class MLP:
         self.lib = lib
         self.ws = [torch.zeros(lib.brk_fc_bias_grad_workspace(width), dtype=torch.uint8, device=device)
                    for _ in range(layers)]
+        # column-sum partials of dz_l (written by bwd-data of layer l+1, reduced by upd of layer l)
+        self.colsum = [torch.zeros(batch // 32, width, dtype=torch.float32, device=device)
+                       for _ in range(layers + 1)]
+        upd_bytes = max(int(lib.brk_fc_upd_workspace(batch, width, width)), 16)
+        self.upd_ws = [torch.zeros(upd_bytes, dtype=torch.uint8, device=device) for _ in range(layers)]
         self.graph = None
         self.launches_per_step = 0
 
@@ -105,20 +110,23 @@ class MLP:
                                          self.bias[L - 1].data_ptr() if apply_sgd else None, lr, stream))
         launches += 1
         for l in range(L, 0, -1):
-            # bwd-data first (it reads W_l before the fused SGD rewrites it)
+            # bwd-data first (it reads W_l before the fused SGD rewrites it); its epilogue
+            # applies layer l-1's ReLU mask and writes column-sum partials of dz_{l-1}
             mask = self.y[l - 1].data_ptr() if l > 1 else None
+            colsum = self.colsum[l - 1].data_ptr() if l > 1 else None
             self._check(lib.brk_fc_bwd_data(self.dz[l].data_ptr(), self.w[l - 1].data_ptr(), mask,
-                                            self.dz[l - 1].data_ptr(), n, c, c, B, B, B, _lib.BRK_BF16, stream))
+                                            self.dz[l - 1].data_ptr(), colsum, n, c, c, B, B, B,
+                                            _lib.BRK_BF16, stream))
             launches += 1
+            # weight update (+ SGD); for l < L it also reduces dz_l's column sums into db_l (+ bias SGD)
+            parts = self.colsum[l].data_ptr() if l < L else None
             self._check(lib.brk_fc_upd(self.y[l - 1].data_ptr(), self.dz[l].data_ptr(), self.dw[l - 1].data_ptr(),
-                                       self.w[l - 1].data_ptr() if apply_sgd else None, lr, n, c, c, B, B, B,
-                                       _lib.BRK_BF16, stream))
+                                       self.w[l - 1].data_ptr() if apply_sgd else None, lr,
+                                       parts, n // 32, self.db[l - 1].data_ptr() if parts else None,
+                                       self.bias[l - 1].data_ptr() if (parts and apply_sgd) else None, lr,
+                                       self.upd_ws[l - 1].data_ptr(), self.upd_ws[l - 1].numel(),
+                                       n, c, c, B, B, B, _lib.BRK_BF16, stream))
             launches += 1
-            if l > 1:
-                self._check(lib.brk_fc_bias_grad(self.dz[l - 1].data_ptr(), None, None, self.db[l - 2].data_ptr(),
-                                                 self.ws[l - 2].data_ptr(), n, c, B, B,
-                                                 self.bias[l - 2].data_ptr() if apply_sgd else None, lr, stream))
-                launches += 1
         return launches
 
     def step(self, stream: int | None = None) -> int:

@@ -24,6 +24,7 @@ from paper_1906_06440_b200.fc import (  # noqa: E402
     fc_weight_update,
 )
 from paper_1906_06440_b200.tensor import (  # noqa: E402
+    BlockedTensor,
     LayoutError,
     block_fc_activation,
     block_weight_2d,
@@ -110,6 +111,7 @@ def _device_layer(n, c, k, seed, act=Activation.RELU, b=64, dtype=torch.bfloat16
     p = FcParams.from_dense(w, n, b_n=b, b_c=b, b_k=b, activation=act, bias=bias).to("cuda", dtype)
     xb = block_fc_activation(x, b, b).to("cuda", dtype)
     dyb = block_fc_activation(dy, b, b).to("cuda", dtype)
+    dyb = BlockedTensor(dyb.data, n_outer=2, logical_dims={"n": (0, 2), "k": (1, 3)})  # output-gradient naming
     return w, x, bias, dy, p, xb, dyb
 
 
