@@ -1,0 +1,342 @@
+"""Direct convolution on blocked layouts — drop-in for ``brkernels.cnn`` plus the
+north-star backward-data and weight-update passes.
+
+Reference algorithm (``pkg/src/brkernels/cnn.py:201-334``, paper Alg. 4): for
+every (image, output-channel block, output row, pixel tile) the weight and
+input sub-blocks of all (r, s, c) triples form ONE batch-reduce GEMM, so the
+output tile is accumulated without ever being reloaded.  Here every such
+output block of a pass is one job of ONE grouped tcgen05 BRGEMM launch
+(``brk_brgemm_grouped``) whose device-side batch lists are exactly the
+reference's pointer lists (``cnn.py:241-252, 304-310``):
+
+* fwd   job (img, kb, oj): C = O[img][kb][oj][:]            (Q x b_k)
+        entries (c_b, r, s): A = W[kb][c_b][r][s]            (b_c x b_k)
+                              B = I_pad[img][c_b][oj*str+r][s::str]  (Q x b_c, row stride str*b_c)
+* bwd   "dual convolution": dI = conv(dO padded by R-1-pad,
+        flipped W with C<->K swapped) for stride 1; 1x1 stride-s layers
+        scatter a 1x1 GEMM to the strided input positions.
+* upd   job (kb, c_b, r, s): C = dW[kb][c_b][r][s]           (b_c x b_k)
+        entries (img, oj):   A = dO[img][kb][oj]             (Q x b_k)
+                             B = I_pad[img][c_b][oj*str+r][s::str]^T (b_c x Q)
+
+Zero padding is materialised on the device (the reference pads by copy,
+``cnn.py:234-237``).  All arithmetic runs in libbrk_sm100.so; there is no CPU
+fallback.  Strategies / worker counts of the CPU reference only reorder work
+and are accepted for API compatibility.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from enum import Enum
+
+import numpy as np
+
+from ._device import require_cuda
+from ._grouped import addr_table, run_grouped
+from .brgemm import get_default_precision
+from .tensor import (
+    BlockedTensor,
+    LayoutError,
+    clamp_block,
+    make_conv_output,
+)
+
+WEIGHT_SLICE_BUDGET = 512 * 1024
+STRATEGY_WEIGHT_BUDGET = 1024 * 1024
+DEFAULT_CHANNEL_BLOCK = 64
+
+
+class StrategyKind(Enum):
+    MINIBATCH_FIRST = "minibatch"
+    TASK_GRID = "task-grid"
+    FEATURE_MAP_FIRST = "feature-map"
+
+
+@dataclass(frozen=True)
+class ParallelStrategy:
+    kind: StrategyKind
+    workers: int = 1
+
+
+@dataclass
+class ConvSpec:
+    """Convolution descriptor plus blocking (reference cnn.py:52-135).
+
+    Same-padding ((r-1)/2) by default for odd filters; channel blocks default
+    to min(64, extent); ``b_q`` / ``cb_chunk`` are the CPU tiling knobs
+    (validated; the GPU reduces all of C_b, R, S in one TMEM chain).
+    """
+
+    n: int
+    c: int
+    k: int
+    h: int
+    w: int
+    r: int
+    s: int
+    stride: int = 1
+    pad_h: int | None = None
+    pad_w: int | None = None
+    b_c: int | None = None
+    b_k: int | None = None
+    b_q: int | None = None
+    cb_chunk: int | None = None
+
+    def __post_init__(self):
+        if self.pad_h is None:
+            if self.r % 2 == 0:
+                raise LayoutError(f"even filter height r={self.r} needs an explicit pad_h")
+            self.pad_h = (self.r - 1) // 2
+        if self.pad_w is None:
+            if self.s % 2 == 0:
+                raise LayoutError(f"even filter width s={self.s} needs an explicit pad_w")
+            self.pad_w = (self.s - 1) // 2
+        self.b_c = clamp_block(self.c, DEFAULT_CHANNEL_BLOCK if self.b_c is None else self.b_c)
+        self.b_k = clamp_block(self.k, DEFAULT_CHANNEL_BLOCK if self.b_k is None else self.b_k)
+        self.validate()
+
+    def validate(self) -> None:
+        for name in ("n", "c", "k", "h", "w", "r", "s"):
+            if getattr(self, name) < 1:
+                raise LayoutError(f"{name} must be >= 1, got {getattr(self, name)}")
+        if self.stride < 1:
+            raise LayoutError(f"stride must be >= 1, got {self.stride}")
+        if self.pad_h < 0 or self.pad_w < 0:
+            raise LayoutError("padding must be >= 0")
+        if self.c % self.b_c:
+            raise LayoutError(f"b_c={self.b_c} does not divide C={self.c}")
+        if self.k % self.b_k:
+            raise LayoutError(f"b_k={self.b_k} does not divide K={self.k}")
+        if self.h + 2 * self.pad_h < self.r or self.w + 2 * self.pad_w < self.s:
+            raise LayoutError("filter larger than padded input")
+        if self.out_h < 1 or self.out_w < 1:
+            raise LayoutError("output spatial extents must be >= 1")
+        if self.b_q is not None and self.b_q < 1:
+            raise LayoutError(f"b_q must be >= 1, got {self.b_q}")
+        if self.cb_chunk is not None and (self.cb_chunk < 1 or self.c_blocks % self.cb_chunk):
+            raise LayoutError(f"cb_chunk={self.cb_chunk} must divide C_b={self.c_blocks}")
+
+    @property
+    def out_h(self) -> int:
+        return (self.h + 2 * self.pad_h - self.r) // self.stride + 1
+
+    @property
+    def out_w(self) -> int:
+        return (self.w + 2 * self.pad_w - self.s) // self.stride + 1
+
+    @property
+    def c_blocks(self) -> int:
+        return self.c // self.b_c
+
+    @property
+    def k_blocks(self) -> int:
+        return self.k // self.b_k
+
+    @property
+    def weight_bytes(self) -> int:
+        return self.k * self.c * self.r * self.s * 4
+
+
+@dataclass(frozen=True)
+class PixelCollapse:
+    applied: bool
+    extent: int
+
+
+def collapse_pixels(spec: ConvSpec) -> PixelCollapse:
+    """1x1 unit-stride unpadded convolutions walk P*Q pixels as one extent (cnn.py:146-155)."""
+    ok = spec.r == 1 and spec.s == 1 and spec.stride == 1 and spec.pad_h == 0 and spec.pad_w == 0
+    return PixelCollapse(applied=ok, extent=spec.out_h * spec.out_w if ok else spec.out_w)
+
+
+def choose_strategy(spec: ConvSpec, workers: int, cache_budget: int = STRATEGY_WEIGHT_BUDGET) -> ParallelStrategy:
+    """Task-assignment strategy of the CPU reference (cnn.py:158-176); never changes results."""
+    if workers < 1:
+        raise ValueError(f"workers must be >= 1, got {workers}")
+    if spec.n >= workers:
+        kind = StrategyKind.MINIBATCH_FIRST
+    elif spec.weight_bytes > cache_budget:
+        kind = StrategyKind.FEATURE_MAP_FIRST
+    else:
+        kind = StrategyKind.TASK_GRID
+    return ParallelStrategy(kind=kind, workers=workers)
+
+
+def _check_layouts(spec: ConvSpec, inp: BlockedTensor, wgt: BlockedTensor) -> None:
+    want_in = {"n": spec.n, "c": spec.c, "h": spec.h, "w": spec.w}
+    if inp.logical_shape() != want_in or inp.inner_shape != (spec.b_c,):
+        raise LayoutError(f"input layout {inp.logical_shape()}/{inp.inner_shape} does not match spec")
+    want_w = {"k": spec.k, "c": spec.c, "r": spec.r, "s": spec.s}
+    if wgt.logical_shape() != want_w or wgt.inner_shape != (spec.b_c, spec.b_k):
+        raise LayoutError(f"weight layout {wgt.logical_shape()}/{wgt.inner_shape} does not match spec")
+
+
+def _dtype(precision, *tensors):
+    torch = require_cuda()
+    for t in tensors:
+        if t is not None and t.on_device and t.data.dtype == torch.bfloat16:
+            return "bf16", torch.bfloat16
+    prec = precision or get_default_precision()
+    return prec, (torch.bfloat16 if prec == "bf16" else torch.float32)
+
+
+def _stage(bt: BlockedTensor, dt):
+    if bt.on_device and bt.data.dtype == dt:
+        return bt.data.contiguous()
+    return bt.to("cuda", dt).data
+
+
+def _pad_device(x, pad_h, pad_w):
+    """[N][C_b][H][W][b_c] -> zero-padded copy (device plumbing)."""
+    torch = require_cuda()
+    if not pad_h and not pad_w:
+        return x
+    n, cb, h, w, bc = x.shape
+    out = torch.zeros((n, cb, h + 2 * pad_h, w + 2 * pad_w, bc), dtype=x.dtype, device=x.device)
+    out[:, :, pad_h:pad_h + h, pad_w:pad_w + w] = x
+    return out
+
+
+def _grid(*ranges, device="cuda"):
+    """Flattened index grids (row-major over the given extents) as int64 device tensors."""
+    torch = require_cuda()
+    axes = [torch.arange(r, device=device, dtype=torch.int64) for r in ranges]
+    mesh = torch.meshgrid(*axes, indexing="ij")
+    return [m.reshape(-1) for m in mesh]
+
+
+def conv2d_forward(spec: ConvSpec, inp: BlockedTensor, wgt: BlockedTensor, strategy: ParallelStrategy | None = None,
+                   collapse: bool | None = None, tile_force=None, precision: str | None = None) -> BlockedTensor:
+    """O[N][K_b][P][Q][b_k] from I[N][C_b][H][W][b_c] and W[K_b][C_b][R][S][b_c][b_k] (cnn.py:201-334)."""
+    spec.validate()
+    _check_layouts(spec, inp, wgt)
+    if strategy is not None and strategy.workers < 1:
+        raise ValueError(f"workers must be >= 1, got {strategy.workers}")
+    torch = require_cuda()
+    host = not inp.on_device
+    prec, dt = _dtype(precision, inp, wgt)
+    x = _pad_device(_stage(inp, dt), spec.pad_h, spec.pad_w)
+    w = _stage(wgt, dt)
+    p_, q_ = spec.out_h, spec.out_w
+    n, kb_n, cb_n, r_n, s_n = spec.n, spec.k_blocks, spec.c_blocks, spec.r, spec.s
+    b_c, b_k, st = spec.b_c, spec.b_k, spec.stride
+    hp, wp = spec.h + 2 * spec.pad_h, spec.w + 2 * spec.pad_w
+    out = torch.empty((n, kb_n, p_, q_, b_k), dtype=dt, device="cuda")
+    # jobs (img, kb, oj); entries (cb, r, s)
+    ji, jk, jo = _grid(n, kb_n, p_)
+    ec, er, es = _grid(cb_n, r_n, s_n)
+    a_off = (((jk[:, None] * cb_n + ec[None, :]) * r_n + er[None, :]) * s_n + es[None, :]) * (b_c * b_k)
+    b_off = (((ji[:, None] * cb_n + ec[None, :]) * hp + (jo[:, None] * st + er[None, :])) * wp + es[None, :]) * b_c
+    c_off = ((ji * kb_n + jk) * p_ + jo) * (q_ * b_k)
+    run_grouped(a_ptrs=addr_table(w, a_off.reshape(-1)), b_ptrs=addr_table(x, b_off.reshape(-1)),
+                c_ptrs=addr_table(out, c_off), m=b_k, n=q_, k=b_c, batch=cb_n * r_n * s_n,
+                a_sk=b_k, a_sm=1, b_sn=st * b_c, b_sk=1, ldc=b_k,
+                in_bf16=dt == torch.bfloat16, out_bf16=dt == torch.bfloat16, precision=prec, exc=LayoutError)
+    res = BlockedTensor(out, n_outer=4, logical_dims={"n": 0, "k": (1, 4), "p": 2, "q": 3})
+    return res.to("cpu") if host else res
+
+
+def conv2d_backward_data(spec: ConvSpec, dout: BlockedTensor, wgt: BlockedTensor,
+                         precision: str | None = None) -> BlockedTensor:
+    """dI[N][C_b][H][W][b_c] from dO[N][K_b][P][Q][b_k] (north star; restated in oracle/).
+
+    Stride 1: dual convolution of dO (padded by R-1-pad) with the flipped,
+    C<->K-swapped filter.  1x1 stride-s: a 1x1 GEMM scattered to the strided
+    input pixels (other pixels receive no gradient).
+    """
+    spec.validate()
+    want = {"n": spec.n, "k": spec.k, "p": spec.out_h, "q": spec.out_w}
+    if dout.logical_shape() != want or dout.inner_shape != (spec.b_k,):
+        raise LayoutError(f"dout layout {dout.logical_shape()}/{dout.inner_shape} does not match spec")
+    want_w = {"k": spec.k, "c": spec.c, "r": spec.r, "s": spec.s}
+    if wgt.logical_shape() != want_w or wgt.inner_shape != (spec.b_c, spec.b_k):
+        raise LayoutError("weight layout does not match spec")
+    torch = require_cuda()
+    host = not dout.on_device
+    prec, dt = _dtype(precision, dout, wgt)
+    do = _stage(dout, dt)
+    w = _stage(wgt, dt)
+    n, kb_n, cb_n, r_n, s_n = spec.n, spec.k_blocks, spec.c_blocks, spec.r, spec.s
+    b_c, b_k, st = spec.b_c, spec.b_k, spec.stride
+    p_, q_ = spec.out_h, spec.out_w
+    h, wd = spec.h, spec.w
+    din = torch.zeros((n, cb_n, h, wd, b_c), dtype=dt, device="cuda")
+    in_bf16 = dt == torch.bfloat16
+    if st == 1:
+        ph, pw = r_n - 1 - spec.pad_h, s_n - 1 - spec.pad_w
+        if ph < 0 or pw < 0:
+            raise LayoutError("backward-data needs pad <= filter-1")
+        dop = _pad_device(do, ph, pw)
+        hp, wp = p_ + 2 * ph, q_ + 2 * pw
+        # dual conv output extent must equal the input extent
+        if hp - r_n + 1 != h or wp - s_n + 1 != wd:
+            raise LayoutError("backward-data: stride-1 dual convolution does not reproduce the input extent")
+        ji, jc, jh = _grid(n, cb_n, h)
+        ek, er, es = _grid(kb_n, r_n, s_n)
+        # A_i = W[kb][cb][R-1-r][S-1-s] viewed (k = b_k rows, m = b_c cols): a_sk = 1, a_sm = b_k
+        a_off = (((ek[None, :] * cb_n + jc[:, None]) * r_n + (r_n - 1 - er[None, :])) * s_n
+                 + (s_n - 1 - es[None, :])) * (b_c * b_k)
+        b_off = (((ji[:, None] * kb_n + ek[None, :]) * hp + (jh[:, None] + er[None, :])) * wp + es[None, :]) * b_k
+        c_off = ((ji * cb_n + jc) * h + jh) * (wd * b_c)
+        run_grouped(a_ptrs=addr_table(w, a_off.reshape(-1)), b_ptrs=addr_table(dop, b_off.reshape(-1)),
+                    c_ptrs=addr_table(din, c_off), m=b_c, n=wd, k=b_k, batch=kb_n * r_n * s_n,
+                    a_sk=1, a_sm=b_k, b_sn=b_k, b_sk=1, ldc=b_c,
+                    in_bf16=in_bf16, out_bf16=in_bf16, precision=prec, exc=LayoutError)
+    elif r_n == 1 and s_n == 1:
+        # dI[n][cb][oj*st - pad][oi*st - pad] = sum_kb dO[n][kb][oj][oi] W[kb][cb]^T
+        if spec.pad_h or spec.pad_w:
+            raise LayoutError("backward-data for padded strided 1x1 convolutions is not supported")
+        ji, jc, jo = _grid(n, cb_n, p_)
+        ek = torch.arange(kb_n, device="cuda", dtype=torch.int64)
+        a_off = (ek[None, :] * cb_n + jc[:, None]) * (b_c * b_k)
+        b_off = ((ji[:, None] * kb_n + ek[None, :]) * p_ + jo[:, None]) * (q_ * b_k)
+        c_off = ((ji * cb_n + jc) * h + jo * st) * (wd * b_c)
+        run_grouped(a_ptrs=addr_table(w, a_off.reshape(-1)), b_ptrs=addr_table(do, b_off.reshape(-1)),
+                    c_ptrs=addr_table(din, c_off), m=b_c, n=q_, k=b_k, batch=kb_n,
+                    a_sk=1, a_sm=b_k, b_sn=b_k, b_sk=1, ldc=st * b_c,
+                    in_bf16=in_bf16, out_bf16=in_bf16, precision=prec, exc=LayoutError)
+    else:
+        raise LayoutError("backward-data supports stride 1 (any filter) and 1x1 strided convolutions")
+    res = BlockedTensor(din, n_outer=4, logical_dims={"n": 0, "c": (1, 4), "h": 2, "w": 3})
+    return res.to("cpu") if host else res
+
+
+def conv2d_weight_update(spec: ConvSpec, inp: BlockedTensor, dout: BlockedTensor,
+                         precision: str | None = None) -> BlockedTensor:
+    """dW[K_b][C_b][R][S][b_c][b_k] (fp32) = sum over (n, p, q) of dO x I_pad (north star)."""
+    spec.validate()
+    want_in = {"n": spec.n, "c": spec.c, "h": spec.h, "w": spec.w}
+    if inp.logical_shape() != want_in or inp.inner_shape != (spec.b_c,):
+        raise LayoutError("input layout does not match spec")
+    want = {"n": spec.n, "k": spec.k, "p": spec.out_h, "q": spec.out_w}
+    if dout.logical_shape() != want or dout.inner_shape != (spec.b_k,):
+        raise LayoutError("dout layout does not match spec")
+    torch = require_cuda()
+    host = not inp.on_device
+    prec, dt = _dtype(precision, inp, dout)
+    x = _pad_device(_stage(inp, dt), spec.pad_h, spec.pad_w)
+    do = _stage(dout, dt)
+    n, kb_n, cb_n, r_n, s_n = spec.n, spec.k_blocks, spec.c_blocks, spec.r, spec.s
+    b_c, b_k, st = spec.b_c, spec.b_k, spec.stride
+    p_, q_ = spec.out_h, spec.out_w
+    hp, wp = spec.h + 2 * spec.pad_h, spec.w + 2 * spec.pad_w
+    dw = torch.empty((kb_n, cb_n, r_n, s_n, b_c, b_k), dtype=torch.float32, device="cuda")
+    jk, jc, jr, js = _grid(kb_n, cb_n, r_n, s_n)
+    ei, eo = _grid(n, p_)
+    # A_i = dO[img][kb][oj] (k = Q pixels, m = b_k); B_i = I_pad[img][cb][oj*st+r][s::st]^T (n = b_c, k = Q)
+    a_off = ((ei[None, :] * kb_n + jk[:, None]) * p_ + eo[None, :]) * (q_ * b_k)
+    b_off = (((ei[None, :] * cb_n + jc[:, None]) * hp + (eo[None, :] * st + jr[:, None])) * wp + js[:, None]) * b_c
+    c_off = (((jk * cb_n + jc) * r_n + jr) * s_n + js) * (b_c * b_k)
+    run_grouped(a_ptrs=addr_table(do, a_off.reshape(-1)), b_ptrs=addr_table(x, b_off.reshape(-1)),
+                c_ptrs=addr_table(dw, c_off), m=b_k, n=b_c, k=q_, batch=n * p_,
+                a_sk=b_k, a_sm=1, b_sn=1, b_sk=st * b_c, ldc=b_k,
+                in_bf16=dt == torch.bfloat16, out_bf16=False, precision=prec, exc=LayoutError)
+    res = BlockedTensor(dw, n_outer=4, logical_dims={"k": (0, 5), "c": (1, 4), "r": 2, "s": 3})
+    return res.to("cpu") if host else res
+
+
+__all__ = [
+    "ConvSpec", "ParallelStrategy", "PixelCollapse", "StrategyKind", "choose_strategy", "collapse_pixels",
+    "conv2d_forward", "conv2d_backward_data", "conv2d_weight_update", "make_conv_output",
+]
