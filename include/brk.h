@@ -152,6 +152,29 @@ BRK_API int brk_colsum_blocked(const void* dy, const void* y, void* dz_out, floa
  * w in BRK_F32 or BRK_BF16 storage, dw fp32 in the same layout. */
 BRK_API int brk_sgd_apply(void* w, const float* dw, float lr, int64_t n, int w_dtype, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * LSTM recurrent steps (reference lstm.py:217-327, Eqs. 1-6; gate order
+ * i, c, f, o per lstm.py:28).  Storage fp32 (h, s, gates, gradients as in
+ * the reference), tensor-core inputs TF32 or BF16 (compute code).
+ *   R  : [4][K/b_k][K/b_k][b_k][b_k]  the four recurrent matrices, blocked as
+ *        block_weight_2d(r_g, b_k, b_k) (tensor.py:143-158)
+ *   gx : [N][4][K] = W_g x_t + b_g (precomputed for all t by one grouped BRGEMM)
+ * ------------------------------------------------------------------------- */
+/* Replaces the per-step work item of lstm_forward (lstm.py:268-317): one launch
+ * computes h_t, s_t and the activated gates [N][4][K] of all items. s_prev may be NULL (zeros). */
+BRK_API int brk_lstm_fwd_step(const float* h_prev, const float* s_prev, const float* gx, const float* R,
+                              float* h_out, float* s_out, float* gates_out, int N, int K, int b_k, int compute,
+                              void* stream);
+/* BPTT step (north star): dpre_t [N][4][K] and ds_out = ds * f from dh_in (dL/dh_t
+ * from the output), the recurrent gradient sum_g dpre_{t+1,g} R_g (dpre_next may be
+ * NULL at t = T-1), the stored gates / s_t / s_{t-1} (NULL = 0) and ds_in (NULL = 0). */
+BRK_API int brk_lstm_bwd_step(const float* dpre_next, const float* R, const float* dh_in, const float* gates,
+                              const float* s_cur, const float* s_prev, const float* ds_in, float* dpre_out,
+                              float* ds_out, int N, int K, int b_k, int compute, void* stream);
+/* out[N][K] = sum_g dpre[N][g][:] R_g  (gradient w.r.t. h_init). */
+BRK_API int brk_lstm_recurrent_grad(const float* dpre, const float* R, float* out, int N, int K, int b_k,
+                                    int compute, void* stream);
+
 /* Diagnostic (not on the product path): TMA global->shared streaming
  * throughput of `ctas` CTAs, each moving `iters` slots of loads_per_slot
  * boxes (64 bf16 x box_rows) of a rows x cols bf16 matrix through a ring of

@@ -47,6 +47,10 @@ SIGNATURES: dict[str, tuple] = {
                             _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _vp]),
     "brk_fc_upd_workspace": (ctypes.c_size_t, [_c_int, _c_int, _c_int]),
     "brk_diag_set_timestamps": (None, [_vp]),
+    "brk_lstm_fwd_step": (_c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp]),
+    "brk_lstm_bwd_step": (_c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int,
+                                   _vp]),
+    "brk_lstm_recurrent_grad": (_c_int, [_vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp]),
     "brk_diag_tmem_ld": (_c_int, [_c_int, _c_int, _vp, _vp]),
     "brk_diag_tma_bw": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int,
                                  ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_double)]),
