@@ -359,7 +359,7 @@ def main():
         run_reference(args, n_gpus, rank)
         return
     pg = None
-    if world > 1:
+    if world > 1 or os.environ.get("BRK_FORCE_DP") == "1":  # torchrun: NCCL data parallel
         import torch
         import torch.distributed as dist
 

@@ -99,8 +99,13 @@ class MLP:
                                        self.y[l + 1].data_ptr(), n, c, c, B, B, B, 1, _lib.BRK_BF16, stream))
         return self.L
 
-    def backward_update(self, stream: int, apply_sgd: bool = True) -> int:
-        """bwd-data + bias grad + weight update for all layers; returns launches issued."""
+    def backward_update(self, stream: int, apply_sgd: bool = True, reducer=None) -> int:
+        """bwd-data + bias grad + weight update for all layers; returns launches issued.
+
+        With a ``reducer`` (data parallel) each layer's (dW, db) all-reduce is
+        submitted on the communication stream right after its weight update,
+        overlapping the remaining backward passes.
+        """
         lib, n, c, L = self.lib, self.N, self.C, self.L
         lr = self.lr if apply_sgd else 0.0
         launches = 0
@@ -127,6 +132,8 @@ class MLP:
                                        self.upd_ws[l - 1].data_ptr(), self.upd_ws[l - 1].numel(),
                                        n, c, c, B, B, B, _lib.BRK_BF16, stream))
             launches += 1
+            if reducer is not None:
+                reducer.submit([self.dw[l - 1], self.db[l - 1]])
         return launches
 
     def step(self, stream: int | None = None) -> int:
@@ -136,28 +143,32 @@ class MLP:
         if self.pg is None:
             n = self.forward(s) + self.backward_update(s, apply_sgd=True)
         else:
-            n = self.forward(s) + self.backward_update(s, apply_sgd=False)
+            n = self.forward(s) + self.backward_update(s, apply_sgd=False, reducer=self._reducer())
             n += self._allreduce_apply(s)
         self.launches_per_step = n
         return n
 
-    def _allreduce_apply(self, stream: int) -> int:
-        """DP exchange: allreduce(sum) dW/db per layer, then SGD with lr / world."""
-        import torch.distributed as dist
+    def _reducer(self):
+        if getattr(self, "_grad_reducer", None) is None:
+            from .dist import GradientReducer
 
-        torch = self.torch
-        world = dist.get_world_size(self.pg)
+            self._grad_reducer = GradientReducer(group=self.pg)
+        return self._grad_reducer
+
+    def _allreduce_apply(self, stream: int) -> int:
+        """DP exchange: wait for the per-layer all-reduces (sum), then SGD with lr / world."""
+        from .dist import sgd_scale
+
+        red = self._reducer()
+        red.wait()
+        scale = sgd_scale(self.lr, red.world)
         launches = 0
         for l in range(self.L - 1, -1, -1):
-            dist.all_reduce(self.dw[l], group=self.pg)
-            dist.all_reduce(self.db[l], group=self.pg)
-            scale = self.lr / world
             self._check(self.lib.brk_sgd_apply(self.w[l].data_ptr(), self.dw[l].data_ptr(), scale,
                                                self.dw[l].numel(), _lib.BRK_BF16, stream))
             self._check(self.lib.brk_sgd_apply(self.bias[l].data_ptr(), self.db[l].data_ptr(), scale,
                                                self.db[l].numel(), _lib.BRK_F32, stream))
             launches += 2
-        del torch
         return launches
 
     # ------------------------------------------------------------------ graphs
