@@ -153,6 +153,35 @@ BRK_API int brk_colsum_blocked(const void* dy, const void* y, void* dz_out, floa
 BRK_API int brk_sgd_apply(void* w, const float* dw, float lr, int64_t n, int w_dtype, void* stream);
 
 /* ---------------------------------------------------------------------------
+ * Direct convolution on the reference's blocked layouts (cnn.py:201-334;
+ * tensor.py:160-235), implicit GEMM with TMA im2col operand fetch:
+ *   in, din : [N][C/64][H][W][64]     out, dout : [N][K/64][P][Q][64]
+ *   w       : [K/64][C/64][R][S][64 c][64 k]   dw : like w, fp32
+ * Engine path: bf16 storage, b_c = b_k = 64, C and K multiples of 64; stride
+ * 1 (pad <= 15, R, S <= 16) or 1x1 stride 2 without padding.
+ * ------------------------------------------------------------------------- */
+/* Replaces brkernels.cnn.conv2d_forward (cnn.py:201-334): out = act(conv(in, w) + bias);
+ * bias (fp32, K) may be NULL; act as brk_fc_fwd. */
+BRK_API int brk_conv_fwd(const void* in, const void* w, const float* bias, void* out, int N, int C, int K, int H,
+                         int W, int R, int S, int stride, int pad_h, int pad_w, int b_c, int b_k, int act, int dtype,
+                         void* stream);
+/* Backward-data (north star, the paper's dual convolution): din = conv^T(dout, w).
+ * Every element of din is written (1x1 stride 2: zeros at the odd positions). */
+BRK_API int brk_conv_bwd_data(const void* dout, const void* w, void* din, int N, int C, int K, int H, int W, int R,
+                              int S, int stride, int pad_h, int pad_w, int b_c, int b_k, int dtype, void* stream);
+/* Weight update (north star): dw = sum over (n, p, q) of dout x in (fp32); if w_sgd != NULL also
+ * w_sgd -= lr * dw (bf16 weights).  workspace: brk_conv_upd_workspace(...) bytes (may be 0 = NULL ok);
+ * deterministic (split partials are summed in split order). */
+BRK_API int brk_conv_upd(const void* in, const void* dout, float* dw, void* w_sgd, float lr, void* workspace,
+                         size_t ws_bytes, int N, int C, int K, int H, int W, int R, int S, int stride, int pad_h,
+                         int pad_w, int b_c, int b_k, int dtype, void* stream);
+BRK_API size_t brk_conv_upd_workspace(int N, int C, int K, int H, int W, int R, int S, int stride, int pad_h,
+                                      int pad_w);
+/* Diagnostic: engine tile plan of a pass (0 fwd, 1 bwd-data, 2 upd) -> out3 = {pair, bn, splits}. */
+BRK_API int brk_conv_plan(int pass, int N, int C, int K, int H, int W, int R, int S, int stride, int pad_h,
+                          int pad_w, int* out3);
+
+/* ---------------------------------------------------------------------------
  * LSTM recurrent steps (reference lstm.py:217-327, Eqs. 1-6; gate order
  * i, c, f, o per lstm.py:28).  Storage fp32 (h, s, gates, gradients as in
  * the reference), tensor-core inputs TF32 or BF16 (compute code).

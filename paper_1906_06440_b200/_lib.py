@@ -58,6 +58,11 @@ SIGNATURES: dict[str, tuple] = {
     "brk_fc_bias_grad_workspace": (ctypes.c_size_t, [_c_int]),
     "brk_colsum_blocked": (_c_int, [_vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp]),
     "brk_sgd_apply": (_c_int, [_vp, _vp, _c_f, _c_i64, _c_int, _vp]),
+    "brk_conv_fwd": (_c_int, [_vp, _vp, _vp, _vp] + [_c_int] * 14 + [_vp]),
+    "brk_conv_bwd_data": (_c_int, [_vp, _vp, _vp] + [_c_int] * 13 + [_vp]),
+    "brk_conv_upd": (_c_int, [_vp, _vp, _vp, _vp, _c_f, _vp, ctypes.c_size_t] + [_c_int] * 13 + [_vp]),
+    "brk_conv_upd_workspace": (ctypes.c_size_t, [_c_int] * 10),
+    "brk_conv_plan": (_c_int, [_c_int] * 11 + [ctypes.POINTER(_c_int)]),
     "brk_brgemm_offs": (
         _c_int,
         [_vp, _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_i64, _c_i64, _c_i64,

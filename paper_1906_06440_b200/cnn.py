@@ -32,7 +32,10 @@ from enum import Enum
 
 import numpy as np
 
-from ._device import require_cuda
+import os
+
+from . import _lib
+from ._device import require_cuda, stream_ptr
 from ._grouped import addr_table, run_grouped
 from .brgemm import get_default_precision
 from .tensor import (
@@ -198,6 +201,53 @@ def _pad_device(x, pad_h, pad_w):
     return out
 
 
+def _engine_ok(spec: "ConvSpec", dt, pass_: str, engine: bool | None) -> bool:
+    """Whether a pass runs on the implicit-GEMM tcgen05 engine (brk_conv_*):
+    bf16 storage, 64-channel blocks, stride 1 or 1x1 stride 2 (include/brk.h).
+    Everything else (fp32/TF32, other blockings, the 3-channel stem) runs on the
+    grouped BRGEMM path, which follows the reference's batch lists directly."""
+    torch = require_cuda()
+    if engine is False or os.environ.get("BRK_CONV_ENGINE", "1") == "0":
+        return False
+    ok = (dt == torch.bfloat16 and spec.b_c == 64 and spec.b_k == 64 and spec.c % 64 == 0
+          and spec.k % 64 == 0 and max(spec.pad_h, spec.pad_w) <= 15 and max(spec.r, spec.s) <= 16)
+    if ok and spec.stride == 1:
+        if pass_ == "bwd":
+            ok = spec.out_h == spec.h and spec.out_w == spec.w
+    elif ok:
+        ok = spec.stride == 2 and spec.r == 1 and spec.s == 1 and spec.pad_h == 0 and spec.pad_w == 0
+        if ok and pass_ == "bwd":
+            ok = spec.h == 2 * spec.out_h and spec.w == 2 * spec.out_w
+    if engine and not ok:
+        raise LayoutError(f"conv {pass_}: shape/dtype not served by the engine path")
+    return ok
+
+
+def _geom(spec: "ConvSpec"):
+    return (spec.n, spec.c, spec.k, spec.h, spec.w, spec.r, spec.s, spec.stride, spec.pad_h, spec.pad_w)
+
+
+_WS: dict = {}
+
+
+def _workspace(nbytes: int):
+    torch = require_cuda()
+    dev = torch.cuda.current_device()
+    buf = _WS.get(dev)
+    if nbytes and (buf is None or buf.numel() < nbytes):
+        buf = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+        _WS[dev] = buf
+    return buf
+
+
+def engine_plan(spec: "ConvSpec", pass_: int):
+    """(pair, BN, splits) the engine uses for pass 0 fwd / 1 bwd-data / 2 upd (diagnostic)."""
+    import ctypes
+    out = (ctypes.c_int * 3)()
+    _lib.check(_lib.load().brk_conv_plan(pass_, *_geom(spec), out), LayoutError)
+    return tuple(out)
+
+
 def _grid(*ranges, device="cuda"):
     """Flattened index grids (row-major over the given extents) as int64 device tensors."""
     torch = require_cuda()
@@ -207,8 +257,13 @@ def _grid(*ranges, device="cuda"):
 
 
 def conv2d_forward(spec: ConvSpec, inp: BlockedTensor, wgt: BlockedTensor, strategy: ParallelStrategy | None = None,
-                   collapse: bool | None = None, tile_force=None, precision: str | None = None) -> BlockedTensor:
-    """O[N][K_b][P][Q][b_k] from I[N][C_b][H][W][b_c] and W[K_b][C_b][R][S][b_c][b_k] (cnn.py:201-334)."""
+                   collapse: bool | None = None, tile_force=None, precision: str | None = None,
+                   engine: bool | None = None) -> BlockedTensor:
+    """O[N][K_b][P][Q][b_k] from I[N][C_b][H][W][b_c] and W[K_b][C_b][R][S][b_c][b_k] (cnn.py:201-334).
+
+    ``engine``: None = the implicit-GEMM engine when the shape allows it,
+    True = require it, False = the grouped BRGEMM path.
+    """
     spec.validate()
     _check_layouts(spec, inp, wgt)
     if strategy is not None and strategy.workers < 1:
@@ -216,6 +271,13 @@ def conv2d_forward(spec: ConvSpec, inp: BlockedTensor, wgt: BlockedTensor, strat
     torch = require_cuda()
     host = not inp.on_device
     prec, dt = _dtype(precision, inp, wgt)
+    if _engine_ok(spec, dt, "fwd", engine):
+        x, w = _stage(inp, dt), _stage(wgt, dt)
+        out = torch.empty((spec.n, spec.k_blocks, spec.out_h, spec.out_w, spec.b_k), dtype=dt, device="cuda")
+        _lib.check(_lib.load().brk_conv_fwd(x.data_ptr(), w.data_ptr(), None, out.data_ptr(), *_geom(spec), 64, 64,
+                                            0, _lib.BRK_BF16, stream_ptr()), LayoutError)
+        res = BlockedTensor(out, n_outer=4, logical_dims={"n": 0, "k": (1, 4), "p": 2, "q": 3})
+        return res.to("cpu") if host else res
     x = _pad_device(_stage(inp, dt), spec.pad_h, spec.pad_w)
     w = _stage(wgt, dt)
     p_, q_ = spec.out_h, spec.out_w
@@ -238,7 +300,7 @@ def conv2d_forward(spec: ConvSpec, inp: BlockedTensor, wgt: BlockedTensor, strat
 
 
 def conv2d_backward_data(spec: ConvSpec, dout: BlockedTensor, wgt: BlockedTensor,
-                         precision: str | None = None) -> BlockedTensor:
+                         precision: str | None = None, engine: bool | None = None) -> BlockedTensor:
     """dI[N][C_b][H][W][b_c] from dO[N][K_b][P][Q][b_k] (north star; restated in oracle/).
 
     Stride 1: dual convolution of dO (padded by R-1-pad) with the flipped,
@@ -257,6 +319,12 @@ def conv2d_backward_data(spec: ConvSpec, dout: BlockedTensor, wgt: BlockedTensor
     prec, dt = _dtype(precision, dout, wgt)
     do = _stage(dout, dt)
     w = _stage(wgt, dt)
+    if _engine_ok(spec, dt, "bwd", engine):
+        din = torch.empty((spec.n, spec.c_blocks, spec.h, spec.w, spec.b_c), dtype=dt, device="cuda")
+        _lib.check(_lib.load().brk_conv_bwd_data(do.data_ptr(), w.data_ptr(), din.data_ptr(), *_geom(spec), 64, 64,
+                                                 _lib.BRK_BF16, stream_ptr()), LayoutError)
+        res = BlockedTensor(din, n_outer=4, logical_dims={"n": 0, "c": (1, 4), "h": 2, "w": 3})
+        return res.to("cpu") if host else res
     n, kb_n, cb_n, r_n, s_n = spec.n, spec.k_blocks, spec.c_blocks, spec.r, spec.s
     b_c, b_k, st = spec.b_c, spec.b_k, spec.stride
     p_, q_ = spec.out_h, spec.out_w
@@ -303,7 +371,7 @@ def conv2d_backward_data(spec: ConvSpec, dout: BlockedTensor, wgt: BlockedTensor
 
 
 def conv2d_weight_update(spec: ConvSpec, inp: BlockedTensor, dout: BlockedTensor,
-                         precision: str | None = None) -> BlockedTensor:
+                         precision: str | None = None, engine: bool | None = None) -> BlockedTensor:
     """dW[K_b][C_b][R][S][b_c][b_k] (fp32) = sum over (n, p, q) of dO x I_pad (north star)."""
     spec.validate()
     want_in = {"n": spec.n, "c": spec.c, "h": spec.h, "w": spec.w}
@@ -315,6 +383,18 @@ def conv2d_weight_update(spec: ConvSpec, inp: BlockedTensor, dout: BlockedTensor
     torch = require_cuda()
     host = not inp.on_device
     prec, dt = _dtype(precision, inp, dout)
+    if _engine_ok(spec, dt, "upd", engine):
+        x, do = _stage(inp, dt), _stage(dout, dt)
+        dw = torch.empty((spec.k_blocks, spec.c_blocks, spec.r, spec.s, spec.b_c, spec.b_k), dtype=torch.float32,
+                         device="cuda")
+        lib = _lib.load()
+        nbytes = lib.brk_conv_upd_workspace(*_geom(spec))
+        ws = _workspace(nbytes)
+        _lib.check(lib.brk_conv_upd(x.data_ptr(), do.data_ptr(), dw.data_ptr(), None, 0.0,
+                                    ws.data_ptr() if nbytes else None, nbytes, *_geom(spec), 64, 64,
+                                    _lib.BRK_BF16, stream_ptr()), LayoutError)
+        res = BlockedTensor(dw, n_outer=4, logical_dims={"k": (0, 5), "c": (1, 4), "r": 2, "s": 3})
+        return res.to("cpu") if host else res
     x = _pad_device(_stage(inp, dt), spec.pad_h, spec.pad_w)
     do = _stage(dout, dt)
     n, kb_n, cb_n, r_n, s_n = spec.n, spec.k_blocks, spec.c_blocks, spec.r, spec.s
@@ -338,5 +418,5 @@ def conv2d_weight_update(spec: ConvSpec, inp: BlockedTensor, dout: BlockedTensor
 
 __all__ = [
     "ConvSpec", "ParallelStrategy", "PixelCollapse", "StrategyKind", "choose_strategy", "collapse_pixels",
-    "conv2d_forward", "conv2d_backward_data", "conv2d_weight_update", "make_conv_output",
+    "conv2d_forward", "conv2d_backward_data", "conv2d_weight_update", "engine_plan", "make_conv_output",
 ]

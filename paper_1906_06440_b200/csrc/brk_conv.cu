@@ -1,0 +1,428 @@
+// brk_conv.cu — direct convolution on the reference's blocked layouts
+// (cnn.py:201-334; tensor.py:160-235) as implicit-GEMM launches of the tcgen05
+// BRGEMM engine, each pass ONE launch whose per-tile batch list is the
+// reference's (c_b, r, s) list (Alg. 4):
+//
+//   fwd : O [N][K_b][P][Q][64]  rows = output pixels, batch over (c_b, r, s)
+//   bwd : dI[N][C_b][H][W][64]  "dual convolution": stride 1 is
+//         a convolution of dO (padding R-1-pad) with the flipped, C<->K
+//         swapped filter; 1x1 stride 2 scatters the 1x1 GEMM to the even input
+//         positions and zero-fills the rest in the same epilogue
+//   upd : dW[K_b][C_b][R][S][64 c][64 k] (fp32)  rows = (r, s, c), batch over
+//         pixel chunks of 64, split across CTAs into fp32 slices that a
+//         deterministic reduction sums in split order
+//
+// The activation side of every pass is fetched by TMA in im2col mode: the
+// blocked tensor [N][X_b][H][W][64] is a 5-d map (64 ch, W, H, N, X_b) whose
+// pixel walk (W, H, then N) is the GEMM row / reduction order; padding comes
+// from the map's bounding box (zero fill), so no padded copy is materialised
+// (the reference pads by copy, cnn.py:234-237).  Filter taps are im2col
+// offsets; channel blocks are the outermost coordinate.  Weights are tiled
+// 5-d maps (64 k, 64 c, RS, C_b, K_b); the backward pass reads them K-major
+// at the flipped tap (no transposed copy).
+//
+// Engine path contract: bf16 storage, b_c = b_k = 64, C, K multiples of 64;
+// stride 1 (any odd R = S with same padding) or 1x1 stride 2 (even H, W).
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <cuda_bf16.h>
+
+#include "brk_engine.h"
+#include "brk_internal.h"
+#include "brk_ptx.cuh"
+#include "brk_tma_host.h"
+
+namespace brk {
+
+int launch_engine(const EngineParams& p, int bn, int tf32, int pair, int max_units, cudaStream_t stream);
+int engine_sm_count();
+
+namespace {
+
+constexpr int kB = 64;
+
+struct ConvGeom {
+  int N, C, K, H, W, R, S, stride, pad_h, pad_w, P, Q;
+};
+
+int check_conv(const ConvGeom& g, int b_c, int b_k, int dtype) {
+  char buf[256];
+  if (dtype != BRK_BF16) return set_error(BRK_ERR_CONTRACT, "conv engine path: bf16 storage only");
+  if (b_c != kB || b_k != kB) {
+    std::snprintf(buf, sizeof(buf), "conv engine path needs b_c=b_k=64, got (%d,%d)", b_c, b_k);
+    return set_error(BRK_ERR_CONTRACT, buf);
+  }
+  if (g.N <= 0 || g.C <= 0 || g.K <= 0 || g.C % kB || g.K % kB || g.H <= 0 || g.W <= 0 || g.R <= 0 ||
+      g.S <= 0) {
+    std::snprintf(buf, sizeof(buf), "conv engine path needs C, K multiples of 64 (C=%d K=%d)", g.C, g.K);
+    return set_error(BRK_ERR_CONTRACT, buf);
+  }
+  if (g.P <= 0 || g.Q <= 0) return set_error(BRK_ERR_CONTRACT, "conv: empty output");
+  if (g.stride != 1 && !(g.stride == 2 && g.R == 1 && g.S == 1 && g.pad_h == 0 && g.pad_w == 0))
+    return set_error(BRK_ERR_CONTRACT, "conv engine path: stride 1, or 1x1 stride 2 without padding");
+  if (g.pad_h > 15 || g.pad_w > 15 || g.R > 16 || g.S > 16)
+    return set_error(BRK_ERR_CONTRACT, "conv engine path: filter / padding too large for im2col corners");
+  if (static_cast<int64_t>(g.N) * g.H * g.W >= (int64_t(1) << 31))
+    return set_error(BRK_ERR_CONTRACT, "conv engine path: N*H*W must fit int32");
+  return BRK_OK;
+}
+
+struct ConvPlan {
+  int pair, bn, splits;
+  int64_t tiles;
+};
+
+// Tile choice for rows x cols outputs (rows need not divide the tile: the
+// pixel walk is clamped and the epilogue masks).  Per-SM tensor-pipe efficiency
+// in SS mode (measured on the MLP shapes): CTA pair N=256 ~1, N=128 ~2/3;
+// single CTA N=256 ~2/3, N=128 ~1/2, N=64 ~1/3.
+ConvPlan choose(int64_t rows, int cols, int k_steps, bool split_ok) {
+  int forced_pair = -1, forced_bn = 0, forced_splits = 0;
+  if (const char* env = std::getenv("BRK_CONV_TILE")) std::sscanf(env, "%d,%d", &forced_pair, &forced_bn);
+  if (const char* env = std::getenv("BRK_CONV_SPLITS")) forced_splits = std::atoi(env);
+  struct Opt { int pair, bn; double eff; };
+  const Opt opts[] = {{1, 256, 1.0}, {1, 128, 0.67}, {0, 256, 0.67}, {0, 128, 0.5}, {0, 64, 0.4}};
+  const int sms = engine_sm_count();
+  ConvPlan best{0, 0, 1, 0};
+  double best_cost = 0;
+  for (const Opt& o : opts) {
+    if (cols % o.bn) continue;
+    if (forced_pair >= 0 && (o.pair != forced_pair || o.bn != forced_bn)) continue;
+    const int tr = o.pair ? 256 : 128;
+    const int64_t tiles = ((rows + tr - 1) / tr) * (cols / o.bn);
+    const int64_t units = o.pair ? sms / 2 : sms;
+    const double per_tile = static_cast<double>(tr) * o.bn * k_steps / ((o.pair ? 2.0 : 1.0) * o.eff);
+    int max_split = 1;
+    if (split_ok) max_split = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(k_steps / 8, 2 * units / std::max<int64_t>(1, tiles))));
+    if (forced_splits > 0) max_split = std::min(forced_splits, std::max(1, k_steps));
+    for (int sp = forced_splits > 0 ? max_split : 1; sp <= max_split; ++sp) {
+      const int64_t work = tiles * sp;
+      const int64_t waves = (work + units - 1) / units;
+      const double cost = waves * per_tile / sp + (sp > 1 ? 0.05 * per_tile : 0.0) + 2.0e5;
+      if (best.bn == 0 || cost < best_cost) {
+        // every split must own >= 1 k-step: ceil(k / ceil(k / sp)) splits
+        const int per = (k_steps + sp - 1) / sp;
+        best = ConvPlan{o.pair, o.bn, (k_steps + per - 1) / per, tiles};
+        best_cost = cost;
+      }
+    }
+  }
+  return best;
+}
+
+// 5-d im2col map over a blocked activation [N][X_b][Hh][Ww][64]:
+// dims (64, Ww, Hh, N, X_b).  The filter window of output pixel (p, q) starts
+// at (p*stride - pad_h, q*stride - pad_w); the last pixel's window ends at
+// (P-1)*stride - pad + R-1, expressed as the bounding-box upper corner.
+int im2col_map(CUtensorMap* map, const void* ptr, int N, int X, int Hh, int Ww, int R, int S, int stride,
+               int pad_h, int pad_w, uint32_t pixels) {
+  const uint64_t dims[5] = {kB, (uint64_t)Ww, (uint64_t)Hh, (uint64_t)N, (uint64_t)(X / kB)};
+  const uint64_t hw = (uint64_t)Hh * Ww * kB;
+  const uint64_t strides[5] = {1, kB, (uint64_t)Ww * kB, (uint64_t)(X / kB) * hw, hw};
+  const int lower[3] = {-pad_w, -pad_h, 0};
+  // 2 extra images of zero fill past N: a K-side pixel walk that runs off the
+  // end reads zeros instead of wrapping into the next channel block.
+  const int upper[3] = {pad_w - (S - 1), pad_h - (R - 1), 2};
+  const uint32_t es[5] = {1, (uint32_t)stride, (uint32_t)stride, 1, 1};
+  return encode_tmap_im2col(map, ptr, dims, strides, lower, upper, kB, pixels, es);
+}
+
+// Weights [K_b][C_b][R][S][64 c][64 k]: dims (64 k, 64 c, RS, C_b, K_b)
+int weight_map(CUtensorMap* map, const void* w, int C, int K, int RS, uint32_t box_cb, uint32_t box_kb) {
+  const uint64_t dims[5] = {kB, kB, (uint64_t)RS, (uint64_t)(C / kB), (uint64_t)(K / kB)};
+  const uint64_t strides[5] = {1, kB, kB * kB, (uint64_t)RS * kB * kB, (uint64_t)(C / kB) * RS * kB * kB};
+  const uint32_t box[5] = {kB, kB, 1, box_cb, box_kb};
+  return encode_tmap(map, w, true, 5, dims, strides, box);
+}
+
+void init_params(EngineParams& p) {
+  std::memset(&p, 0, sizeof(p));
+  p.ca.kdiv0 = p.cb.kdiv0 = 1 << 30;
+  p.ca.kdiv1 = p.cb.kdiv1 = 1;
+  p.alpha = 1.0f;
+  p.om.rb2 = int64_t(1) << 62;
+  const char* dbg = std::getenv("BRK_DEBUG_FLAGS");
+  p.debug_flags = dbg ? std::atoi(dbg) : 0;
+}
+
+void pixel_walk(OperandCoords& oc, int kind, int P, int Q, int stride, int pad_h, int pad_w, int64_t total) {
+  oc.kind = kind;
+  oc.P = P;
+  oc.Q = Q;
+  oc.cstride = stride;
+  oc.pad_h = pad_h;
+  oc.pad_w = pad_w;
+  oc.total_pix = static_cast<int32_t>(total);
+  oc.ndims = 5;
+}
+
+// dW[i] = sum_s ws[s * n + i] in split order (deterministic), optional SGD on
+// bf16 weights in the same layout.
+__global__ void __launch_bounds__(256) split_reduce_kernel(const float4* __restrict__ ws, int splits, int64_t n4,
+                                                           float4* __restrict__ dw, __nv_bfloat16* w_sgd, float lr) {
+  pdl_launch_dependents();
+  pdl_wait();
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float4 a = __ldcs(ws + i);
+    for (int s = 1; s < splits; ++s) {
+      const float4 b = __ldcs(ws + s * n4 + i);
+      a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+    }
+    dw[i] = a;
+    if (w_sgd != nullptr) {
+      __nv_bfloat162* w2 = reinterpret_cast<__nv_bfloat162*>(w_sgd) + 2 * i;
+      const float2 w0 = __bfloat1622float2(w2[0]), w1 = __bfloat1622float2(w2[1]);
+      w2[0] = __floats2bfloat162_rn(w0.x - lr * a.x, w0.y - lr * a.y);
+      w2[1] = __floats2bfloat162_rn(w1.x - lr * a.z, w1.y - lr * a.w);
+    }
+  }
+}
+
+int launch_split_reduce(const float* ws, int splits, int64_t n, float* dw, void* w_sgd, float lr,
+                        cudaStream_t stream) {
+  const int64_t n4 = n / 4;
+  int blocks = static_cast<int>(std::min<int64_t>((n4 + 255) / 256, 4 * engine_sm_count()));
+  if (blocks < 1) blocks = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(256);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr.val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  g_launches.fetch_add(1);
+  cudaError_t err = cudaLaunchKernelEx(&cfg, split_reduce_kernel, reinterpret_cast<const float4*>(ws), splits, n4,
+                                       reinterpret_cast<float4*>(dw), static_cast<__nv_bfloat16*>(w_sgd), lr);
+  if (err != cudaSuccess) return set_cuda_error(err, "conv split reduce launch");
+  return BRK_OK;
+}
+
+ConvGeom geom(int N, int C, int K, int H, int W, int R, int S, int stride, int pad_h, int pad_w) {
+  ConvGeom g{N, C, K, H, W, R, S, stride, pad_h, pad_w, 0, 0};
+  if (stride > 0) {
+    g.P = (H + 2 * pad_h - R) / stride + 1;
+    g.Q = (W + 2 * pad_w - S) / stride + 1;
+  }
+  return g;
+}
+
+ConvPlan upd_plan(const ConvGeom& g) {
+  const int64_t atoms = static_cast<int64_t>(g.C / kB) * g.R * g.S;
+  const int64_t pix = static_cast<int64_t>(g.N) * g.P * g.Q;
+  const int k_steps = static_cast<int>((pix + 63) / 64);
+  return choose(atoms * kB, g.K, k_steps, true);
+}
+
+}  // namespace
+}  // namespace brk
+
+using namespace brk;
+
+extern "C" {
+
+BRK_API int brk_conv_fwd(const void* in, const void* w, const float* bias, void* out, int N, int C, int K, int H,
+                         int W, int R, int S, int stride, int pad_h, int pad_w, int b_c, int b_k, int act, int dtype,
+                         void* stream) {
+  const ConvGeom g = geom(N, C, K, H, W, R, S, stride, pad_h, pad_w);
+  int rc = check_conv(g, b_c, b_k, dtype);
+  if (rc) return rc;
+  if (act < kActNone || act > kActSigmoid) return set_error(BRK_ERR_CONTRACT, "unknown activation");
+  const int64_t rows = static_cast<int64_t>(N) * g.P * g.Q;
+  const int k_steps = (C / kB) * R * S;
+  const ConvPlan pl = choose(rows, K, k_steps, false);
+  if (pl.bn == 0) return set_error(BRK_ERR_CONTRACT, "conv fwd: no engine tile fits K");
+  const int brows = pl.pair ? pl.bn / 2 : pl.bn;
+  EngineParams p;
+  init_params(p);
+  // A: input pixels (K-major rows of 64 channels), taps (s, r) as im2col offsets
+  if ((rc = im2col_map(&p.map_a, in, N, C, H, W, R, S, stride, pad_h, pad_w, 128))) return rc;
+  p.ca.kdiv0 = S;
+  p.ca.kdiv1 = R;
+  p.ca.kc[2][4] = 1;  // channel block c_b = d2
+  p.ca.ok[0][0] = 1;  // w tap = s
+  p.ca.ok[1][1] = 1;  // h tap = r
+  p.ca.n_loads = 1;
+  p.ca.load_bytes = 128 * 128;
+  p.ca.mn_major = 0;
+  pixel_walk(p.ca, 1, g.P, g.Q, stride, pad_h, pad_w, rows);
+  // B: W[kb][c_b][r][s] (64 c x 64 k, k contiguous = MN-major), brows/64 K blocks
+  if ((rc = weight_map(&p.map_b, w, C, K, R * S, 1, brows / kB))) return rc;
+  p.cb.kdiv0 = S;
+  p.cb.kdiv1 = R;
+  p.cb.kc[0][2] = 1;
+  p.cb.kc[1][2] = S;
+  p.cb.kc[2][3] = 1;
+  p.cb.rc[4] = brows / kB;
+  p.cb.n_loads = 1;
+  p.cb.load_bytes = brows * 128;
+  p.cb.mn_major = 1;
+  p.cb.ndims = 5;
+  p.m_tiles = static_cast<int>((rows + (pl.pair ? 255 : 127)) / (pl.pair ? 256 : 128));
+  p.n_tiles = K / pl.bn;
+  p.k_steps = k_steps;
+  p.rows = static_cast<int>(rows);
+  p.cols = K;
+  p.out = out;
+  p.out_bf16 = 1;
+  const int64_t pq = static_cast<int64_t>(g.P) * g.Q;
+  p.om = OutMap{pq, 0, kB, kB, pq * kB, 1, pq, (int64_t)(K / kB) * pq * kB};
+  p.bias = bias;
+  p.act = act;
+  g_launches.fetch_add(1);
+  return launch_engine(p, pl.bn, 0, pl.pair, 0, static_cast<cudaStream_t>(stream));
+}
+
+BRK_API int brk_conv_bwd_data(const void* dout, const void* w, void* din, int N, int C, int K, int H, int W, int R,
+                              int S, int stride, int pad_h, int pad_w, int b_c, int b_k, int dtype, void* stream) {
+  const ConvGeom g = geom(N, C, K, H, W, R, S, stride, pad_h, pad_w);
+  int rc = check_conv(g, b_c, b_k, dtype);
+  if (rc) return rc;
+  if (stride == 1 && (g.P != H || g.Q != W))
+    return set_error(BRK_ERR_CONTRACT, "conv bwd engine path: stride 1 needs same padding");
+  if (stride == 2 && (H != 2 * g.P || W != 2 * g.Q))
+    return set_error(BRK_ERR_CONTRACT, "conv bwd engine path: 1x1 stride 2 needs even H, W");
+  EngineParams p;
+  init_params(p);
+  // rows: input pixels (stride 1) or output pixels scattered to (2p, 2q) (stride 2)
+  const int64_t rows = stride == 1 ? static_cast<int64_t>(N) * H * W : static_cast<int64_t>(N) * g.P * g.Q;
+  const int k_steps = (K / kB) * R * S;
+  const ConvPlan pl = choose(rows, C, k_steps, false);
+  if (pl.bn == 0) return set_error(BRK_ERR_CONTRACT, "conv bwd: no engine tile fits C");
+  const int brows = pl.pair ? pl.bn / 2 : pl.bn;
+  // A: dO pixels; the dual convolution pads by R-1-pad and walks taps (s', r')
+  const int dph = stride == 1 ? R - 1 - pad_h : 0, dpw = stride == 1 ? S - 1 - pad_w : 0;
+  if ((rc = im2col_map(&p.map_a, dout, N, K, g.P, g.Q, R, S, 1, dph, dpw, 128))) return rc;
+  p.ca.kdiv0 = S;
+  p.ca.kdiv1 = R;
+  p.ca.kc[2][4] = 1;  // output-channel block k_b = d2
+  p.ca.ok[0][0] = 1;
+  p.ca.ok[1][1] = 1;
+  p.ca.n_loads = 1;
+  p.ca.load_bytes = 128 * 128;
+  p.ca.mn_major = 0;
+  if (stride == 1) pixel_walk(p.ca, 1, H, W, 1, dph, dpw, rows);
+  else pixel_walk(p.ca, 1, g.P, g.Q, 1, 0, 0, rows);
+  // B: W[kb][cb][R-1-r'][S-1-s'] read K-major (rows c, 64 k contiguous)
+  if ((rc = weight_map(&p.map_b, w, C, K, R * S, brows / kB, 1))) return rc;
+  p.cb.kdiv0 = S;
+  p.cb.kdiv1 = R;
+  p.cb.base[2] = R * S - 1;
+  p.cb.kc[0][2] = -1;
+  p.cb.kc[1][2] = -S;
+  p.cb.kc[2][4] = 1;
+  p.cb.rc[3] = brows / kB;
+  p.cb.n_loads = 1;
+  p.cb.load_bytes = brows * 128;
+  p.cb.mn_major = 0;
+  p.cb.ndims = 5;
+  p.m_tiles = static_cast<int>((rows + (pl.pair ? 255 : 127)) / (pl.pair ? 256 : 128));
+  p.n_tiles = C / pl.bn;
+  p.k_steps = k_steps;
+  p.rows = static_cast<int>(rows);
+  p.cols = C;
+  p.out = din;
+  p.out_bf16 = 1;
+  const int64_t hw = static_cast<int64_t>(H) * W;
+  if (stride == 1) {
+    p.om = OutMap{hw, 0, kB, kB, hw * kB, 1, hw, (int64_t)(C / kB) * hw * kB};
+  } else {
+    const int64_t pq = static_cast<int64_t>(g.P) * g.Q;
+    p.om = OutMap{g.Q, 2 * (int64_t)W * kB, 2 * kB, kB, hw * kB, 1, pq, (int64_t)(C / kB) * hw * kB};
+    p.zf_w = kB;
+    p.zf_h = static_cast<int64_t>(W) * kB;
+  }
+  g_launches.fetch_add(1);
+  return launch_engine(p, pl.bn, 0, pl.pair, 0, static_cast<cudaStream_t>(stream));
+}
+
+BRK_API size_t brk_conv_upd_workspace(int N, int C, int K, int H, int W, int R, int S, int stride, int pad_h,
+                                      int pad_w) {
+  const ConvGeom g = geom(N, C, K, H, W, R, S, stride, pad_h, pad_w);
+  if (check_conv(g, kB, kB, BRK_BF16)) return 0;
+  const ConvPlan pl = upd_plan(g);
+  if (pl.splits <= 1) return 0;
+  return static_cast<size_t>(pl.splits) * C * K * R * S * sizeof(float);
+}
+
+BRK_API int brk_conv_upd(const void* in, const void* dout, float* dw, void* w_sgd, float lr, void* workspace,
+                         size_t ws_bytes, int N, int C, int K, int H, int W, int R, int S, int stride, int pad_h,
+                         int pad_w, int b_c, int b_k, int dtype, void* stream) {
+  const ConvGeom g = geom(N, C, K, H, W, R, S, stride, pad_h, pad_w);
+  int rc = check_conv(g, b_c, b_k, dtype);
+  if (rc) return rc;
+  ConvPlan pl = upd_plan(g);
+  if (pl.bn == 0) return set_error(BRK_ERR_CONTRACT, "conv upd: no engine tile fits K");
+  const int64_t dw_elems = static_cast<int64_t>(C) * K * R * S;
+  if (pl.splits > 1 && (workspace == nullptr || ws_bytes < static_cast<size_t>(pl.splits) * dw_elems * 4))
+    return set_error(BRK_ERR_CONTRACT, "conv upd: workspace too small (see brk_conv_upd_workspace)");
+  const int brows = pl.pair ? pl.bn / 2 : pl.bn;
+  const int64_t pix = static_cast<int64_t>(N) * g.P * g.Q;
+  const int64_t atoms = static_cast<int64_t>(C / kB) * R * S;
+  EngineParams p;
+  init_params(p);
+  // A: input pixels (K side, 64 per step) as 2 MN-major atoms (c_b, rs) of 64 channels
+  if ((rc = im2col_map(&p.map_a, in, N, C, H, W, R, S, stride, pad_h, pad_w, 64))) return rc;
+  p.ca.n_loads = 2;
+  p.ca.load_bytes = 64 * 128;
+  p.ca.mn_major = 1;
+  p.ca.atom_cb = C / kB;
+  p.ca.atom_s = S;
+  pixel_walk(p.ca, 2, g.P, g.Q, stride, pad_h, pad_w, pix);
+  // B: dO pixels (K side) as brows/64 MN-major atoms of 64 output channels
+  if ((rc = im2col_map(&p.map_b, dout, N, K, g.P, g.Q, 1, 1, 1, 0, 0, 64))) return rc;
+  p.cb.rc[4] = brows / kB;
+  p.cb.lc[4] = 1;
+  p.cb.n_loads = brows / kB;
+  p.cb.load_bytes = 64 * 128;
+  p.cb.mn_major = 1;
+  pixel_walk(p.cb, 3, g.P, g.Q, 1, 0, 0, pix);
+  p.m_tiles = static_cast<int>((atoms * kB + (pl.pair ? 255 : 127)) / (pl.pair ? 256 : 128));
+  p.n_tiles = K / pl.bn;
+  p.k_steps = static_cast<int>((pix + 63) / 64);
+  p.rows = static_cast<int>(atoms * kB);
+  p.cols = K;
+  p.out_bf16 = 0;
+  // row = (rs * C_b + c_b) * 64 + c  ->  ((kb*C_b + c_b)*RS + rs)*4096 + c*64 + k
+  const int64_t rs_n = static_cast<int64_t>(R) * S;
+  p.om = OutMap{kB, rs_n * kB * kB, kB, kB, (int64_t)(C / kB) * rs_n * kB * kB, 1, (int64_t)(C / kB) * kB,
+                kB * kB};
+  if (pl.splits > 1) {
+    p.k_splits = pl.splits;
+    p.split_slice = dw_elems;
+    p.out = workspace;
+  } else {
+    p.out = dw;
+    p.sgd_w = w_sgd;
+    p.sgd_lr = lr;
+  }
+  g_launches.fetch_add(1);
+  rc = launch_engine(p, pl.bn, 0, pl.pair, 0, static_cast<cudaStream_t>(stream));
+  if (rc || pl.splits <= 1) return rc;
+  return launch_split_reduce(static_cast<const float*>(workspace), pl.splits, dw_elems, dw, w_sgd, lr,
+                             static_cast<cudaStream_t>(stream));
+}
+
+// Diagnostic: the engine plan the conv passes would use ("pair,bn,splits").
+BRK_API int brk_conv_plan(int pass, int N, int C, int K, int H, int W, int R, int S, int stride, int pad_h,
+                          int pad_w, int* out3) {
+  const ConvGeom g = geom(N, C, K, H, W, R, S, stride, pad_h, pad_w);
+  int rc = check_conv(g, kB, kB, BRK_BF16);
+  if (rc) return rc;
+  ConvPlan pl;
+  if (pass == 0) pl = choose(static_cast<int64_t>(N) * g.P * g.Q, K, (C / kB) * R * S, false);
+  else if (pass == 1)
+    pl = choose(stride == 1 ? static_cast<int64_t>(N) * H * W : static_cast<int64_t>(N) * g.P * g.Q, C,
+                (K / kB) * R * S, false);
+  else pl = upd_plan(g);
+  out3[0] = pl.pair;
+  out3[1] = pl.bn;
+  out3[2] = pl.splits;
+  return BRK_OK;
+}
+
+}  // extern "C"

@@ -61,27 +61,59 @@ struct EngineCfg {
 };
 
 template <bool kPair>
-__device__ __forceinline__ void issue_operand(const CUtensorMap* map, const OperandCoords& oc,
-                                              int rowblk, int s, uint8_t* dst, uint64_t* bar) {
-  const int q = s / oc.kdiv, r = s - q * oc.kdiv;
+__device__ __forceinline__ void issue_operand(const CUtensorMap* map, const OperandCoords& oc, int rowblk, int s,
+                                              uint8_t* dst, uint64_t* bar) {
+  const int d0 = s % oc.kdiv0, t = s / oc.kdiv0;
+  const int d1 = t % oc.kdiv1, d2 = t / oc.kdiv1;
+  int32_t cs[5];
+#pragma unroll
+  for (int d = 0; d < 5; ++d) cs[d] = oc.base[d] + oc.rc[d] * rowblk + oc.kc[0][d] * d0 + oc.kc[1][d] * d1 + oc.kc[2][d] * d2;
+  uint16_t off[3] = {0, 0, 0};
+  if (oc.kind != 0) {
+    // implicit-GEMM pixel walk: first pixel of this box -> (n, p, q)
+    int pix = oc.kind == 1 ? rowblk * kEngineBM : s * 64;
+    if (pix >= oc.total_pix) pix = oc.total_pix - 1;  // rows-side only (masked rows)
+    const int pq = oc.P * oc.Q;
+    const int n = pix / pq, rem = pix - n * pq;
+    const int pp = rem / oc.Q, q = rem - pp * oc.Q;
+    cs[1] += q * oc.cstride - oc.pad_w;
+    cs[2] += pp * oc.cstride - oc.pad_h;
+    cs[3] += n;
+    if (oc.kind == 1) {
+      off[0] = static_cast<uint16_t>(oc.ok[0][0] * d0 + oc.ok[0][1] * d1 + oc.ok[0][2] * d2);
+      off[1] = static_cast<uint16_t>(oc.ok[1][0] * d0 + oc.ok[1][1] * d1 + oc.ok[1][2] * d2);
+    }
+  }
   for (int l = 0; l < oc.n_loads; ++l) {
     int32_t c[5];
 #pragma unroll
-    for (int d = 0; d < 5; ++d) c[d] = oc.rc[d] * rowblk + oc.kq[d] * q + oc.kr[d] * r + oc.lc[d] * l;
+    for (int d = 0; d < 5; ++d) c[d] = cs[d] + oc.lc[d] * l;
     uint8_t* p = dst + l * oc.load_bytes;
+    if (oc.kind != 0) {
+      if (oc.kind == 2) {
+        const int atom = rowblk * oc.n_loads + l;
+        const int rs = atom / oc.atom_cb;
+        c[4] += atom - rs * oc.atom_cb;
+        const int r = rs / oc.atom_s;
+        off[0] = static_cast<uint16_t>(rs - r * oc.atom_s);
+        off[1] = static_cast<uint16_t>(r);
+      }
+      tma_load_im2col5<kPair>(p, map, bar, c, off);
+      continue;
+    }
     if constexpr (kPair) {
       switch (oc.ndims) {
         case 2: { const int32_t cc[2] = {c[0], c[1]}; tma_load_pair<2>(p, map, bar, cc); break; }
         case 3: { const int32_t cc[3] = {c[0], c[1], c[2]}; tma_load_pair<3>(p, map, bar, cc); break; }
         case 4: { const int32_t cc[4] = {c[0], c[1], c[2], c[3]}; tma_load_pair<4>(p, map, bar, cc); break; }
-        default: { const int32_t cc[5] = {c[0], c[1], c[2], c[3], c[4]}; tma_load_pair<5>(p, map, bar, cc); break; }
+        default: { tma_load_pair<5>(p, map, bar, c); break; }
       }
     } else {
       switch (oc.ndims) {
         case 2: { const int32_t cc[2] = {c[0], c[1]}; tma_load<2>(p, map, bar, cc); break; }
         case 3: { const int32_t cc[3] = {c[0], c[1], c[2]}; tma_load<3>(p, map, bar, cc); break; }
         case 4: { const int32_t cc[4] = {c[0], c[1], c[2], c[3]}; tma_load<4>(p, map, bar, cc); break; }
-        default: { const int32_t cc[5] = {c[0], c[1], c[2], c[3], c[4]}; tma_load<5>(p, map, bar, cc); break; }
+        default: { tma_load<5>(p, map, bar, c); break; }
       }
     }
   }
@@ -193,6 +225,14 @@ __device__ __forceinline__ void epilogue_finish(const EngineParams& p, float (&f
         w.z = pack_bf16x2(f[q * 8 + 4], f[q * 8 + 5]);
         w.w = pack_bf16x2(f[q * 8 + 6], f[q * 8 + 7]);
         dst[q] = w;
+      }
+      if (p.zf_w != 0) {  // stride-2 scatter: the three skipped input positions get zeros
+        const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+        uint4* d1 = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out) + off + p.zf_w);
+        uint4* d2 = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out) + off + p.zf_h);
+        uint4* d3 = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out) + off + p.zf_w + p.zf_h);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) { d1[q] = z; d2[q] = z; d3[q] = z; }
       }
       if (p.colsum_ws != nullptr) {  // column sums see the stored (rounded) values
 #pragma unroll
@@ -399,9 +439,11 @@ __global__ void __launch_bounds__(EngineCfg<BN, kPair>::kThreads, 1)
       const int row = tile_row0 + row_in_tile;
       const int warp_row0 = tile_row0 + quarter * 32;
       const bool row_ok = row < p.rows;
-      const int64_t roff = (row / p.om.rb) * p.om.rh + (row % p.om.rb) * p.om.rl;
+      const int64_t rrem = row % p.om.rb2;
+      const int64_t roff = (row / p.om.rb2) * p.om.rh2 + (rrem / p.om.rb) * p.om.rh + (rrem % p.om.rb) * p.om.rl +
+                           (splits > 1 && p.split_ws == nullptr ? sp * p.split_slice : 0);
       const uint32_t tbase = tmem_base + acc * BN + (static_cast<uint32_t>(quarter * 32) << 16) + cbeg;
-      if (splits == 1) {
+      if (splits == 1 || p.split_ws == nullptr) {
         // column offset maintained incrementally (32 columns never straddle an
         // output block: cb % 32 == 0, host guarantees); TMEM loads are software-
         // pipelined one chunk ahead so the ld latency overlaps the epilogue math.
@@ -435,8 +477,8 @@ __global__ void __launch_bounds__(EngineCfg<BN, kPair>::kThreads, 1)
         __syncwarp();
         if (threadIdx.x == 0) BRK_TS(12);
         if (lane == 0) {
-          if constexpr (kPair) mbar_arrive_cluster(tempty_leader + acc * 8);
-          else mbar_arrive(&tempty[acc]);
+          if constexpr (kPair) mbar_arrive_cluster_relaxed(tempty_leader + acc * 8);
+          else mbar_arrive_relaxed(&tempty[acc]);
         }
         if (threadIdx.x == 0) BRK_TS(13);
       } else {
@@ -457,8 +499,8 @@ __global__ void __launch_bounds__(EngineCfg<BN, kPair>::kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
-          if constexpr (kPair) mbar_arrive_cluster(tempty_leader + acc * 8);
-          else mbar_arrive(&tempty[acc]);
+          if constexpr (kPair) mbar_arrive_cluster_relaxed(tempty_leader + acc * 8);
+          else mbar_arrive_relaxed(&tempty[acc]);
         }
         __threadfence();
         named_bar_sync(1, kEpiThreads);
@@ -578,7 +620,9 @@ int launch_engine(const EngineParams& p, int bn, int tf32, int pair, int max_uni
   const int splits = p.k_splits > 1 ? p.k_splits : 1;
   const int work = p.m_tiles * p.n_tiles * splits;
   if (work <= 0) return BRK_OK;
-  if (splits > 1 && (p.split_ws == nullptr || p.split_counters == nullptr))
+  if (splits > 1 && (splits - 1) * ((p.k_steps + splits - 1) / splits) >= p.k_steps)
+    return set_error(BRK_ERR_CONTRACT, "engine: a split-K chunk would be empty (splits > ceil(k/ceil(k/splits)))");
+  if (splits > 1 && p.split_slice == 0 && (p.split_ws == nullptr || p.split_counters == nullptr))
     return set_error(BRK_ERR_CONTRACT, "engine: split-K needs a workspace");
   const int sms = engine_sm_count();
   int units = pair ? sms / 2 : sms;

@@ -16,25 +16,49 @@ namespace brk {
 
 constexpr int kEngineBM = 128;  // tile rows per CTA = TMEM lanes
 
-// How one operand's k-step box(es) are located.
-//   coord[d] = rc[d]*rowblk + kq[d]*(s / kdiv) + kr[d]*(s % kdiv) + lc[d]*load
-// for load in [0, n_loads); each load writes load_bytes to consecutive smem.
+// How one operand's k-step box(es) are located.  The k-step s is split into
+// mixed-radix digits d0 = s % kdiv0, d1 = (s / kdiv0) % kdiv1,
+// d2 = s / (kdiv0 * kdiv1) (e.g. conv: (s, r, c_b)); then for load l:
+//   coord[d] = base[d] + rc[d]*rowblk + sum_j kc[j][d]*d_j + lc[d]*l
+// and each load writes load_bytes to consecutive smem.
+//
+// kind != 0 selects TMA im2col mode on a 5-d map (64 channels, W, H, N, X)
+// of a blocked activation [N][X_b][H][W][64] (X = channel blocks), whose
+// pixel walk (W fastest, then H, then N) is the implicit-GEMM row/K order:
+//   kind 1: rows are output pixels, pix = rowblk * 128 (clamped to the last
+//           pixel; rows past the end are masked in the epilogue); the filter
+//           tap offsets (w, h) = (ok[0] . d, ok[1] . d)
+//   kind 2: the reduction runs over pixels, pix = s * 64; atom a = rowblk *
+//           n_loads + l is (c_b, rs) = (a % atom_cb, a / atom_cb) with the
+//           tap (rs % atom_s, rs / atom_s)  (conv weight update, input side)
+//   kind 3: the reduction runs over pixels, pix = s * 64, no tap offsets
+//           (conv weight update, output-gradient side)
+// pixel -> (n, p, q) adds (q*cstride - pad_w, p*cstride - pad_h, n) to coords
+// 1..3.  The maps' bounding boxes extend two images past N (zero fill), so a
+// pixel walk that runs off the end reads zeros (K-side kinds rely on it).
 struct OperandCoords {
+  int32_t base[5];
   int32_t rc[5];
-  int32_t kq[5];
-  int32_t kr[5];
+  int32_t kc[3][5];
   int32_t lc[5];
-  int32_t kdiv;
+  int32_t kdiv0, kdiv1;
   int32_t n_loads;
   uint32_t load_bytes;
   int32_t mn_major;  // 0: K-major rows of 128 B; 1: MN-major 64-wide atoms
   int32_t ndims;
+  int32_t kind;
+  int32_t P, Q, cstride, pad_h, pad_w, total_pix;
+  int32_t ok[2][3];
+  int32_t atom_cb, atom_s;
 };
 
-// Output addressing: off(r, c) = (r/rb)*rh + (r%rb)*rl + (c/cb)*ch + (c%cb)*cl
+// Output addressing:
+//   off(r, c) = (r / rb2)*rh2 + ((r % rb2) / rb)*rh + (r % rb)*rl
+//             + (c / cb)*ch + (c % cb)*cl
 struct OutMap {
   int64_t rb, rh, rl;
   int64_t cb, ch, cl;
+  int64_t rb2, rh2;
 };
 
 enum EpiAct : int { kActNone = 0, kActRelu = 1, kActSigmoid = 2 };
@@ -74,6 +98,13 @@ struct EngineParams {
   float* db_out;
   float* bias_sgd;
   float bias_lr;
+  // split-K into slices: when k_splits > 1 and split_ws == null, split sp
+  // writes its partial result (plain store, no epilogue ops) to out + sp *
+  // split_slice elements; a separate deterministic reduction sums them.
+  int64_t split_slice;
+  // stride-2 1x1 backward-data scatter: besides out[off], zero
+  // out[off + zf_w], out[off + zf_h], out[off + zf_w + zf_h] (bf16 output)
+  int64_t zf_w, zf_h;
   int32_t debug_flags;  // bit0: skip MMA, bit1: skip TMA, bit2: no k rotation (diagnostics)
   // diagnostics: per-CTA %globaltimer stamps [blockIdx.x][8]:
   // 0 entry, 1 setup done, 2 first TMA issued, 3 first full-barrier passed (MMA),

@@ -74,7 +74,8 @@ Plan choose_plan(int rows, int cols, int k_steps, bool allow_split) {
       const long waves = (work + units - 1) / units;
       const double cost = waves * per_tile / sp * (sp > 1 ? 1.1 : 1.0) + 2.0e5;  // + fixed launch cost
       if (best.bn == 0 || cost < best_cost) {
-        best = Plan{o.pair, o.bn, sp, static_cast<int>(tiles)};
+        const int per = (k_steps + sp - 1) / sp;
+        best = Plan{o.pair, o.bn, (k_steps + per - 1) / per, static_cast<int>(tiles)};
         best_cost = cost;
       }
     }
@@ -108,8 +109,9 @@ void set_coords(OperandCoords& oc, std::initializer_list<int> rc, std::initializ
   int d = 0;
   for (int v : rc) oc.rc[d++] = v;
   d = 0;
-  for (int v : kq) oc.kq[d++] = v;
-  oc.kdiv = 1;
+  for (int v : kq) oc.kc[0][d++] = v;
+  oc.kdiv0 = 1 << 30;
+  oc.kdiv1 = 1;
   oc.n_loads = 1;
   oc.load_bytes = load_bytes;
   oc.mn_major = mn_major;
@@ -239,7 +241,7 @@ BRK_API int brk_fc_fwd(const void* x, const void* w, const float* bias, void* y,
   p.cols = K;
   p.out = y;
   p.out_bf16 = 1;
-  p.om = OutMap{kB, (int64_t)(K / kB) * kB * kB, kB, kB, kB * kB, 1};
+  p.om = OutMap{kB, (int64_t)(K / kB) * kB * kB, kB, kB, kB * kB, 1, int64_t(1) << 62, 0};
   p.alpha = 1.0f;
   p.bias = bias;
   p.act = act;
@@ -271,7 +273,7 @@ BRK_API int brk_fc_bwd_data(const void* dz, const void* w, const void* mask, voi
   p.cols = C;
   p.out = dx;
   p.out_bf16 = 1;
-  p.om = OutMap{kB, (int64_t)(C / kB) * kB * kB, kB, kB, kB * kB, 1};
+  p.om = OutMap{kB, (int64_t)(C / kB) * kB * kB, kB, kB, kB * kB, 1, int64_t(1) << 62, 0};
   p.alpha = 1.0f;
   p.mask = mask;
   p.debug_flags = debug_flags();
@@ -330,7 +332,7 @@ BRK_API int brk_fc_upd(const void* x, const void* dz, float* dw, void* w_sgd, fl
   p.out = dw;
   p.out_bf16 = 0;
   // dW [Kb][Cb][64 c][64 k]: row c -> (c/64)*4096 + (c%64)*64 ; col k -> (k/64)*Cb*4096 + k%64
-  p.om = OutMap{kB, kB * kB, kB, kB, (int64_t)(C / kB) * kB * kB, 1};
+  p.om = OutMap{kB, kB * kB, kB, kB, (int64_t)(C / kB) * kB * kB, 1, int64_t(1) << 62, 0};
   p.alpha = 1.0f;
   p.sgd_w = w_sgd;
   p.sgd_lr = lr;

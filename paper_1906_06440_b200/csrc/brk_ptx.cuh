@@ -310,6 +310,17 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t saddr, uint32_t rank) {
   return r;
 }
 
+// Relaxed arrives: for barriers that only order tcgen05 (TMEM) accesses, which
+// tcgen05.fence::before_thread_sync already orders.  The default .release
+// arrive makes the arriving warp wait for all of its outstanding global
+// stores (MEMBAR + ERRBAR), serialising the epilogue's stores with the next tile.
+__device__ __forceinline__ void mbar_arrive_relaxed(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
                : "memory");
@@ -345,6 +356,32 @@ __device__ __forceinline__ void tma_load_pair(void* smem_dst, const CUtensorMap*
         "cp.async.bulk.tensor.5d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
         " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(dst), "l"(desc), "r"(mb), "r"(c[0]), "r"(c[1]),
         "r"(c[2]), "r"(c[3]), "r"(c[4])
+        : "memory");
+  }
+}
+
+// TMA im2col load on a 5-d map (C, W, H, D, N): coordinates c[] are the
+// starting pixel's position (already including the lower padding corner),
+// off = filter-tap offsets (w, h, d).  kPair: completes on the leader's barrier.
+template <bool kPair>
+__device__ __forceinline__ void tma_load_im2col5(void* smem_dst, const CUtensorMap* map, uint64_t* bar,
+                                                 const int32_t (&c)[5], const uint16_t (&off)[3]) {
+  const uint32_t dst = smem_u32(smem_dst);
+  const uint32_t mb = kPair ? (smem_u32(bar) & 0xFEFFFFFFu) : smem_u32(bar);
+  const uint64_t desc = reinterpret_cast<uint64_t>(map);
+  if constexpr (kPair) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.cta_group::2.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6, %7}], [%2], {%8, %9, %10};" ::"r"(dst),
+        "l"(desc), "r"(mb), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "h"(off[0]), "h"(off[1]),
+        "h"(off[2])
+        : "memory");
+  } else {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6, %7}], [%2], {%8, %9, %10};" ::"r"(dst),
+        "l"(desc), "r"(mb), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "h"(off[0]), "h"(off[1]),
+        "h"(off[2])
         : "memory");
   }
 }

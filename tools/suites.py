@@ -1,0 +1,191 @@
+"""Device-timed workload suites used by bench.py (and runnable alone):
+
+* ``resnet_suite``  — the 20 ResNet-50 convolution shapes of the reference's
+  bench table (pkg/src/brkernels/bench.py:57-79, occurrence counts n_i summing
+  to 53) at minibatch N, fwd / bwd-data / weight update, with the reference's
+  weighted efficiency  sum(n_i F_i) / sum(n_i t_i) / peak  (bench.py:142-152).
+* ``lstm_suite``    — the LSTM cell C=K=1024, N=168, T=50 fwd and bwd+upd.
+
+Timing: every launch is bracketed by CUDA events on the launching stream with
+an L2 flush (a 256 MiB write) between launches, outside the events.
+
+    python tools/suites.py conv [N]      python tools/suites.py lstm
+"""
+
+from __future__ import annotations
+
+import json
+import statistics
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+# (id, C, K, H, W, R, S, stride, count) — reference bench.py:57-79
+RESNET50_ROWS = (
+    (1, 3, 64, 224, 224, 7, 7, 2, 1),
+    (2, 64, 256, 56, 56, 1, 1, 1, 4),
+    (3, 64, 64, 56, 56, 1, 1, 1, 1),
+    (4, 64, 64, 56, 56, 3, 3, 1, 3),
+    (5, 256, 64, 56, 56, 1, 1, 1, 2),
+    (6, 256, 512, 56, 56, 1, 1, 2, 1),
+    (7, 256, 128, 56, 56, 1, 1, 2, 1),
+    (8, 128, 128, 28, 28, 3, 3, 1, 4),
+    (9, 128, 512, 28, 28, 1, 1, 1, 4),
+    (10, 512, 128, 28, 28, 1, 1, 1, 3),
+    (11, 512, 1024, 28, 28, 1, 1, 2, 1),
+    (12, 512, 256, 28, 28, 1, 1, 2, 1),
+    (13, 256, 256, 14, 14, 3, 3, 1, 6),
+    (14, 256, 1024, 14, 14, 1, 1, 1, 6),
+    (15, 1024, 256, 14, 14, 1, 1, 1, 5),
+    (16, 1024, 2048, 14, 14, 1, 1, 2, 1),
+    (17, 1024, 512, 14, 14, 1, 1, 2, 1),
+    (18, 512, 512, 7, 7, 3, 3, 1, 3),
+    (19, 512, 2048, 7, 7, 1, 1, 1, 3),
+    (20, 2048, 512, 7, 7, 1, 1, 1, 2),
+)
+
+
+def _peaks():
+    try:
+        pk = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+        return pk["bf16_tflops"], pk["hbm_gbs"], "measured"
+    except (OSError, ValueError, KeyError):
+        return 1590.0, 6650.0, "fallback"
+
+
+class _Timer:
+    def __init__(self, torch):
+        self.torch = torch
+        self.flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    def __call__(self, fn, iters, warmup=2):
+        torch = self.torch
+        stream = torch.cuda.current_stream()
+        for _ in range(warmup):
+            fn(stream.cuda_stream)
+        torch.cuda.synchronize()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(iters)]
+        for i in range(iters):
+            self.flush.fill_(float(i))
+            evs[i][0].record(stream)
+            fn(stream.cuda_stream)
+            evs[i][1].record(stream)
+        torch.cuda.synchronize()
+        ts = [a.elapsed_time(b) * 1e-3 for a, b in evs]
+        return statistics.fmean(ts), min(ts)
+
+
+def resnet_suite(n=256, iters=10, layers=None, passes=("fwd", "bwd", "upd")):
+    """Per-layer device time of the conv passes at minibatch n (bf16 storage, 64-channel blocks)."""
+    import torch
+
+    from paper_1906_06440_b200 import _lib
+    from paper_1906_06440_b200.cnn import ConvSpec, conv2d_backward_data, conv2d_forward, conv2d_weight_update
+    from paper_1906_06440_b200.tensor import BlockedTensor
+
+    lib = _lib.load()
+    peak, hbm, src = _peaks()
+    timer = _Timer(torch)
+    rows = []
+    tot = {p: [0.0, 0.0, 0.0] for p in passes}  # sum n_i F_i, sum n_i t_i, sum n_i t_roof
+    g = torch.Generator(device="cuda").manual_seed(0)
+    for lid, c, k, h, w, r, s, st, cnt in RESNET50_ROWS:
+        if layers and lid not in layers:
+            continue
+        t_layer = time.time()
+        spec = ConvSpec(n=n, c=c, k=k, h=h, w=w, r=r, s=s, stride=st)
+        p_, q_ = spec.out_h, spec.out_w
+        bc, bk = spec.b_c, spec.b_k
+        geom = (n, c, k, h, w, r, s, st, spec.pad_h, spec.pad_w)
+        x = (torch.rand((n, c // bc, h, w, bc), generator=g, device="cuda") * 2 - 1).bfloat16()
+        wt = ((torch.rand((k // bk, c // bc, r, s, bc, bk), generator=g, device="cuda") * 2 - 1) * 0.05).bfloat16()
+        dout = (torch.rand((n, k // bk, p_, q_, bk), generator=g, device="cuda") * 2 - 1).bfloat16()
+        flops = 2.0 * n * k * c * r * s * p_ * q_
+        e = 2
+        act_in, act_out, wbytes = n * c * h * w * e, n * k * p_ * q_ * e, k * c * r * s * e
+        bytes_ = {"fwd": act_in + wbytes + act_out, "bwd": act_out + wbytes + act_in,
+                  "upd": act_in + act_out + k * c * r * s * 4}
+        engine = bc == 64 and bk == 64
+        calls = {}
+        if engine:
+            out = torch.empty((n, k // 64, p_, q_, 64), dtype=torch.bfloat16, device="cuda")
+            din = torch.empty_like(x)
+            dw = torch.empty((k // 64, c // 64, r, s, 64, 64), dtype=torch.float32, device="cuda")
+            nbytes = lib.brk_conv_upd_workspace(*geom)
+            ws = torch.empty(max(nbytes, 16), dtype=torch.uint8, device="cuda")
+            calls["fwd"] = lambda sp: _lib.check(lib.brk_conv_fwd(x.data_ptr(), wt.data_ptr(), None, out.data_ptr(),
+                                                                  *geom, 64, 64, 0, _lib.BRK_BF16, sp))
+            calls["bwd"] = lambda sp: _lib.check(lib.brk_conv_bwd_data(dout.data_ptr(), wt.data_ptr(), din.data_ptr(),
+                                                                       *geom, 64, 64, _lib.BRK_BF16, sp))
+            calls["upd"] = lambda sp: _lib.check(lib.brk_conv_upd(x.data_ptr(), dout.data_ptr(), dw.data_ptr(), None,
+                                                                  0.0, ws.data_ptr() if nbytes else None, nbytes,
+                                                                  *geom, 64, 64, _lib.BRK_BF16, sp))
+            path = "engine"
+        else:
+            xi = BlockedTensor(x, 4, {"n": 0, "c": (1, 4), "h": 2, "w": 3})
+            wi = BlockedTensor(wt, 4, {"k": (0, 5), "c": (1, 4), "r": 2, "s": 3})
+            do = BlockedTensor(dout, 4, {"n": 0, "k": (1, 4), "p": 2, "q": 3})
+            calls["fwd"] = lambda sp: conv2d_forward(spec, xi, wi)
+            calls["upd"] = lambda sp: conv2d_weight_update(spec, xi, do)
+            path = "grouped"
+        row = {"id": lid, "count": cnt, "path": path, "C": c, "K": k, "H": h, "W": w, "R": r, "stride": st,
+               "gflop": flops / 1e9}
+        for p in passes:
+            if p not in calls:
+                row[p] = None
+                continue
+            mean, best = timer(calls[p], iters)
+            t_roof = max(flops / (peak * 1e12), bytes_[p] / (hbm * 1e9))
+            row[p] = {"us": mean * 1e6, "us_min": best * 1e6, "tflops": flops / mean / 1e12,
+                      "roof_frac": t_roof / mean}
+            if p == "bwd" and lid == 1:
+                continue
+            tot[p][0] += cnt * flops
+            tot[p][1] += cnt * mean
+            tot[p][2] += cnt * t_roof
+        if engine:
+            row["plan"] = {pn: list(_plan(lib, i, geom)) for i, pn in enumerate(("fwd", "bwd", "upd"))}
+        row["wall_s"] = round(time.time() - t_layer, 2)
+        rows.append(row)
+        print(json.dumps(row), flush=True)
+        del x, wt, dout
+        torch.cuda.empty_cache()
+    summary = {}
+    for p, (f, t, tr) in tot.items():
+        if t > 0:
+            summary[p] = {"tflops": f / t / 1e12, "weighted_eff_vs_peak": f / t / (peak * 1e12),
+                          "frac_of_roofline": tr / t, "ms": t * 1e3}
+    F = sum(v[0] for v in tot.values())
+    T = sum(v[1] for v in tot.values())
+    TR = sum(v[2] for v in tot.values())
+    summary["all"] = {"tflops": F / T / 1e12, "weighted_eff_vs_peak": F / T / (peak * 1e12),
+                      "frac_of_roofline": TR / T, "ms": T * 1e3, "gflop": F / 1e9}
+    return {"n": n, "peak_tflops": peak, "hbm_gbs": hbm, "peak_source": src, "layers": rows, "summary": summary}
+
+
+def _plan(lib, pass_, geom):
+    import ctypes
+    out = (ctypes.c_int * 3)()
+    lib.brk_conv_plan(pass_, *geom, out)
+    return tuple(out)
+
+
+if __name__ == "__main__":
+    what = sys.argv[1] if len(sys.argv) > 1 else "conv"
+    if what == "conv":
+        n = int(sys.argv[2]) if len(sys.argv) > 2 else 256
+        layers = [int(v) for v in sys.argv[3].split(",")] if len(sys.argv) > 3 else None
+        res = resnet_suite(n=n, layers=layers)
+        for row in res["layers"]:
+            cells = []
+            for p in ("fwd", "bwd", "upd"):
+                v = row.get(p)
+                cells.append(f"{p} {v['us']:8.1f}us {v['tflops']:7.1f}TF {v['roof_frac']*100:5.1f}%roof"
+                             if v else f"{p} {'n/a':>30}")
+            print(f"L{row['id']:2d} x{row['count']} {row['path']:7s} {row.get('plan', '')}  " + " | ".join(cells))
+        print(json.dumps(res["summary"], indent=1))
+        (ROOT / "gpurun_out").mkdir(exist_ok=True)
+        (ROOT / "gpurun_out" / f"resnet_n{n}.json").write_text(json.dumps(res, indent=1))
