@@ -142,7 +142,7 @@ void init_params(EngineParams& p) {
   p.ca.kdiv0 = p.cb.kdiv0 = 1 << 30;
   p.ca.kdiv1 = p.cb.kdiv1 = 1;
   p.alpha = 1.0f;
-  p.om.rb2 = int64_t(1) << 62;
+  p.om.rb2 = int64_t(0x7fffffff);
   const char* dbg = std::getenv("BRK_DEBUG_FLAGS");
   p.debug_flags = dbg ? std::atoi(dbg) : 0;
 }

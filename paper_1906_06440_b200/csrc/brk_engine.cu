@@ -51,7 +51,12 @@ struct EngineCfg {
   static constexpr int kBRows = kPair ? BN / 2 : BN;  // B rows staged per CTA
   static constexpr int kTileBBytes = kBRows * 128;
   static constexpr int kStageBytes = kTileABytes + kTileBBytes;
-  static constexpr int kStages = (200 * 1024) / kStageBytes > 8 ? 8 : (200 * 1024) / kStageBytes;
+  static constexpr int kAvail = 232448 - 1024 - 256;  // 227 KB opt-in max
+  // ring depth: as many stages as fit (<= 8), rounded down to a multiple of 4
+  // or 3 so that 3-4 producer warps share it (one issuing warp sustains only
+  // ~12 B/clk/SM of TMA traffic, profiles/r01_summary.md)
+  static constexpr int kFit = kAvail / kStageBytes > 8 ? 8 : kAvail / kStageBytes;
+  static constexpr int kStages = kFit >= 8 ? 8 : (kFit >= 6 ? 6 : (kFit >= 4 ? 4 : kFit));
   static constexpr int kTmemCols = 2 * BN;
   static constexpr int kSmem = kStages * kStageBytes + 1024 + 256;
   static constexpr int kProducers = kStages % 4 == 0 ? 4 : (kStages % 3 == 0 ? 3 : (kStages % 2 == 0 ? 2 : 1));
@@ -265,7 +270,34 @@ __device__ __forceinline__ void epilogue_finish(const EngineParams& p, float (&f
   }
 }
 
-template <int BN, bool kTF32, bool kPair>
+// Plain epilogue of one 32-column chunk: optional bias (+ReLU), store in the
+// output dtype.  The compact path for the conv / FC-forward passes: a small
+// loop body keeps the unrolled epilogue inside the instruction cache.
+__device__ __forceinline__ void epilogue_plain(const EngineParams& p, float (&f)[32], bool valid, int64_t off,
+                                               float bias_lane) {
+  if (p.bias != nullptr) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) f[j] += __shfl_sync(0xffffffffu, bias_lane, j);
+  }
+  if (p.act == kActRelu) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) f[j] = fmaxf(f[j], 0.0f);
+  }
+  if (!valid) return;
+  if (p.out_bf16) {
+    uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out) + off);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      dst[q] = make_uint4(pack_bf16x2(f[q * 8 + 0], f[q * 8 + 1]), pack_bf16x2(f[q * 8 + 2], f[q * 8 + 3]),
+                          pack_bf16x2(f[q * 8 + 4], f[q * 8 + 5]), pack_bf16x2(f[q * 8 + 6], f[q * 8 + 7]));
+  } else {
+    float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.out) + off);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) dst[q] = make_float4(f[q * 4], f[q * 4 + 1], f[q * 4 + 2], f[q * 4 + 3]);
+  }
+}
+
+template <int BN, bool kTF32, bool kPair, bool kFullEpi>
 __global__ void __launch_bounds__(EngineCfg<BN, kPair>::kThreads, 1)
     engine_kernel(const __grid_constant__ EngineParams p) {
   using Cfg = EngineCfg<BN, kPair>;
@@ -439,38 +471,47 @@ __global__ void __launch_bounds__(EngineCfg<BN, kPair>::kThreads, 1)
       const int row = tile_row0 + row_in_tile;
       const int warp_row0 = tile_row0 + quarter * 32;
       const bool row_ok = row < p.rows;
-      const int64_t rrem = row % p.om.rb2;
-      const int64_t roff = (row / p.om.rb2) * p.om.rh2 + (rrem / p.om.rb) * p.om.rh + (rrem % p.om.rb) * p.om.rl +
+      // 32-bit index math (rows and block extents < 2^31)
+      const uint32_t ur = static_cast<uint32_t>(row);
+      const uint32_t q2 = ur / static_cast<uint32_t>(p.om.rb2), rem2 = ur - q2 * static_cast<uint32_t>(p.om.rb2);
+      const uint32_t q1 = rem2 / static_cast<uint32_t>(p.om.rb), rem1 = rem2 - q1 * static_cast<uint32_t>(p.om.rb);
+      const int64_t roff = static_cast<int64_t>(q2) * p.om.rh2 + static_cast<int64_t>(q1) * p.om.rh +
+                           static_cast<int64_t>(rem1) * p.om.rl +
                            (splits > 1 && p.split_ws == nullptr ? sp * p.split_slice : 0);
       const uint32_t tbase = tmem_base + acc * BN + (static_cast<uint32_t>(quarter * 32) << 16) + cbeg;
       if (splits == 1 || p.split_ws == nullptr) {
         // column offset maintained incrementally (32 columns never straddle an
         // output block: cb % 32 == 0, host guarantees); TMEM loads are software-
         // pipelined one chunk ahead so the ld latency overlaps the epilogue math.
-        int64_t cq = (static_cast<int64_t>(nb) * BN + cbeg) / p.om.cb;
-        int64_t cr = (static_cast<int64_t>(nb) * BN + cbeg) % p.om.cb;
+        const int cfirst = nb * BN + cbeg;
+        int cq = cfirst / static_cast<int>(p.om.cb);
+        int cr = cfirst - cq * static_cast<int>(p.om.cb);
         uint32_t v[32];
         tmem_ld32(tbase, v);
 #pragma unroll
         for (int c = 0; c < kCW / 32; ++c) {
           tmem_ld_wait();
           float f[32];
-          if (p.alpha == 1.0f) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
-          } else {
+          if (kFullEpi && p.alpha != 1.0f) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]) * p.alpha;
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
           }
           if (c + 1 < kCW / 32) tmem_ld32(tbase + (c + 1) * 32, v);
-          const int col0 = nb * BN + cbeg + c * 32;
-          const int64_t off = roff + cq * p.om.ch + cr * p.om.cl;
+          const int col0 = cfirst + c * 32;
+          const int64_t off = roff + static_cast<int64_t>(cq) * p.om.ch + static_cast<int64_t>(cr) * p.om.cl;
           cr += 32;
           if (cr == p.om.cb) { cr = 0; ++cq; }
           if (p.out == nullptr) continue;  // diagnostic: mainloop-only timing
-          if (threadIdx.x == 0 && c < 2) BRK_TS(8 + 2 * c);
-          epilogue_finish(p, f, row_ok && col0 < p.cols, off, col0, warp_row0, lane, bias_r[c]);
-          if (threadIdx.x == 0 && c < 2) BRK_TS(9 + 2 * c);
+          if constexpr (kFullEpi) {
+            if (threadIdx.x == 0 && c < 2) BRK_TS(8 + 2 * c);
+            epilogue_finish(p, f, row_ok && col0 < p.cols, off, col0, warp_row0, lane, bias_r[c]);
+            if (threadIdx.x == 0 && c < 2) BRK_TS(9 + 2 * c);
+          } else {
+            epilogue_plain(p, f, row_ok && col0 < p.cols, off, bias_r[c]);
+          }
         }
         tmem_ld_wait();
         tc_fence_before();
@@ -481,7 +522,7 @@ __global__ void __launch_bounds__(EngineCfg<BN, kPair>::kThreads, 1)
           else mbar_arrive_relaxed(&tempty[acc]);
         }
         if (threadIdx.x == 0) BRK_TS(13);
-      } else {
+      } else if constexpr (kFullEpi) {
         // split-K: park the partial accumulator, last chunk reduces in chunk order
         float* ws_tile = p.split_ws + (static_cast<int64_t>(t) * halves + rank) * splits * (kEngineBM * BN);
         float* mine = ws_tile + static_cast<int64_t>(sp) * (kEngineBM * BN) + row_in_tile * BN + cbeg;
@@ -540,7 +581,7 @@ __global__ void __launch_bounds__(EngineCfg<BN, kPair>::kThreads, 1)
         }
       }
       // bias gradient from column-sum partials of a previous pass (+ fused bias SGD)
-      if (p.db_partials != nullptr && mb == 0 && rank == 0 && sp == 0) {
+      if (kFullEpi && p.db_partials != nullptr && mb == 0 && rank == 0 && sp == 0) {
         for (int c = threadIdx.x; c < BN; c += kEpiThreads) {
           const int col = nb * BN + c;
           if (col >= p.cols) continue;
@@ -563,10 +604,10 @@ __global__ void __launch_bounds__(EngineCfg<BN, kPair>::kThreads, 1)
   if (threadIdx.x == 0) BRK_TS(7);
 }
 
-template <int BN, bool kTF32, bool kPair>
+template <int BN, bool kTF32, bool kPair, bool kFullEpi>
 int launch_engine_t(const EngineParams& p, int grid, cudaStream_t stream, bool pdl) {
   using Cfg = EngineCfg<BN, kPair>;
-  auto kern = engine_kernel<BN, kTF32, kPair>;
+  auto kern = engine_kernel<BN, kTF32, kPair, kFullEpi>;
   static int attr_set = 0;  // per instantiation; the attribute is per-context state
   cudaError_t err;
   if (!attr_set) {
@@ -630,19 +671,24 @@ int launch_engine(const EngineParams& p, int bn, int tf32, int pair, int max_uni
   if (max_units > 0 && units > max_units) units = max_units;
   const int grid = pair ? units * 2 : units;
   const bool pdl = true;
-#define BRK_ENGINE_CASE(BN_)                                                                  \
-  if (bn == BN_) {                                                                            \
-    if (pair) return tf32 ? launch_engine_t<BN_, true, true>(p, grid, stream, pdl)            \
-                          : launch_engine_t<BN_, false, true>(p, grid, stream, pdl);          \
-    return tf32 ? launch_engine_t<BN_, true, false>(p, grid, stream, pdl)                     \
-                : launch_engine_t<BN_, false, false>(p, grid, stream, pdl);                   \
+  // the compact epilogue serves plain stores with optional bias + ReLU
+  const bool full = p.mask != nullptr || p.colsum_ws != nullptr || p.sgd_w != nullptr || p.beta != 0.0f ||
+                    p.alpha != 1.0f || (p.act != kActNone && p.act != kActRelu) || p.zf_w != 0 ||
+                    p.db_partials != nullptr || (splits > 1 && p.split_ws != nullptr) || (p.debug_flags & 8) ||
+                    (p.debug_flags & 64);  // bit6: force the full epilogue (diagnostic)
+#define BRK_ENGINE_CASE(BN_, PAIR_)                                                                  \
+  if (bn == BN_ && pair == PAIR_) {                                                                  \
+    if (full) return tf32 ? launch_engine_t<BN_, true, PAIR_, true>(p, grid, stream, pdl)            \
+                          : launch_engine_t<BN_, false, PAIR_, true>(p, grid, stream, pdl);          \
+    return tf32 ? launch_engine_t<BN_, true, PAIR_, false>(p, grid, stream, pdl)                     \
+                : launch_engine_t<BN_, false, PAIR_, false>(p, grid, stream, pdl);                   \
   }
-  BRK_ENGINE_CASE(256)
-  BRK_ENGINE_CASE(128)
+  BRK_ENGINE_CASE(256, true)
+  BRK_ENGINE_CASE(128, true)
+  BRK_ENGINE_CASE(256, false)
+  BRK_ENGINE_CASE(128, false)
+  BRK_ENGINE_CASE(64, false)
 #undef BRK_ENGINE_CASE
-  if (bn == 64 && !pair)
-    return tf32 ? launch_engine_t<64, true, false>(p, grid, stream, pdl)
-                : launch_engine_t<64, false, false>(p, grid, stream, pdl);
   return set_error(BRK_ERR_CONTRACT, "engine: BN must be 128 or 256 (pair) / 64, 128, 256 (single)");
 }
 

@@ -241,7 +241,7 @@ BRK_API int brk_fc_fwd(const void* x, const void* w, const float* bias, void* y,
   p.cols = K;
   p.out = y;
   p.out_bf16 = 1;
-  p.om = OutMap{kB, (int64_t)(K / kB) * kB * kB, kB, kB, kB * kB, 1, int64_t(1) << 62, 0};
+  p.om = OutMap{kB, (int64_t)(K / kB) * kB * kB, kB, kB, kB * kB, 1, int64_t(0x7fffffff), 0};
   p.alpha = 1.0f;
   p.bias = bias;
   p.act = act;
@@ -273,7 +273,7 @@ BRK_API int brk_fc_bwd_data(const void* dz, const void* w, const void* mask, voi
   p.cols = C;
   p.out = dx;
   p.out_bf16 = 1;
-  p.om = OutMap{kB, (int64_t)(C / kB) * kB * kB, kB, kB, kB * kB, 1, int64_t(1) << 62, 0};
+  p.om = OutMap{kB, (int64_t)(C / kB) * kB * kB, kB, kB, kB * kB, 1, int64_t(0x7fffffff), 0};
   p.alpha = 1.0f;
   p.mask = mask;
   p.debug_flags = debug_flags();
@@ -332,7 +332,7 @@ BRK_API int brk_fc_upd(const void* x, const void* dz, float* dw, void* w_sgd, fl
   p.out = dw;
   p.out_bf16 = 0;
   // dW [Kb][Cb][64 c][64 k]: row c -> (c/64)*4096 + (c%64)*64 ; col k -> (k/64)*Cb*4096 + k%64
-  p.om = OutMap{kB, kB * kB, kB, kB, (int64_t)(C / kB) * kB * kB, 1, int64_t(1) << 62, 0};
+  p.om = OutMap{kB, kB * kB, kB, kB, (int64_t)(C / kB) * kB * kB, 1, int64_t(0x7fffffff), 0};
   p.alpha = 1.0f;
   p.sgd_w = w_sgd;
   p.sgd_lr = lr;

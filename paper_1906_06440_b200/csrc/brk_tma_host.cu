@@ -96,3 +96,4 @@ int encode_tmap_im2col(CUtensorMap* out, const void* ptr, const uint64_t* dims, 
 }
 
 }  // namespace brk
+
