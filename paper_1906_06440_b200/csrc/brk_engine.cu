@@ -51,14 +51,16 @@ struct EngineCfg {
   static constexpr int kBRows = kPair ? BN / 2 : BN;  // B rows staged per CTA
   static constexpr int kTileBBytes = kBRows * 128;
   static constexpr int kStageBytes = kTileABytes + kTileBBytes;
-  static constexpr int kAvail = 232448 - 1024 - 256;  // 227 KB opt-in max
+  // epilogue staging: one 32-row x 128 B tile per epilogue warp (coalesced stores)
+  static constexpr int kEpiStageBytes = kEpiWarps * 4096;
+  static constexpr int kAvail = 232448 - 1024 - 256 - kEpiStageBytes;  // 227 KB opt-in max
   // ring depth: as many stages as fit (<= 8), rounded down to a multiple of 4
   // or 3 so that 3-4 producer warps share it (one issuing warp sustains only
   // ~12 B/clk/SM of TMA traffic, profiles/r01_summary.md)
   static constexpr int kFit = kAvail / kStageBytes > 8 ? 8 : kAvail / kStageBytes;
   static constexpr int kStages = kFit >= 8 ? 8 : (kFit >= 6 ? 6 : (kFit >= 4 ? 4 : kFit));
   static constexpr int kTmemCols = 2 * BN;
-  static constexpr int kSmem = kStages * kStageBytes + 1024 + 256;
+  static constexpr int kSmem = kStages * kStageBytes + kEpiStageBytes + 1024 + 256;
   static constexpr int kProducers = kStages % 4 == 0 ? 4 : (kStages % 3 == 0 ? 3 : (kStages % 2 == 0 ? 2 : 1));
   static constexpr int kMmaWarp = kEpiWarps;
   static constexpr int kThreads = (kEpiWarps + 1 + kProducers) * 32;
@@ -270,11 +272,13 @@ __device__ __forceinline__ void epilogue_finish(const EngineParams& p, float (&f
   }
 }
 
-// Plain epilogue of one 32-column chunk: optional bias (+ReLU), store in the
-// output dtype.  The compact path for the conv / FC-forward passes: a small
-// loop body keeps the unrolled epilogue inside the instruction cache.
-__device__ __forceinline__ void epilogue_plain(const EngineParams& p, float (&f)[32], bool valid, int64_t off,
-                                               float bias_lane) {
+// Plain epilogue, part 1: bias (+ReLU) on one 32-column chunk of this lane's
+// row, written into the warp's staging tile (32 rows x 128 B, 16 B slot j of
+// row r at slot j ^ (r % 8): conflict-free for both the row-wise writes here
+// and the segment-wise reads of epilogue_flush).  bf16: chunk = 4 slots
+// (two chunks fill a 128 B row segment); fp32: chunk = 8 slots.
+__device__ __forceinline__ void epilogue_stage(const EngineParams& p, float (&f)[32], float bias_lane, uint8_t* row,
+                                               int lane, int slot0) {
   if (p.bias != nullptr) {
 #pragma unroll
     for (int j = 0; j < 32; ++j) f[j] += __shfl_sync(0xffffffffu, bias_lane, j);
@@ -283,18 +287,50 @@ __device__ __forceinline__ void epilogue_plain(const EngineParams& p, float (&f)
 #pragma unroll
     for (int j = 0; j < 32; ++j) f[j] = fmaxf(f[j], 0.0f);
   }
-  if (!valid) return;
   if (p.out_bf16) {
-    uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out) + off);
 #pragma unroll
     for (int q = 0; q < 4; ++q)
-      dst[q] = make_uint4(pack_bf16x2(f[q * 8 + 0], f[q * 8 + 1]), pack_bf16x2(f[q * 8 + 2], f[q * 8 + 3]),
-                          pack_bf16x2(f[q * 8 + 4], f[q * 8 + 5]), pack_bf16x2(f[q * 8 + 6], f[q * 8 + 7]));
+      *reinterpret_cast<uint4*>(row + (((slot0 + q) ^ (lane & 7)) << 4)) =
+          make_uint4(pack_bf16x2(f[q * 8 + 0], f[q * 8 + 1]), pack_bf16x2(f[q * 8 + 2], f[q * 8 + 3]),
+                     pack_bf16x2(f[q * 8 + 4], f[q * 8 + 5]), pack_bf16x2(f[q * 8 + 6], f[q * 8 + 7]));
   } else {
-    float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.out) + off);
 #pragma unroll
-    for (int q = 0; q < 8; ++q) dst[q] = make_float4(f[q * 4], f[q * 4 + 1], f[q * 4 + 2], f[q * 4 + 3]);
+    for (int q = 0; q < 8; ++q)
+      *reinterpret_cast<float4*>(row + ((q ^ (lane & 7)) << 4)) =
+          make_float4(f[q * 4], f[q * 4 + 1], f[q * 4 + 2], f[q * 4 + 3]);
   }
+}
+
+// Plain epilogue, part 2: write the staged 32 x 128 B tile as coalesced
+// 16 B stores (8 lanes per row segment, 4 rows per instruction) instead of
+// one 16 B store per row per lane (32 lines per instruction).  ro[i] is the
+// element offset of row 4i + lane/8, ok its validity bit; coff the segment's
+// column offset.  Stride-2 scatters also zero the three skipped positions.
+// kLanes = 16 B slots per row segment: 8 (128 B) or 4 (64 B, bf16 BN=64 tiles).
+template <int kLanes>
+__device__ __forceinline__ void epilogue_flush(const EngineParams& p, const uint8_t* stage, const int64_t (&ro)[8],
+                                               uint32_t ok, int64_t coff, int lane) {
+  __syncwarp();
+  constexpr int kRowsPer = 32 / kLanes;
+  const int s = lane & (kLanes - 1);
+  const int esz = p.out_bf16 ? 2 : 4;
+  uint8_t* out = static_cast<uint8_t*>(p.out);
+#pragma unroll
+  for (int i = 0; i < kLanes; ++i) {
+    const int r = kRowsPer * i + lane / kLanes;
+    const uint4 v = *reinterpret_cast<const uint4*>(stage + r * 128 + ((s ^ (r & 7)) << 4));
+    if ((ok >> r) & 1u) {
+      uint8_t* dst = out + (ro[i] + coff) * esz + s * 16;
+      *reinterpret_cast<uint4*>(dst) = v;
+      if (p.zf_w != 0) {
+        const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+        *reinterpret_cast<uint4*>(dst + p.zf_w * 2) = z;
+        *reinterpret_cast<uint4*>(dst + p.zf_h * 2) = z;
+        *reinterpret_cast<uint4*>(dst + (p.zf_w + p.zf_h) * 2) = z;
+      }
+    }
+  }
+  __syncwarp();
 }
 
 template <int BN, bool kTF32, bool kPair, bool kFullEpi>
@@ -308,7 +344,7 @@ __global__ void __launch_bounds__(EngineCfg<BN, kPair>::kThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * Cfg::kStageBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * Cfg::kStageBytes + Cfg::kEpiStageBytes);
   uint64_t* empty = full + kStages;
   uint64_t* tfull = empty + kStages;  // [2]
   uint64_t* tempty = tfull + 2;       // [2]
@@ -484,6 +520,18 @@ __global__ void __launch_bounds__(EngineCfg<BN, kPair>::kThreads, 1)
         // output block: cb % 32 == 0, host guarantees); TMEM loads are software-
         // pipelined one chunk ahead so the ld latency overlaps the epilogue math.
         const int cfirst = nb * BN + cbeg;
+        // plain epilogue: staging tile, and the row offsets each lane stores in epilogue_flush
+        uint8_t* stage = smem + kStages * Cfg::kStageBytes + warp * 4096;
+        int64_t ro[8];
+        uint32_t ok_bits = 0;
+        int64_t seg_coff = 0;
+        if constexpr (!kFullEpi) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            ro[i] = __shfl_sync(0xffffffffu, roff,
+                                (kCW == 32 && p.out_bf16) ? 8 * (i & 3) + (lane >> 2) : 4 * i + (lane >> 3));
+          ok_bits = __ballot_sync(0xffffffffu, row_ok);
+        }
         int cq = cfirst / static_cast<int>(p.om.cb);
         int cr = cfirst - cq * static_cast<int>(p.om.cb);
         uint32_t v[32];
@@ -510,7 +558,20 @@ __global__ void __launch_bounds__(EngineCfg<BN, kPair>::kThreads, 1)
             epilogue_finish(p, f, row_ok && col0 < p.cols, off, col0, warp_row0, lane, bias_r[c]);
             if (threadIdx.x == 0 && c < 2) BRK_TS(9 + 2 * c);
           } else {
-            epilogue_plain(p, f, row_ok && col0 < p.cols, off, bias_r[c]);
+            const int64_t coff = off - roff;
+            if (kCW == 32 && p.out_bf16) {  // 64 B row segments
+              epilogue_stage(p, f, bias_r[c], stage + lane * 128, lane, 0);
+              if (col0 < p.cols) epilogue_flush<4>(p, stage, ro, ok_bits, coff, lane);
+              else __syncwarp();
+            } else {
+              const bool second = p.out_bf16 && (c & 1);
+              if (!second) seg_coff = coff;
+              epilogue_stage(p, f, bias_r[c], stage + lane * 128, lane, second ? 4 : 0);
+              if (!p.out_bf16 || second) {
+                if (col0 < p.cols) epilogue_flush<8>(p, stage, ro, ok_bits, seg_coff, lane);
+                else __syncwarp();
+              }
+            }
           }
         }
         tmem_ld_wait();
@@ -673,7 +734,7 @@ int launch_engine(const EngineParams& p, int bn, int tf32, int pair, int max_uni
   const bool pdl = true;
   // the compact epilogue serves plain stores with optional bias + ReLU
   const bool full = p.mask != nullptr || p.colsum_ws != nullptr || p.sgd_w != nullptr || p.beta != 0.0f ||
-                    p.alpha != 1.0f || (p.act != kActNone && p.act != kActRelu) || p.zf_w != 0 ||
+                    p.alpha != 1.0f || (p.act != kActNone && p.act != kActRelu) ||
                     p.db_partials != nullptr || (splits > 1 && p.split_ws != nullptr) || (p.debug_flags & 8) ||
                     (p.debug_flags & 64);  // bit6: force the full epilogue (diagnostic)
 #define BRK_ENGINE_CASE(BN_, PAIR_)                                                                  \
