@@ -250,6 +250,30 @@ def kernel_roofline(mlp, torch, peak_tflops):
             "us_per_launch": {k: v * 1e6 for k, v in out.items()}}
 
 
+def other_workloads():
+    """The metric's other two workloads on this GPU (informational; the headline
+    is the MLP config): ResNet-50 conv fwd/bwd/upd at N=256 (reference weighted
+    efficiency over the 53 convs) and the LSTM cell (T=50, N=168, C=K=1024)."""
+    from tools.suites import lstm_suite, resnet_suite
+
+    out = {}
+    try:
+        res = resnet_suite(n=256, iters=5, layers=list(range(2, 21)))
+        out["resnet50_conv_n256"] = {
+            "summary": res["summary"], "peak_tflops": res["peak_tflops"], "hbm_gbs": res["hbm_gbs"],
+            "note": "layers 2-20 (52 of 53 convs) on the implicit-GEMM engine, bf16 storage, L2 flushed "
+                    "between launches; layer 1 (C=3 stem) is not on the engine path",
+            "per_layer_us": {r["id"]: {p: round(r[p]["us"], 1) for p in ("fwd", "bwd", "upd") if r.get(p)}
+                             for r in res["layers"]}}
+    except Exception as exc:  # noqa: BLE001 - informational block must not kill the headline line
+        out["resnet50_conv_n256"] = {"error": repr(exc)[:300]}
+    try:
+        out["lstm_t50_n168_c1024"] = lstm_suite(iters=2)
+    except Exception as exc:  # noqa: BLE001
+        out["lstm_t50_n168_c1024"] = {"error": repr(exc)[:300]}
+    return out
+
+
 def run_gpu(args, n_gpus, rank, local_rank, pg):
     import torch
 
@@ -319,6 +343,9 @@ def run_gpu(args, n_gpus, rank, local_rank, pg):
     e2e_value = n_gpus * flops / e2e_sec / 1e12
     if rank != 0:
         return
+    workloads = None
+    if n_gpus == 1 and os.environ.get("BRK_BENCH_SUITES", "1") != "0":
+        workloads = other_workloads()
     roof = kernel_roofline(mlp, torch, pk["bf16_tflops"])
     roof["peak_source"] = f"{pk_kind} bf16 dense (burst, kernel timed alone)"
     cpu = cpu_baseline_sample()
@@ -338,6 +365,7 @@ def run_gpu(args, n_gpus, rank, local_rank, pg):
         "cpu_baseline": cpu,
         "clocks": clocks,
         "lib_launch_counter": _lib.launch_count(),
+        "workloads": workloads,
     }
     print(json.dumps(line), flush=True)
 

@@ -182,6 +182,40 @@ BRK_API int brk_conv_plan(int pass, int N, int C, int K, int H, int W, int R, in
                           int pad_w, int* out3);
 
 /* ---------------------------------------------------------------------------
+ * Dense row-major GEMM on the same engine (batch list = the K/64 consecutive
+ * 64-wide slices of the operands): C[M][N] = act(alpha*A.B^T + bias) + beta*C,
+ * A M x K (a_kmajor: A[m][k] at m*lda+k, else k*lda+m), B N x K (b_kmajor: B[n][k]
+ * at n*ldb+k, else k*ldb+n), bf16 operands, C fp32 (c_bf16=0) or bf16, row stride
+ * ldc.  N, K multiples of 64.  workspace (may be NULL): brk_gemm_dense_workspace
+ * bytes enable deterministic split-K for fp32 outputs without epilogue ops.
+ * Used by the LSTM drivers (input projection, backward-data, weight gradients).
+ * ------------------------------------------------------------------------- */
+BRK_API int brk_gemm_dense(const void* a, int64_t lda, int a_kmajor, const void* b, int64_t ldb, int b_kmajor,
+                           void* c, int64_t ldc, int c_bf16, int64_t M, int N, int K, float alpha, float beta,
+                           const float* bias, int act, void* workspace, size_t ws_bytes, void* stream);
+BRK_API size_t brk_gemm_dense_workspace(int64_t M, int N, int K);
+
+/* ---------------------------------------------------------------------------
+ * LSTM over a whole sequence, one persistent launch per direction (reference
+ * lstm.py:217-327; BPTT restated in oracle/brk_oracle.py:305-350).  bf16
+ * tensor-core operands, fp32 state.  N <= 256, K % 64 == 0, K <= 1024.
+ *   gx      [T][N][4][K] fp32   W_g x_t + b_g (gate order i, c, f, o)
+ *   r_cat   [4K][K] bf16        rows g*K + k = R_g[k][:]
+ *   rt_cat  [4K][K] bf16        rows g*K + j = R_g[:][j]  (transposed)
+ *   h_bf    [T+1][N][K] bf16    slot 0 = h0 (caller), slot t+1 = h_t (kernel)
+ *   flags   brk_lstm_seq_flags_bytes(K) bytes of device scratch
+ * fwd writes h, s [T][N][K] and the activated gates [T][N][4][K] (fp32).
+ * bwd reads dh [T][N][K] (dL/dh_t), gates, s, s0 (may be NULL) and writes
+ * dpre [T][N][4][K] (bf16 pre-activation gradients) and ds0 [N][K].
+ * ------------------------------------------------------------------------- */
+BRK_API size_t brk_lstm_seq_flags_bytes(int K);
+BRK_API int brk_lstm_seq_fwd(const float* gx, const void* r_cat, const float* s0, void* h_bf, float* h_out,
+                             float* s_out, float* gates_out, unsigned* flags, int T, int N, int K, void* stream);
+BRK_API int brk_lstm_seq_bwd(const float* dh, const float* gates, const float* s, const float* s0,
+                             const void* rt_cat, void* dpre, float* ds0, unsigned* flags, int T, int N, int K,
+                             void* stream);
+
+/* ---------------------------------------------------------------------------
  * LSTM recurrent steps (reference lstm.py:217-327, Eqs. 1-6; gate order
  * i, c, f, o per lstm.py:28).  Storage fp32 (h, s, gates, gradients as in
  * the reference), tensor-core inputs TF32 or BF16 (compute code).

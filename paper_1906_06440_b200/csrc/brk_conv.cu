@@ -181,8 +181,10 @@ __global__ void __launch_bounds__(256) split_reduce_kernel(const float4* __restr
   }
 }
 
-int launch_split_reduce(const float* ws, int splits, int64_t n, float* dw, void* w_sgd, float lr,
-                        cudaStream_t stream) {
+}  // namespace
+
+// shared with brk_gemm.cu
+int split_reduce(const float* ws, int splits, int64_t n, float* dw, void* w_sgd, float lr, cudaStream_t stream) {
   const int64_t n4 = n / 4;
   int blocks = static_cast<int>(std::min<int64_t>((n4 + 255) / 256, 4 * engine_sm_count()));
   if (blocks < 1) blocks = 1;
@@ -201,6 +203,8 @@ int launch_split_reduce(const float* ws, int splits, int64_t n, float* dw, void*
   if (err != cudaSuccess) return set_cuda_error(err, "conv split reduce launch");
   return BRK_OK;
 }
+
+namespace {
 
 ConvGeom geom(int N, int C, int K, int H, int W, int R, int S, int stride, int pad_h, int pad_w) {
   ConvGeom g{N, C, K, H, W, R, S, stride, pad_h, pad_w, 0, 0};
@@ -403,7 +407,7 @@ BRK_API int brk_conv_upd(const void* in, const void* dout, float* dw, void* w_sg
   g_launches.fetch_add(1);
   rc = launch_engine(p, pl.bn, 0, pl.pair, 0, static_cast<cudaStream_t>(stream));
   if (rc || pl.splits <= 1) return rc;
-  return launch_split_reduce(static_cast<const float*>(workspace), pl.splits, dw_elems, dw, w_sgd, lr,
+  return split_reduce(static_cast<const float*>(workspace), pl.splits, dw_elems, dw, w_sgd, lr,
                              static_cast<cudaStream_t>(stream));
 }
 

@@ -1,0 +1,612 @@
+// brk_lstm_seq.cu — the LSTM cell over a whole sequence as ONE persistent launch
+// per direction (reference lstm.py:217-327, paper Alg. 2 / Eqs. 1-6; BPTT as
+// restated in oracle/brk_oracle.py:305-350).
+//
+// The input projections W x_t + b of all steps are one large BRGEMM before the
+// loop (brk_gemm_dense), so only the recurrent batch-reduce  sum_j h[n][j] R[.][j]
+// sits on the serial path.  Each CTA keeps its slice of the recurrent weights
+// resident in shared memory for all T steps and streams the previous step's
+// h (bf16) by TMA, one 64-wide K chunk per ring stage; the accumulators live in
+// TMEM and the gate / cell-state epilogue is fused (s_t stays in registers).
+// There is no grid-wide barrier: K chunk kc of step t is released by a
+// per-chunk counter that the CTAs owning those hidden units bump after
+// writing their slice of h_t, so step t+1's loads start chunk by chunk.
+//
+// forward  : CTA c owns hidden units j0 = 8c .. 8c+7 of all four gates
+//            (MMA N = 32: rows g*8 + jj of R_cat = [R_i; R_c; R_f; R_o]).
+// backward : a cluster of 4 CTAs (one per gate g) owns 32 hidden units; CTA g
+//            computes the partial recurrent gradient  dpre_g(t+1) R_g  for them
+//            (R_g^T slice resident), the four partials are summed through
+//            distributed shared memory and each CTA of the cluster finishes
+//            the BPTT element math for a quarter of the minibatch rows.
+#include <cstdio>
+#include <cstring>
+#include <cuda_bf16.h>
+
+#include "brk_internal.h"
+#include "brk_ptx.cuh"
+#include "brk_tma_host.h"
+
+namespace brk {
+namespace {
+
+constexpr int kStagesS = 4;          // A ring (4 producers, one stage each)
+constexpr int kStageBytesS = 32768;  // 2 M-tiles x 128 rows x 128 B
+constexpr int kThreadsS = 9 * 32;    // 4 epilogue, 1 MMA, 4 producer warps
+constexpr int kJf = 8;               // forward: hidden units per CTA
+constexpr int kJb = 32;              // backward: hidden units per cluster
+
+struct SeqParams {
+  CUtensorMap map_a;  // streamed operand, 3-d (cols, N, slots) bf16, box (64, 128, 1)
+  CUtensorMap map_w;  // resident operand rows, 2-d (K, rows) bf16, box (64, 8 | 32)
+  int T, N, K;
+  // forward
+  const float* gx;       // [T][N][4][K]  W x_t + b
+  const float* s0;       // [N][K] or null
+  float* h_out;          // [T][N][K]
+  float* s_out;          // [T][N][K]
+  float* gates_out;      // [T][N][4][K] activated i, c, f, o
+  __nv_bfloat16* h_bf;   // [T+1][N][K]  slot 0 = h0 (filled by the host)
+  // backward
+  const float* dh;       // [T][N][K]
+  const float* gates;    // [T][N][4][K]
+  const float* s;        // [T][N][K]
+  __nv_bfloat16* dpre;   // [T][N][4][K] (bf16; A operand of the next step and of the weight gradients)
+  float* ds0;            // [N][K] dL/ds_{-1}
+  unsigned* flags;       // per 64-column chunk release counters (zeroed by the host)
+};
+
+__device__ __forceinline__ float sigm_s(float x) {
+  const float e = __expf(-fabsf(x));
+  const float r = __fdividef(1.0f, 1.0f + e);
+  return x >= 0.0f ? r : e * r;
+}
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load3(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
+  const int32_t c[3] = {c0, c1, c2};
+  tma_load<3>(dst, map, bar, c);
+}
+__device__ __forceinline__ void mbar_wait_acq_cluster(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%1], %2;\n\t"
+        "selp.b32 %0, 1, 0, P;\n\t}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ float4 ld_dsmem_f4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr)
+               : "memory");
+  return v;
+}
+
+// ------------------------------------------------------------------ forward
+__global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_fwd_kernel(const __grid_constant__ SeqParams p) {
+  constexpr int kGN = 4 * kJf;  // 32 gate columns
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int KC = p.K / 64;
+  uint8_t* ring = smem;
+  uint8_t* wsm = smem + kStagesS * kStageBytesS;
+  uint64_t* full = reinterpret_cast<uint64_t*>(wsm + KC * kGN * 128);
+  uint64_t* empty = full + kStagesS;
+  uint64_t* tfull = empty + kStagesS;
+  uint64_t* tempty = tfull + 1;
+  uint64_t* wbar = tempty + 1;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(wbar + 1);
+  const int warp = warp_id(), lane = threadIdx.x & 31;
+  const int j0 = blockIdx.x * kJf;
+  const int n_mt = p.N > 128 ? 2 : 1;
+  const int chunk_owners = 64 / kJf;  // CTAs writing one 64-column chunk of h
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStagesS; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 4);
+    mbar_init(wbar, 1);
+    fence_barrier_init();
+  }
+  if (warp == 4) tmem_alloc(tslot, 64);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp >= 5) {
+    // ---------------------------------------------------------------- producers
+    const int pid = warp - 5;
+    if (elect_one()) {
+      if (pid == 0) {  // resident R slice: rows g*8+jj of chunk kc <- R_cat[g*K + j0 + jj][64kc ..]
+        mbar_arrive_expect_tx(wbar, KC * kGN * 128);
+        for (int kc = 0; kc < KC; ++kc)
+          for (int g = 0; g < 4; ++g) {
+            const int32_t c[2] = {kc * 64, g * p.K + j0};
+            tma_load<2>(wsm + kc * kGN * 128 + g * 1024, &p.map_w, wbar, c);
+          }
+      }
+      const int total = p.T * KC;
+      for (int gi = pid; gi < total; gi += kStagesS) {
+        const int t = gi / KC, kc = gi - t * KC;
+        const uint32_t ph = (gi / kStagesS) & 1;
+        if (t > 0) {
+          while (ld_acquire(&p.flags[kc]) < static_cast<unsigned>(chunk_owners * t)) {
+          }
+          fence_proxy_async_global();
+        }
+        mbar_wait(&empty[pid], ph ^ 1);
+        mbar_arrive_expect_tx(&full[pid], n_mt * 16384);
+        for (int mt = 0; mt < n_mt; ++mt)
+          tma_load3(ring + pid * kStageBytesS + mt * 16384, &p.map_a, &full[pid], kc * 64, mt * 128, t);
+      }
+    }
+  } else if (warp == 4) {
+    // ---------------------------------------------------------------- MMA issuer
+    const uint32_t idesc = make_idesc(kFmtBF16, 128, kGN, 0, 0);
+    mbar_wait(wbar, 0);
+    for (int t = 0; t < p.T; ++t) {
+      mbar_wait(tempty, (t & 1) ^ 1);
+      tc_fence_after();
+      for (int kc = 0; kc < KC; ++kc) {
+        const int gi = t * KC + kc, st = gi % kStagesS;
+        mbar_wait(&full[st], (gi / kStagesS) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t a0 = smem_u32(ring + st * kStageBytesS);
+          const uint32_t b0 = smem_u32(wsm + kc * kGN * 128);
+          for (int mt = 0; mt < n_mt; ++mt)
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              mma_ss<false>(tmem + mt * kGN, make_smem_desc(a0 + mt * 16384 + kk * 32, 16, 1024, kSwizzle128B),
+                            make_smem_desc(b0 + kk * 32, 16, 1024, kSwizzle128B), idesc, (kc | kk) ? 1u : 0u);
+          mma_commit(&empty[st]);
+          if (kc == KC - 1) mma_commit(tfull);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    // ---------------------------------------------------------------- epilogue (warps 0-3)
+    float sreg[2][kJf];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      const int n = mt * 128 + warp * 32 + lane;
+#pragma unroll
+      for (int jj = 0; jj < kJf; ++jj)
+        sreg[mt][jj] = (p.s0 != nullptr && n < p.N) ? p.s0[static_cast<int64_t>(n) * p.K + j0 + jj] : 0.0f;
+    }
+    for (int t = 0; t < p.T; ++t) {
+      mbar_wait(tfull, t & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        if (mt >= n_mt) break;
+        uint32_t v[32];
+        tmem_ld32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + mt * kGN, v);
+        tmem_ld_wait();
+        const int n = mt * 128 + warp * 32 + lane;
+        if (n < p.N) {
+          const int64_t row = static_cast<int64_t>(t) * p.N + n;
+          const float* gxr = p.gx + row * 4 * p.K + j0;
+          float pre[4][kJf];
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            const float4 a = *reinterpret_cast<const float4*>(gxr + g * p.K);
+            const float4 b = *reinterpret_cast<const float4*>(gxr + g * p.K + 4);
+            pre[g][0] = a.x; pre[g][1] = a.y; pre[g][2] = a.z; pre[g][3] = a.w;
+            pre[g][4] = b.x; pre[g][5] = b.y; pre[g][6] = b.z; pre[g][7] = b.w;
+#pragma unroll
+            for (int jj = 0; jj < kJf; ++jj) pre[g][jj] += __uint_as_float(v[g * kJf + jj]);
+          }
+          float hv[kJf];
+#pragma unroll
+          for (int jj = 0; jj < kJf; ++jj) {
+            const float gi = sigm_s(pre[0][jj]), gc = tanhf(pre[1][jj]);
+            const float gf = sigm_s(pre[2][jj]), go = sigm_s(pre[3][jj]);
+            const float sv = gf * sreg[mt][jj] + gi * gc;
+            sreg[mt][jj] = sv;
+            hv[jj] = go * tanhf(sv);
+            pre[0][jj] = gi; pre[1][jj] = gc; pre[2][jj] = gf; pre[3][jj] = go;
+          }
+          float* go_ = p.gates_out + row * 4 * p.K + j0;
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            *reinterpret_cast<float4*>(go_ + g * p.K) = make_float4(pre[g][0], pre[g][1], pre[g][2], pre[g][3]);
+            *reinterpret_cast<float4*>(go_ + g * p.K + 4) = make_float4(pre[g][4], pre[g][5], pre[g][6], pre[g][7]);
+          }
+          float* ho = p.h_out + row * p.K + j0;
+          float* so = p.s_out + row * p.K + j0;
+          *reinterpret_cast<float4*>(ho) = make_float4(hv[0], hv[1], hv[2], hv[3]);
+          *reinterpret_cast<float4*>(ho + 4) = make_float4(hv[4], hv[5], hv[6], hv[7]);
+          *reinterpret_cast<float4*>(so) = make_float4(sreg[mt][0], sreg[mt][1], sreg[mt][2], sreg[mt][3]);
+          *reinterpret_cast<float4*>(so + 4) = make_float4(sreg[mt][4], sreg[mt][5], sreg[mt][6], sreg[mt][7]);
+          *reinterpret_cast<uint4*>(p.h_bf + (static_cast<int64_t>(t + 1) * p.N + n) * p.K + j0) =
+              make_uint4(pack_bf16x2(hv[0], hv[1]), pack_bf16x2(hv[2], hv[3]), pack_bf16x2(hv[4], hv[5]),
+                         pack_bf16x2(hv[6], hv[7]));
+        }
+      }
+      tc_fence_before();
+      fence_proxy_async_global();  // h_t (bf16) is read by other CTAs' TMA (async proxy)
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty);
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(&p.flags[j0 / 64], 1u);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 4) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 64);
+  }
+}
+
+// ------------------------------------------------------------------ backward
+// Cluster of 4 CTAs: rank g = gate.  Units u0 = 32 * cluster .. +31.
+__global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_bwd_kernel(const __grid_constant__ SeqParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int KC = p.K / 64;
+  uint8_t* ring = smem;
+  uint8_t* wsm = smem + kStagesS * kStageBytesS;           // R_g^T slice: 32 rows x K
+  float* part = reinterpret_cast<float*>(wsm + KC * kJb * 128);  // [256][32] partial dh_rec
+  uint64_t* full = reinterpret_cast<uint64_t*>(part + 256 * kJb);
+  uint64_t* empty = full + kStagesS;
+  uint64_t* tfull = empty + kStagesS;
+  uint64_t* tempty = tfull + 1;
+  uint64_t* wbar = tempty + 1;
+  uint64_t* pready = wbar + 1;  // all 16 epilogue warps of the cluster wrote their partials
+  uint64_t* pfree = pready + 1;  // all 16 finished reading them
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(pfree + 1);
+  const int warp = warp_id(), lane = threadIdx.x & 31;
+  const int g = static_cast<int>(cluster_ctarank());
+  const int u0 = (blockIdx.x >> 2) * kJb;
+  const int n_mt = p.N > 128 ? 2 : 1;
+  const int chunk_owners = 2 * 4;  // 64-column chunk of dpre = 2 clusters x 4 CTAs (row quarters)
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStagesS; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 4);
+    mbar_init(wbar, 1);
+    mbar_init(pready, 16);
+    mbar_init(pfree, 16);
+    fence_barrier_init();
+  }
+  if (warp == 4) tmem_alloc(tslot, 64);
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp >= 5) {
+    const int pid = warp - 5;
+    if (elect_one()) {
+      if (pid == 0) {  // R_g^T rows u0 .. u0+31 (RT_cat[g*K + u][k] = R_g[k][u])
+        mbar_arrive_expect_tx(wbar, KC * kJb * 128);
+        for (int kc = 0; kc < KC; ++kc) {
+          const int32_t c[2] = {kc * 64, g * p.K + u0};
+          tma_load<2>(wsm + kc * kJb * 128, &p.map_w, wbar, c);
+        }
+      }
+      // steps t = T-2 .. 0 read dpre(t+1) gate g; step T-1 has no recurrent term
+      const int steps = p.T - 1;
+      const int total = steps * KC;
+      for (int gi = pid; gi < total; gi += kStagesS) {
+        const int it = gi / KC, kc = gi - it * KC;
+        const int tsrc = p.T - 1 - it;  // dpre slot read by this iteration
+        const int fidx = g * KC + kc;
+        while (ld_acquire(&p.flags[fidx]) < static_cast<unsigned>(chunk_owners * (it + 1))) {
+        }
+        fence_proxy_async_global();
+        const uint32_t ph = (gi / kStagesS) & 1;
+        mbar_wait(&empty[pid], ph ^ 1);
+        mbar_arrive_expect_tx(&full[pid], n_mt * 16384);
+        for (int mt = 0; mt < n_mt; ++mt)
+          tma_load3(ring + pid * kStageBytesS + mt * 16384, &p.map_a, &full[pid], g * p.K + kc * 64, mt * 128,
+                    tsrc);
+      }
+    }
+  } else if (warp == 4) {
+    const uint32_t idesc = make_idesc(kFmtBF16, 128, kJb, 0, 0);
+    mbar_wait(wbar, 0);
+    for (int it = 0; it < p.T - 1; ++it) {
+      mbar_wait(tempty, (it & 1) ^ 1);
+      tc_fence_after();
+      for (int kc = 0; kc < KC; ++kc) {
+        const int gi = it * KC + kc, st = gi % kStagesS;
+        mbar_wait(&full[st], (gi / kStagesS) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t a0 = smem_u32(ring + st * kStageBytesS);
+          const uint32_t b0 = smem_u32(wsm + kc * kJb * 128);
+          for (int mt = 0; mt < n_mt; ++mt)
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              mma_ss<false>(tmem + mt * kJb, make_smem_desc(a0 + mt * 16384 + kk * 32, 16, 1024, kSwizzle128B),
+                            make_smem_desc(b0 + kk * 32, 16, 1024, kSwizzle128B), idesc, (kc | kk) ? 1u : 0u);
+          mma_commit(&empty[st]);
+          if (kc == KC - 1) mma_commit(tfull);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    // ------------------------------------------------ epilogue: 128 threads
+    // finalize rows r = 64*g + tid/2 (this CTA's quarter), units half = tid%2 (16 units)
+    const int tid = threadIdx.x;
+    const int rq = 64 * g + (tid >> 1);
+    const int uh = (tid & 1) * 16;
+    float dsc[16];  // ds_t * f_t carried to step t-1
+#pragma unroll
+    for (int q = 0; q < 16; ++q) dsc[q] = 0.0f;
+    uint32_t part_peer[4], ready_peer[4], free_peer[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      part_peer[r] = mapa_shared(smem_u32(part), r);
+      ready_peer[r] = mapa_shared(smem_u32(pready), r);
+      free_peer[r] = mapa_shared(smem_u32(pfree), r);
+    }
+    for (int t = p.T - 1; t >= 0; --t) {
+      const int it = p.T - 1 - t;
+      const int q = it - 1;  // index of the recurrent step (t < T-1)
+      if (t < p.T - 1) {
+        if (q > 0) mbar_wait_acq_cluster(pfree, (q - 1) & 1);  // peers done reading the last partials
+        mbar_wait(tfull, q & 1);
+        tc_fence_after();
+        // partial dh_rec rows (both M-tiles) -> own smem [256][32]
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          if (mt >= n_mt) break;
+          uint32_t v[32];
+          tmem_ld32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + mt * kJb, v);
+          tmem_ld_wait();
+          float4* dst = reinterpret_cast<float4*>(part + (mt * 128 + warp * 32 + lane) * kJb);
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            dst[q] = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                                 __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(tempty);
+#pragma unroll
+          for (int r = 0; r < 4; ++r) mbar_arrive_cluster(ready_peer[r]);  // release: partial rows written
+        }
+        mbar_wait_acq_cluster(pready, q & 1);  // the four gate partials are in the cluster's smem
+      }
+      if (rq < p.N) {
+        float dhr[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) dhr[q] = 0.0f;
+        if (t < p.T - 1) {
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            const uint32_t base = part_peer[r] + static_cast<uint32_t>((rq * kJb + uh) * 4);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float4 v4 = ld_dsmem_f4(base + q * 16);
+              dhr[4 * q] += v4.x; dhr[4 * q + 1] += v4.y; dhr[4 * q + 2] += v4.z; dhr[4 * q + 3] += v4.w;
+            }
+          }
+        }
+        const int64_t row = static_cast<int64_t>(t) * p.N + rq;
+        const float* gr = p.gates + row * 4 * p.K + u0 + uh;
+        const float* sr = p.s + row * p.K + u0 + uh;
+        const float* spr = t > 0 ? p.s + (row - p.N) * p.K + u0 + uh : (p.s0 ? p.s0 + rq * p.K + u0 + uh : nullptr);
+        const float* dhi = p.dh + row * p.K + u0 + uh;
+        __nv_bfloat16* dp = p.dpre + row * 4 * p.K + u0 + uh;
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const float4 vi = *reinterpret_cast<const float4*>(gr + q4 * 4);
+          const float4 vc = *reinterpret_cast<const float4*>(gr + p.K + q4 * 4);
+          const float4 vf = *reinterpret_cast<const float4*>(gr + 2 * p.K + q4 * 4);
+          const float4 vo = *reinterpret_cast<const float4*>(gr + 3 * p.K + q4 * 4);
+          const float4 vs = *reinterpret_cast<const float4*>(sr + q4 * 4);
+          const float4 vsp = spr ? *reinterpret_cast<const float4*>(spr + q4 * 4) : make_float4(0, 0, 0, 0);
+          const float4 vdh = *reinterpret_cast<const float4*>(dhi + q4 * 4);
+          const float ai[4] = {vi.x, vi.y, vi.z, vi.w}, ac[4] = {vc.x, vc.y, vc.z, vc.w};
+          const float af[4] = {vf.x, vf.y, vf.z, vf.w}, ao[4] = {vo.x, vo.y, vo.z, vo.w};
+          const float as[4] = {vs.x, vs.y, vs.z, vs.w}, asp[4] = {vsp.x, vsp.y, vsp.z, vsp.w};
+          const float adh[4] = {vdh.x, vdh.y, vdh.z, vdh.w};
+          float o_i[4], o_c[4], o_f[4], o_o[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int q = q4 * 4 + e;
+            const float dht = adh[e] + dhr[q];
+            const float ts = tanhf(as[e]);
+            const float ds = dht * ao[e] * (1.0f - ts * ts) + dsc[q];
+            o_i[e] = ds * ac[e] * ai[e] * (1.0f - ai[e]);
+            o_c[e] = ds * ai[e] * (1.0f - ac[e] * ac[e]);
+            o_f[e] = ds * asp[e] * af[e] * (1.0f - af[e]);
+            o_o[e] = dht * ts * ao[e] * (1.0f - ao[e]);
+            dsc[q] = ds * af[e];
+          }
+          *reinterpret_cast<uint2*>(dp + q4 * 4) = make_uint2(pack_bf16x2(o_i[0], o_i[1]), pack_bf16x2(o_i[2], o_i[3]));
+          *reinterpret_cast<uint2*>(dp + p.K + q4 * 4) =
+              make_uint2(pack_bf16x2(o_c[0], o_c[1]), pack_bf16x2(o_c[2], o_c[3]));
+          *reinterpret_cast<uint2*>(dp + 2 * p.K + q4 * 4) =
+              make_uint2(pack_bf16x2(o_f[0], o_f[1]), pack_bf16x2(o_f[2], o_f[3]));
+          *reinterpret_cast<uint2*>(dp + 3 * p.K + q4 * 4) =
+              make_uint2(pack_bf16x2(o_o[0], o_o[1]), pack_bf16x2(o_o[2], o_o[3]));
+        }
+        if (t == 0 && p.ds0 != nullptr) {
+          float* d0 = p.ds0 + static_cast<int64_t>(rq) * p.K + u0 + uh;
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4)
+            *reinterpret_cast<float4*>(d0 + 4 * q4) = make_float4(dsc[4 * q4], dsc[4 * q4 + 1], dsc[4 * q4 + 2],
+                                                                  dsc[4 * q4 + 3]);
+        }
+      }
+      fence_proxy_async_global();
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (threadIdx.x == 0) {
+        __threadfence();
+        // this CTA wrote rows of its quarter for units u0..u0+31 of all four gates
+#pragma unroll
+        for (int gg = 0; gg < 4; ++gg) atomicAdd(&p.flags[(gg * p.K + u0) / 64], 1u);
+      }
+      if (t < p.T - 1) {
+        __syncwarp();
+        if (lane == 0) {
+#pragma unroll
+          for (int r = 0; r < 4; ++r) mbar_arrive_cluster(free_peer[r]);  // done reading the partials
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // no CTA leaves while a peer may still read its shared memory
+  if (warp == 4) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 64);
+  }
+}
+
+int smem_fwd(int K) { return kStagesS * kStageBytesS + (K / 64) * 4 * kJf * 128 + 256 + 1024; }
+int smem_bwd(int K) { return kStagesS * kStageBytesS + (K / 64) * kJb * 128 + 256 * kJb * 4 + 256 + 1024; }
+
+int check_seq(int T, int N, int K) {
+  char buf[200];
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (T <= 0 || N <= 0 || N > 256 || K <= 0 || K % 64 || K / kJf > sms || smem_fwd(K) > 232448 ||
+      smem_bwd(K) > 232448) {
+    std::snprintf(buf, sizeof(buf),
+                  "lstm sequence kernels need 1 <= N <= 256, K %% 64 == 0, K/8 <= %d SMs, K <= 1024 "
+                  "(T=%d N=%d K=%d)", sms, T, N, K);
+    return set_error(BRK_ERR_CONTRACT, buf);
+  }
+  return BRK_OK;
+}
+
+}  // namespace
+}  // namespace brk
+
+using namespace brk;
+
+extern "C" {
+
+BRK_API size_t brk_lstm_seq_flags_bytes(int K) { return static_cast<size_t>(4 * (K / 64) + 4) * sizeof(unsigned); }
+
+BRK_API int brk_lstm_seq_fwd(const float* gx, const void* r_cat, const float* s0, void* h_bf, float* h_out,
+                             float* s_out, float* gates_out, unsigned* flags, int T, int N, int K, void* stream) {
+  int rc = check_seq(T, N, K);
+  if (rc) return rc;
+  SeqParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.T = T; p.N = N; p.K = K;
+  p.gx = gx; p.s0 = s0; p.h_out = h_out; p.s_out = s_out; p.gates_out = gates_out;
+  p.h_bf = static_cast<__nv_bfloat16*>(h_bf);
+  p.flags = flags;
+  {
+    const uint64_t dims[3] = {(uint64_t)K, (uint64_t)N, (uint64_t)(T + 1)};
+    const uint64_t strides[3] = {1, (uint64_t)K, (uint64_t)N * K};
+    const uint32_t box[3] = {64, 128, 1};
+    if ((rc = encode_tmap(&p.map_a, h_bf, true, 3, dims, strides, box))) return rc;
+  }
+  {
+    const uint64_t dims[2] = {(uint64_t)K, (uint64_t)(4 * K)};
+    const uint64_t strides[2] = {1, (uint64_t)K};
+    const uint32_t box[2] = {64, 8};
+    if ((rc = encode_tmap(&p.map_w, r_cat, true, 2, dims, strides, box))) return rc;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t err = cudaMemsetAsync(flags, 0, brk_lstm_seq_flags_bytes(K), st);
+  if (err != cudaSuccess) return set_cuda_error(err, "lstm seq flags");
+  const int smem = smem_fwd(K);
+  err = cudaFuncSetAttribute(lstm_seq_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (err != cudaSuccess) return set_cuda_error(err, "lstm seq fwd smem");
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(K / kJf);
+  cfg.blockDim = dim3(kThreadsS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (they wait on each other's chunks)
+  attr.val.cooperative = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  g_launches.fetch_add(1);
+  err = cudaLaunchKernelEx(&cfg, lstm_seq_fwd_kernel, p);
+  return err == cudaSuccess ? BRK_OK : set_cuda_error(err, "lstm seq fwd launch");
+}
+
+BRK_API int brk_lstm_seq_bwd(const float* dh, const float* gates, const float* s, const float* s0,
+                             const void* rt_cat, void* dpre, float* ds0, unsigned* flags, int T, int N, int K,
+                             void* stream) {
+  int rc = check_seq(T, N, K);
+  if (rc) return rc;
+  if (K % kJb) return set_error(BRK_ERR_CONTRACT, "lstm seq bwd: K must be a multiple of 32");
+  SeqParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.T = T; p.N = N; p.K = K;
+  p.dh = dh; p.gates = gates; p.s = s; p.s0 = s0;
+  p.dpre = static_cast<__nv_bfloat16*>(dpre);
+  p.ds0 = ds0;
+  p.flags = flags;
+  {
+    const uint64_t dims[3] = {(uint64_t)(4 * K), (uint64_t)N, (uint64_t)T};
+    const uint64_t strides[3] = {1, (uint64_t)(4 * K), (uint64_t)N * 4 * K};
+    const uint32_t box[3] = {64, 128, 1};
+    if ((rc = encode_tmap(&p.map_a, dpre, true, 3, dims, strides, box))) return rc;
+  }
+  {
+    const uint64_t dims[2] = {(uint64_t)K, (uint64_t)(4 * K)};
+    const uint64_t strides[2] = {1, (uint64_t)K};
+    const uint32_t box[2] = {64, 32};
+    if ((rc = encode_tmap(&p.map_w, rt_cat, true, 2, dims, strides, box))) return rc;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t err = cudaMemsetAsync(flags, 0, brk_lstm_seq_flags_bytes(K), st);
+  if (err != cudaSuccess) return set_cuda_error(err, "lstm seq flags");
+  const int smem = smem_bwd(K);
+  err = cudaFuncSetAttribute(lstm_seq_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (err != cudaSuccess) return set_cuda_error(err, "lstm seq bwd smem");
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(4 * (K / kJb));
+  cfg.blockDim = dim3(kThreadsS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 4;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int max_clusters = 0;
+  err = cudaOccupancyMaxActiveClusters(&max_clusters, lstm_seq_bwd_kernel, &cfg);
+  if (err != cudaSuccess) return set_cuda_error(err, "lstm seq bwd occupancy");
+  if (max_clusters < K / kJb) {
+    char buf[160];
+    std::snprintf(buf, sizeof(buf), "lstm seq bwd: %d co-resident 4-CTA clusters needed, device offers %d",
+                  K / kJb, max_clusters);
+    return set_error(BRK_ERR_CONTRACT, buf);
+  }
+  g_launches.fetch_add(1);
+  err = cudaLaunchKernelEx(&cfg, lstm_seq_bwd_kernel, p);
+  return err == cudaSuccess ? BRK_OK : set_cuda_error(err, "lstm seq bwd launch");
+}
+
+}  // extern "C"

@@ -236,6 +236,72 @@ def _to_dev(a, shape=None):
     return t
 
 
+class _SeqCell:
+    """bf16 dense operands of the persistent sequence kernels (cached on the params):
+    W_cat [4K][C] (rows g*K + k = W_g[k]), R_cat [4K][K], RT_cat [4K][K] (R_g^T), bias [4K]."""
+
+    def __init__(self, params: LstmParams, dc: _DeviceCell):
+        torch = require_cuda()
+        k, c = params.k, params.c
+
+        def dense(blk, cols):  # [K_b][X_b][b_x][b_k] -> (K, X)
+            return blk.permute(0, 3, 1, 2).reshape(k, cols)
+
+        w = [dense(dc.W[i], c) for i in range(4)]
+        r = [dense(dc.R[i], k) for i in range(4)]
+        self.w_cat = torch.cat(w).to(torch.bfloat16).contiguous()
+        self.r_cat = torch.cat(r).to(torch.bfloat16).contiguous()
+        self.rt_cat = torch.cat([ri.t() for ri in r]).to(torch.bfloat16).contiguous()
+        self.bias = dc.bias
+
+
+def _seq_cell(params: LstmParams) -> _SeqCell:
+    cache = getattr(params, "_brk_seq_cell", None)
+    if cache is None:
+        cache = _SeqCell(params, _device_cell(params))
+        object.__setattr__(params, "_brk_seq_cell", cache)
+    return cache
+
+
+def _seq_ok(params: LstmParams, prec: str) -> bool:
+    """The persistent sequence kernels (brk_lstm_seq_*) serve bf16 compute with
+    N <= 256, K % 64 == 0, K <= 1024 and C % 8 == 0; other shapes and TF32 use
+    the per-step kernels."""
+    import os
+    if os.environ.get("BRK_LSTM_SEQ", "1") == "0":
+        return False
+    return (prec == "bf16" and params.n <= 256 and params.k % 64 == 0 and params.k <= 1024
+            and params.c % 8 == 0)
+
+
+def _flags(k):
+    torch = require_cuda()
+    nbytes = _lib.load().brk_lstm_seq_flags_bytes(k)
+    return torch.zeros(nbytes // 4, dtype=torch.int32, device="cuda")
+
+
+def _forward_seq(params, xd, h0, s0, prec):
+    from ._dense import gemm
+
+    torch = require_cuda()
+    T, N, C, K = params.t_steps, params.n, params.c, params.k
+    sc = _seq_cell(params)
+    xb = xd.to(torch.bfloat16)
+    gx = torch.empty((T * N, 4 * K), dtype=torch.float32, device="cuda")
+    gemm(xb, sc.w_cat, gx, bias=sc.bias)  # all steps' input projections: one BRGEMM launch
+    h = torch.empty((T, N, K), dtype=torch.float32, device="cuda")
+    s = torch.empty((T, N, K), dtype=torch.float32, device="cuda")
+    gates = torch.empty((T, N, 4, K), dtype=torch.float32, device="cuda")
+    h_bf = torch.empty((T + 1, N, K), dtype=torch.bfloat16, device="cuda")
+    h_bf[0].copy_(h0)
+    flags = _flags(K)
+    rc = _lib.load().brk_lstm_seq_fwd(gx.data_ptr(), sc.r_cat.data_ptr(), s0.data_ptr() if s0 is not None else None,
+                                      h_bf.data_ptr(), h.data_ptr(), s.data_ptr(), gates.data_ptr(), flags.data_ptr(),
+                                      T, N, K, stream_ptr())
+    _lib.check(rc, LayoutError)
+    return h, s, gates, h_bf
+
+
 def _compute(precision):
     prec = precision or get_default_precision()
     return prec, (_lib.BRK_COMPUTE_TF32 if prec == "tf32" else _lib.BRK_COMPUTE_BF16)
@@ -279,6 +345,12 @@ def lstm_forward(params: LstmParams, x, h_init=None, s_init=None, workers: int =
     prec, code = _compute(precision)
     dc = _device_cell(params)
     xd = _to_dev(x).reshape(t_steps * n, c)
+    if _seq_ok(params, prec):
+        h0 = _to_dev(h_init, (n, k)) if h_init is not None else torch.zeros((n, k), dtype=torch.float32,
+                                                                             device="cuda")
+        s0 = _to_dev(s_init, (n, k)) if s_init is not None else None
+        h, s, gates, h_bf = _forward_seq(params, xd, h0, s0, prec)
+        return _finish_forward(h, s, gates, host, keep_gates, h_bf)
     gx = _input_projection(dc, params, xd, prec).reshape(t_steps, n, 4, k)
     h = torch.empty((t_steps, n, k), dtype=torch.float32, device="cuda")
     s = torch.empty((t_steps, n, k), dtype=torch.float32, device="cuda")
@@ -294,6 +366,10 @@ def lstm_forward(params: LstmParams, x, h_init=None, s_init=None, workers: int =
                                    dc.R.data_ptr(), h[t].data_ptr(), s[t].data_ptr(), gates[t].data_ptr(),
                                    n, k, params.b_k, code, st)
         _lib.check(rc, LayoutError)
+    return _finish_forward(h, s, gates, host, keep_gates, None)
+
+
+def _finish_forward(h, s, gates, host, keep_gates, h_bf):
     if host:
         g_np = gates.cpu().numpy()
         gd = {g: np.ascontiguousarray(g_np[:, :, i]) for i, g in enumerate(GATE_NAMES)} if keep_gates else None
@@ -302,6 +378,7 @@ def lstm_forward(params: LstmParams, x, h_init=None, s_init=None, workers: int =
         gd = {g: gates[:, :, i] for i, g in enumerate(GATE_NAMES)} if keep_gates else None
         seq = LstmStateSequence(h=h, s=s, gates=gd)
     seq._brk_gates_dev = gates  # BPTT needs all four gates of every step
+    seq._brk_h_bf = h_bf        # bf16 h_{t-1} of every step (sequence kernels): the dR operand
     return seq
 
 
@@ -331,6 +408,14 @@ def lstm_backward(params: LstmParams, x, seq: LstmStateSequence, dh, h_init=None
     xd = _to_dev(x).reshape(t_steps * n, c)
     h0 = _to_dev(h_init) if h_init is not None else torch.zeros((n, k), dtype=torch.float32, device="cuda")
     s0 = _to_dev(s_init) if s_init is not None else None
+    if _seq_ok(params, prec) and k % 32 == 0:
+        out = _backward_seq(params, xd, hd, sd, gates, dhd, h0, s0, getattr(seq, "_brk_h_bf", None))
+        if host:
+            cpu = lambda t: t.cpu().numpy()  # noqa: E731
+            out = LstmGrads(dx=cpu(out.dx), dw={g: cpu(v) for g, v in out.dw.items()},
+                            dr={g: cpu(v) for g, v in out.dr.items()}, db={g: cpu(v) for g, v in out.db.items()},
+                            dh0=cpu(out.dh0), ds0=cpu(out.ds0))
+        return out
     dpre = torch.empty((t_steps, n, 4, k), dtype=torch.float32, device="cuda")
     ds = [torch.empty((n, k), dtype=torch.float32, device="cuda") for _ in range(2)]
     lib = _lib.load()
@@ -395,3 +480,45 @@ def lstm_backward(params: LstmParams, x, seq: LstmStateSequence, dh, h_init=None
                         dr={g: cpu(v) for g, v in out.dr.items()}, db={g: cpu(v) for g, v in out.db.items()},
                         dh0=cpu(dh0), ds0=cpu(ds0))
     return out
+
+
+def _backward_seq(params, xd, hd, sd, gates, dhd, h0, s0, h_bf):
+    """BPTT on the persistent backward kernel, then the step-independent
+    products as single BRGEMM launches over all T*N rows: dx = dpre W,
+    dW = dpre^T x, dR = dpre^T h_prev, dh0 = dpre_0 R, db = column sums."""
+    from ._dense import gemm
+
+    torch = require_cuda()
+    T, N, C, K = params.t_steps, params.n, params.c, params.k
+    sc = _seq_cell(params)
+    lib = _lib.load()
+    st = stream_ptr()
+    dpre = torch.empty((T, N, 4, K), dtype=torch.bfloat16, device="cuda")
+    ds0 = torch.empty((N, K), dtype=torch.float32, device="cuda")
+    flags = _flags(K)
+    rc = lib.brk_lstm_seq_bwd(dhd.data_ptr(), gates.data_ptr(), sd.data_ptr(),
+                              s0.data_ptr() if s0 is not None else None, sc.rt_cat.data_ptr(), dpre.data_ptr(),
+                              ds0.data_ptr(), flags.data_ptr(), T, N, K, st)
+    _lib.check(rc, LayoutError)
+    rows = T * N
+    dp2 = dpre.reshape(rows, 4 * K)
+    dh0 = torch.empty((N, K), dtype=torch.float32, device="cuda")
+    gemm(dp2[:N], sc.r_cat, dh0, b_t=True)                   # dh0 = dpre_0 [R_i; R_c; R_f; R_o]
+    dx = torch.empty((rows, C), dtype=torch.float32, device="cuda")
+    gemm(dp2, sc.w_cat, dx, b_t=True)                        # dx = dpre W_cat
+    xb = xd.to(torch.bfloat16)
+    if h_bf is None:
+        h_bf = torch.empty((T + 1, N, K), dtype=torch.bfloat16, device="cuda")
+        h_bf[0].copy_(h0)
+        h_bf[1:].copy_(hd)
+    hp = h_bf[:T].reshape(rows, K)
+    dw = torch.empty((4 * K, C), dtype=torch.float32, device="cuda")
+    gemm(dp2, xb, dw, a_t=True, b_t=True)                    # dW_cat = dpre^T x (reduction over T*N in TMEM)
+    dr = torch.empty((4 * K, K), dtype=torch.float32, device="cuda")
+    gemm(dp2, hp, dr, a_t=True, b_t=True)                    # dR_cat = dpre^T h_prev
+    db = torch.empty(4 * K, dtype=torch.float32, device="cuda")
+    _lib.check(lib.brk_colsum_blocked(dp2.data_ptr(), None, None, db.data_ptr(), rows, 4 * K, rows, 4 * K,
+                                      _lib.BRK_BF16, st), LayoutError)
+    sl = lambda t: [t[i * K:(i + 1) * K] for i in range(4)]  # noqa: E731
+    return LstmGrads(dx=dx.reshape(T, N, C), dw=dict(zip(GATE_NAMES, sl(dw))), dr=dict(zip(GATE_NAMES, sl(dr))),
+                     db=dict(zip(GATE_NAMES, sl(db))), dh0=dh0, ds0=ds0)

@@ -116,3 +116,42 @@ def test_causality_and_determinism():
     for t in (1, 3, 5):
         part = lstm_forward(LstmParams.from_dense(wt, t, 4, b_k=4, b_c=4, b_n=2), x[:t].copy())
         assert np.array_equal(part.h, full.h[:t])
+
+
+@pytest.mark.parametrize("shape", [(3, 168, 1024, 1024), (6, 200, 128, 256), (2, 40, 32, 64)])
+def test_sequence_kernels_vs_oracle(shape):
+    """The persistent sequence kernels (brk_lstm_seq_fwd/bwd, bf16) at the
+    benchmark width (128 CTAs fwd, 32 four-CTA clusters bwd) and odd sizes."""
+    t, n, c, k = shape
+    rng = np.random.default_rng(sum(shape))
+    wt = LstmCellWeights.random(rng, c, k)
+    x = rng.uniform(-1, 1, (t, n, c)).astype(F32)
+    h0 = rng.uniform(-1, 1, (n, k)).astype(F32)
+    s0 = rng.uniform(-1, 1, (n, k)).astype(F32)
+    dh = rng.uniform(-1, 1, (t, n, k)).astype(F32)
+    params = LstmParams.from_dense(wt, t, n)
+    w, r, bias = oracle_args(wt)
+    fwd_ref = orc.lstm_forward_reference(w, r, bias, x, h0, s0)
+    with precision("bf16"):
+        seq = lstm_forward(params, x, h0, s0, keep_gates=True)
+        grads = lstm_backward(params, x, seq, dh, h0, s0)
+    assert orc.scale_rel_error(seq.h, fwd_ref["h"]) <= 1e-2
+    assert orc.scale_rel_error(seq.s, fwd_ref["s"]) <= 1e-2
+    ref = orc.lstm_backward_reference(w, r, x, {"h": seq.h, "s": seq.s, "gates": seq.gates}, dh, h0, s0)
+    for name in ("dx", "dh0", "ds0"):
+        assert orc.scale_rel_error(getattr(grads, name), ref[name]) <= 2e-2, name
+    for g in GATE_NAMES:
+        assert orc.scale_rel_error(grads.dw[g], ref["dw"][g]) <= 2e-2, g
+        assert orc.scale_rel_error(grads.dr[g], ref["dr"][g]) <= 2e-2, g
+        assert orc.scale_rel_error(grads.db[g], ref["db"][g]) <= 2e-2, g
+
+
+def test_sequence_and_step_paths_agree(monkeypatch):
+    rng = np.random.default_rng(3)
+    wt = LstmCellWeights.random(rng, 128, 128)
+    x = rng.uniform(-1, 1, (5, 64, 128)).astype(F32)
+    with precision("bf16"):
+        a = lstm_forward(LstmParams.from_dense(wt, 5, 64), x)
+        monkeypatch.setenv("BRK_LSTM_SEQ", "0")
+        b = lstm_forward(LstmParams.from_dense(wt, 5, 64), x)
+    assert orc.scale_rel_error(a.h, b.h) <= 1e-2

@@ -166,6 +166,38 @@ def resnet_suite(n=256, iters=10, layers=None, passes=("fwd", "bwd", "upd")):
     return {"n": n, "peak_tflops": peak, "hbm_gbs": hbm, "peak_source": src, "layers": rows, "summary": summary}
 
 
+def lstm_suite(t_steps=50, n=168, c=1024, k=1024, iters=3, precision="bf16"):
+    """LSTM cell (BASELINE config 3): fwd and bwd+upd device time at T steps.
+
+    FLOPs as the reference (bench.py:97-103): fwd 2TN(4KC+4KK); bwd+upd twice that.
+    """
+    import numpy as np
+    import torch
+
+    from paper_1906_06440_b200 import precision as prec_ctx
+    from paper_1906_06440_b200.lstm import LstmCellWeights, LstmParams, lstm_backward, lstm_forward
+
+    rng = np.random.default_rng([0, 303])
+    wt = LstmCellWeights.random(rng, c, k)
+    params = LstmParams.from_dense(wt, t_steps, n)
+    x = torch.from_numpy(rng.uniform(-1, 1, (t_steps, n, c)).astype(np.float32)).cuda()
+    dh = torch.from_numpy(rng.uniform(-1, 1, (t_steps, n, k)).astype(np.float32)).cuda()
+    flops_fwd = 2.0 * t_steps * n * (4 * k * c + 4 * k * k)
+    timer = _Timer(torch)
+    out = {}
+    with prec_ctx(precision):
+        seq = lstm_forward(params, x)
+        fwd_mean, fwd_min = timer(lambda sp: lstm_forward(params, x), iters, warmup=1)
+        bwd_mean, bwd_min = timer(lambda sp: lstm_backward(params, x, seq, dh), iters, warmup=1)
+    peak, _, src = _peaks()
+    out["fwd"] = {"ms": fwd_mean * 1e3, "tflops": flops_fwd / fwd_mean / 1e12}
+    out["bwd_upd"] = {"ms": bwd_mean * 1e3, "tflops": 2 * flops_fwd / bwd_mean / 1e12}
+    tot = 3 * flops_fwd / (fwd_mean + bwd_mean)
+    out["all"] = {"tflops": tot / 1e12, "frac_of_peak": tot / (peak * 1e12), "gflop": 3 * flops_fwd / 1e9}
+    out["config"] = {"T": t_steps, "N": n, "C": c, "K": k, "compute": precision, "storage": "fp32 h/s/gates"}
+    return out
+
+
 def _plan(lib, pass_, geom):
     import ctypes
     out = (ctypes.c_int * 3)()
@@ -189,3 +221,5 @@ if __name__ == "__main__":
         print(json.dumps(res["summary"], indent=1))
         (ROOT / "gpurun_out").mkdir(exist_ok=True)
         (ROOT / "gpurun_out" / f"resnet_n{n}.json").write_text(json.dumps(res, indent=1))
+    elif what == "lstm":
+        print(json.dumps(lstm_suite(), indent=1))
