@@ -209,6 +209,8 @@ BRK_API size_t brk_gemm_dense_workspace(int64_t M, int N, int K);
  * dpre [T][N][4][K] (bf16 pre-activation gradients) and ds0 [N][K].
  * ------------------------------------------------------------------------- */
 BRK_API size_t brk_lstm_seq_flags_bytes(int K);
+/* Diagnostic: per-step %globaltimer stamps of CTA 0 ([T][8] u64) for subsequent sequence launches; NULL disables. */
+BRK_API void brk_diag_lstm_timestamps(unsigned long long* ts);
 BRK_API int brk_lstm_seq_fwd(const float* gx, const void* r_cat, const float* s0, void* h_bf, float* h_out,
                              float* s_out, float* gates_out, unsigned* flags, int T, int N, int K, void* stream);
 BRK_API int brk_lstm_seq_bwd(const float* dh, const float* gates, const float* s, const float* s0,

@@ -67,6 +67,7 @@ SIGNATURES: dict[str, tuple] = {
                                 _c_int, _c_f, _c_f, _vp, _c_int, _vp, ctypes.c_size_t, _vp]),
     "brk_gemm_dense_workspace": (ctypes.c_size_t, [_c_i64, _c_int, _c_int]),
     "brk_lstm_seq_flags_bytes": (ctypes.c_size_t, [_c_int]),
+    "brk_diag_lstm_timestamps": (None, [_vp]),
     "brk_lstm_seq_fwd": (_c_int, [_vp] * 8 + [_c_int, _c_int, _c_int, _vp]),
     "brk_lstm_seq_bwd": (_c_int, [_vp] * 8 + [_c_int, _c_int, _c_int, _vp]),
     "brk_brgemm_offs": (

@@ -16,16 +16,22 @@ __device__ __forceinline__ void st_any(void* p, int64_t i, float v, int bf16) {
   else static_cast<float*>(p)[i] = v;
 }
 
-// One thread per column k; rows summed in ascending n (deterministic).
-__global__ void colsum_blocked_kernel(const void* dy, const void* y, void* dz_out, float* db, int N, int K,
-                                      int b_n, int b_k, int bf16) {
+// Column sums in two deterministic passes: pass 1, CTA (column tile, row split)
+// sums its rows per column (threads = consecutive columns: coalesced rows of
+// the blocked layout); pass 2 adds the split partials in split order.
+__device__ __forceinline__ int64_t blk_off(int n, int k, int Kb, int b_n, int b_k) {
+  return (static_cast<int64_t>(n / b_n) * Kb + k / b_k) * b_n * b_k + static_cast<int64_t>(n % b_n) * b_k + k % b_k;
+}
+
+__global__ void colsum_partial_kernel(const void* dy, const void* y, void* dz_out, float* part, int N, int K,
+                                      int b_n, int b_k, int bf16, int rows_per) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= K) return;
   const int Kb = K / b_k;
-  const int kb = k / b_k, ki = k % b_k;
+  const int n0 = blockIdx.y * rows_per, n1 = min(N, n0 + rows_per);
   float s = 0.0f;
-  for (int n = 0; n < N; ++n) {
-    const int64_t off = (static_cast<int64_t>(n / b_n) * Kb + kb) * b_n * b_k + static_cast<int64_t>(n % b_n) * b_k + ki;
+  for (int n = n0; n < n1; ++n) {
+    const int64_t off = blk_off(n, k, Kb, b_n, b_k);
     float g = ld_any(dy, off, bf16);
     if (y != nullptr) {
       if (!(ld_any(y, off, bf16) > 0.0f)) g = 0.0f;
@@ -33,6 +39,14 @@ __global__ void colsum_blocked_kernel(const void* dy, const void* y, void* dz_ou
     }
     s += g;
   }
+  part[static_cast<int64_t>(blockIdx.y) * K + k] = s;
+}
+
+__global__ void colsum_final_kernel(const float* part, int splits, int K, float* db) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  float s = 0.0f;
+  for (int i = 0; i < splits; ++i) s += part[static_cast<int64_t>(i) * K + k];
   db[k] = s;
 }
 
@@ -55,11 +69,23 @@ BRK_API int brk_colsum_blocked(const void* dy, const void* y, void* dz_out, floa
   if (N <= 0 || K <= 0 || b_n <= 0 || b_k <= 0 || N % b_n || K % b_k)
     return set_error(BRK_ERR_CONTRACT, "colsum: block factors must divide N and K");
   if (dtype != BRK_F32 && dtype != BRK_BF16) return set_error(BRK_ERR_CONTRACT, "colsum: bad dtype");
-  g_launches.fetch_add(1);
-  colsum_blocked_kernel<<<(K + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(
-      dy, y, dz_out, db, N, K, b_n, b_k, dtype == BRK_BF16);
-  cudaError_t err = cudaGetLastError();
-  return err == cudaSuccess ? BRK_OK : set_cuda_error(err, "colsum launch");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int tiles = (K + 255) / 256;
+  int splits = (148 * 8) / tiles;
+  splits = splits < 1 ? 1 : (splits > N ? N : splits);
+  const int rows_per = (N + splits - 1) / splits;
+  splits = (N + rows_per - 1) / rows_per;
+  float* part = nullptr;  // stream-ordered scratch
+  cudaError_t err = cudaMallocAsync(reinterpret_cast<void**>(&part), static_cast<size_t>(splits) * K * sizeof(float), st);
+  if (err != cudaSuccess) return set_cuda_error(err, "colsum scratch");
+  g_launches.fetch_add(2);
+  colsum_partial_kernel<<<dim3(tiles, splits), 256, 0, st>>>(dy, y, dz_out, part, N, K, b_n, b_k, dtype == BRK_BF16,
+                                                             rows_per);
+  colsum_final_kernel<<<tiles, 256, 0, st>>>(part, splits, K, db);
+  err = cudaGetLastError();
+  cudaError_t err2 = cudaFreeAsync(part, st);
+  if (err != cudaSuccess) return set_cuda_error(err, "colsum launch");
+  return err2 == cudaSuccess ? BRK_OK : set_cuda_error(err2, "colsum scratch free");
 }
 
 BRK_API int brk_sgd_apply(void* w, const float* dw, float lr, int64_t n, int w_dtype, void* stream) {

@@ -54,12 +54,29 @@ struct SeqParams {
   __nv_bfloat16* dpre;   // [T][N][4][K] (bf16; A operand of the next step and of the weight gradients)
   float* ds0;            // [N][K] dL/ds_{-1}
   unsigned* flags;       // per 64-column chunk release counters (zeroed by the host)
+  unsigned long long* ts;  // diagnostics: per-step %globaltimer stamps of CTA 0 [T][8] (or null)
 };
+
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define SEQ_TS(step, slot)                                                          \
+  do {                                                                              \
+    if (p.ts != nullptr && blockIdx.x == 0) p.ts[(step) * 8 + (slot)] = gtime();    \
+  } while (0)
 
 __device__ __forceinline__ float sigm_s(float x) {
   const float e = __expf(-fabsf(x));
   const float r = __fdividef(1.0f, 1.0f + e);
   return x >= 0.0f ? r : e * r;
+}
+
+// tanh(x) = 1 - 2 / (e^{2x} + 1), saturating correctly at both ends
+__device__ __forceinline__ float tanh_f(float x) {
+  const float e = __expf(2.0f * x);
+  return 1.0f - __fdividef(2.0f, e + 1.0f);
 }
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
@@ -85,6 +102,29 @@ __device__ __forceinline__ void mbar_wait_acq_cluster(uint64_t* bar, uint32_t pa
         : "r"(smem_u32(bar)), "r"(parity)
         : "memory");
   } while (!ok);
+}
+__device__ __forceinline__ uint32_t cluster_nctas() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+// 3-d TMA load multicast to every CTA of the cluster in `mask` (same smem offset,
+// complete_tx on the same-offset mbarrier of each destination CTA)
+__device__ __forceinline__ void tma_load3_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
+                                             uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "h"(mask)
+      : "memory");
+}
+// arrive (when this CTA's prior MMAs complete) on the same-offset barrier of every CTA in `mask`
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
 }
 __device__ __forceinline__ float4 ld_dsmem_f4(uint32_t addr) {
   float4 v;
@@ -113,9 +153,15 @@ __global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_fwd_kernel(const __grid
   const int j0 = blockIdx.x * kJf;
   const int n_mt = p.N > 128 ? 2 : 1;
   const int chunk_owners = 64 / kJf;  // CTAs writing one 64-column chunk of h
+  // The CTAs of a cluster share each streamed chunk: CTA r loads rows
+  // [r*256/cs, (r+1)*256/cs) of the 256-row tile and multicasts them to all.
+  const int cs = static_cast<int>(cluster_nctas());
+  const int crank = static_cast<int>(cluster_ctarank());
+  const uint16_t cmask = static_cast<uint16_t>((1u << cs) - 1u);
+  const int slice = 256 / cs;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStagesS; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < kStagesS; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], cs); }
     mbar_init(tfull, 1);
     mbar_init(tempty, 4);
     mbar_init(wbar, 1);
@@ -123,7 +169,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_fwd_kernel(const __grid
   }
   if (warp == 4) tmem_alloc(tslot, 64);
   tc_fence_before();
-  __syncthreads();
+  cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem = *tslot;
 
@@ -148,10 +194,12 @@ __global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_fwd_kernel(const __grid
           }
           fence_proxy_async_global();
         }
-        mbar_wait(&empty[pid], ph ^ 1);
-        mbar_arrive_expect_tx(&full[pid], n_mt * 16384);
-        for (int mt = 0; mt < n_mt; ++mt)
-          tma_load3(ring + pid * kStageBytesS + mt * 16384, &p.map_a, &full[pid], kc * 64, mt * 128, t);
+        if (kc == 0) SEQ_TS(t, 0);       // chunk 0 of h_{t-1} released
+        if (kc == KC - 1) SEQ_TS(t, 1);  // last chunk released
+        mbar_wait(&empty[pid], ph ^ 1);  // every CTA of the cluster consumed this stage
+        mbar_arrive_expect_tx(&full[pid], kStageBytesS);
+        tma_load3_mc(ring + pid * kStageBytesS + crank * slice * 128, &p.map_a, &full[pid], kc * 64, crank * slice,
+                     t, cmask);
       }
     }
   } else if (warp == 4) {
@@ -165,6 +213,8 @@ __global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_fwd_kernel(const __grid
         const int gi = t * KC + kc, st = gi % kStagesS;
         mbar_wait(&full[st], (gi / kStagesS) & 1);
         tc_fence_after();
+        if (lane == 0 && kc == 0) SEQ_TS(t, 2);       // first chunk landed
+        if (lane == 0 && kc == KC - 1) SEQ_TS(t, 3);  // last chunk landed
         if (elect_one()) {
           const uint32_t a0 = smem_u32(ring + st * kStageBytesS);
           const uint32_t b0 = smem_u32(wsm + kc * kGN * 128);
@@ -173,7 +223,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_fwd_kernel(const __grid
             for (int kk = 0; kk < 4; ++kk)
               mma_ss<false>(tmem + mt * kGN, make_smem_desc(a0 + mt * 16384 + kk * 32, 16, 1024, kSwizzle128B),
                             make_smem_desc(b0 + kk * 32, 16, 1024, kSwizzle128B), idesc, (kc | kk) ? 1u : 0u);
-          mma_commit(&empty[st]);
+          mma_commit_mc(&empty[st], cmask);  // the stage is free in the whole cluster once all CTAs arrive
           if (kc == KC - 1) mma_commit(tfull);
         }
         __syncwarp();
@@ -181,6 +231,9 @@ __global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_fwd_kernel(const __grid
     }
   } else {
     // ---------------------------------------------------------------- epilogue (warps 0-3)
+    // Critical path per step: accumulator -> h_t (bf16) -> chunk release.  The
+    // step's input projections are prefetched while the MMAs run, and the fp32
+    // h / s / gate stores are issued only after the release.
     float sreg[2][kJf];
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt) {
@@ -190,8 +243,25 @@ __global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_fwd_kernel(const __grid
         sreg[mt][jj] = (p.s0 != nullptr && n < p.N) ? p.s0[static_cast<int64_t>(n) * p.K + j0 + jj] : 0.0f;
     }
     for (int t = 0; t < p.T; ++t) {
+      float pre[2][4][kJf];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        const int n = mt * 128 + warp * 32 + lane;
+        if (mt < n_mt && n < p.N) {
+          const float* gxr = p.gx + (static_cast<int64_t>(t) * p.N + n) * 4 * p.K + j0;
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            const float4 a = __ldcs(reinterpret_cast<const float4*>(gxr + g * p.K));
+            const float4 b = __ldcs(reinterpret_cast<const float4*>(gxr + g * p.K + 4));
+            pre[mt][g][0] = a.x; pre[mt][g][1] = a.y; pre[mt][g][2] = a.z; pre[mt][g][3] = a.w;
+            pre[mt][g][4] = b.x; pre[mt][g][5] = b.y; pre[mt][g][6] = b.z; pre[mt][g][7] = b.w;
+          }
+        }
+      }
       mbar_wait(tfull, t & 1);
       tc_fence_after();
+      if (threadIdx.x == 0) SEQ_TS(t, 4);  // accumulator ready
+      float hv[2][kJf];
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt) {
         if (mt >= n_mt) break;
@@ -200,43 +270,20 @@ __global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_fwd_kernel(const __grid
         tmem_ld_wait();
         const int n = mt * 128 + warp * 32 + lane;
         if (n < p.N) {
-          const int64_t row = static_cast<int64_t>(t) * p.N + n;
-          const float* gxr = p.gx + row * 4 * p.K + j0;
-          float pre[4][kJf];
-#pragma unroll
-          for (int g = 0; g < 4; ++g) {
-            const float4 a = *reinterpret_cast<const float4*>(gxr + g * p.K);
-            const float4 b = *reinterpret_cast<const float4*>(gxr + g * p.K + 4);
-            pre[g][0] = a.x; pre[g][1] = a.y; pre[g][2] = a.z; pre[g][3] = a.w;
-            pre[g][4] = b.x; pre[g][5] = b.y; pre[g][6] = b.z; pre[g][7] = b.w;
-#pragma unroll
-            for (int jj = 0; jj < kJf; ++jj) pre[g][jj] += __uint_as_float(v[g * kJf + jj]);
-          }
-          float hv[kJf];
 #pragma unroll
           for (int jj = 0; jj < kJf; ++jj) {
-            const float gi = sigm_s(pre[0][jj]), gc = tanhf(pre[1][jj]);
-            const float gf = sigm_s(pre[2][jj]), go = sigm_s(pre[3][jj]);
+            const float gi = sigm_s(pre[mt][0][jj] + __uint_as_float(v[jj]));
+            const float gc = tanh_f(pre[mt][1][jj] + __uint_as_float(v[kJf + jj]));
+            const float gf = sigm_s(pre[mt][2][jj] + __uint_as_float(v[2 * kJf + jj]));
+            const float go = sigm_s(pre[mt][3][jj] + __uint_as_float(v[3 * kJf + jj]));
             const float sv = gf * sreg[mt][jj] + gi * gc;
             sreg[mt][jj] = sv;
-            hv[jj] = go * tanhf(sv);
-            pre[0][jj] = gi; pre[1][jj] = gc; pre[2][jj] = gf; pre[3][jj] = go;
+            hv[mt][jj] = go * tanh_f(sv);
+            pre[mt][0][jj] = gi; pre[mt][1][jj] = gc; pre[mt][2][jj] = gf; pre[mt][3][jj] = go;
           }
-          float* go_ = p.gates_out + row * 4 * p.K + j0;
-#pragma unroll
-          for (int g = 0; g < 4; ++g) {
-            *reinterpret_cast<float4*>(go_ + g * p.K) = make_float4(pre[g][0], pre[g][1], pre[g][2], pre[g][3]);
-            *reinterpret_cast<float4*>(go_ + g * p.K + 4) = make_float4(pre[g][4], pre[g][5], pre[g][6], pre[g][7]);
-          }
-          float* ho = p.h_out + row * p.K + j0;
-          float* so = p.s_out + row * p.K + j0;
-          *reinterpret_cast<float4*>(ho) = make_float4(hv[0], hv[1], hv[2], hv[3]);
-          *reinterpret_cast<float4*>(ho + 4) = make_float4(hv[4], hv[5], hv[6], hv[7]);
-          *reinterpret_cast<float4*>(so) = make_float4(sreg[mt][0], sreg[mt][1], sreg[mt][2], sreg[mt][3]);
-          *reinterpret_cast<float4*>(so + 4) = make_float4(sreg[mt][4], sreg[mt][5], sreg[mt][6], sreg[mt][7]);
           *reinterpret_cast<uint4*>(p.h_bf + (static_cast<int64_t>(t + 1) * p.N + n) * p.K + j0) =
-              make_uint4(pack_bf16x2(hv[0], hv[1]), pack_bf16x2(hv[2], hv[3]), pack_bf16x2(hv[4], hv[5]),
-                         pack_bf16x2(hv[6], hv[7]));
+              make_uint4(pack_bf16x2(hv[mt][0], hv[mt][1]), pack_bf16x2(hv[mt][2], hv[mt][3]),
+                         pack_bf16x2(hv[mt][4], hv[mt][5]), pack_bf16x2(hv[mt][6], hv[mt][7]));
         }
       }
       tc_fence_before();
@@ -245,13 +292,37 @@ __global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_fwd_kernel(const __grid
       if (lane == 0) mbar_arrive(tempty);
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (threadIdx.x == 0) {
+        SEQ_TS(t, 5);  // epilogue done
         __threadfence();
         atomicAdd(&p.flags[j0 / 64], 1u);
+      }
+      // off the critical path: fp32 h, s and the activated gates (BPTT inputs)
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        const int n = mt * 128 + warp * 32 + lane;
+        if (mt < n_mt && n < p.N) {
+          const int64_t row = static_cast<int64_t>(t) * p.N + n;
+          float* go_ = p.gates_out + row * 4 * p.K + j0;
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            __stcs(reinterpret_cast<float4*>(go_ + g * p.K),
+                   make_float4(pre[mt][g][0], pre[mt][g][1], pre[mt][g][2], pre[mt][g][3]));
+            __stcs(reinterpret_cast<float4*>(go_ + g * p.K + 4),
+                   make_float4(pre[mt][g][4], pre[mt][g][5], pre[mt][g][6], pre[mt][g][7]));
+          }
+          float* ho = p.h_out + row * p.K + j0;
+          float* so = p.s_out + row * p.K + j0;
+          __stcs(reinterpret_cast<float4*>(ho), make_float4(hv[mt][0], hv[mt][1], hv[mt][2], hv[mt][3]));
+          __stcs(reinterpret_cast<float4*>(ho + 4), make_float4(hv[mt][4], hv[mt][5], hv[mt][6], hv[mt][7]));
+          __stcs(reinterpret_cast<float4*>(so), make_float4(sreg[mt][0], sreg[mt][1], sreg[mt][2], sreg[mt][3]));
+          __stcs(reinterpret_cast<float4*>(so + 4), make_float4(sreg[mt][4], sreg[mt][5], sreg[mt][6], sreg[mt][7]));
+        }
       }
     }
   }
   tc_fence_before();
   __syncthreads();
+  cluster_sync_all();  // peers may still multicast into / arrive on this CTA's shared memory
   if (warp == 4) {
     tc_fence_after();
     tmem_dealloc(tmem, 64);
@@ -316,6 +387,8 @@ __global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_bwd_kernel(const __grid
         while (ld_acquire(&p.flags[fidx]) < static_cast<unsigned>(chunk_owners * (it + 1))) {
         }
         fence_proxy_async_global();
+        if (kc == 0) SEQ_TS(it, 0);
+        if (kc == KC - 1) SEQ_TS(it, 1);
         const uint32_t ph = (gi / kStagesS) & 1;
         mbar_wait(&empty[pid], ph ^ 1);
         mbar_arrive_expect_tx(&full[pid], n_mt * 16384);
@@ -334,6 +407,8 @@ __global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_bwd_kernel(const __grid
         const int gi = it * KC + kc, st = gi % kStagesS;
         mbar_wait(&full[st], (gi / kStagesS) & 1);
         tc_fence_after();
+        if (lane == 0 && kc == 0) SEQ_TS(it, 2);
+        if (lane == 0 && kc == KC - 1) SEQ_TS(it, 3);
         if (elect_one()) {
           const uint32_t a0 = smem_u32(ring + st * kStageBytesS);
           const uint32_t b0 = smem_u32(wsm + kc * kJb * 128);
@@ -367,10 +442,50 @@ __global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_bwd_kernel(const __grid
     for (int t = p.T - 1; t >= 0; --t) {
       const int it = p.T - 1 - t;
       const int q = it - 1;  // index of the recurrent step (t < T-1)
+      // Everything but the recurrent term is known before the MMAs finish: load
+      // this step's gates / states / dh and fold them into per-element factors
+      //   ds = (dh + dh_rec) * A + dsc ; dpre_i = ds*CI ; dpre_c = ds*IC ;
+      //   dpre_f = ds*SF ; dpre_o = (dh + dh_rec) * B ; dsc <- ds * f
+      float fdh[16], fA[16], fB[16], fCI[16], fIC[16], fSF[16], ff[16];
+      const bool row_ok = rq < p.N;
+      const int64_t row = static_cast<int64_t>(t) * p.N + rq;
+      if (row_ok) {
+        const float* gr = p.gates + row * 4 * p.K + u0 + uh;
+        const float* sr = p.s + row * p.K + u0 + uh;
+        const float* spr = t > 0 ? p.s + (row - p.N) * p.K + u0 + uh : (p.s0 ? p.s0 + rq * p.K + u0 + uh : nullptr);
+        const float* dhi = p.dh + row * p.K + u0 + uh;
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const float4 vi = __ldcs(reinterpret_cast<const float4*>(gr + q4 * 4));
+          const float4 vc = __ldcs(reinterpret_cast<const float4*>(gr + p.K + q4 * 4));
+          const float4 vf = __ldcs(reinterpret_cast<const float4*>(gr + 2 * p.K + q4 * 4));
+          const float4 vo = __ldcs(reinterpret_cast<const float4*>(gr + 3 * p.K + q4 * 4));
+          const float4 vs = *reinterpret_cast<const float4*>(sr + q4 * 4);
+          const float4 vsp = spr ? *reinterpret_cast<const float4*>(spr + q4 * 4) : make_float4(0, 0, 0, 0);
+          const float4 vdh = __ldcs(reinterpret_cast<const float4*>(dhi + q4 * 4));
+          const float ai[4] = {vi.x, vi.y, vi.z, vi.w}, ac[4] = {vc.x, vc.y, vc.z, vc.w};
+          const float af[4] = {vf.x, vf.y, vf.z, vf.w}, ao[4] = {vo.x, vo.y, vo.z, vo.w};
+          const float as[4] = {vs.x, vs.y, vs.z, vs.w}, asp[4] = {vsp.x, vsp.y, vsp.z, vsp.w};
+          const float adh[4] = {vdh.x, vdh.y, vdh.z, vdh.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int k = q4 * 4 + e;
+            const float ts = tanh_f(as[e]);
+            fdh[k] = adh[e];
+            fA[k] = ao[e] * (1.0f - ts * ts);
+            fB[k] = ts * ao[e] * (1.0f - ao[e]);
+            fCI[k] = ac[e] * ai[e] * (1.0f - ai[e]);
+            fIC[k] = ai[e] * (1.0f - ac[e] * ac[e]);
+            fSF[k] = asp[e] * af[e] * (1.0f - af[e]);
+            ff[k] = af[e];
+          }
+        }
+      }
       if (t < p.T - 1) {
         if (q > 0) mbar_wait_acq_cluster(pfree, (q - 1) & 1);  // peers done reading the last partials
         mbar_wait(tfull, q & 1);
         tc_fence_after();
+        if (threadIdx.x == 0) SEQ_TS(q, 4);
         // partial dh_rec rows (both M-tiles) -> own smem [256][32]
 #pragma unroll
         for (int mt = 0; mt < 2; ++mt) {
@@ -392,8 +507,9 @@ __global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_bwd_kernel(const __grid
           for (int r = 0; r < 4; ++r) mbar_arrive_cluster(ready_peer[r]);  // release: partial rows written
         }
         mbar_wait_acq_cluster(pready, q & 1);  // the four gate partials are in the cluster's smem
+        if (threadIdx.x == 0) SEQ_TS(q, 5);
       }
-      if (rq < p.N) {
+      if (row_ok) {
         float dhr[16];
 #pragma unroll
         for (int q = 0; q < 16; ++q) dhr[q] = 0.0f;
@@ -408,37 +524,20 @@ __global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_bwd_kernel(const __grid
             }
           }
         }
-        const int64_t row = static_cast<int64_t>(t) * p.N + rq;
-        const float* gr = p.gates + row * 4 * p.K + u0 + uh;
-        const float* sr = p.s + row * p.K + u0 + uh;
-        const float* spr = t > 0 ? p.s + (row - p.N) * p.K + u0 + uh : (p.s0 ? p.s0 + rq * p.K + u0 + uh : nullptr);
-        const float* dhi = p.dh + row * p.K + u0 + uh;
         __nv_bfloat16* dp = p.dpre + row * 4 * p.K + u0 + uh;
 #pragma unroll
         for (int q4 = 0; q4 < 4; ++q4) {
-          const float4 vi = *reinterpret_cast<const float4*>(gr + q4 * 4);
-          const float4 vc = *reinterpret_cast<const float4*>(gr + p.K + q4 * 4);
-          const float4 vf = *reinterpret_cast<const float4*>(gr + 2 * p.K + q4 * 4);
-          const float4 vo = *reinterpret_cast<const float4*>(gr + 3 * p.K + q4 * 4);
-          const float4 vs = *reinterpret_cast<const float4*>(sr + q4 * 4);
-          const float4 vsp = spr ? *reinterpret_cast<const float4*>(spr + q4 * 4) : make_float4(0, 0, 0, 0);
-          const float4 vdh = *reinterpret_cast<const float4*>(dhi + q4 * 4);
-          const float ai[4] = {vi.x, vi.y, vi.z, vi.w}, ac[4] = {vc.x, vc.y, vc.z, vc.w};
-          const float af[4] = {vf.x, vf.y, vf.z, vf.w}, ao[4] = {vo.x, vo.y, vo.z, vo.w};
-          const float as[4] = {vs.x, vs.y, vs.z, vs.w}, asp[4] = {vsp.x, vsp.y, vsp.z, vsp.w};
-          const float adh[4] = {vdh.x, vdh.y, vdh.z, vdh.w};
           float o_i[4], o_c[4], o_f[4], o_o[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const int q = q4 * 4 + e;
-            const float dht = adh[e] + dhr[q];
-            const float ts = tanhf(as[e]);
-            const float ds = dht * ao[e] * (1.0f - ts * ts) + dsc[q];
-            o_i[e] = ds * ac[e] * ai[e] * (1.0f - ai[e]);
-            o_c[e] = ds * ai[e] * (1.0f - ac[e] * ac[e]);
-            o_f[e] = ds * asp[e] * af[e] * (1.0f - af[e]);
-            o_o[e] = dht * ts * ao[e] * (1.0f - ao[e]);
-            dsc[q] = ds * af[e];
+            const int k = q4 * 4 + e;
+            const float dht = fdh[k] + dhr[k];
+            const float ds = dht * fA[k] + dsc[k];
+            o_i[e] = ds * fCI[k];
+            o_c[e] = ds * fIC[k];
+            o_f[e] = ds * fSF[k];
+            o_o[e] = dht * fB[k];
+            dsc[k] = ds * ff[k];
           }
           *reinterpret_cast<uint2*>(dp + q4 * 4) = make_uint2(pack_bf16x2(o_i[0], o_i[1]), pack_bf16x2(o_i[2], o_i[3]));
           *reinterpret_cast<uint2*>(dp + p.K + q4 * 4) =
@@ -459,6 +558,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_bwd_kernel(const __grid
       fence_proxy_async_global();
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (threadIdx.x == 0) {
+        if (t < p.T - 1) SEQ_TS(it - 1, 6);
         __threadfence();
         // this CTA wrote rows of its quarter for units u0..u0+31 of all four gates
 #pragma unroll
@@ -481,6 +581,8 @@ __global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_bwd_kernel(const __grid
     tmem_dealloc(tmem, 64);
   }
 }
+
+unsigned long long* g_seq_ts = nullptr;
 
 int smem_fwd(int K) { return kStagesS * kStageBytesS + (K / 64) * 4 * kJf * 128 + 256 + 1024; }
 int smem_bwd(int K) { return kStagesS * kStageBytesS + (K / 64) * kJb * 128 + 256 * kJb * 4 + 256 + 1024; }
@@ -507,6 +609,9 @@ using namespace brk;
 
 extern "C" {
 
+// Diagnostic: subsequent sequence launches record per-step %globaltimer stamps of CTA 0 ([T][8]); NULL disables.
+BRK_API void brk_diag_lstm_timestamps(unsigned long long* ts) { g_seq_ts = ts; }
+
 BRK_API size_t brk_lstm_seq_flags_bytes(int K) { return static_cast<size_t>(4 * (K / 64) + 4) * sizeof(unsigned); }
 
 BRK_API int brk_lstm_seq_fwd(const float* gx, const void* r_cat, const float* s0, void* h_bf, float* h_out,
@@ -519,10 +624,40 @@ BRK_API int brk_lstm_seq_fwd(const float* gx, const void* r_cat, const float* s0
   p.gx = gx; p.s0 = s0; p.h_out = h_out; p.s_out = s_out; p.gates_out = gates_out;
   p.h_bf = static_cast<__nv_bfloat16*>(h_bf);
   p.flags = flags;
+  p.ts = g_seq_ts;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int smem = smem_fwd(K);
+  cudaError_t err = cudaFuncSetAttribute(lstm_seq_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (err != cudaSuccess) return set_cuda_error(err, "lstm seq fwd smem");
+  cudaFuncSetAttribute(lstm_seq_fwd_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(K / kJf);
+  cfg.blockDim = dim3(kThreadsS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  // largest cluster (<= 8, dividing the grid) whose clusters are all co-resident:
+  // the CTAs wait on each other's chunks, so the whole grid must be resident
+  int cs = 8;
+  for (; cs >= 1; cs /= 2) {
+    if ((K / kJf) % cs) continue;
+    attr[0].val.clusterDim.x = cs;
+    int max_clusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&max_clusters, lstm_seq_fwd_kernel, &cfg) == cudaSuccess &&
+        max_clusters * cs >= K / kJf)
+      break;
+    cudaGetLastError();
+  }
+  if (cs < 1) return set_error(BRK_ERR_CONTRACT, "lstm seq fwd: grid cannot be co-resident");
   {
     const uint64_t dims[3] = {(uint64_t)K, (uint64_t)N, (uint64_t)(T + 1)};
     const uint64_t strides[3] = {1, (uint64_t)K, (uint64_t)N * K};
-    const uint32_t box[3] = {64, 128, 1};
+    const uint32_t box[3] = {64, (uint32_t)(256 / cs), 1};
     if ((rc = encode_tmap(&p.map_a, h_bf, true, 3, dims, strides, box))) return rc;
   }
   {
@@ -531,22 +666,8 @@ BRK_API int brk_lstm_seq_fwd(const float* gx, const void* r_cat, const float* s0
     const uint32_t box[2] = {64, 8};
     if ((rc = encode_tmap(&p.map_w, r_cat, true, 2, dims, strides, box))) return rc;
   }
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  cudaError_t err = cudaMemsetAsync(flags, 0, brk_lstm_seq_flags_bytes(K), st);
+  err = cudaMemsetAsync(flags, 0, brk_lstm_seq_flags_bytes(K), st);
   if (err != cudaSuccess) return set_cuda_error(err, "lstm seq flags");
-  const int smem = smem_fwd(K);
-  err = cudaFuncSetAttribute(lstm_seq_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (err != cudaSuccess) return set_cuda_error(err, "lstm seq fwd smem");
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(K / kJf);
-  cfg.blockDim = dim3(kThreadsS);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr;
-  attr.id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (they wait on each other's chunks)
-  attr.val.cooperative = 1;
-  cfg.attrs = &attr;
-  cfg.numAttrs = 1;
   g_launches.fetch_add(1);
   err = cudaLaunchKernelEx(&cfg, lstm_seq_fwd_kernel, p);
   return err == cudaSuccess ? BRK_OK : set_cuda_error(err, "lstm seq fwd launch");
@@ -565,6 +686,7 @@ BRK_API int brk_lstm_seq_bwd(const float* dh, const float* gates, const float* s
   p.dpre = static_cast<__nv_bfloat16*>(dpre);
   p.ds0 = ds0;
   p.flags = flags;
+  p.ts = g_seq_ts;
   {
     const uint64_t dims[3] = {(uint64_t)(4 * K), (uint64_t)N, (uint64_t)T};
     const uint64_t strides[3] = {1, (uint64_t)(4 * K), (uint64_t)N * 4 * K};

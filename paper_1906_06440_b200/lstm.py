@@ -265,13 +265,13 @@ def _seq_cell(params: LstmParams) -> _SeqCell:
 
 def _seq_ok(params: LstmParams, prec: str) -> bool:
     """The persistent sequence kernels (brk_lstm_seq_*) serve bf16 compute with
-    N <= 256, K % 64 == 0, K <= 1024 and C % 8 == 0; other shapes and TF32 use
+    N <= 256, K % 64 == 0, K <= 1024 and C % 64 == 0; other shapes and TF32 use
     the per-step kernels."""
     import os
     if os.environ.get("BRK_LSTM_SEQ", "1") == "0":
         return False
     return (prec == "bf16" and params.n <= 256 and params.k % 64 == 0 and params.k <= 1024
-            and params.c % 8 == 0)
+            and params.c % 64 == 0)
 
 
 def _flags(k):

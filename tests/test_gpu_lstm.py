@@ -118,7 +118,7 @@ def test_causality_and_determinism():
         assert np.array_equal(part.h, full.h[:t])
 
 
-@pytest.mark.parametrize("shape", [(3, 168, 1024, 1024), (6, 200, 128, 256), (2, 40, 32, 64)])
+@pytest.mark.parametrize("shape", [(3, 168, 1024, 1024), (6, 200, 128, 256), (2, 40, 64, 64)])
 def test_sequence_kernels_vs_oracle(shape):
     """The persistent sequence kernels (brk_lstm_seq_fwd/bwd, bf16) at the
     benchmark width (128 CTAs fwd, 32 four-CTA clusters bwd) and odd sizes."""
