@@ -138,6 +138,19 @@ BRK_API int brk_fc_upd(const void* x, const void* dz, float* dw, void* w_sgd, fl
                        void* workspace, size_t ws_bytes, int N, int C, int K, int b_n, int b_c, int b_k,
                        int dtype, void* stream);
 BRK_API size_t brk_fc_upd_workspace(int N, int C, int K);
+/* The whole MLP training step as ONE persistent launch (BASELINE config 2):
+ * L forward layers y[l+1] = relu(W_l y[l] + b_l), the top gradient
+ * dz[L] = dy * (y[L] > 0) (fused in the last forward epilogue), and per layer l
+ * from the top bwd-data dz[l-1] = (W_{l-1}^T dz[l]) * (y[l-1] > 0) and the
+ * weight update dW = dz[l] y[l-1]^T with fused SGD of W and b (lr).  Arrays of
+ * device pointers: y, dz, colsum have L+1 entries (colsum[l]: fp32 [N/32][C]
+ * column-sum partials of dz[l]), w, bias, dw, db have L.  Blocked bf16 layouts
+ * as brk_fc_*, N and C multiples of 256, L <= 4.  counters:
+ * brk_mlp_step_counters_bytes(L) bytes of device scratch (zeroed by the call). */
+BRK_API int brk_mlp_step(int L, int N, int C, const void* const* y, void* const* dz, const void* dy,
+                         void* const* w, float* const* bias, float* const* dw, float* const* db,
+                         float* const* colsum, float lr, unsigned* counters, void* stream);
+BRK_API size_t brk_mlp_step_counters_bytes(int L);
 /* Bias gradient (north star): dz_out = dy * (y > 0) if y != NULL; db[K] = sum over N of dz;
  * if bias_sgd != NULL also bias_sgd -= lr * db (fused SGD).  Deterministic.
  * workspace: brk_fc_bias_grad_workspace(K) bytes, zeroed once before first use. */

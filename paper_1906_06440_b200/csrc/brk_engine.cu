@@ -52,18 +52,23 @@ struct EngineCfg {
   static constexpr int kTileBBytes = kBRows * 128;
   static constexpr int kStageBytes = kTileABytes + kTileBBytes;
   // epilogue staging: one 32-row x 128 B tile per epilogue warp (coalesced stores)
-  static constexpr int kEpiStageBytes = kEpiWarps * 4096;
+  static constexpr int kEpiStageBytes = kEpiWarps * (4096 + 256 + 512);  // staging tile, 32 row offsets, bias
   static constexpr int kAvail = 232448 - 1024 - 256 - kEpiStageBytes;  // 227 KB opt-in max
-  // ring depth: as many stages as fit (<= 8), rounded down to a multiple of 4
-  // or 3 so that 3-4 producer warps share it (one issuing warp sustains only
-  // ~12 B/clk/SM of TMA traffic, profiles/r01_summary.md)
-  static constexpr int kFit = kAvail / kStageBytes > 8 ? 8 : kAvail / kStageBytes;
-  static constexpr int kStages = kFit >= 8 ? 8 : (kFit >= 6 ? 6 : (kFit >= 4 ? 4 : kFit));
+  // ring depth: as many stages as fit (<= 8), rounded to 8, 6 or 4
+  static constexpr int kFit = kAvail / kStageBytes > 7 ? 7 : kAvail / kStageBytes;
+  static constexpr int kStages = kFit >= 6 ? kFit : (kFit >= 4 ? 4 : kFit);
   static constexpr int kTmemCols = 2 * BN;
   static constexpr int kSmem = kStages * kStageBytes + kEpiStageBytes + 1024 + 256;
-  static constexpr int kProducers = kStages % 4 == 0 ? 4 : (kStages % 3 == 0 ? 3 : (kStages % 2 == 0 ? 2 : 1));
+  // 7 producer warps: a TMA-issuing warp keeps about one box in flight (~1 box
+  // per ~930 clk of latency, profiles/r01_tma_sweep.txt), so the per-SM operand
+  // rate scales with the number of issuing warps.  8 epilogue + 1 MMA + 7
+  // producer warps = 4 warpgroups; setmaxnreg moves registers from the
+  // producer/MMA warpgroups (56) to the epilogue warpgroups (192).
+  // one producer per stage (a producer refills only its own stage, so the
+  // mbarrier parity waits cannot alias); warps beyond 8 + 1 + kStages idle
+  static constexpr int kProducers = kStages;
   static constexpr int kMmaWarp = kEpiWarps;
-  static constexpr int kThreads = (kEpiWarps + 1 + kProducers) * 32;
+  static constexpr int kThreads = 16 * 32;  // 4 warpgroups (setmaxnreg is per warpgroup)
   static constexpr int kColsPerWarp = BN >= 64 ? BN / 2 : BN;  // column half per epilogue warp
 };
 
@@ -144,9 +149,17 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+// grouped launches: per-CTA, per-local-tile stamps [blockIdx.x][16 tiles][4]:
+// 0 producer 0 dependencies satisfied, 1 MMA first stage full, 2 MMA last commit, 3 epilogue released,
+// 4 epilogue got the accumulator, 5 stores issued, 6 proxy fence + barrier passed
+#define BRK_TT(tile, slot)                                                                      \
+  do {                                                                                          \
+    if (gs != nullptr && P[0].debug_ts != nullptr && (tile) < 16)                               \
+      P[0].debug_ts[(blockIdx.x * 16 + (tile)) * 8 + (slot)] = gtimer();                         \
+  } while (0)
 #define BRK_TS(slot)                                                              \
   do {                                                                            \
-    if (p.debug_ts != nullptr) p.debug_ts[blockIdx.x * 16 + (slot)] = gtimer();   \
+    if (gs == nullptr && P[0].debug_ts != nullptr) P[0].debug_ts[blockIdx.x * 16 + (slot)] = gtimer();   \
   } while (0)
 
 __device__ __forceinline__ void named_bar_sync(int id, int threads) {
@@ -241,7 +254,25 @@ __device__ __forceinline__ void epilogue_finish(const EngineParams& p, float (&f
 #pragma unroll
         for (int q = 0; q < 4; ++q) { d1[q] = z; d2[q] = z; d3[q] = z; }
       }
-      if (p.colsum_ws != nullptr) {  // column sums see the stored (rounded) values
+      if (p.aux_in != nullptr) {
+        // fused output-gradient mask: aux_out = aux_in * (out > 0); the column
+        // sums (bias gradient of the next pass) then see aux_out
+        const uint4* ai = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.aux_in) + off);
+        uint4* ao = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.aux_out) + off);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 w = ai[q];
+          __nv_bfloat16* h = reinterpret_cast<__nv_bfloat16*>(&w);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float y = __bfloat162float(__float2bfloat16_rn(f[q * 8 + j]));
+            const float a = y > 0.0f ? __bfloat162float(h[j]) : 0.0f;
+            h[j] = __float2bfloat16_rn(a);
+            f[q * 8 + j] = a;
+          }
+          ao[q] = w;
+        }
+      } else if (p.colsum_ws != nullptr) {  // column sums see the stored (rounded) values
 #pragma unroll
         for (int j = 0; j < 32; ++j) f[j] = __bfloat162float(__float2bfloat16_rn(f[j]));
       }
@@ -272,70 +303,259 @@ __device__ __forceinline__ void epilogue_finish(const EngineParams& p, float (&f
   }
 }
 
-// Plain epilogue, part 1: bias (+ReLU) on one 32-column chunk of this lane's
-// row, written into the warp's staging tile (32 rows x 128 B, 16 B slot j of
-// row r at slot j ^ (r % 8): conflict-free for both the row-wise writes here
-// and the segment-wise reads of epilogue_flush).  bf16: chunk = 4 slots
-// (two chunks fill a 128 B row segment); fp32: chunk = 8 slots.
-__device__ __forceinline__ void epilogue_stage(const EngineParams& p, float (&f)[32], float bias_lane, uint8_t* row,
+__device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr)
+               : "memory");
+  return v;
+}
+
+// Staged epilogue, part 1: bias, activation on one 32-column chunk of this
+// lane's row, written into the warp's staging tile (32 rows x 128 B at the
+// shared address `row`; 16 B slot j of row r at slot j ^ (r % 8): conflict-free
+// for the row-wise writes here and the segment-wise reads of epilogue_flush).
+// bf16: chunk = 4 slots (two chunks fill a 128 B row segment); fp32: 8 slots.
+__device__ __forceinline__ void epilogue_stage(const EngineParams& p, float (&f)[32], uint32_t btab, uint32_t row,
                                                int lane, int slot0) {
-  if (p.bias != nullptr) {
+  if (p.bias != nullptr) {  // the chunk's 32 bias values, preloaded into shared memory (broadcast reads)
 #pragma unroll
-    for (int j = 0; j < 32; ++j) f[j] += __shfl_sync(0xffffffffu, bias_lane, j);
+    for (int q = 0; q < 8; ++q) {
+      float4 b;
+      asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+                   : "r"(btab + q * 16) : "memory");
+      f[4 * q] += b.x; f[4 * q + 1] += b.y; f[4 * q + 2] += b.z; f[4 * q + 3] += b.w;
+    }
   }
   if (p.act == kActRelu) {
 #pragma unroll
     for (int j = 0; j < 32; ++j) f[j] = fmaxf(f[j], 0.0f);
+  } else if (p.act == kActSigmoid) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const float e = __expf(-fabsf(f[j]));
+      const float r = __fdividef(1.0f, 1.0f + e);
+      f[j] = f[j] >= 0.0f ? r : e * r;
+    }
   }
   if (p.out_bf16) {
 #pragma unroll
     for (int q = 0; q < 4; ++q)
-      *reinterpret_cast<uint4*>(row + (((slot0 + q) ^ (lane & 7)) << 4)) =
-          make_uint4(pack_bf16x2(f[q * 8 + 0], f[q * 8 + 1]), pack_bf16x2(f[q * 8 + 2], f[q * 8 + 3]),
-                     pack_bf16x2(f[q * 8 + 4], f[q * 8 + 5]), pack_bf16x2(f[q * 8 + 6], f[q * 8 + 7]));
+      sts128(row + (((slot0 + q) ^ (lane & 7)) << 4),
+             make_uint4(pack_bf16x2(f[q * 8 + 0], f[q * 8 + 1]), pack_bf16x2(f[q * 8 + 2], f[q * 8 + 3]),
+                        pack_bf16x2(f[q * 8 + 4], f[q * 8 + 5]), pack_bf16x2(f[q * 8 + 6], f[q * 8 + 7])));
   } else {
 #pragma unroll
     for (int q = 0; q < 8; ++q)
-      *reinterpret_cast<float4*>(row + ((q ^ (lane & 7)) << 4)) =
-          make_float4(f[q * 4], f[q * 4 + 1], f[q * 4 + 2], f[q * 4 + 3]);
+      sts128(row + ((q ^ (lane & 7)) << 4),
+             make_uint4(__float_as_uint(f[q * 4]), __float_as_uint(f[q * 4 + 1]), __float_as_uint(f[q * 4 + 2]),
+                        __float_as_uint(f[q * 4 + 3])));
   }
 }
 
-// Plain epilogue, part 2: write the staged 32 x 128 B tile as coalesced
-// 16 B stores (8 lanes per row segment, 4 rows per instruction) instead of
-// one 16 B store per row per lane (32 lines per instruction).  ro[i] is the
-// element offset of row 4i + lane/8, ok its validity bit; coff the segment's
-// column offset.  Stride-2 scatters also zero the three skipped positions.
-// kLanes = 16 B slots per row segment: 8 (128 B) or 4 (64 B, bf16 BN=64 tiles).
+// Staged epilogue, part 2: write the staged 32 x 128 B tile as coalesced 16 B
+// stores (kLanes lanes per row segment: 8 for 128 B, 4 for 64 B) instead of one
+// 16 B store per row per lane.  roff is this lane's row offset (element), ok
+// the row validity bits, coff the segment's column offset.  kFull adds, per
+// 16 B element group and still coalesced: the ReLU-derivative mask (bf16
+// outputs), the fused output-gradient mask (aux), the SGD update of bf16
+// weights (fp32 outputs) and the 32-row column sums (colsum_ws row
+// warp_row0 / 32, columns col_seg ..).  All global loads of the segment are
+// issued before any is consumed (one latency per flush, not per row).
+// Global operands the full flush reads (ReLU mask / aux gradient for bf16
+// outputs, SGD weights for fp32 outputs) do not depend on the accumulator:
+// they are fetched for the first segments before the epilogue waits for it.
+__device__ __forceinline__ const void* flush_src(const EngineParams& p) {
+  return p.out_bf16 ? (p.mask != nullptr ? p.mask : p.aux_in) : p.sgd_w;
+}
 template <int kLanes>
-__device__ __forceinline__ void epilogue_flush(const EngineParams& p, const uint8_t* stage, const int64_t (&ro)[8],
-                                               uint32_t ok, int64_t coff, int lane) {
+__device__ __forceinline__ void epilogue_prefetch(const EngineParams& p, uint32_t rtab, uint32_t ok, int64_t coff,
+                                                  int lane, uint4 (&pre)[8]) {
+  const void* src = flush_src(p);
+  if (src == nullptr) return;
+  constexpr int kRowsPer = 32 / kLanes;
+  const int s = lane & (kLanes - 1);
+  const int esz = p.out_bf16 ? 2 : 4;
+#pragma unroll
+  for (int i = 0; i < kLanes; ++i) {
+    const int r = kRowsPer * i + lane / kLanes;
+    if (!((ok >> r) & 1u)) continue;
+    int64_t ro;
+    asm volatile("ld.shared.s64 %0, [%1];" : "=l"(ro) : "r"(rtab + r * 8) : "memory");
+    const int64_t e = ro + coff + s * (16 / esz);
+    if (p.out_bf16) pre[i] = __ldcs(reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(src) + e));
+    else {
+      const uint2 w2 = *reinterpret_cast<const uint2*>(static_cast<const __nv_bfloat16*>(src) + e);
+      pre[i] = make_uint4(w2.x, w2.y, 0u, 0u);
+    }
+  }
+}
+
+template <int kLanes, bool kFull>
+__device__ __forceinline__ void epilogue_flush(const EngineParams& p, uint32_t stage, uint32_t rtab, uint32_t ok,
+                                               int64_t coff, int lane, int warp_row0 = 0, int col_seg = 0,
+                                               const uint4* pre = nullptr) {
   __syncwarp();
   constexpr int kRowsPer = 32 / kLanes;
   const int s = lane & (kLanes - 1);
   const int esz = p.out_bf16 ? 2 : 4;
   uint8_t* out = static_cast<uint8_t*>(p.out);
+  int64_t eo[kLanes];
+  uint4 v[kLanes];
+  uint4 ld[kLanes];
+  bool okr[kLanes];
 #pragma unroll
   for (int i = 0; i < kLanes; ++i) {
     const int r = kRowsPer * i + lane / kLanes;
-    const uint4 v = *reinterpret_cast<const uint4*>(stage + r * 128 + ((s ^ (r & 7)) << 4));
-    if ((ok >> r) & 1u) {
-      uint8_t* dst = out + (ro[i] + coff) * esz + s * 16;
-      *reinterpret_cast<uint4*>(dst) = v;
-      if (p.zf_w != 0) {
-        const uint4 z = make_uint4(0u, 0u, 0u, 0u);
-        *reinterpret_cast<uint4*>(dst + p.zf_w * 2) = z;
-        *reinterpret_cast<uint4*>(dst + p.zf_h * 2) = z;
-        *reinterpret_cast<uint4*>(dst + (p.zf_w + p.zf_h) * 2) = z;
+    int64_t ro;
+    asm volatile("ld.shared.s64 %0, [%1];" : "=l"(ro) : "r"(rtab + r * 8) : "memory");
+    eo[i] = ro + coff + s * (16 / esz);
+    v[i] = lds128(stage + r * 128 + ((s ^ (r & 7)) << 4));
+    okr[i] = (ok >> r) & 1u;
+  }
+  if (kFull && pre != nullptr) {
+#pragma unroll
+    for (int i = 0; i < kLanes; ++i) ld[i] = pre[i];
+  } else if (kFull) {
+    const void* src = flush_src(p);
+    if (src != nullptr) {
+#pragma unroll
+      for (int i = 0; i < kLanes; ++i) {
+        if (!okr[i]) continue;
+        if (p.out_bf16) ld[i] = *reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(src) + eo[i]);
+        else {
+          const uint2 w2 = *reinterpret_cast<const uint2*>(static_cast<const __nv_bfloat16*>(src) + eo[i]);
+          ld[i] = make_uint4(w2.x, w2.y, 0u, 0u);
+        }
       }
+    }
+  }
+  float cs[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+  for (int i = 0; i < kLanes; ++i) {
+    if (!okr[i]) continue;
+    uint8_t* dst = out + eo[i] * esz;
+    if (kFull && p.out_bf16) {
+      __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&v[i]);
+      if (p.mask != nullptr) {
+        const __nv_bfloat162* mh = reinterpret_cast<const __nv_bfloat162*>(&ld[i]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 m2 = __bfloat1622float2(mh[j]);
+          float2 v2 = __bfloat1622float2(h[j]);
+          v2.x = m2.x > 0.0f ? v2.x : 0.0f;
+          v2.y = m2.y > 0.0f ? v2.y : 0.0f;
+          h[j] = __floats2bfloat162_rn(v2.x, v2.y);
+        }
+      }
+      *reinterpret_cast<uint4*>(dst) = v[i];
+      if (p.aux_in != nullptr) {  // (mask and aux are not combined: aux only on forward outputs)
+        uint4 a = ld[i];
+        __nv_bfloat162* ah = reinterpret_cast<__nv_bfloat162*>(&a);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 y2 = __bfloat1622float2(h[j]);
+          float2 a2 = __bfloat1622float2(ah[j]);
+          a2.x = y2.x > 0.0f ? a2.x : 0.0f;
+          a2.y = y2.y > 0.0f ? a2.y : 0.0f;
+          ah[j] = __floats2bfloat162_rn(a2.x, a2.y);
+        }
+        *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.aux_out) + eo[i]) = a;
+        v[i] = a;  // column sums of the gradient
+      }
+      if (p.colsum_ws != nullptr) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 c2 = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(&v[i])[j]);
+          cs[2 * j] += c2.x;
+          cs[2 * j + 1] += c2.y;
+        }
+      }
+    } else if (kFull) {  // fp32 output
+      *reinterpret_cast<uint4*>(dst) = v[i];
+      const float4 f4 = *reinterpret_cast<const float4*>(&v[i]);
+      if (p.sgd_w != nullptr) {
+        const __nv_bfloat162* wo = reinterpret_cast<const __nv_bfloat162*>(&ld[i]);
+        const float2 w0 = __bfloat1622float2(wo[0]), w1 = __bfloat1622float2(wo[1]);
+        __nv_bfloat162* wp = reinterpret_cast<__nv_bfloat162*>(static_cast<__nv_bfloat16*>(p.sgd_w) + eo[i]);
+        wp[0] = __floats2bfloat162_rn(w0.x - p.sgd_lr * f4.x, w0.y - p.sgd_lr * f4.y);
+        wp[1] = __floats2bfloat162_rn(w1.x - p.sgd_lr * f4.z, w1.y - p.sgd_lr * f4.w);
+      }
+      if (p.colsum_ws != nullptr) { cs[0] += f4.x; cs[1] += f4.y; cs[2] += f4.z; cs[3] += f4.w; }
+    } else {
+      *reinterpret_cast<uint4*>(dst) = v[i];
+    }
+    if (p.zf_w != 0) {
+      const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+      *reinterpret_cast<uint4*>(dst + p.zf_w * 2) = z;
+      *reinterpret_cast<uint4*>(dst + p.zf_h * 2) = z;
+      *reinterpret_cast<uint4*>(dst + (p.zf_w + p.zf_h) * 2) = z;
+    }
+  }
+  if (kFull && p.colsum_ws != nullptr) {
+#pragma unroll
+    for (int off = kLanes; off < 32; off <<= 1)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) cs[j] += __shfl_xor_sync(0xffffffffu, cs[j], off);
+    const int per = p.out_bf16 ? 8 : 4;  // columns per 16 B group
+    if (lane < kLanes && warp_row0 < p.rows) {
+      float* dst = p.colsum_ws + static_cast<int64_t>(warp_row0 / 32) * p.cols + col_seg + s * per;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j < per) dst[j] = cs[j];
     }
   }
   __syncwarp();
 }
 
-template <int BN, bool kTF32, bool kPair, bool kFullEpi>
-__global__ void __launch_bounds__(EngineCfg<BN, kPair>::kThreads, 1)
-    engine_kernel(const __grid_constant__ EngineParams p) {
+// Work unit u of a launch -> (problem, tile index t, split sp).  Single-problem
+// launches (gs == null) order tiles column-block-major (mb fastest); grouped
+// launches order each problem row-major (nb fastest) so that the tiles of one
+// row block finish together and release the dependent problem's row block early.
+__device__ __forceinline__ void locate(const EngineParams* P, const GroupSched* gs, int u, int splits, int& prob,
+                                       int& mb, int& nb, int& t, int& sp) {
+  if (gs == nullptr) {
+    prob = 0;
+    t = u / splits;
+    sp = u - t * splits;
+    mb = t % P[0].m_tiles;
+    nb = t / P[0].m_tiles;
+    return;
+  }
+  prob = 0;
+  while (prob + 1 < gs->n_probs && u >= gs->tile_begin[prob + 1]) ++prob;
+  t = u - gs->tile_begin[prob];
+  sp = 0;
+  nb = t % P[prob].n_tiles;
+  mb = t / P[prob].n_tiles;
+}
+
+// Grouped launches: block until the tiles this tile consumes are complete.
+// Relaxed polling (no L1 invalidation per probe), one acquire fence on success.
+__device__ __forceinline__ void wait_deps(const GroupSched* gs, const EngineParams* P, int prob, int mb,
+                                          int halves) {
+  for (int d = 0; d < kMaxDeps; ++d) {
+    const int q = gs->dep_prob[prob][d];
+    if (q < 0) continue;
+    const bool whole = gs->dep_mode[prob][d] != 0;
+    const unsigned* c = gs->counters + q * kCounterStride + (whole ? kCounterStride - 1 : mb);
+    const unsigned need = static_cast<unsigned>(halves * (whole ? P[q].m_tiles * P[q].n_tiles : P[q].n_tiles));
+    unsigned v;
+    long long spins = 0;
+    do {
+      asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
+      if (++spins > (1ll << 31)) __trap();  // a dependency that never completes is a bug: fail loudly
+    } while (v < need);
+  }
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  asm volatile("fence.proxy.async.global;" ::: "memory");  // the producer's TMA reads follow
+}
+
+template <int BN, bool kTF32, bool kPair, bool kFullEpi, bool kGroup>
+__device__ __forceinline__ void engine_body(const EngineParams* P, const GroupSched* gs) {
   using Cfg = EngineCfg<BN, kPair>;
   constexpr int kStages = Cfg::kStages;
   constexpr int kMmaWarp = Cfg::kMmaWarp;
@@ -357,14 +577,17 @@ __global__ void __launch_bounds__(EngineCfg<BN, kPair>::kThreads, 1)
   const bool leader = rank == 0;
   const int unit0 = kPair ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
   const int n_units = kPair ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x);
-  const int splits = p.k_splits > 1 ? p.k_splits : 1;
-  const int ks_per = (p.k_steps + splits - 1) / splits;
-  const int num_work = p.m_tiles * p.n_tiles * splits;
+  const EngineParams& p0 = P[0];
+  const int splits = (gs == nullptr && p0.k_splits > 1) ? p0.k_splits : 1;
+  const int num_work = gs == nullptr ? p0.m_tiles * p0.n_tiles * splits : gs->tile_begin[gs->n_probs];
+  const int n_probs = gs == nullptr ? 1 : gs->n_probs;
   if (threadIdx.x == 0) BRK_TS(0);
 
   if (warp == kMmaWarp + 1 && lane == 0) {
-    tma_prefetch_desc(&p.map_a);
-    tma_prefetch_desc(&p.map_b);
+    for (int q = 0; q < n_probs; ++q) {
+      tma_prefetch_desc(&P[q].map_a);
+      tma_prefetch_desc(&P[q].map_b);
+    }
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -386,16 +609,25 @@ __global__ void __launch_bounds__(EngineCfg<BN, kPair>::kThreads, 1)
   if (threadIdx.x == 0) BRK_TS(1);
   pdl_launch_dependents();  // let the next kernel's prologue start early
 
+  if (warp >= kMmaWarp) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;" ::: "memory");
+  else asm volatile("setmaxnreg.inc.sync.aligned.u32 192;" ::: "memory");
+
   if (warp > kMmaWarp) {
     // ------------------------------------------------------------ producers
     const int pid = warp - kMmaWarp - 1;
-    if (elect_one()) {
+    if (pid < kProducers && elect_one()) {
       pdl_wait();  // inputs are produced by the previous kernel
-      const uint32_t bytes = (p.ca.n_loads * p.ca.load_bytes + p.cb.n_loads * p.cb.load_bytes) * (kPair ? 2 : 1);
       int g = 0;  // global k-step counter of this CTA (same sequence as the MMA issuer)
+      int ltile = 0;
       for (int u = unit0; u < num_work; u += n_units) {
-        const int t = u / splits, sp = u - t * splits;
-        const int mb = t % p.m_tiles, nb = t / p.m_tiles;
+        int prob, mb, nb, t, sp;
+        locate(P, gs, u, splits, prob, mb, nb, t, sp);
+        const EngineParams& p = P[prob];
+        const int ks_per = (p.k_steps + splits - 1) / splits;
+        const uint32_t bytes = (p.ca.n_loads * p.ca.load_bytes + p.cb.n_loads * p.cb.load_bytes) * (kPair ? 2 : 1);
+        if (gs != nullptr) wait_deps(gs, P, prob, mb, kPair ? 2 : 1);
+        if (pid == 0) BRK_TT(ltile, 0);
+        ++ltile;
         const int arow = kPair ? mb * 2 + static_cast<int>(rank) : mb;
         const int brow = kPair ? nb * 2 + static_cast<int>(rank) : nb;
         const int s_begin = sp * ks_per;
@@ -427,13 +659,16 @@ __global__ void __launch_bounds__(EngineCfg<BN, kPair>::kThreads, 1)
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer (leader CTA)
     if (leader) {
-      const uint32_t idesc = make_idesc(kTF32 ? kFmtTF32 : kFmtBF16, kPair ? 256 : kEngineBM, BN,
-                                        p.ca.mn_major, p.cb.mn_major);
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
       for (int u = unit0; u < num_work; u += n_units, ++local) {
-        const int sp = u % splits;
+        int prob, mb, nb, t, sp;
+        locate(P, gs, u, splits, prob, mb, nb, t, sp);
+        const EngineParams& p = P[prob];
+        const uint32_t idesc = make_idesc(kTF32 ? kFmtTF32 : kFmtBF16, kPair ? 256 : kEngineBM, BN,
+                                          p.ca.mn_major, p.cb.mn_major);
+        const int ks_per = (p.k_steps + splits - 1) / splits;
         const int s_begin = sp * ks_per;
         const int n_steps = min(p.k_steps, s_begin + ks_per) - s_begin;
         const int acc = local & 1;
@@ -444,6 +679,7 @@ __global__ void __launch_bounds__(EngineCfg<BN, kPair>::kThreads, 1)
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           if (local == 0 && s == 0 && lane == 0) BRK_TS(3);
+          if (s == 0 && lane == 0) BRK_TT(local, 1);
           if (elect_one()) {
             if (p.debug_flags & 1) {
               if constexpr (kPair) {
@@ -477,6 +713,7 @@ __global__ void __launch_bounds__(EngineCfg<BN, kPair>::kThreads, 1)
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
         if (lane == 0) BRK_TS(4);
+        if (lane == 0) BRK_TT(local, 2);
       }
     }
   } else {
@@ -490,19 +727,20 @@ __global__ void __launch_bounds__(EngineCfg<BN, kPair>::kThreads, 1)
     const int halves = kPair ? 2 : 1;
     int local = 0;
     for (int u = unit0; u < num_work; u += n_units, ++local) {
-      const int t = u / splits, sp = u - t * splits;
-      const int mb = t % p.m_tiles, nb = t / p.m_tiles;
+      int prob, mb, nb, t, sp;
+      locate(P, gs, u, splits, prob, mb, nb, t, sp);
+      const EngineParams& p = P[prob];
       const int acc = local & 1;
-      // bias for this warp's columns, one value per lane per 32-column chunk
+      // bias for this warp's columns, one value per lane per 32-column chunk (legacy path)
       float bias_r[kCW / 32];
 #pragma unroll
       for (int c = 0; c < kCW / 32; ++c) {
         const int col = nb * BN + cbeg + c * 32 + lane;
         bias_r[c] = (p.bias != nullptr && col < p.cols) ? __ldg(p.bias + col) : 0.0f;
       }
-      mbar_wait(&tfull[acc], (local >> 1) & 1);
-      tc_fence_after();
-      if (threadIdx.x == 0) BRK_TS(5);
+      const uint32_t stage = smem_u32(smem + kStages * Cfg::kStageBytes + warp * (4096 + 256 + 512));
+      const uint32_t rtab = stage + 4096;  // this warp's 32 row offsets (read by epilogue_flush)
+      const uint32_t btab = rtab + 256;    // this warp's kCW bias values
       const int tile_row0 = kPair ? mb * 256 + static_cast<int>(rank) * 128 : mb * kEngineBM;
       const int row = tile_row0 + row_in_tile;
       const int warp_row0 = tile_row0 + quarter * 32;
@@ -515,23 +753,52 @@ __global__ void __launch_bounds__(EngineCfg<BN, kPair>::kThreads, 1)
                            static_cast<int64_t>(rem1) * p.om.rl +
                            (splits > 1 && p.split_ws == nullptr ? sp * p.split_slice : 0);
       const uint32_t tbase = tmem_base + acc * BN + (static_cast<uint32_t>(quarter * 32) << 16) + cbeg;
+      // Everything the epilogue needs besides the accumulator is set up before waiting for it:
+      // row-offset and bias tables in shared memory, and the flush's global operands.
+      const bool staged = !kFullEpi || kGroup || (p.beta == 0.0f && p.split_ws == nullptr);
+      uint32_t ok_bits = 0;
+      constexpr int kSegLanes = kCW == 32 ? 4 : 8;  // bf16 segments of a BN=64 tile are 64 B
+      uint4 pre[2][8];
+      if (staged && (splits == 1 || p.split_ws == nullptr)) {
+        ok_bits = __ballot_sync(0xffffffffu, row_ok);
+        __syncwarp();  // the previous tile's flushes have read the tables
+        asm volatile("st.shared.s64 [%0], %1;" ::"r"(rtab + lane * 8), "l"(roff) : "memory");
+        if (p.bias != nullptr) {
+#pragma unroll
+          for (int c = 0; c < kCW / 32; ++c)
+            asm volatile("st.shared.f32 [%0], %1;" ::"r"(btab + (c * 32 + lane) * 4), "f"(bias_r[c]) : "memory");
+        }
+        __syncwarp();
+        if constexpr (kFullEpi) {
+          // grouped launches: the prefetched operands (e.g. the ReLU mask) may be produced by
+          // earlier problems of this launch, so the epilogue acquires the tile's dependencies too
+          if (gs != nullptr && flush_src(p) != nullptr) wait_deps(gs, P, prob, mb, kPair ? 2 : 1);
+          const int cfirst = nb * BN + cbeg;
+          const int seg_cols = (p.out_bf16 && kSegLanes == 8) ? 64 : 32;
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int col = cfirst + j * seg_cols;
+            if (col - cfirst >= kCW || col >= p.cols) break;
+            const int cq = col / static_cast<int>(p.om.cb), cr = col - cq * static_cast<int>(p.om.cb);
+            const int64_t coff = static_cast<int64_t>(cq) * p.om.ch + static_cast<int64_t>(cr) * p.om.cl;
+            if (p.out_bf16 && kSegLanes == 4) epilogue_prefetch<4>(p, rtab, ok_bits, coff, lane, pre[j]);
+            else epilogue_prefetch<8>(p, rtab, ok_bits, coff, lane, pre[j]);
+          }
+        }
+      }
+      mbar_wait(&tfull[acc], (local >> 1) & 1);
+      tc_fence_after();
+      if (threadIdx.x == 0) BRK_TS(5);
+      if (threadIdx.x == 0) BRK_TT(local, 4);
       if (splits == 1 || p.split_ws == nullptr) {
         // column offset maintained incrementally (32 columns never straddle an
         // output block: cb % 32 == 0, host guarantees); TMEM loads are software-
         // pipelined one chunk ahead so the ld latency overlaps the epilogue math.
         const int cfirst = nb * BN + cbeg;
         // plain epilogue: staging tile, and the row offsets each lane stores in epilogue_flush
-        uint8_t* stage = smem + kStages * Cfg::kStageBytes + warp * 4096;
-        int64_t ro[8];
-        uint32_t ok_bits = 0;
         int64_t seg_coff = 0;
-        if constexpr (!kFullEpi) {
-#pragma unroll
-          for (int i = 0; i < 8; ++i)
-            ro[i] = __shfl_sync(0xffffffffu, roff,
-                                (kCW == 32 && p.out_bf16) ? 8 * (i & 3) + (lane >> 2) : 4 * i + (lane >> 3));
-          ok_bits = __ballot_sync(0xffffffffu, row_ok);
-        }
+        int seg_col = 0;
+        int seg = 0;  // staged flush index (the first two use prefetched operands)
         int cq = cfirst / static_cast<int>(p.om.cb);
         int cr = cfirst - cq * static_cast<int>(p.om.cb);
         uint32_t v[32];
@@ -553,23 +820,32 @@ __global__ void __launch_bounds__(EngineCfg<BN, kPair>::kThreads, 1)
           cr += 32;
           if (cr == p.om.cb) { cr = 0; ++cq; }
           if (p.out == nullptr) continue;  // diagnostic: mainloop-only timing
-          if constexpr (kFullEpi) {
-            if (threadIdx.x == 0 && c < 2) BRK_TS(8 + 2 * c);
-            epilogue_finish(p, f, row_ok && col0 < p.cols, off, col0, warp_row0, lane, bias_r[c]);
-            if (threadIdx.x == 0 && c < 2) BRK_TS(9 + 2 * c);
+          if (kFullEpi && !kGroup && !staged) {
+            if constexpr (kFullEpi && !kGroup) {
+              if (threadIdx.x == 0 && c < 2) BRK_TS(8 + 2 * c);
+              epilogue_finish(p, f, row_ok && col0 < p.cols, off, col0, warp_row0, lane, bias_r[c]);
+              if (threadIdx.x == 0 && c < 2) BRK_TS(9 + 2 * c);
+            }
           } else {
             const int64_t coff = off - roff;
+            if (threadIdx.x == 0 && c < 2) BRK_TS(8 + 2 * c);
             if (kCW == 32 && p.out_bf16) {  // 64 B row segments
-              epilogue_stage(p, f, bias_r[c], stage + lane * 128, lane, 0);
-              if (col0 < p.cols) epilogue_flush<4>(p, stage, ro, ok_bits, coff, lane);
+              epilogue_stage(p, f, btab + c * 128, stage + lane * 128, lane, 0);
+              if (col0 < p.cols) epilogue_flush<4, kFullEpi>(p, stage, rtab, ok_bits, coff, lane, warp_row0, col0,
+                                                             seg < 2 ? pre[seg] : nullptr);
               else __syncwarp();
+              ++seg;
             } else {
               const bool second = p.out_bf16 && (c & 1);
-              if (!second) seg_coff = coff;
-              epilogue_stage(p, f, bias_r[c], stage + lane * 128, lane, second ? 4 : 0);
+              if (!second) { seg_coff = coff; seg_col = col0; }
+              epilogue_stage(p, f, btab + c * 128, stage + lane * 128, lane, second ? 4 : 0);
               if (!p.out_bf16 || second) {
-                if (col0 < p.cols) epilogue_flush<8>(p, stage, ro, ok_bits, seg_coff, lane);
+                if (threadIdx.x == 0 && c < 2) BRK_TS(9 + 2 * c);
+                if (col0 < p.cols)
+                  epilogue_flush<8, kFullEpi>(p, stage, rtab, ok_bits, seg_coff, lane, warp_row0, seg_col,
+                                              seg < 2 ? pre[seg] : nullptr);
                 else __syncwarp();
+                ++seg;
               }
             }
           }
@@ -583,7 +859,7 @@ __global__ void __launch_bounds__(EngineCfg<BN, kPair>::kThreads, 1)
           else mbar_arrive_relaxed(&tempty[acc]);
         }
         if (threadIdx.x == 0) BRK_TS(13);
-      } else if constexpr (kFullEpi) {
+      } else if constexpr (kFullEpi && !kGroup) {
         // split-K: park the partial accumulator, last chunk reduces in chunk order
         float* ws_tile = p.split_ws + (static_cast<int64_t>(t) * halves + rank) * splits * (kEngineBM * BN);
         float* mine = ws_tile + static_cast<int64_t>(sp) * (kEngineBM * BN) + row_in_tile * BN + cbeg;
@@ -643,6 +919,7 @@ __global__ void __launch_bounds__(EngineCfg<BN, kPair>::kThreads, 1)
       }
       // bias gradient from column-sum partials of a previous pass (+ fused bias SGD)
       if (kFullEpi && p.db_partials != nullptr && mb == 0 && rank == 0 && sp == 0) {
+        if (gs != nullptr) wait_deps(gs, P, prob, mb, kPair ? 2 : 1);  // partials come from an earlier problem
         for (int c = threadIdx.x; c < BN; c += kEpiThreads) {
           const int col = nb * BN + c;
           if (col >= p.cols) continue;
@@ -650,6 +927,19 @@ __global__ void __launch_bounds__(EngineCfg<BN, kPair>::kThreads, 1)
           for (int q = 0; q < p.db_parts; ++q) s += p.db_partials[static_cast<int64_t>(q) * p.cols + col];
           p.db_out[col] = s;
           if (p.bias_sgd != nullptr) p.bias_sgd[col] -= p.bias_lr * s;
+        }
+      }
+      if (gs != nullptr) {
+        // release this CTA's half of the tile to dependent problems (their TMA reads it)
+        if (threadIdx.x == 0) BRK_TT(local, 5);
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        named_bar_sync(1, kEpiThreads);
+        if (threadIdx.x == 0) BRK_TT(local, 6);
+        if (threadIdx.x == 0) {
+          __threadfence();
+          atomicAdd(gs->counters + prob * kCounterStride + mb, 1u);
+          atomicAdd(gs->counters + prob * kCounterStride + kCounterStride - 1, 1u);
+          BRK_TT(local, 3);
         }
       }
       if (threadIdx.x == 0) BRK_TS(6);
@@ -663,6 +953,20 @@ __global__ void __launch_bounds__(EngineCfg<BN, kPair>::kThreads, 1)
     else tmem_dealloc(tmem_base, Cfg::kTmemCols);
   }
   if (threadIdx.x == 0) BRK_TS(7);
+}
+
+template <int BN, bool kTF32, bool kPair, bool kFullEpi>
+__global__ void __launch_bounds__(EngineCfg<BN, kPair>::kThreads, 1)
+    engine_kernel(const __grid_constant__ EngineParams p) {
+  engine_body<BN, kTF32, kPair, kFullEpi, false>(&p, nullptr);
+}
+
+// Several dependent problems in one persistent launch (e.g. a whole MLP step):
+// tiles of all problems in one global order, tile-level dependency counters.
+template <int BN, bool kPair>
+__global__ void __launch_bounds__(EngineCfg<BN, kPair>::kThreads, 1)
+    engine_group_kernel(const __grid_constant__ EngineGroup G) {
+  engine_body<BN, false, kPair, true, true>(G.probs, &G.sched);
 }
 
 template <int BN, bool kTF32, bool kPair, bool kFullEpi>
@@ -753,8 +1057,67 @@ int launch_engine(const EngineParams& p, int bn, int tf32, int pair, int max_uni
   return set_error(BRK_ERR_CONTRACT, "engine: BN must be 128 or 256 (pair) / 64, 128, 256 (single)");
 }
 
+template <int BN, bool kPair>
+int launch_group_t(const EngineGroup& G, int grid, cudaStream_t stream) {
+  using Cfg = EngineCfg<BN, kPair>;
+  auto kern = engine_group_kernel<BN, kPair>;
+  static int attr_set = 0;
+  cudaError_t err;
+  if (!attr_set) {
+    err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
+    if (err != cudaSuccess) return set_cuda_error(err, "engine group smem attribute");
+    attr_set = 1;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(Cfg::kThreads);
+  cfg.dynamicSmemBytes = Cfg::kSmem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attrs[2];
+  int na = 0;
+  if (kPair) {
+    attrs[na].id = cudaLaunchAttributeClusterDimension;
+    attrs[na].val.clusterDim.x = 2;
+    attrs[na].val.clusterDim.y = 1;
+    attrs[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  attrs[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[na].val.programmaticStreamSerializationAllowed = 1;
+  ++na;
+  cfg.attrs = attrs;
+  cfg.numAttrs = na;
+  err = cudaLaunchKernelEx(&cfg, kern, G);
+  if (err != cudaSuccess) return set_cuda_error(err, "engine group launch");
+  return BRK_OK;
+}
+
 size_t engine_split_ws_bytes(int tiles, int splits, int bn, int pair) {
   return static_cast<size_t>(tiles) * (pair ? 2 : 1) * splits * kEngineBM * bn * sizeof(float);
+}
+
+// Persistent grouped launch: one CTA (pair) per SM (pair of SMs), all co-resident,
+// so tiles may wait on tiles of earlier problems (dependencies point backwards
+// in the global tile order, which every CTA walks in increasing order).
+int launch_engine_group(const EngineGroup& G, int bn, int pair, cudaStream_t stream) {
+  const GroupSched& gs = G.sched;
+  if (gs.n_probs < 1 || gs.n_probs > kMaxProbs || gs.counters == nullptr)
+    return set_error(BRK_ERR_CONTRACT, "engine group: 1..12 problems and a counter buffer");
+  for (int q = 0; q < gs.n_probs; ++q) {
+    if (G.probs[q].k_splits > 1) return set_error(BRK_ERR_CONTRACT, "engine group: no split-K");
+    if (G.probs[q].m_tiles > kCounterStride - 1) return set_error(BRK_ERR_CONTRACT, "engine group: > 64 row blocks");
+    for (int d = 0; d < kMaxDeps; ++d)
+      if (gs.dep_prob[q][d] >= q) return set_error(BRK_ERR_CONTRACT, "engine group: dependencies must point back");
+  }
+  const int work = gs.tile_begin[gs.n_probs];
+  if (work <= 0) return BRK_OK;
+  const int sms = engine_sm_count();
+  const int units = pair ? sms / 2 : sms;
+  const int grid = pair ? units * 2 : units;
+  if (bn == 128 && pair) return launch_group_t<128, true>(G, grid, stream);
+  if (bn == 256 && pair) return launch_group_t<256, true>(G, grid, stream);
+  if (bn == 128 && !pair) return launch_group_t<128, false>(G, grid, stream);
+  return set_error(BRK_ERR_CONTRACT, "engine group: BN 128/256 pair or 128 single");
 }
 
 }  // namespace brk

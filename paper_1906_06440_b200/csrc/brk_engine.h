@@ -105,11 +105,37 @@ struct EngineParams {
   // stride-2 1x1 backward-data scatter: besides out[off], zero
   // out[off + zf_w], out[off + zf_h], out[off + zf_w + zf_h] (bf16 output)
   int64_t zf_w, zf_h;
+  // aux gradient output (fused top-layer ReLU mask): aux_out = aux_in * (out > 0),
+  // bf16 in the output layout; column sums (colsum_ws) then see aux_out
+  const void* aux_in;
+  void* aux_out;
   int32_t debug_flags;  // bit0: skip MMA, bit1: skip TMA, bit2: no k rotation (diagnostics)
   // diagnostics: per-CTA %globaltimer stamps [blockIdx.x][8]:
   // 0 entry, 1 setup done, 2 first TMA issued, 3 first full-barrier passed (MMA),
   // 4 last MMA committed, 5 epilogue got accumulator, 6 epilogue done, 7 exit
   unsigned long long* debug_ts;
+};
+
+
+constexpr int kMaxProbs = 12;
+constexpr int kMaxDeps = 3;
+constexpr int kCounterStride = 65;  // per problem: 64 row-block counters + 1 whole-problem counter
+
+// Tile schedule of a grouped launch: problem q owns work units
+// [tile_begin[q], tile_begin[q+1]); a tile of q waits until, for every
+// dependency d, counters[dep_prob][mb] (dep_mode 0: the same 256-row block)
+// or counters[dep_prob][64] (dep_mode 1: the whole problem) shows all tiles done.
+struct GroupSched {
+  int32_t n_probs;
+  int32_t tile_begin[kMaxProbs + 1];
+  int32_t dep_prob[kMaxProbs][kMaxDeps];  // -1: none
+  int32_t dep_mode[kMaxProbs][kMaxDeps];
+  unsigned* counters;                     // [n_probs][kCounterStride], zeroed before the launch
+};
+
+struct EngineGroup {
+  EngineParams probs[kMaxProbs];
+  GroupSched sched;
 };
 
 }  // namespace brk

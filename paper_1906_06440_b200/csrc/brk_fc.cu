@@ -44,7 +44,17 @@ struct Plan {
 // efficiency in SS mode (measured): 1-CTA N=128 ~1/2, N=256 ~2/3, CTA pair
 // N=128 ~2/3 (L2-fed), N=256 ~1.  Split-K only when tiles cannot fill the
 // machine; each chunk keeps >= 4 k-steps.
+// Grouped (whole-step) launches build every problem with one tile shape and
+// collect the parameter blocks instead of launching them.
+thread_local const Plan* g_force_plan = nullptr;
+thread_local EngineParams* g_capture = nullptr;
+
 Plan choose_plan(int rows, int cols, int k_steps, bool allow_split) {
+  if (g_force_plan != nullptr) {
+    Plan f = *g_force_plan;
+    f.tiles = (rows / (f.pair ? 256 : 128)) * (cols / f.bn);
+    return f;
+  }
   Plan forced{-1, 0, 0, 0};
   if (const char* env = std::getenv("BRK_TILE")) {  // "pair,bn" e.g. "1,256"
     int a = 0, b = 0;
@@ -145,6 +155,15 @@ int debug_flags() {
 }
 
 unsigned long long* g_debug_ts = nullptr;  // set by brk_diag_set_timestamps
+
+int finish(const EngineParams& p, const Plan& pl, void* stream) {
+  if (g_capture != nullptr) {
+    *g_capture = p;
+    return BRK_OK;
+  }
+  g_launches.fetch_add(1);
+  return launch_engine(p, pl.bn, 0, pl.pair, 0, static_cast<cudaStream_t>(stream));
+}
 
 // ---------------------------------------------------------------------------
 // dZ = dY * (Y > 0) (optional) and db[k] = sum_n dZ[n][k]  — deterministic:
@@ -247,8 +266,7 @@ BRK_API int brk_fc_fwd(const void* x, const void* w, const float* bias, void* y,
   p.act = act;
   p.debug_flags = debug_flags();
   p.debug_ts = g_debug_ts;
-  g_launches.fetch_add(1);
-  return launch_engine(p, pl.bn, 0, pl.pair, 0, static_cast<cudaStream_t>(stream));
+  return finish(p, pl, stream);
 }
 
 BRK_API int brk_fc_bwd_data(const void* dz, const void* w, const void* mask, void* dx, float* colsum_ws,
@@ -278,8 +296,7 @@ BRK_API int brk_fc_bwd_data(const void* dz, const void* w, const void* mask, voi
   p.mask = mask;
   p.debug_flags = debug_flags();
   p.debug_ts = g_debug_ts;
-  g_launches.fetch_add(1);
-  return launch_engine(p, pl.bn, 0, pl.pair, 0, static_cast<cudaStream_t>(stream));
+  return finish(p, pl, stream);
 }
 
 // Split-K workspace of brk_fc_upd: [counters: 4 KiB][fp32 partial tiles].
@@ -338,8 +355,7 @@ BRK_API int brk_fc_upd(const void* x, const void* dz, float* dw, void* w_sgd, fl
   p.sgd_lr = lr;
   p.debug_flags = debug_flags();
   p.debug_ts = g_debug_ts;
-  g_launches.fetch_add(1);
-  return launch_engine(p, pl.bn, 0, pl.pair, 0, static_cast<cudaStream_t>(stream));
+  return finish(p, pl, stream);
 }
 
 // dz_out = dy * (y > 0) when y != NULL (dz_out may alias dy), db = column sums,
@@ -375,6 +391,90 @@ BRK_API void brk_diag_set_timestamps(unsigned long long* ts) { g_debug_ts = ts; 
 
 BRK_API size_t brk_fc_bias_grad_workspace(int K) {
   return static_cast<size_t>(kSplit) * K * sizeof(float) + static_cast<size_t>(K / kB + 1) * sizeof(unsigned);
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// The whole MLP training step (BASELINE config 2) as ONE persistent grouped
+// launch of the engine: 3L dependent problems (L forward, then per layer from
+// the top bwd-data and weight update), tile-level dependency counters instead
+// of kernel boundaries, so the tail of one GEMM overlaps the head of the next.
+// ---------------------------------------------------------------------------
+namespace brk {
+int launch_engine_group(const EngineGroup& G, int bn, int pair, cudaStream_t stream);
+}
+
+extern "C" {
+
+BRK_API size_t brk_mlp_step_counters_bytes(int L) {
+  return static_cast<size_t>(3 * L) * kCounterStride * sizeof(unsigned);
+}
+
+BRK_API int brk_mlp_step(int L, int N, int C, const void* const* y, void* const* dz, const void* dy,
+                         void* const* w, float* const* bias, float* const* dw, float* const* db,
+                         float* const* colsum, float lr, unsigned* counters, void* stream) {
+  if (L < 1 || 3 * L > kMaxProbs) return set_error(BRK_ERR_CONTRACT, "mlp_step: 1 <= layers <= 4");
+  int rc = check_fc(N, C, C, kB, kB, kB, BRK_BF16);
+  if (rc) return rc;
+  if (N % 256 || C % 256 || N / 256 > kCounterStride - 1)
+    return set_error(BRK_ERR_CONTRACT, "mlp_step: N, C multiples of 256, N <= 16384");
+  static EngineGroup G;  // large: keep off the stack (host-side staging of the kernel parameter block)
+  std::memset(&G, 0, sizeof(G));
+  GroupSched& gs = G.sched;
+  const Plan force{1, 128, 1, 0};
+  g_force_plan = &force;
+  int q = 0;
+  auto capture = [&](auto&& build) -> int {
+    g_capture = &G.probs[q];
+    const int r = build();
+    g_capture = nullptr;
+    for (int d = 0; d < kMaxDeps; ++d) gs.dep_prob[q][d] = -1;
+    return r;
+  };
+  int fwd_of[8], bwd_of[8], upd_of[8];
+  for (int l = 0; l < L && !rc; ++l) {  // forward: y[l+1] = relu(W_l y[l] + b_l)
+    rc = capture([&] {
+      return brk_fc_fwd(y[l], w[l], bias[l], const_cast<void*>(y[l + 1]), N, C, C, kB, kB, kB, kActRelu, BRK_BF16,
+                        stream);
+    });
+    if (l > 0) { gs.dep_prob[q][0] = fwd_of[l - 1]; gs.dep_mode[q][0] = 0; }
+    if (l == L - 1) {  // top layer also emits dz_L = dy * (y_L > 0) and its column sums
+      G.probs[q].aux_in = dy;
+      G.probs[q].aux_out = dz[L];
+      G.probs[q].colsum_ws = colsum[L];
+    }
+    fwd_of[l] = q++;
+  }
+  for (int l = L; l >= 1 && !rc; --l) {  // layer l (weights w[l-1]): bwd-data, then the weight update
+    const int dz_src = l == L ? fwd_of[L - 1] : bwd_of[l + 1];
+    rc = capture([&] {
+      return brk_fc_bwd_data(dz[l], w[l - 1], l > 1 ? y[l - 1] : nullptr, dz[l - 1], l > 1 ? colsum[l - 1] : nullptr,
+                             N, C, C, kB, kB, kB, BRK_BF16, stream);
+    });
+    gs.dep_prob[q][0] = dz_src; gs.dep_mode[q][0] = 0;  // the same rows of dz_l
+    bwd_of[l] = q++;
+    if (rc) break;
+    rc = capture([&] {
+      return brk_fc_upd(y[l - 1], dz[l], dw[l - 1], w[l - 1], lr, colsum[l], N / 32, db[l - 1], bias[l - 1], lr,
+                        nullptr, 0, N, C, C, kB, kB, kB, BRK_BF16, stream);
+    });
+    gs.dep_prob[q][0] = dz_src; gs.dep_mode[q][0] = 1;     // all of dz_l (reduction over N)
+    gs.dep_prob[q][1] = bwd_of[l]; gs.dep_mode[q][1] = 1;  // W_{l-1} read by bwd-data before the SGD rewrites it
+    upd_of[l] = q++;
+  }
+  g_force_plan = nullptr;
+  (void)upd_of;
+  if (rc) return rc;
+  gs.n_probs = q;
+  gs.tile_begin[0] = 0;
+  for (int i = 0; i < q; ++i) gs.tile_begin[i + 1] = gs.tile_begin[i] + G.probs[i].m_tiles * G.probs[i].n_tiles;
+  gs.counters = counters;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t err = cudaMemsetAsync(counters, 0, brk_mlp_step_counters_bytes(L), st);
+  if (err != cudaSuccess) return set_cuda_error(err, "mlp_step counters");
+  g_launches.fetch_add(1);
+  return launch_engine_group(G, 128, 1, st);
 }
 
 }  // extern "C"

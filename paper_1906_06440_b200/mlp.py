@@ -75,6 +75,17 @@ class MLP:
         self.upd_ws = [torch.zeros(upd_bytes, dtype=torch.uint8, device=device) for _ in range(layers)]
         self.graph = None
         self.launches_per_step = 0
+        # whole-step persistent launch (brk_mlp_step): device pointer tables + dependency counters
+        import ctypes
+        import os
+
+        self.fused = (os.environ.get("BRK_MLP_FUSED", "1") != "0" and layers <= 4
+                      and width % 256 == 0 and batch % 256 == 0)
+        arr = lambda ts: (ctypes.c_void_p * len(ts))(*[t.data_ptr() for t in ts])  # noqa: E731
+        self._tables = (arr(self.y), arr(self.dz), arr(self.w), arr(self.bias), arr(self.dw), arr(self.db),
+                        arr(self.colsum))
+        self.counters = torch.zeros(max(int(lib.brk_mlp_step_counters_bytes(layers)), 16) // 4, dtype=torch.int32,
+                                    device=device)
 
     # ------------------------------------------------------------------ params
     def params(self, l: int) -> FcParams:
@@ -136,11 +147,21 @@ class MLP:
                 reducer.submit([self.dw[l - 1], self.db[l - 1]])
         return launches
 
+    def fused_step(self, stream: int) -> int:
+        """The whole step as ONE persistent engine launch (brk_mlp_step): 3L
+        dependent GEMM problems with tile-level dependency counters."""
+        y, dz, w, b, dw, db, cs = self._tables
+        self._check(self.lib.brk_mlp_step(self.L, self.N, self.C, y, dz, self.dy.data_ptr(), w, b, dw, db, cs,
+                                          self.lr, self.counters.data_ptr(), stream))
+        return 1
+
     def step(self, stream: int | None = None) -> int:
         """One fwd/bwd/upd step on the current buffers (single GPU: SGD fused)."""
         torch = self.torch
         s = torch.cuda.current_stream().cuda_stream if stream is None else stream
-        if self.pg is None:
+        if self.pg is None and self.fused:
+            n = self.fused_step(s)
+        elif self.pg is None:
             n = self.forward(s) + self.backward_update(s, apply_sgd=True)
         else:
             n = self.forward(s) + self.backward_update(s, apply_sgd=False, reducer=self._reducer())

@@ -31,7 +31,7 @@ def w_dense(wb):  # [Kb][Cb][64c][64k] -> (K, C)
     return wb.permute(0, 3, 1, 2).reshape(kb * B, cb * B)
 
 
-@pytest.mark.parametrize("layers,width,batch", [(2, 256, 256), (4, 512, 384)])
+@pytest.mark.parametrize("layers,width,batch", [(2, 256, 256), (4, 512, 384), (4, 1024, 2048), (3, 512, 512)])
 def test_mlp_step_matches_oracle(layers, width, batch):
     lr = 0.05
     mlp = MLP(layers=layers, width=width, batch=batch, lr=lr, seed=1)
@@ -96,3 +96,22 @@ def test_mlp_step_deterministic():
         outs.append([t.clone() for t in m.dw + m.db])
     for a, b in zip(*outs):
         assert torch.equal(a, b)
+
+
+def test_fused_step_matches_per_pass_launches(monkeypatch):
+    """brk_mlp_step (one persistent grouped launch) vs the 13 per-pass launches."""
+    outs = []
+    for fused in ("1", "0"):
+        monkeypatch.setenv("BRK_MLP_FUSED", fused)
+        mlp = MLP(layers=4, width=512, batch=1024, lr=0.05, seed=3)
+        assert mlp.fused == (fused == "1")
+        g = torch.Generator(device="cpu").manual_seed(4)
+        x = (torch.rand(1024, 512, generator=g) * 2 - 1).bfloat16()
+        dy = (torch.rand(1024, 512, generator=g) * 2 - 1).bfloat16()
+        mlp.load_input(blk(x).cuda(), blk(dy).cuda())
+        for _ in range(2):
+            mlp.step()
+        torch.cuda.synchronize()
+        outs.append([t.float().cpu() for t in mlp.w + mlp.dw + mlp.db + mlp.y[1:]])
+    for a, b in zip(*outs):
+        assert (a - b).abs().max().item() <= 2e-2 * max(b.abs().max().item(), 1e-6)

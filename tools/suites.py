@@ -78,7 +78,7 @@ class _Timer:
         return statistics.fmean(ts), min(ts)
 
 
-def resnet_suite(n=256, iters=10, layers=None, passes=("fwd", "bwd", "upd")):
+def resnet_suite(n=256, iters=10, layers=None, passes=("fwd", "bwd", "upd"), verbose=False):
     """Per-layer device time of the conv passes at minibatch n (bf16 storage, 64-channel blocks)."""
     import torch
 
@@ -150,7 +150,8 @@ def resnet_suite(n=256, iters=10, layers=None, passes=("fwd", "bwd", "upd")):
             row["plan"] = {pn: list(_plan(lib, i, geom)) for i, pn in enumerate(("fwd", "bwd", "upd"))}
         row["wall_s"] = round(time.time() - t_layer, 2)
         rows.append(row)
-        print(json.dumps(row), flush=True)
+        if verbose:
+            print(json.dumps(row), flush=True)
         del x, wt, dout
         torch.cuda.empty_cache()
     summary = {}
@@ -210,7 +211,7 @@ if __name__ == "__main__":
     if what == "conv":
         n = int(sys.argv[2]) if len(sys.argv) > 2 else 256
         layers = [int(v) for v in sys.argv[3].split(",")] if len(sys.argv) > 3 else None
-        res = resnet_suite(n=n, layers=layers)
+        res = resnet_suite(n=n, layers=layers, verbose=True)
         for row in res["layers"]:
             cells = []
             for p in ("fwd", "bwd", "upd"):
