@@ -52,11 +52,11 @@ struct EngineCfg {
   static constexpr int kTileBBytes = kBRows * 128;
   static constexpr int kStageBytes = kTileABytes + kTileBBytes;
   // epilogue staging: one 32-row x 128 B tile per epilogue warp (coalesced stores)
-  static constexpr int kEpiStageBytes = kEpiWarps * (4096 + 256 + 512);  // staging tile, 32 row offsets, bias
+  static constexpr int kEpiStageBytes = kEpiWarps * 4096;  // one staging tile per epilogue warp
   static constexpr int kAvail = 232448 - 1024 - 256 - kEpiStageBytes;  // 227 KB opt-in max
-  // ring depth: as many stages as fit (<= 8), rounded to 8, 6 or 4
+  // ring depth: as many stages as fit (<= 7), one producer warp each
   static constexpr int kFit = kAvail / kStageBytes > 7 ? 7 : kAvail / kStageBytes;
-  static constexpr int kStages = kFit >= 6 ? kFit : (kFit >= 4 ? 4 : kFit);
+  static constexpr int kStages = kFit;
   static constexpr int kTmemCols = 2 * BN;
   static constexpr int kSmem = kStages * kStageBytes + kEpiStageBytes + 1024 + 256;
   // 7 producer warps: a TMA-issuing warp keeps about one box in flight (~1 box
@@ -303,6 +303,26 @@ __device__ __forceinline__ void epilogue_finish(const EngineParams& p, float (&f
   }
 }
 
+// The epilogue's view of a problem, loaded into registers once per tile: in
+// grouped launches every EngineParams field access is an indexed constant-bank
+// load, which serialises the epilogue if repeated per element group.
+struct EpiView {
+  void* out;
+  const float* bias;
+  const void* mask;
+  const void* aux_in;
+  void* aux_out;
+  float* colsum_ws;
+  void* sgd_w;
+  int64_t zf_w, zf_h;
+  float sgd_lr;
+  int out_bf16, act, rows, cols;
+  __device__ __forceinline__ explicit EpiView(const EngineParams& p)
+      : out(p.out), bias(p.bias), mask(p.mask), aux_in(p.aux_in), aux_out(p.aux_out), colsum_ws(p.colsum_ws),
+        sgd_w(p.sgd_w), zf_w(p.zf_w), zf_h(p.zf_h), sgd_lr(p.sgd_lr), out_bf16(p.out_bf16), act(p.act),
+        rows(p.rows), cols(p.cols) {}
+};
+
 __device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
                : "memory");
@@ -319,14 +339,13 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
 // shared address `row`; 16 B slot j of row r at slot j ^ (r % 8): conflict-free
 // for the row-wise writes here and the segment-wise reads of epilogue_flush).
 // bf16: chunk = 4 slots (two chunks fill a 128 B row segment); fp32: 8 slots.
-__device__ __forceinline__ void epilogue_stage(const EngineParams& p, float (&f)[32], uint32_t btab, uint32_t row,
+__device__ __forceinline__ void epilogue_stage(const EpiView& p, float (&f)[32], int col0, uint32_t row,
                                                int lane, int slot0) {
-  if (p.bias != nullptr) {  // the chunk's 32 bias values, preloaded into shared memory (broadcast reads)
+  if (p.bias != nullptr) {  // the chunk's 32 bias values: uniform-address loads (L1 prefetched per tile)
+    const float4* b4 = reinterpret_cast<const float4*>(p.bias + col0);
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      float4 b;
-      asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
-                   : "r"(btab + q * 16) : "memory");
+      const float4 b = __ldg(b4 + q);
       f[4 * q] += b.x; f[4 * q + 1] += b.y; f[4 * q + 2] += b.z; f[4 * q + 3] += b.w;
     }
   }
@@ -368,11 +387,11 @@ __device__ __forceinline__ void epilogue_stage(const EngineParams& p, float (&f)
 // Global operands the full flush reads (ReLU mask / aux gradient for bf16
 // outputs, SGD weights for fp32 outputs) do not depend on the accumulator:
 // they are fetched for the first segments before the epilogue waits for it.
-__device__ __forceinline__ const void* flush_src(const EngineParams& p) {
+__device__ __forceinline__ const void* flush_src(const EpiView& p) {
   return p.out_bf16 ? (p.mask != nullptr ? p.mask : p.aux_in) : p.sgd_w;
 }
 template <int kLanes>
-__device__ __forceinline__ void epilogue_prefetch(const EngineParams& p, uint32_t rtab, uint32_t ok, int64_t coff,
+__device__ __forceinline__ void epilogue_prefetch(const EpiView& p, int64_t roff, uint32_t ok, int64_t coff,
                                                   int lane, uint4 (&pre)[8]) {
   const void* src = flush_src(p);
   if (src == nullptr) return;
@@ -382,9 +401,8 @@ __device__ __forceinline__ void epilogue_prefetch(const EngineParams& p, uint32_
 #pragma unroll
   for (int i = 0; i < kLanes; ++i) {
     const int r = kRowsPer * i + lane / kLanes;
+    const int64_t ro = __shfl_sync(0xffffffffu, roff, r);
     if (!((ok >> r) & 1u)) continue;
-    int64_t ro;
-    asm volatile("ld.shared.s64 %0, [%1];" : "=l"(ro) : "r"(rtab + r * 8) : "memory");
     const int64_t e = ro + coff + s * (16 / esz);
     if (p.out_bf16) pre[i] = __ldcs(reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(src) + e));
     else {
@@ -395,7 +413,7 @@ __device__ __forceinline__ void epilogue_prefetch(const EngineParams& p, uint32_
 }
 
 template <int kLanes, bool kFull>
-__device__ __forceinline__ void epilogue_flush(const EngineParams& p, uint32_t stage, uint32_t rtab, uint32_t ok,
+__device__ __forceinline__ void epilogue_flush(const EpiView& p, uint32_t stage, int64_t roff, uint32_t ok,
                                                int64_t coff, int lane, int warp_row0 = 0, int col_seg = 0,
                                                const uint4* pre = nullptr) {
   __syncwarp();
@@ -410,9 +428,7 @@ __device__ __forceinline__ void epilogue_flush(const EngineParams& p, uint32_t s
 #pragma unroll
   for (int i = 0; i < kLanes; ++i) {
     const int r = kRowsPer * i + lane / kLanes;
-    int64_t ro;
-    asm volatile("ld.shared.s64 %0, [%1];" : "=l"(ro) : "r"(rtab + r * 8) : "memory");
-    eo[i] = ro + coff + s * (16 / esz);
+    eo[i] = __shfl_sync(0xffffffffu, roff, r) + coff + s * (16 / esz);
     v[i] = lds128(stage + r * 128 + ((s ^ (r & 7)) << 4));
     okr[i] = (ok >> r) & 1u;
   }
@@ -730,6 +746,7 @@ __device__ __forceinline__ void engine_body(const EngineParams* P, const GroupSc
       int prob, mb, nb, t, sp;
       locate(P, gs, u, splits, prob, mb, nb, t, sp);
       const EngineParams& p = P[prob];
+      const EpiView ev(p);
       const int acc = local & 1;
       // bias for this warp's columns, one value per lane per 32-column chunk (legacy path)
       float bias_r[kCW / 32];
@@ -738,9 +755,7 @@ __device__ __forceinline__ void engine_body(const EngineParams* P, const GroupSc
         const int col = nb * BN + cbeg + c * 32 + lane;
         bias_r[c] = (p.bias != nullptr && col < p.cols) ? __ldg(p.bias + col) : 0.0f;
       }
-      const uint32_t stage = smem_u32(smem + kStages * Cfg::kStageBytes + warp * (4096 + 256 + 512));
-      const uint32_t rtab = stage + 4096;  // this warp's 32 row offsets (read by epilogue_flush)
-      const uint32_t btab = rtab + 256;    // this warp's kCW bias values
+      const uint32_t stage = smem_u32(smem + kStages * Cfg::kStageBytes + warp * 4096);
       const int tile_row0 = kPair ? mb * 256 + static_cast<int>(rank) * 128 : mb * kEngineBM;
       const int row = tile_row0 + row_in_tile;
       const int warp_row0 = tile_row0 + quarter * 32;
@@ -761,18 +776,14 @@ __device__ __forceinline__ void engine_body(const EngineParams* P, const GroupSc
       uint4 pre[2][8];
       if (staged && (splits == 1 || p.split_ws == nullptr)) {
         ok_bits = __ballot_sync(0xffffffffu, row_ok);
-        __syncwarp();  // the previous tile's flushes have read the tables
-        asm volatile("st.shared.s64 [%0], %1;" ::"r"(rtab + lane * 8), "l"(roff) : "memory");
-        if (p.bias != nullptr) {
-#pragma unroll
-          for (int c = 0; c < kCW / 32; ++c)
-            asm volatile("st.shared.f32 [%0], %1;" ::"r"(btab + (c * 32 + lane) * 4), "f"(bias_r[c]) : "memory");
+        if (p.bias != nullptr && lane < kCW / 32) {  // warm L1 with this warp's bias slice
+          const float* bp = p.bias + nb * BN + cbeg + lane * 32;
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(bp) : "memory");
         }
-        __syncwarp();
         if constexpr (kFullEpi) {
           // grouped launches: the prefetched operands (e.g. the ReLU mask) may be produced by
           // earlier problems of this launch, so the epilogue acquires the tile's dependencies too
-          if (gs != nullptr && flush_src(p) != nullptr) wait_deps(gs, P, prob, mb, kPair ? 2 : 1);
+          if (gs != nullptr && flush_src(ev) != nullptr) wait_deps(gs, P, prob, mb, kPair ? 2 : 1);
           const int cfirst = nb * BN + cbeg;
           const int seg_cols = (p.out_bf16 && kSegLanes == 8) ? 64 : 32;
 #pragma unroll
@@ -781,8 +792,8 @@ __device__ __forceinline__ void engine_body(const EngineParams* P, const GroupSc
             if (col - cfirst >= kCW || col >= p.cols) break;
             const int cq = col / static_cast<int>(p.om.cb), cr = col - cq * static_cast<int>(p.om.cb);
             const int64_t coff = static_cast<int64_t>(cq) * p.om.ch + static_cast<int64_t>(cr) * p.om.cl;
-            if (p.out_bf16 && kSegLanes == 4) epilogue_prefetch<4>(p, rtab, ok_bits, coff, lane, pre[j]);
-            else epilogue_prefetch<8>(p, rtab, ok_bits, coff, lane, pre[j]);
+            if (ev.out_bf16 && kSegLanes == 4) epilogue_prefetch<4>(ev, roff, ok_bits, coff, lane, pre[j]);
+            else epilogue_prefetch<8>(ev, roff, ok_bits, coff, lane, pre[j]);
           }
         }
       }
@@ -830,19 +841,19 @@ __device__ __forceinline__ void engine_body(const EngineParams* P, const GroupSc
             const int64_t coff = off - roff;
             if (threadIdx.x == 0 && c < 2) BRK_TS(8 + 2 * c);
             if (kCW == 32 && p.out_bf16) {  // 64 B row segments
-              epilogue_stage(p, f, btab + c * 128, stage + lane * 128, lane, 0);
-              if (col0 < p.cols) epilogue_flush<4, kFullEpi>(p, stage, rtab, ok_bits, coff, lane, warp_row0, col0,
+              epilogue_stage(ev, f, col0, stage + lane * 128, lane, 0);
+              if (col0 < ev.cols) epilogue_flush<4, kFullEpi>(ev, stage, roff, ok_bits, coff, lane, warp_row0, col0,
                                                              seg < 2 ? pre[seg] : nullptr);
               else __syncwarp();
               ++seg;
             } else {
               const bool second = p.out_bf16 && (c & 1);
               if (!second) { seg_coff = coff; seg_col = col0; }
-              epilogue_stage(p, f, btab + c * 128, stage + lane * 128, lane, second ? 4 : 0);
+              epilogue_stage(ev, f, col0, stage + lane * 128, lane, second ? 4 : 0);
               if (!p.out_bf16 || second) {
                 if (threadIdx.x == 0 && c < 2) BRK_TS(9 + 2 * c);
                 if (col0 < p.cols)
-                  epilogue_flush<8, kFullEpi>(p, stage, rtab, ok_bits, seg_coff, lane, warp_row0, seg_col,
+                  epilogue_flush<8, kFullEpi>(ev, stage, roff, ok_bits, seg_coff, lane, warp_row0, seg_col,
                                               seg < 2 ? pre[seg] : nullptr);
                 else __syncwarp();
                 ++seg;
