@@ -449,63 +449,77 @@ __device__ __forceinline__ void epilogue_flush(const EpiView& p, uint32_t stage,
       }
     }
   }
+  // One short loop per feature (branch outside, rows inside): the code size is
+  // the sum of the features, not their product, so the epilogue stays in the
+  // instruction cache.
   float cs[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (kFull && p.out_bf16 && p.mask != nullptr) {
 #pragma unroll
-  for (int i = 0; i < kLanes; ++i) {
-    if (!okr[i]) continue;
-    uint8_t* dst = out + eo[i] * esz;
-    if (kFull && p.out_bf16) {
+    for (int i = 0; i < kLanes; ++i) {
       __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&v[i]);
-      if (p.mask != nullptr) {
-        const __nv_bfloat162* mh = reinterpret_cast<const __nv_bfloat162*>(&ld[i]);
+      const __nv_bfloat162* mh = reinterpret_cast<const __nv_bfloat162*>(&ld[i]);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float2 m2 = __bfloat1622float2(mh[j]);
-          float2 v2 = __bfloat1622float2(h[j]);
-          v2.x = m2.x > 0.0f ? v2.x : 0.0f;
-          v2.y = m2.y > 0.0f ? v2.y : 0.0f;
-          h[j] = __floats2bfloat162_rn(v2.x, v2.y);
-        }
+      for (int j = 0; j < 4; ++j) {
+        const float2 m2 = __bfloat1622float2(mh[j]);
+        const float2 v2 = __bfloat1622float2(h[j]);
+        h[j] = __floats2bfloat162_rn(m2.x > 0.0f ? v2.x : 0.0f, m2.y > 0.0f ? v2.y : 0.0f);
       }
-      *reinterpret_cast<uint4*>(dst) = v[i];
-      if (p.aux_in != nullptr) {  // (mask and aux are not combined: aux only on forward outputs)
-        uint4 a = ld[i];
-        __nv_bfloat162* ah = reinterpret_cast<__nv_bfloat162*>(&a);
+    }
+  }
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float2 y2 = __bfloat1622float2(h[j]);
-          float2 a2 = __bfloat1622float2(ah[j]);
-          a2.x = y2.x > 0.0f ? a2.x : 0.0f;
-          a2.y = y2.y > 0.0f ? a2.y : 0.0f;
-          ah[j] = __floats2bfloat162_rn(a2.x, a2.y);
-        }
-        *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.aux_out) + eo[i]) = a;
-        v[i] = a;  // column sums of the gradient
+  for (int i = 0; i < kLanes; ++i)
+    if (okr[i]) *reinterpret_cast<uint4*>(out + eo[i] * esz) = v[i];
+  if (kFull && p.out_bf16 && p.aux_in != nullptr) {  // (aux only on forward outputs, never with mask)
+#pragma unroll
+    for (int i = 0; i < kLanes; ++i) {
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v[i]);
+      __nv_bfloat162* ah = reinterpret_cast<__nv_bfloat162*>(&ld[i]);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 y2 = __bfloat1622float2(h[j]);
+        const float2 a2 = __bfloat1622float2(ah[j]);
+        ah[j] = __floats2bfloat162_rn(y2.x > 0.0f ? a2.x : 0.0f, y2.y > 0.0f ? a2.y : 0.0f);
       }
-      if (p.colsum_ws != nullptr) {
+      if (okr[i]) *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.aux_out) + eo[i]) = ld[i];
+      v[i] = ld[i];  // column sums of the gradient
+    }
+  }
+  if (kFull && !p.out_bf16 && p.sgd_w != nullptr) {
+#pragma unroll
+    for (int i = 0; i < kLanes; ++i) {
+      const float4 f4 = *reinterpret_cast<const float4*>(&v[i]);
+      const __nv_bfloat162* wo = reinterpret_cast<const __nv_bfloat162*>(&ld[i]);
+      const float2 w0 = __bfloat1622float2(wo[0]), w1 = __bfloat1622float2(wo[1]);
+      const __nv_bfloat162 n0 = __floats2bfloat162_rn(w0.x - p.sgd_lr * f4.x, w0.y - p.sgd_lr * f4.y);
+      const __nv_bfloat162 n1 = __floats2bfloat162_rn(w1.x - p.sgd_lr * f4.z, w1.y - p.sgd_lr * f4.w);
+      if (okr[i])
+        *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(p.sgd_w) + eo[i]) =
+            make_uint2(*reinterpret_cast<const uint32_t*>(&n0), *reinterpret_cast<const uint32_t*>(&n1));
+    }
+  }
+  if (kFull && p.colsum_ws != nullptr) {
+#pragma unroll
+    for (int i = 0; i < kLanes; ++i) {
+      if (!okr[i]) continue;
+      if (p.out_bf16) {
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const float2 c2 = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(&v[i])[j]);
           cs[2 * j] += c2.x;
           cs[2 * j + 1] += c2.y;
         }
+      } else {
+        const float4 f4 = *reinterpret_cast<const float4*>(&v[i]);
+        cs[0] += f4.x; cs[1] += f4.y; cs[2] += f4.z; cs[3] += f4.w;
       }
-    } else if (kFull) {  // fp32 output
-      *reinterpret_cast<uint4*>(dst) = v[i];
-      const float4 f4 = *reinterpret_cast<const float4*>(&v[i]);
-      if (p.sgd_w != nullptr) {
-        const __nv_bfloat162* wo = reinterpret_cast<const __nv_bfloat162*>(&ld[i]);
-        const float2 w0 = __bfloat1622float2(wo[0]), w1 = __bfloat1622float2(wo[1]);
-        __nv_bfloat162* wp = reinterpret_cast<__nv_bfloat162*>(static_cast<__nv_bfloat16*>(p.sgd_w) + eo[i]);
-        wp[0] = __floats2bfloat162_rn(w0.x - p.sgd_lr * f4.x, w0.y - p.sgd_lr * f4.y);
-        wp[1] = __floats2bfloat162_rn(w1.x - p.sgd_lr * f4.z, w1.y - p.sgd_lr * f4.w);
-      }
-      if (p.colsum_ws != nullptr) { cs[0] += f4.x; cs[1] += f4.y; cs[2] += f4.z; cs[3] += f4.w; }
-    } else {
-      *reinterpret_cast<uint4*>(dst) = v[i];
     }
-    if (p.zf_w != 0) {
-      const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+  }
+  if (p.zf_w != 0) {
+    const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+    for (int i = 0; i < kLanes; ++i) {
+      if (!okr[i]) continue;
+      uint8_t* dst = out + eo[i] * esz;
       *reinterpret_cast<uint4*>(dst + p.zf_w * 2) = z;
       *reinterpret_cast<uint4*>(dst + p.zf_h * 2) = z;
       *reinterpret_cast<uint4*>(dst + (p.zf_w + p.zf_h) * 2) = z;
@@ -814,7 +828,8 @@ __device__ __forceinline__ void engine_body(const EngineParams* P, const GroupSc
         int cr = cfirst - cq * static_cast<int>(p.om.cb);
         uint32_t v[32];
         tmem_ld32(tbase, v);
-#pragma unroll
+        // the full (grouped / fused-feature) epilogue keeps one copy of the chunk body
+#pragma unroll(kFullEpi ? 1 : kCW / 32)
         for (int c = 0; c < kCW / 32; ++c) {
           tmem_ld_wait();
           float f[32];
@@ -843,7 +858,7 @@ __device__ __forceinline__ void engine_body(const EngineParams* P, const GroupSc
             if (kCW == 32 && p.out_bf16) {  // 64 B row segments
               epilogue_stage(ev, f, col0, stage + lane * 128, lane, 0);
               if (col0 < ev.cols) epilogue_flush<4, kFullEpi>(ev, stage, roff, ok_bits, coff, lane, warp_row0, col0,
-                                                             seg < 2 ? pre[seg] : nullptr);
+                                                             seg == 0 ? pre[0] : (seg == 1 ? pre[1] : nullptr));
               else __syncwarp();
               ++seg;
             } else {
@@ -854,7 +869,7 @@ __device__ __forceinline__ void engine_body(const EngineParams* P, const GroupSc
                 if (threadIdx.x == 0 && c < 2) BRK_TS(9 + 2 * c);
                 if (col0 < p.cols)
                   epilogue_flush<8, kFullEpi>(ev, stage, roff, ok_bits, seg_coff, lane, warp_row0, seg_col,
-                                              seg < 2 ? pre[seg] : nullptr);
+                                              seg == 0 ? pre[0] : (seg == 1 ? pre[1] : nullptr));
                 else __syncwarp();
                 ++seg;
               }
