@@ -145,10 +145,12 @@ BRK_API size_t brk_fc_upd_workspace(int N, int C, int K);
  * weight update dW = dz[l] y[l-1]^T with fused SGD of W and b (lr).  Arrays of
  * device pointers: y, dz, colsum have L+1 entries (colsum[l]: fp32 [N/32][C]
  * column-sum partials of dz[l]), w, bias, dw, db have L.  Blocked bf16 layouts
- * as brk_fc_*, N and C multiples of 256, L <= 4.  counters:
+ * as brk_fc_*, N and C multiples of 256, L <= 4.  w_next (may be NULL = in-place SGD)
+ * receives the updated weights W - lr dW, so the weight updates need not wait
+ * for the bwd-data passes that read W (double-buffered weights).  counters:
  * brk_mlp_step_counters_bytes(L) bytes of device scratch (zeroed by the call). */
 BRK_API int brk_mlp_step(int L, int N, int C, const void* const* y, void* const* dz, const void* dy,
-                         void* const* w, float* const* bias, float* const* dw, float* const* db,
+                         void* const* w, void* const* w_next, float* const* bias, float* const* dw, float* const* db,
                          float* const* colsum, float lr, unsigned* counters, void* stream);
 BRK_API size_t brk_mlp_step_counters_bytes(int L);
 /* Bias gradient (north star): dz_out = dy * (y > 0) if y != NULL; db[K] = sum over N of dz;

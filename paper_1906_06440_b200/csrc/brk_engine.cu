@@ -314,12 +314,13 @@ struct EpiView {
   void* aux_out;
   float* colsum_ws;
   void* sgd_w;
+  const void* sgd_src;
   int64_t zf_w, zf_h;
   float sgd_lr;
   int out_bf16, act, rows, cols;
   __device__ __forceinline__ explicit EpiView(const EngineParams& p)
       : out(p.out), bias(p.bias), mask(p.mask), aux_in(p.aux_in), aux_out(p.aux_out), colsum_ws(p.colsum_ws),
-        sgd_w(p.sgd_w), zf_w(p.zf_w), zf_h(p.zf_h), sgd_lr(p.sgd_lr), out_bf16(p.out_bf16), act(p.act),
+        sgd_w(p.sgd_w), sgd_src(p.sgd_src != nullptr ? p.sgd_src : p.sgd_w), zf_w(p.zf_w), zf_h(p.zf_h), sgd_lr(p.sgd_lr), out_bf16(p.out_bf16), act(p.act),
         rows(p.rows), cols(p.cols) {}
 };
 
@@ -388,7 +389,7 @@ __device__ __forceinline__ void epilogue_stage(const EpiView& p, float (&f)[32],
 // outputs, SGD weights for fp32 outputs) do not depend on the accumulator:
 // they are fetched for the first segments before the epilogue waits for it.
 __device__ __forceinline__ const void* flush_src(const EpiView& p) {
-  return p.out_bf16 ? (p.mask != nullptr ? p.mask : p.aux_in) : p.sgd_w;
+  return p.out_bf16 ? (p.mask != nullptr ? p.mask : p.aux_in) : (p.sgd_w != nullptr ? p.sgd_src : nullptr);
 }
 template <int kLanes>
 __device__ __forceinline__ void epilogue_prefetch(const EpiView& p, int64_t roff, uint32_t ok, int64_t coff,

@@ -86,6 +86,7 @@ struct EngineParams {
   int32_t act;           // EpiAct
   const void* mask;      // bf16 tensor in the OUTPUT layout; out *= (mask > 0)
   void* sgd_w;           // bf16 weights in the OUTPUT layout: w -= lr * out
+  const void* sgd_src;   // if set: sgd_w = sgd_src - lr * out (double-buffered weights, staged path)
   float sgd_lr;
   // fused column sums of the final output (bias gradient of the next pass):
   // colsum_ws[(row / 32) * cols + col] = sum of the 32 rows' values

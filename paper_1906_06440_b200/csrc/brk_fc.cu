@@ -412,7 +412,7 @@ BRK_API size_t brk_mlp_step_counters_bytes(int L) {
 }
 
 BRK_API int brk_mlp_step(int L, int N, int C, const void* const* y, void* const* dz, const void* dy,
-                         void* const* w, float* const* bias, float* const* dw, float* const* db,
+                         void* const* w, void* const* w_next, float* const* bias, float* const* dw, float* const* db,
                          float* const* colsum, float lr, unsigned* counters, void* stream) {
   if (L < 1 || 3 * L > kMaxProbs) return set_error(BRK_ERR_CONTRACT, "mlp_step: 1 <= layers <= 4");
   int rc = check_fc(N, C, C, kB, kB, kB, BRK_BF16);
@@ -455,12 +455,17 @@ BRK_API int brk_mlp_step(int L, int N, int C, const void* const* y, void* const*
     gs.dep_prob[q][0] = dz_src; gs.dep_mode[q][0] = 0;  // the same rows of dz_l
     bwd_of[l] = q++;
     if (rc) break;
+    void* w_out = w_next != nullptr ? w_next[l - 1] : w[l - 1];
     rc = capture([&] {
-      return brk_fc_upd(y[l - 1], dz[l], dw[l - 1], w[l - 1], lr, colsum[l], N / 32, db[l - 1], bias[l - 1], lr,
+      return brk_fc_upd(y[l - 1], dz[l], dw[l - 1], w_out, lr, colsum[l], N / 32, db[l - 1], bias[l - 1], lr,
                         nullptr, 0, N, C, C, kB, kB, kB, BRK_BF16, stream);
     });
-    gs.dep_prob[q][0] = dz_src; gs.dep_mode[q][0] = 1;     // all of dz_l (reduction over N)
-    gs.dep_prob[q][1] = bwd_of[l]; gs.dep_mode[q][1] = 1;  // W_{l-1} read by bwd-data before the SGD rewrites it
+    gs.dep_prob[q][0] = dz_src; gs.dep_mode[q][0] = 1;  // all of dz_l (reduction over N)
+    if (w_next != nullptr) {
+      G.probs[q].sgd_src = w[l - 1];  // double-buffered weights: no write-after-read on W_{l-1}
+    } else {
+      gs.dep_prob[q][1] = bwd_of[l]; gs.dep_mode[q][1] = 1;  // W_{l-1} read by bwd-data before the SGD rewrites it
+    }
     upd_of[l] = q++;
   }
   g_force_plan = nullptr;

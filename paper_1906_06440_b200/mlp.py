@@ -52,11 +52,12 @@ class MLP:
         bf = torch.bfloat16
         cb = width // B
         nb = batch // B
-        self.w = []      # bf16 [Kb][Cb][64][64]
+        self._wbuf = [[], []]  # bf16 [Kb][Cb][64][64]; the fused step reads _wbuf[cur], writes _wbuf[1-cur]
+        self._cur = 0
         self.bias = []   # fp32 [K]
         for _ in range(layers):
             w = (torch.rand(width, width, generator=g) * 2 - 1) / np.sqrt(width)
-            self.w.append(w.reshape(cb, B, cb, B).permute(0, 2, 3, 1).contiguous().to(device, bf))
+            self._wbuf[0].append(w.reshape(cb, B, cb, B).permute(0, 2, 3, 1).contiguous().to(device, bf))
             self.bias.append(((torch.rand(width, generator=g) * 2 - 1) * 0.1).to(device))
         # activations: y[0] is the input, y[l] the output of layer l
         self.y = [torch.empty(nb, cb, B, B, dtype=bf, device=device) for _ in range(layers + 1)]
@@ -81,11 +82,20 @@ class MLP:
 
         self.fused = (os.environ.get("BRK_MLP_FUSED", "1") != "0" and layers <= 4
                       and width % 256 == 0 and batch % 256 == 0)
+        # double-buffered weights: the weight update writes W - lr dW to the other buffer, so it
+        # need not wait for the bwd-data pass that reads W (brk_mlp_step w_next)
+        self._wbuf[1] = [w.clone() for w in self._wbuf[0]] if self.fused else self._wbuf[0]
         arr = lambda ts: (ctypes.c_void_p * len(ts))(*[t.data_ptr() for t in ts])  # noqa: E731
-        self._tables = (arr(self.y), arr(self.dz), arr(self.w), arr(self.bias), arr(self.dw), arr(self.db),
-                        arr(self.colsum))
+        self._tables = [(arr(self.y), arr(self.dz), arr(self._wbuf[c]), arr(self._wbuf[1 - c]), arr(self.bias),
+                         arr(self.dw), arr(self.db), arr(self.colsum)) for c in (0, 1)]
+        self.graphs = None
         self.counters = torch.zeros(max(int(lib.brk_mlp_step_counters_bytes(layers)), 16) // 4, dtype=torch.int32,
                                     device=device)
+
+    @property
+    def w(self):
+        """Current (latest) bf16 weights of every layer."""
+        return self._wbuf[self._cur]
 
     # ------------------------------------------------------------------ params
     def params(self, l: int) -> FcParams:
@@ -150,9 +160,10 @@ class MLP:
     def fused_step(self, stream: int) -> int:
         """The whole step as ONE persistent engine launch (brk_mlp_step): 3L
         dependent GEMM problems with tile-level dependency counters."""
-        y, dz, w, b, dw, db, cs = self._tables
-        self._check(self.lib.brk_mlp_step(self.L, self.N, self.C, y, dz, self.dy.data_ptr(), w, b, dw, db, cs,
-                                          self.lr, self.counters.data_ptr(), stream))
+        y, dz, w, w_next, b, dw, db, cs = self._tables[self._cur]
+        self._check(self.lib.brk_mlp_step(self.L, self.N, self.C, y, dz, self.dy.data_ptr(), w, w_next, b, dw, db,
+                                          cs, self.lr, self.counters.data_ptr(), stream))
+        self._cur ^= 1
         return 1
 
     def step(self, stream: int | None = None) -> int:
@@ -204,14 +215,24 @@ class MLP:
             self.step(side.cuda_stream)  # warm: encodes tensor maps, sets smem attributes
         torch.cuda.current_stream().wait_stream(side)
         torch.cuda.synchronize()
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=side):
-            self.step(side.cuda_stream)
-        self.graph = g
-        return g
+        # one graph per weight-buffer parity (the fused step alternates the buffers)
+        self.graphs = {}
+        for _ in range(2 if self.fused else 1):
+            g = torch.cuda.CUDAGraph()
+            cur = self._cur
+            with torch.cuda.graph(g, stream=side):
+                self.step(side.cuda_stream)
+            self._cur = cur
+            self.graphs[cur] = g
+            if self.fused:
+                self._cur ^= 1
+        self.graph = self.graphs[self._cur]
+        return self.graph
 
     def replay(self):
-        self.graph.replay()
+        self.graphs[self._cur].replay()
+        if self.fused:
+            self._cur ^= 1
 
     def train_step(self, x_host, dy_host, out_host=None):
         """Public end-to-end step: H2D of the step's input and output gradient
@@ -222,7 +243,7 @@ class MLP:
         self.y[0].copy_(x_host, non_blocking=True)
         self.dy.copy_(dy_host, non_blocking=True)
         if self.graph is not None:
-            self.graph.replay()
+            self.replay()
         else:
             self.step()
         if out_host is None:
