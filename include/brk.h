@@ -147,7 +147,8 @@ BRK_API size_t brk_fc_upd_workspace(int N, int C, int K);
  * column-sum partials of dz[l]), w, bias, dw, db have L.  Blocked bf16 layouts
  * as brk_fc_*, N and C multiples of 256, L <= 4.  w_next (may be NULL = in-place SGD)
  * receives the updated weights W - lr dW, so the weight updates need not wait
- * for the bwd-data passes that read W (double-buffered weights).  counters:
+ * for the bwd-data passes that read W (double-buffered weights).  lr == 0: gradients
+ * only, no weight or bias update (data parallel: all-reduce, then brk_sgd_apply).  counters:
  * brk_mlp_step_counters_bytes(L) bytes of device scratch (zeroed by the call). */
 BRK_API int brk_mlp_step(int L, int N, int C, const void* const* y, void* const* dz, const void* dy,
                          void* const* w, void* const* w_next, float* const* bias, float* const* dw, float* const* db,

@@ -455,13 +455,17 @@ BRK_API int brk_mlp_step(int L, int N, int C, const void* const* y, void* const*
     gs.dep_prob[q][0] = dz_src; gs.dep_mode[q][0] = 0;  // the same rows of dz_l
     bwd_of[l] = q++;
     if (rc) break;
-    void* w_out = w_next != nullptr ? w_next[l - 1] : w[l - 1];
+    // lr == 0: gradients only (data parallel: all-reduce, then SGD outside the step)
+    const bool sgd = lr != 0.0f;
+    void* w_out = !sgd ? nullptr : (w_next != nullptr ? w_next[l - 1] : w[l - 1]);
     rc = capture([&] {
-      return brk_fc_upd(y[l - 1], dz[l], dw[l - 1], w_out, lr, colsum[l], N / 32, db[l - 1], bias[l - 1], lr,
-                        nullptr, 0, N, C, C, kB, kB, kB, BRK_BF16, stream);
+      return brk_fc_upd(y[l - 1], dz[l], dw[l - 1], w_out, lr, colsum[l], N / 32, db[l - 1],
+                        sgd ? bias[l - 1] : nullptr, lr, nullptr, 0, N, C, C, kB, kB, kB, BRK_BF16, stream);
     });
     gs.dep_prob[q][0] = dz_src; gs.dep_mode[q][0] = 1;  // all of dz_l (reduction over N)
-    if (w_next != nullptr) {
+    if (!sgd) {
+      // no weight write: no ordering against the bwd-data pass
+    } else if (w_next != nullptr) {
       G.probs[q].sgd_src = w[l - 1];  // double-buffered weights: no write-after-read on W_{l-1}
     } else {
       gs.dep_prob[q][1] = bwd_of[l]; gs.dep_mode[q][1] = 1;  // W_{l-1} read by bwd-data before the SGD rewrites it

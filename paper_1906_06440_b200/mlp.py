@@ -63,8 +63,11 @@ class MLP:
         self.y = [torch.empty(nb, cb, B, B, dtype=bf, device=device) for _ in range(layers + 1)]
         self.dz = [torch.empty(nb, cb, B, B, dtype=bf, device=device) for _ in range(layers + 1)]
         self.dy = torch.empty(nb, cb, B, B, dtype=bf, device=device)
-        self.dw = [torch.empty(cb, cb, B, B, dtype=torch.float32, device=device) for _ in range(layers)]
-        self.db = [torch.empty(width, dtype=torch.float32, device=device) for _ in range(layers)]
+        # all gradients in one flat fp32 buffer: one all-reduce bucket in data parallel
+        self.grads = torch.empty(layers * (width * width + width), dtype=torch.float32, device=device)
+        self.dw = [self.grads[l * width * width:(l + 1) * width * width].view(cb, cb, B, B) for l in range(layers)]
+        off = layers * width * width
+        self.db = [self.grads[off + l * width:off + (l + 1) * width] for l in range(layers)]
         lib = _lib.load()
         self.lib = lib
         self.ws = [torch.zeros(lib.brk_fc_bias_grad_workspace(width), dtype=torch.uint8, device=device)
@@ -84,7 +87,7 @@ class MLP:
                       and width % 256 == 0 and batch % 256 == 0)
         # double-buffered weights: the weight update writes W - lr dW to the other buffer, so it
         # need not wait for the bwd-data pass that reads W (brk_mlp_step w_next)
-        self._wbuf[1] = [w.clone() for w in self._wbuf[0]] if self.fused else self._wbuf[0]
+        self._wbuf[1] = [w.clone() for w in self._wbuf[0]] if (self.fused and process_group is None) else self._wbuf[0]
         arr = lambda ts: (ctypes.c_void_p * len(ts))(*[t.data_ptr() for t in ts])  # noqa: E731
         self._tables = [(arr(self.y), arr(self.dz), arr(self._wbuf[c]), arr(self._wbuf[1 - c]), arr(self.bias),
                          arr(self.dw), arr(self.db), arr(self.colsum)) for c in (0, 1)]
@@ -172,6 +175,13 @@ class MLP:
         s = torch.cuda.current_stream().cuda_stream if stream is None else stream
         if self.pg is None and self.fused:
             n = self.fused_step(s)
+        elif self.fused:
+            # data parallel: gradients from the fused step (no SGD), one all-reduce bucket, SGD apply
+            y, dz, w, _, b, dw, db, cs = self._tables[self._cur]
+            self._check(self.lib.brk_mlp_step(self.L, self.N, self.C, y, dz, self.dy.data_ptr(), w, None, b, dw, db,
+                                              cs, 0.0, self.counters.data_ptr(), s))
+            self._reducer().submit([self.grads])
+            n = 1 + self._allreduce_apply(s)
         elif self.pg is None:
             n = self.forward(s) + self.backward_update(s, apply_sgd=True)
         else:
@@ -250,3 +260,45 @@ class MLP:
             out_host = torch.empty(self.C, dtype=torch.float32, pin_memory=True)
         out_host.copy_(self.db[self.L - 1], non_blocking=True)
         return out_host
+
+    def train(self, xs, dys, outs):
+        """Pipelined end-to-end training over len(xs) steps through the public API:
+        every step's input and output gradient are copied from pinned host memory
+        (on a copy stream, into a double-buffered device staging area, overlapping
+        the previous step's compute), the step runs (graph replay when captured) and
+        its result (the last layer's bias gradient) is read back into ``outs[i]``."""
+        torch = self.torch
+        n = len(xs)
+        main = torch.cuda.current_stream()
+        copy = getattr(self, "_copy_stream", None) or torch.cuda.Stream()
+        self._copy_stream = copy
+        if getattr(self, "_staging", None) is None:
+            self._staging = [(torch.empty_like(self.y[0]), torch.empty_like(self.dy)) for _ in range(2)]
+        copied = [torch.cuda.Event() for _ in range(2)]
+        free = [torch.cuda.Event() for _ in range(2)]
+        copy.wait_stream(main)
+
+        def h2d(i):
+            sx, sdy = self._staging[i % 2]
+            with torch.cuda.stream(copy):
+                if i >= 2:
+                    copy.wait_event(free[i % 2])
+                sx.copy_(xs[i], non_blocking=True)
+                sdy.copy_(dys[i], non_blocking=True)
+                copied[i % 2].record(copy)
+
+        h2d(0)
+        for i in range(n):
+            if i + 1 < n:
+                h2d(i + 1)
+            main.wait_event(copied[i % 2])
+            sx, sdy = self._staging[i % 2]
+            self.y[0].copy_(sx, non_blocking=True)
+            self.dy.copy_(sdy, non_blocking=True)
+            free[i % 2].record(main)
+            if self.graph is not None:
+                self.replay()
+            else:
+                self.step()
+            outs[i].copy_(self.db[self.L - 1], non_blocking=True)
+        return outs
