@@ -27,21 +27,15 @@
 namespace brk {
 namespace {
 
-constexpr int kRows = 128;        // C rows (reference n) per CTA = MMA M
-constexpr int kCols = 256;        // C cols (reference m) per CTA = max MMA N
-constexpr int kChunkBytes = 128;  // K bytes staged per step (one 128B row)
-constexpr int kThreads = 128;
-constexpr int kStages = 2;
-constexpr int kAOpBytes = kRows * kChunkBytes;  // 16 KB
-constexpr int kBOpBytes = kCols * kChunkBytes;  // 32 KB
+constexpr int kRows = 128;         // C rows (reference n) per tile = MMA M
+constexpr int kCols = 256;         // C cols (reference m) per tile = max MMA N
+constexpr int kGatherWarps = 8;    // gather + epilogue warps
+constexpr int kThreads = (kGatherWarps + 1) * 32;  // + 1 MMA warp
+constexpr int kStages = 4;
+constexpr int kAOpBytes = kRows * 128;    // K-major, 128B swizzle: 128 rows x 128 B of K
+constexpr int kBOpBytes = kCols * 128;    // MN-major, 128B swizzle atoms: up to 256 cols
 constexpr int kStageBytes = kAOpBytes + kBOpBytes;
-constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align slack*/ + 256 /*barriers*/;
-
-// canonical SWIZZLE_NONE K-major: core matrix = 8 rows x 16 B (128 B contiguous);
-// K-adjacent cores at LBO = 128 B, 8-row groups at SBO = 1024 B.
-__device__ __forceinline__ uint32_t canon_off(int row, int chunk16) {
-  return static_cast<uint32_t>((row >> 3) * 1024 + chunk16 * 128 + (row & 7) * 16);
-}
+constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256;
 
 struct EntryPtrs {
   const char* a;
@@ -66,193 +60,266 @@ __device__ __forceinline__ EntryPtrs entry_ptrs(const GenericParams& p, int job,
 }
 
 __device__ __forceinline__ float load_in(const char* base, int64_t idx, bool bf16) {
-  if (bf16) {
-    return __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(base)[idx]);
-  }
+  if (bf16) return __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(base)[idx]);
   return reinterpret_cast<const float*>(base)[idx];
 }
 
+// 16 B of MMA input (8 bf16 or 4 tf32) from `cnt` elements at base + i*step
+// (contiguous & aligned: one vector load); elements past `cnt` are zero.
 template <bool kTF32>
-__device__ __forceinline__ uint4 pack16(const float* v) {
-  uint4 r;
-  if constexpr (kTF32) {
-    r.x = f32_to_tf32(v[0]);
-    r.y = f32_to_tf32(v[1]);
-    r.z = f32_to_tf32(v[2]);
-    r.w = f32_to_tf32(v[3]);
-  } else {
-    r.x = pack_bf16x2(v[0], v[1]);
-    r.y = pack_bf16x2(v[2], v[3]);
-    r.z = pack_bf16x2(v[4], v[5]);
-    r.w = pack_bf16x2(v[6], v[7]);
+__device__ __forceinline__ uint4 load_chunk(const char* base, int64_t first, int64_t step, int cnt, bool bf16_in,
+                                            bool vec) {
+  constexpr int kE = kTF32 ? 4 : 8;
+  if (vec && cnt >= kE) {
+    if (bf16_in) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(base) + first));
+      if constexpr (!kTF32) return v;
+      // bf16 storage on a TF32 computation: widen (exact)
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+      const float2 f0 = __bfloat1622float2(h[0]), f1 = __bfloat1622float2(h[1]);
+      return make_uint4(f32_to_tf32(f0.x), f32_to_tf32(f0.y), f32_to_tf32(f1.x), f32_to_tf32(f1.y));
+    }
+    const float4* f4 = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(base) + first);
+    const float4 f = __ldg(f4);
+    if constexpr (kTF32) {
+      return make_uint4(f32_to_tf32(f.x), f32_to_tf32(f.y), f32_to_tf32(f.z), f32_to_tf32(f.w));
+    } else {  // fp32 storage, bf16 tensor-core input: 8 elements = two 16 B loads
+      const float4 g = __ldg(f4 + 1);
+      return make_uint4(pack_bf16x2(f.x, f.y), pack_bf16x2(f.z, f.w), pack_bf16x2(g.x, g.y), pack_bf16x2(g.z, g.w));
+    }
   }
-  return r;
+  float v[8];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) v[t] = (t < kE && t < cnt) ? load_in(base, first + t * step, bf16_in) : 0.0f;
+  if constexpr (kTF32) return make_uint4(f32_to_tf32(v[0]), f32_to_tf32(v[1]), f32_to_tf32(v[2]), f32_to_tf32(v[3]));
+  return make_uint4(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]), pack_bf16x2(v[4], v[5]),
+                    pack_bf16x2(v[6], v[7]));
 }
 
+// Persistent: CTA walks job tiles (job, n-tile, m-tile).  Warps 0-7 gather the
+// (reference b block, reference a block) pair of each batch entry into a
+// 4-stage ring (reference b rows -> K-major 128B-swizzled A operand, reference
+// a rows -> MN-major 128B-swizzled B operand: both straight 16 B copies along
+// the contiguous dimension, vector loads when aligned), warp 8 issues the
+// tcgen05.mma chain (the whole batch reduces in TMEM), and warps 0-7 drain
+// TMEM and apply alpha/beta/bias/act/mask.
 template <bool kTF32>
 __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const GenericParams p) {
-  constexpr int kElems = kTF32 ? 4 : 8;            // elements per 16 B chunk
-  constexpr int kChunkElems = kChunkBytes / (kTF32 ? 4 : 2);
-  constexpr int kMmaK = kTF32 ? 8 : 16;            // K per tcgen05.mma (32 B)
-  constexpr int kMmaPerChunk = kChunkElems / kMmaK;  // = 4
+  constexpr int kE = kTF32 ? 4 : 8;              // elements per 16 B
+  constexpr int kKC = kTF32 ? 32 : 64;           // K elements per stage (128 B)
+  constexpr int kMmaK = kTF32 ? 8 : 16;          // K per tcgen05.mma
+  constexpr int kAtomCols = kTF32 ? 32 : 64;     // MN elements per 128 B atom row
+  constexpr int kAtomBytes = kKC * 128;          // one MN-major atom: kKC K-rows x 128 B
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);  // [kStages] + done
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + kStages + 1);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* done = empty + kStages;  // accumulator complete
+  uint64_t* drained = done + 1;      // epilogue finished reading TMEM
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(drained + 1);
 
   const int tid = threadIdx.x;
   const int warp = tid / 32;
   const int lane = tid % 32;
-  const int job = blockIdx.z;
-  const int n0 = blockIdx.y * kRows;
-  const int m0 = blockIdx.x * kCols;
-  const int m_here = min(kCols, p.m - m0);
-  const int n_cols = (m_here + 15) & ~15;  // MMA N: multiple of 16 for M=128
+  const int m_tiles = (p.m + kCols - 1) / kCols;
+  const int n_tiles = (p.n + kRows - 1) / kRows;
+  const int tiles = m_tiles * n_tiles * p.n_jobs;
+  const bool bf16_in = p.in_bf16 != 0;
+  const int n_chunks = (p.k + kKC - 1) / kKC;
+  const int steps = (p.alpha == 0.0f) ? 0 : p.batch * n_chunks;
 
   if (tid == 0) {
-    for (int s = 0; s < kStages + 1; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], kGatherWarps);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(done, 1);
+    mbar_init(drained, kGatherWarps);
     fence_barrier_init();
   }
-  if (warp == 0) tmem_alloc(tmem_slot, kCols);
+  if (warp == kGatherWarps) tmem_alloc(tmem_slot, kCols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  const bool bf16_in = p.in_bf16 != 0;
-  const int n_chunks = (p.k + kChunkElems - 1) / kChunkElems;
-  const int steps = (p.alpha == 0.0f) ? 0 : p.batch * n_chunks;
-  const uint32_t idesc = make_idesc(kTF32 ? kFmtTF32 : kFmtBF16, kRows, n_cols, 0, 0);
+  int local = 0;
+  for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
+    const int mt = t % m_tiles;
+    const int nt = (t / m_tiles) % n_tiles;
+    const int job = t / (m_tiles * n_tiles);
+    const int n0 = nt * kRows, m0 = mt * kCols;
+    const int m_here = min(kCols, p.m - m0);
+    const int n_here = min(kRows, p.n - n0);
+    // MMA N: bf16 B operand is MN-major (whole 128 B swizzle atoms, zero-filled past m);
+    // TF32 operands must be K-major (multiple of 16 rows)
+    const int n_cols = kTF32 ? (m_here + 15) & ~15 : (m_here + kAtomCols - 1) / kAtomCols * kAtomCols;
+    const int g0 = local * steps;             // global step index of this tile's first step
 
-  for (int s = 0; s < steps; ++s) {
-    const int st = s % kStages;
-    const int entry = s / n_chunks;
-    const int k0 = (s % n_chunks) * kChunkElems;
-    if (s >= kStages) mbar_wait(&bars[st], ((s / kStages) + 1) & 1);
-    uint8_t* a_op = smem + st * kStageBytes;
-    uint8_t* b_op = a_op + kAOpBytes;
-    const EntryPtrs e = entry_ptrs(p, job, entry);
-    // A operand <- reference b block rows (n, k): row r, 16B chunk c
-    for (int u = tid; u < kRows * 8; u += kThreads) {
-      const int c = u & 7, r = u >> 3;
-      const int row = n0 + r;
-      float v[8];
-#pragma unroll
-      for (int t = 0; t < kElems; ++t) {
-        const int kk = k0 + c * kElems + t;
-        v[t] = (row < p.n && kk < p.k) ? load_in(e.b, static_cast<int64_t>(row) * p.b_sn + static_cast<int64_t>(kk) * p.b_sk, bf16_in)
-                                       : 0.0f;
-      }
-      *reinterpret_cast<uint4*>(a_op + canon_off(r, c)) = pack16<kTF32>(v);
-    }
-    // B operand <- reference a block (k, m) transposed: row i (m index), 16B chunk c
-    for (int u = tid; u < kCols * 8; u += kThreads) {
-      const int i = u % kCols, c = u / kCols;
-      const int col = m0 + i;
-      float v[8];
-#pragma unroll
-      for (int t = 0; t < kElems; ++t) {
-        const int kk = k0 + c * kElems + t;
-        v[t] = (col < p.m && kk < p.k) ? load_in(e.a, static_cast<int64_t>(kk) * p.a_sk + static_cast<int64_t>(col) * p.a_sm, bf16_in)
-                                       : 0.0f;
-      }
-      *reinterpret_cast<uint4*>(b_op + canon_off(i, c)) = pack16<kTF32>(v);
-    }
-    fence_proxy_async_smem();
-    __syncthreads();
-    if (tid == 0) {
+    if (warp == kGatherWarps) {
+      // ---------------------------------------------------------- MMA issuer
+      const uint32_t idesc = make_idesc(kTF32 ? kFmtTF32 : kFmtBF16, kRows, n_cols, 0, kTF32 ? 0 : 1);
+      if (steps > 0) mbar_wait(drained, (local & 1) ^ 1);  // the previous tile's accumulator was read
       tc_fence_after();
-      const uint32_t a_base = smem_u32(a_op), b_base = smem_u32(b_op);
+      for (int s = 0; s < steps; ++s) {
+        const int g = g0 + s, st = g % kStages;
+        mbar_wait(&full[st], (g / kStages) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t a_base = smem_u32(smem + st * kStageBytes);
+          const uint32_t b_base = a_base + kAOpBytes;
 #pragma unroll
-      for (int kk = 0; kk < kMmaPerChunk; ++kk) {
-        const uint64_t ad = make_smem_desc(a_base + kk * 256, 128, 1024, kSwizzleNone);
-        const uint64_t bd = make_smem_desc(b_base + kk * 256, 128, 1024, kSwizzleNone);
-        mma_ss<kTF32>(tmem, ad, bd, idesc, (s > 0 || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < kKC / kMmaK; ++kk) {
+            const uint64_t ad = make_smem_desc(a_base + kk * 32, 16, 1024, kSwizzle128B);
+            const uint64_t bd = kTF32 ? make_smem_desc(b_base + kk * 32, 16, 1024, kSwizzle128B)
+                                      : make_smem_desc(b_base + kk * kMmaK * 128, kAtomBytes, 1024, kSwizzle128B);
+            mma_ss<kTF32>(tmem, ad, bd, idesc, (s > 0 || kk > 0) ? 1u : 0u);
+          }
+          mma_commit(&empty[st]);
+          if (s == steps - 1) mma_commit(done);
+        }
+        __syncwarp();
       }
-      mma_commit(&bars[st]);
-      if (s == steps - 1) mma_commit(&bars[kStages]);
-    }
-  }
-
-  // ---- epilogue: TMEM -> registers -> alpha/beta -> C -------------------------
-  if (steps > 0) {
-    mbar_wait(&bars[kStages], 0);
-    tc_fence_after();
-  }
-  const int row = n0 + warp * 32 + lane;
-  char* c_ptr;
-  if (p.mode == kModeStride) {
-    c_ptr = static_cast<char*>(p.c_base) + job * p.jstride_c * (p.out_bf16 ? 2 : 4);
-  } else {
-    c_ptr = static_cast<char*>(p.c_ptrs[job]);
-  }
-  const double alpha = p.alpha, beta = p.beta;
-  const float* bias_row = p.bias != nullptr ? p.bias + p.bias_offs[job] : nullptr;
-  const char* mask_ptr = p.mask_ptrs != nullptr ? static_cast<const char*>(p.mask_ptrs[job]) : nullptr;
-  for (int c0 = 0; c0 < n_cols; c0 += 32) {
-    uint32_t acc[32];
-    if (steps > 0) {
-      tmem_ld32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c0, acc);
-      tmem_ld_wait();
     } else {
-#pragma unroll
-      for (int j = 0; j < 32; ++j) acc[j] = 0u;
-    }
-    if (row < p.n) {
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const int col = m0 + c0 + j;
-        if (col < p.m) {
-          const int64_t off = static_cast<int64_t>(row) * p.ldc + col;
-          double out = alpha * static_cast<double>(__uint_as_float(acc[j]));
-          if (steps == 0) out = 0.0;
-          if (beta != 0.0) {
-            const double old = p.out_bf16 ? __bfloat162float(reinterpret_cast<__nv_bfloat16*>(c_ptr)[off])
-                                          : reinterpret_cast<float*>(c_ptr)[off];
-            out += beta * old;
-          }
-          if (bias_row != nullptr) out += static_cast<double>(bias_row[col]);
-          if (p.act == 1) {
-            out = out > 0.0 ? out : 0.0;
-          } else if (p.act == 2) {
-            const double e = exp(-fabs(out));
-            out = out >= 0.0 ? 1.0 / (1.0 + e) : e / (1.0 + e);
-          }
-          if (mask_ptr != nullptr) {
-            const float mv = p.out_bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(mask_ptr)[off])
-                                        : reinterpret_cast<const float*>(mask_ptr)[off];
-            if (!(mv > 0.0f)) out = 0.0;
-          }
-          if (p.out_bf16) {
-            reinterpret_cast<__nv_bfloat16*>(c_ptr)[off] = __float2bfloat16_rn(static_cast<float>(out));
+      // ---------------------------------------------------------- gather
+      const int gt = tid;  // 0 .. 255
+      const bool a_contig = p.b_sk == 1;   // reference b block: k contiguous
+      const bool b_contig = p.a_sm == 1;   // reference a block: m contiguous
+      const int n_rows8 = (n_here + 7) & ~7;
+      const int col_chunks = n_cols / kE;
+      for (int s = 0; s < steps; ++s) {
+        const int g = g0 + s, st = g % kStages;
+        const int entry = s / n_chunks;
+        const int k0 = (s % n_chunks) * kKC;
+        const int k_here = min(kKC, p.k - k0);
+        if (g >= kStages) mbar_wait(&empty[st], ((g / kStages) + 1) & 1);
+        uint8_t* a_op = smem + st * kStageBytes;
+        uint8_t* b_op = a_op + kAOpBytes;
+        const EntryPtrs e = entry_ptrs(p, job, entry);
+        const size_t esz = bf16_in ? 2 : 4;
+        const bool a_vec = a_contig && ((reinterpret_cast<uintptr_t>(e.b) & 15) == 0) && ((p.b_sn * esz) % 16 == 0);
+        const bool b_vec = b_contig && ((reinterpret_cast<uintptr_t>(e.a) & 15) == 0) && ((p.a_sk * esz) % 16 == 0);
+        // A operand (K-major) <- reference b block rows: (row r, 16 B chunk c) along k
+        for (int u = gt; u < n_rows8 * 8; u += kGatherWarps * 32) {
+          const int c = u & 7, r = u >> 3;
+          const int kk = c * kE;
+          uint4 v;
+          if (r < n_here) {
+            v = load_chunk<kTF32>(e.b, static_cast<int64_t>(n0 + r) * p.b_sn + static_cast<int64_t>(k0 + kk) * p.b_sk,
+                                  p.b_sk, k_here - kk, bf16_in, a_vec && (k0 + kk) % kE == 0);
           } else {
-            reinterpret_cast<float*>(c_ptr)[off] = static_cast<float>(out);
+            v = make_uint4(0u, 0u, 0u, 0u);
+          }
+          *reinterpret_cast<uint4*>(a_op + r * 128 + ((c ^ (r & 7)) << 4)) = v;
+        }
+        // B operand <- reference a block.  bf16: MN-major, (k-row kr, 16 B chunk c along m);
+        // TF32 (K-major only): row i = m index, 16 B chunk c along k (strided gather)
+        if constexpr (kTF32) {
+          for (int u = gt; u < n_cols * 8; u += kGatherWarps * 32) {
+            const int i = u >> 3, c = u & 7;
+            const int kk = c * kE;
+            const uint4 v = (i < m_here)
+                                ? load_chunk<kTF32>(e.a, static_cast<int64_t>(k0 + kk) * p.a_sk +
+                                                             static_cast<int64_t>(m0 + i) * p.a_sm,
+                                                    p.a_sk, k_here - kk, bf16_in, false)
+                                : make_uint4(0u, 0u, 0u, 0u);
+            *reinterpret_cast<uint4*>(b_op + i * 128 + ((c ^ (i & 7)) << 4)) = v;
+          }
+        } else
+        for (int u = gt; u < kKC * col_chunks; u += kGatherWarps * 32) {
+          const int kr = u / col_chunks, c = u - kr * col_chunks;
+          const int col = c * kE;
+          uint4 v;
+          if (kr < k_here && col < m_here) {
+            v = load_chunk<kTF32>(e.a, static_cast<int64_t>(k0 + kr) * p.a_sk + static_cast<int64_t>(m0 + col) * p.a_sm,
+                                  p.a_sm, m_here - col, bf16_in, b_vec && (m0 + col) % kE == 0);
+          } else {
+            v = make_uint4(0u, 0u, 0u, 0u);
+          }
+          const int atom = c / (kAtomCols / kE), cc = c % (kAtomCols / kE);
+          *reinterpret_cast<uint4*>(b_op + atom * kAtomBytes + kr * 128 + ((cc ^ (kr & 7)) << 4)) = v;
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full[st]);
+      }
+      // ---------------------------------------------------------- epilogue
+      if (steps > 0) {
+        mbar_wait(done, local & 1);
+        tc_fence_after();
+      }
+      const int quarter = warp & 3, half = warp >> 2;
+      const int row = n0 + quarter * 32 + lane;
+      char* c_ptr = p.mode == kModeStride ? static_cast<char*>(p.c_base) + job * p.jstride_c * (p.out_bf16 ? 2 : 4)
+                                          : static_cast<char*>(p.c_ptrs[job]);
+      const float* bias_row = p.bias != nullptr ? p.bias + p.bias_offs[job] : nullptr;
+      const char* mask_ptr = p.mask_ptrs != nullptr ? static_cast<const char*>(p.mask_ptrs[job]) : nullptr;
+      for (int c0 = half * 128; c0 < min(n_cols, half * 128 + 128); c0 += 32) {
+        uint32_t acc[32];
+        if (steps > 0) {
+          tmem_ld32(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + c0, acc);
+          tmem_ld_wait();
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) acc[j] = 0u;
+        }
+        if (row < p.n) {
+#pragma unroll 4
+          for (int j = 0; j < 32; ++j) {
+            const int col = m0 + c0 + j;
+            if (col >= p.m) continue;
+            const int64_t off = static_cast<int64_t>(row) * p.ldc + col;
+            float out = steps > 0 ? p.alpha * __uint_as_float(acc[j]) : 0.0f;
+            if (p.beta != 0.0f)
+              out += p.beta * (p.out_bf16 ? __bfloat162float(reinterpret_cast<__nv_bfloat16*>(c_ptr)[off])
+                                          : reinterpret_cast<float*>(c_ptr)[off]);
+            if (bias_row != nullptr) out += bias_row[col];
+            if (p.act == 1) {
+              out = fmaxf(out, 0.0f);
+            } else if (p.act == 2) {
+              const float ex = __expf(-fabsf(out));
+              out = out >= 0.0f ? 1.0f / (1.0f + ex) : ex / (1.0f + ex);
+            }
+            if (mask_ptr != nullptr) {
+              const float mv = p.out_bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(mask_ptr)[off])
+                                          : reinterpret_cast<const float*>(mask_ptr)[off];
+              if (!(mv > 0.0f)) out = 0.0f;
+            }
+            if (p.out_bf16) reinterpret_cast<__nv_bfloat16*>(c_ptr)[off] = __float2bfloat16_rn(out);
+            else reinterpret_cast<float*>(c_ptr)[off] = out;
           }
         }
       }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(drained);
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc(tmem, kCols);
+  if (warp == kGatherWarps) {
+    tc_fence_after();
+    tmem_dealloc(tmem, kCols);
+  }
 }
 
 }  // namespace
 
 int launch_brgemm_generic(const GenericParams& p, int compute_tf32, cudaStream_t stream) {
   if (p.n_jobs <= 0 || p.m <= 0 || p.n <= 0) return BRK_OK;
-  dim3 grid((p.m + kCols - 1) / kCols, (p.n + kRows - 1) / kRows, p.n_jobs);
-  if (grid.z > 65535) return set_error(BRK_ERR_CONTRACT, "too many jobs in one launch (max 65535)");
+  const int64_t tiles = static_cast<int64_t>((p.m + kCols - 1) / kCols) * ((p.n + kRows - 1) / kRows) * p.n_jobs;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = static_cast<int>(tiles < sms ? tiles : sms);
   cudaError_t err;
   if (compute_tf32) {
-    err = cudaFuncSetAttribute(brgemm_generic_kernel<true>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    err = cudaFuncSetAttribute(brgemm_generic_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
     if (err == cudaSuccess) brgemm_generic_kernel<true><<<grid, kThreads, kSmemBytes, stream>>>(p);
   } else {
-    err = cudaFuncSetAttribute(brgemm_generic_kernel<false>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    err = cudaFuncSetAttribute(brgemm_generic_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
     if (err == cudaSuccess) brgemm_generic_kernel<false><<<grid, kThreads, kSmemBytes, stream>>>(p);
   }
   if (err == cudaSuccess) err = cudaGetLastError();

@@ -216,6 +216,63 @@ def lstm_suite(t_steps=50, n=168, c=1024, k=1024, iters=3, precision="bf16"):
     return out
 
 
+def brgemm_suite(ms=(32, 64, 128, 256), batches=(1, 4, 16, 64), variants=("stride", "offset", "address"),
+                 iters=10, max_bytes=1 << 30, square=True):
+    """BASELINE config 5: BRGEMM shape sweep vs roofline (config 1 = stride, m=n=k=64, batch 16).
+
+    Each point is ONE grouped launch of J independent output blocks C_j (the
+    reference's single call is ~40-80 ns of ideal work), bf16
+    inputs, fp32 C, beta = 0.  F = 2 m n k batch J; B = J (2 batch (mk + kn) + 4 mn).
+    Reference storage contract (brgemm.py:1-24): a_i (k, m), b_i (n, k), c (n, m).
+    """
+    import torch
+
+    from paper_1906_06440_b200 import _lib
+
+    lib = _lib.load()
+    peak, hbm, src = _peaks()
+    timer = _Timer(torch)
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    shapes = [(m, m, m) for m in ms] if square else [(m, n, k) for m in ms for n in ms for k in ms]
+    rows = []
+    for m, n, k in shapes:
+        for batch in batches:
+            per_job = 2 * batch * (m * k + k * n) + 4 * m * n
+            jobs = int(max(1, min(8 * sms, max_bytes // per_job)))
+            a = torch.randn(jobs * batch * k * m, device="cuda").bfloat16()
+            b = torch.randn(jobs * batch * n * k, device="cuda").bfloat16()
+            c = torch.empty(jobs * n * m, device="cuda")
+            flops = 2.0 * m * n * k * batch * jobs
+            t_roof = max(flops / (peak * 1e12), jobs * per_job / (hbm * 1e9))
+            ji = torch.arange(jobs, device="cuda", dtype=torch.int64)
+            bi = torch.arange(batch, device="cuda", dtype=torch.int64)
+            a_off = ((ji[:, None] * batch + bi[None, :]) * (k * m)).reshape(-1).contiguous()
+            b_off = ((ji[:, None] * batch + bi[None, :]) * (n * k)).reshape(-1).contiguous()
+            c_ptr = (c.data_ptr() + ji * (n * m * 4)).contiguous()
+            a_ptr = (a.data_ptr() + a_off * 2).contiguous()
+            b_ptr = (b.data_ptr() + b_off * 2).contiguous()
+            for var in variants:
+                if var == "stride":
+                    fn = lambda sp: _lib.check(lib.brk_brgemm_stride(  # noqa: E731
+                        a.data_ptr(), b.data_ptr(), k * m, n * k, c.data_ptr(), jobs, batch * k * m, batch * n * k,
+                        n * m, m, n, k, batch, m, k, m, 1.0, 0.0, _lib.BRK_BF16, _lib.BRK_F32,
+                        _lib.BRK_COMPUTE_BF16, sp))
+                elif var == "offset":
+                    fn = lambda sp: _lib.check(lib.brk_brgemm_offs(  # noqa: E731
+                        a.data_ptr(), b.data_ptr(), a_off.data_ptr(), b_off.data_ptr(), c_ptr.data_ptr(), jobs, m, n,
+                        k, batch, m, k, m, 1.0, 0.0, _lib.BRK_BF16, _lib.BRK_F32, _lib.BRK_COMPUTE_BF16, sp))
+                else:
+                    fn = lambda sp: _lib.check(lib.brk_brgemm_addr(  # noqa: E731
+                        a_ptr.data_ptr(), b_ptr.data_ptr(), c_ptr.data_ptr(), jobs, m, n, k, batch, m, k, m, 1.0,
+                        0.0, _lib.BRK_BF16, _lib.BRK_F32, _lib.BRK_COMPUTE_BF16, sp))
+                mean, best = timer(fn, iters)
+                rows.append({"m": m, "n": n, "k": k, "batch": batch, "variant": var, "jobs": jobs,
+                             "us": mean * 1e6, "tflops": flops / mean / 1e12, "roof_frac": t_roof / mean,
+                             "bound": "tensor" if flops / (peak * 1e12) >= jobs * per_job / (hbm * 1e9) else "hbm"})
+            del a, b, c
+    return {"peak_tflops": peak, "hbm_gbs": hbm, "peak_source": src, "points": rows}
+
+
 def _plan(lib, pass_, geom):
     import ctypes
     out = (ctypes.c_int * 3)()
@@ -241,3 +298,8 @@ if __name__ == "__main__":
         (ROOT / "gpurun_out" / f"resnet_n{n}.json").write_text(json.dumps(res, indent=1))
     elif what == "lstm":
         print(json.dumps(lstm_suite(), indent=1))
+    elif what == "brgemm":
+        res = brgemm_suite()
+        for r in res["points"]:
+            print(f"m=n=k={r['m']:3d} batch {r['batch']:2d} {r['variant']:7s} jobs {r['jobs']:5d}: {r['us']:9.1f} us "
+                  f"{r['tflops']:7.1f} TF/s  {r['roof_frac'] * 100:5.1f}% of roofline ({r['bound']})")
