@@ -254,7 +254,7 @@ def other_workloads():
     """The metric's other two workloads on this GPU (informational; the headline
     is the MLP config): ResNet-50 conv fwd/bwd/upd at N=256 (reference weighted
     efficiency over the 53 convs) and the LSTM cell (T=50, N=168, C=K=1024)."""
-    from tools.suites import lstm_suite, resnet_suite
+    from tools.suites import brgemm_suite, lstm_suite, resnet_suite
 
     out = {}
     try:
@@ -271,6 +271,16 @@ def other_workloads():
         out["lstm_t50_n168_c1024"] = lstm_suite(iters=2)
     except Exception as exc:  # noqa: BLE001
         out["lstm_t50_n168_c1024"] = {"error": repr(exc)[:300]}
+    try:  # configs 1 and 5: the reference-API BRGEMM (grouped launch of J independent C blocks)
+        res = brgemm_suite(iters=5)
+        pts = res["points"]
+        c1 = [r for r in pts if r["m"] == 64 and r["batch"] == 16 and r["variant"] == "stride"][0]
+        out["brgemm"] = {
+            "config1_stride_16x64x64x64": {k: c1[k] for k in ("jobs", "us", "tflops", "roof_frac", "bound")},
+            "sweep": [{k: r[k] for k in ("m", "batch", "variant", "jobs", "tflops", "roof_frac")} for r in pts],
+            "note": "m=n=k in 32..256, batch 1..64, bf16 in / fp32 C, one grouped launch per point"}
+    except Exception as exc:  # noqa: BLE001
+        out["brgemm"] = {"error": repr(exc)[:300]}
     return out
 
 

@@ -825,6 +825,9 @@ __device__ __forceinline__ void engine_body(const EngineParams* P, const GroupSc
         int64_t seg_coff = 0;
         int seg_col = 0;
         int seg = 0;  // staged flush index (the first two use prefetched operands)
+        // problems without mask / aux / SGD / column sums take the compact store-only flush
+        const bool plain_here = ev.mask == nullptr && ev.aux_in == nullptr && ev.sgd_w == nullptr &&
+                                ev.colsum_ws == nullptr;
         int cq = cfirst / static_cast<int>(p.om.cb);
         int cr = cfirst - cq * static_cast<int>(p.om.cb);
         uint32_t v[32];
@@ -868,10 +871,11 @@ __device__ __forceinline__ void engine_body(const EngineParams* P, const GroupSc
               epilogue_stage(ev, f, col0, stage + lane * 128, lane, second ? 4 : 0);
               if (!p.out_bf16 || second) {
                 if (threadIdx.x == 0 && c < 2) BRK_TS(9 + 2 * c);
-                if (col0 < p.cols)
-                  epilogue_flush<8, kFullEpi>(ev, stage, roff, ok_bits, seg_coff, lane, warp_row0, seg_col,
-                                              seg == 0 ? pre[0] : (seg == 1 ? pre[1] : nullptr));
-                else __syncwarp();
+                if (col0 >= ev.cols) __syncwarp();
+                else if (kFullEpi && !plain_here)
+                  epilogue_flush<8, true>(ev, stage, roff, ok_bits, seg_coff, lane, warp_row0, seg_col,
+                                          seg == 0 ? pre[0] : (seg == 1 ? pre[1] : nullptr));
+                else epilogue_flush<8, false>(ev, stage, roff, ok_bits, seg_coff, lane);
                 ++seg;
               }
             }
