@@ -194,27 +194,21 @@ def cpu_baseline_sample():
 # GPU arm
 # ---------------------------------------------------------------------------
 def kernel_roofline(mlp, torch, peak_tflops):
-    """Average device duration of each engine GEMM launch (graph of 10 launches, CUDA events on
-    the launching stream) -> achieved TFLOP/s for the dominant kernel."""
+    """Roofline block for the dominant kernel of the timed step: the grouped
+    persistent engine launch that runs the whole MLP step (brk_mlp_step,
+    engine_group_kernel).  Algorithmic FLOPs per launch = 12 * 2NCK (SURVEY
+    8(d)); time per launch from CUDA events around a graph of 10 launches on
+    the launching stream; traffic = ncu dram read + write bytes of one launch
+    (profiles/r01b_kernels.json).  The standalone per-pass kernels (the
+    13-launch path) are timed the same way and reported alongside."""
     from paper_1906_06440_b200 import _lib
+    from paper_1906_06440_b200.mlp import flops_per_step
 
     lib, n, c = mlp.lib, mlp.N, mlp.C
     B = 64
     stream = torch.cuda.Stream()
-    calls = {
-        "fwd": lambda s: lib.brk_fc_fwd(mlp.y[0].data_ptr(), mlp.w[0].data_ptr(), mlp.bias[0].data_ptr(),
-                                        mlp.y[1].data_ptr(), n, c, c, B, B, B, 1, _lib.BRK_BF16, s),
-        "bwd": lambda s: lib.brk_fc_bwd_data(mlp.dz[2].data_ptr(), mlp.w[1].data_ptr(), mlp.y[1].data_ptr(),
-                                             mlp.dz[1].data_ptr(), mlp.colsum[1].data_ptr(), n, c, c, B, B, B,
-                                             _lib.BRK_BF16, s),
-        "upd": lambda s: lib.brk_fc_upd(mlp.y[0].data_ptr(), mlp.dz[1].data_ptr(), mlp.dw[0].data_ptr(), None,
-                                        0.0, mlp.colsum[1].data_ptr(), n // 32, mlp.db[0].data_ptr(), None, 0.0,
-                                        mlp.upd_ws[0].data_ptr(), mlp.upd_ws[0].numel(),
-                                        n, c, c, B, B, B, _lib.BRK_BF16, s),
-    }
-    out = {}
-    reps = 10
-    for name, fn in calls.items():
+
+    def graph_time(fn, reps=10):
         with torch.cuda.stream(stream):
             fn(stream.cuda_stream)
         stream.synchronize()
@@ -232,22 +226,45 @@ def kernel_roofline(mlp, torch, peak_tflops):
                 g.replay()
             e1.record(stream)
         e1.synchronize()
-        out[name] = e0.elapsed_time(e1) / (5 * reps) * 1e-3
-    flops = 2.0 * n * c * c
-    avg = statistics.fmean(out.values())
-    achieved = flops / avg / 1e12
+        return e0.elapsed_time(e1) / (5 * reps) * 1e-3
+
+    step_flops = flops_per_step(mlp.L, n, c, c)
+    t_step = graph_time(lambda s: mlp.fused_step(s)) if mlp.fused else None
+    passes = {
+        "fwd": lambda s: lib.brk_fc_fwd(mlp.y[0].data_ptr(), mlp.w[0].data_ptr(), mlp.bias[0].data_ptr(),
+                                        mlp.y[1].data_ptr(), n, c, c, B, B, B, 1, _lib.BRK_BF16, s),
+        "bwd": lambda s: lib.brk_fc_bwd_data(mlp.dz[2].data_ptr(), mlp.w[1].data_ptr(), mlp.y[1].data_ptr(),
+                                             mlp.dz[1].data_ptr(), mlp.colsum[1].data_ptr(), n, c, c, B, B, B,
+                                             _lib.BRK_BF16, s),
+        "upd": lambda s: lib.brk_fc_upd(mlp.y[0].data_ptr(), mlp.dz[1].data_ptr(), mlp.dw[0].data_ptr(), None,
+                                        0.0, mlp.colsum[1].data_ptr(), n // 32, mlp.db[0].data_ptr(), None, 0.0,
+                                        mlp.upd_ws[0].data_ptr(), mlp.upd_ws[0].numel(),
+                                        n, c, c, B, B, B, _lib.BRK_BF16, s),
+    }
+    per_pass = {k: graph_time(fn) * 1e6 for k, fn in passes.items()}
     traffic = None
-    tf = ROOT / "profiles" / "engine_traffic.json"
+    tf = ROOT / "profiles" / "r01b_kernels.json"
     if tf.exists():
         try:
-            traffic = json.loads(tf.read_text()).get("bytes_per_launch")
-        except ValueError:
+            for recs in json.loads(tf.read_text()).values():
+                for r in recs:
+                    if "engine_group_kernel" in r["kernel"]:
+                        rd = float(r["dram__bytes_read.sum"].split()[0])
+                        wr = float(r["dram__bytes_write.sum"].split()[0])
+                        traffic = (rd + wr) * 1e6  # ncu reports Mbyte
+        except (ValueError, KeyError):
             traffic = None
+    if t_step is None:  # data-parallel / unfused configuration: the per-pass engine kernel dominates
+        t_step = statistics.fmean(per_pass.values()) * 1e-6
+        step_flops = 2.0 * n * c * c
+        kernel = "brk engine_kernel (one FC pass)"
+    else:
+        kernel = "brk engine_group_kernel<128, pair>: the whole MLP step (12 GEMMs) in one persistent launch"
+    achieved = step_flops / t_step / 1e12
     return {"bound": "tensor", "achieved": achieved, "peak": peak_tflops, "unit": "TFLOP/s",
-            "frac": achieved / peak_tflops, "traffic": traffic,
-            "kernel": "brk engine_kernel (TMA->tcgen05.mma->TMEM, bf16, fp32 acc)",
-            "flops_per_launch": flops,
-            "us_per_launch": {k: v * 1e6 for k, v in out.items()}}
+            "frac": achieved / peak_tflops, "traffic": traffic, "kernel": kernel,
+            "flops_per_launch": step_flops, "us_per_launch": t_step * 1e6,
+            "standalone_pass_us": per_pass}
 
 
 def other_workloads():
