@@ -565,7 +565,6 @@ __device__ __forceinline__ void locate(const EngineParams* P, const GroupSched* 
 }
 
 // Grouped launches: block until the tiles this tile consumes are complete.
-// Relaxed polling (no L1 invalidation per probe), one acquire fence on success.
 __device__ __forceinline__ void wait_deps(const GroupSched* gs, const EngineParams* P, int prob, int mb,
                                           int halves) {
   for (int d = 0; d < kMaxDeps; ++d) {
@@ -577,11 +576,12 @@ __device__ __forceinline__ void wait_deps(const GroupSched* gs, const EnginePara
     unsigned v;
     long long spins = 0;
     do {
-      asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
+      // acquiring probes: measured to observe the producer's release sooner than relaxed
+      // polling followed by a fence (profiles/r01b_summary.md)
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
       if (++spins > (1ll << 31)) __trap();  // a dependency that never completes is a bug: fail loudly
     } while (v < need);
   }
-  asm volatile("fence.acq_rel.gpu;" ::: "memory");
   asm volatile("fence.proxy.async.global;" ::: "memory");  // the producer's TMA reads follow
 }
 
