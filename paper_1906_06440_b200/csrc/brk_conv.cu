@@ -75,32 +75,47 @@ struct ConvPlan {
 };
 
 // Tile choice for rows x cols outputs (rows need not divide the tile: the
-// pixel walk is clamped and the epilogue masks).  Per-SM tensor-pipe efficiency
-// in SS mode (measured on the MLP shapes): CTA pair N=256 ~1, N=128 ~2/3;
-// single CTA N=256 ~2/3, N=128 ~1/2, N=64 ~1/3.
-ConvPlan choose(int64_t rows, int cols, int k_steps, bool split_ok) {
+// pixel walk is clamped and the epilogue masks).  Cost = max(MMA time, memory
+// time).  MMA: per-SM tensor-pipe efficiency in SS mode (measured): CTA pair
+// N=256 ~1, N=128 ~2/3; single CTA N=256 ~2/3, N=128 ~1/2, N=64 ~0.4.
+// Memory: each operand is read once from HBM, and again once per tile along
+// the other dimension (from L2 when it fits, else HBM); split-K slices are
+// written and read back by the reduction.
+ConvPlan choose(int64_t rows, int cols, int k_steps, bool split_ok, double a_bytes = 0, double b_bytes = 0,
+                double out_bytes = 0, double slice_bytes = 0) {
   int forced_pair = -1, forced_bn = 0, forced_splits = 0;
   if (const char* env = std::getenv("BRK_CONV_TILE")) std::sscanf(env, "%d,%d", &forced_pair, &forced_bn);
   if (const char* env = std::getenv("BRK_CONV_SPLITS")) forced_splits = std::atoi(env);
   struct Opt { int pair, bn; double eff; };
   const Opt opts[] = {{1, 256, 1.0}, {1, 128, 0.67}, {0, 256, 0.67}, {0, 128, 0.5}, {0, 64, 0.4}};
   const int sms = engine_sm_count();
+  constexpr double kHbm = 6.5e12, kL2 = 18e12, kL2Fit = 60e6;
+  constexpr double kSmFlops = 8192.0 * 1.9e9;  // dense bf16 per SM per second
   ConvPlan best{0, 0, 1, 0};
   double best_cost = 0;
   for (const Opt& o : opts) {
     if (cols % o.bn) continue;
     if (forced_pair >= 0 && (o.pair != forced_pair || o.bn != forced_bn)) continue;
     const int tr = o.pair ? 256 : 128;
-    const int64_t tiles = ((rows + tr - 1) / tr) * (cols / o.bn);
+    const int64_t m_t = (rows + tr - 1) / tr, n_t = cols / o.bn;
+    const int64_t tiles = m_t * n_t;
     const int64_t units = o.pair ? sms / 2 : sms;
-    const double per_tile = static_cast<double>(tr) * o.bn * k_steps / ((o.pair ? 2.0 : 1.0) * o.eff);
+    // one work unit (tile x k-steps) on one SM (pair: each SM does half the rows)
+    const double unit_s = 128.0 * o.bn * 64 * 2 * k_steps / (kSmFlops * o.eff);
+    const double reread = a_bytes * (n_t - 1) / (a_bytes < kL2Fit ? kL2 : kHbm) +
+                          b_bytes * (m_t - 1) / (b_bytes < kL2Fit ? kL2 : kHbm);
+    const double base_mem = (a_bytes + b_bytes + out_bytes) / kHbm;
     int max_split = 1;
     if (split_ok) max_split = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(k_steps / 8, 2 * units / std::max<int64_t>(1, tiles))));
     if (forced_splits > 0) max_split = std::min(forced_splits, std::max(1, k_steps));
     for (int sp = forced_splits > 0 ? max_split : 1; sp <= max_split; ++sp) {
       const int64_t work = tiles * sp;
       const int64_t waves = (work + units - 1) / units;
-      const double cost = waves * per_tile / sp + (sp > 1 ? 0.05 * per_tile : 0.0) + 2.0e5;
+      const double t_mma = waves * unit_s / sp;
+      // weight updates (split_ok): the memory term over-penalised splits in measurement
+      // (slices mostly stay in L2); they keep the MMA-time model
+      const double t_mem = split_ok ? 0.0 : base_mem + reread;
+      const double cost = std::max(t_mma, t_mem) + (sp > 1 ? 0.05 * unit_s : 0.0) + 2.0e-6;
       if (best.bn == 0 || cost < best_cost) {
         // every split must own >= 1 k-step: ceil(k / ceil(k / sp)) splits
         const int per = (k_steps + sp - 1) / sp;
@@ -219,7 +234,8 @@ ConvPlan upd_plan(const ConvGeom& g) {
   const int64_t atoms = static_cast<int64_t>(g.C / kB) * g.R * g.S;
   const int64_t pix = static_cast<int64_t>(g.N) * g.P * g.Q;
   const int k_steps = static_cast<int>((pix + 63) / 64);
-  return choose(atoms * kB, g.K, k_steps, true);
+  const double in_b = 2.0 * g.N * g.C * g.H * g.W, out_b = 2.0 * g.N * g.K * g.P * g.Q;
+  return choose(atoms * kB, g.K, k_steps, true, in_b, out_b, 0.0, 4.0 * g.C * g.K * g.R * g.S);
 }
 
 }  // namespace
@@ -238,7 +254,8 @@ BRK_API int brk_conv_fwd(const void* in, const void* w, const float* bias, void*
   if (act < kActNone || act > kActSigmoid) return set_error(BRK_ERR_CONTRACT, "unknown activation");
   const int64_t rows = static_cast<int64_t>(N) * g.P * g.Q;
   const int k_steps = (C / kB) * R * S;
-  const ConvPlan pl = choose(rows, K, k_steps, false);
+  const ConvPlan pl = choose(rows, K, k_steps, false, 2.0 * N * C * H * W, 2.0 * K * C * R * S,
+                             2.0 * N * K * g.P * g.Q);
   if (pl.bn == 0) return set_error(BRK_ERR_CONTRACT, "conv fwd: no engine tile fits K");
   const int brows = pl.pair ? pl.bn / 2 : pl.bn;
   EngineParams p;
@@ -295,7 +312,8 @@ BRK_API int brk_conv_bwd_data(const void* dout, const void* w, void* din, int N,
   // rows: input pixels (stride 1) or output pixels scattered to (2p, 2q) (stride 2)
   const int64_t rows = stride == 1 ? static_cast<int64_t>(N) * H * W : static_cast<int64_t>(N) * g.P * g.Q;
   const int k_steps = (K / kB) * R * S;
-  const ConvPlan pl = choose(rows, C, k_steps, false);
+  const ConvPlan pl = choose(rows, C, k_steps, false, 2.0 * N * K * g.P * g.Q, 2.0 * K * C * R * S,
+                             2.0 * N * C * H * W);
   if (pl.bn == 0) return set_error(BRK_ERR_CONTRACT, "conv bwd: no engine tile fits C");
   const int brows = pl.pair ? pl.bn / 2 : pl.bn;
   // A: dO pixels; the dual convolution pads by R-1-pad and walks taps (s', r')
@@ -418,10 +436,12 @@ BRK_API int brk_conv_plan(int pass, int N, int C, int K, int H, int W, int R, in
   int rc = check_conv(g, kB, kB, BRK_BF16);
   if (rc) return rc;
   ConvPlan pl;
-  if (pass == 0) pl = choose(static_cast<int64_t>(N) * g.P * g.Q, K, (C / kB) * R * S, false);
+  if (pass == 0)
+    pl = choose(static_cast<int64_t>(N) * g.P * g.Q, K, (C / kB) * R * S, false, 2.0 * N * C * H * W,
+                2.0 * K * C * R * S, 2.0 * N * K * g.P * g.Q);
   else if (pass == 1)
     pl = choose(stride == 1 ? static_cast<int64_t>(N) * H * W : static_cast<int64_t>(N) * g.P * g.Q, C,
-                (K / kB) * R * S, false);
+                (K / kB) * R * S, false, 2.0 * N * K * g.P * g.Q, 2.0 * K * C * R * S, 2.0 * N * C * H * W);
   else pl = upd_plan(g);
   out3[0] = pl.pair;
   out3[1] = pl.bn;
