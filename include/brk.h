@@ -148,12 +148,13 @@ BRK_API size_t brk_fc_upd_workspace(int N, int C, int K);
  * as brk_fc_*, N and C multiples of 256, L <= 4.  w_next (may be NULL = in-place SGD)
  * receives the updated weights W - lr dW, so the weight updates need not wait
  * for the bwd-data passes that read W (double-buffered weights).  lr == 0: gradients
- * only, no weight or bias update (data parallel: all-reduce, then brk_sgd_apply).  counters:
- * brk_mlp_step_counters_bytes(L) bytes of device scratch (zeroed by the call). */
+ * only, no weight or bias update (data parallel: all-reduce, then brk_sgd_apply).  workspace:
+ * >= brk_mlp_step_workspace_bytes(L, N, C) bytes of device scratch (the tile dependency counters,
+ * zeroed by the call). */
 BRK_API int brk_mlp_step(int L, int N, int C, const void* const* y, void* const* dz, const void* dy,
                          void* const* w, void* const* w_next, float* const* bias, float* const* dw, float* const* db,
-                         float* const* colsum, float lr, unsigned* counters, void* stream);
-BRK_API size_t brk_mlp_step_counters_bytes(int L);
+                         float* const* colsum, float lr, void* workspace, size_t ws_bytes, void* stream);
+BRK_API size_t brk_mlp_step_workspace_bytes(int L, int N, int C);
 /* Bias gradient (north star): dz_out = dy * (y > 0) if y != NULL; db[K] = sum over N of dz;
  * if bias_sgd != NULL also bias_sgd -= lr * db (fused SGD).  Deterministic.
  * workspace: brk_fc_bias_grad_workspace(K) bytes, zeroed once before first use. */

@@ -335,21 +335,37 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
   return v;
 }
 
+// a[c] for a loop-variant c without dynamic register indexing (rolled epilogue loops)
+template <int N>
+__device__ __forceinline__ float pick(const float (&a)[N], int c) {
+  float v = a[0];
+#pragma unroll
+  for (int i = 1; i < N; ++i) v = c == i ? a[i] : v;
+  return v;
+}
+
 // Staged epilogue, part 1: bias, activation on one 32-column chunk of this
 // lane's row, written into the warp's staging tile (32 rows x 128 B at the
 // shared address `row`; 16 B slot j of row r at slot j ^ (r % 8): conflict-free
 // for the row-wise writes here and the segment-wise reads of epilogue_flush).
 // bf16: chunk = 4 slots (two chunks fill a 128 B row segment); fp32: 8 slots.
-__device__ __forceinline__ void epilogue_stage(const EpiView& p, float (&f)[32], int col0, uint32_t row,
-                                               int lane, int slot0) {
-  if (p.bias != nullptr) {  // the chunk's 32 bias values: uniform-address loads (L1 prefetched per tile)
-    const float4* b4 = reinterpret_cast<const float4*>(p.bias + col0);
+__device__ __forceinline__ void epilogue_stage(const EpiView& p, float (&f)[32], float bias_lane, uint32_t row,
+                                               int lane, int slot0, int col0x = 0) {
+#ifdef BRK_NO_BIAS_SHFL
+  if (p.bias != nullptr) {
+    const float4* b4 = reinterpret_cast<const float4*>(p.bias + col0x);
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const float4 b = __ldg(b4 + q);
       f[4 * q] += b.x; f[4 * q + 1] += b.y; f[4 * q + 2] += b.z; f[4 * q + 3] += b.w;
     }
   }
+#else
+  if (p.bias != nullptr) {  // the chunk's 32 bias values: lane j holds column j's (loaded before the accumulator wait)
+#pragma unroll
+    for (int j = 0; j < 32; ++j) f[j] += __shfl_sync(0xffffffffu, bias_lane, j);
+  }
+#endif
   if (p.act == kActRelu) {
 #pragma unroll
     for (int j = 0; j < 32; ++j) f[j] = fmaxf(f[j], 0.0f);
@@ -546,10 +562,12 @@ __device__ __forceinline__ void epilogue_flush(const EpiView& p, uint32_t stage,
 // launches (gs == null) order tiles column-block-major (mb fastest); grouped
 // launches order each problem row-major (nb fastest) so that the tiles of one
 // row block finish together and release the dependent problem's row block early.
+// nsp = the batch-list splits of the unit's problem (grouped problems are not split).
 __device__ __forceinline__ void locate(const EngineParams* P, const GroupSched* gs, int u, int splits, int& prob,
-                                       int& mb, int& nb, int& t, int& sp) {
+                                       int& mb, int& nb, int& t, int& sp, int& nsp) {
   if (gs == nullptr) {
     prob = 0;
+    nsp = splits;
     t = u / splits;
     sp = u - t * splits;
     mb = t % P[0].m_tiles;
@@ -558,13 +576,35 @@ __device__ __forceinline__ void locate(const EngineParams* P, const GroupSched* 
   }
   prob = 0;
   while (prob + 1 < gs->n_probs && u >= gs->tile_begin[prob + 1]) ++prob;
-  t = u - gs->tile_begin[prob];
+  const int rel = u - gs->tile_begin[prob];
+  nsp = 1;
+  t = rel;
   sp = 0;
   nb = t % P[prob].n_tiles;
   mb = t / P[prob].n_tiles;
 }
 
-// Grouped launches: block until the tiles this tile consumes are complete.
+#ifndef BRK_POLL_SLEEP
+#define BRK_POLL_SLEEP 128
+#endif
+constexpr unsigned kPollSleepNs = BRK_POLL_SLEEP;
+
+// Grouped launches: block until the tiles this tile consumes are complete.  One
+// thread per CTA polls the global counters (producer 0) and publishes the tile
+// ordinal in shared memory; the other producers and the epilogue wait on that
+// (polling pressure on the counters' L2 lines slowed the whole step down).
+__device__ __forceinline__ void publish_deps(uint32_t* seq, uint32_t ordinal) {
+  asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"(smem_u32(seq)), "r"(ordinal) : "memory");
+}
+__device__ __forceinline__ void wait_published(const uint32_t* seq, uint32_t ordinal, bool async_reads) {
+  uint32_t v;
+  long long spins = 0;
+  do {
+    asm volatile("ld.acquire.cta.shared.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(seq)) : "memory");
+    if (++spins > (1ll << 31)) __trap();
+  } while (static_cast<int32_t>(v - ordinal) < 0);
+  if (async_reads) asm volatile("fence.proxy.async.global;" ::: "memory");  // TMA reads follow
+}
 __device__ __forceinline__ void wait_deps(const GroupSched* gs, const EngineParams* P, int prob, int mb,
                                           int halves) {
   for (int d = 0; d < kMaxDeps; ++d) {
@@ -580,6 +620,7 @@ __device__ __forceinline__ void wait_deps(const GroupSched* gs, const EnginePara
       // polling followed by a fence (profiles/r01b_summary.md)
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
       if (++spins > (1ll << 31)) __trap();  // a dependency that never completes is a bug: fail loudly
+      if (v < need) __nanosleep(kPollSleepNs);  // back off: fewer probes on the counter's L2 line
     } while (v < need);
   }
   asm volatile("fence.proxy.async.global;" ::: "memory");  // the producer's TMA reads follow
@@ -601,6 +642,7 @@ __device__ __forceinline__ void engine_body(const EngineParams* P, const GroupSc
   uint64_t* tempty = tfull + 2;       // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   uint32_t* split_flag = tmem_slot + 1;
+  uint32_t* deps_seq = tmem_slot + 2;  // grouped launches: tiles whose dependencies producer 0 acquired
 
   const int warp = warp_id();
   const int lane = threadIdx.x & 31;
@@ -619,6 +661,7 @@ __device__ __forceinline__ void engine_body(const EngineParams* P, const GroupSc
       tma_prefetch_desc(&P[q].map_a);
       tma_prefetch_desc(&P[q].map_b);
     }
+    *deps_seq = 0u;
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -651,12 +694,25 @@ __device__ __forceinline__ void engine_body(const EngineParams* P, const GroupSc
       int g = 0;  // global k-step counter of this CTA (same sequence as the MMA issuer)
       int ltile = 0;
       for (int u = unit0; u < num_work; u += n_units) {
-        int prob, mb, nb, t, sp;
-        locate(P, gs, u, splits, prob, mb, nb, t, sp);
+        int prob, mb, nb, t, sp, nsp;
+        locate(P, gs, u, splits, prob, mb, nb, t, sp, nsp);
         const EngineParams& p = P[prob];
-        const int ks_per = (p.k_steps + splits - 1) / splits;
+        const int ks_per = (p.k_steps + nsp - 1) / nsp;
         const uint32_t bytes = (p.ca.n_loads * p.ca.load_bytes + p.cb.n_loads * p.cb.load_bytes) * (kPair ? 2 : 1);
-        if (gs != nullptr) wait_deps(gs, P, prob, mb, kPair ? 2 : 1);
+        // deps are acquired before the first A load of this producer's k-steps (and before
+        // its B load unless the problem's B operand is independent of them)
+        // (producer 0 polls the counters first thing and publishes; with b_first the
+        // others issue their first B block before waiting for that)
+        const uint32_t ordinal = static_cast<uint32_t>(ltile + 1);
+        bool deps_pending = gs != nullptr;
+        if (deps_pending && pid == 0) {
+          wait_deps(gs, P, prob, mb, kPair ? 2 : 1);
+          publish_deps(deps_seq, ordinal);
+          deps_pending = false;
+        } else if (deps_pending && !p.b_first) {
+          wait_published(deps_seq, ordinal, true);
+          deps_pending = false;
+        }
         if (pid == 0) BRK_TT(ltile, 0);
         ++ltile;
         const int arow = kPair ? mb * 2 + static_cast<int>(rank) : mb;
@@ -679,8 +735,15 @@ __device__ __forceinline__ void engine_body(const EngineParams* P, const GroupSc
             if (leader) mbar_arrive(&full[stage]);
           } else {
             if (leader) mbar_arrive_expect_tx(&full[stage], bytes);
-            issue_operand<kPair>(&p.map_a, p.ca, arow, s, sa, &full[stage]);
-            issue_operand<kPair>(&p.map_b, p.cb, brow, s, sb, &full[stage]);
+            if (deps_pending) {
+              issue_operand<kPair>(&p.map_b, p.cb, brow, s, sb, &full[stage]);
+              wait_published(deps_seq, ordinal, true);
+              deps_pending = false;
+              issue_operand<kPair>(&p.map_a, p.ca, arow, s, sa, &full[stage]);
+            } else {
+              issue_operand<kPair>(&p.map_a, p.ca, arow, s, sa, &full[stage]);
+              issue_operand<kPair>(&p.map_b, p.cb, brow, s, sb, &full[stage]);
+            }
           }
           if (gg == 0 && pid == 0) BRK_TS(2);
         }
@@ -694,12 +757,12 @@ __device__ __forceinline__ void engine_body(const EngineParams* P, const GroupSc
       uint32_t phase = 0;
       int local = 0;
       for (int u = unit0; u < num_work; u += n_units, ++local) {
-        int prob, mb, nb, t, sp;
-        locate(P, gs, u, splits, prob, mb, nb, t, sp);
+        int prob, mb, nb, t, sp, nsp;
+        locate(P, gs, u, splits, prob, mb, nb, t, sp, nsp);
         const EngineParams& p = P[prob];
         const uint32_t idesc = make_idesc(kTF32 ? kFmtTF32 : kFmtBF16, kPair ? 256 : kEngineBM, BN,
                                           p.ca.mn_major, p.cb.mn_major);
-        const int ks_per = (p.k_steps + splits - 1) / splits;
+        const int ks_per = (p.k_steps + nsp - 1) / nsp;
         const int s_begin = sp * ks_per;
         const int n_steps = min(p.k_steps, s_begin + ks_per) - s_begin;
         const int acc = local & 1;
@@ -758,12 +821,13 @@ __device__ __forceinline__ void engine_body(const EngineParams* P, const GroupSc
     const int halves = kPair ? 2 : 1;
     int local = 0;
     for (int u = unit0; u < num_work; u += n_units, ++local) {
-      int prob, mb, nb, t, sp;
-      locate(P, gs, u, splits, prob, mb, nb, t, sp);
+      int prob, mb, nb, t, sp, nsp;
+      locate(P, gs, u, splits, prob, mb, nb, t, sp, nsp);
       const EngineParams& p = P[prob];
       const EpiView ev(p);
       const int acc = local & 1;
-      // bias for this warp's columns, one value per lane per 32-column chunk (legacy path)
+      // bias for this warp's columns, one value per lane per 32-column chunk, loaded before
+      // the accumulator wait (the staged epilogue broadcasts it with shuffles)
       float bias_r[kCW / 32];
 #pragma unroll
       for (int c = 0; c < kCW / 32; ++c) {
@@ -791,14 +855,10 @@ __device__ __forceinline__ void engine_body(const EngineParams* P, const GroupSc
       uint4 pre[2][8];
       if (staged && (splits == 1 || p.split_ws == nullptr)) {
         ok_bits = __ballot_sync(0xffffffffu, row_ok);
-        if (p.bias != nullptr && lane < kCW / 32) {  // warm L1 with this warp's bias slice
-          const float* bp = p.bias + nb * BN + cbeg + lane * 32;
-          asm volatile("prefetch.global.L1 [%0];" ::"l"(bp) : "memory");
-        }
         if constexpr (kFullEpi) {
           // grouped launches: the prefetched operands (e.g. the ReLU mask) may be produced by
           // earlier problems of this launch, so the epilogue acquires the tile's dependencies too
-          if (gs != nullptr && flush_src(ev) != nullptr) wait_deps(gs, P, prob, mb, kPair ? 2 : 1);
+          if (gs != nullptr && flush_src(ev) != nullptr) wait_published(deps_seq, local + 1, false);
           const int cfirst = nb * BN + cbeg;
           const int seg_cols = (p.out_bf16 && kSegLanes == 8) ? 64 : 32;
 #pragma unroll
@@ -822,6 +882,9 @@ __device__ __forceinline__ void engine_body(const EngineParams* P, const GroupSc
         // pipelined one chunk ahead so the ld latency overlaps the epilogue math.
         const int cfirst = nb * BN + cbeg;
         // plain epilogue: staging tile, and the row offsets each lane stores in epilogue_flush
+        // diagnostics (debug_flags & 128): run the chunk loop twice (i-cache cold vs warm timing)
+        const int reps = (p.debug_flags & 128) ? 2 : 1;
+        for (int rep = 0; rep < reps; ++rep) {
         int64_t seg_coff = 0;
         int seg_col = 0;
         int seg = 0;  // staged flush index (the first two use prefetched operands)
@@ -837,12 +900,11 @@ __device__ __forceinline__ void engine_body(const EngineParams* P, const GroupSc
         for (int c = 0; c < kCW / 32; ++c) {
           tmem_ld_wait();
           float f[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
           if (kFullEpi && p.alpha != 1.0f) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]) * p.alpha;
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
+            for (int j = 0; j < 32; ++j) f[j] *= p.alpha;
           }
           if (c + 1 < kCW / 32) tmem_ld32(tbase + (c + 1) * 32, v);
           const int col0 = cfirst + c * 32;
@@ -860,7 +922,7 @@ __device__ __forceinline__ void engine_body(const EngineParams* P, const GroupSc
             const int64_t coff = off - roff;
             if (threadIdx.x == 0 && c < 2) BRK_TS(8 + 2 * c);
             if (kCW == 32 && p.out_bf16) {  // 64 B row segments
-              epilogue_stage(ev, f, col0, stage + lane * 128, lane, 0);
+              epilogue_stage(ev, f, pick(bias_r, c), stage + lane * 128, lane, 0, col0);
               if (col0 < ev.cols) epilogue_flush<4, kFullEpi>(ev, stage, roff, ok_bits, coff, lane, warp_row0, col0,
                                                              seg == 0 ? pre[0] : (seg == 1 ? pre[1] : nullptr));
               else __syncwarp();
@@ -868,7 +930,7 @@ __device__ __forceinline__ void engine_body(const EngineParams* P, const GroupSc
             } else {
               const bool second = p.out_bf16 && (c & 1);
               if (!second) { seg_coff = coff; seg_col = col0; }
-              epilogue_stage(ev, f, col0, stage + lane * 128, lane, second ? 4 : 0);
+              epilogue_stage(ev, f, pick(bias_r, c), stage + lane * 128, lane, second ? 4 : 0, col0);
               if (!p.out_bf16 || second) {
                 if (threadIdx.x == 0 && c < 2) BRK_TS(9 + 2 * c);
                 if (col0 >= ev.cols) __syncwarp();
@@ -882,6 +944,8 @@ __device__ __forceinline__ void engine_body(const EngineParams* P, const GroupSc
           }
         }
         tmem_ld_wait();
+        if (threadIdx.x == 0) BRK_TS(14 + rep);
+        }
         tc_fence_before();
         __syncwarp();
         if (threadIdx.x == 0) BRK_TS(12);
@@ -949,16 +1013,49 @@ __device__ __forceinline__ void engine_body(const EngineParams* P, const GroupSc
         }
       }
       // bias gradient from column-sum partials of a previous pass (+ fused bias SGD)
-      if (kFullEpi && p.db_partials != nullptr && mb == 0 && rank == 0 && sp == 0) {
-        if (gs != nullptr) wait_deps(gs, P, prob, mb, kPair ? 2 : 1);  // partials come from an earlier problem
-        for (int c = threadIdx.x; c < BN; c += kEpiThreads) {
-          const int col = nb * BN + c;
-          if (col >= p.cols) continue;
-          float s = 0.0f;
-          for (int q = 0; q < p.db_parts; ++q) s += p.db_partials[static_cast<int64_t>(q) * p.cols + col];
+      if (kFullEpi && p.db_partials != nullptr && mb == 0 && rank == 0 && (kGroup || sp == 0)) {
+        if (gs != nullptr) wait_published(deps_seq, local + 1, false);  // partials come from an earlier problem
+        // kG thread groups per column, each summing a contiguous run of partials with batched
+        // independent loads; the groups' sums meet in shared memory in group order (deterministic)
+#ifdef BRK_NO_DB_PAR
+        constexpr int kG = 1;
+#else
+        constexpr int kG = kEpiThreads / BN > 0 ? kEpiThreads / BN : 1;
+#endif
+        const int c = threadIdx.x % BN, g = threadIdx.x / BN;
+        const int col = nb * BN + c;
+        float s = 0.0f;
+        if (g < kG && col < p.cols) {
+          const int per = (p.db_parts + kG - 1) / kG;
+          const int q1 = min(p.db_parts, (g + 1) * per);
+          for (int q = g * per; q < q1; q += 8) {
+            float v[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              v[j] = q + j < q1 ? __ldcg(p.db_partials + static_cast<int64_t>(q + j) * p.cols + col) : 0.0f;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) s += v[j];
+          }
+        }
+        // each thread parks its sum in its own warp's staging tile (free after the flushes)
+        const uint32_t red0 = smem_u32(smem + kStages * Cfg::kStageBytes);
+        const uint32_t red = red0 + warp * 4096 + lane * 4;
+        if (kG > 1) {
+          asm volatile("st.shared.f32 [%0], %1;" ::"r"(red), "f"(s) : "memory");
+          named_bar_sync(1, kEpiThreads);
+        }
+        if (g == 0 && col < p.cols) {
+#pragma unroll
+          for (int h = 1; h < kG; ++h) {
+            float o;
+            const int t2 = threadIdx.x + h * BN;
+            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(o) : "r"(red0 + (t2 >> 5) * 4096 + (t2 & 31) * 4) : "memory");
+            s += o;
+          }
           p.db_out[col] = s;
           if (p.bias_sgd != nullptr) p.bias_sgd[col] -= p.bias_lr * s;
         }
+        if (kG > 1) named_bar_sync(1, kEpiThreads);  // staging tiles are reused by the next tile
       }
       if (gs != nullptr) {
         // release this CTA's half of the tile to dependent problems (their TMA reads it)
@@ -1135,7 +1232,12 @@ int launch_engine_group(const EngineGroup& G, int bn, int pair, cudaStream_t str
   if (gs.n_probs < 1 || gs.n_probs > kMaxProbs || gs.counters == nullptr)
     return set_error(BRK_ERR_CONTRACT, "engine group: 1..12 problems and a counter buffer");
   for (int q = 0; q < gs.n_probs; ++q) {
-    if (G.probs[q].k_splits > 1) return set_error(BRK_ERR_CONTRACT, "engine group: no split-K");
+    // (splitting a grouped problem in two halves that meet in the epilogue was measured
+    // slower at the MLP shape: the weight-update units are epilogue-bound)
+    const EngineParams& p = G.probs[q];
+    if (p.k_splits > 1) return set_error(BRK_ERR_CONTRACT, "engine group: no split-K");
+    if (gs.tile_begin[q + 1] - gs.tile_begin[q] != p.m_tiles * p.n_tiles)
+      return set_error(BRK_ERR_CONTRACT, "engine group: tile_begin does not match the problem's work units");
     if (G.probs[q].m_tiles > kCounterStride - 1) return set_error(BRK_ERR_CONTRACT, "engine group: > 64 row blocks");
     for (int d = 0; d < kMaxDeps; ++d)
       if (gs.dep_prob[q][d] >= q) return set_error(BRK_ERR_CONTRACT, "engine group: dependencies must point back");

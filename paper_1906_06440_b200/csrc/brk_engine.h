@@ -111,6 +111,9 @@ struct EngineParams {
   const void* aux_in;
   void* aux_out;
   int32_t debug_flags;  // bit0: skip MMA, bit1: skip TMA, bit2: no k rotation (diagnostics)
+  // grouped launches: the B operand does not depend on this problem's dependencies
+  // (e.g. layer weights): each producer issues its first B block before waiting for them
+  int32_t b_first;
   // diagnostics: per-CTA %globaltimer stamps [blockIdx.x][8]:
   // 0 entry, 1 setup done, 2 first TMA issued, 3 first full-barrier passed (MMA),
   // 4 last MMA committed, 5 epilogue got accumulator, 6 epilogue done, 7 exit

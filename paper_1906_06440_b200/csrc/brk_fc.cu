@@ -407,18 +407,37 @@ int launch_engine_group(const EngineGroup& G, int bn, int pair, cudaStream_t str
 
 extern "C" {
 
-BRK_API size_t brk_mlp_step_counters_bytes(int L) {
-  return static_cast<size_t>(3 * L) * kCounterStride * sizeof(unsigned);
+}  // extern "C"
+
+namespace {
+// MLP step workspace: the dependency counters (zeroed by every call)
+size_t mlp_counter_bytes(int L) { return static_cast<size_t>(3 * L) * kCounterStride * sizeof(unsigned); }
+}  // namespace
+
+extern "C" {
+
+BRK_API size_t brk_mlp_step_workspace_bytes(int L, int N, int C) {
+  (void)N;
+  (void)C;
+  if (L < 1) return 0;
+  return mlp_counter_bytes(L);
 }
 
 BRK_API int brk_mlp_step(int L, int N, int C, const void* const* y, void* const* dz, const void* dy,
                          void* const* w, void* const* w_next, float* const* bias, float* const* dw, float* const* db,
-                         float* const* colsum, float lr, unsigned* counters, void* stream) {
+                         float* const* colsum, float lr, void* workspace, size_t ws_bytes, void* stream) {
   if (L < 1 || 3 * L > kMaxProbs) return set_error(BRK_ERR_CONTRACT, "mlp_step: 1 <= layers <= 4");
   int rc = check_fc(N, C, C, kB, kB, kB, BRK_BF16);
   if (rc) return rc;
   if (N % 256 || C % 256 || N / 256 > kCounterStride - 1)
     return set_error(BRK_ERR_CONTRACT, "mlp_step: N, C multiples of 256, N <= 16384");
+  if (workspace == nullptr || ws_bytes < brk_mlp_step_workspace_bytes(L, N, C))
+    return set_error(BRK_ERR_CONTRACT, "mlp_step: workspace smaller than brk_mlp_step_workspace_bytes(L, N, C)");
+  unsigned* counters = static_cast<unsigned*>(workspace);
+  // BRK_MLP_BFIRST=0 (diagnostics): producers wait for a tile's dependencies before loading
+  // the weight operand too
+  const char* bfirst_env = std::getenv("BRK_MLP_BFIRST");
+  const int b_first = bfirst_env ? std::atoi(bfirst_env) : 1;
   static EngineGroup G;  // large: keep off the stack (host-side staging of the kernel parameter block)
   std::memset(&G, 0, sizeof(G));
   GroupSched& gs = G.sched;
@@ -439,6 +458,7 @@ BRK_API int brk_mlp_step(int L, int N, int C, const void* const* y, void* const*
                         stream);
     });
     if (l > 0) { gs.dep_prob[q][0] = fwd_of[l - 1]; gs.dep_mode[q][0] = 0; }
+    G.probs[q].b_first = b_first;  // B = W_l, not written in this launch before the weight updates
     if (l == L - 1) {  // top layer also emits dz_L = dy * (y_L > 0) and its column sums
       G.probs[q].aux_in = dy;
       G.probs[q].aux_out = dz[L];
@@ -446,15 +466,19 @@ BRK_API int brk_mlp_step(int L, int N, int C, const void* const* y, void* const*
     }
     fwd_of[l] = q++;
   }
-  for (int l = L; l >= 1 && !rc; --l) {  // layer l (weights w[l-1]): bwd-data, then the weight update
+  auto add_bwd = [&](int l) {  // layer l (weights w[l-1]): bwd-data
     const int dz_src = l == L ? fwd_of[L - 1] : bwd_of[l + 1];
     rc = capture([&] {
       return brk_fc_bwd_data(dz[l], w[l - 1], l > 1 ? y[l - 1] : nullptr, dz[l - 1], l > 1 ? colsum[l - 1] : nullptr,
                              N, C, C, kB, kB, kB, BRK_BF16, stream);
     });
     gs.dep_prob[q][0] = dz_src; gs.dep_mode[q][0] = 0;  // the same rows of dz_l
+    // B = W_{l-1}: with in-place SGD it is rewritten only after this pass completes (dependency below)
+    G.probs[q].b_first = b_first;
     bwd_of[l] = q++;
-    if (rc) break;
+  };
+  auto add_upd = [&](int l) {  // layer l: weight update (+ fused SGD)
+    const int dz_src = l == L ? fwd_of[L - 1] : bwd_of[l + 1];
     // lr == 0: gradients only (data parallel: all-reduce, then SGD outside the step)
     const bool sgd = lr != 0.0f;
     void* w_out = !sgd ? nullptr : (w_next != nullptr ? w_next[l - 1] : w[l - 1]);
@@ -471,16 +495,26 @@ BRK_API int brk_mlp_step(int L, int N, int C, const void* const* y, void* const*
       gs.dep_prob[q][1] = bwd_of[l]; gs.dep_mode[q][1] = 1;  // W_{l-1} read by bwd-data before the SGD rewrites it
     }
     upd_of[l] = q++;
+  };
+  // Work-unit order (CTA pairs take units round-robin and run them in order): the weight
+  // update of layer l is placed after the bwd-data pass of layer l - lag, so the units of the
+  // bwd-data chain (the critical path) are not queued behind the longer weight-update units.
+  const char* lag_env = std::getenv("BRK_MLP_UPD_LAG");
+  const int lag = lag_env ? std::max(0, std::atoi(lag_env)) : 1;
+  for (int l = L; l >= 1 - lag && !rc; --l) {
+    if (l >= 1) add_bwd(l);
+    if (!rc && l + lag <= L && l + lag >= 1) add_upd(l + lag);
   }
   g_force_plan = nullptr;
   (void)upd_of;
   if (rc) return rc;
   gs.n_probs = q;
   gs.tile_begin[0] = 0;
-  for (int i = 0; i < q; ++i) gs.tile_begin[i + 1] = gs.tile_begin[i] + G.probs[i].m_tiles * G.probs[i].n_tiles;
+  for (int i = 0; i < q; ++i)
+    gs.tile_begin[i + 1] = gs.tile_begin[i] + G.probs[i].m_tiles * G.probs[i].n_tiles;
   gs.counters = counters;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  cudaError_t err = cudaMemsetAsync(counters, 0, brk_mlp_step_counters_bytes(L), st);
+  cudaError_t err = cudaMemsetAsync(counters, 0, mlp_counter_bytes(L), st);
   if (err != cudaSuccess) return set_cuda_error(err, "mlp_step counters");
   g_launches.fetch_add(1);
   return launch_engine_group(G, 128, 1, st);

@@ -92,8 +92,9 @@ class MLP:
         self._tables = [(arr(self.y), arr(self.dz), arr(self._wbuf[c]), arr(self._wbuf[1 - c]), arr(self.bias),
                          arr(self.dw), arr(self.db), arr(self.colsum)) for c in (0, 1)]
         self.graphs = None
-        self.counters = torch.zeros(max(int(lib.brk_mlp_step_counters_bytes(layers)), 16) // 4, dtype=torch.int32,
-                                    device=device)
+        # dependency counters + split tickets (zeroed by every call) and parked half-accumulators
+        self.step_ws = torch.zeros(max(int(lib.brk_mlp_step_workspace_bytes(layers, batch, width)), 16),
+                                   dtype=torch.uint8, device=device)
 
     @property
     def w(self):
@@ -165,7 +166,8 @@ class MLP:
         dependent GEMM problems with tile-level dependency counters."""
         y, dz, w, w_next, b, dw, db, cs = self._tables[self._cur]
         self._check(self.lib.brk_mlp_step(self.L, self.N, self.C, y, dz, self.dy.data_ptr(), w, w_next, b, dw, db,
-                                          cs, self.lr, self.counters.data_ptr(), stream))
+                                          cs, self.lr, self.step_ws.data_ptr(), self.step_ws.numel(),
+                                          stream))
         self._cur ^= 1
         return 1
 
@@ -179,7 +181,7 @@ class MLP:
             # data parallel: gradients from the fused step (no SGD), one all-reduce bucket, SGD apply
             y, dz, w, _, b, dw, db, cs = self._tables[self._cur]
             self._check(self.lib.brk_mlp_step(self.L, self.N, self.C, y, dz, self.dy.data_ptr(), w, None, b, dw, db,
-                                              cs, 0.0, self.counters.data_ptr(), s))
+                                              cs, 0.0, self.step_ws.data_ptr(), self.step_ws.numel(), s))
             self._reducer().submit([self.grads])
             n = 1 + self._allreduce_apply(s)
         elif self.pg is None:

@@ -115,3 +115,4 @@ def test_fused_step_matches_per_pass_launches(monkeypatch):
         outs.append([t.float().cpu() for t in mlp.w + mlp.dw + mlp.db + mlp.y[1:]])
     for a, b in zip(*outs):
         assert (a - b).abs().max().item() <= 2e-2 * max(b.abs().max().item(), 1e-6)
+

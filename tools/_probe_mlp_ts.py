@@ -26,9 +26,16 @@ valid = a[:, :, 3] > 0
 t0 = a[:, :, 0][valid & (a[:, :, 0] > 0)].min()
 n_units = 74
 # global order of tiles per pair: u = unit + i * n_units; problems: tile_begin from sizes
-sizes = [64] * 4 + [64, 32] * 4
+import os
+lag = int(os.environ.get("BRK_MLP_UPD_LAG", "1"))
+names = ["fwd1", "fwd2", "fwd3", "fwd4"]
+for l in range(4, -lag, -1):
+    if l >= 1:
+        names.append(f"bwd{l}")
+    if 1 <= l + lag <= 4:
+        names.append(f"upd{l + lag}")
+sizes = [32 if n.startswith("upd") else 64 for n in names]
 begin = np.cumsum([0] + sizes)
-names = ["fwd1", "fwd2", "fwd3", "fwd4", "bwd4", "upd4", "bwd3", "upd3", "bwd2", "upd2", "bwd1", "upd1"]
 rows = []
 for unit in range(n_units):
     for i in range(16):
