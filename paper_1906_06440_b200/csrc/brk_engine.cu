@@ -350,22 +350,11 @@ __device__ __forceinline__ float pick(const float (&a)[N], int c) {
 // for the row-wise writes here and the segment-wise reads of epilogue_flush).
 // bf16: chunk = 4 slots (two chunks fill a 128 B row segment); fp32: 8 slots.
 __device__ __forceinline__ void epilogue_stage(const EpiView& p, float (&f)[32], float bias_lane, uint32_t row,
-                                               int lane, int slot0, int col0x = 0) {
-#ifdef BRK_NO_BIAS_SHFL
-  if (p.bias != nullptr) {
-    const float4* b4 = reinterpret_cast<const float4*>(p.bias + col0x);
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const float4 b = __ldg(b4 + q);
-      f[4 * q] += b.x; f[4 * q + 1] += b.y; f[4 * q + 2] += b.z; f[4 * q + 3] += b.w;
-    }
-  }
-#else
+                                               int lane, int slot0) {
   if (p.bias != nullptr) {  // the chunk's 32 bias values: lane j holds column j's (loaded before the accumulator wait)
 #pragma unroll
     for (int j = 0; j < 32; ++j) f[j] += __shfl_sync(0xffffffffu, bias_lane, j);
   }
-#endif
   if (p.act == kActRelu) {
 #pragma unroll
     for (int j = 0; j < 32; ++j) f[j] = fmaxf(f[j], 0.0f);
@@ -922,7 +911,7 @@ __device__ __forceinline__ void engine_body(const EngineParams* P, const GroupSc
             const int64_t coff = off - roff;
             if (threadIdx.x == 0 && c < 2) BRK_TS(8 + 2 * c);
             if (kCW == 32 && p.out_bf16) {  // 64 B row segments
-              epilogue_stage(ev, f, pick(bias_r, c), stage + lane * 128, lane, 0, col0);
+              epilogue_stage(ev, f, pick(bias_r, c), stage + lane * 128, lane, 0);
               if (col0 < ev.cols) epilogue_flush<4, kFullEpi>(ev, stage, roff, ok_bits, coff, lane, warp_row0, col0,
                                                              seg == 0 ? pre[0] : (seg == 1 ? pre[1] : nullptr));
               else __syncwarp();
@@ -930,7 +919,7 @@ __device__ __forceinline__ void engine_body(const EngineParams* P, const GroupSc
             } else {
               const bool second = p.out_bf16 && (c & 1);
               if (!second) { seg_coff = coff; seg_col = col0; }
-              epilogue_stage(ev, f, pick(bias_r, c), stage + lane * 128, lane, second ? 4 : 0, col0);
+              epilogue_stage(ev, f, pick(bias_r, c), stage + lane * 128, lane, second ? 4 : 0);
               if (!p.out_bf16 || second) {
                 if (threadIdx.x == 0 && c < 2) BRK_TS(9 + 2 * c);
                 if (col0 >= ev.cols) __syncwarp();
@@ -1017,11 +1006,7 @@ __device__ __forceinline__ void engine_body(const EngineParams* P, const GroupSc
         if (gs != nullptr) wait_published(deps_seq, local + 1, false);  // partials come from an earlier problem
         // kG thread groups per column, each summing a contiguous run of partials with batched
         // independent loads; the groups' sums meet in shared memory in group order (deterministic)
-#ifdef BRK_NO_DB_PAR
-        constexpr int kG = 1;
-#else
         constexpr int kG = kEpiThreads / BN > 0 ? kEpiThreads / BN : 1;
-#endif
         const int c = threadIdx.x % BN, g = threadIdx.x / BN;
         const int col = nb * BN + c;
         float s = 0.0f;

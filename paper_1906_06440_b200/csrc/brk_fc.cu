@@ -460,9 +460,13 @@ BRK_API int brk_mlp_step(int L, int N, int C, const void* const* y, void* const*
     if (l > 0) { gs.dep_prob[q][0] = fwd_of[l - 1]; gs.dep_mode[q][0] = 0; }
     G.probs[q].b_first = b_first;  // B = W_l, not written in this launch before the weight updates
     if (l == L - 1) {  // top layer also emits dz_L = dy * (y_L > 0) and its column sums
-      G.probs[q].aux_in = dy;
-      G.probs[q].aux_out = dz[L];
-      G.probs[q].colsum_ws = colsum[L];
+      const char* de = std::getenv("BRK_MLP_DIAG");  // diagnostics only: drop parts of the top epilogue
+      const int diag = de ? std::atoi(de) : 0;
+      if (!(diag & 1)) {
+        G.probs[q].aux_in = dy;
+        G.probs[q].aux_out = dz[L];
+      }
+      if (!(diag & 2)) G.probs[q].colsum_ws = colsum[L];
     }
     fwd_of[l] = q++;
   }

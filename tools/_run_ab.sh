@@ -1,7 +1,4 @@
 J='import json,sys; d=json.loads(sys.stdin.read()); print(d["value"], d["ms_per_step"], d["e2e"]["value"], d["clocks"]["sm_mhz"])'
-python -m pytest tests/test_gpu_mlp.py -x -q 2>&1 | tail -2
-for i in 1 2; do
-  echo -n "new "; python bench.py --steps 100 --warmup 5 2>&1 | tail -1 | python -c "$J"
-  for v in S1 S2; do echo -n "$v "; (cd _v/$v && python bench.py --steps 100 --warmup 5 2>&1 | tail -1 | python -c "$J"); done
-done
+python -m pytest tests/test_gpu_mlp.py tests/test_gpu_fc.py tests/test_gpu_conv_engine.py -x -q 2>&1 | tail -2
+for i in 1 2; do python bench.py --steps 100 --warmup 5 2>&1 | tail -1 | python -c "$J"; done
 python tools/_probe_mlp_ts.py 2>&1 | tail -13
