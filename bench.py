@@ -199,7 +199,7 @@ def kernel_roofline(mlp, torch, peak_tflops):
     engine_group_kernel).  Algorithmic FLOPs per launch = 12 * 2NCK (SURVEY
     8(d)); time per launch from CUDA events around a graph of 10 launches on
     the launching stream; traffic = ncu dram read + write bytes of one launch
-    (profiles/r01b_kernels.json).  The standalone per-pass kernels (the
+    (profiles/r01c_mlp_kernel.json).  The standalone per-pass kernels (the
     13-launch path) are timed the same way and reported alongside."""
     from paper_1906_06440_b200 import _lib
     from paper_1906_06440_b200.mlp import flops_per_step
@@ -243,7 +243,7 @@ def kernel_roofline(mlp, torch, peak_tflops):
     }
     per_pass = {k: graph_time(fn) * 1e6 for k, fn in passes.items()}
     traffic = None
-    tf = ROOT / "profiles" / "r01b_kernels.json"
+    tf = ROOT / "profiles" / "r01c_mlp_kernel.json"
     if tf.exists():
         try:
             for recs in json.loads(tf.read_text()).values():
