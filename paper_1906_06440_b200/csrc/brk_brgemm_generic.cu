@@ -21,21 +21,29 @@
 // TMEM lanes  <-> reference n (rows of C),  TMEM columns <-> reference m.
 // tcgen05 A operand = reference B blocks (n x k, K-major)
 // tcgen05 B operand = reference A blocks (k x m) transposed into K-major rows of m.
+#include <algorithm>
+
 #include "brk_internal.h"
 #include "brk_ptx.cuh"
+#include "brk_tma_host.h"
 
 namespace brk {
 namespace {
 
 constexpr int kRows = 128;         // C rows (reference n) per tile = MMA M
 constexpr int kCols = 256;         // C cols (reference m) per tile = max MMA N
-constexpr int kGatherWarps = 8;    // gather + epilogue warps
-constexpr int kThreads = (kGatherWarps + 1) * 32;  // + 1 MMA warp
-constexpr int kStages = 4;
+constexpr int kGatherWarps = 8;    // warps 0-7: operand gather (cp.async / converting loads)
+constexpr int kMmaWarp = 8;        // warp 8: tcgen05.mma issuer
+constexpr int kTmaWarp = 9;        // warps 9-12: TMA producers (stride / offset variants)
+constexpr int kTmaWarps = 4;       // a warp keeps ~one box in flight: four of them per SM
+constexpr int kEpiWarp0 = kTmaWarp + kTmaWarps;  // warps 13-16: epilogue (one per TMEM lane quarter)
+constexpr int kEpiWarps = 4;
+constexpr int kThreads = (kEpiWarp0 + kEpiWarps) * 32;
+constexpr int kMaxStages = 8;
+constexpr int kRingBytes = 4 * (kRows * 128 + kCols * 128);  // 192 KB of operand ring
+constexpr int kAtomColsBf16 = 64;  // bf16 elements per 128 B swizzle-atom row
 constexpr int kAOpBytes = kRows * 128;    // K-major, 128B swizzle: 128 rows x 128 B of K
-constexpr int kBOpBytes = kCols * 128;    // MN-major, 128B swizzle atoms: up to 256 cols
-constexpr int kStageBytes = kAOpBytes + kBOpBytes;
-constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256;
+constexpr int kSmemBytes = kRingBytes + 1024 + 256;
 
 struct EntryPtrs {
   const char* a;
@@ -96,15 +104,31 @@ __device__ __forceinline__ uint4 load_chunk(const char* base, int64_t first, int
                     pack_bf16x2(v[6], v[7]));
 }
 
-// Persistent: CTA walks job tiles (job, n-tile, m-tile).  Warps 0-7 gather the
-// (reference b block, reference a block) pair of each batch entry into a
-// 4-stage ring (reference b rows -> K-major 128B-swizzled A operand, reference
-// a rows -> MN-major 128B-swizzled B operand: both straight 16 B copies along
-// the contiguous dimension, vector loads when aligned), warp 8 issues the
-// tcgen05.mma chain (the whole batch reduces in TMEM), and warps 0-7 drain
-// TMEM and apply alpha/beta/bias/act/mask.
+// element offsets of an entry's blocks from the buffer bases (offset / stride variants)
+__device__ __forceinline__ void entry_offs(const GenericParams& p, int job, int i, int64_t& oa, int64_t& ob) {
+  const int64_t idx = static_cast<int64_t>(job) * p.batch + i;
+  if (p.mode == kModeOffs) {
+    oa = p.a_offs[idx];
+    ob = p.b_offs[idx];
+  } else {
+    oa = job * p.jstride_a + i * p.stride_a;
+    ob = job * p.jstride_b + i * p.stride_b;
+  }
+}
+
+// Persistent: CTA walks job tiles (job, n-tile, m-tile) with four decoupled roles:
+//  * the TMA warp loads an entry's (reference b block, reference a block) pair as one box
+//    each when the blocks do not wrap a row of their buffer's 2-d view (stride / offset
+//    variants, bf16);
+//  * warps 0-7 gather every other entry (cp.async for aligned contiguous bf16 rows, else
+//    converting loads) — reference b rows -> K-major 128B-swizzled A operand, reference a
+//    rows -> MN-major (bf16) or K-major (TF32) B operand;
+//  * warp 8 issues the tcgen05.mma chain (the whole batch reduces in TMEM), two
+//    accumulators so a tile's MMAs overlap the previous tile's epilogue;
+//  * warps 10-13 drain TMEM and apply alpha / beta / bias / act / mask.
+// Ring stages are sized by the tile (16 KB A + the B atoms actually used).
 template <bool kTF32>
-__global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const GenericParams p) {
+__global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __grid_constant__ GenericParams p) {
   constexpr int kE = kTF32 ? 4 : 8;              // elements per 16 B
   constexpr int kKC = kTF32 ? 32 : 64;           // K elements per stage (128 B)
   constexpr int kMmaK = kTF32 ? 8 : 16;          // K per tcgen05.mma
@@ -114,11 +138,11 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const Gener
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
-  uint64_t* empty = full + kStages;
-  uint64_t* done = empty + kStages;  // accumulator complete
-  uint64_t* drained = done + 1;      // epilogue finished reading TMEM
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(drained + 1);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRingBytes);
+  uint64_t* empty = full + kMaxStages;
+  uint64_t* done = empty + kMaxStages;  // [2] accumulator complete
+  uint64_t* drained = done + 2;         // [2] epilogue finished reading TMEM
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(drained + 2);
 
   const int tid = threadIdx.x;
   const int warp = tid / 32;
@@ -129,82 +153,172 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const Gener
   const bool bf16_in = p.in_bf16 != 0;
   const int n_chunks = (p.k + kKC - 1) / kKC;
   const int steps = (p.alpha == 0.0f) ? 0 : p.batch * n_chunks;
+  // ring geometry: the B operand of the widest tile (MN-major atoms for bf16, K-major rows for TF32)
+  const int m_max = min(p.m, kCols);
+  const int b_bytes = kTF32 ? ((m_max + 15) & ~15) * 128 : (m_max + kAtomCols - 1) / kAtomCols * kAtomBytes;
+  const int stage_bytes = (kAOpBytes + b_bytes + 1023) & ~1023;
+  // (a multiple of the TMA producer count: each stage always has the same producer, so the
+  // parity waits on its empty barrier cannot alias)
+  const int n_stages = min(kMaxStages, kRingBytes / stage_bytes) / kTmaWarps * kTmaWarps;
 
   if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], kGatherWarps);
+    for (int s = 0; s < kMaxStages; ++s) {
+      mbar_init(&full[s], 1);  // TMA: the producer's expect_tx; gather: one arrive after the copies
       mbar_init(&empty[s], 1);
     }
-    mbar_init(done, 1);
-    mbar_init(drained, kGatherWarps);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&done[a], 1);
+      mbar_init(&drained[a], kEpiWarps);
+    }
     fence_barrier_init();
   }
-  if (warp == kGatherWarps) tmem_alloc(tmem_slot, kCols);
+  if (warp == kMmaWarp) tmem_alloc(tmem_slot, 2 * kCols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  int local = 0;
-  for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
-    const int mt = t % m_tiles;
-    const int nt = (t / m_tiles) % n_tiles;
-    const int job = t / (m_tiles * n_tiles);
-    const int n0 = nt * kRows, m0 = mt * kCols;
-    const int m_here = min(kCols, p.m - m0);
-    const int n_here = min(kRows, p.n - n0);
-    // MMA N: bf16 B operand is MN-major (whole 128 B swizzle atoms, zero-filled past m);
-    // TF32 operands must be K-major (multiple of 16 rows)
-    const int n_cols = kTF32 ? (m_here + 15) & ~15 : (m_here + kAtomCols - 1) / kAtomCols * kAtomCols;
-    const int g0 = local * steps;             // global step index of this tile's first step
+  // Does batch entry `entry` of `job` go through TMA (all roles evaluate it identically), and
+  // where do its boxes start in the 2-d views.  Evaluated once per entry, not per K chunk.
+  struct EntryBox {
+    bool tma;
+    int32_t ca, ra, cb, rb;
+  };
+  auto entry_box = [&](int job, int entry) -> EntryBox {
+    EntryBox eb{false, 0, 0, 0, 0};
+    if (kTF32 || !p.tma) return eb;
+    int64_t oa, ob;
+    entry_offs(p, job, entry, oa, ob);
+    int64_t qa, qb;
+    if (((oa | ob) >> 32) == 0) {  // 32-bit division when the offsets allow it
+      qa = static_cast<uint32_t>(oa) / static_cast<uint32_t>(p.a_sk);
+      qb = static_cast<uint32_t>(ob) / static_cast<uint32_t>(p.b_sn);
+    } else {
+      qa = oa / p.a_sk;
+      qb = ob / p.b_sn;
+    }
+    eb.ra = static_cast<int32_t>(qa);
+    eb.ca = static_cast<int32_t>(oa - qa * p.a_sk);
+    eb.rb = static_cast<int32_t>(qb);
+    eb.cb = static_cast<int32_t>(ob - qb * p.b_sn);
+    eb.tma = eb.cb + p.k <= p.b_sn && eb.ca + p.m <= p.a_sk;
+    return eb;
+  };
 
-    if (warp == kGatherWarps) {
-      // ---------------------------------------------------------- MMA issuer
+  if (warp == kMmaWarp) {
+    // ------------------------------------------------------------ MMA issuer
+    int local = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
+      if (steps == 0) continue;
+      const int mt = t % m_tiles;
+      const int m_here = min(kCols, p.m - mt * kCols);
+      const int n_cols = kTF32 ? (m_here + 15) & ~15 : (m_here + kAtomCols - 1) / kAtomCols * kAtomCols;
       const uint32_t idesc = make_idesc(kTF32 ? kFmtTF32 : kFmtBF16, kRows, n_cols, 0, kTF32 ? 0 : 1);
-      if (steps > 0) mbar_wait(drained, (local & 1) ^ 1);  // the previous tile's accumulator was read
+      const int acc = local & 1;
+      mbar_wait(&drained[acc], ((local >> 1) & 1) ^ 1);  // the epilogue read this accumulator two tiles ago
       tc_fence_after();
+      const uint32_t d_tmem = tmem + acc * kCols;
+      const int g0 = local * steps;
       for (int s = 0; s < steps; ++s) {
-        const int g = g0 + s, st = g % kStages;
-        mbar_wait(&full[st], (g / kStages) & 1);
+        const int g = g0 + s, st = g % n_stages;
+        mbar_wait(&full[st], (g / n_stages) & 1);
         tc_fence_after();
+        fence_proxy_async_smem();  // gathered stages were written through the generic proxy
         if (elect_one()) {
-          const uint32_t a_base = smem_u32(smem + st * kStageBytes);
+          const uint32_t a_base = smem_u32(smem + st * stage_bytes);
           const uint32_t b_base = a_base + kAOpBytes;
 #pragma unroll
           for (int kk = 0; kk < kKC / kMmaK; ++kk) {
             const uint64_t ad = make_smem_desc(a_base + kk * 32, 16, 1024, kSwizzle128B);
             const uint64_t bd = kTF32 ? make_smem_desc(b_base + kk * 32, 16, 1024, kSwizzle128B)
                                       : make_smem_desc(b_base + kk * kMmaK * 128, kAtomBytes, 1024, kSwizzle128B);
-            mma_ss<kTF32>(tmem, ad, bd, idesc, (s > 0 || kk > 0) ? 1u : 0u);
+            mma_ss<kTF32>(d_tmem, ad, bd, idesc, (s > 0 || kk > 0) ? 1u : 0u);
           }
           mma_commit(&empty[st]);
-          if (s == steps - 1) mma_commit(done);
+          if (s == steps - 1) mma_commit(&done[acc]);
         }
         __syncwarp();
       }
-    } else {
-      // ---------------------------------------------------------- gather
-      const int gt = tid;  // 0 .. 255
-      const bool a_contig = p.b_sk == 1;   // reference b block: k contiguous
-      const bool b_contig = p.a_sm == 1;   // reference a block: m contiguous
+    }
+  } else if (warp >= kTmaWarp && warp < kTmaWarp + kTmaWarps) {
+    // ------------------------------------------------------------ TMA producers (stage g: warp g % 4)
+    const int pid = warp - kTmaWarp;
+    if (!kTF32 && p.tma && elect_one()) {
+      int local = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
+        const int mt = t % m_tiles;
+        const int nt = (t / m_tiles) % n_tiles;
+        const int job = t / (m_tiles * n_tiles);
+        const int n0 = nt * kRows, m0 = mt * kCols;
+        const int m_here = min(kCols, p.m - m0);
+        const int atoms = (m_here + kAtomCols - 1) / kAtomCols;
+        const uint32_t bytes = static_cast<uint32_t>(p.nbox * 128 + atoms * p.abox * 128);
+        int g = local * steps;
+        for (int entry = 0; entry < p.batch && steps > 0; ++entry) {
+          const EntryBox eb = entry_box(job, entry);
+          if (!eb.tma) { g += n_chunks; continue; }
+          for (int ch = 0; ch < n_chunks; ++ch, ++g) {
+            if (g % kTmaWarps != pid) continue;
+            const int k0 = ch * kKC, st = g % n_stages;
+            if (g >= n_stages) mbar_wait(&empty[st], ((g / n_stages) + 1) & 1);
+            uint8_t* a_op = smem + st * stage_bytes;
+            mbar_arrive_expect_tx(&full[st], bytes);
+            const int32_t cA[2] = {eb.cb + k0, eb.rb + n0};
+            tma_load<2>(a_op, &p.map_bop, &full[st], cA);
+            for (int at = 0; at < atoms; ++at) {
+              const int32_t cB[2] = {eb.ca + m0 + at * kAtomCols, eb.ra + k0};
+              tma_load<2>(a_op + kAOpBytes + at * kAtomBytes, &p.map_aop, &full[st], cB);
+            }
+          }
+        }
+      }
+    }
+  } else if (warp < kGatherWarps) {
+    // ------------------------------------------------------------ gather
+    const int gt = tid;  // 0 .. 255
+    const bool a_contig = p.b_sk == 1;   // reference b block: k contiguous
+    const bool b_contig = p.a_sm == 1;   // reference a block: m contiguous
+    int local = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
+      const int mt = t % m_tiles;
+      const int nt = (t / m_tiles) % n_tiles;
+      const int job = t / (m_tiles * n_tiles);
+      const int n0 = nt * kRows, m0 = mt * kCols;
+      const int m_here = min(kCols, p.m - m0);
+      const int n_here = min(kRows, p.n - n0);
+      const int n_cols = kTF32 ? (m_here + 15) & ~15 : (m_here + kAtomCols - 1) / kAtomCols * kAtomCols;
       const int n_rows8 = (n_here + 7) & ~7;
       const int col_chunks = n_cols / kE;
+      const int g0 = local * steps;
+      bool skip = false;
       for (int s = 0; s < steps; ++s) {
-        const int g = g0 + s, st = g % kStages;
         const int entry = s / n_chunks;
+        if (s % n_chunks == 0) skip = entry_box(job, entry).tma;
+        if (skip) continue;
+        const int g = g0 + s, st = g % n_stages;
         const int k0 = (s % n_chunks) * kKC;
         const int k_here = min(kKC, p.k - k0);
-        if (g >= kStages) mbar_wait(&empty[st], ((g / kStages) + 1) & 1);
-        uint8_t* a_op = smem + st * kStageBytes;
+        if (g >= n_stages) mbar_wait(&empty[st], ((g / n_stages) + 1) & 1);
+        uint8_t* a_op = smem + st * stage_bytes;
         uint8_t* b_op = a_op + kAOpBytes;
         const EntryPtrs e = entry_ptrs(p, job, entry);
         const size_t esz = bf16_in ? 2 : 4;
         const bool a_vec = a_contig && ((reinterpret_cast<uintptr_t>(e.b) & 15) == 0) && ((p.b_sn * esz) % 16 == 0);
         const bool b_vec = b_contig && ((reinterpret_cast<uintptr_t>(e.a) & 15) == 0) && ((p.a_sk * esz) % 16 == 0);
+        // bf16 in / bf16 MMA with 16 B-aligned contiguous rows: asynchronous copies (cp.async,
+        // zero-filled tails), so each gather thread keeps all ring stages' loads in flight
+        const bool fast_a = !kTF32 && bf16_in && a_vec;
+        const bool fast_b = !kTF32 && bf16_in && b_vec;
         // A operand (K-major) <- reference b block rows: (row r, 16 B chunk c) along k
         for (int u = gt; u < n_rows8 * 8; u += kGatherWarps * 32) {
           const int c = u & 7, r = u >> 3;
           const int kk = c * kE;
+          if (fast_a) {
+            const int bytes = r < n_here ? max(0, min(16, (k_here - kk) * 2)) : 0;
+            const char* src = bytes > 0 ? e.b + (static_cast<int64_t>(n0 + r) * p.b_sn + (k0 + kk)) * 2 : e.b;
+            cp_async16(smem_u32(a_op + r * 128 + ((c ^ (r & 7)) << 4)), src, bytes);
+            continue;
+          }
           uint4 v;
           if (r < n_here) {
             v = load_chunk<kTF32>(e.b, static_cast<int64_t>(n0 + r) * p.b_sn + static_cast<int64_t>(k0 + kk) * p.b_sk,
@@ -227,81 +341,112 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const Gener
                                 : make_uint4(0u, 0u, 0u, 0u);
             *reinterpret_cast<uint4*>(b_op + i * 128 + ((c ^ (i & 7)) << 4)) = v;
           }
-        } else
-        for (int u = gt; u < kKC * col_chunks; u += kGatherWarps * 32) {
-          const int kr = u / col_chunks, c = u - kr * col_chunks;
-          const int col = c * kE;
-          uint4 v;
-          if (kr < k_here && col < m_here) {
-            v = load_chunk<kTF32>(e.a, static_cast<int64_t>(k0 + kr) * p.a_sk + static_cast<int64_t>(m0 + col) * p.a_sm,
-                                  p.a_sm, m_here - col, bf16_in, b_vec && (m0 + col) % kE == 0);
-          } else {
-            v = make_uint4(0u, 0u, 0u, 0u);
+        } else {
+          for (int u = gt; u < kKC * col_chunks; u += kGatherWarps * 32) {
+            const int kr = u / col_chunks, c = u - kr * col_chunks;
+            const int col = c * kE;
+            const int atom = c / (kAtomCols / kE), cc = c % (kAtomCols / kE);
+            if (fast_b) {
+              const int bytes = kr < k_here ? max(0, min(16, (m_here - col) * 2)) : 0;
+              const char* src = bytes > 0 ? e.a + (static_cast<int64_t>(k0 + kr) * p.a_sk + (m0 + col)) * 2 : e.a;
+              cp_async16(smem_u32(b_op + atom * kAtomBytes + kr * 128 + ((cc ^ (kr & 7)) << 4)), src, bytes);
+              continue;
+            }
+            uint4 v;
+            if (kr < k_here && col < m_here) {
+              v = load_chunk<kTF32>(e.a,
+                                    static_cast<int64_t>(k0 + kr) * p.a_sk + static_cast<int64_t>(m0 + col) * p.a_sm,
+                                    p.a_sm, m_here - col, bf16_in, b_vec && (m0 + col) % kE == 0);
+            } else {
+              v = make_uint4(0u, 0u, 0u, 0u);
+            }
+            *reinterpret_cast<uint4*>(b_op + atom * kAtomBytes + kr * 128 + ((cc ^ (kr & 7)) << 4)) = v;
           }
-          const int atom = c / (kAtomCols / kE), cc = c % (kAtomCols / kE);
-          *reinterpret_cast<uint4*>(b_op + atom * kAtomBytes + kr * 128 + ((cc ^ (kr & 7)) << 4)) = v;
         }
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&full[st]);
+        fence_proxy_async_smem();   // this thread's st.shared -> the MMA's async-proxy reads
+        cp_async_arrive(&full[st]);  // pending +1 now, -1 when this thread's copies land
+        asm volatile("bar.sync 1, %0;" ::"r"(kGatherWarps * 32) : "memory");
+        if (gt == 0) mbar_arrive(&full[st]);  // the stage's one expected arrival
       }
-      // ---------------------------------------------------------- epilogue
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue (warps 13-16)
+    const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+    const float* bias_base = p.bias;
+    int local = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
+      const int mt = t % m_tiles;
+      const int nt = (t / m_tiles) % n_tiles;
+      const int job = t / (m_tiles * n_tiles);
+      const int n0 = nt * kRows, m0 = mt * kCols;
+      const int m_here = min(kCols, p.m - m0);
+      const int n_cols = kTF32 ? (m_here + 15) & ~15 : (m_here + kAtomCols - 1) / kAtomCols * kAtomCols;
+      const int acc = local & 1;
       if (steps > 0) {
-        mbar_wait(done, local & 1);
+        mbar_wait(&done[acc], (local >> 1) & 1);
         tc_fence_after();
       }
-      const int quarter = warp & 3, half = warp >> 2;
       const int row = n0 + quarter * 32 + lane;
       char* c_ptr = p.mode == kModeStride ? static_cast<char*>(p.c_base) + job * p.jstride_c * (p.out_bf16 ? 2 : 4)
                                           : static_cast<char*>(p.c_ptrs[job]);
-      const float* bias_row = p.bias != nullptr ? p.bias + p.bias_offs[job] : nullptr;
+      const float* bias_row = bias_base != nullptr ? bias_base + p.bias_offs[job] : nullptr;
       const char* mask_ptr = p.mask_ptrs != nullptr ? static_cast<const char*>(p.mask_ptrs[job]) : nullptr;
-      for (int c0 = half * 128; c0 < min(n_cols, half * 128 + 128); c0 += 32) {
-        uint32_t acc[32];
+      // plain fp32 output with 16 B-aligned rows: one float4 store per 4 columns
+      const bool vec_out = !p.out_bf16 && p.beta == 0.0f && bias_row == nullptr && mask_ptr == nullptr &&
+                           p.act == 0 && (p.ldc & 3) == 0 && (reinterpret_cast<uintptr_t>(c_ptr) & 15) == 0;
+      for (int c0 = 0; c0 < n_cols; c0 += 32) {
+        uint32_t accv[32];
         if (steps > 0) {
-          tmem_ld32(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + c0, acc);
+          tmem_ld32(tmem + acc * kCols + (static_cast<uint32_t>(quarter * 32) << 16) + c0, accv);
           tmem_ld_wait();
         } else {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) acc[j] = 0u;
+          for (int j = 0; j < 32; ++j) accv[j] = 0u;
         }
-        if (row < p.n) {
+        if (row < p.n && vec_out && m0 + c0 + 32 <= p.m) {
+          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(c_ptr) + static_cast<int64_t>(row) * p.ldc +
+                                                  m0 + c0);
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            dst[q] = make_float4(p.alpha * __uint_as_float(accv[4 * q]), p.alpha * __uint_as_float(accv[4 * q + 1]),
+                                 p.alpha * __uint_as_float(accv[4 * q + 2]), p.alpha * __uint_as_float(accv[4 * q + 3]));
+        } else if (row < p.n) {
 #pragma unroll 4
-          for (int j = 0; j < 32; ++j) {
-            const int col = m0 + c0 + j;
-            if (col >= p.m) continue;
-            const int64_t off = static_cast<int64_t>(row) * p.ldc + col;
-            float out = steps > 0 ? p.alpha * __uint_as_float(acc[j]) : 0.0f;
-            if (p.beta != 0.0f)
-              out += p.beta * (p.out_bf16 ? __bfloat162float(reinterpret_cast<__nv_bfloat16*>(c_ptr)[off])
-                                          : reinterpret_cast<float*>(c_ptr)[off]);
-            if (bias_row != nullptr) out += bias_row[col];
-            if (p.act == 1) {
-              out = fmaxf(out, 0.0f);
-            } else if (p.act == 2) {
-              const float ex = __expf(-fabsf(out));
-              out = out >= 0.0f ? 1.0f / (1.0f + ex) : ex / (1.0f + ex);
-            }
-            if (mask_ptr != nullptr) {
-              const float mv = p.out_bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(mask_ptr)[off])
-                                          : reinterpret_cast<const float*>(mask_ptr)[off];
-              if (!(mv > 0.0f)) out = 0.0f;
-            }
-            if (p.out_bf16) reinterpret_cast<__nv_bfloat16*>(c_ptr)[off] = __float2bfloat16_rn(out);
-            else reinterpret_cast<float*>(c_ptr)[off] = out;
+        for (int j = 0; j < 32; ++j) {
+          const int col = m0 + c0 + j;
+          if (col >= p.m) continue;
+          const int64_t off = static_cast<int64_t>(row) * p.ldc + col;
+          float out = steps > 0 ? p.alpha * __uint_as_float(accv[j]) : 0.0f;
+          if (p.beta != 0.0f)
+            out += p.beta * (p.out_bf16 ? __bfloat162float(reinterpret_cast<__nv_bfloat16*>(c_ptr)[off])
+                                        : reinterpret_cast<float*>(c_ptr)[off]);
+          if (bias_row != nullptr) out += bias_row[col];
+          if (p.act == 1) {
+            out = fmaxf(out, 0.0f);
+          } else if (p.act == 2) {
+            const float ex = __expf(-fabsf(out));
+            out = out >= 0.0f ? 1.0f / (1.0f + ex) : ex / (1.0f + ex);
           }
+          if (mask_ptr != nullptr) {
+            const float mv = p.out_bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(mask_ptr)[off])
+                                        : reinterpret_cast<const float*>(mask_ptr)[off];
+            if (!(mv > 0.0f)) out = 0.0f;
+          }
+          if (p.out_bf16) reinterpret_cast<__nv_bfloat16*>(c_ptr)[off] = __float2bfloat16_rn(out);
+          else reinterpret_cast<float*>(c_ptr)[off] = out;
+        }
         }
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(drained);
+      if (steps > 0 && lane == 0) mbar_arrive(&drained[acc]);
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == kGatherWarps) {
+  if (warp == kMmaWarp) {
     tc_fence_after();
-    tmem_dealloc(tmem, kCols);
+    tmem_dealloc(tmem, 2 * kCols);
   }
 }
 
@@ -314,13 +459,35 @@ int launch_brgemm_generic(const GenericParams& p, int compute_tf32, cudaStream_t
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = static_cast<int>(tiles < sms ? tiles : sms);
+  // TMA operand fetch: bf16 in and MMA, contiguous rows of 16 B-aligned strides, whole
+  // 64-deep K chunks, box extents that stay inside each block (no reads past a block)
+  GenericParams q = p;
+  q.tma = 0;
+  const bool rows_ok = (p.n <= kRows || p.n % kRows == 0) && p.m % kAtomColsBf16 == 0;
+  if (!compute_tf32 && p.in_bf16 && p.mode != kModeAddr && p.k % 64 == 0 && rows_ok && p.a_sm == 1 && p.b_sk == 1 &&
+      (p.a_sk * 2) % 16 == 0 && (p.b_sn * 2) % 16 == 0 && p.a_sk >= p.m && p.b_sn >= p.k &&
+      (reinterpret_cast<uintptr_t>(p.a_base) & 15) == 0 && (reinterpret_cast<uintptr_t>(p.b_base) & 15) == 0 &&
+      std::getenv("BRK_GENERIC_NO_TMA") == nullptr) {
+    q.nbox = std::min(p.n, kRows);
+    q.abox = kAtomColsBf16;
+    // the views span every row an in-bounds offset can address (the kernel reads only boxes
+    // inside blocks, so the declared extent is never dereferenced beyond them)
+    const uint64_t rows_b = std::min<uint64_t>(0x7fffffffull, (1ull << 38) / (p.b_sn * 2));
+    const uint64_t rows_a = std::min<uint64_t>(0x7fffffffull, (1ull << 38) / (p.a_sk * 2));
+    const uint64_t db[2] = {static_cast<uint64_t>(p.b_sn), rows_b}, sb[2] = {1, static_cast<uint64_t>(p.b_sn)};
+    const uint64_t da[2] = {static_cast<uint64_t>(p.a_sk), rows_a}, sa[2] = {1, static_cast<uint64_t>(p.a_sk)};
+    const uint32_t bb[2] = {64, static_cast<uint32_t>(q.nbox)}, ba[2] = {static_cast<uint32_t>(q.abox), 64};
+    if (encode_tmap(&q.map_bop, p.b_base, true, 2, db, sb, bb) == BRK_OK &&
+        encode_tmap(&q.map_aop, p.a_base, true, 2, da, sa, ba) == BRK_OK)
+      q.tma = 1;
+  }
   cudaError_t err;
   if (compute_tf32) {
     err = cudaFuncSetAttribute(brgemm_generic_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-    if (err == cudaSuccess) brgemm_generic_kernel<true><<<grid, kThreads, kSmemBytes, stream>>>(p);
+    if (err == cudaSuccess) brgemm_generic_kernel<true><<<grid, kThreads, kSmemBytes, stream>>>(q);
   } else {
     err = cudaFuncSetAttribute(brgemm_generic_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-    if (err == cudaSuccess) brgemm_generic_kernel<false><<<grid, kThreads, kSmemBytes, stream>>>(p);
+    if (err == cudaSuccess) brgemm_generic_kernel<false><<<grid, kThreads, kSmemBytes, stream>>>(q);
   }
   if (err == cudaSuccess) err = cudaGetLastError();
   if (err != cudaSuccess) return set_cuda_error(err, "brgemm_generic launch");

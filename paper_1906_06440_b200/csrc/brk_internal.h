@@ -2,6 +2,7 @@
 #pragma once
 #include <atomic>
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "../../include/brk.h"
@@ -12,6 +13,14 @@ enum EntryMode : int { kModeAddr = 0, kModeOffs = 1, kModeStride = 2 };
 
 // Parameters of one generic BRGEMM launch (see brk_brgemm_generic.cu).
 struct GenericParams {
+  // TMA path (set by launch_brgemm_generic, not by the callers): 2-d views of the
+  // reference b buffer ([rows][b_sn], box 64 k x nbox rows) and of the reference a
+  // buffer ([rows][a_sk], box abox m x 64 k), 128B swizzle.  An entry whose block
+  // start (element offset o) satisfies o % ld + extent <= ld is one box per operand
+  // at (o % ld + k0, o / ld + row0); other entries take the cp.async gather.
+  alignas(64) CUtensorMap map_bop;
+  alignas(64) CUtensorMap map_aop;
+  int tma, nbox, abox;
   int mode;    // EntryMode
   int n_jobs;  // number of independent output blocks C_j
   int m, n, k, batch;

@@ -1,0 +1,97 @@
+"""GPU parity of the TMA operand path of the generic BRGEMM (stride / offset variants, bf16).
+
+The stride and offset variants fetch an entry's blocks with one TMA box per
+operand when the block does not wrap a row of its buffer's 2-d view; the
+address variant always takes the cp.async gather.  With integer-valued inputs
+every path is exact, so the TMA results must equal the gather results bit for
+bit, and both must equal the fp64 oracle (reference brgemm.py:260-337).
+"""
+
+import numpy as np
+import pytest
+
+import brk_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_1906_06440_b200 import _lib  # noqa: E402
+
+BF16, F32, CBF16 = _lib.BRK_BF16, _lib.BRK_F32, _lib.BRK_COMPUTE_BF16
+
+
+def ints(g, *shape):
+    return torch.randint(-3, 4, shape, generator=g).float()
+
+
+def run_addr(lib, a_ptrs, b_ptrs, c, jobs, m, n, k, batch, lda, ldb):
+    c_ptrs = torch.tensor([c.data_ptr() + j * n * m * 4 for j in range(jobs)], dtype=torch.int64, device="cuda")
+    ap = torch.tensor(a_ptrs, dtype=torch.int64, device="cuda")
+    bp = torch.tensor(b_ptrs, dtype=torch.int64, device="cuda")
+    _lib.check(lib.brk_brgemm_addr(ap.data_ptr(), bp.data_ptr(), c_ptrs.data_ptr(), jobs, m, n, k, batch, lda, ldb,
+                                   m, 1.0, 0.0, BF16, F32, CBF16, None))
+    torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("m,n,k,batch,jobs", [(64, 64, 64, 16, 300), (128, 256, 128, 3, 40), (64, 100, 192, 5, 37),
+                                              (256, 128, 64, 4, 20), (192, 64, 64, 2, 9)])
+def test_stride_tma_matches_gather_and_oracle(m, n, k, batch, jobs):
+    lib = _lib.load()
+    g = torch.Generator(device="cpu").manual_seed(m + n + k)
+    a = ints(g, jobs, batch, k, m).cuda().bfloat16()
+    b = ints(g, jobs, batch, n, k).cuda().bfloat16()
+    c = torch.zeros(jobs, n, m, device="cuda")
+    _lib.check(lib.brk_brgemm_stride(a.data_ptr(), b.data_ptr(), k * m, n * k, c.data_ptr(), jobs, batch * k * m,
+                                     batch * n * k, n * m, m, n, k, batch, m, k, m, 1.0, 0.0, BF16, F32, CBF16, None))
+    torch.cuda.synchronize()
+    c2 = torch.zeros_like(c)
+    run_addr(lib, [a[j, i].data_ptr() for j in range(jobs) for i in range(batch)],
+             [b[j, i].data_ptr() for j in range(jobs) for i in range(batch)], c2, jobs, m, n, k, batch, m, k)
+    assert torch.equal(c, c2)
+    for j in (0, jobs // 2, jobs - 1):
+        ref = orc.brgemm_reference(list(a[j].float().cpu().numpy()), list(b[j].float().cpu().numpy()),
+                                   np.zeros((n, m), np.float32), 1.0, 0.0)
+        assert np.array_equal(c[j].cpu().numpy(), ref)
+
+
+def test_offset_tma_with_wrapping_blocks():
+    """Blocks carved out of wider matrices at arbitrary (8-aligned) offsets: entries whose
+    block wraps a row of the 2-d view take the gather, the rest TMA — same bits as the
+    address variant."""
+    lib = _lib.load()
+    m, n, k, batch, jobs = 64, 64, 128, 6, 24
+    lda, ldb = 3 * m + 8, 2 * k + 24  # row strides of the buffers the blocks live in
+    g = torch.Generator(device="cpu").manual_seed(11)
+    rows_a, rows_b = 4 * k, 4 * n
+    a = ints(g, rows_a * lda).cuda().bfloat16()
+    b = ints(g, rows_b * ldb).cuda().bfloat16()
+    rng = np.random.default_rng(5)
+    a_off = []
+    b_off = []
+    for _ in range(jobs * batch):
+        ra, ca = rng.integers(0, rows_a - k), int(rng.integers(0, (lda - 8) // 8)) * 8  # some wrap: ca + m > lda
+        rb, cb = rng.integers(0, rows_b - n), int(rng.integers(0, (ldb - 8) // 8)) * 8
+        a_off.append(min(int(ra * lda + ca), a.numel() - (k - 1) * lda - m))
+        b_off.append(min(int(rb * ldb + cb), b.numel() - (n - 1) * ldb - k))
+    wraps = sum((o % lda) + m > lda for o in a_off) + sum((o % ldb) + k > ldb for o in b_off)
+    assert 0 < wraps < 2 * jobs * batch
+    c = torch.zeros(jobs, n, m, device="cuda")
+    c_ptrs = torch.tensor([c[j].data_ptr() for j in range(jobs)], dtype=torch.int64, device="cuda")
+    ao = torch.tensor(a_off, dtype=torch.int64, device="cuda")
+    bo = torch.tensor(b_off, dtype=torch.int64, device="cuda")
+    _lib.check(lib.brk_brgemm_offs(a.data_ptr(), b.data_ptr(), ao.data_ptr(), bo.data_ptr(), c_ptrs.data_ptr(), jobs,
+                                   m, n, k, batch, lda, ldb, m, 1.0, 0.0, BF16, F32, CBF16, None))
+    torch.cuda.synchronize()
+    c2 = torch.zeros_like(c)
+    run_addr(lib, [a.data_ptr() + 2 * o for o in a_off], [b.data_ptr() + 2 * o for o in b_off], c2, jobs, m, n, k,
+             batch, lda, ldb)
+    assert torch.equal(c, c2)
+    a_np, b_np = a.float().cpu().numpy(), b.float().cpu().numpy()
+    for j in (0, jobs - 1):
+        ab = [np.lib.stride_tricks.as_strided(a_np[a_off[j * batch + i]:], (k, m), (lda * 4, 4)) for i in range(batch)]
+        bb = [np.lib.stride_tricks.as_strided(b_np[b_off[j * batch + i]:], (n, k), (ldb * 4, 4)) for i in range(batch)]
+        ref = orc.brgemm_reference(ab, bb, np.zeros((n, m), np.float32), 1.0, 0.0)
+        assert np.array_equal(c[j].cpu().numpy(), ref)
