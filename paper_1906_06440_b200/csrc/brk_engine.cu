@@ -459,17 +459,16 @@ __device__ __forceinline__ void epilogue_flush(const EpiView& p, uint32_t stage,
   // the sum of the features, not their product, so the epilogue stays in the
   // instruction cache.
   float cs[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  // masks as packed bf16x2 ops (v * (m > 0): exact, one compare + one multiply per pair —
+  // a quarter of the unpack / select / repack code, which is fetched cold once per SM)
+  const __nv_bfloat162 zero2 = __float2bfloat162_rn(0.0f);
   if (kFull && p.out_bf16 && p.mask != nullptr) {
 #pragma unroll
     for (int i = 0; i < kLanes; ++i) {
       __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&v[i]);
       const __nv_bfloat162* mh = reinterpret_cast<const __nv_bfloat162*>(&ld[i]);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float2 m2 = __bfloat1622float2(mh[j]);
-        const float2 v2 = __bfloat1622float2(h[j]);
-        h[j] = __floats2bfloat162_rn(m2.x > 0.0f ? v2.x : 0.0f, m2.y > 0.0f ? v2.y : 0.0f);
-      }
+      for (int j = 0; j < 4; ++j) h[j] = __hmul2(h[j], __hgt2(mh[j], zero2));
     }
   }
 #pragma unroll
@@ -481,11 +480,7 @@ __device__ __forceinline__ void epilogue_flush(const EpiView& p, uint32_t stage,
       const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v[i]);
       __nv_bfloat162* ah = reinterpret_cast<__nv_bfloat162*>(&ld[i]);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float2 y2 = __bfloat1622float2(h[j]);
-        const float2 a2 = __bfloat1622float2(ah[j]);
-        ah[j] = __floats2bfloat162_rn(y2.x > 0.0f ? a2.x : 0.0f, y2.y > 0.0f ? a2.y : 0.0f);
-      }
+      for (int j = 0; j < 4; ++j) ah[j] = __hmul2(ah[j], __hgt2(h[j], zero2));
       if (okr[i]) *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.aux_out) + eo[i]) = ld[i];
       v[i] = ld[i];  // column sums of the gradient
     }

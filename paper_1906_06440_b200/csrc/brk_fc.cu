@@ -452,6 +452,7 @@ BRK_API int brk_mlp_step(int L, int N, int C, const void* const* y, void* const*
     return r;
   };
   int fwd_of[8], bwd_of[8], upd_of[8];
+  for (int i = 0; i < 8; ++i) fwd_of[i] = bwd_of[i] = upd_of[i] = -1;
   for (int l = 0; l < L && !rc; ++l) {  // forward: y[l+1] = relu(W_l y[l] + b_l)
     rc = capture([&] {
       return brk_fc_fwd(y[l], w[l], bias[l], const_cast<void*>(y[l + 1]), N, C, C, kB, kB, kB, kActRelu, BRK_BF16,
@@ -472,6 +473,7 @@ BRK_API int brk_mlp_step(int L, int N, int C, const void* const* y, void* const*
   }
   auto add_bwd = [&](int l) {  // layer l (weights w[l-1]): bwd-data
     const int dz_src = l == L ? fwd_of[L - 1] : bwd_of[l + 1];
+    if (dz_src < 0 || bwd_of[l] >= 0) { rc = set_error(BRK_ERR_CONTRACT, "mlp_step: unit order breaks a dependency"); return; }
     rc = capture([&] {
       return brk_fc_bwd_data(dz[l], w[l - 1], l > 1 ? y[l - 1] : nullptr, dz[l - 1], l > 1 ? colsum[l - 1] : nullptr,
                              N, C, C, kB, kB, kB, BRK_BF16, stream);
@@ -483,6 +485,10 @@ BRK_API int brk_mlp_step(int L, int N, int C, const void* const* y, void* const*
   };
   auto add_upd = [&](int l) {  // layer l: weight update (+ fused SGD)
     const int dz_src = l == L ? fwd_of[L - 1] : bwd_of[l + 1];
+    if (dz_src < 0 || upd_of[l] >= 0 || (lr != 0.0f && w_next == nullptr && bwd_of[l] < 0)) {
+      rc = set_error(BRK_ERR_CONTRACT, "mlp_step: unit order breaks a dependency");
+      return;
+    }
     // lr == 0: gradients only (data parallel: all-reduce, then SGD outside the step)
     const bool sgd = lr != 0.0f;
     void* w_out = !sgd ? nullptr : (w_next != nullptr ? w_next[l - 1] : w[l - 1]);
@@ -503,11 +509,26 @@ BRK_API int brk_mlp_step(int L, int N, int C, const void* const* y, void* const*
   // Work-unit order (CTA pairs take units round-robin and run them in order): the weight
   // update of layer l is placed after the bwd-data pass of layer l - lag, so the units of the
   // bwd-data chain (the critical path) are not queued behind the longer weight-update units.
+  // BRK_MLP_ORDER (tuning): the backward units as a string of (kind, layer) pairs, e.g.
+  // "b4b3u4b2u3u2u1b1"; every bwd-data (b) and weight update (u) exactly once, each after
+  // the units it reads.
   const char* lag_env = std::getenv("BRK_MLP_UPD_LAG");
-  const int lag = lag_env ? std::max(0, std::atoi(lag_env)) : 1;
-  for (int l = L; l >= 1 - lag && !rc; --l) {
-    if (l >= 1) add_bwd(l);
-    if (!rc && l + lag <= L && l + lag >= 1) add_upd(l + lag);
+  const char* order_env = std::getenv("BRK_MLP_ORDER");
+  if (order_env != nullptr) {
+    int n = 0;
+    for (const char* c = order_env; c[0] && c[1] && !rc; c += 2, ++n) {
+      const int l = c[1] - '0';
+      if (l < 1 || l > L || (c[0] != 'b' && c[0] != 'u')) rc = set_error(BRK_ERR_CONTRACT, "mlp_step: bad BRK_MLP_ORDER");
+      else if (c[0] == 'b') add_bwd(l);
+      else add_upd(l);
+    }
+    if (!rc && n != 2 * L) rc = set_error(BRK_ERR_CONTRACT, "mlp_step: BRK_MLP_ORDER must list 2L units");
+  } else {
+    const int lag = lag_env ? std::max(0, std::atoi(lag_env)) : 1;
+    for (int l = L; l >= 1 - lag && !rc; --l) {
+      if (l >= 1) add_bwd(l);
+      if (!rc && l + lag <= L && l + lag >= 1) add_upd(l + lag);
+    }
   }
   g_force_plan = nullptr;
   (void)upd_of;

@@ -29,11 +29,15 @@ n_units = 74
 import os
 lag = int(os.environ.get("BRK_MLP_UPD_LAG", "1"))
 names = ["fwd1", "fwd2", "fwd3", "fwd4"]
-for l in range(4, -lag, -1):
-    if l >= 1:
-        names.append(f"bwd{l}")
-    if 1 <= l + lag <= 4:
-        names.append(f"upd{l + lag}")
+order = os.environ.get("BRK_MLP_ORDER")
+if order:
+    names += [("bwd" if order[i] == "b" else "upd") + order[i + 1] for i in range(0, len(order), 2)]
+else:
+    for l in range(4, -lag, -1):
+        if l >= 1:
+            names.append(f"bwd{l}")
+        if 1 <= l + lag <= 4:
+            names.append(f"upd{l + lag}")
 sizes = [32 if n.startswith("upd") else 64 for n in names]
 begin = np.cumsum([0] + sizes)
 rows = []

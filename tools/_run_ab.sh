@@ -1,9 +1,5 @@
-timeout 300 python -m pytest tests/test_gpu_brgemm_tma.py tests/test_gpu_brgemm.py -x -q 2>&1 | tail -15
-timeout 300 python - <<'PY'
-import sys, json
-sys.path.insert(0, '.'); sys.path.insert(0, 'tools')
-import suites
-r = suites.brgemm_suite(ms=(32, 64, 128, 256), batches=(1, 16, 64), variants=("stride", "offset", "address"))
-for p in r["points"]:
-    print(p["m"], p["batch"], p["variant"], p["jobs"], round(p["us"], 1), round(p["tflops"], 2), round(p["roof_frac"], 3), p["bound"])
-PY
+J='import json,sys; d=json.loads(sys.stdin.read()); print(d["value"], d["ms_per_step"])'
+for o in b4b3u4b2u3b1u2u1 b4b3u4b2u3u2u1b1 b4b3u4b2u3u1u2b1 b4u4b3b2u3u1b1u2 b4b3u4b2u1u3u2b1 b4b3b2u4u1u3b1u2 b4b3u4b2u3u1b1u2; do
+  echo -n "$o "; BRK_MLP_ORDER=$o python bench.py --steps 100 --warmup 5 2>&1 | tail -1 | python -c "$J"
+done
+BRK_MLP_ORDER=b4b3u4b2u3u1b1u2 python tools/_probe_mlp_ts.py 2>&1 | tail -8
