@@ -95,3 +95,31 @@ def test_offset_tma_with_wrapping_blocks():
         bb = [np.lib.stride_tricks.as_strided(b_np[b_off[j * batch + i]:], (n, k), (ldb * 4, 4)) for i in range(batch)]
         ref = orc.brgemm_reference(ab, bb, np.zeros((n, m), np.float32), 1.0, 0.0)
         assert np.array_equal(c[j].cpu().numpy(), ref)
+
+
+def test_python_address_api_routes_one_storage_lists_to_offsets():
+    """brgemm() with block lists from one allocation runs as the offset variant (TMA for
+    aligned blocks); lists spanning allocations keep the address variant — same bits."""
+    from paper_1906_06440_b200 import BrgemmSpec, brgemm, brgemm_strided
+
+    g = torch.Generator(device="cpu").manual_seed(21)
+    m, n, k, batch = 128, 64, 128, 8
+    a = ints(g, batch, k, m).cuda().bfloat16()
+    b = ints(g, batch, n, k).cuda().bfloat16()
+    spec = BrgemmSpec(m=m, n=n, k=k, batch=batch, beta=0.0)
+    c1 = torch.zeros(n, m, device="cuda")
+    brgemm(list(a), list(b), c1, spec)  # one storage per operand -> offsets (reversed order below too)
+    c2 = torch.zeros(n, m, device="cuda")
+    brgemm_strided(a, b, k * m, n * k, c2, spec)
+    assert torch.equal(c1, c2)
+    c3 = torch.zeros(n, m, device="cuda")
+    brgemm([x.clone() for x in a], [y.clone() for y in b], c3, spec)  # separate allocations -> addresses
+    assert torch.equal(c1, c3)
+    ref = orc.brgemm_reference(list(a.float().cpu().numpy()), list(b.float().cpu().numpy()),
+                               np.zeros((n, m), np.float32), 1.0, 0.0)
+    assert np.array_equal(c1.cpu().numpy(), ref)
+    c4 = torch.zeros(n, m, device="cuda")
+    brgemm(list(a)[::-1], list(b)[::-1], c4, spec)  # offsets need not be ordered
+    ref4 = orc.brgemm_reference(list(a.float().cpu().numpy())[::-1], list(b.float().cpu().numpy())[::-1],
+                                np.zeros((n, m), np.float32), 1.0, 0.0)
+    assert np.array_equal(c4.cpu().numpy(), ref4)
