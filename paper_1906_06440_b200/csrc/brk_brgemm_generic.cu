@@ -187,6 +187,12 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
   auto entry_box = [&](int job, int entry) -> EntryBox {
     EntryBox eb{false, 0, 0, 0, 0};
     if (kTF32 || !p.tma) return eb;
+    if (p.all_tma) {
+      eb.tma = true;
+      eb.ra = static_cast<int32_t>(job * p.rj_a + entry * p.rs_a);
+      eb.rb = static_cast<int32_t>(job * p.rj_b + entry * p.rs_b);
+      return eb;
+    }
     int64_t oa, ob;
     entry_offs(p, job, entry, oa, ob);
     int64_t qa, qb;
@@ -279,7 +285,7 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
     const bool a_contig = p.b_sk == 1;   // reference b block: k contiguous
     const bool b_contig = p.a_sm == 1;   // reference a block: m contiguous
     int local = 0;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
+    for (int t = p.all_tma && !kTF32 ? tiles : blockIdx.x; t < tiles; t += gridDim.x, ++local) {
       const int mt = t % m_tiles;
       const int nt = (t / m_tiles) % n_tiles;
       const int job = t / (m_tiles * n_tiles);
@@ -480,6 +486,17 @@ int launch_brgemm_generic(const GenericParams& p, int compute_tf32, cudaStream_t
     if (encode_tmap(&q.map_bop, p.b_base, true, 2, db, sb, bb) == BRK_OK &&
         encode_tmap(&q.map_aop, p.a_base, true, 2, da, sa, ba) == BRK_OK)
       q.tma = 1;
+    q.all_tma = 0;
+    if (q.tma && p.mode == kModeStride && p.stride_a % p.a_sk == 0 && p.jstride_a % p.a_sk == 0 &&
+        p.stride_b % p.b_sn == 0 && p.jstride_b % p.b_sn == 0 &&
+        static_cast<int64_t>(p.n_jobs) * (p.jstride_a / p.a_sk + p.batch * (p.stride_a / p.a_sk)) < (1ll << 31) &&
+        static_cast<int64_t>(p.n_jobs) * (p.jstride_b / p.b_sn + p.batch * (p.stride_b / p.b_sn)) < (1ll << 31)) {
+      q.all_tma = 1;
+      q.rs_a = p.stride_a / p.a_sk;
+      q.rj_a = p.jstride_a / p.a_sk;
+      q.rs_b = p.stride_b / p.b_sn;
+      q.rj_b = p.jstride_b / p.b_sn;
+    }
   }
   cudaError_t err;
   if (compute_tf32) {

@@ -21,6 +21,10 @@ struct GenericParams {
   alignas(64) CUtensorMap map_bop;
   alignas(64) CUtensorMap map_aop;
   int tma, nbox, abox;
+  // stride variant whose block starts all sit at column 0 of the views: every entry is one
+  // box per operand at view row job * rj + i * rs (no per-entry division, no gather work)
+  int all_tma;
+  int64_t rs_a, rj_a, rs_b, rj_b;
   int mode;    // EntryMode
   int n_jobs;  // number of independent output blocks C_j
   int m, n, k, batch;

@@ -1,6 +1,9 @@
-J='import json,sys; d=json.loads(sys.stdin.read()); print(d["value"], d["ms_per_step"])'
-python -m pytest tests/test_gpu_mlp.py -x -q 2>&1 | tail -2
-for i in 1 2; do
-for w in 0 1; do echo -n "whole=$w "; BRK_MLP_UPD_WHOLE=$w python bench.py --steps 100 --warmup 5 2>&1 | tail -1 | python -c "$J"; done
-done
-python tools/_probe_mlp_ts.py 2>&1 | tail -8
+python -m pytest tests/test_gpu_brgemm_tma.py tests/test_gpu_brgemm.py -x -q 2>&1 | tail -2
+timeout 300 python - <<'PY'
+import sys
+sys.path.insert(0, '.'); sys.path.insert(0, 'tools')
+import suites
+r = suites.brgemm_suite(ms=(64, 128, 256), batches=(1, 16, 64), variants=("stride", "offset"))
+for p in r["points"]:
+    print(p["m"], p["batch"], p["variant"], p["jobs"], round(p["us"], 1), round(p["tflops"], 2), round(p["roof_frac"], 3))
+PY
