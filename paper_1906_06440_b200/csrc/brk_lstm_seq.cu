@@ -79,6 +79,19 @@ __device__ __forceinline__ float tanh_f(float x) {
   return 1.0f - __fdividef(2.0f, e + 1.0f);
 }
 
+// release counters: one per 128 B line (pollers of different chunks hit different L2 lines),
+// polled with a short back-off (the MLP step measured polling pressure on shared lines)
+#ifndef BRK_LSTM_FLAG_STRIDE
+#define BRK_LSTM_FLAG_STRIDE 32
+#endif
+#ifndef BRK_LSTM_POLL_NS
+#define BRK_LSTM_POLL_NS 64
+#endif
+constexpr int kFlagStride = BRK_LSTM_FLAG_STRIDE;
+__device__ __forceinline__ void poll_backoff() {
+  if (BRK_LSTM_POLL_NS > 0) __nanosleep(BRK_LSTM_POLL_NS);
+}
+
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -190,8 +203,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_fwd_kernel(const __grid
         const int t = gi / KC, kc = gi - t * KC;
         const uint32_t ph = (gi / kStagesS) & 1;
         if (t > 0) {
-          while (ld_acquire(&p.flags[kc]) < static_cast<unsigned>(chunk_owners * t)) {
-          }
+          while (ld_acquire(&p.flags[kc * kFlagStride]) < static_cast<unsigned>(chunk_owners * t)) poll_backoff();
           fence_proxy_async_global();
         }
         if (kc == 0) SEQ_TS(t, 0);       // chunk 0 of h_{t-1} released
@@ -294,7 +306,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_fwd_kernel(const __grid
       if (threadIdx.x == 0) {
         SEQ_TS(t, 5);  // epilogue done
         __threadfence();
-        atomicAdd(&p.flags[j0 / 64], 1u);
+        atomicAdd(&p.flags[(j0 / 64) * kFlagStride], 1u);
       }
       // off the critical path: fp32 h, s and the activated gates (BPTT inputs)
 #pragma unroll
@@ -384,8 +396,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_bwd_kernel(const __grid
         const int it = gi / KC, kc = gi - it * KC;
         const int tsrc = p.T - 1 - it;  // dpre slot read by this iteration
         const int fidx = g * KC + kc;
-        while (ld_acquire(&p.flags[fidx]) < static_cast<unsigned>(chunk_owners * (it + 1))) {
-        }
+        while (ld_acquire(&p.flags[fidx * kFlagStride]) < static_cast<unsigned>(chunk_owners * (it + 1))) poll_backoff();
         fence_proxy_async_global();
         if (kc == 0) SEQ_TS(it, 0);
         if (kc == KC - 1) SEQ_TS(it, 1);
@@ -562,7 +573,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_bwd_kernel(const __grid
         __threadfence();
         // this CTA wrote rows of its quarter for units u0..u0+31 of all four gates
 #pragma unroll
-        for (int gg = 0; gg < 4; ++gg) atomicAdd(&p.flags[(gg * p.K + u0) / 64], 1u);
+        for (int gg = 0; gg < 4; ++gg) atomicAdd(&p.flags[((gg * p.K + u0) / 64) * kFlagStride], 1u);
       }
       if (t < p.T - 1) {
         __syncwarp();
@@ -612,7 +623,9 @@ extern "C" {
 // Diagnostic: subsequent sequence launches record per-step %globaltimer stamps of CTA 0 ([T][8]); NULL disables.
 BRK_API void brk_diag_lstm_timestamps(unsigned long long* ts) { g_seq_ts = ts; }
 
-BRK_API size_t brk_lstm_seq_flags_bytes(int K) { return static_cast<size_t>(4 * (K / 64) + 4) * sizeof(unsigned); }
+BRK_API size_t brk_lstm_seq_flags_bytes(int K) {
+  return static_cast<size_t>(4 * (K / 64) + 4) * kFlagStride * sizeof(unsigned);
+}
 
 BRK_API int brk_lstm_seq_fwd(const float* gx, const void* r_cat, const float* s0, void* h_bf, float* h_out,
                              float* s_out, float* gates_out, unsigned* flags, int T, int N, int K, void* stream) {

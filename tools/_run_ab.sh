@@ -1,9 +1,6 @@
-python -m pytest tests/test_gpu_brgemm_tma.py tests/test_gpu_brgemm.py -x -q 2>&1 | tail -2
-timeout 300 python - <<'PY'
-import sys
-sys.path.insert(0, '.'); sys.path.insert(0, 'tools')
-import suites
-r = suites.brgemm_suite(ms=(64, 128, 256), batches=(1, 16, 64), variants=("stride", "offset"))
-for p in r["points"]:
-    print(p["m"], p["batch"], p["variant"], p["jobs"], round(p["us"], 1), round(p["tflops"], 2), round(p["roof_frac"], 3))
-PY
+P='import sys; sys.path.insert(0, "."); sys.path.insert(0, "tools"); import suites; r = suites.lstm_suite(iters=5); print(round(r["fwd"]["tflops"],1), round(r["bwd_upd"]["tflops"],1), round(r["all"]["tflops"],1))'
+python -m pytest tests/test_gpu_lstm.py -x -q 2>&1 | tail -2
+for i in 1 2; do
+  echo -n "new "; python -c "$P" 2>&1 | tail -1
+  for v in O S B L; do echo -n "$v "; (cd _v/$v && python -c "$P" 2>&1 | tail -1); done
+done
