@@ -20,6 +20,7 @@
 //            distributed shared memory and each CTA of the cluster finishes
 //            the BPTT element math for a quarter of the minibatch rows.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <cuda_bf16.h>
 
@@ -55,6 +56,7 @@ struct SeqParams {
   float* ds0;            // [N][K] dL/ds_{-1}
   unsigned* flags;       // per 64-column chunk release counters (zeroed by the host)
   unsigned long long* ts;  // diagnostics: per-step %globaltimer stamps of CTA 0 [T][8] (or null)
+  int slice;               // forward: rows of h each cluster CTA loads and multicasts (multiple of 8)
 };
 
 __device__ __forceinline__ unsigned long long gtime() {
@@ -171,7 +173,9 @@ __global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_fwd_kernel(const __grid
   const int cs = static_cast<int>(cluster_nctas());
   const int crank = static_cast<int>(cluster_ctarank());
   const uint16_t cmask = static_cast<uint16_t>((1u << cs) - 1u);
-  const int slice = 256 / cs;
+  // only the N valid rows (rounded to 8-row swizzle groups per CTA) are streamed, not the
+  // whole 256-row tile: the chunk stream is bound by each SM's L2 ingress bandwidth
+  const int slice = p.slice;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStagesS; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], cs); }
@@ -209,7 +213,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_fwd_kernel(const __grid
         if (kc == 0) SEQ_TS(t, 0);       // chunk 0 of h_{t-1} released
         if (kc == KC - 1) SEQ_TS(t, 1);  // last chunk released
         mbar_wait(&empty[pid], ph ^ 1);  // every CTA of the cluster consumed this stage
-        mbar_arrive_expect_tx(&full[pid], kStageBytesS);
+        mbar_arrive_expect_tx(&full[pid], static_cast<uint32_t>(slice * cs * 128));
         tma_load3_mc(ring + pid * kStageBytesS + crank * slice * 128, &p.map_a, &full[pid], kc * 64, crank * slice,
                      t, cmask);
       }
@@ -670,7 +674,9 @@ BRK_API int brk_lstm_seq_fwd(const float* gx, const void* r_cat, const float* s0
   {
     const uint64_t dims[3] = {(uint64_t)K, (uint64_t)N, (uint64_t)(T + 1)};
     const uint64_t strides[3] = {1, (uint64_t)K, (uint64_t)N * K};
-    const uint32_t box[3] = {64, (uint32_t)(256 / cs), 1};
+    const char* full_env = std::getenv("BRK_LSTM_FULL_TILE");  // diagnostics: stream all 256 rows
+    p.slice = (full_env != nullptr && std::atoi(full_env) != 0) ? 256 / cs : ((N + cs - 1) / cs + 7) / 8 * 8;
+    const uint32_t box[3] = {64, static_cast<uint32_t>(p.slice), 1};
     if ((rc = encode_tmap(&p.map_a, h_bf, true, 3, dims, strides, box))) return rc;
   }
   {
