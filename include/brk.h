@@ -195,6 +195,14 @@ BRK_API int brk_conv_upd(const void* in, const void* dout, float* dw, void* w_sg
 BRK_API size_t brk_conv_upd_workspace(int N, int C, int K, int H, int W, int R, int S, int stride, int pad_h,
                                       int pad_w);
 /* Diagnostic: engine tile plan of a pass (0 fwd, 1 bwd-data, 2 upd) -> out3 = {pair, bn, splits}. */
+/* Small-channel convolutions (C < 64, e.g. the 3-channel stem; reference cnn.py:201-334 with
+ * b_c = C): explicit im2col + brk_gemm_dense.  col[(n,p,q)][(r*S+s)*C+c] (bf16, row stride ldcol,
+ * a multiple of 8 >= R*S*C, zero outside the image; columns past R*S*C are left as they are) from the blocked input
+ * [N][C_b][H][W][b_c]; col2im sums dcol back onto the input pixels (gather, fp32, deterministic). */
+BRK_API int brk_conv_im2col(const void* in, void* col, int N, int C, int H, int W, int R, int S, int stride,
+                            int pad_h, int pad_w, int b_c, int64_t ldcol, void* stream);
+BRK_API int brk_conv_col2im(const void* dcol, void* dx, int N, int C, int H, int W, int R, int S, int stride,
+                            int pad_h, int pad_w, int b_c, int64_t ldcol, void* stream);
 BRK_API int brk_conv_plan(int pass, int N, int C, int K, int H, int W, int R, int S, int stride, int pad_h,
                           int pad_w, int* out3);
 

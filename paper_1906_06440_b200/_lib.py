@@ -66,6 +66,8 @@ SIGNATURES: dict[str, tuple] = {
     "brk_conv_upd": (_c_int, [_vp, _vp, _vp, _vp, _c_f, _vp, ctypes.c_size_t] + [_c_int] * 13 + [_vp]),
     "brk_conv_upd_workspace": (ctypes.c_size_t, [_c_int] * 10),
     "brk_conv_plan": (_c_int, [_c_int] * 11 + [ctypes.POINTER(_c_int)]),
+    "brk_conv_im2col": (_c_int, [_vp, _vp] + [_c_int] * 10 + [_c_i64, _vp]),
+    "brk_conv_col2im": (_c_int, [_vp, _vp] + [_c_int] * 10 + [_c_i64, _vp]),
     "brk_gemm_dense": (_c_int, [_vp, _c_i64, _c_int, _vp, _c_i64, _c_int, _vp, _c_i64, _c_int, _c_i64, _c_int,
                                 _c_int, _c_f, _c_f, _vp, _c_int, _vp, ctypes.c_size_t, _vp]),
     "brk_gemm_dense_workspace": (ctypes.c_size_t, [_c_i64, _c_int, _c_int]),

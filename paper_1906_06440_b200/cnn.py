@@ -223,6 +223,36 @@ def _engine_ok(spec: "ConvSpec", dt, pass_: str, engine: bool | None) -> bool:
     return ok
 
 
+def _small_ok(spec: "ConvSpec", dt, engine: bool | None) -> bool:
+    """Small-channel convs (the 3-channel ResNet stem): explicit im2col + the dense
+    tcgen05 GEMM (brk_conv_im2col / brk_gemm_dense / brk_conv_col2im) instead of a
+    64-channel im2col box that would be almost all padding.  bf16, K = 64."""
+    torch = require_cuda()
+    if engine is False or os.environ.get("BRK_CONV_ENGINE", "1") == "0":
+        return False
+    return dt == torch.bfloat16 and spec.c < 64 and spec.k == 64 and spec.b_k == 64
+
+
+def _small_weights(spec: "ConvSpec", w):
+    """W2[k][(r, s, c)] (bf16, columns padded to a multiple of 64) from [1][C_b][R][S][b_c][64]."""
+    torch = require_cuda()
+    rsc = spec.r * spec.s * spec.c
+    ld = -(-rsc // 64) * 64
+    w2 = torch.zeros((64, ld), dtype=torch.bfloat16, device="cuda")
+    w2[:, :rsc] = w.permute(0, 2, 3, 1, 4, 5).reshape(rsc, 64).t()
+    return w2, rsc, ld
+
+
+def _small_im2col(spec: "ConvSpec", x, ld: int):
+    torch = require_cuda()
+    pix = spec.n * spec.out_h * spec.out_w
+    col = torch.empty((pix, ld), dtype=torch.bfloat16, device="cuda")
+    _lib.check(_lib.load().brk_conv_im2col(x.data_ptr(), col.data_ptr(), spec.n, spec.c, spec.h, spec.w, spec.r,
+                                           spec.s, spec.stride, spec.pad_h, spec.pad_w, spec.b_c, ld, stream_ptr()),
+               LayoutError)
+    return col
+
+
 def _geom(spec: "ConvSpec"):
     return (spec.n, spec.c, spec.k, spec.h, spec.w, spec.r, spec.s, spec.stride, spec.pad_h, spec.pad_w)
 
@@ -271,6 +301,15 @@ def conv2d_forward(spec: ConvSpec, inp: BlockedTensor, wgt: BlockedTensor, strat
     torch = require_cuda()
     host = not inp.on_device
     prec, dt = _dtype(precision, inp, wgt)
+    if _small_ok(spec, dt, engine):
+        from ._dense import gemm
+        x, w = _stage(inp, dt), _stage(wgt, dt)
+        w2, rsc, ld = _small_weights(spec, w)
+        col = _small_im2col(spec, x, ld)
+        out = torch.empty((spec.n, 1, spec.out_h, spec.out_w, 64), dtype=dt, device="cuda")
+        gemm(col[:, :rsc], w2[:, :rsc], out.view(-1, 64))
+        res = BlockedTensor(out, n_outer=4, logical_dims={"n": 0, "k": (1, 4), "p": 2, "q": 3})
+        return res.to("cpu") if host else res
     if _engine_ok(spec, dt, "fwd", engine):
         x, w = _stage(inp, dt), _stage(wgt, dt)
         out = torch.empty((spec.n, spec.k_blocks, spec.out_h, spec.out_w, spec.b_k), dtype=dt, device="cuda")
@@ -319,6 +358,18 @@ def conv2d_backward_data(spec: ConvSpec, dout: BlockedTensor, wgt: BlockedTensor
     prec, dt = _dtype(precision, dout, wgt)
     do = _stage(dout, dt)
     w = _stage(wgt, dt)
+    if _small_ok(spec, dt, engine):
+        from ._dense import gemm
+        w2, rsc, ld = _small_weights(spec, w)
+        pix = spec.n * spec.out_h * spec.out_w
+        dcol = torch.empty((pix, ld), dtype=dt, device="cuda")
+        gemm(do.reshape(pix, 64), w2, dcol, b_t=True)  # dcol[pix][(r,s,c)] = dO[pix] . W[:, (r,s,c)]
+        din = torch.empty((spec.n, spec.c_blocks, spec.h, spec.w, spec.b_c), dtype=dt, device="cuda")
+        _lib.check(_lib.load().brk_conv_col2im(dcol.data_ptr(), din.data_ptr(), spec.n, spec.c, spec.h, spec.w,
+                                               spec.r, spec.s, spec.stride, spec.pad_h, spec.pad_w, spec.b_c, ld,
+                                               stream_ptr()), LayoutError)
+        res = BlockedTensor(din, n_outer=4, logical_dims={"n": 0, "c": (1, 4), "h": 2, "w": 3})
+        return res.to("cpu") if host else res
     if _engine_ok(spec, dt, "bwd", engine):
         din = torch.empty((spec.n, spec.c_blocks, spec.h, spec.w, spec.b_c), dtype=dt, device="cuda")
         _lib.check(_lib.load().brk_conv_bwd_data(do.data_ptr(), w.data_ptr(), din.data_ptr(), *_geom(spec), 64, 64,
@@ -383,6 +434,19 @@ def conv2d_weight_update(spec: ConvSpec, inp: BlockedTensor, dout: BlockedTensor
     torch = require_cuda()
     host = not inp.on_device
     prec, dt = _dtype(precision, inp, dout)
+    if _small_ok(spec, dt, engine):
+        from ._dense import gemm
+        x, do = _stage(inp, dt), _stage(dout, dt)
+        rsc = spec.r * spec.s * spec.c
+        ld = -(-rsc // 64) * 64
+        col = _small_im2col(spec, x, ld)
+        pix = spec.n * spec.out_h * spec.out_w
+        dwt = torch.empty((rsc, 64), dtype=torch.float32, device="cuda")
+        gemm(col[:, :rsc], do.reshape(pix, 64), dwt, a_t=True, b_t=True)  # reduction over all pixels in TMEM
+        dw = (dwt.reshape(spec.r, spec.s, spec.c_blocks, spec.b_c, 64).permute(2, 0, 1, 3, 4)
+              .unsqueeze(0).contiguous())
+        res = BlockedTensor(dw, n_outer=4, logical_dims={"k": (0, 5), "c": (1, 4), "r": 2, "s": 3})
+        return res.to("cpu") if host else res
     if _engine_ok(spec, dt, "upd", engine):
         x, do = _stage(inp, dt), _stage(dout, dt)
         dw = torch.empty((spec.k_blocks, spec.c_blocks, spec.r, spec.s, spec.b_c, spec.b_k), dtype=torch.float32,

@@ -91,6 +91,7 @@ def resnet_suite(n=256, iters=10, layers=None, passes=("fwd", "bwd", "upd"), ver
     timer = _Timer(torch)
     rows = []
     tot = {p: [0.0, 0.0, 0.0] for p in passes}  # sum n_i F_i, sum n_i t_i, sum n_i t_roof
+    tot_engine = {p: [0.0, 0.0, 0.0] for p in passes}  # the same over the implicit-GEMM engine layers
     g = torch.Generator(device="cuda").manual_seed(0)
     for lid, c, k, h, w, r, s, st, cnt in RESNET50_ROWS:
         if layers and lid not in layers:
@@ -129,8 +130,9 @@ def resnet_suite(n=256, iters=10, layers=None, passes=("fwd", "bwd", "upd"), ver
             wi = BlockedTensor(wt, 4, {"k": (0, 5), "c": (1, 4), "r": 2, "s": 3})
             do = BlockedTensor(dout, 4, {"n": 0, "k": (1, 4), "p": 2, "q": 3})
             calls["fwd"] = lambda sp: conv2d_forward(spec, xi, wi)
+            calls["bwd"] = lambda sp: conv2d_backward_data(spec, do, wi)
             calls["upd"] = lambda sp: conv2d_weight_update(spec, xi, do)
-            path = "grouped"
+            path = "im2col-gemm" if c < 64 and k == 64 else "grouped"
         row = {"id": lid, "count": cnt, "path": path, "C": c, "K": k, "H": h, "W": w, "R": r, "stride": st,
                "gflop": flops / 1e9}
         for p in passes:
@@ -143,9 +145,10 @@ def resnet_suite(n=256, iters=10, layers=None, passes=("fwd", "bwd", "upd"), ver
                       "roof_frac": t_roof / mean}
             if p == "bwd" and lid == 1:
                 continue
-            tot[p][0] += cnt * flops
-            tot[p][1] += cnt * mean
-            tot[p][2] += cnt * t_roof
+            for tt in (tot, tot_engine) if engine else (tot,):
+                tt[p][0] += cnt * flops
+                tt[p][1] += cnt * mean
+                tt[p][2] += cnt * t_roof
         if engine:
             row["plan"] = {pn: list(_plan(lib, i, geom)) for i, pn in enumerate(("fwd", "bwd", "upd"))}
         row["wall_s"] = round(time.time() - t_layer, 2)
@@ -154,17 +157,22 @@ def resnet_suite(n=256, iters=10, layers=None, passes=("fwd", "bwd", "upd"), ver
             print(json.dumps(row), flush=True)
         del x, wt, dout
         torch.cuda.empty_cache()
-    summary = {}
-    for p, (f, t, tr) in tot.items():
-        if t > 0:
-            summary[p] = {"tflops": f / t / 1e12, "weighted_eff_vs_peak": f / t / (peak * 1e12),
+    def summarize(totals):
+        out = {}
+        for p, (f, t, tr) in totals.items():
+            if t > 0:
+                out[p] = {"tflops": f / t / 1e12, "weighted_eff_vs_peak": f / t / (peak * 1e12),
                           "frac_of_roofline": tr / t, "ms": t * 1e3}
-    F = sum(v[0] for v in tot.values())
-    T = sum(v[1] for v in tot.values())
-    TR = sum(v[2] for v in tot.values())
-    summary["all"] = {"tflops": F / T / 1e12, "weighted_eff_vs_peak": F / T / (peak * 1e12),
-                      "frac_of_roofline": TR / T, "ms": T * 1e3, "gflop": F / 1e9}
-    return {"n": n, "peak_tflops": peak, "hbm_gbs": hbm, "peak_source": src, "layers": rows, "summary": summary}
+        F = sum(v[0] for v in totals.values())
+        T = sum(v[1] for v in totals.values())
+        TR = sum(v[2] for v in totals.values())
+        if T > 0:
+            out["all"] = {"tflops": F / T / 1e12, "weighted_eff_vs_peak": F / T / (peak * 1e12),
+                          "frac_of_roofline": TR / T, "ms": T * 1e3, "gflop": F / 1e9}
+        return out
+
+    return {"n": n, "peak_tflops": peak, "hbm_gbs": hbm, "peak_source": src, "layers": rows,
+            "summary": summarize(tot), "summary_engine_layers": summarize(tot_engine)}
 
 
 def lstm_suite(t_steps=50, n=168, c=1024, k=1024, iters=3, precision="bf16"):
