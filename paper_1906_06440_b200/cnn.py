@@ -304,8 +304,8 @@ def conv2d_forward(spec: ConvSpec, inp: BlockedTensor, wgt: BlockedTensor, strat
     if _small_ok(spec, dt, engine):
         from ._dense import gemm
         x, w = _stage(inp, dt), _stage(wgt, dt)
-        w2, rsc, ld = _small_weights(spec, w)
-        col = _small_im2col(spec, x, ld)
+        w2, rsc, _ = _small_weights(spec, w)
+        col = _small_im2col(spec, x, -(-rsc // 8) * 8)  # dense rows: the GEMM reads K = R*S*C
         out = torch.empty((spec.n, 1, spec.out_h, spec.out_w, 64), dtype=dt, device="cuda")
         gemm(col[:, :rsc], w2[:, :rsc], out.view(-1, 64))
         res = BlockedTensor(out, n_outer=4, logical_dims={"n": 0, "k": (1, 4), "p": 2, "q": 3})
@@ -438,8 +438,7 @@ def conv2d_weight_update(spec: ConvSpec, inp: BlockedTensor, dout: BlockedTensor
         from ._dense import gemm
         x, do = _stage(inp, dt), _stage(dout, dt)
         rsc = spec.r * spec.s * spec.c
-        ld = -(-rsc // 64) * 64
-        col = _small_im2col(spec, x, ld)
+        col = _small_im2col(spec, x, -(-rsc // 8) * 8)
         pix = spec.n * spec.out_h * spec.out_w
         dwt = torch.empty((rsc, 64), dtype=torch.float32, device="cuda")
         gemm(col[:, :rsc], do.reshape(pix, 64), dwt, a_t=True, b_t=True)  # reduction over all pixels in TMEM

@@ -11,14 +11,19 @@ rsc, ld = r * s * c, 192
 pix = n * p * q
 x = torch.randn(n, 1, h, w, c, device="cuda").bfloat16()
 col = torch.empty(pix, ld, device="cuda", dtype=torch.bfloat16)
+col152 = torch.empty(pix, 152, device="cuda", dtype=torch.bfloat16)
 w2 = torch.randn(64, ld, device="cuda").bfloat16()
 out = torch.empty(pix, 64, device="cuda", dtype=torch.bfloat16)
 do = torch.randn(pix, 64, device="cuda").bfloat16()
 dwt = torch.empty(rsc, 64, device="cuda")
 dcol = torch.empty(pix, ld, device="cuda", dtype=torch.bfloat16)
+col152 = torch.empty(pix, 152, device="cuda", dtype=torch.bfloat16)
 dx = torch.empty(n, 1, h, w, c, device="cuda", dtype=torch.bfloat16)
 ops = {
     "im2col": lambda: lib.brk_conv_im2col(x.data_ptr(), col.data_ptr(), n, c, h, w, r, s, st, pad, pad, c, ld, None),
+    "im2col152": lambda: lib.brk_conv_im2col(x.data_ptr(), col152.data_ptr(), n, c, h, w, r, s, st, pad, pad, c, 152,
+                                             None),
+    "gemm_fwd152": lambda: gemm(col152[:, :rsc], w2[:, :rsc], out),
     "gemm_fwd": lambda: gemm(col[:, :rsc], w2[:, :rsc], out),
     "gemm_upd": lambda: gemm(col[:, :rsc], do, dwt, a_t=True, b_t=True),
     "gemm_bwd": lambda: gemm(do, w2, dcol, b_t=True),
