@@ -300,6 +300,11 @@ def other_workloads():
             "note": "m=n=k in 32..256, batch 1..64, bf16 in / fp32 C, one grouped launch per point"}
     except Exception as exc:  # noqa: BLE001
         out["brgemm"] = {"error": repr(exc)[:300]}
+    try:  # TMEM-resident batch reduction vs split GEMMs accumulating through memory
+        from tools.suites import split_gemm_baseline
+        out["brgemm_vs_split_gemm"] = split_gemm_baseline(iters=5)
+    except Exception as exc:  # noqa: BLE001
+        out["brgemm_vs_split_gemm"] = {"error": repr(exc)[:300]}
     return out
 
 

@@ -281,6 +281,44 @@ def brgemm_suite(ms=(32, 64, 128, 256), batches=(1, 4, 16, 64), variants=("strid
     return {"peak_tflops": peak, "hbm_gbs": hbm, "peak_source": src, "points": rows}
 
 
+def split_gemm_baseline(m=64, n=64, k=64, batch=16, iters=10):
+    """SURVEY 8(f)3 / reference tests/test_acceptance.py:268-292: the batch-reduce GEMM
+    (the batch sum stays in TMEM, one store) against the split-GEMM formulation of the
+    same work — one GEMM launch per batch entry accumulating C through memory
+    (beta = 1).  BASELINE config 1 shape, 8 jobs per SM, bf16 -> fp32."""
+    import torch
+
+    from paper_1906_06440_b200 import _lib
+
+    lib = _lib.load()
+    timer = _Timer(torch)
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    jobs = 8 * sms
+    a = torch.randn(jobs * batch * k * m, device="cuda").bfloat16()
+    b = torch.randn(jobs * batch * n * k, device="cuda").bfloat16()
+    c = torch.empty(jobs * n * m, device="cuda")
+    c2 = torch.empty_like(c)
+
+    def stride(sp, base_a, base_b, nb, beta, out):
+        _lib.check(lib.brk_brgemm_stride(base_a, base_b, k * m, n * k, out.data_ptr(), jobs, batch * k * m,
+                                         batch * n * k, n * m, m, n, k, nb, m, k, m, 1.0, beta, _lib.BRK_BF16,
+                                         _lib.BRK_F32, _lib.BRK_COMPUTE_BF16, sp))
+
+    def brgemm(sp):
+        stride(sp, a.data_ptr(), b.data_ptr(), batch, 0.0, c)
+
+    def split(sp):
+        for i in range(batch):
+            stride(sp, a.data_ptr() + 2 * i * k * m, b.data_ptr() + 2 * i * n * k, 1, 0.0 if i == 0 else 1.0, c2)
+
+    t_br, _ = timer(brgemm, iters)
+    t_sp, _ = timer(split, iters)
+    torch.cuda.synchronize()
+    err = (c - c2).abs().max().item() / max(c.abs().max().item(), 1e-30)
+    return {"shape": f"m=n=k={m} batch={batch} jobs={jobs}", "brgemm_us": t_br * 1e6, "split_gemm_us": t_sp * 1e6,
+            "speedup": t_sp / t_br, "split_launches": batch, "max_rel_diff": err}
+
+
 def _plan(lib, pass_, geom):
     import ctypes
     out = (ctypes.c_int * 3)()
