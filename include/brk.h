@@ -149,8 +149,8 @@ BRK_API size_t brk_fc_upd_workspace(int N, int C, int K);
  * receives the updated weights W - lr dW, so the weight updates need not wait
  * for the bwd-data passes that read W (double-buffered weights).  lr == 0: gradients
  * only, no weight or bias update (data parallel: all-reduce, then brk_sgd_apply).  workspace:
- * >= brk_mlp_step_workspace_bytes(L, N, C) bytes of device scratch (the tile dependency counters,
- * zeroed by the call). */
+ * >= brk_mlp_step_workspace_bytes(L, N, C) bytes of device scratch (the tile dependency counters):
+ * zero it once before the first call; every call leaves it zeroed again (no per-step memset). */
 BRK_API int brk_mlp_step(int L, int N, int C, const void* const* y, void* const* dz, const void* dy,
                          void* const* w, void* const* w_next, float* const* bias, float* const* dw, float* const* db,
                          float* const* colsum, float lr, void* workspace, size_t ws_bytes, void* stream);

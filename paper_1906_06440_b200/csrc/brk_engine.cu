@@ -1060,6 +1060,19 @@ __device__ __forceinline__ void engine_body(const EngineParams* P, const GroupSc
     if constexpr (kPair) tmem_dealloc_pair(tmem_base, Cfg::kTmemCols);
     else tmem_dealloc(tmem_base, Cfg::kTmemCols);
   }
+  if (gs != nullptr) {
+    // every CTA is done with the dependency counters: the last one out re-zeroes them
+    // (all its threads, in parallel)
+    unsigned* exit_ctr = gs->counters + gs->n_probs * kCounterStride;
+    if (threadIdx.x == 0) {
+      __threadfence();  // this CTA's counter increments precede its exit ticket
+      *split_flag = atomicAdd(exit_ctr, 1u) == gridDim.x - 1 ? 1u : 0u;
+    }
+    __syncthreads();
+    if (*split_flag) {
+      for (int i = threadIdx.x; i <= gs->n_probs * kCounterStride; i += blockDim.x) gs->counters[i] = 0u;
+    }
+  }
   if (threadIdx.x == 0) BRK_TS(7);
 }
 

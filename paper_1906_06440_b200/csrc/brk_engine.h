@@ -134,7 +134,9 @@ struct GroupSched {
   int32_t tile_begin[kMaxProbs + 1];
   int32_t dep_prob[kMaxProbs][kMaxDeps];  // -1: none
   int32_t dep_mode[kMaxProbs][kMaxDeps];
-  unsigned* counters;                     // [n_probs][kCounterStride], zeroed before the launch
+  // [n_probs][kCounterStride] + 1 exit counter, all zero at launch; the last CTA to finish
+  // zeroes them again, so back-to-back launches need no memset
+  unsigned* counters;
 };
 
 struct EngineGroup {

@@ -411,7 +411,7 @@ extern "C" {
 
 namespace {
 // MLP step workspace: the dependency counters (zeroed by every call)
-size_t mlp_counter_bytes(int L) { return static_cast<size_t>(3 * L) * kCounterStride * sizeof(unsigned); }
+size_t mlp_counter_bytes(int L) { return (static_cast<size_t>(3 * L) * kCounterStride + 1) * sizeof(unsigned); }
 }  // namespace
 
 extern "C" {
@@ -539,8 +539,8 @@ BRK_API int brk_mlp_step(int L, int N, int C, const void* const* y, void* const*
     gs.tile_begin[i + 1] = gs.tile_begin[i] + G.probs[i].m_tiles * G.probs[i].n_tiles;
   gs.counters = counters;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  cudaError_t err = cudaMemsetAsync(counters, 0, mlp_counter_bytes(L), st);
-  if (err != cudaSuccess) return set_cuda_error(err, "mlp_step counters");
+  // the counters are zero: zero-initialised once by the caller, re-zeroed by every launch's
+  // last CTA (no memset between back-to-back steps)
   g_launches.fetch_add(1);
   return launch_engine_group(G, 128, 1, st);
 }

@@ -1,8 +1,4 @@
-timeout 900 python - <<'PY'
-import sys, json
-sys.path.insert(0, '.'); sys.path.insert(0, 'tools')
-import suites
-r = suites.resnet_suite(n=256, iters=5, layers=[1])
-for row in r["layers"]:
-    print(row["id"], row["path"], {p: (round(row[p]["us"], 1), round(row[p]["tflops"], 1), round(row[p]["roof_frac"], 3)) for p in ("fwd", "bwd", "upd")})
-PY
+J='import json,sys; d=json.loads(sys.stdin.read()); print(d["value"], d["ms_per_step"], d["e2e"]["value"], d["roofline"]["us_per_launch"])'
+python -m pytest tests/test_gpu_mlp.py tests/test_gpu_fc.py -x -q 2>&1 | tail -2
+for i in 1 2; do python bench.py --steps 100 --warmup 5 2>&1 | tail -1 | python -c "$J"; done
+python tools/_probe_mlp.py && echo probe-ok
