@@ -38,14 +38,17 @@ __global__ void __launch_bounds__(256) im2col_kernel(const __nv_bfloat16* __rest
   // column j -> (s, offset of (r, c) in the staged rows): no divisions in the hot loop
   int2* tab = reinterpret_cast<int2*>(sm);
   __nv_bfloat16* rows = reinterpret_cast<__nv_bfloat16*>(sm + ((groups * 8 * sizeof(int2) + 15) / 16) * 16);
+  // stored element-major (tab[e * groups + grp]): the threads of a warp read consecutive
+  // entries for the same e (a group-major table put them 64 B apart: 16-way bank conflicts)
   for (int j = threadIdx.x; j < groups * 8; j += blockDim.x) {
+    const int grp = j >> 3, e = j & 7;
+    int2 v = make_int2(-1, 0);
     if (j < rsc) {
       const int t = j / g.C, c = j - (j / g.C) * g.C;
       const int r = t / g.S, s = t - (t / g.S) * g.S;
-      tab[j] = make_int2(s, r * wc + c);
-    } else {
-      tab[j] = make_int2(-1, 0);
+      v = make_int2(s, r * wc + c);
     }
+    tab[e * groups + grp] = v;
   }
   const bool dense_rows = cb_n == 1 && wc % 8 == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0;
   for (int np = blockIdx.x; np < g.N * g.P; np += gridDim.x) {
@@ -74,7 +77,7 @@ __global__ void __launch_bounds__(256) im2col_kernel(const __nv_bfloat16* __rest
       __align__(16) __nv_bfloat16 v[8];
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        const int2 te = tab[grp * 8 + e];
+        const int2 te = tab[e * groups + grp];
         const int w = w0 + te.x;
         v[e] = (te.x >= 0 && w >= 0 && w < g.W) ? rows[te.y + w * g.C] : __float2bfloat16_rn(0.0f);
       }
