@@ -106,7 +106,9 @@ ConvPlan choose(int64_t rows, int cols, int k_steps, bool split_ok, double a_byt
                           b_bytes * (m_t - 1) / (b_bytes < kL2Fit ? kL2 : kHbm);
     const double base_mem = (a_bytes + b_bytes + out_bytes) / kHbm;
     int max_split = 1;
-    if (split_ok) max_split = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(k_steps / 8, 2 * units / std::max<int64_t>(1, tiles))));
+    // (at most one wave of work units: a second wave of split units measured slower than
+    // fewer, longer splits — each unit pays its pipeline fill and a partial-tile epilogue)
+    if (split_ok) max_split = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(k_steps / 8, units / std::max<int64_t>(1, tiles))));
     if (forced_splits > 0) max_split = std::min(forced_splits, std::max(1, k_steps));
     for (int sp = forced_splits > 0 ? max_split : 1; sp <= max_split; ++sp) {
       const int64_t work = tiles * sp;
