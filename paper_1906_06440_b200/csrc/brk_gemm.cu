@@ -77,7 +77,7 @@ GemmPlan gemm_plan(int64_t M, int N, int k_steps, bool split_ok) {
     const double per_tile = static_cast<double>(tr) * o.bn * k_steps / ((o.pair ? 2.0 : 1.0) * o.eff);
     int max_split = 1;
     if (split_ok)
-      max_split = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(k_steps / 8, 2 * units / std::max<int64_t>(1, tiles))));
+      max_split = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(k_steps / 8, units / std::max<int64_t>(1, tiles))));
     for (int sp = 1; sp <= max_split; ++sp) {
       const int64_t waves = (tiles * sp + units - 1) / units;
       const double cost = waves * per_tile / sp + (sp > 1 ? 0.05 * per_tile : 0.0) + 2.0e5;
