@@ -1,4 +1,4 @@
-python tools/_probe_stem.py 2>&1 | grep gemm_upd
-P='import sys; sys.path.insert(0, "."); sys.path.insert(0, "tools"); import suites; r = suites.lstm_suite(iters=5); print(round(r["fwd"]["tflops"],1), round(r["bwd_upd"]["tflops"],1), round(r["all"]["tflops"],1))'
-python -c "$P"; python -c "$P"
-python -m pytest tests/test_gpu_dense.py tests/test_gpu_lstm.py tests/test_gpu_conv_small.py -q 2>&1 | tail -1
+J='import json,sys; d=json.loads(sys.stdin.read()); print(d["value"], d["ms_per_step"], d["roofline"]["us_per_launch"])'
+python -m pytest tests/test_gpu_mlp.py tests/test_gpu_fc.py -x -q 2>&1 | tail -1
+for i in 1 2; do for w in 1 0; do echo -n "warm=$w "; BRK_MLP_WARM=$w python bench.py --steps 100 --warmup 5 2>&1 | tail -1 | python -c "$J"; done; done
+python tools/_probe_mlp_ts.py 2>&1 | grep -E "fwd|bwd4"
