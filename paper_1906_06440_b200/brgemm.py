@@ -250,10 +250,31 @@ def _one_storage(ts):
     return all(t.untyped_storage().data_ptr() == base and t.dtype == ts[0].dtype for t in ts)
 
 
+def _check_device_dtypes(operands, outputs) -> bool:
+    """Device operands: every A/B block one dtype in {float32, bfloat16}, every C
+    float32 or bfloat16, all on the GPU.  Returns whether the inputs are bf16."""
+    torch = require_cuda()
+    ok = (torch.float32, torch.bfloat16)
+    in_dt = operands[0].dtype if operands else torch.float32
+    for t in operands:
+        if not is_torch(t) or not t.is_cuda:
+            raise BrgemmError("device BRGEMM: every A/B block must be a CUDA tensor")
+        if t.dtype != in_dt:
+            raise BrgemmError(f"device BRGEMM: mixed operand dtypes ({in_dt} and {t.dtype})")
+    if in_dt not in ok:
+        raise BrgemmError(f"device BRGEMM: operand dtype {in_dt} (need float32 or bfloat16)")
+    for t in outputs:
+        if not is_torch(t) or not t.is_cuda:
+            raise BrgemmError("device BRGEMM: C must be a CUDA tensor")
+        if t.dtype not in ok or t.dtype != outputs[0].dtype:
+            raise BrgemmError(f"device BRGEMM: C dtype {t.dtype} (need one of float32 / bfloat16)")
+    return in_dt == torch.bfloat16
+
+
 def _run_addr_torch(a_list, b_list, c_list, m, n, k, batch, alpha, beta, spec):
     """All operands are CUDA tensors; a_list/b_list are job-major flat lists."""
     torch = require_cuda()
-    in_bf16 = any(t.dtype == torch.bfloat16 for t in (a_list + b_list)[:1])
+    in_bf16 = _check_device_dtypes(a_list + b_list, c_list)
     out_bf16 = c_list[0].dtype == torch.bfloat16
     compute, in_code = _codes(spec, in_bf16)
     lda = _torch_ld(a_list, m) if a_list else m
@@ -404,7 +425,7 @@ def brgemm_strided(a_base, b_base, stride_a: int, stride_b: int, c, spec: Brgemm
         dev_c = c
         if not dev_c.is_contiguous():
             raise BrgemmError("device c must be contiguous for the stride variant")
-    in_bf16 = dev_a is not None and dev_a.dtype == torch.bfloat16
+    in_bf16 = _check_device_dtypes([t for t in (dev_a, dev_b) if t is not None], [dev_c])
     compute, in_code = _codes(spec, in_bf16)
     lib = _lib.load()
     rc = lib.brk_brgemm_stride(
@@ -458,7 +479,7 @@ def brgemm_offset(a_base, b_base, a_offsets, b_offsets, c, spec: BrgemmSpec,
     c_tab = ptr_table([dev_c.data_ptr()])
     a_off = torch.tensor(a_offsets or [0], dtype=torch.int64, device="cuda")
     b_off = torch.tensor(b_offsets or [0], dtype=torch.int64, device="cuda")
-    compute, in_code = _codes(spec, dev_a.dtype == torch.bfloat16)
+    compute, in_code = _codes(spec, _check_device_dtypes([dev_a, dev_b], [dev_c]))
     lib = _lib.load()
     rc = lib.brk_brgemm_offs(
         dev_a.data_ptr(), dev_b.data_ptr(), a_off.data_ptr(), b_off.data_ptr(), c_tab.data_ptr(),

@@ -12,9 +12,9 @@ reference's pointer lists (``cnn.py:241-252, 304-310``):
 * fwd   job (img, kb, oj): C = O[img][kb][oj][:]            (Q x b_k)
         entries (c_b, r, s): A = W[kb][c_b][r][s]            (b_c x b_k)
                               B = I_pad[img][c_b][oj*str+r][s::str]  (Q x b_c, row stride str*b_c)
-* bwd   "dual convolution": dI = conv(dO padded by R-1-pad,
-        flipped W with C<->K swapped) for stride 1; 1x1 stride-s layers
-        scatter a 1x1 GEMM to the strided input positions.
+* bwd   "dual convolution": dI = conv(dO dilated by the stride
+        and padded by R-1-pad, flipped W with C<->K swapped); unpadded 1x1
+        stride-s layers scatter a 1x1 GEMM to the strided input positions.
 * upd   job (kb, c_b, r, s): C = dW[kb][c_b][r][s]           (b_c x b_k)
         entries (img, oj):   A = dO[img][kb][oj]             (Q x b_k)
                              B = I_pad[img][c_b][oj*str+r][s::str]^T (b_c x Q)
@@ -342,9 +342,9 @@ def conv2d_backward_data(spec: ConvSpec, dout: BlockedTensor, wgt: BlockedTensor
                          precision: str | None = None, engine: bool | None = None) -> BlockedTensor:
     """dI[N][C_b][H][W][b_c] from dO[N][K_b][P][Q][b_k] (north star; restated in oracle/).
 
-    Stride 1: dual convolution of dO (padded by R-1-pad) with the flipped,
-    C<->K-swapped filter.  1x1 stride-s: a 1x1 GEMM scattered to the strided
-    input pixels (other pixels receive no gradient).
+    Dual convolution of dO (dilated by the stride, padded by R-1-pad) with the
+    flipped, C<->K-swapped filter; unpadded 1x1 stride-s: a 1x1 GEMM scattered
+    to the strided input pixels (other pixels receive no gradient).
     """
     spec.validate()
     want = {"n": spec.n, "k": spec.k, "p": spec.out_h, "q": spec.out_w}
@@ -382,15 +382,24 @@ def conv2d_backward_data(spec: ConvSpec, dout: BlockedTensor, wgt: BlockedTensor
     h, wd = spec.h, spec.w
     din = torch.zeros((n, cb_n, h, wd, b_c), dtype=dt, device="cuda")
     in_bf16 = dt == torch.bfloat16
-    if st == 1:
+    if st == 1 or r_n > 1 or s_n > 1 or spec.pad_h or spec.pad_w:
+        # dual convolution: dO dilated by the stride (zero insertion; a no-op for
+        # stride 1), padded by R-1-pad on the leading side and by
+        # R-1-pad + ((H + 2 pad - R) mod stride) on the trailing side, convolved
+        # at stride 1 with the flipped, C<->K-swapped filter -> exactly H x W.
         ph, pw = r_n - 1 - spec.pad_h, s_n - 1 - spec.pad_w
         if ph < 0 or pw < 0:
             raise LayoutError("backward-data needs pad <= filter-1")
-        dop = _pad_device(do, ph, pw)
-        hp, wp = p_ + 2 * ph, q_ + 2 * pw
+        pd, qd = (p_ - 1) * st + 1, (q_ - 1) * st + 1
+        hp, wp = h + r_n - 1, wd + s_n - 1
+        if st == 1 and hp == p_ + 2 * ph and wp == q_ + 2 * pw:
+            dop = _pad_device(do, ph, pw)
+        else:
+            dop = torch.zeros((n, kb_n, hp, wp, b_k), dtype=do.dtype, device="cuda")
+            dop[:, :, ph:ph + pd:st, pw:pw + qd:st] = do
         # dual conv output extent must equal the input extent
         if hp - r_n + 1 != h or wp - s_n + 1 != wd:
-            raise LayoutError("backward-data: stride-1 dual convolution does not reproduce the input extent")
+            raise LayoutError("backward-data: dual convolution does not reproduce the input extent")
         ji, jc, jh = _grid(n, cb_n, h)
         ek, er, es = _grid(kb_n, r_n, s_n)
         # A_i = W[kb][cb][R-1-r][S-1-s] viewed (k = b_k rows, m = b_c cols): a_sk = 1, a_sm = b_k
@@ -402,10 +411,9 @@ def conv2d_backward_data(spec: ConvSpec, dout: BlockedTensor, wgt: BlockedTensor
                     c_ptrs=addr_table(din, c_off), m=b_c, n=wd, k=b_k, batch=kb_n * r_n * s_n,
                     a_sk=1, a_sm=b_k, b_sn=b_k, b_sk=1, ldc=b_c,
                     in_bf16=in_bf16, out_bf16=in_bf16, precision=prec, exc=LayoutError)
-    elif r_n == 1 and s_n == 1:
-        # dI[n][cb][oj*st - pad][oi*st - pad] = sum_kb dO[n][kb][oj][oi] W[kb][cb]^T
-        if spec.pad_h or spec.pad_w:
-            raise LayoutError("backward-data for padded strided 1x1 convolutions is not supported")
+    else:
+        # unpadded strided 1x1: dI[n][cb][oj*st][oi*st] = sum_kb dO[n][kb][oj][oi] W[kb][cb]^T,
+        # the other input pixels receive no gradient (din is zero-initialised)
         ji, jc, jo = _grid(n, cb_n, p_)
         ek = torch.arange(kb_n, device="cuda", dtype=torch.int64)
         a_off = (ek[None, :] * cb_n + jc[:, None]) * (b_c * b_k)
@@ -415,8 +423,6 @@ def conv2d_backward_data(spec: ConvSpec, dout: BlockedTensor, wgt: BlockedTensor
                     c_ptrs=addr_table(din, c_off), m=b_c, n=q_, k=b_k, batch=kb_n,
                     a_sk=1, a_sm=b_k, b_sn=b_k, b_sk=1, ldc=st * b_c,
                     in_bf16=in_bf16, out_bf16=in_bf16, precision=prec, exc=LayoutError)
-    else:
-        raise LayoutError("backward-data supports stride 1 (any filter) and 1x1 strided convolutions")
     res = BlockedTensor(din, n_outer=4, logical_dims={"n": 0, "c": (1, 4), "h": 2, "w": 3})
     return res.to("cpu") if host else res
 

@@ -201,7 +201,8 @@ class LstmGrads:
 
 
 class _DeviceCell:
-    """Device-resident fp32 copies of one LstmParams (cached on the params object)."""
+    """Device-resident fp32 copies of one LstmParams (cached on the params object,
+    keyed on the source arrays' identity and content version, see _params_key)."""
 
     def __init__(self, params: LstmParams):
         torch = require_cuda()
@@ -217,12 +218,35 @@ class _DeviceCell:
                                for b in bias]).to("cuda").contiguous()
 
 
+def _params_key(params: LstmParams) -> tuple:
+    """Identity + content version of every source array of ``params``: device tensors
+    by (storage pointer, autograd version counter, which in-place updates bump),
+    host arrays by (address, crc32 of the bytes).  The device copies below are
+    rebuilt whenever the key changes, so in-place weight updates (e.g. SGD on
+    ``w_i.data`` or the bias arrays) are seen by the next call, as in the
+    reference, which reads the params on every call."""
+    import zlib
+
+    key = []
+    for g in GATE_NAMES:
+        for a in (getattr(params, f"w_{g}").data, getattr(params, f"r_{g}").data, getattr(params, f"bias_{g}")):
+            if is_torch(a):
+                key.append((a.data_ptr(), a._version, tuple(a.shape), str(a.dtype)))
+            else:
+                arr = np.ascontiguousarray(a)
+                key.append((arr.__array_interface__["data"][0], zlib.crc32(arr.view(np.uint8).reshape(-1)),
+                            arr.shape, arr.dtype.str))
+    return tuple(key)
+
+
 def _device_cell(params: LstmParams) -> _DeviceCell:
+    key = _params_key(params)
     cache = getattr(params, "_brk_device_cell", None)
-    if cache is None:
-        cache = _DeviceCell(params)
+    if cache is None or cache[0] != key:
+        cache = (key, _DeviceCell(params))
         object.__setattr__(params, "_brk_device_cell", cache)
-    return cache
+        object.__setattr__(params, "_brk_seq_cell", None)
+    return cache[1]
 
 
 def _to_dev(a, shape=None):
@@ -256,9 +280,10 @@ class _SeqCell:
 
 
 def _seq_cell(params: LstmParams) -> _SeqCell:
+    dc = _device_cell(params)  # revalidates the source arrays (and drops a stale _SeqCell)
     cache = getattr(params, "_brk_seq_cell", None)
     if cache is None:
-        cache = _SeqCell(params, _device_cell(params))
+        cache = _SeqCell(params, dc)
         object.__setattr__(params, "_brk_seq_cell", cache)
     return cache
 

@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 
 import brk_oracle as orc
-from conftest import load_golden
+from conftest import check_parity, load_golden
 
 pytestmark = pytest.mark.gpu
 
@@ -92,18 +92,17 @@ def test_forward_backward_vs_oracle(shape, prec):
         seq = lstm_forward(params, x, h0, s0, keep_gates=True)
         grads = lstm_backward(params, x, seq, dh, h0, s0)
     tol = TOL[prec]
-    assert orc.scale_rel_error(seq.h, fwd_ref["h"]) <= tol
-    assert orc.scale_rel_error(seq.s, fwd_ref["s"]) <= tol
+    case = f"{shape}"
+    check_parity(f"lstm.step.{prec}.h", case, orc.scale_rel_error(seq.h, fwd_ref["h"]), tol)
+    check_parity(f"lstm.step.{prec}.s", case, orc.scale_rel_error(seq.s, fwd_ref["s"]), tol)
     # BPTT against the oracle fed the GPU's own forward states (isolates the backward)
     gpu_fwd = {"h": seq.h, "s": seq.s, "gates": seq.gates}
     ref = orc.lstm_backward_reference(w, r, x, gpu_fwd, dh, h0, s0)
-    assert orc.scale_rel_error(grads.dx, ref["dx"]) <= 2 * tol
-    assert orc.scale_rel_error(grads.dh0, ref["dh0"]) <= 2 * tol
-    assert orc.scale_rel_error(grads.ds0, ref["ds0"]) <= 2 * tol
+    for name in ("dx", "dh0", "ds0"):
+        check_parity(f"lstm.step.{prec}.{name}", case, orc.scale_rel_error(getattr(grads, name), ref[name]), tol)
     for g in GATE_NAMES:
-        assert orc.scale_rel_error(grads.dw[g], ref["dw"][g]) <= 2 * tol, g
-        assert orc.scale_rel_error(grads.dr[g], ref["dr"][g]) <= 2 * tol, g
-        assert orc.scale_rel_error(grads.db[g], ref["db"][g]) <= 2 * tol, g
+        for fld in ("dw", "dr", "db"):
+            check_parity(f"lstm.step.{prec}.{fld}", (case, g), orc.scale_rel_error(getattr(grads, fld)[g], ref[fld][g]), tol)
 
 
 def test_causality_and_determinism():
@@ -135,15 +134,15 @@ def test_sequence_kernels_vs_oracle(shape):
     with precision("bf16"):
         seq = lstm_forward(params, x, h0, s0, keep_gates=True)
         grads = lstm_backward(params, x, seq, dh, h0, s0)
-    assert orc.scale_rel_error(seq.h, fwd_ref["h"]) <= 1e-2
-    assert orc.scale_rel_error(seq.s, fwd_ref["s"]) <= 1e-2
+    case = f"{shape}"
+    check_parity("lstm.seq.bf16.h", case, orc.scale_rel_error(seq.h, fwd_ref["h"]), 1e-2)
+    check_parity("lstm.seq.bf16.s", case, orc.scale_rel_error(seq.s, fwd_ref["s"]), 1e-2)
     ref = orc.lstm_backward_reference(w, r, x, {"h": seq.h, "s": seq.s, "gates": seq.gates}, dh, h0, s0)
     for name in ("dx", "dh0", "ds0"):
-        assert orc.scale_rel_error(getattr(grads, name), ref[name]) <= 2e-2, name
+        check_parity(f"lstm.seq.bf16.{name}", case, orc.scale_rel_error(getattr(grads, name), ref[name]), 1e-2)
     for g in GATE_NAMES:
-        assert orc.scale_rel_error(grads.dw[g], ref["dw"][g]) <= 2e-2, g
-        assert orc.scale_rel_error(grads.dr[g], ref["dr"][g]) <= 2e-2, g
-        assert orc.scale_rel_error(grads.db[g], ref["db"][g]) <= 2e-2, g
+        for fld in ("dw", "dr", "db"):
+            check_parity(f"lstm.seq.bf16.{fld}", (case, g), orc.scale_rel_error(getattr(grads, fld)[g], ref[fld][g]), 1e-2)
 
 
 def test_sequence_and_step_paths_agree(monkeypatch):
@@ -155,3 +154,23 @@ def test_sequence_and_step_paths_agree(monkeypatch):
         monkeypatch.setenv("BRK_LSTM_SEQ", "0")
         b = lstm_forward(LstmParams.from_dense(wt, 5, 64), x)
     assert orc.scale_rel_error(a.h, b.h) <= 1e-2
+
+
+def test_in_place_weight_update_is_seen():
+    """device copies of the params are keyed on the source arrays'
+    content, so an in-place update (SGD on the blocked weights / biases) is
+    used by the next call, as in the reference (which reads params every call)."""
+    rng = np.random.default_rng(12)
+    wt = LstmCellWeights.random(rng, 64, 64)
+    x = rng.uniform(-1, 1, (3, 8, 64)).astype(F32)
+    params = LstmParams.from_dense(wt, 3, 8)
+    with precision("tf32"):
+        lstm_forward(params, x)
+        params.w_i.data *= 0.5
+        params.bias_f[:] += 0.25
+        seq = lstm_forward(params, x)
+    wt.w_i *= 0.5
+    wt.bias_f += 0.25
+    w, r, bias = oracle_args(wt)
+    ref = orc.lstm_forward_reference(w, r, bias, x)
+    check_parity("lstm.in_place_update.tf32.h", "3x8x64", orc.scale_rel_error(seq.h, ref["h"]), 1e-3)

@@ -4,6 +4,7 @@ import numpy as np
 import pytest
 
 import brk_oracle as orc
+from conftest import check_parity
 
 pytestmark = pytest.mark.gpu
 
@@ -46,21 +47,23 @@ def test_mlp_step_matches_oracle(layers, width, batch):
     fwd = orc.mlp_step_reference(ws, bs, x.float().numpy(), dy.float().numpy(), lr=lr, store=orc.round_bf16)
     # forward activations (bf16-stored between layers): 1e-2 scale-relative
     gpu_y = [unblk(mlp.y[l]).float().cpu().numpy() for l in range(1, layers + 1)]
+    case = f"{layers}x{width} N={batch}"
     for l in range(1, layers + 1):
-        assert orc.scale_rel_error(gpu_y[l - 1], fwd["y"][l]) <= 2e-2, f"y{l}"
+        check_parity(f"mlp.y{l}", case, orc.scale_rel_error(gpu_y[l - 1], fwd["y"][l]), 1e-2)
     # backward / update against the oracle fed the GPU's own activations (same ReLU masks)
     ref = orc.mlp_step_reference(ws, bs, x.float().numpy(), dy.float().numpy(), lr=lr, store=orc.round_bf16,
                                  activations=gpu_y)
     for l in range(layers):
-        assert orc.scale_rel_error(w_dense(mlp.dw[l]).cpu().numpy(), ref["dw"][l]) <= 3e-2, f"dw{l}"
-        assert orc.scale_rel_error(mlp.db[l].cpu().numpy(), ref["db"][l]) <= 3e-2, f"db{l}"
+        check_parity(f"mlp.dw{l}", case, orc.scale_rel_error(w_dense(mlp.dw[l]).cpu().numpy(), ref["dw"][l]), 1e-2)
+        check_parity(f"mlp.db{l}", case, orc.scale_rel_error(mlp.db[l].cpu().numpy(), ref["db"][l]), 1e-2)
         # SGD applied in the upd epilogue (bf16 weights) and in the bias-grad kernel
         w_new = w_dense(mlp.w[l]).float().cpu().numpy()
         # bf16 rounding of the stored weight + lr * (the dW tolerance)
-        w_tol = 2.0 ** -8 * np.max(np.abs(ref["w_new"][l])) + lr * 3e-2 * np.max(np.abs(ref["dw"][l]))
+        w_tol = 2.0 ** -8 * np.max(np.abs(ref["w_new"][l])) + lr * 1e-2 * np.max(np.abs(ref["dw"][l]))
         assert np.max(np.abs(w_new - ref["w_new"][l])) <= w_tol, f"w{l}"
-        assert np.allclose(mlp.bias[l].cpu().numpy(), ref["b_new"][l], atol=2e-2 * lr * 50)
-    assert orc.scale_rel_error(unblk(mlp.dz[0]).float().cpu().numpy(), ref["dx"]) <= 3e-2
+        b_tol = lr * 1e-2 * np.max(np.abs(ref["db"][l])) + 1e-6
+        assert np.max(np.abs(mlp.bias[l].cpu().numpy() - ref["b_new"][l])) <= b_tol, f"b{l}"
+    check_parity("mlp.dx", case, orc.scale_rel_error(unblk(mlp.dz[0]).float().cpu().numpy(), ref["dx"]), 1e-2)
 
 
 def test_graph_replay_equals_eager_step():
