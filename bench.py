@@ -14,7 +14,7 @@ all-reduce of dW/db per layer; time = max over ranks of device time.
 
 `--impl reference` times the reference algorithm's CPU implementation (the
 oracle port of the blocked FC BRGEMM loops, oracle/brk_oracle.py, all host
-threads) on one FC layer's fwd+bwd+upd at the full size, rank 0 only.
+threads) on the same 4-layer step at the full size, rank 0 only.
 """
 
 from __future__ import annotations
@@ -116,9 +116,14 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # reference arm (CPU)
 # ---------------------------------------------------------------------------
-def run_reference(args, n_gpus, rank):
-    if rank != 0:
-        return
+def reference_step():
+    """(step_fn, threads): one full MLP step of the benchmarked config (4 layers, C=K=1024,
+    N=2048, bias + ReLU) with the reference's blocked FC BRGEMM algorithm on the host
+    (oracle port of fc.py:99-163 over brgemm.py:260-293, float64 block accumulation, all
+    host threads): forward through the 4 layers, then per layer from the top the
+    backward-data, weight-update and bias-gradient passes (restated, oracle/brk_oracle.py).
+    The reference is Python/NumPy and cannot travel to the GPU box, so its algorithm runs
+    from the port; the SGD apply is elementwise and omitted (it has no GEMM flops)."""
     import numpy as np
 
     sys.path.insert(0, str(ROOT / "oracle"))
@@ -127,19 +132,34 @@ def run_reference(args, n_gpus, rank):
     threads = orc.cpu_threads()
     rng = np.random.default_rng([0, 202])
     b = 64
-    w = (rng.uniform(-1, 1, (WIDTH, WIDTH)) / 32).astype(np.float32)
-    x = rng.uniform(-1, 1, (BATCH, WIDTH)).astype(np.float32)
-    dy = rng.uniform(-1, 1, (BATCH, WIDTH)).astype(np.float32)
-    bias = rng.uniform(-0.1, 0.1, WIDTH).astype(np.float32)
-    wb = w.reshape(WIDTH // b, b, WIDTH // b, b).transpose(0, 2, 3, 1).copy()
-    xb = x.reshape(BATCH // b, b, WIDTH // b, b).transpose(0, 2, 1, 3).copy()
-    dyb = dy.reshape(BATCH // b, b, WIDTH // b, b).transpose(0, 2, 1, 3).copy()
+    blk_w = lambda w: w.reshape(WIDTH // b, b, WIDTH // b, b).transpose(0, 2, 3, 1).copy()  # noqa: E731
+    blk_x = lambda x: x.reshape(BATCH // b, b, WIDTH // b, b).transpose(0, 2, 1, 3).copy()  # noqa: E731
+    wbs = [blk_w((rng.uniform(-1, 1, (WIDTH, WIDTH)) / 32).astype(np.float32)) for _ in range(LAYERS)]
+    biases = [rng.uniform(-0.1, 0.1, WIDTH).astype(np.float32) for _ in range(LAYERS)]
+    xb = blk_x(rng.uniform(-1, 1, (BATCH, WIDTH)).astype(np.float32))
+    dyb = blk_x(rng.uniform(-1, 1, (BATCH, WIDTH)).astype(np.float32))
 
     def step():
-        yb = orc.fc_forward_blocked(wb, xb, "relu", bias, workers=threads)
-        orc.fc_backward_blocked(wb, xb, yb, dyb, "relu", workers=threads)
+        ys = [xb]
+        for wb, bias in zip(wbs, biases):
+            ys.append(orc.fc_forward_blocked(wb, ys[-1], "relu", bias, workers=threads))
+        d = dyb
+        for l in range(LAYERS - 1, -1, -1):
+            d, _, _ = orc.fc_backward_blocked(wbs[l], ys[l], ys[l + 1], d, "relu", workers=threads)
 
-    flops = 3 * 2 * BATCH * WIDTH * WIDTH
+    return step, threads
+
+
+REF_SAMPLE = (f"the full benchmarked MLP step ({LAYERS} x FC C=K={WIDTH}, N={BATCH}, bias+ReLU: fwd of every "
+              f"layer, then bwd-data + weight-update + bias-grad of every layer) with the reference's blocked "
+              f"BRGEMM algorithm (oracle port, float64 block accumulation)")
+
+
+def run_reference(args, n_gpus, rank):
+    if rank != 0:
+        return
+    step, threads = reference_step()
+    flops = LAYERS * 3 * 2 * BATCH * WIDTH * WIDTH
     for _ in range(args.warmup):
         step()
     times = []
@@ -149,45 +169,28 @@ def run_reference(args, n_gpus, rank):
         times.append(time.perf_counter() - t0)
     sec = statistics.fmean(times)
     value = flops / sec / 1e12
-    sample = (f"one FC layer (C=K={WIDTH}, N={BATCH}, bias+ReLU) fwd + bwd-data + weight-update + "
-              f"bias-grad per step, reference blocked BRGEMM algorithm (oracle port, float64 block "
-              f"accumulation), {threads} threads")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n_gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64-accumulate/f32-storage", "data": "synthetic",
             "config": base_config(n_gpus),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": f"{REF_SAMPLE}, {threads} threads, one step per timed step"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 def cpu_baseline_sample():
-    """Bounded CPU sample for the GPU arm's cpu_baseline key (~10-30 s)."""
-    import numpy as np
-
-    sys.path.insert(0, str(ROOT / "oracle"))
-    import brk_oracle as orc
-
-    threads = orc.cpu_threads()
-    rng = np.random.default_rng([0, 202])
-    b = 64
-    w = (rng.uniform(-1, 1, (WIDTH, WIDTH)) / 32).astype(np.float32)
-    x = rng.uniform(-1, 1, (BATCH, WIDTH)).astype(np.float32)
-    dy = rng.uniform(-1, 1, (BATCH, WIDTH)).astype(np.float32)
-    wb = w.reshape(WIDTH // b, b, WIDTH // b, b).transpose(0, 2, 3, 1).copy()
-    xb = x.reshape(BATCH // b, b, WIDTH // b, b).transpose(0, 2, 1, 3).copy()
-    dyb = dy.reshape(BATCH // b, b, WIDTH // b, b).transpose(0, 2, 1, 3).copy()
+    """Bounded CPU sample for the GPU arm's cpu_baseline key (~10-30 s): whole reference steps."""
+    step, threads = reference_step()
     reps, t_total = 0, 0.0
     while t_total < 10.0 and reps < 20:
         t0 = time.perf_counter()
-        yb = orc.fc_forward_blocked(wb, xb, "relu", None, workers=threads)
-        orc.fc_backward_blocked(wb, xb, yb, dyb, "relu", workers=threads)
+        step()
         t_total += time.perf_counter() - t0
         reps += 1
-    value = reps * 3 * 2 * BATCH * WIDTH * WIDTH / t_total / 1e12
+    value = reps * LAYERS * 3 * 2 * BATCH * WIDTH * WIDTH / t_total / 1e12
     return {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"{reps} x one FC layer fwd+bwd+upd (C=K={WIDTH}, N={BATCH}) with the reference's blocked "
-                      f"BRGEMM algorithm (oracle port, f64 block accumulation), {t_total:.1f} s, {threads} threads"}
+            "sample": f"{reps} x {REF_SAMPLE}, {t_total:.1f} s, {threads} threads"}
 
 
 # ---------------------------------------------------------------------------
@@ -308,6 +311,21 @@ def other_workloads():
     return out
 
 
+def dp_workloads(pg):
+    """The conv and LSTM workloads as data-parallel training steps at this world size
+    (train.py): ResNet-50's 53 convs at global minibatch 256 (strong scaling) and the
+    LSTM cell at N=168 per GPU (weak scaling); whole-job TFLOP/s, max over ranks."""
+    from tools.suites import lstm_dp_suite, resnet_dp_suite
+
+    out = {}
+    for name, fn in (("resnet50_convs_dp_n256", resnet_dp_suite), ("lstm_dp_n168_per_gpu", lstm_dp_suite)):
+        try:
+            out[name] = fn(pg)
+        except Exception as exc:  # noqa: BLE001 - informational block must not kill the headline line
+            out[name] = {"error": repr(exc)[:300]}
+    return out
+
+
 def run_gpu(args, n_gpus, rank, local_rank, pg):
     import torch
 
@@ -316,7 +334,7 @@ def run_gpu(args, n_gpus, rank, local_rank, pg):
 
     torch.cuda.set_device(local_rank)
     pk, pk_kind = peaks()
-    mlp = MLP(layers=LAYERS, width=WIDTH, batch=BATCH, lr=1e-4, seed=rank, process_group=pg)
+    mlp = MLP(layers=LAYERS, width=WIDTH, batch=BATCH, lr=1e-4, seed=0, process_group=pg)  # data: seed 100+rank
     g = torch.Generator(device="cpu").manual_seed(100 + rank)
     blk = lambda t: t.reshape(BATCH // 64, 64, WIDTH // 64, 64).permute(0, 2, 1, 3).contiguous()  # noqa: E731
     x_host = blk((torch.rand(BATCH, WIDTH, generator=g) * 2 - 1).bfloat16()).pin_memory()
@@ -387,11 +405,15 @@ def run_gpu(args, n_gpus, rank, local_rank, pg):
     launches = mlp.launches_per_step
     value = n_gpus * flops / sec / 1e12
     e2e_value = n_gpus * flops / e2e_sec / 1e12
+    suites = os.environ.get("BRK_BENCH_SUITES", "1") != "0"
+    dp = dp_workloads(pg) if suites else None  # every rank takes part (collectives)
     if rank != 0:
         return
     workloads = None
-    if n_gpus == 1 and os.environ.get("BRK_BENCH_SUITES", "1") != "0":
+    if n_gpus == 1 and suites:
         workloads = other_workloads()
+    if dp is not None:
+        workloads = dict(workloads or {}, **dp)
     roof = kernel_roofline(mlp, torch, pk["bf16_tflops"])
     roof["peak_source"] = f"{pk_kind} bf16 dense (burst, kernel timed alone)"
     cpu = cpu_baseline_sample()
@@ -418,6 +440,25 @@ def run_gpu(args, n_gpus, rank, local_rank, pg):
     print(json.dumps(line), flush=True)
 
 
+def spawn_ranks(args) -> int:
+    """Re-launch this script under torch.distributed.run with one rank per GPU."""
+    import socket
+
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {have}", file=sys.stderr)
+        return 2
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()),
+           "--gpus", str(args.gpus), "--steps", str(args.steps), "--warmup", str(args.warmup)]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -430,10 +471,17 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    n_gpus = world if world > 1 else args.gpus
     if args.impl == "reference":
-        run_reference(args, n_gpus, rank)
+        run_reference(args, world if world > 1 else args.gpus, rank)
         return
+    if world == 1 and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # --gpus N without a launcher: start N ranks ourselves (one process per GPU),
+        # never scale a one-process number
+        sys.exit(spawn_ranks(args))
+    if world != args.gpus and "WORLD_SIZE" in os.environ:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(2)
+    n_gpus = world
     pg = None
     if world > 1 or os.environ.get("BRK_FORCE_DP") == "1":  # torchrun: NCCL data parallel
         import torch

@@ -87,6 +87,15 @@ class GradientReducer:
             torch.cuda.current_stream().wait_stream(self.stream)
 
 
+def broadcast_params(tensors, group=None) -> None:
+    """Make every rank's parameters equal to the group's first rank's (in place)."""
+    import torch.distributed as dist
+
+    src = dist.get_global_rank(group, 0) if group is not None and group != dist.group.WORLD else 0
+    for t in tensors:
+        dist.broadcast(t, src=src, group=group)
+
+
 def sgd_scale(lr: float, world: int) -> float:
     """Step size applied to the all-reduced SUM so the update uses the global-mean gradient."""
     if world < 1:

@@ -408,12 +408,14 @@ def _finish_forward(h, s, gates, host, keep_gates, h_bf):
 
 
 def lstm_backward(params: LstmParams, x, seq: LstmStateSequence, dh, h_init=None, s_init=None,
-                  precision: str | None = None) -> LstmGrads:
+                  precision: str | None = None, reducer=None) -> LstmGrads:
     """BPTT + weight update for the forward above (north star; oracle lstm_backward_reference).
 
     ``dh`` is dL/dh_t for every step [T][N][K].  Returns dense per-gate
     gradients dW_g (K, C), dR_g (K, K), db_g (K,), plus dx [T][N][C],
-    dh0 / ds0 [N][K].
+    dh0 / ds0 [N][K].  With a ``reducer`` (data parallel, dist.GradientReducer)
+    each weight-gradient buffer's all-reduce is submitted as soon as its
+    product is issued, overlapping the remaining BPTT products (dx, dh0).
     """
     t_steps, n, c, k = params.t_steps, params.n, params.c, params.k
     if tuple(dh.shape) != (t_steps, n, k):
@@ -434,7 +436,7 @@ def lstm_backward(params: LstmParams, x, seq: LstmStateSequence, dh, h_init=None
     h0 = _to_dev(h_init) if h_init is not None else torch.zeros((n, k), dtype=torch.float32, device="cuda")
     s0 = _to_dev(s_init) if s_init is not None else None
     if _seq_ok(params, prec) and k % 32 == 0:
-        out = _backward_seq(params, xd, hd, sd, gates, dhd, h0, s0, getattr(seq, "_brk_h_bf", None))
+        out = _backward_seq(params, xd, hd, sd, gates, dhd, h0, s0, getattr(seq, "_brk_h_bf", None), reducer)
         if host:
             cpu = lambda t: t.cpu().numpy()  # noqa: E731
             out = LstmGrads(dx=cpu(out.dx), dw={g: cpu(v) for g, v in out.dw.items()},
@@ -491,6 +493,8 @@ def lstm_backward(params: LstmParams, x, seq: LstmStateSequence, dh, h_init=None
     db = torch.empty(4 * k, dtype=torch.float32, device="cuda")
     _lib.check(lib.brk_colsum_blocked(dpre2.data_ptr(), None, None, db.data_ptr(), rows, 4 * k, rows, 4 * k,
                                       _lib.BRK_F32, st), LayoutError)
+    if reducer is not None:
+        reducer.submit([dw_blk, dr_blk, db])
 
     def dense(blk, cols):  # [4][K_b][X_b][b_x][b_k] -> 4 x (K, X)
         return [blk[i].permute(0, 3, 1, 2).reshape(k, cols) for i in range(4)]
@@ -507,7 +511,7 @@ def lstm_backward(params: LstmParams, x, seq: LstmStateSequence, dh, h_init=None
     return out
 
 
-def _backward_seq(params, xd, hd, sd, gates, dhd, h0, s0, h_bf):
+def _backward_seq(params, xd, hd, sd, gates, dhd, h0, s0, h_bf, reducer=None):
     """BPTT on the persistent backward kernel, then the step-independent
     products as single BRGEMM launches over all T*N rows: dx = dpre W,
     dW = dpre^T x, dR = dpre^T h_prev, dh0 = dpre_0 R, db = column sums."""
@@ -527,10 +531,7 @@ def _backward_seq(params, xd, hd, sd, gates, dhd, h0, s0, h_bf):
     _lib.check(rc, LayoutError)
     rows = T * N
     dp2 = dpre.reshape(rows, 4 * K)
-    dh0 = torch.empty((N, K), dtype=torch.float32, device="cuda")
-    gemm(dp2[:N], sc.r_cat, dh0, b_t=True)                   # dh0 = dpre_0 [R_i; R_c; R_f; R_o]
-    dx = torch.empty((rows, C), dtype=torch.float32, device="cuda")
-    gemm(dp2, sc.w_cat, dx, b_t=True)                        # dx = dpre W_cat
+    # weight gradients first: in data parallel their all-reduces overlap dx / dh0 below
     xb = xd.to(torch.bfloat16)
     if h_bf is None:
         h_bf = torch.empty((T + 1, N, K), dtype=torch.bfloat16, device="cuda")
@@ -539,11 +540,19 @@ def _backward_seq(params, xd, hd, sd, gates, dhd, h0, s0, h_bf):
     hp = h_bf[:T].reshape(rows, K)
     dw = torch.empty((4 * K, C), dtype=torch.float32, device="cuda")
     gemm(dp2, xb, dw, a_t=True, b_t=True)                    # dW_cat = dpre^T x (reduction over T*N in TMEM)
+    if reducer is not None:
+        reducer.submit([dw])
     dr = torch.empty((4 * K, K), dtype=torch.float32, device="cuda")
     gemm(dp2, hp, dr, a_t=True, b_t=True)                    # dR_cat = dpre^T h_prev
     db = torch.empty(4 * K, dtype=torch.float32, device="cuda")
     _lib.check(lib.brk_colsum_blocked(dp2.data_ptr(), None, None, db.data_ptr(), rows, 4 * K, rows, 4 * K,
                                       _lib.BRK_BF16, st), LayoutError)
+    if reducer is not None:
+        reducer.submit([dr, db])
+    dh0 = torch.empty((N, K), dtype=torch.float32, device="cuda")
+    gemm(dp2[:N], sc.r_cat, dh0, b_t=True)                   # dh0 = dpre_0 [R_i; R_c; R_f; R_o]
+    dx = torch.empty((rows, C), dtype=torch.float32, device="cuda")
+    gemm(dp2, sc.w_cat, dx, b_t=True)                        # dx = dpre W_cat
     sl = lambda t: [t[i * K:(i + 1) * K] for i in range(4)]  # noqa: E731
     return LstmGrads(dx=dx.reshape(T, N, C), dw=dict(zip(GATE_NAMES, sl(dw))), dr=dict(zip(GATE_NAMES, sl(dr))),
                      db=dict(zip(GATE_NAMES, sl(db))), dh0=dh0, ds0=ds0)

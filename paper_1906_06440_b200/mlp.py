@@ -59,6 +59,12 @@ class MLP:
             w = (torch.rand(width, width, generator=g) * 2 - 1) / np.sqrt(width)
             self._wbuf[0].append(w.reshape(cb, B, cb, B).permute(0, 2, 3, 1).contiguous().to(device, bf))
             self.bias.append(((torch.rand(width, generator=g) * 2 - 1) * 0.1).to(device))
+        if process_group is not None:
+            # data parallel: every replica starts from rank 0's parameters (the ranks'
+            # seeds may differ; only their data shards should)
+            from .dist import broadcast_params
+
+            broadcast_params(self._wbuf[0] + self.bias, process_group)
         # activations: y[0] is the input, y[l] the output of layer l
         self.y = [torch.empty(nb, cb, B, B, dtype=bf, device=device) for _ in range(layers + 1)]
         self.dz = [torch.empty(nb, cb, B, B, dtype=bf, device=device) for _ in range(layers + 1)]

@@ -169,8 +169,8 @@ def test_in_place_weight_update_is_seen():
         params.w_i.data *= 0.5
         params.bias_f[:] += 0.25
         seq = lstm_forward(params, x)
-    wt.w_i *= 0.5
-    wt.bias_f += 0.25
     w, r, bias = oracle_args(wt)
+    w["i"] = w["i"] * 0.5
+    bias["f"] = np.asarray(params.bias_f).copy()  # (from_dense shares the bias arrays with wt)
     ref = orc.lstm_forward_reference(w, r, bias, x)
     check_parity("lstm.in_place_update.tf32.h", "3x8x64", orc.scale_rel_error(seq.h, ref["h"]), 1e-3)

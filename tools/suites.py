@@ -107,8 +107,11 @@ def resnet_suite(n=256, iters=10, layers=None, passes=("fwd", "bwd", "upd"), ver
         flops = 2.0 * n * k * c * r * s * p_ * q_
         e = 2
         act_in, act_out, wbytes = n * c * h * w * e, n * k * p_ * q_ * e, k * c * r * s * e
-        bytes_ = {"fwd": act_in + wbytes + act_out, "bwd": act_out + wbytes + act_in,
-                  "upd": act_in + act_out + k * c * r * s * 4}
+        # a 1x1 strided conv reads only the sampled input pixels (one in stride^2) in fwd / upd;
+        # bwd-data writes the whole input gradient (the skipped pixels get zeros)
+        act_read = n * c * p_ * q_ * e if (r == 1 and s == 1 and st > 1) else act_in
+        bytes_ = {"fwd": act_read + wbytes + act_out, "bwd": act_out + wbytes + act_in,
+                  "upd": act_read + act_out + k * c * r * s * 4}
         engine = bc == 64 and bk == 64
         calls = {}
         if engine:
@@ -142,7 +145,8 @@ def resnet_suite(n=256, iters=10, layers=None, passes=("fwd", "bwd", "upd"), ver
             mean, best = timer(calls[p], iters)
             t_roof = max(flops / (peak * 1e12), bytes_[p] / (hbm * 1e9))
             row[p] = {"us": mean * 1e6, "us_min": best * 1e6, "tflops": flops / mean / 1e12,
-                      "roof_frac": t_roof / mean}
+                      "roof_frac": t_roof / mean, "gbs": bytes_[p] / mean / 1e9,
+                      "bound": "tensor" if flops / (peak * 1e12) >= bytes_[p] / (hbm * 1e9) else "hbm"}
             if p == "bwd" and lid == 1:
                 continue
             for tt in (tot, tot_engine) if engine else (tot,):
@@ -317,6 +321,79 @@ def split_gemm_baseline(m=64, n=64, k=64, batch=16, iters=10):
     err = (c - c2).abs().max().item() / max(c.abs().max().item(), 1e-30)
     return {"shape": f"m=n=k={m} batch={batch} jobs={jobs}", "brgemm_us": t_br * 1e6, "split_gemm_us": t_sp * 1e6,
             "speedup": t_sp / t_br, "split_launches": batch, "max_rel_diff": err}
+
+
+def _dp_time(step, pg, iters, warmup=1):
+    """Mean device time of ``step`` (CUDA events on the current stream), max over ranks."""
+    import torch
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    if pg is not None:
+        import torch.distributed as dist
+        dist.barrier(group=pg)
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(iters):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    sec = e0.elapsed_time(e1) * 1e-3 / iters
+    if pg is not None:
+        import torch.distributed as dist
+        t = torch.tensor([sec], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=pg)
+        sec = float(t.item())
+    return sec
+
+
+def resnet_dp_suite(pg=None, n_global=256, iters=3):
+    """ResNet-50's 53 convs as one data-parallel training step (train.ResNetConvs): global
+    minibatch n_global split over the ranks (strong scaling), fwd + bwd-data + upd of every
+    conv, per-layer dW all-reduce overlapping the backward, SGD.  Whole-job TFLOP/s."""
+    from paper_1906_06440_b200.train import ResNetConvs
+
+    import torch
+
+    net = ResNetConvs(n_global=n_global, process_group=pg)
+    sec = _dp_time(net.step, pg, iters)
+    world = net.world
+    flops = net.flops_per_step(local=False)
+    peak, _, src = _peaks()
+    out = {"n_global": n_global, "n_per_gpu": net.n_local, "gpus": world, "ms_per_step": sec * 1e3,
+           "tflops": flops / sec / 1e12, "tflops_per_gpu": flops / sec / 1e12 / world,
+           "frac_of_peak_per_gpu": flops / sec / 1e12 / world / peak, "gflop_per_step": flops / 1e9,
+           "scaling": "strong", "convs": len(net.layers),
+           "note": "53 convs (20 shapes x count), bf16, fwd + bwd-data (stem included) + upd, per-layer NCCL "
+                   "all-reduce of dW on a comm stream in reverse order, SGD; device time, max over ranks"}
+    del net
+    torch.cuda.empty_cache()
+    return out
+
+
+def lstm_dp_suite(pg=None, n_per_gpu=168, iters=2):
+    """LSTM cell C=K=1024, T=50 data parallel (train.LstmDP): N=168 sequences per rank (weak
+    scaling), fwd + BPTT + weight update, dW/dR/db all-reduce overlapping dx, SGD."""
+    from paper_1906_06440_b200.train import LstmDP
+
+    import torch
+
+    net = LstmDP(n_local=n_per_gpu, process_group=pg)
+    sec = _dp_time(net.step, pg, iters)
+    world = net.world
+    flops = net.flops_per_step() * world
+    peak, _, src = _peaks()
+    out = {"n_per_gpu": n_per_gpu, "n_global": n_per_gpu * world, "gpus": world, "ms_per_step": sec * 1e3,
+           "tflops": flops / sec / 1e12, "tflops_per_gpu": flops / sec / 1e12 / world,
+           "frac_of_peak_per_gpu": flops / sec / 1e12 / world / peak, "gflop_per_step": flops / 1e9,
+           "scaling": "weak",
+           "note": "T=50, C=K=1024, bf16 compute, fwd + BPTT + upd, dW/dR/db NCCL all-reduce overlapping dx, "
+                   "SGD; device time, max over ranks"}
+    del net
+    torch.cuda.empty_cache()
+    return out
 
 
 def _plan(lib, pass_, geom):
