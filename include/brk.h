@@ -170,6 +170,21 @@ BRK_API int brk_colsum_blocked(const void* dy, const void* y, void* dz_out, floa
 BRK_API int brk_sgd_apply(void* w, const float* dw, float lr, int64_t n, int w_dtype, void* stream);
 
 /* ---------------------------------------------------------------------------
+ * Device layout transform.  Replaces the reference's blocked-layout copies
+ * (pkg/src/brkernels/tensor.py:143-275: block_weight_2d, block_conv_input,
+ * block_conv_weight, block_fc_activation, unblock_*, pad_spatial) on device
+ * tensors.  dst (contiguous, ndims <= 8 extents `shape`) receives
+ *   dst[i] = src[sum_d (i_d - pad_lo[d]) * src_strides[d]]  when every
+ *            0 <= i_d - pad_lo[d] < src_extent[d], else 0,
+ * with src_strides in elements (any permutation / split of a tensor);
+ * pad_lo / src_extent may be NULL (no padding).  in_dtype / out_dtype
+ * BRK_F32 or BRK_BF16 (conversion fused).  One HBM read + write per element.
+ * ------------------------------------------------------------------------- */
+BRK_API int brk_layout_transform(const void* src, void* dst, int ndims, const int64_t* shape,
+                                 const int64_t* src_strides, const int64_t* pad_lo, const int64_t* src_extent,
+                                 int in_dtype, int out_dtype, void* stream);
+
+/* ---------------------------------------------------------------------------
  * Direct convolution on the reference's blocked layouts (cnn.py:201-334;
  * tensor.py:160-235), implicit GEMM with TMA im2col operand fetch:
  *   in, din : [N][C/64][H][W][64]     out, dout : [N][K/64][P][Q][64]
@@ -218,6 +233,16 @@ BRK_API int brk_conv_plan(int pass, int N, int C, int K, int H, int W, int R, in
 BRK_API int brk_gemm_dense(const void* a, int64_t lda, int a_kmajor, const void* b, int64_t ldb, int b_kmajor,
                            void* c, int64_t ldc, int c_bf16, int64_t M, int N, int K, float alpha, float beta,
                            const float* bias, int act, void* workspace, size_t ws_bytes, void* stream);
+/* fp32 operands on the TF32 tensor cores (kind::tf32; the fp32 bit patterns are
+ * consumed as TF32 — pre-round with brk_round_tf32 for round-to-nearest);
+ * otherwise exactly brk_gemm_dense (same workspace query). */
+BRK_API int brk_gemm_dense_f32(const float* a, int64_t lda, int a_kmajor, const float* b, int64_t ldb,
+                               int b_kmajor, void* c, int64_t ldc, int c_bf16, int64_t M, int N, int K, float alpha,
+                               float beta, const float* bias, int act, void* workspace, size_t ws_bytes,
+                               void* stream);
+/* dst = round-to-nearest (ties away, cvt.rna) of fp32 src to TF32 precision, stored as fp32
+ * (dst may alias src).  The engine's TF32 paths feed on these. */
+BRK_API int brk_round_tf32(const float* src, float* dst, int64_t n, void* stream);
 BRK_API size_t brk_gemm_dense_workspace(int64_t M, int N, int K);
 
 /* ---------------------------------------------------------------------------

@@ -61,6 +61,7 @@ SIGNATURES: dict[str, tuple] = {
     "brk_fc_bias_grad_workspace": (ctypes.c_size_t, [_c_int]),
     "brk_colsum_blocked": (_c_int, [_vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp]),
     "brk_sgd_apply": (_c_int, [_vp, _vp, _c_f, _c_i64, _c_int, _vp]),
+    "brk_layout_transform": (_c_int, [_vp, _vp, _c_int, _vp, _vp, _vp, _vp, _c_int, _c_int, _vp]),
     "brk_conv_fwd": (_c_int, [_vp, _vp, _vp, _vp] + [_c_int] * 14 + [_vp]),
     "brk_conv_bwd_data": (_c_int, [_vp, _vp, _vp] + [_c_int] * 13 + [_vp]),
     "brk_conv_upd": (_c_int, [_vp, _vp, _vp, _vp, _c_f, _vp, ctypes.c_size_t] + [_c_int] * 13 + [_vp]),
@@ -71,6 +72,9 @@ SIGNATURES: dict[str, tuple] = {
     "brk_gemm_dense": (_c_int, [_vp, _c_i64, _c_int, _vp, _c_i64, _c_int, _vp, _c_i64, _c_int, _c_i64, _c_int,
                                 _c_int, _c_f, _c_f, _vp, _c_int, _vp, ctypes.c_size_t, _vp]),
     "brk_gemm_dense_workspace": (ctypes.c_size_t, [_c_i64, _c_int, _c_int]),
+    "brk_gemm_dense_f32": (_c_int, [_vp, _c_i64, _c_int, _vp, _c_i64, _c_int, _vp, _c_i64, _c_int, _c_i64, _c_int,
+                                    _c_int, _c_f, _c_f, _vp, _c_int, _vp, ctypes.c_size_t, _vp]),
+    "brk_round_tf32": (_c_int, [_vp, _vp, _c_i64, _vp]),
     "brk_lstm_seq_flags_bytes": (ctypes.c_size_t, [_c_int]),
     "brk_diag_lstm_timestamps": (None, [_vp]),
     "brk_lstm_seq_fwd": (_c_int, [_vp] * 8 + [_c_int, _c_int, _c_int, _vp]),

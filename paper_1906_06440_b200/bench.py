@@ -174,8 +174,10 @@ def _time(fn, iters: int) -> tuple[float, float]:
         graph.replay()
         torch.cuda.synchronize()
         run = graph.replay
-    except Exception:  # noqa: BLE001 - uncapturable call: eager timing
+    except Exception as exc:  # noqa: BLE001 - uncapturable call: eager timing, said out loud
         torch.cuda.synchronize()
+        _log(f"note: call not capturable in a CUDA graph ({type(exc).__name__}); timed eagerly "
+             f"(host-side work included)")
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(iters)]
     for a, b in evs:
         a.record()
@@ -209,6 +211,15 @@ def _verify(got, ref, name) -> bool:
     return ok
 
 
+def _maybe_dump(cfg: "BenchConfig", name: str, tensor) -> None:
+    """--dump DIR: the reference's binary dump of a workload's tensors (reference bench.py:267-271)."""
+    if cfg.dump:
+        from .tensor import dump_tensor
+        d = Path(cfg.dump)
+        d.mkdir(parents=True, exist_ok=True)
+        dump_tensor(tensor, d / f"{name}.bin")
+
+
 def _oracle():
     root = Path(__file__).resolve().parents[1]
     sys.path.insert(0, str(root / "oracle"))  # test infrastructure: only for --verify
@@ -233,17 +244,35 @@ def _run_conv(cfg: BenchConfig, rows: list[str]) -> int:
         inp, wgt = inp.to("cuda", torch.bfloat16), wgt.to("cuda", torch.bfloat16)
         flops = flops_conv(spec, spec.n)
         verified = None
-        if cfg.verify:
+        if cfg.verify or cfg.dump:
             got = unblock_conv_output(conv2d_forward(spec, inp, wgt).to("cpu"))
-            ref = _oracle().conv2d_forward_reference(i_d, w_d, stride=spec.stride, pad_h=spec.pad_h, pad_w=spec.pad_w)
-            verified = _verify(got, ref, f"conv id={lid}")
-            failures += 0 if verified else 1
+            if cfg.verify:
+                ref = _oracle().conv2d_forward_reference(i_d, w_d, stride=spec.stride, pad_h=spec.pad_h,
+                                                         pad_w=spec.pad_w)
+                verified = _verify(got, ref, f"conv id={lid}")
+                failures += 0 if verified else 1
+            _maybe_dump(cfg, f"conv_{lid:02d}_input", i_d)
+            _maybe_dump(cfg, f"conv_{lid:02d}_weights", w_d)
+            _maybe_dump(cfg, f"conv_{lid:02d}_output", got)
         res = None
         if cfg.iters > 0:
-            mean, tmin = _time(lambda: conv2d_forward(spec, inp, wgt), cfg.iters)
+            if cfg.include_reformat:
+                # the paper's reformatting cost on the device: dense fp32 NCHW / KCRS
+                # -> blocked bf16 (layout kernel, conversion fused), the conv, blocked -> dense fp32 output
+                i_dev, w_dev = torch.from_numpy(i_d).cuda(), torch.from_numpy(w_d).cuda()
+
+                def step():
+                    xi, wi = block_conv_tensors(i_dev, w_dev, spec.b_c, spec.b_k, dtype=torch.bfloat16)
+                    unblock_conv_output(conv2d_forward(spec, xi, wi))
+            else:
+                def step():
+                    conv2d_forward(spec, inp, wgt)
+            mean, tmin = _time(step, cfg.iters)
             res = BenchResult(flops, mean, tmin, cfg.iters, cfg.workers, verified)
             timed.append((res, rec.count))
-        nbytes = 2.0 * (spec.n * spec.c * spec.h * spec.w + spec.k * spec.c * spec.r * spec.s +
+        # algorithmic bytes: a 1x1 strided conv reads only the sampled input pixels
+        in_px = spec.out_h * spec.out_w if (spec.r == 1 and spec.s == 1 and spec.stride > 1) else spec.h * spec.w
+        nbytes = 2.0 * (spec.n * spec.c * in_px + spec.k * spec.c * spec.r * spec.s +
                         spec.n * spec.k * spec.out_h * spec.out_w)
         rows.append(_row("conv", lid, spec.n, cfg, flops, res, verified, nbytes))
     if timed:
@@ -257,38 +286,83 @@ def _run_lstm(cfg: BenchConfig, rows: list[str]) -> int:
 
     from . import precision
     from .lstm import LstmCellWeights, LstmParams, lstm_forward
-    rng = np.random.default_rng(cfg.seed)
-    params = LstmParams.from_dense(LstmCellWeights.random(rng, cfg.c, cfg.k), cfg.t_steps, cfg.minibatch)
-    x = torch.from_numpy(rng.uniform(-1, 1, (cfg.t_steps, cfg.minibatch, cfg.c)).astype(np.float32)).cuda()
-    flops = flops_lstm_fwd(cfg.t_steps, cfg.minibatch, cfg.c, cfg.k)
+    rng = np.random.default_rng([cfg.seed, 101])  # reference bench.py:331-334
+    t_steps, n, c, k = cfg.t_steps, cfg.minibatch, cfg.c, cfg.k
+    weights = LstmCellWeights.random(rng, c, k)
+    x_h = rng.uniform(-1, 1, (t_steps, n, c)).astype(np.float32)
+    params = LstmParams.from_dense(weights, t_steps, n)
+    x = torch.from_numpy(x_h).cuda()
+    flops = flops_lstm_fwd(t_steps, n, c, k)
+    failures, verified = 0, None
     with precision("bf16"):
+        if cfg.verify or cfg.dump:
+            seq = lstm_forward(params, x_h)
+            if cfg.verify:
+                orc = _oracle()
+                g = ("i", "c", "f", "o")
+                ref = orc.lstm_forward_reference({q: getattr(weights, f"w_{q}") for q in g},
+                                                 {q: getattr(weights, f"r_{q}") for q in g},
+                                                 {q: getattr(weights, f"bias_{q}") for q in g}, x_h)
+                verified = _verify(seq.h, ref["h"], "lstm h") and _verify(seq.s, ref["s"], "lstm s")
+                failures += 0 if verified else 1
+            _maybe_dump(cfg, "lstm_input", x_h)
+            _maybe_dump(cfg, "lstm_hidden", seq.h)
+            _maybe_dump(cfg, "lstm_state", seq.s)
         res = None
         if cfg.iters > 0:
-            mean, tmin = _time(lambda: lstm_forward(params, x), cfg.iters)
-            res = BenchResult(flops, mean, tmin, cfg.iters, cfg.workers)
-    rows.append(_row("lstm", 0, cfg.minibatch, cfg, flops, res, None))
-    return 0
+            if cfg.include_reformat:  # re-block the weights every call (reference bench.py:350-353)
+                def step():
+                    lstm_forward(LstmParams.from_dense(weights, t_steps, n), x)
+            else:
+                def step():
+                    lstm_forward(params, x)
+            mean, tmin = _time(step, cfg.iters)
+            res = BenchResult(flops, mean, tmin, cfg.iters, cfg.workers, verified)
+    rows.append(_row("lstm", 0, n, cfg, flops, res, verified))
+    return failures
 
 
 def _run_fc(cfg: BenchConfig, rows: list[str]) -> int:
     import torch
 
     from .fc import Activation, FcParams, fc_forward
-    from .tensor import block_fc_activation
-    rng = np.random.default_rng(cfg.seed)
+    from .tensor import block_fc_activation, unblock_fc_activation
+    rng = np.random.default_rng([cfg.seed, 202])  # reference bench.py:374-378
     n, c, k = cfg.minibatch, cfg.c, cfg.k
+    act = Activation(cfg.activation)
     w = rng.uniform(-1, 1, (k, c)).astype(np.float32)
-    params = FcParams.from_dense(w, n, activation=Activation(cfg.activation))
+    x_d = rng.uniform(-1, 1, (n, c)).astype(np.float32)
+    params = FcParams.from_dense(w, n, activation=act)
     params.w = params.w.to("cuda", torch.bfloat16)
-    x = block_fc_activation(rng.uniform(-1, 1, (n, c)).astype(np.float32), params.b_n, params.b_c)
-    x = x.to("cuda", torch.bfloat16)
+    x = block_fc_activation(x_d, params.b_n, params.b_c).to("cuda", torch.bfloat16)
     flops = flops_fc(n, c, k)
+    failures, verified = 0, None
+    if cfg.verify or cfg.dump:
+        y = unblock_fc_activation(fc_forward(params, x).to("cpu"))
+        if cfg.verify:
+            ref = _oracle().fc_forward_reference(w, x_d.T, act.value).T
+            verified = _verify(y, ref, "fc")
+            failures += 0 if verified else 1
+        _maybe_dump(cfg, "fc_input", x_d)
+        _maybe_dump(cfg, "fc_weights", w)
+        _maybe_dump(cfg, "fc_output", y)
     res = None
     if cfg.iters > 0:
-        mean, tmin = _time(lambda: fc_forward(params, x), cfg.iters)
-        res = BenchResult(flops, mean, tmin, cfg.iters, cfg.workers)
-    rows.append(_row("fc", 0, n, cfg, flops, res, None, 2.0 * (n * c + k * c + n * k)))
-    return 0
+        if cfg.include_reformat:  # dense fp32 on device -> blocked bf16 (layout kernel) every call
+            w_dev, x_dev = torch.from_numpy(w).cuda(), torch.from_numpy(x_d).cuda()
+            from .tensor import block_weight_2d
+
+            def step():
+                p = FcParams(w=block_weight_2d(w_dev, params.b_c, params.b_k, dtype=torch.bfloat16), n=n, c=c, k=k,
+                             b_n=params.b_n, b_c=params.b_c, b_k=params.b_k, activation=act)
+                unblock_fc_activation(fc_forward(p, block_fc_activation(x_dev, p.b_n, p.b_c, dtype=torch.bfloat16)))
+        else:
+            def step():
+                fc_forward(params, x)
+        mean, tmin = _time(step, cfg.iters)
+        res = BenchResult(flops, mean, tmin, cfg.iters, cfg.workers, verified)
+    rows.append(_row("fc", 0, n, cfg, flops, res, verified, 2.0 * (n * c + k * c + n * k)))
+    return failures
 
 
 def _run_brgemm(cfg: BenchConfig, rows: list[str]) -> int:
@@ -305,9 +379,22 @@ def _run_brgemm(cfg: BenchConfig, rows: list[str]) -> int:
     rows.append(_row("brgemm", 0, 1, cfg, flops, BenchResult(flops, mean, tmin, cfg.iters, 1), None,
                      2.0 * batch * (k * m + n * k) + 4.0 * n * m))
     if cfg.baseline:  # batched GEMM: one output per pair, no reduction (brgemm.py:340-353)
+        from . import _lib
+        from ._device import ptr_table, stream_ptr
         cs = torch.zeros(batch, n, m, device="cuda")
-        al, bl, cl = list(a), list(b), list(cs)
-        mean, tmin = _time(lambda: batched_gemm(al, bl, cl, spec), max(cfg.iters, 1))
+        batched_gemm(list(a), list(b), list(cs), spec)  # the public call once (checks, warm-up)
+        # the same launch batched_gemm issues, with its address tables built once outside the
+        # timed call so the graph capture sees only the kernel
+        ta = ptr_table([t.data_ptr() for t in a])
+        tb = ptr_table([t.data_ptr() for t in b])
+        tc = ptr_table([t.data_ptr() for t in cs])
+        lib = _lib.load()
+
+        def base():
+            _lib.check(lib.brk_brgemm_addr(ta.data_ptr(), tb.data_ptr(), tc.data_ptr(), batch, m, n, k, 1, m, k, m,
+                                           1.0, 0.0, _lib.BRK_BF16, _lib.BRK_F32, _lib.BRK_COMPUTE_BF16,
+                                           stream_ptr()))
+        mean, tmin = _time(base, max(cfg.iters, 1))
         rows.append(_row("brgemm_baseline", 0, 1, cfg, flops, BenchResult(flops, mean, tmin, cfg.iters, 1), None,
                          2.0 * batch * (k * m + n * k) + 4.0 * batch * n * m))
     return 0
@@ -335,8 +422,9 @@ def _build_parser() -> argparse.ArgumentParser:
     common.add_argument("--verify", action="store_true", help="check against the fp64 oracle before timing")
     common.add_argument("--peak-gflops", type=float, default=None, help="peak GFLOP/s for efficiency")
     common.add_argument("--csv", type=str, default=None, help="CSV output path")
-    common.add_argument("--dump", type=str, default=None, help="accepted for CLI compatibility")
-    common.add_argument("--include-reformat", action="store_true", help="accepted for CLI compatibility")
+    common.add_argument("--dump", type=str, default=None, help="directory for binary tensor dumps")
+    common.add_argument("--include-reformat", action="store_true",
+                        help="time the dense -> blocked layout transforms (device kernel) with each call")
     common.add_argument("--seed", type=int, default=0)
     parser = argparse.ArgumentParser(prog="bench", description="Batch-reduce GEMM kernel benchmarks (B200)")
     sub = parser.add_subparsers(dest="workload", required=True)

@@ -8,6 +8,27 @@
 namespace brk {
 namespace {
 
+// fp32 -> TF32 (10-bit mantissa) round-to-nearest, ties away (cvt.rna.tf32.f32), kept as fp32 bits
+__global__ void round_tf32_kernel(const float* __restrict__ src, float* __restrict__ dst, int64_t n) {
+  const int64_t nv = n / 4;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nv;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float4 v = reinterpret_cast<const float4*>(src)[i];
+    uint32_t r[4];
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r[0]) : "f"(v.x));
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r[1]) : "f"(v.y));
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r[2]) : "f"(v.z));
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r[3]) : "f"(v.w));
+    reinterpret_cast<float4*>(dst)[i] = make_float4(__uint_as_float(r[0]), __uint_as_float(r[1]),
+                                                    __uint_as_float(r[2]), __uint_as_float(r[3]));
+  }
+  if (blockIdx.x == 0 && threadIdx.x < n - nv * 4) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(src[nv * 4 + threadIdx.x]));
+    dst[nv * 4 + threadIdx.x] = __uint_as_float(r);
+  }
+}
+
 __device__ __forceinline__ float ld_any(const void* p, int64_t i, int bf16) {
   return bf16 ? __bfloat162float(static_cast<const __nv_bfloat16*>(p)[i]) : static_cast<const float*>(p)[i];
 }
@@ -86,6 +107,19 @@ BRK_API int brk_colsum_blocked(const void* dy, const void* y, void* dz_out, floa
   cudaError_t err2 = cudaFreeAsync(part, st);
   if (err != cudaSuccess) return set_cuda_error(err, "colsum launch");
   return err2 == cudaSuccess ? BRK_OK : set_cuda_error(err2, "colsum scratch free");
+}
+
+BRK_API int brk_round_tf32(const float* src, float* dst, int64_t n, void* stream) {
+  if (n < 0) return set_error(BRK_ERR_CONTRACT, "round_tf32: n must be >= 0");
+  if (n == 0) return BRK_OK;
+  if ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15)
+    return set_error(BRK_ERR_CONTRACT, "round_tf32: 16-byte aligned buffers");
+  g_launches.fetch_add(1);
+  const int64_t vec = (n + 3) / 4;
+  const int blocks = static_cast<int>(vec / 256 + 1 < 148 * 8 ? vec / 256 + 1 : 148 * 8);
+  round_tf32_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(src, dst, n);
+  cudaError_t err = cudaGetLastError();
+  return err == cudaSuccess ? BRK_OK : set_cuda_error(err, "round_tf32 launch");
 }
 
 BRK_API int brk_sgd_apply(void* w, const float* dw, float lr, int64_t n, int w_dtype, void* stream) {

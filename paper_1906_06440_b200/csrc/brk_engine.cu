@@ -394,7 +394,20 @@ __device__ __forceinline__ void epilogue_stage(const EpiView& p, float (&f)[32],
 // outputs, SGD weights for fp32 outputs) do not depend on the accumulator:
 // they are fetched for the first segments before the epilogue waits for it.
 __device__ __forceinline__ const void* flush_src(const EpiView& p) {
-  return p.out_bf16 ? (p.mask != nullptr ? p.mask : p.aux_in) : (p.sgd_w != nullptr ? p.sgd_src : nullptr);
+  if (p.out_bf16) return p.mask != nullptr ? p.mask : p.aux_in;
+  // fp32 outputs: the fp32 ReLU mask (TF32 backward-data) or the bf16 weights of the fused SGD
+  return p.mask != nullptr ? p.mask : (p.sgd_w != nullptr ? p.sgd_src : nullptr);
+}
+// The 16 B flush operand of destination element e: 8 bf16 (bf16 outputs), 4 fp32 (fp32 mask),
+// or 4 bf16 widened into the low half (bf16 SGD weights of an fp32 weight gradient).
+__device__ __forceinline__ uint4 flush_load(const EpiView& p, const void* src, int64_t e, bool streaming) {
+  if (p.out_bf16) {
+    const uint4* q = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(src) + e);
+    return streaming ? __ldcs(q) : *q;
+  }
+  if (p.mask != nullptr) return *reinterpret_cast<const uint4*>(static_cast<const float*>(src) + e);
+  const uint2 w2 = *reinterpret_cast<const uint2*>(static_cast<const __nv_bfloat16*>(src) + e);
+  return make_uint4(w2.x, w2.y, 0u, 0u);
 }
 template <int kLanes>
 __device__ __forceinline__ void epilogue_prefetch(const EpiView& p, int64_t roff, uint32_t ok, int64_t coff,
@@ -410,11 +423,7 @@ __device__ __forceinline__ void epilogue_prefetch(const EpiView& p, int64_t roff
     const int64_t ro = __shfl_sync(0xffffffffu, roff, r);
     if (!((ok >> r) & 1u)) continue;
     const int64_t e = ro + coff + s * (16 / esz);
-    if (p.out_bf16) pre[i] = __ldcs(reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(src) + e));
-    else {
-      const uint2 w2 = *reinterpret_cast<const uint2*>(static_cast<const __nv_bfloat16*>(src) + e);
-      pre[i] = make_uint4(w2.x, w2.y, 0u, 0u);
-    }
+    pre[i] = flush_load(p, src, e, true);
   }
 }
 
@@ -447,11 +456,7 @@ __device__ __forceinline__ void epilogue_flush(const EpiView& p, uint32_t stage,
 #pragma unroll
       for (int i = 0; i < kLanes; ++i) {
         if (!okr[i]) continue;
-        if (p.out_bf16) ld[i] = *reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(src) + eo[i]);
-        else {
-          const uint2 w2 = *reinterpret_cast<const uint2*>(static_cast<const __nv_bfloat16*>(src) + eo[i]);
-          ld[i] = make_uint4(w2.x, w2.y, 0u, 0u);
-        }
+        ld[i] = flush_load(p, src, eo[i], false);
       }
     }
   }
@@ -469,6 +474,15 @@ __device__ __forceinline__ void epilogue_flush(const EpiView& p, uint32_t stage,
       const __nv_bfloat162* mh = reinterpret_cast<const __nv_bfloat162*>(&ld[i]);
 #pragma unroll
       for (int j = 0; j < 4; ++j) h[j] = __hmul2(h[j], __hgt2(mh[j], zero2));
+    }
+  }
+  if (kFull && !p.out_bf16 && p.mask != nullptr) {  // fp32 outputs (TF32 path): v * (mask > 0)
+#pragma unroll
+    for (int i = 0; i < kLanes; ++i) {
+      float* f4 = reinterpret_cast<float*>(&v[i]);
+      const float* m4 = reinterpret_cast<const float*>(&ld[i]);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) f4[j] = m4[j] > 0.0f ? f4[j] : 0.0f;
     }
   }
 #pragma unroll
@@ -1203,10 +1217,35 @@ int launch_group_t(const EngineGroup& G, int grid, cudaStream_t stream) {
     attrs[na].val.clusterDim.z = 1;
     ++na;
   }
+  cfg.attrs = attrs;
+  cfg.numAttrs = na;
+  // The grouped kernel's tiles spin on completion counters of earlier problems, so every
+  // CTA of the grid must be resident at once.  Verified once per instantiation against the
+  // occupancy calculator (clusters for CTA pairs); a grid that cannot be co-resident is a
+  // contract error instead of a hang.  (Concurrent work that occupies SMs — another stream,
+  // MPS with an SM limit — can still delay residency; the step is launched alone.)
+  static int resident_units = -1;
+  if (resident_units < 0) {
+    int units = 0;
+    if (kPair) {
+      err = cudaOccupancyMaxActiveClusters(&units, kern, &cfg);
+    } else {
+      int per_sm = 0;
+      err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Cfg::kThreads, Cfg::kSmem);
+      units = per_sm * engine_sm_count();
+    }
+    if (err != cudaSuccess) return set_cuda_error(err, "engine group occupancy");
+    resident_units = units;
+  }
+  if (resident_units * (kPair ? 2 : 1) < grid) {
+    char buf[160];
+    std::snprintf(buf, sizeof(buf), "engine group: %d CTAs must be co-resident, the device holds %d",
+                  grid, resident_units * (kPair ? 2 : 1));
+    return set_error(BRK_ERR_CONTRACT, buf);
+  }
   attrs[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attrs[na].val.programmaticStreamSerializationAllowed = 1;
   ++na;
-  cfg.attrs = attrs;
   cfg.numAttrs = na;
   err = cudaLaunchKernelEx(&cfg, kern, G);
   if (err != cudaSuccess) return set_cuda_error(err, "engine group launch");

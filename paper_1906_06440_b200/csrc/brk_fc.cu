@@ -128,10 +128,49 @@ void set_coords(OperandCoords& oc, std::initializer_list<int> rc, std::initializ
   oc.ndims = 4;
 }
 
+// fp32 storage (TF32 tensor cores): a 64-wide block row is 256 B, two 128 B swizzle
+// atoms.  The maps view every blocked tensor with the 64-wide inner dimension split
+// into (32 elements, half) — the half as its own dimension with a 32-element
+// stride — so one TMA box is one 32-wide (128 B) atom column, a k-step covers 32
+// elements of the reduction (k-step s: half s % 2, block s / 2) and an MN-major
+// box lists its 32 x 32 atoms in MN order.  Dims: (x32, r_in, xhalf, xb, rb) for
+// [Rb][Xb][64 r][64 x] (x innermost), strides (1, 64, 32, 4096, Xb*4096).
+struct Map5 {
+  uint64_t dims[5];
+  uint64_t strides[5];
+};
+Map5 split_layout(int64_t rows, int64_t xs) {
+  Map5 a;
+  a.dims[0] = 32; a.dims[1] = kB; a.dims[2] = 2; a.dims[3] = xs / kB; a.dims[4] = rows / kB;
+  a.strides[0] = 1; a.strides[1] = kB; a.strides[2] = 32; a.strides[3] = kB * kB; a.strides[4] = (xs / kB) * kB * kB;
+  return a;
+}
+int enc5(CUtensorMap* map, const void* ptr, const Map5& l, std::initializer_list<uint32_t> box) {
+  uint32_t b[5];
+  int d = 0;
+  for (uint32_t v : box) b[d++] = v;
+  return encode_tmap(map, ptr, false, 5, l.dims, l.strides, b);
+}
+// f32 coordinates: rowblk advances dim rdim by rstep; k-step s: dim hdim += hstep * (s % 2),
+// dim bdim += s / 2
+void set_coords_f32(OperandCoords& oc, int rdim, int rstep, int hdim, int hstep, int bdim, uint32_t load_bytes,
+                    int n_loads, int mn_major) {
+  std::memset(&oc, 0, sizeof(oc));
+  oc.rc[rdim] = rstep;
+  oc.kc[0][hdim] = hstep;
+  oc.kc[1][bdim] = 1;
+  oc.kdiv0 = 2;
+  oc.kdiv1 = 1 << 30;
+  oc.n_loads = n_loads;
+  oc.load_bytes = load_bytes;
+  oc.mn_major = mn_major;
+  oc.ndims = 5;
+}
+
 int check_fc(int N, int C, int K, int b_n, int b_c, int b_k, int dtype) {
   char buf[256];
-  if (dtype != BRK_BF16)
-    return set_error(BRK_ERR_CONTRACT, "fc engine path: bf16 storage only (use the generic BRGEMM path)");
+  if (dtype != BRK_BF16 && dtype != BRK_F32)
+    return set_error(BRK_ERR_CONTRACT, "fc engine path: bf16 (kind::f16) or fp32 (kind::tf32) storage");
   if (b_n != kB || b_c != kB || b_k != kB) {
     std::snprintf(buf, sizeof(buf), "fc engine path needs b_n=b_c=b_k=64, got (%d,%d,%d)", b_n, b_c, b_k);
     return set_error(BRK_ERR_CONTRACT, buf);
@@ -156,13 +195,13 @@ int debug_flags() {
 
 unsigned long long* g_debug_ts = nullptr;  // set by brk_diag_set_timestamps
 
-int finish(const EngineParams& p, const Plan& pl, void* stream) {
+int finish(const EngineParams& p, const Plan& pl, void* stream, int tf32 = 0) {
   if (g_capture != nullptr) {
     *g_capture = p;
     return BRK_OK;
   }
   g_launches.fetch_add(1);
-  return launch_engine(p, pl.bn, 0, pl.pair, 0, static_cast<cudaStream_t>(stream));
+  return launch_engine(p, pl.bn, tf32, pl.pair, 0, static_cast<cudaStream_t>(stream));
 }
 
 // ---------------------------------------------------------------------------
@@ -245,28 +284,40 @@ BRK_API int brk_fc_fwd(const void* x, const void* w, const float* bias, void* y,
   if (act < kActNone || act > kActSigmoid) return set_error(BRK_ERR_CONTRACT, "unknown activation");
   EngineParams p;
   std::memset(&p, 0, sizeof(p));
+  const bool f32 = dtype == BRK_F32;
   const Plan pl = choose_plan(N, K, C / kB, false);
   const int brows = pl.pair ? pl.bn / 2 : pl.bn;
-  // A = X (rows n, red c) K-major: box (c 64, n 64, cb 1, nb 2) = 128 rows
-  if ((rc = enc(&p.map_a, x, act_layout(N, C), 64, 64, 1, 2))) return rc;
-  set_coords(p.ca, {0, 0, 0, 2}, {0, 0, 1, 0}, 128 * 128, 0);
-  // B = W (rows k, red c) MN-major: box (k 64, c 64, cb 1, kb brows/64)
-  if ((rc = enc(&p.map_b, w, w_layout(K, C), 64, 64, 1, brows / 64))) return rc;
-  set_coords(p.cb, {0, 0, 0, brows / 64}, {0, 0, 1, 0}, brows * 128, 1);
+  if (!f32) {
+    // A = X (rows n, red c) K-major: box (c 64, n 64, cb 1, nb 2) = 128 rows
+    if ((rc = enc(&p.map_a, x, act_layout(N, C), 64, 64, 1, 2))) return rc;
+    set_coords(p.ca, {0, 0, 0, 2}, {0, 0, 1, 0}, 128 * 128, 0);
+    // B = W (rows k, red c) MN-major: box (k 64, c 64, cb 1, kb brows/64)
+    if ((rc = enc(&p.map_b, w, w_layout(K, C), 64, 64, 1, brows / 64))) return rc;
+    set_coords(p.cb, {0, 0, 0, brows / 64}, {0, 0, 1, 0}, brows * 128, 1);
+  } else {
+    // A = X K-major: box (c 32, n 64, half 1, cb 1, nb 2) = 128 rows x 128 B
+    if ((rc = enc5(&p.map_a, x, split_layout(N, C), {32, 64, 1, 1, 2}))) return rc;
+    set_coords_f32(p.ca, 4, 2, 2, 1, 3, 128 * 128, 1, 0);
+    // B = W MN-major (x = k, r = c): box (k 32, c 32, khalf 2, cb 1, kb brows/64): brows/32 atoms
+    if ((rc = enc5(&p.map_b, w, split_layout(K, C), {32, 32, 2, 1, (uint32_t)(brows / 64)}))) return rc;
+    // (W's blocked layout [Kb][Cb][64 c][64 k] is split_layout(rows = K, xs = C) with the roles
+    //  of its inner dims read as (k32, c_in, khalf, cb, kb): strides (1, 64, 32, 4096, Cb*4096))
+    set_coords_f32(p.cb, 4, brows / 64, 1, 32, 3, brows * 128, 1, 1);
+  }
   p.m_tiles = N / (pl.pair ? 256 : 128);
   p.n_tiles = K / pl.bn;
-  p.k_steps = C / kB;
+  p.k_steps = f32 ? C / 32 : C / kB;
   p.rows = N;
   p.cols = K;
   p.out = y;
-  p.out_bf16 = 1;
+  p.out_bf16 = f32 ? 0 : 1;
   p.om = OutMap{kB, (int64_t)(K / kB) * kB * kB, kB, kB, kB * kB, 1, int64_t(0x7fffffff), 0};
   p.alpha = 1.0f;
   p.bias = bias;
   p.act = act;
   p.debug_flags = debug_flags();
   p.debug_ts = g_debug_ts;
-  return finish(p, pl, stream);
+  return finish(p, pl, stream, f32);
 }
 
 BRK_API int brk_fc_bwd_data(const void* dz, const void* w, const void* mask, void* dx, float* colsum_ws,
@@ -276,27 +327,37 @@ BRK_API int brk_fc_bwd_data(const void* dz, const void* w, const void* mask, voi
   EngineParams p;
   std::memset(&p, 0, sizeof(p));
   p.colsum_ws = colsum_ws;
+  const bool f32 = dtype == BRK_F32;
   const Plan pl = choose_plan(N, C, K / kB, false);
   const int brows = pl.pair ? pl.bn / 2 : pl.bn;
-  // A = dZ (rows n, red k) K-major
-  if ((rc = enc(&p.map_a, dz, act_layout(N, K), 64, 64, 1, 2))) return rc;
-  set_coords(p.ca, {0, 0, 0, 2}, {0, 0, 1, 0}, 128 * 128, 0);
-  // B = W (rows c, red k) K-major: dims (k_in, c_in, cb, kb), box (64, 64, brows/64, 1)
-  if ((rc = enc(&p.map_b, w, w_layout(K, C), 64, 64, brows / 64, 1))) return rc;
-  set_coords(p.cb, {0, 0, brows / 64, 0}, {0, 0, 0, 1}, brows * 128, 0);
+  if (!f32) {
+    // A = dZ (rows n, red k) K-major
+    if ((rc = enc(&p.map_a, dz, act_layout(N, K), 64, 64, 1, 2))) return rc;
+    set_coords(p.ca, {0, 0, 0, 2}, {0, 0, 1, 0}, 128 * 128, 0);
+    // B = W (rows c, red k) K-major: dims (k_in, c_in, cb, kb), box (64, 64, brows/64, 1)
+    if ((rc = enc(&p.map_b, w, w_layout(K, C), 64, 64, brows / 64, 1))) return rc;
+    set_coords(p.cb, {0, 0, brows / 64, 0}, {0, 0, 0, 1}, brows * 128, 0);
+  } else {
+    // A = dZ K-major: box (k 32, n 64, half 1, kb 1, nb 2)
+    if ((rc = enc5(&p.map_a, dz, split_layout(N, K), {32, 64, 1, 1, 2}))) return rc;
+    set_coords_f32(p.ca, 4, 2, 2, 1, 3, 128 * 128, 1, 0);
+    // B = W (rows c, red k) K-major on (k32, c_in, khalf, cb, kb): box (32, 64, 1, brows/64, 1)
+    if ((rc = enc5(&p.map_b, w, split_layout(K, C), {32, 64, 1, (uint32_t)(brows / 64), 1}))) return rc;
+    set_coords_f32(p.cb, 3, brows / 64, 2, 1, 4, brows * 128, 1, 0);
+  }
   p.m_tiles = N / (pl.pair ? 256 : 128);
   p.n_tiles = C / pl.bn;
-  p.k_steps = K / kB;
+  p.k_steps = f32 ? K / 32 : K / kB;
   p.rows = N;
   p.cols = C;
   p.out = dx;
-  p.out_bf16 = 1;
+  p.out_bf16 = f32 ? 0 : 1;
   p.om = OutMap{kB, (int64_t)(C / kB) * kB * kB, kB, kB, kB * kB, 1, int64_t(0x7fffffff), 0};
   p.alpha = 1.0f;
   p.mask = mask;
   p.debug_flags = debug_flags();
   p.debug_ts = g_debug_ts;
-  return finish(p, pl, stream);
+  return finish(p, pl, stream, f32);
 }
 
 // Split-K workspace of brk_fc_upd: [counters: 4 KiB][fp32 partial tiles].
@@ -335,15 +396,27 @@ BRK_API int brk_fc_upd(const void* x, const void* dz, float* dw, void* w_sgd, fl
     p.bias_lr = bias_lr;
   }
   const int brows = pl.pair ? pl.bn / 2 : pl.bn;
-  // A = X^T (rows c, red n) MN-major: box (c 64, n 64, cb 2, nb 1) -> 2 atoms of 64 rows
-  if ((rc = enc(&p.map_a, x, act_layout(N, C), 64, 64, 2, 1))) return rc;
-  set_coords(p.ca, {0, 0, 2, 0}, {0, 0, 0, 1}, 128 * 128, 1);
-  // B = dZ^T (rows k, red n) MN-major: box (k 64, n 64, kb brows/64, nb 1)
-  if ((rc = enc(&p.map_b, dz, act_layout(N, K), 64, 64, brows / 64, 1))) return rc;
-  set_coords(p.cb, {0, 0, brows / 64, 0}, {0, 0, 0, 1}, brows * 128, 1);
+  const bool f32 = dtype == BRK_F32;
+  if (f32 && w_sgd != nullptr)
+    return set_error(BRK_ERR_CONTRACT, "fc_upd: the fused SGD updates bf16 weights (fp32: use brk_sgd_apply)");
+  if (!f32) {
+    // A = X^T (rows c, red n) MN-major: box (c 64, n 64, cb 2, nb 1) -> 2 atoms of 64 rows
+    if ((rc = enc(&p.map_a, x, act_layout(N, C), 64, 64, 2, 1))) return rc;
+    set_coords(p.ca, {0, 0, 2, 0}, {0, 0, 0, 1}, 128 * 128, 1);
+    // B = dZ^T (rows k, red n) MN-major: box (k 64, n 64, kb brows/64, nb 1)
+    if ((rc = enc(&p.map_b, dz, act_layout(N, K), 64, 64, brows / 64, 1))) return rc;
+    set_coords(p.cb, {0, 0, brows / 64, 0}, {0, 0, 0, 1}, brows * 128, 1);
+  } else {
+    // A = X^T MN-major on (c32, n_in, chalf, cb, nb): box (32, 32, 2, 2, 1) = 4 atoms (128 rows)
+    if ((rc = enc5(&p.map_a, x, split_layout(N, C), {32, 32, 2, 2, 1}))) return rc;
+    set_coords_f32(p.ca, 3, 2, 1, 32, 4, 128 * 128, 1, 1);
+    // B = dZ^T MN-major: box (32, 32, 2, brows/64, 1)
+    if ((rc = enc5(&p.map_b, dz, split_layout(N, K), {32, 32, 2, (uint32_t)(brows / 64), 1}))) return rc;
+    set_coords_f32(p.cb, 3, brows / 64, 1, 32, 4, brows * 128, 1, 1);
+  }
   p.m_tiles = C / (pl.pair ? 256 : 128);
   p.n_tiles = K / pl.bn;
-  p.k_steps = N / kB;
+  p.k_steps = f32 ? N / 32 : N / kB;
   p.rows = C;
   p.cols = K;
   p.out = dw;
@@ -355,7 +428,7 @@ BRK_API int brk_fc_upd(const void* x, const void* dz, float* dw, void* w_sgd, fl
   p.sgd_lr = lr;
   p.debug_flags = debug_flags();
   p.debug_ts = g_debug_ts;
-  return finish(p, pl, stream);
+  return finish(p, pl, stream, f32);
 }
 
 // dz_out = dy * (y > 0) when y != NULL (dz_out may alias dy), db = column sums,

@@ -30,11 +30,35 @@ namespace {
 //   K-major : 2-d (K, rows), box (64, box_rows)            -> one load
 //   MN-major: 2-d (rows, K), box (64, 64), box_rows/64 loads (64-wide atoms)
 int operand_map(CUtensorMap* map, OperandCoords& oc, const void* ptr, int64_t rows, int64_t K, int64_t ld,
-                int kmajor, int box_rows) {
+                int kmajor, int box_rows, bool f32 = false) {
   std::memset(&oc, 0, sizeof(oc));
   oc.kdiv0 = 1 << 30;
   oc.kdiv1 = 1;
   oc.ndims = 2;
+  if (f32) {
+    // fp32 (TF32): one k-step = 32 elements of K (a 128 B swizzle atom column)
+    if (kmajor) {
+      const uint64_t dims[2] = {(uint64_t)K, (uint64_t)rows};
+      const uint64_t strides[2] = {1, (uint64_t)ld};
+      const uint32_t box[2] = {32, (uint32_t)box_rows};
+      oc.rc[1] = box_rows;
+      oc.kc[0][0] = 32;
+      oc.n_loads = 1;
+      oc.load_bytes = box_rows * 128;
+      oc.mn_major = 0;
+      return encode_tmap(map, ptr, false, 2, dims, strides, box);
+    }
+    const uint64_t dims[2] = {(uint64_t)rows, (uint64_t)K};
+    const uint64_t strides[2] = {1, (uint64_t)ld};
+    const uint32_t box[2] = {32, 32};
+    oc.rc[0] = box_rows;
+    oc.lc[0] = 32;
+    oc.kc[0][1] = 32;
+    oc.n_loads = box_rows / 32;
+    oc.load_bytes = 32 * 128;
+    oc.mn_major = 1;
+    return encode_tmap(map, ptr, false, 2, dims, strides, box);
+  }
   if (kmajor) {
     const uint64_t dims[2] = {(uint64_t)K, (uint64_t)rows};
     const uint64_t strides[2] = {1, (uint64_t)ld};
@@ -110,12 +134,12 @@ extern "C" {
 
 BRK_API size_t brk_gemm_dense_workspace(int64_t M, int N, int K) { return gemm_dense_workspace(M, N, K); }
 
-BRK_API int brk_gemm_dense(const void* a, int64_t lda, int a_kmajor, const void* b, int64_t ldb, int b_kmajor,
+static int gemm_dense_impl(const void* a, int64_t lda, int a_kmajor, const void* b, int64_t ldb, int b_kmajor,
                            void* c, int64_t ldc, int c_bf16, int64_t M, int N, int K, float alpha, float beta,
-                           const float* bias, int act, void* workspace, size_t ws_bytes, void* stream) {
+                           const float* bias, int act, void* workspace, size_t ws_bytes, void* stream, bool f32) {
   char buf[256];
-  // K need not be a multiple of 64: the operand maps zero-fill the tail of the last k-step
-  if (M <= 0 || N <= 0 || K <= 0 || N % 64 || lda % 8 || ldb % 8 || ldc % 4) {
+  // K need not be a multiple of the k-step: the operand maps zero-fill the tail of the last k-step
+  if (M <= 0 || N <= 0 || K <= 0 || N % 64 || lda % (f32 ? 4 : 8) || ldb % (f32 ? 4 : 8) || ldc % 4) {
     std::snprintf(buf, sizeof(buf),
                   "gemm_dense: need M, N, K > 0, N a multiple of 64, 16-byte aligned rows (M=%lld N=%d K=%d)",
                   (long long)M, N, K);
@@ -123,10 +147,11 @@ BRK_API int brk_gemm_dense(const void* a, int64_t lda, int a_kmajor, const void*
   }
   if (M >= (int64_t(1) << 31)) return set_error(BRK_ERR_CONTRACT, "gemm_dense: M must fit int32");
   if (act < kActNone || act > kActSigmoid) return set_error(BRK_ERR_CONTRACT, "unknown activation");
-  const int k_steps = (K + 63) / 64;
+  const int k_steps = f32 ? (K + 31) / 32 : (K + 63) / 64;
   const bool split_ok = workspace != nullptr && beta == 0.0f && bias == nullptr && act == kActNone && !c_bf16 &&
                         alpha == 1.0f;
-  const GemmPlan pl = gemm_plan(M, N, k_steps, split_ok);
+  // planned in 64-element k-steps for both storage types (matches brk_gemm_dense_workspace)
+  const GemmPlan pl = gemm_plan(M, N, (K + 63) / 64, split_ok);
   if (pl.bn == 0) return set_error(BRK_ERR_CONTRACT, "gemm_dense: no engine tile fits N");
   if (pl.splits > 1 && ws_bytes < static_cast<size_t>(pl.splits) * M * N * sizeof(float))
     return set_error(BRK_ERR_CONTRACT, "gemm_dense: workspace too small (see brk_gemm_dense_workspace)");
@@ -135,8 +160,8 @@ BRK_API int brk_gemm_dense(const void* a, int64_t lda, int a_kmajor, const void*
   EngineParams p;
   std::memset(&p, 0, sizeof(p));
   int rc;
-  if ((rc = operand_map(&p.map_a, p.ca, a, M, K, lda, a_kmajor, 128))) return rc;
-  if ((rc = operand_map(&p.map_b, p.cb, b, N, K, ldb, b_kmajor, brows))) return rc;
+  if ((rc = operand_map(&p.map_a, p.ca, a, M, K, lda, a_kmajor, 128, f32))) return rc;
+  if ((rc = operand_map(&p.map_b, p.cb, b, N, K, ldb, b_kmajor, brows, f32))) return rc;
   p.m_tiles = static_cast<int>((M + (pl.pair ? 255 : 127)) / (pl.pair ? 256 : 128));
   p.n_tiles = N / pl.bn;
   p.k_steps = k_steps;
@@ -160,10 +185,25 @@ BRK_API int brk_gemm_dense(const void* a, int64_t lda, int a_kmajor, const void*
     p.out = c;
   }
   g_launches.fetch_add(1);
-  rc = launch_engine(p, pl.bn, 0, pl.pair, 0, static_cast<cudaStream_t>(stream));
+  rc = launch_engine(p, pl.bn, f32 ? 1 : 0, pl.pair, 0, static_cast<cudaStream_t>(stream));
   if (rc || pl.splits <= 1) return rc;
   return split_reduce(static_cast<const float*>(workspace), pl.splits, M * static_cast<int64_t>(N),
                       static_cast<float*>(c), nullptr, 0.0f, static_cast<cudaStream_t>(stream));
+}
+
+BRK_API int brk_gemm_dense(const void* a, int64_t lda, int a_kmajor, const void* b, int64_t ldb, int b_kmajor,
+                           void* c, int64_t ldc, int c_bf16, int64_t M, int N, int K, float alpha, float beta,
+                           const float* bias, int act, void* workspace, size_t ws_bytes, void* stream) {
+  return gemm_dense_impl(a, lda, a_kmajor, b, ldb, b_kmajor, c, ldc, c_bf16, M, N, K, alpha, beta, bias, act,
+                         workspace, ws_bytes, stream, false);
+}
+
+BRK_API int brk_gemm_dense_f32(const float* a, int64_t lda, int a_kmajor, const float* b, int64_t ldb,
+                               int b_kmajor, void* c, int64_t ldc, int c_bf16, int64_t M, int N, int K, float alpha,
+                               float beta, const float* bias, int act, void* workspace, size_t ws_bytes,
+                               void* stream) {
+  return gemm_dense_impl(a, lda, a_kmajor, b, ldb, b_kmajor, c, ldc, c_bf16, M, N, K, alpha, beta, bias, act,
+                         workspace, ws_bytes, stream, true);
 }
 
 }  // extern "C"
