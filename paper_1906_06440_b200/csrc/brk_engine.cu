@@ -138,9 +138,13 @@ __device__ __forceinline__ uint64_t operand_desc(uint32_t base, int mn_major, in
     // K-major, 128B swizzle: 8-row groups 1024 B apart; K advance = 32 B.
     return make_smem_desc(base + kk * 32, 16, 1024, kSwizzle128B);
   }
-  // MN-major, 128B swizzle: atom = 128 B of MN x BK rows; 8 K-rows = 1024 B.
+  // MN-major: atom = 128 B of MN x BK rows (BK = 64 bf16 / 32 TF32 K-rows).  bf16: 128B
+  // swizzle, 8 K-rows = 1024 B (SBO).  TF32 requires the 32 B-chunk 128B swizzle
+  // (SWIZZLE_128B_BASE32B, TMA CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) whose K groups are
+  // 4 rows = 512 B; one MMA (K = 8) spans two of them.
   constexpr uint32_t kRowsPerMma = kTF32 ? 8 : 16;
   constexpr uint32_t kAtomBytes = (kTF32 ? 32 : 64) * 128;  // BK rows x 128 B
+  if constexpr (kTF32) return make_smem_desc(base + kk * kRowsPerMma * 128, kAtomBytes, 512, kSwizzle128B32);
   return make_smem_desc(base + kk * kRowsPerMma * 128, kAtomBytes, 1024, kSwizzle128B);
 }
 

@@ -145,11 +145,13 @@ Map5 split_layout(int64_t rows, int64_t xs) {
   a.strides[0] = 1; a.strides[1] = kB; a.strides[2] = 32; a.strides[3] = kB * kB; a.strides[4] = (xs / kB) * kB * kB;
   return a;
 }
-int enc5(CUtensorMap* map, const void* ptr, const Map5& l, std::initializer_list<uint32_t> box) {
+// mn_major: the 32 B-chunk swizzle UMMA reads MN-major TF32 operands in
+int enc5(CUtensorMap* map, const void* ptr, const Map5& l, std::initializer_list<uint32_t> box,
+         bool mn_major = false) {
   uint32_t b[5];
   int d = 0;
   for (uint32_t v : box) b[d++] = v;
-  return encode_tmap(map, ptr, false, 5, l.dims, l.strides, b);
+  return encode_tmap(map, ptr, false, 5, l.dims, l.strides, b, mn_major);
 }
 // f32 coordinates: rowblk advances dim rdim by rstep; k-step s: dim hdim += hstep * (s % 2),
 // dim bdim += s / 2
@@ -299,7 +301,7 @@ BRK_API int brk_fc_fwd(const void* x, const void* w, const float* bias, void* y,
     if ((rc = enc5(&p.map_a, x, split_layout(N, C), {32, 64, 1, 1, 2}))) return rc;
     set_coords_f32(p.ca, 4, 2, 2, 1, 3, 128 * 128, 1, 0);
     // B = W MN-major (x = k, r = c): box (k 32, c 32, khalf 2, cb 1, kb brows/64): brows/32 atoms
-    if ((rc = enc5(&p.map_b, w, split_layout(K, C), {32, 32, 2, 1, (uint32_t)(brows / 64)}))) return rc;
+    if ((rc = enc5(&p.map_b, w, split_layout(K, C), {32, 32, 2, 1, (uint32_t)(brows / 64)}, true))) return rc;
     // (W's blocked layout [Kb][Cb][64 c][64 k] is split_layout(rows = K, xs = C) with the roles
     //  of its inner dims read as (k32, c_in, khalf, cb, kb): strides (1, 64, 32, 4096, Cb*4096))
     set_coords_f32(p.cb, 4, brows / 64, 1, 32, 3, brows * 128, 1, 1);
@@ -408,10 +410,10 @@ BRK_API int brk_fc_upd(const void* x, const void* dz, float* dw, void* w_sgd, fl
     set_coords(p.cb, {0, 0, brows / 64, 0}, {0, 0, 0, 1}, brows * 128, 1);
   } else {
     // A = X^T MN-major on (c32, n_in, chalf, cb, nb): box (32, 32, 2, 2, 1) = 4 atoms (128 rows)
-    if ((rc = enc5(&p.map_a, x, split_layout(N, C), {32, 32, 2, 2, 1}))) return rc;
+    if ((rc = enc5(&p.map_a, x, split_layout(N, C), {32, 32, 2, 2, 1}, true))) return rc;
     set_coords_f32(p.ca, 3, 2, 1, 32, 4, 128 * 128, 1, 1);
     // B = dZ^T MN-major: box (32, 32, 2, brows/64, 1)
-    if ((rc = enc5(&p.map_b, dz, split_layout(N, K), {32, 32, 2, (uint32_t)(brows / 64), 1}))) return rc;
+    if ((rc = enc5(&p.map_b, dz, split_layout(N, K), {32, 32, 2, (uint32_t)(brows / 64), 1}, true))) return rc;
     set_coords_f32(p.cb, 3, brows / 64, 1, 32, 4, brows * 128, 1, 1);
   }
   p.m_tiles = C / (pl.pair ? 256 : 128);

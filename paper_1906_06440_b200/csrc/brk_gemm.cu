@@ -57,7 +57,7 @@ int operand_map(CUtensorMap* map, OperandCoords& oc, const void* ptr, int64_t ro
     oc.n_loads = box_rows / 32;
     oc.load_bytes = 32 * 128;
     oc.mn_major = 1;
-    return encode_tmap(map, ptr, false, 2, dims, strides, box);
+    return encode_tmap(map, ptr, false, 2, dims, strides, box, true);
   }
   if (kmajor) {
     const uint64_t dims[2] = {(uint64_t)K, (uint64_t)rows};

@@ -188,7 +188,8 @@ __device__ __forceinline__ void tc_fence_after() {
 // ----------------------------------------------------------------------------
 // tcgen05: descriptors
 // ----------------------------------------------------------------------------
-enum SmemSwizzle : uint32_t { kSwizzleNone = 0, kSwizzle128B = 2, kSwizzle64B = 4, kSwizzle32B = 6 };
+// kSwizzle128B32: 128 B swizzle of 32 B chunks (4-row period) — MN-major TF32 operands
+enum SmemSwizzle : uint32_t { kSwizzleNone = 0, kSwizzle128B32 = 1, kSwizzle128B = 2, kSwizzle64B = 4, kSwizzle32B = 6 };
 
 // Shared-memory matrix descriptor (sm_100 "version 1").
 //   [0,14)  start address >> 4

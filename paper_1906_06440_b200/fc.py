@@ -163,9 +163,30 @@ def _stage_bias(bias):
 
 
 def _engine_ok(p: FcParams, dtype) -> bool:
+    """The TMA / tcgen05 engine serves 64-element blocks with N, C, K multiples of 128:
+    bf16 storage on kind::f16, fp32 storage on kind::tf32 (other blockings take the
+    grouped BRGEMM path, which follows the reference's batch lists directly)."""
     torch = require_cuda()
-    return (dtype == torch.bfloat16 and p.b_n == 64 and p.b_c == 64 and p.b_k == 64
+    return (dtype in (torch.bfloat16, torch.float32) and p.b_n == 64 and p.b_c == 64 and p.b_k == 64
             and p.n % 128 == 0 and p.c % 128 == 0 and p.k % 128 == 0)
+
+
+def _dcode(dt) -> int:
+    torch = require_cuda()
+    return _lib.BRK_BF16 if dt == torch.bfloat16 else _lib.BRK_F32
+
+
+def tf32_operand(t):
+    """fp32 operand of a TF32 engine pass, rounded to TF32 (round-to-nearest, cvt.rna) into
+    a new device tensor (``brk_round_tf32``): the tensor cores read fp32 bit patterns
+    truncated to TF32, whose bias (~7e-4 of a dot product) would eat most of the 1e-3
+    TF32 tolerance; rounded inputs give ~3e-4.  bf16 tensors pass through."""
+    torch = require_cuda()
+    if t is None or t.dtype != torch.float32:
+        return t
+    out = torch.empty_like(t)
+    _lib.check(_lib.load().brk_round_tf32(t.data_ptr(), out.data_ptr(), t.numel(), stream_ptr()), LayoutError)
+    return out
 
 
 def _act_blocked(data) -> BlockedTensor:
@@ -204,9 +225,10 @@ def fc_forward(params: FcParams, x: BlockedTensor, workers: int = 1, reduce_bloc
     nb, kb, cb = params.n_blocks, params.k_blocks, params.c_blocks
     y = torch.empty((nb, kb, params.b_n, params.b_k), dtype=dt, device="cuda")
     if _engine_ok(params, dt):
+        xd, wd = tf32_operand(xd), tf32_operand(wd)
         rc = _lib.load().brk_fc_fwd(xd.data_ptr(), wd.data_ptr(), bias.data_ptr() if bias is not None else None,
                                     y.data_ptr(), params.n, params.c, params.k, 64, 64, 64,
-                                    params.activation.code, _lib.BRK_BF16, stream_ptr())
+                                    params.activation.code, _dcode(dt), stream_ptr())
         _lib.check(rc, LayoutError)
     else:
         b_n, b_c, b_k = params.b_n, params.b_c, params.b_k
@@ -249,9 +271,10 @@ def fc_backward_data(params: FcParams, dz: BlockedTensor, mask: BlockedTensor | 
     nb, kb, cb = params.n_blocks, params.k_blocks, params.c_blocks
     dx = torch.empty((nb, cb, params.b_n, params.b_c), dtype=dt, device="cuda")
     if _engine_ok(params, dt):
+        dzd, wd = tf32_operand(dzd), tf32_operand(wd)
         rc = _lib.load().brk_fc_bwd_data(dzd.data_ptr(), wd.data_ptr(), md.data_ptr() if md is not None else None,
                                          dx.data_ptr(), None, params.n, params.c, params.k, 64, 64, 64,
-                                         _lib.BRK_BF16, stream_ptr())
+                                         _dcode(dt), stream_ptr())
         _lib.check(rc, LayoutError)
     else:
         b_n, b_c, b_k = params.b_n, params.b_c, params.b_k
@@ -295,14 +318,20 @@ def fc_weight_update(params: FcParams, x: BlockedTensor, dz: BlockedTensor, lr: 
         if not params.w.on_device:
             raise LayoutError("the fused SGD update needs device-resident weights (FcParams.to)")
         sgd_w = params.w.data
-    if _engine_ok(params, dt) and (sgd_w is None or sgd_w.dtype == torch.bfloat16):
+    if _engine_ok(params, dt):
         lib = _lib.load()
         ws = upd_workspace(params.n, params.c, params.k)
+        fused = sgd_w is not None and sgd_w.dtype == torch.bfloat16 and dt == torch.bfloat16
+        xd, dzd = tf32_operand(xd), tf32_operand(dzd)
         rc = lib.brk_fc_upd(xd.data_ptr(), dzd.data_ptr(), dw.data_ptr(),
-                            sgd_w.data_ptr() if sgd_w is not None else None, float(lr or 0.0),
+                            sgd_w.data_ptr() if fused else None, float(lr or 0.0) if fused else 0.0,
                             None, 0, None, None, 0.0, ws.data_ptr(), ws.numel(),
-                            params.n, params.c, params.k, 64, 64, 64, _lib.BRK_BF16, stream_ptr())
+                            params.n, params.c, params.k, 64, 64, 64, _dcode(dt), stream_ptr())
         _lib.check(rc, LayoutError)
+        if sgd_w is not None and not fused:
+            rc = lib.brk_sgd_apply(sgd_w.data_ptr(), dw.data_ptr(), float(lr), dw.numel(),
+                                   _dcode(sgd_w.dtype), stream_ptr())
+            _lib.check(rc, LayoutError)
     else:
         b_n, b_c, b_k = params.b_n, params.b_c, params.b_k
         dev = "cuda"

@@ -50,6 +50,14 @@ def main():
         if M == N == K == 8192:
             af, bf = a.float(), b.float()
             cf = torch.empty(M, N, device="cuda")
+            from paper_1906_06440_b200 import _lib
+            from paper_1906_06440_b200._device import stream_ptr
+            lib = _lib.load()
+            # engine TF32 on pre-rounded fp32 operands (rounding passes excluded: kernel ceiling)
+            t_e32 = timed(lambda: _lib.check(lib.brk_gemm_dense_f32(
+                af.data_ptr(), K, 1, bf.data_ptr(), K, 1, cf.data_ptr(), N, 0, M, N, K, 1.0, 0.0, None, 0,
+                None, 0, stream_ptr())), iters=10)
+            row["engine_tf32_tflops"] = fl / t_e32 / 1e12
             torch.backends.cuda.matmul.allow_tf32 = True
             t_tf = timed(lambda: torch.matmul(af, bf.t(), out=cf), iters=10)
             torch.backends.cuda.matmul.allow_tf32 = False
