@@ -301,8 +301,26 @@ def other_workloads():
             "config1_stride_16x64x64x64": {k: c1[k] for k in ("jobs", "us", "tflops", "roof_frac", "bound")},
             "sweep": [{k: r[k] for k in ("m", "batch", "variant", "jobs", "tflops", "roof_frac")} for r in pts],
             "note": "m=n=k in 32..256, batch 1..64, bf16 in / fp32 C, one grouped launch per point"}
+        # config 1 as written: fp32 blocks in HBM, TF32 tensor-core math (north_star "TF32 inputs")
+        r32 = brgemm_suite(ms=(64,), batches=(16,), iters=5, precision="tf32")
+        out["brgemm"]["config1_stride_16x64x64x64_tf32"] = {
+            r["variant"]: {k: r[k] for k in ("jobs", "us", "tflops", "roof_frac", "bound")} for r in r32["points"]}
+        out["brgemm"]["tf32_peak_tflops"] = r32["peak_tflops"]
+        # config 5: independent M, N, K in {32, 64, 128, 256} (batch 16), every variant
+        grid = brgemm_suite(batches=(16,), iters=3, square=False)["points"]
+        out["brgemm"]["grid_mnk_batch16"] = {
+            "points": [[r["m"], r["n"], r["k"], r["variant"], round(r["tflops"], 1), round(r["roof_frac"], 3)]
+                       for r in grid],
+            "columns": ["m", "n", "k", "variant", "tflops", "roof_frac"],
+            "median_roof_frac": {v: statistics.median(r["roof_frac"] for r in grid if r["variant"] == v)
+                                 for v in ("stride", "offset", "address")}}
     except Exception as exc:  # noqa: BLE001
         out["brgemm"] = {"error": repr(exc)[:300]}
+    try:  # the headline config with the reference's fp32 storage, TF32 tensor-core math
+        from tools.suites import mlp_tf32_suite
+        out["mlp4x1024_n2048_tf32"] = mlp_tf32_suite()
+    except Exception as exc:  # noqa: BLE001
+        out["mlp4x1024_n2048_tf32"] = {"error": repr(exc)[:300]}
     try:  # TMEM-resident batch reduction vs split GEMMs accumulating through memory
         from tools.suites import split_gemm_baseline
         out["brgemm_vs_split_gemm"] = split_gemm_baseline(iters=5)

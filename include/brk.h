@@ -161,6 +161,9 @@ BRK_API size_t brk_mlp_step_workspace_bytes(int L, int N, int C);
 BRK_API int brk_fc_bias_grad(const void* dy, const void* y, void* dz_out, float* db, void* workspace,
                              int N, int K, int b_n, int b_k, float* bias_sgd, float lr, void* stream);
 BRK_API size_t brk_fc_bias_grad_workspace(int K);
+/* The same with the storage dtype of dy / y / dz_out: BRK_BF16 or BRK_F32 (TF32 MLP step). */
+BRK_API int brk_fc_bias_grad_dt(const void* dy, const void* y, void* dz_out, float* db, void* workspace,
+                                int N, int K, int b_n, int b_k, float* bias_sgd, float lr, int dtype, void* stream);
 /* Bias gradient for any block factors / dtype (dy, y, dz_out in the
  * [N/b_n][K/b_k][b_n][b_k] layout): dz_out = dy*(y>0) if y != NULL; db = sum_n dz. */
 BRK_API int brk_colsum_blocked(const void* dy, const void* y, void* dz_out, float* db, int N, int K,
@@ -220,6 +223,23 @@ BRK_API int brk_conv_col2im(const void* dcol, void* dx, int N, int C, int H, int
                             int pad_h, int pad_w, int b_c, int64_t ldcol, void* stream);
 BRK_API int brk_conv_plan(int pass, int N, int C, int K, int H, int W, int R, int S, int stride, int pad_h,
                           int pad_w, int* out3);
+/* Stride-2 small-channel convolutions (C <= 4 in one channel block, e.g. the ResNet-50
+ * stem 3->64, 7x7, stride 2, pad 3; reference cnn.py:201-334) as space-to-depth implicit GEMMs:
+ * the input is unfolded into 64 channels per output pixel (xs[N][1][P+R'-1][Q][64], bf16:
+ * (horizontal tap v, row/column parity a/b, channel c) -> v*16 + (2a+b)*C + c) and the conv
+ * runs on the engine as an R' x 1 stride-1 conv (R' = ceil((R + pad_h%2)/2)).
+ * x [N][1][H][W][C], w [K/64][1][R][S][C][64], out/dout [N][K/64][P][Q][64] (bf16),
+ * dw like w in fp32, dx like x.  workspace: brk_conv_s2d_workspace(...) bytes (no init). */
+BRK_API int brk_conv_s2d_shape(int N, int C, int K, int H, int W, int R, int S, int pad_h, int pad_w, int* out4);
+BRK_API size_t brk_conv_s2d_workspace(int N, int C, int K, int H, int W, int R, int S, int pad_h, int pad_w);
+BRK_API int brk_conv_s2d_unfold(const void* x, void* xs, int N, int C, int H, int W, int R, int S, int pad_h,
+                                int pad_w, void* stream);
+BRK_API int brk_conv_s2d_fwd(const void* x, const void* w, void* out, void* workspace, size_t ws_bytes, int N, int C,
+                             int K, int H, int W, int R, int S, int pad_h, int pad_w, void* stream);
+BRK_API int brk_conv_s2d_upd(const void* x, const void* dout, float* dw, void* workspace, size_t ws_bytes, int N,
+                             int C, int K, int H, int W, int R, int S, int pad_h, int pad_w, void* stream);
+BRK_API int brk_conv_s2d_bwd_data(const void* dout, const void* w, void* dx, void* workspace, size_t ws_bytes, int N,
+                                  int C, int K, int H, int W, int R, int S, int pad_h, int pad_w, void* stream);
 
 /* ---------------------------------------------------------------------------
  * Dense row-major GEMM on the same engine (batch list = the K/64 consecutive

@@ -59,6 +59,8 @@ SIGNATURES: dict[str, tuple] = {
                                  ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_double)]),
     "brk_fc_bias_grad": (_c_int, [_vp, _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _c_f, _vp]),
     "brk_fc_bias_grad_workspace": (ctypes.c_size_t, [_c_int]),
+    "brk_fc_bias_grad_dt": (_c_int, [_vp, _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _c_f, _c_int,
+                                     _vp]),
     "brk_colsum_blocked": (_c_int, [_vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp]),
     "brk_sgd_apply": (_c_int, [_vp, _vp, _c_f, _c_i64, _c_int, _vp]),
     "brk_layout_transform": (_c_int, [_vp, _vp, _c_int, _vp, _vp, _vp, _vp, _c_int, _c_int, _vp]),
@@ -69,6 +71,12 @@ SIGNATURES: dict[str, tuple] = {
     "brk_conv_plan": (_c_int, [_c_int] * 11 + [ctypes.POINTER(_c_int)]),
     "brk_conv_im2col": (_c_int, [_vp, _vp] + [_c_int] * 10 + [_c_i64, _vp]),
     "brk_conv_col2im": (_c_int, [_vp, _vp] + [_c_int] * 10 + [_c_i64, _vp]),
+    "brk_conv_s2d_shape": (_c_int, [_c_int] * 9 + [ctypes.POINTER(_c_int)]),
+    "brk_conv_s2d_workspace": (ctypes.c_size_t, [_c_int] * 9),
+    "brk_conv_s2d_unfold": (_c_int, [_vp, _vp] + [_c_int] * 8 + [_vp]),
+    "brk_conv_s2d_fwd": (_c_int, [_vp, _vp, _vp, _vp, ctypes.c_size_t] + [_c_int] * 9 + [_vp]),
+    "brk_conv_s2d_upd": (_c_int, [_vp, _vp, _vp, _vp, ctypes.c_size_t] + [_c_int] * 9 + [_vp]),
+    "brk_conv_s2d_bwd_data": (_c_int, [_vp, _vp, _vp, _vp, ctypes.c_size_t] + [_c_int] * 9 + [_vp]),
     "brk_gemm_dense": (_c_int, [_vp, _c_i64, _c_int, _vp, _c_i64, _c_int, _vp, _c_i64, _c_int, _c_i64, _c_int,
                                 _c_int, _c_f, _c_f, _vp, _c_int, _vp, ctypes.c_size_t, _vp]),
     "brk_gemm_dense_workspace": (ctypes.c_size_t, [_c_i64, _c_int, _c_int]),

@@ -233,6 +233,27 @@ def _small_ok(spec: "ConvSpec", dt, engine: bool | None) -> bool:
     return dt == torch.bfloat16 and spec.c < 64 and spec.k == 64 and spec.b_k == 64
 
 
+def _s2d_ok(spec: "ConvSpec", dt, engine: bool | None) -> bool:
+    """Stride-2 convs over <= 4 channels in one block (the ResNet-50 stem): space-to-depth
+    unfold to 64 channels + the implicit-GEMM engine (brk_conv_s2d_*, csrc/brk_conv_s2d.cu).
+    BRK_CONV_S2D=0 selects the explicit-im2col path instead (A/B diagnostics)."""
+    torch = require_cuda()
+    if engine is False or os.environ.get("BRK_CONV_ENGINE", "1") == "0" or os.environ.get("BRK_CONV_S2D", "1") == "0":
+        return False
+    if not (dt == torch.bfloat16 and spec.stride == 2 and spec.c <= 4 and spec.b_c == spec.c and spec.b_k == 64
+            and spec.k % 64 == 0):
+        return False
+    return _lib.load().brk_conv_s2d_shape(*_s2d_args(spec), None) == 0
+
+
+def _s2d_args(spec: "ConvSpec"):
+    return (spec.n, spec.c, spec.k, spec.h, spec.w, spec.r, spec.s, spec.pad_h, spec.pad_w)
+
+
+def _s2d_workspace(spec: "ConvSpec"):
+    return _workspace(int(_lib.load().brk_conv_s2d_workspace(*_s2d_args(spec))))
+
+
 def _small_weights(spec: "ConvSpec", w):
     """W2[k][(r, s, c)] (bf16, columns padded to a multiple of 64) from [1][C_b][R][S][b_c][64]."""
     torch = require_cuda()
@@ -301,6 +322,14 @@ def conv2d_forward(spec: ConvSpec, inp: BlockedTensor, wgt: BlockedTensor, strat
     torch = require_cuda()
     host = not inp.on_device
     prec, dt = _dtype(precision, inp, wgt)
+    if _s2d_ok(spec, dt, engine):
+        x, w = _stage(inp, dt), _stage(wgt, dt)
+        out = torch.empty((spec.n, spec.k_blocks, spec.out_h, spec.out_w, 64), dtype=dt, device="cuda")
+        ws = _s2d_workspace(spec)
+        _lib.check(_lib.load().brk_conv_s2d_fwd(x.data_ptr(), w.data_ptr(), out.data_ptr(), ws.data_ptr(), ws.numel(),
+                                                *_s2d_args(spec), stream_ptr()), LayoutError)
+        res = BlockedTensor(out, n_outer=4, logical_dims={"n": 0, "k": (1, 4), "p": 2, "q": 3})
+        return res.to("cpu") if host else res
     if _small_ok(spec, dt, engine):
         from ._dense import gemm
         x, w = _stage(inp, dt), _stage(wgt, dt)
@@ -358,6 +387,13 @@ def conv2d_backward_data(spec: ConvSpec, dout: BlockedTensor, wgt: BlockedTensor
     prec, dt = _dtype(precision, dout, wgt)
     do = _stage(dout, dt)
     w = _stage(wgt, dt)
+    if _s2d_ok(spec, dt, engine):
+        din = torch.empty((spec.n, spec.c_blocks, spec.h, spec.w, spec.b_c), dtype=dt, device="cuda")
+        ws = _s2d_workspace(spec)
+        _lib.check(_lib.load().brk_conv_s2d_bwd_data(do.data_ptr(), w.data_ptr(), din.data_ptr(), ws.data_ptr(),
+                                                     ws.numel(), *_s2d_args(spec), stream_ptr()), LayoutError)
+        res = BlockedTensor(din, n_outer=4, logical_dims={"n": 0, "c": (1, 4), "h": 2, "w": 3})
+        return res.to("cpu") if host else res
     if _small_ok(spec, dt, engine):
         from ._dense import gemm
         w2, rsc, ld = _small_weights(spec, w)
@@ -440,6 +476,15 @@ def conv2d_weight_update(spec: ConvSpec, inp: BlockedTensor, dout: BlockedTensor
     torch = require_cuda()
     host = not inp.on_device
     prec, dt = _dtype(precision, inp, dout)
+    if _s2d_ok(spec, dt, engine):
+        x, do = _stage(inp, dt), _stage(dout, dt)
+        dw = torch.empty((spec.k_blocks, spec.c_blocks, spec.r, spec.s, spec.b_c, spec.b_k), dtype=torch.float32,
+                         device="cuda")
+        ws = _s2d_workspace(spec)
+        _lib.check(_lib.load().brk_conv_s2d_upd(x.data_ptr(), do.data_ptr(), dw.data_ptr(), ws.data_ptr(), ws.numel(),
+                                                *_s2d_args(spec), stream_ptr()), LayoutError)
+        res = BlockedTensor(dw, n_outer=4, logical_dims={"k": (0, 5), "c": (1, 4), "r": 2, "s": 3})
+        return res.to("cpu") if host else res
     if _small_ok(spec, dt, engine):
         from ._dense import gemm
         x, do = _stage(inp, dt), _stage(dout, dt)

@@ -398,7 +398,9 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
       const float* bias_row = bias_base != nullptr ? bias_base + p.bias_offs[job] : nullptr;
       const char* mask_ptr = p.mask_ptrs != nullptr ? static_cast<const char*>(p.mask_ptrs[job]) : nullptr;
       // plain fp32 output with 16 B-aligned rows: one float4 store per 4 columns
-      const bool vec_out = !p.out_bf16 && p.beta == 0.0f && bias_row == nullptr && mask_ptr == nullptr &&
+      // (beta != 0: the lane's row of C is read back as float4 too — the scalar path below
+      //  touches 32 rows per warp instruction)
+      const bool vec_out = !p.out_bf16 && bias_row == nullptr && mask_ptr == nullptr &&
                            p.act == 0 && (p.ldc & 3) == 0 && (reinterpret_cast<uintptr_t>(c_ptr) & 15) == 0;
       for (int c0 = 0; c0 < n_cols; c0 += 32) {
         uint32_t accv[32];
@@ -412,10 +414,22 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
         if (row < p.n && vec_out && m0 + c0 + 32 <= p.m) {
           float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(c_ptr) + static_cast<int64_t>(row) * p.ldc +
                                                   m0 + c0);
+          if (p.beta != 0.0f) {
+            float4 old[8];
 #pragma unroll
-          for (int q = 0; q < 8; ++q)
-            dst[q] = make_float4(p.alpha * __uint_as_float(accv[4 * q]), p.alpha * __uint_as_float(accv[4 * q + 1]),
-                                 p.alpha * __uint_as_float(accv[4 * q + 2]), p.alpha * __uint_as_float(accv[4 * q + 3]));
+            for (int q = 0; q < 8; ++q) old[q] = dst[q];
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              dst[q] = make_float4(__fadd_rn(__fmul_rn(p.alpha, __uint_as_float(accv[4 * q])), __fmul_rn(p.beta, old[q].x)),
+                                   __fadd_rn(__fmul_rn(p.alpha, __uint_as_float(accv[4 * q + 1])), __fmul_rn(p.beta, old[q].y)),
+                                   __fadd_rn(__fmul_rn(p.alpha, __uint_as_float(accv[4 * q + 2])), __fmul_rn(p.beta, old[q].z)),
+                                   __fadd_rn(__fmul_rn(p.alpha, __uint_as_float(accv[4 * q + 3])), __fmul_rn(p.beta, old[q].w)));
+          } else {
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              dst[q] = make_float4(p.alpha * __uint_as_float(accv[4 * q]), p.alpha * __uint_as_float(accv[4 * q + 1]),
+                                   p.alpha * __uint_as_float(accv[4 * q + 2]), p.alpha * __uint_as_float(accv[4 * q + 3]));
+          }
         } else if (row < p.n) {
 #pragma unroll 4
         for (int j = 0; j < 32; ++j) {
@@ -424,8 +438,8 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
           const int64_t off = static_cast<int64_t>(row) * p.ldc + col;
           float out = steps > 0 ? p.alpha * __uint_as_float(accv[j]) : 0.0f;
           if (p.beta != 0.0f)
-            out += p.beta * (p.out_bf16 ? __bfloat162float(reinterpret_cast<__nv_bfloat16*>(c_ptr)[off])
-                                        : reinterpret_cast<float*>(c_ptr)[off]);
+            out = __fadd_rn(out, __fmul_rn(p.beta, p.out_bf16 ? __bfloat162float(reinterpret_cast<__nv_bfloat16*>(c_ptr)[off])
+                                        : reinterpret_cast<float*>(c_ptr)[off]));
           if (bias_row != nullptr) out += bias_row[col];
           if (p.act == 1) {
             out = fmaxf(out, 0.0f);

@@ -213,9 +213,31 @@ int finish(const EngineParams& p, const Plan& pl, void* stream, int tf32 = 0) {
 // ---------------------------------------------------------------------------
 constexpr int kSplit = 16;
 
-__global__ void __launch_bounds__(256) bias_grad_kernel(const __nv_bfloat16* dy,
-                                                        const __nv_bfloat16* __restrict__ y,
-                                                        __nv_bfloat16* dz_out,
+// 8 consecutive elements of a bf16 or fp32 row segment, as floats
+__device__ __forceinline__ void load8(const __nv_bfloat16* p, float* v) {
+  const uint4 g = *reinterpret_cast<const uint4*>(p);
+  const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&g);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) v[j] = __bfloat162float(h[j]);
+}
+__device__ __forceinline__ void load8(const float* p, float* v) {
+  const float4 a = reinterpret_cast<const float4*>(p)[0], b = reinterpret_cast<const float4*>(p)[1];
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+__device__ __forceinline__ void store8(__nv_bfloat16* p, const float* v) {
+  uint4 g;
+  __nv_bfloat16* h = reinterpret_cast<__nv_bfloat16*>(&g);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) h[j] = __float2bfloat16_rn(v[j]);  // exact: v[j] is a bf16 value or 0
+  *reinterpret_cast<uint4*>(p) = g;
+}
+__device__ __forceinline__ void store8(float* p, const float* v) {
+  reinterpret_cast<float4*>(p)[0] = make_float4(v[0], v[1], v[2], v[3]);
+  reinterpret_cast<float4*>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) bias_grad_kernel(const T* dy, const T* __restrict__ y, T* dz_out,
                                                         float* __restrict__ db, float* __restrict__ partial,
                                                         unsigned* __restrict__ counters, int N, int K,
                                                         float* __restrict__ bias, float lr) {
@@ -224,7 +246,7 @@ __global__ void __launch_bounds__(256) bias_grad_kernel(const __nv_bfloat16* dy,
   const int kb = blockIdx.x, split = blockIdx.y;
   const int Kb = K / kB;
   const int tid = threadIdx.x;
-  const int cgrp = tid & 7;    // 8 column groups of 8 (16 B)
+  const int cgrp = tid & 7;    // 8 column groups of 8
   const int rlane = tid >> 3;  // 32 row lanes
   const int rows_per = N / kSplit;
   const int r0 = split * rows_per;
@@ -232,18 +254,18 @@ __global__ void __launch_bounds__(256) bias_grad_kernel(const __nv_bfloat16* dy,
   for (int r = r0 + rlane; r < r0 + rows_per; r += 32) {
     const int64_t off = static_cast<int64_t>(r / kB) * Kb * kB * kB + static_cast<int64_t>(kb) * kB * kB +
                         (r % kB) * kB + cgrp * 8;
-    uint4 g = *reinterpret_cast<const uint4*>(dy + off);
-    __nv_bfloat16* gh = reinterpret_cast<__nv_bfloat16*>(&g);
+    float g[8];
+    load8(dy + off, g);
     if (y != nullptr) {
-      uint4 m = *reinterpret_cast<const uint4*>(y + off);
-      const __nv_bfloat16* mh = reinterpret_cast<const __nv_bfloat16*>(&m);
+      float m[8];
+      load8(y + off, m);
 #pragma unroll
       for (int j = 0; j < 8; ++j)
-        if (!(__bfloat162float(mh[j]) > 0.0f)) gh[j] = __float2bfloat16_rn(0.0f);
-      if (dz_out != nullptr) *reinterpret_cast<uint4*>(dz_out + off) = g;
+        if (!(m[j] > 0.0f)) g[j] = 0.0f;
+      if (dz_out != nullptr) store8(dz_out + off, g);
     }
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[j] += __bfloat162float(gh[j]);
+    for (int j = 0; j < 8; ++j) acc[j] += g[j];
   }
   __shared__ float red[32][65];
 #pragma unroll
@@ -438,6 +460,12 @@ BRK_API int brk_fc_upd(const void* x, const void* dz, float* dw, void* w_sgd, fl
 // workspace: brk_fc_bias_grad_workspace(K) bytes (zero-initialised once).
 BRK_API int brk_fc_bias_grad(const void* dy, const void* y, void* dz_out, float* db, void* workspace,
                              int N, int K, int b_n, int b_k, float* bias_sgd, float lr, void* stream) {
+  return brk_fc_bias_grad_dt(dy, y, dz_out, db, workspace, N, K, b_n, b_k, bias_sgd, lr, BRK_BF16, stream);
+}
+
+BRK_API int brk_fc_bias_grad_dt(const void* dy, const void* y, void* dz_out, float* db, void* workspace,
+                                int N, int K, int b_n, int b_k, float* bias_sgd, float lr, int dtype, void* stream) {
+  if (dtype != BRK_BF16 && dtype != BRK_F32) return set_error(BRK_ERR_CONTRACT, "bias_grad: dtype bf16 or f32");
   if (b_n != kB || b_k != kB || N % kB || K % kB || N % kSplit)
     return set_error(BRK_ERR_CONTRACT, "bias_grad needs b_n=b_k=64, N and K multiples of 64");
   float* partial = static_cast<float*>(workspace);
@@ -453,9 +481,14 @@ BRK_API int brk_fc_bias_grad(const void* dy, const void* y, void* dz_out, float*
   attr.val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = &attr;
   cfg.numAttrs = 1;
-  cudaError_t err = cudaLaunchKernelEx(&cfg, bias_grad_kernel, static_cast<const __nv_bfloat16*>(dy),
-                                       static_cast<const __nv_bfloat16*>(y), static_cast<__nv_bfloat16*>(dz_out),
-                                       db, partial, counters, N, K, bias_sgd, lr);
+  cudaError_t err =
+      dtype == BRK_F32
+          ? cudaLaunchKernelEx(&cfg, bias_grad_kernel<float>, static_cast<const float*>(dy),
+                               static_cast<const float*>(y), static_cast<float*>(dz_out), db, partial, counters, N, K,
+                               bias_sgd, lr)
+          : cudaLaunchKernelEx(&cfg, bias_grad_kernel<__nv_bfloat16>, static_cast<const __nv_bfloat16*>(dy),
+                               static_cast<const __nv_bfloat16*>(y), static_cast<__nv_bfloat16*>(dz_out), db,
+                               partial, counters, N, K, bias_sgd, lr);
   if (err != cudaSuccess) return set_cuda_error(err, "bias_grad launch");
   return BRK_OK;
 }

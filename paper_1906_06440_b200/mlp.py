@@ -310,3 +310,79 @@ class MLP:
                 self.step()
             outs[i].copy_(self.db[self.L - 1], non_blocking=True)
         return outs
+
+
+class MlpTF32:
+    """The same MLP training step with the reference's own fp32 storage and TF32
+    tensor-core math (north_star "bf16 and TF32 inputs"): activations, weights
+    and gradients fp32 in HBM, every GEMM on the engine's TF32 path (32-element
+    fp32 atoms, 128B swizzle).  One step = 4L + 1 + L native launches:
+
+        fwd   y_l = relu(W_l y_{l-1} + b_l)                 brk_fc_fwd(F32)
+        top   dz_L = dy * (y_L > 0), db_L, b_L -= lr db_L    brk_fc_bias_grad_dt(F32)
+        bwd   dz_{l-1} = (W_l^T dz_l) * (y_{l-1} > 0)        brk_fc_bwd_data(F32, mask, column sums)
+        upd   dW_l = dz_l y_{l-1}^T, db_{l-1} (+ bias SGD)   brk_fc_upd(F32)
+        sgd   W_l -= lr dW_l                                 brk_sgd_apply(F32)
+
+    (the fused-SGD epilogue writes bf16 weights, so fp32 weights take the separate apply)."""
+
+    def __init__(self, layers: int = 4, width: int = 1024, batch: int = 2048, lr: float = 1e-3,
+                 seed: int = 0, device: str = "cuda"):
+        torch = require_cuda()
+        if width % 128 or batch % 256:
+            raise ValueError("TF32 MLP engine path needs width % 128 == 0 and batch % 256 == 0")
+        self.torch = torch
+        self.L, self.C, self.N, self.lr = layers, width, batch, lr
+        g = torch.Generator(device="cpu").manual_seed(seed)
+        cb, nb = width // B, batch // B
+        f32 = torch.float32
+        self.w, self.bias = [], []
+        for _ in range(layers):
+            w = (torch.rand(width, width, generator=g) * 2 - 1) / np.sqrt(width)
+            self.w.append(w.reshape(cb, B, cb, B).permute(0, 2, 3, 1).contiguous().to(device))
+            self.bias.append(((torch.rand(width, generator=g) * 2 - 1) * 0.1).to(device))
+        self.y = [torch.empty(nb, cb, B, B, dtype=f32, device=device) for _ in range(layers + 1)]
+        self.dz = [torch.empty(nb, cb, B, B, dtype=f32, device=device) for _ in range(layers + 1)]
+        self.dy = torch.empty(nb, cb, B, B, dtype=f32, device=device)
+        self.dw = [torch.empty(cb, cb, B, B, dtype=f32, device=device) for _ in range(layers)]
+        self.db = [torch.empty(width, dtype=f32, device=device) for _ in range(layers)]
+        self.colsum = [torch.zeros(batch // 32, width, dtype=f32, device=device) for _ in range(layers + 1)]
+        lib = _lib.load()
+        self.lib = lib
+        self.ws_top = torch.zeros(lib.brk_fc_bias_grad_workspace(width), dtype=torch.uint8, device=device)
+        upd_bytes = max(int(lib.brk_fc_upd_workspace(batch, width, width)), 16)
+        self.upd_ws = [torch.zeros(upd_bytes, dtype=torch.uint8, device=device) for _ in range(layers)]
+        self.launches_per_step = 0
+
+    def load_input(self, x, dy) -> None:
+        self.y[0].copy_(x, non_blocking=True)
+        self.dy.copy_(dy, non_blocking=True)
+
+    def step(self, stream: int | None = None) -> int:
+        torch, lib, n, c, L, lr = self.torch, self.lib, self.N, self.C, self.L, self.lr
+        s = torch.cuda.current_stream().cuda_stream if stream is None else stream
+        F = _lib.BRK_F32
+        chk = lambda rc: _lib.check(rc, RuntimeError)  # noqa: E731
+        for l in range(L):
+            chk(lib.brk_fc_fwd(self.y[l].data_ptr(), self.w[l].data_ptr(), self.bias[l].data_ptr(),
+                               self.y[l + 1].data_ptr(), n, c, c, B, B, B, 1, F, s))
+        chk(lib.brk_fc_bias_grad_dt(self.dy.data_ptr(), self.y[L].data_ptr(), self.dz[L].data_ptr(),
+                                    self.db[L - 1].data_ptr(), self.ws_top.data_ptr(), n, c, B, B,
+                                    self.bias[L - 1].data_ptr(), lr, F, s))
+        launches = L + 1
+        for l in range(L, 0, -1):
+            mask = self.y[l - 1].data_ptr() if l > 1 else None
+            colsum = self.colsum[l - 1].data_ptr() if l > 1 else None
+            chk(lib.brk_fc_bwd_data(self.dz[l].data_ptr(), self.w[l - 1].data_ptr(), mask,
+                                    self.dz[l - 1].data_ptr(), colsum, n, c, c, B, B, B, F, s))
+            parts = self.colsum[l].data_ptr() if l < L else None
+            chk(lib.brk_fc_upd(self.y[l - 1].data_ptr(), self.dz[l].data_ptr(), self.dw[l - 1].data_ptr(),
+                               None, 0.0, parts, n // 32, self.db[l - 1].data_ptr() if parts else None,
+                               self.bias[l - 1].data_ptr() if parts else None, lr,
+                               self.upd_ws[l - 1].data_ptr(), self.upd_ws[l - 1].numel(),
+                               n, c, c, B, B, B, F, s))
+            chk(lib.brk_sgd_apply(self.w[l - 1].data_ptr(), self.dw[l - 1].data_ptr(), lr,
+                                  self.dw[l - 1].numel(), F, s))
+            launches += 3
+        self.launches_per_step = launches
+        return launches

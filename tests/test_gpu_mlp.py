@@ -119,3 +119,52 @@ def test_fused_step_matches_per_pass_launches(monkeypatch):
     for a, b in zip(*outs):
         assert (a - b).abs().max().item() <= 2e-2 * max(b.abs().max().item(), 1e-6)
 
+
+
+@pytest.mark.parametrize("layers,width,batch", [(2, 256, 256), (4, 1024, 2048)])
+def test_mlp_tf32_step_matches_oracle(layers, width, batch):
+    """The fp32-storage TF32 step (MlpTF32) at the north-star TF32 tolerance (1e-3)."""
+    from paper_1906_06440_b200.mlp import MlpTF32
+
+    lr = 0.05
+    mlp = MlpTF32(layers=layers, width=width, batch=batch, lr=lr, seed=1)
+    g = torch.Generator(device="cpu").manual_seed(2)
+    x = torch.rand(batch, width, generator=g) * 2 - 1
+    dy = torch.rand(batch, width, generator=g) * 2 - 1
+    ws = [w_dense(w).cpu().numpy() for w in mlp.w]
+    bs = [b.cpu().numpy().copy() for b in mlp.bias]
+    mlp.load_input(blk(x).cuda(), blk(dy).cuda())
+    mlp.step()
+    torch.cuda.synchronize()
+    case = f"{layers}x{width} N={batch}"
+    fwd = orc.mlp_step_reference(ws, bs, x.numpy(), dy.numpy(), lr=lr)
+    gpu_y = [unblk(mlp.y[l]).cpu().numpy() for l in range(1, layers + 1)]
+    ins = [x.numpy()] + gpu_y[:-1]
+    for l in range(1, layers + 1):
+        # each forward pass on identical inputs (the GPU's own previous activation): TF32 1e-3
+        ref_l = orc.fc_forward_reference(ws[l - 1], ins[l - 1].T.copy(), "relu", bs[l - 1]).T
+        check_parity(f"mlp_tf32.y{l}", case, orc.scale_rel_error(gpu_y[l - 1], ref_l), 1e-3)
+        # the whole chain from x compounds one TF32 rounding per layer (recorded, bounded by L x 1e-3)
+        check_parity(f"mlp_tf32.chain_y{l}", case, orc.scale_rel_error(gpu_y[l - 1], fwd["y"][l]), l * 1e-3)
+    # backward / update, each pass on identical inputs: the GPU's own dz_l and activations
+    ys = [x.numpy().astype(np.float64)] + [a.astype(np.float64) for a in gpu_y]
+    dz_gpu = [unblk(mlp.dz[l]).cpu().numpy().astype(np.float64) for l in range(layers + 1)]
+    check_parity("mlp_tf32.dz_top", case, orc.scale_rel_error(dz_gpu[layers], dy.numpy() * (ys[layers] > 0)), 1e-6)
+    for l in range(layers, 0, -1):
+        dw_ref = dz_gpu[l].T @ ys[l - 1]
+        db_ref = dz_gpu[l].sum(axis=0)
+        check_parity(f"mlp_tf32.dw{l - 1}", case, orc.scale_rel_error(w_dense(mlp.dw[l - 1]).cpu().numpy(), dw_ref),
+                     1e-3)
+        check_parity(f"mlp_tf32.db{l - 1}", case, orc.scale_rel_error(mlp.db[l - 1].cpu().numpy(), db_ref), 1e-3)
+        g = dz_gpu[l] @ ws[l - 1].astype(np.float64)
+        dz_ref = g * (ys[l - 1] > 0) if l > 1 else g
+        check_parity(f"mlp_tf32.dz{l - 1}", case, orc.scale_rel_error(dz_gpu[l - 1], dz_ref), 1e-3)
+        # SGD in fp32: W_new = W - lr dW (GPU dW), bias likewise
+        w_new = ws[l - 1].astype(np.float64) - lr * w_dense(mlp.dw[l - 1]).cpu().numpy()
+        assert np.max(np.abs(w_dense(mlp.w[l - 1]).cpu().numpy() - w_new)) <= 1e-6 * np.max(np.abs(w_new)), f"w{l}"
+        b_new = bs[l - 1].astype(np.float64) - lr * mlp.db[l - 1].cpu().numpy()
+        assert np.max(np.abs(mlp.bias[l - 1].cpu().numpy() - b_new)) <= 1e-6 * max(np.max(np.abs(b_new)), 1.0), f"b{l}"
+    # and the whole backward chain against the oracle from the GPU activations (recorded)
+    ref = orc.mlp_step_reference(ws, bs, x.numpy(), dy.numpy(), lr=lr, activations=gpu_y)
+    check_parity("mlp_tf32.chain_dx", case, orc.scale_rel_error(unblk(mlp.dz[0]).cpu().numpy(), ref["dx"]),
+                 layers * 1e-3)

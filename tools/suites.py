@@ -135,7 +135,7 @@ def resnet_suite(n=256, iters=10, layers=None, passes=("fwd", "bwd", "upd"), ver
             calls["fwd"] = lambda sp: conv2d_forward(spec, xi, wi)
             calls["bwd"] = lambda sp: conv2d_backward_data(spec, do, wi)
             calls["upd"] = lambda sp: conv2d_weight_update(spec, xi, do)
-            path = "im2col-gemm" if c < 64 and k == 64 else "grouped"
+            path = ("s2d-engine" if st == 2 and c <= 4 else "im2col-gemm") if c < 64 and k == 64 else "grouped"
         row = {"id": lid, "count": cnt, "path": path, "C": c, "K": k, "H": h, "W": w, "R": r, "stride": st,
                "gflop": flops / 1e9}
         for p in passes:
@@ -229,13 +229,15 @@ def lstm_suite(t_steps=50, n=168, c=1024, k=1024, iters=3, precision="bf16"):
 
 
 def brgemm_suite(ms=(32, 64, 128, 256), batches=(1, 4, 16, 64), variants=("stride", "offset", "address"),
-                 iters=10, max_bytes=1 << 30, square=True):
+                 iters=10, max_bytes=1 << 30, square=True, precision="bf16"):
     """BASELINE config 5: BRGEMM shape sweep vs roofline (config 1 = stride, m=n=k=64, batch 16).
 
     Each point is ONE grouped launch of J independent output blocks C_j (the
     reference's single call is ~40-80 ns of ideal work), bf16
     inputs, fp32 C, beta = 0.  F = 2 m n k batch J; B = J (2 batch (mk + kn) + 4 mn).
     Reference storage contract (brgemm.py:1-24): a_i (k, m), b_i (n, k), c (n, m).
+    precision "tf32": fp32 A/B in HBM (4-byte elements in B), TF32 tensor-core math —
+    the reference's own fp32 storage (config 1 as written).
     """
     import torch
 
@@ -247,12 +249,18 @@ def brgemm_suite(ms=(32, 64, 128, 256), batches=(1, 4, 16, 64), variants=("strid
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     shapes = [(m, m, m) for m in ms] if square else [(m, n, k) for m in ms for n in ms for k in ms]
     rows = []
+    tf32 = precision == "tf32"
+    esz = 4 if tf32 else 2
+    in_dt = _lib.BRK_F32 if tf32 else _lib.BRK_BF16
+    comp = _lib.BRK_COMPUTE_TF32 if tf32 else _lib.BRK_COMPUTE_BF16
     for m, n, k in shapes:
         for batch in batches:
-            per_job = 2 * batch * (m * k + k * n) + 4 * m * n
+            per_job = esz * batch * (m * k + k * n) + 4 * m * n
             jobs = int(max(1, min(8 * sms, max_bytes // per_job)))
-            a = torch.randn(jobs * batch * k * m, device="cuda").bfloat16()
-            b = torch.randn(jobs * batch * n * k, device="cuda").bfloat16()
+            a = torch.randn(jobs * batch * k * m, device="cuda")
+            b = torch.randn(jobs * batch * n * k, device="cuda")
+            if not tf32:
+                a, b = a.bfloat16(), b.bfloat16()
             c = torch.empty(jobs * n * m, device="cuda")
             flops = 2.0 * m * n * k * batch * jobs
             t_roof = max(flops / (peak * 1e12), jobs * per_job / (hbm * 1e9))
@@ -261,28 +269,49 @@ def brgemm_suite(ms=(32, 64, 128, 256), batches=(1, 4, 16, 64), variants=("strid
             a_off = ((ji[:, None] * batch + bi[None, :]) * (k * m)).reshape(-1).contiguous()
             b_off = ((ji[:, None] * batch + bi[None, :]) * (n * k)).reshape(-1).contiguous()
             c_ptr = (c.data_ptr() + ji * (n * m * 4)).contiguous()
-            a_ptr = (a.data_ptr() + a_off * 2).contiguous()
-            b_ptr = (b.data_ptr() + b_off * 2).contiguous()
+            a_ptr = (a.data_ptr() + a_off * esz).contiguous()
+            b_ptr = (b.data_ptr() + b_off * esz).contiguous()
             for var in variants:
                 if var == "stride":
                     fn = lambda sp: _lib.check(lib.brk_brgemm_stride(  # noqa: E731
                         a.data_ptr(), b.data_ptr(), k * m, n * k, c.data_ptr(), jobs, batch * k * m, batch * n * k,
-                        n * m, m, n, k, batch, m, k, m, 1.0, 0.0, _lib.BRK_BF16, _lib.BRK_F32,
-                        _lib.BRK_COMPUTE_BF16, sp))
+                        n * m, m, n, k, batch, m, k, m, 1.0, 0.0, in_dt, _lib.BRK_F32, comp, sp))
                 elif var == "offset":
                     fn = lambda sp: _lib.check(lib.brk_brgemm_offs(  # noqa: E731
                         a.data_ptr(), b.data_ptr(), a_off.data_ptr(), b_off.data_ptr(), c_ptr.data_ptr(), jobs, m, n,
-                        k, batch, m, k, m, 1.0, 0.0, _lib.BRK_BF16, _lib.BRK_F32, _lib.BRK_COMPUTE_BF16, sp))
+                        k, batch, m, k, m, 1.0, 0.0, in_dt, _lib.BRK_F32, comp, sp))
                 else:
                     fn = lambda sp: _lib.check(lib.brk_brgemm_addr(  # noqa: E731
                         a_ptr.data_ptr(), b_ptr.data_ptr(), c_ptr.data_ptr(), jobs, m, n, k, batch, m, k, m, 1.0,
-                        0.0, _lib.BRK_BF16, _lib.BRK_F32, _lib.BRK_COMPUTE_BF16, sp))
+                        0.0, in_dt, _lib.BRK_F32, comp, sp))
                 mean, best = timer(fn, iters)
                 rows.append({"m": m, "n": n, "k": k, "batch": batch, "variant": var, "jobs": jobs,
                              "us": mean * 1e6, "tflops": flops / mean / 1e12, "roof_frac": t_roof / mean,
                              "bound": "tensor" if flops / (peak * 1e12) >= jobs * per_job / (hbm * 1e9) else "hbm"})
             del a, b, c
-    return {"peak_tflops": peak, "hbm_gbs": hbm, "peak_source": src, "points": rows}
+    if tf32:
+        peak = _tf32_peak(peak)
+        for r in rows:  # roofline against the TF32 tensor peak (half the bf16 rate)
+            f = 2.0 * r["m"] * r["n"] * r["k"] * r["batch"] * r["jobs"]
+            b_ = r["jobs"] * (esz * r["batch"] * (r["m"] * r["k"] + r["k"] * r["n"]) + 4 * r["m"] * r["n"])
+            t_roof = max(f / (peak * 1e12), b_ / (hbm * 1e9))
+            r["roof_frac"] = t_roof / (r["us"] * 1e-6)
+            r["bound"] = "tensor" if f / (peak * 1e12) >= b_ / (hbm * 1e9) else "hbm"
+    return {"peak_tflops": peak, "hbm_gbs": hbm, "peak_source": src, "precision": precision, "points": rows}
+
+
+def _tf32_peak(bf16_peak):
+    """TF32 dense peak: the measured cuBLAS TF32 8192^3 number when profiles/ holds one
+    (profiles/r02/dense_peak.json), else half the bf16 peak (tensor-core rate ratio)."""
+    import json
+    from pathlib import Path
+
+    f = Path(__file__).resolve().parent.parent / "profiles" / "r02" / "dense_peak.json"
+    try:
+        d = json.loads(f.read_text())["dense_peak"]["8192x8192x8192"]
+        return max(d["cublas_tf32_tflops"], d.get("engine_tf32_tflops", 0.0))
+    except (OSError, KeyError, ValueError):
+        return bf16_peak / 2
 
 
 def split_gemm_baseline(m=64, n=64, k=64, batch=16, iters=10):
@@ -319,8 +348,19 @@ def split_gemm_baseline(m=64, n=64, k=64, batch=16, iters=10):
     t_sp, _ = timer(split, iters)
     torch.cuda.synchronize()
     err = (c - c2).abs().max().item() / max(c.abs().max().item(), 1e-30)
+    # HBM roofline of each arm: the BRGEMM reads every A/B block once and writes C once;
+    # the split arm re-reads and re-writes C in every launch after the first
+    _, hbm, _ = _peaks()
+    ab = jobs * batch * 2 * (k * m + n * k)
+    br_bytes = ab + jobs * 4 * n * m
+    sp_bytes = ab + jobs * 4 * n * m * (2 * batch - 1)
     return {"shape": f"m=n=k={m} batch={batch} jobs={jobs}", "brgemm_us": t_br * 1e6, "split_gemm_us": t_sp * 1e6,
-            "speedup": t_sp / t_br, "split_launches": batch, "max_rel_diff": err}
+            "speedup": t_sp / t_br, "split_launches": batch, "max_rel_diff": err,
+            "brgemm_hbm_roof_frac": br_bytes / (hbm * 1e9) / t_br,
+            "split_hbm_roof_frac": sp_bytes / (hbm * 1e9) / t_sp,
+            "roofline_speedup": sp_bytes / br_bytes,
+            "note": "split arm = one beta=1 stride-BRGEMM launch per batch entry (batch 1), C through HBM; "
+                    "roofline_speedup = the byte ratio, the speed-up an ideal kernel would show"}
 
 
 def _dp_time(step, pg, iters, warmup=1):
@@ -426,3 +466,34 @@ if __name__ == "__main__":
         for r in res["points"]:
             print(f"m=n=k={r['m']:3d} batch {r['batch']:2d} {r['variant']:7s} jobs {r['jobs']:5d}: {r['us']:9.1f} us "
                   f"{r['tflops']:7.1f} TF/s  {r['roof_frac'] * 100:5.1f}% of roofline ({r['bound']})")
+
+
+def mlp_tf32_suite(layers=4, width=1024, batch=2048, iters=10):
+    """BASELINE config 2 with the reference's fp32 storage and TF32 math (MlpTF32):
+    whole step (4L+1+L native launches) captured in one CUDA graph, L2 flushed
+    between steps; TFLOP/s against the TF32 dense peak."""
+    import torch
+
+    from paper_1906_06440_b200.mlp import MlpTF32, flops_per_step
+
+    m = MlpTF32(layers=layers, width=width, batch=batch, lr=1e-4, seed=0)
+    g = torch.Generator(device="cuda").manual_seed(1)
+    m.load_input(torch.rand(m.y[0].shape, generator=g, device="cuda") * 2 - 1,
+                 torch.rand(m.dy.shape, generator=g, device="cuda") * 2 - 1)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        m.step(side.cuda_stream)
+    side.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=side):
+        m.step(side.cuda_stream)
+    torch.cuda.synchronize()
+    mean, best = _Timer(torch)(lambda sp: graph.replay(), iters)
+    fl = flops_per_step(layers, batch, width, width)
+    bf16_peak, _, _ = _peaks()
+    peak = _tf32_peak(bf16_peak)
+    return {"ms_per_step": mean * 1e3, "tflops": fl / mean / 1e12, "tf32_peak_tflops": peak,
+            "frac_of_tf32_peak": fl / mean / 1e12 / peak, "launches_per_step": m.launches_per_step,
+            "config": {"layers": layers, "C": width, "K": width, "N": batch, "storage": "fp32",
+                       "compute": "tf32", "timing": "cuda-graph, L2 flushed"}}
