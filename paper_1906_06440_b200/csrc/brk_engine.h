@@ -128,7 +128,8 @@ constexpr int kCounterStride = 65;  // per problem: 64 row-block counters + 1 wh
 // Tile schedule of a grouped launch: problem q owns work units
 // [tile_begin[q], tile_begin[q+1]); a tile of q waits until, for every
 // dependency d, counters[dep_prob][mb] (dep_mode 0: the same 256-row block)
-// or counters[dep_prob][64] (dep_mode 1: the whole problem) shows all tiles done.
+// or counters[dep_prob][64] (dep_mode 1: the whole problem) shows all tiles done,
+// or (dep_mode 2) each k-step only for the 64-column chunk it reads (chunk_counters).
 struct GroupSched {
   int32_t n_probs;
   int32_t tile_begin[kMaxProbs + 1];
@@ -137,6 +138,13 @@ struct GroupSched {
   // [n_probs][kCounterStride] + 1 exit counter, all zero at launch; the last CTA to finish
   // zeroes them again, so back-to-back launches need no memset
   unsigned* counters;
+  // dep_mode 2 (64-column chunks): k-step s of a tile in row block mb, CTA rank r, waits only
+  // for the 64 columns [64 s, 64 s + 64) of the same 128 rows of the dependency, i.e. for
+  //   chunk_counters[((dep_prob * chunk_mb + mb) * 2 + r) * chunk_n + s] == chunk_target
+  // (the epilogue warps that store those rows x columns each add one after their stores).  Zero at launch, re-zeroed by the last CTA like `counters`; null: no chunk deps.
+  unsigned* chunk_counters;
+  int32_t chunk_mb, chunk_n;
+  int32_t chunk_target;  // epilogue-warp arrivals per chunk: 8 for BN=128 pairs (both column quarters)
 };
 
 struct EngineGroup {

@@ -520,15 +520,15 @@ extern "C" {
 namespace {
 // MLP step workspace: the dependency counters (zeroed by every call)
 size_t mlp_counter_bytes(int L) { return (static_cast<size_t>(3 * L) * kCounterStride + 1) * sizeof(unsigned); }
+// 64-column chunk counters of the chained passes: [3L][N/256][2][C/64]
+size_t mlp_chunk_counters(int L, int N, int C) { return static_cast<size_t>(3 * L) * (N / 256) * 2 * (C / 64); }
 }  // namespace
 
 extern "C" {
 
 BRK_API size_t brk_mlp_step_workspace_bytes(int L, int N, int C) {
-  (void)N;
-  (void)C;
-  if (L < 1) return 0;
-  return mlp_counter_bytes(L);
+  if (L < 1 || N < 256 || C < 64) return 0;
+  return mlp_counter_bytes(L) + mlp_chunk_counters(L, N, C) * sizeof(unsigned);
 }
 
 BRK_API int brk_mlp_step(int L, int N, int C, const void* const* y, void* const* dz, const void* dy,
@@ -542,6 +542,11 @@ BRK_API int brk_mlp_step(int L, int N, int C, const void* const* y, void* const*
   if (workspace == nullptr || ws_bytes < brk_mlp_step_workspace_bytes(L, N, C))
     return set_error(BRK_ERR_CONTRACT, "mlp_step: workspace smaller than brk_mlp_step_workspace_bytes(L, N, C)");
   unsigned* counters = static_cast<unsigned*>(workspace);
+  // chained passes (fwd l <- fwd l-1, bwd-data l <- bwd-data l+1) wait per 64-column chunk of
+  // the rows they read (dep_mode 2) instead of for the whole 256-row block (mode 0);
+  // BRK_MLP_CHUNK=0 (diagnostics) restores the row-block dependencies
+  const char* chunk_env = std::getenv("BRK_MLP_CHUNK");
+  const int chunk_mode = (chunk_env != nullptr && std::atoi(chunk_env) == 0) ? 0 : 2;
   // BRK_MLP_BFIRST=0 (diagnostics): producers wait for a tile's dependencies before loading
   // the weight operand too
   const char* bfirst_env = std::getenv("BRK_MLP_BFIRST");
@@ -566,7 +571,7 @@ BRK_API int brk_mlp_step(int L, int N, int C, const void* const* y, void* const*
       return brk_fc_fwd(y[l], w[l], bias[l], const_cast<void*>(y[l + 1]), N, C, C, kB, kB, kB, kActRelu, BRK_BF16,
                         stream);
     });
-    if (l > 0) { gs.dep_prob[q][0] = fwd_of[l - 1]; gs.dep_mode[q][0] = 0; }
+    if (l > 0) { gs.dep_prob[q][0] = fwd_of[l - 1]; gs.dep_mode[q][0] = chunk_mode; }
     G.probs[q].b_first = b_first;  // B = W_l, not written in this launch before the weight updates
     if (l == L - 1) {  // top layer also emits dz_L = dy * (y_L > 0) and its column sums
       const char* de = std::getenv("BRK_MLP_DIAG");  // diagnostics only: drop parts of the top epilogue
@@ -586,7 +591,7 @@ BRK_API int brk_mlp_step(int L, int N, int C, const void* const* y, void* const*
       return brk_fc_bwd_data(dz[l], w[l - 1], l > 1 ? y[l - 1] : nullptr, dz[l - 1], l > 1 ? colsum[l - 1] : nullptr,
                              N, C, C, kB, kB, kB, BRK_BF16, stream);
     });
-    gs.dep_prob[q][0] = dz_src; gs.dep_mode[q][0] = 0;  // the same rows of dz_l
+    gs.dep_prob[q][0] = dz_src; gs.dep_mode[q][0] = chunk_mode;  // the same rows of dz_l
     // B = W_{l-1}: with in-place SGD it is rewritten only after this pass completes (dependency below)
     G.probs[q].b_first = b_first;
     bwd_of[l] = q++;
@@ -646,6 +651,10 @@ BRK_API int brk_mlp_step(int L, int N, int C, const void* const* y, void* const*
   for (int i = 0; i < q; ++i)
     gs.tile_begin[i + 1] = gs.tile_begin[i] + G.probs[i].m_tiles * G.probs[i].n_tiles;
   gs.counters = counters;
+  gs.chunk_counters = counters + (mlp_counter_bytes(L) / sizeof(unsigned));
+  gs.chunk_mb = N / 256;
+  gs.chunk_n = C / 64;
+  gs.chunk_target = 4;  // BN=128 pairs: the 4 epilogue warps (TMEM lane quarters) of a column half
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   // the counters are zero: zero-initialised once by the caller, re-zeroed by every launch's
   // last CTA (no memset between back-to-back steps)
