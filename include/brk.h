@@ -67,6 +67,16 @@ BRK_API int brk_brgemm_addr(const void* const* a_ptrs, const void* const* b_ptrs
                     int n_jobs, int m, int n, int k, int batch, int64_t lda, int64_t ldb,
                     int64_t ldc, float alpha, float beta, int in_dtype, int out_dtype,
                     int compute, void* stream);
+/* The address variant with registered views: a_view (a_view_elems elements) and b_view
+ * (b_view_elems) are allocations that hold the A / B blocks.  The kernel turns each entry's
+ * pointers into (row, column) coordinates of a 2-d view of its allocation and fetches blocks
+ * that lie inside it with TMA (bf16); entries outside the views take the gather path, as in
+ * brk_brgemm_addr.  Results are identical to brk_brgemm_addr. */
+BRK_API int brk_brgemm_addr_views(const void* const* a_ptrs, const void* const* b_ptrs, void* const* c_ptrs,
+                                  const void* a_view, int64_t a_view_elems, const void* b_view,
+                                  int64_t b_view_elems, int n_jobs, int m, int n, int k, int batch, int64_t lda,
+                                  int64_t ldb, int64_t ldc, float alpha, float beta, int in_dtype,
+                                  int out_dtype, int compute, void* stream);
 
 /* Grouped address-variant BRGEMM with general block strides and a fused
  * epilogue — the batch-list interface the FC/LSTM/conv drivers use for block

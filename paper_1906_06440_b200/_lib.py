@@ -38,6 +38,11 @@ SIGNATURES: dict[str, tuple] = {
         [_vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_i64, _c_i64, _c_i64,
          _c_f, _c_f, _c_int, _c_int, _c_int, _vp],
     ),
+    "brk_brgemm_addr_views": (
+        _c_int,
+        [_vp, _vp, _vp, _vp, _c_i64, _vp, _c_i64, _c_int, _c_int, _c_int, _c_int, _c_int, _c_i64, _c_i64,
+         _c_i64, _c_f, _c_f, _c_int, _c_int, _c_int, _vp],
+    ),
     "brk_brgemm_grouped": (_c_int, [_vp, _vp]),
     "brk_fc_fwd": (_c_int, [_vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int,
                             _c_int, _c_int, _vp]),
@@ -125,7 +130,9 @@ def load(path: os.PathLike | None = None) -> ctypes.CDLL:
     global _lib
     if _lib is not None and path is None:
         return _lib
-    p = Path(path) if path is not None else LIB_PATH
+    # BRK_LIB: an alternative build of the same library (e.g. the diagnostics build
+    # libbrk_sm100_diag.so with in-kernel timestamps, `make -C csrc diag`)
+    p = Path(path) if path is not None else Path(os.environ.get("BRK_LIB", LIB_PATH))
     if not p.exists():
         raise BrkNativeError(
             f"{p} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'` "

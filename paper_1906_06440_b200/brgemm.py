@@ -283,24 +283,20 @@ def _run_addr_torch(a_list, b_list, c_list, m, n, k, batch, alpha, beta, spec):
     c_tab = ptr_table([t.data_ptr() for t in c_list])
     lib = _lib.load()
     esz = a_list[0].element_size() if a_list else 0
-    if a_list and b_list and _one_storage(a_list) and _one_storage(b_list):
-        # blocks carved from one allocation per operand (the common case): element offsets
-        # from the lowest block — the offset variant fetches non-wrapping blocks with TMA
-        a_ptrs = [t.data_ptr() for t in a_list]
-        b_ptrs = [t.data_ptr() for t in b_list]
-        a0, b0 = min(a_ptrs), min(b_ptrs)
-        if all((p - a0) % esz == 0 for p in a_ptrs) and all((p - b0) % esz == 0 for p in b_ptrs):
-            a_off = ptr_table([(p - a0) // esz for p in a_ptrs])
-            b_off = ptr_table([(p - b0) // esz for p in b_ptrs])
-            rc = lib.brk_brgemm_offs(
-                a0, b0, a_off.data_ptr(), b_off.data_ptr(), c_tab.data_ptr(), len(c_list), m, n, k, batch,
-                lda, ldb, ldc, float(alpha), float(beta), in_code,
-                _lib.BRK_BF16 if out_bf16 else _lib.BRK_F32, compute, stream_ptr(),
-            )
-            _lib.check(rc, BrgemmError)
-            return
     a_tab = ptr_table([t.data_ptr() for t in a_list]) if a_list else None
     b_tab = ptr_table([t.data_ptr() for t in b_list]) if b_list else None
+    if a_list and b_list and _one_storage(a_list) and _one_storage(b_list):
+        # blocks carved from one allocation per operand (the common case): register the two
+        # allocations as views — the kernel turns each entry's pointers into view coordinates
+        # and fetches in-bounds blocks with TMA (no host-side offset tables)
+        sa, sb = a_list[0].untyped_storage(), b_list[0].untyped_storage()
+        rc = lib.brk_brgemm_addr_views(
+            a_tab.data_ptr(), b_tab.data_ptr(), c_tab.data_ptr(), sa.data_ptr(), sa.nbytes() // esz,
+            sb.data_ptr(), sb.nbytes() // esz, len(c_list), m, n, k, batch, lda, ldb, ldc, float(alpha),
+            float(beta), in_code, _lib.BRK_BF16 if out_bf16 else _lib.BRK_F32, compute, stream_ptr(),
+        )
+        _lib.check(rc, BrgemmError)
+        return
     rc = lib.brk_brgemm_addr(
         a_tab.data_ptr() if a_tab is not None else None,
         b_tab.data_ptr() if b_tab is not None else None,

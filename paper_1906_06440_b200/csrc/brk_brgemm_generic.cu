@@ -43,7 +43,7 @@ constexpr int kMaxStages = 8;
 constexpr int kRingBytes = 4 * (kRows * 128 + kCols * 128);  // 192 KB of operand ring
 constexpr int kAtomColsBf16 = 64;  // bf16 elements per 128 B swizzle-atom row
 constexpr int kAOpBytes = kRows * 128;    // K-major, 128B swizzle: 128 rows x 128 B of K
-constexpr int kSmemBytes = kRingBytes + 1024 + 256;
+constexpr int kSmemBytes = kRingBytes + 1024 + 256;  // ring + alignment slack + barriers / TMEM slot
 
 struct EntryPtrs {
   const char* a;
@@ -104,9 +104,20 @@ __device__ __forceinline__ uint4 load_chunk(const char* base, int64_t first, int
                     pack_bf16x2(v[6], v[7]));
 }
 
-// element offsets of an entry's blocks from the buffer bases (offset / stride variants)
-__device__ __forceinline__ void entry_offs(const GenericParams& p, int job, int i, int64_t& oa, int64_t& ob) {
+// element offsets of an entry's blocks from the buffer bases (offset / stride variants, and
+// address lists with views); false when an address-list block is not inside its view
+__device__ __forceinline__ bool entry_offs(const GenericParams& p, int job, int i, int64_t& oa, int64_t& ob) {
   const int64_t idx = static_cast<int64_t>(job) * p.batch + i;
+  if (p.mode == kModeAddr) {
+    const int64_t esz = p.in_bf16 ? 2 : 4;
+    const int64_t da = static_cast<const char*>(p.a_ptrs[idx]) - static_cast<const char*>(p.a_base);
+    const int64_t db = static_cast<const char*>(p.b_ptrs[idx]) - static_cast<const char*>(p.b_base);
+    oa = da / esz;
+    ob = db / esz;
+    return da >= 0 && db >= 0 && da % esz == 0 && db % esz == 0 &&
+           oa + static_cast<int64_t>(p.k - 1) * p.a_sk + p.m <= p.a_view &&
+           ob + static_cast<int64_t>(p.n - 1) * p.b_sn + p.k <= p.b_view;
+  }
   if (p.mode == kModeOffs) {
     oa = p.a_offs[idx];
     ob = p.b_offs[idx];
@@ -114,6 +125,7 @@ __device__ __forceinline__ void entry_offs(const GenericParams& p, int job, int 
     oa = job * p.jstride_a + i * p.stride_a;
     ob = job * p.jstride_b + i * p.stride_b;
   }
+  return true;
 }
 
 // Persistent: CTA walks job tiles (job, n-tile, m-tile) with four decoupled roles:
@@ -142,7 +154,8 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
   uint64_t* empty = full + kMaxStages;
   uint64_t* done = empty + kMaxStages;  // [2] accumulator complete
   uint64_t* drained = done + 2;         // [2] epilogue finished reading TMEM
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(drained + 2);
+  uint64_t* rounded = drained + 2;      // [kMaxStages] TF32 TMA stages rounded in place (RNA)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rounded + kMaxStages);
 
   const int tid = threadIdx.x;
   const int warp = tid / 32;
@@ -153,9 +166,15 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
   const bool bf16_in = p.in_bf16 != 0;
   const int n_chunks = (p.k + kKC - 1) / kKC;
   const int steps = (p.alpha == 0.0f) ? 0 : p.batch * n_chunks;
-  // ring geometry: the B operand of the widest tile (MN-major atoms for bf16, K-major rows for TF32)
+  // TF32 with TMA (stride variant, every entry one box per operand): fp32 blocks land as they
+  // are — A K-major, B MN-major in 32-element atoms (128B swizzle of 32 B chunks) — and the
+  // idle gather warps round each stage to TF32 in place (RNA, like the gather path's
+  // cvt.rna) before the MMA reads it; the tensor core alone would truncate the mantissa
+  const bool tf32_tma = kTF32 && p.tma && p.all_tma;
+  const bool b_mn = !kTF32 || tf32_tma;  // B operand MN-major (atoms) vs K-major rows
+  // ring geometry: the B operand of the widest tile (MN-major atoms, or K-major rows for gathered TF32)
   const int m_max = min(p.m, kCols);
-  const int b_bytes = kTF32 ? ((m_max + 15) & ~15) * 128 : (m_max + kAtomCols - 1) / kAtomCols * kAtomBytes;
+  const int b_bytes = b_mn ? (m_max + kAtomCols - 1) / kAtomCols * kAtomBytes : ((m_max + 15) & ~15) * 128;
   const int stage_bytes = (kAOpBytes + b_bytes + 1023) & ~1023;
   // (a multiple of the TMA producer count: each stage always has the same producer, so the
   // parity waits on its empty barrier cannot alias)
@@ -165,6 +184,7 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
     for (int s = 0; s < kMaxStages; ++s) {
       mbar_init(&full[s], 1);  // TMA: the producer's expect_tx; gather: one arrive after the copies
       mbar_init(&empty[s], 1);
+      mbar_init(&rounded[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&done[a], 1);
@@ -186,7 +206,7 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
   };
   auto entry_box = [&](int job, int entry) -> EntryBox {
     EntryBox eb{false, 0, 0, 0, 0};
-    if (kTF32 || !p.tma) return eb;
+    if (!p.tma || (kTF32 && !p.all_tma)) return eb;  // TF32 boxes only when every entry is one
     if (p.all_tma) {
       eb.tma = true;
       eb.ra = static_cast<int32_t>(job * p.rj_a + entry * p.rs_a);
@@ -194,7 +214,7 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
       return eb;
     }
     int64_t oa, ob;
-    entry_offs(p, job, entry, oa, ob);
+    if (!entry_offs(p, job, entry, oa, ob)) return eb;
     int64_t qa, qb;
     if (((oa | ob) >> 32) == 0) {  // 32-bit division when the offsets allow it
       qa = static_cast<uint32_t>(oa) / static_cast<uint32_t>(p.a_sk);
@@ -219,7 +239,7 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
       const int mt = t % m_tiles;
       const int m_here = min(kCols, p.m - mt * kCols);
       const int n_cols = kTF32 ? (m_here + 15) & ~15 : (m_here + kAtomCols - 1) / kAtomCols * kAtomCols;
-      const uint32_t idesc = make_idesc(kTF32 ? kFmtTF32 : kFmtBF16, kRows, n_cols, 0, kTF32 ? 0 : 1);
+      const uint32_t idesc = make_idesc(kTF32 ? kFmtTF32 : kFmtBF16, kRows, n_cols, 0, b_mn ? 1 : 0);
       const int acc = local & 1;
       mbar_wait(&drained[acc], ((local >> 1) & 1) ^ 1);  // the epilogue read this accumulator two tiles ago
       tc_fence_after();
@@ -227,17 +247,21 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
       const int g0 = local * steps;
       for (int s = 0; s < steps; ++s) {
         const int g = g0 + s, st = g % n_stages;
-        mbar_wait(&full[st], (g / n_stages) & 1);
+        mbar_wait(tf32_tma ? &rounded[st] : &full[st], (g / n_stages) & 1);
         tc_fence_after();
-        fence_proxy_async_smem();  // gathered stages were written through the generic proxy
+        fence_proxy_async_smem();  // gathered / rounded stages were written through the generic proxy
         if (elect_one()) {
           const uint32_t a_base = smem_u32(smem + st * stage_bytes);
           const uint32_t b_base = a_base + kAOpBytes;
 #pragma unroll
           for (int kk = 0; kk < kKC / kMmaK; ++kk) {
             const uint64_t ad = make_smem_desc(a_base + kk * 32, 16, 1024, kSwizzle128B);
-            const uint64_t bd = kTF32 ? make_smem_desc(b_base + kk * 32, 16, 1024, kSwizzle128B)
-                                      : make_smem_desc(b_base + kk * kMmaK * 128, kAtomBytes, 1024, kSwizzle128B);
+            // MN-major B: bf16 atoms of 64 K-rows (8-row swizzle groups, SBO 1024 B); TF32 atoms of
+            // 32 K-rows in the 32 B-chunk swizzle (4-row groups, SBO 512 B); K-major TF32 rows
+            const uint64_t bd =
+                !b_mn ? make_smem_desc(b_base + kk * 32, 16, 1024, kSwizzle128B)
+                      : (kTF32 ? make_smem_desc(b_base + kk * kMmaK * 128, kAtomBytes, 512, kSwizzle128B32)
+                               : make_smem_desc(b_base + kk * kMmaK * 128, kAtomBytes, 1024, kSwizzle128B));
             mma_ss<kTF32>(d_tmem, ad, bd, idesc, (s > 0 || kk > 0) ? 1u : 0u);
           }
           mma_commit(&empty[st]);
@@ -249,7 +273,7 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
   } else if (warp >= kTmaWarp && warp < kTmaWarp + kTmaWarps) {
     // ------------------------------------------------------------ TMA producers (stage g: warp g % 4)
     const int pid = warp - kTmaWarp;
-    if (!kTF32 && p.tma && elect_one()) {
+    if ((!kTF32 || tf32_tma) && p.tma && elect_one()) {
       int local = 0;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
         const int mt = t % m_tiles;
@@ -277,6 +301,34 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
             }
           }
         }
+      }
+    }
+  } else if (warp < kGatherWarps && tf32_tma) {
+    // ------------------------------------------------------------ TF32 rounding (RNA) of TMA stages
+    const int gt = tid;  // 0 .. 255
+    int local = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
+      const int mt = t % m_tiles;
+      const int m_here = min(kCols, p.m - mt * kCols);
+      const int atoms = (m_here + kAtomCols - 1) / kAtomCols;
+      const int vecs = (p.nbox * 128 + atoms * kAtomBytes) / 16;  // the stage bytes the boxes wrote
+      const int g0 = local * steps;
+      for (int s = 0; s < steps; ++s) {
+        const int g = g0 + s, st = g % n_stages;
+        mbar_wait(&full[st], (g / n_stages) & 1);
+        uint4* v4 = reinterpret_cast<uint4*>(smem + st * stage_bytes);
+        const int a_vecs = p.nbox * 8;
+        for (int i = gt; i < vecs; i += kGatherWarps * 32) {
+          // A rows [0, nbox) then the B atoms at kAOpBytes
+          uint4* q = i < a_vecs ? v4 + i : reinterpret_cast<uint4*>(smem + st * stage_bytes + kAOpBytes) + (i - a_vecs);
+          uint4 v = *q;
+          v = make_uint4(f32_to_tf32(__uint_as_float(v.x)), f32_to_tf32(__uint_as_float(v.y)),
+                         f32_to_tf32(__uint_as_float(v.z)), f32_to_tf32(__uint_as_float(v.w)));
+          *q = v;
+        }
+        fence_proxy_async_smem();  // generic-proxy rewrites -> the MMA's async-proxy reads
+        asm volatile("bar.sync 1, %0;" ::"r"(kGatherWarps * 32) : "memory");
+        if (gt == 0) mbar_arrive(&rounded[st]);
       }
     }
   } else if (warp < kGatherWarps) {
@@ -484,7 +536,10 @@ int launch_brgemm_generic(const GenericParams& p, int compute_tf32, cudaStream_t
   GenericParams q = p;
   q.tma = 0;
   const bool rows_ok = (p.n <= kRows || p.n % kRows == 0) && p.m % kAtomColsBf16 == 0;
-  if (!compute_tf32 && p.in_bf16 && p.mode != kModeAddr && p.k % 64 == 0 && rows_ok && p.a_sm == 1 && p.b_sk == 1 &&
+  const bool addr_views = p.mode == kModeAddr && p.a_view > 0 && p.b_view > 0 && p.a_base != nullptr &&
+                          p.b_base != nullptr;
+  if (!compute_tf32 && p.in_bf16 && (p.mode != kModeAddr || addr_views) && p.k % 64 == 0 && rows_ok && p.a_sm == 1 &&
+      p.b_sk == 1 &&
       (p.a_sk * 2) % 16 == 0 && (p.b_sn * 2) % 16 == 0 && p.a_sk >= p.m && p.b_sn >= p.k &&
       (reinterpret_cast<uintptr_t>(p.a_base) & 15) == 0 && (reinterpret_cast<uintptr_t>(p.b_base) & 15) == 0 &&
       std::getenv("BRK_GENERIC_NO_TMA") == nullptr) {
@@ -492,8 +547,12 @@ int launch_brgemm_generic(const GenericParams& p, int compute_tf32, cudaStream_t
     q.abox = kAtomColsBf16;
     // the views span every row an in-bounds offset can address (the kernel reads only boxes
     // inside blocks, so the declared extent is never dereferenced beyond them)
-    const uint64_t rows_b = std::min<uint64_t>(0x7fffffffull, (1ull << 38) / (p.b_sn * 2));
-    const uint64_t rows_a = std::min<uint64_t>(0x7fffffffull, (1ull << 38) / (p.a_sk * 2));
+    uint64_t rows_b = std::min<uint64_t>(0x7fffffffull, (1ull << 38) / (p.b_sn * 2));
+    uint64_t rows_a = std::min<uint64_t>(0x7fffffffull, (1ull << 38) / (p.a_sk * 2));
+    if (addr_views) {  // the views' own extents (rounded up: the kernel bounds-checks each block)
+      rows_b = std::min<uint64_t>(rows_b, static_cast<uint64_t>((p.b_view + p.b_sn - 1) / p.b_sn));
+      rows_a = std::min<uint64_t>(rows_a, static_cast<uint64_t>((p.a_view + p.a_sk - 1) / p.a_sk));
+    }
     const uint64_t db[2] = {static_cast<uint64_t>(p.b_sn), rows_b}, sb[2] = {1, static_cast<uint64_t>(p.b_sn)};
     const uint64_t da[2] = {static_cast<uint64_t>(p.a_sk), rows_a}, sa[2] = {1, static_cast<uint64_t>(p.a_sk)};
     const uint32_t bb[2] = {64, static_cast<uint32_t>(q.nbox)}, ba[2] = {static_cast<uint32_t>(q.abox), 64};
@@ -505,6 +564,33 @@ int launch_brgemm_generic(const GenericParams& p, int compute_tf32, cudaStream_t
         p.stride_b % p.b_sn == 0 && p.jstride_b % p.b_sn == 0 &&
         static_cast<int64_t>(p.n_jobs) * (p.jstride_a / p.a_sk + p.batch * (p.stride_a / p.a_sk)) < (1ll << 31) &&
         static_cast<int64_t>(p.n_jobs) * (p.jstride_b / p.b_sn + p.batch * (p.stride_b / p.b_sn)) < (1ll << 31)) {
+      q.all_tma = 1;
+      q.rs_a = p.stride_a / p.a_sk;
+      q.rj_a = p.jstride_a / p.a_sk;
+      q.rs_b = p.stride_b / p.b_sn;
+      q.rj_b = p.jstride_b / p.b_sn;
+    }
+  }
+  // TF32 on fp32 blocks: the stride variant whose blocks start at view column 0 (every entry
+  // one box per operand; the kernel rounds the landed stages to TF32 in place)
+  if (compute_tf32 && !p.in_bf16 && p.mode == kModeStride && p.k % 32 == 0 &&
+      (p.n <= kRows || p.n % kRows == 0) && p.m % 32 == 0 && p.a_sm == 1 && p.b_sk == 1 && (p.a_sk * 4) % 16 == 0 &&
+      (p.b_sn * 4) % 16 == 0 && p.a_sk >= p.m && p.b_sn >= p.k && p.stride_a % p.a_sk == 0 &&
+      p.jstride_a % p.a_sk == 0 && p.stride_b % p.b_sn == 0 && p.jstride_b % p.b_sn == 0 &&
+      static_cast<int64_t>(p.n_jobs) * (p.jstride_a / p.a_sk + p.batch * (p.stride_a / p.a_sk)) < (1ll << 31) &&
+      static_cast<int64_t>(p.n_jobs) * (p.jstride_b / p.b_sn + p.batch * (p.stride_b / p.b_sn)) < (1ll << 31) &&
+      (reinterpret_cast<uintptr_t>(p.a_base) & 15) == 0 && (reinterpret_cast<uintptr_t>(p.b_base) & 15) == 0 &&
+      std::getenv("BRK_GENERIC_NO_TMA") == nullptr) {
+    q.nbox = std::min(p.n, kRows);
+    q.abox = 32;
+    const uint64_t rows_b = std::min<uint64_t>(0x7fffffffull, (1ull << 38) / (p.b_sn * 4));
+    const uint64_t rows_a = std::min<uint64_t>(0x7fffffffull, (1ull << 38) / (p.a_sk * 4));
+    const uint64_t db[2] = {static_cast<uint64_t>(p.b_sn), rows_b}, sb[2] = {1, static_cast<uint64_t>(p.b_sn)};
+    const uint64_t da[2] = {static_cast<uint64_t>(p.a_sk), rows_a}, sa[2] = {1, static_cast<uint64_t>(p.a_sk)};
+    const uint32_t bb[2] = {32, static_cast<uint32_t>(q.nbox)}, ba[2] = {32, 32};
+    if (encode_tmap(&q.map_bop, p.b_base, false, 2, db, sb, bb) == BRK_OK &&
+        encode_tmap(&q.map_aop, p.a_base, false, 2, da, sa, ba, /*atom32=*/true) == BRK_OK) {
+      q.tma = 1;
       q.all_tma = 1;
       q.rs_a = p.stride_a / p.a_sk;
       q.rj_a = p.jstride_a / p.a_sk;

@@ -110,6 +110,33 @@ int brk_brgemm_addr(const void* const* a_ptrs, const void* const* b_ptrs, void* 
   return run_generic(p, compute, stream);
 }
 
+int brk_brgemm_addr_views(const void* const* a_ptrs, const void* const* b_ptrs, void* const* c_ptrs,
+                          const void* a_view, int64_t a_view_elems, const void* b_view, int64_t b_view_elems,
+                          int n_jobs, int m, int n, int k, int batch, int64_t lda, int64_t ldb, int64_t ldc,
+                          float alpha, float beta, int in_dtype, int out_dtype, int compute, void* stream) {
+  int rc = check_common(m, n, k, batch, lda, ldb, ldc, in_dtype, out_dtype, compute, n_jobs);
+  if (rc) return rc;
+  if (n_jobs == 0 || m == 0 || n == 0) return BRK_OK;
+  if (c_ptrs == nullptr || (batch > 0 && (a_ptrs == nullptr || b_ptrs == nullptr)))
+    return set_error(BRK_ERR_CONTRACT, "null pointer table");
+  if (a_view_elems < 0 || b_view_elems < 0 || (a_view_elems > 0 && a_view == nullptr) ||
+      (b_view_elems > 0 && b_view == nullptr))
+    return set_error(BRK_ERR_CONTRACT, "brgemm_addr_views: a view needs a base and a non-negative extent");
+  GenericParams p{};
+  p.mode = kModeAddr;
+  p.n_jobs = n_jobs;
+  p.m = m; p.n = n; p.k = k; p.batch = batch;
+  p.lda = lda; p.ldb = ldb; p.ldc = ldc;
+  p.a_sk = lda; p.a_sm = 1; p.b_sn = ldb; p.b_sk = 1;
+  p.alpha = alpha; p.beta = beta;
+  p.in_bf16 = in_dtype == BRK_BF16;
+  p.out_bf16 = out_dtype == BRK_BF16;
+  p.a_ptrs = a_ptrs; p.b_ptrs = b_ptrs; p.c_ptrs = c_ptrs;
+  p.a_base = a_view; p.b_base = b_view;
+  p.a_view = a_view_elems; p.b_view = b_view_elems;
+  return run_generic(p, compute, stream);
+}
+
 int brk_brgemm_offs(const void* a_base, const void* b_base, const int64_t* a_offs,
                     const int64_t* b_offs, void* const* c_ptrs, int n_jobs, int m, int n, int k,
                     int batch, int64_t lda, int64_t ldb, int64_t ldc, float alpha, float beta,

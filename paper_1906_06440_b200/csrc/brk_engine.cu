@@ -156,6 +156,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // grouped launches: per-CTA, per-local-tile stamps [blockIdx.x][16 tiles][4]:
 // 0 producer 0 dependencies satisfied, 1 MMA first stage full, 2 MMA last commit, 3 epilogue released,
 // 4 epilogue got the accumulator, 5 stores issued, 6 proxy fence + barrier passed
+// (compiled only into the diagnostics build, `make diag` -> libbrk_sm100_diag.so, selected
+//  with BRK_LIB: the stamps cost ~50 instructions per epilogue tile)
+#ifdef BRK_DIAG
 #define BRK_TT(tile, slot)                                                                      \
   do {                                                                                          \
     if (gs != nullptr && P[0].debug_ts != nullptr && (tile) < 16)                               \
@@ -165,6 +168,14 @@ __device__ __forceinline__ unsigned long long gtimer() {
   do {                                                                            \
     if (gs == nullptr && P[0].debug_ts != nullptr) P[0].debug_ts[blockIdx.x * 16 + (slot)] = gtimer();   \
   } while (0)
+#else
+#define BRK_TT(tile, slot) \
+  do {                     \
+  } while (0)
+#define BRK_TS(slot) \
+  do {               \
+  } while (0)
+#endif
 
 __device__ __forceinline__ void named_bar_sync(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");

@@ -41,6 +41,10 @@ struct GenericParams {
   // mode == kModeOffs / kModeStride: base pointers
   const void* a_base;
   const void* b_base;
+  // mode == kModeAddr with views (brk_brgemm_addr_views): a_base/b_base are allocations of
+  // a_view/b_view elements that hold the blocks; an entry whose pointers fall inside them
+  // (element-aligned, block in bounds) is fetched by TMA like an offset entry
+  int64_t a_view, b_view;
   // mode == kModeOffs: device tables of n_jobs*batch element offsets
   const int64_t* a_offs;
   const int64_t* b_offs;

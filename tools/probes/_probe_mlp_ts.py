@@ -1,5 +1,9 @@
-"""Per-tile timeline of the fused MLP step (brk_mlp_step) from in-kernel %globaltimer stamps."""
+"""Per-tile timeline of the fused MLP step (brk_mlp_step) from in-kernel %globaltimer stamps.
+Needs the diagnostics build: make -C paper_1906_06440_b200/csrc diag (selected below via BRK_LIB)."""
+import os
 import sys
+os.environ.setdefault("BRK_LIB", os.path.join(os.path.dirname(__file__), "..", "..", "paper_1906_06440_b200",
+                                              "libbrk_sm100_diag.so"))
 import numpy as np
 import torch
 sys.path.insert(0, '.')

@@ -280,10 +280,10 @@ def brgemm_suite(ms=(32, 64, 128, 256), batches=(1, 4, 16, 64), variants=("strid
                     fn = lambda sp: _lib.check(lib.brk_brgemm_offs(  # noqa: E731
                         a.data_ptr(), b.data_ptr(), a_off.data_ptr(), b_off.data_ptr(), c_ptr.data_ptr(), jobs, m, n,
                         k, batch, m, k, m, 1.0, 0.0, in_dt, _lib.BRK_F32, comp, sp))
-                else:
-                    fn = lambda sp: _lib.check(lib.brk_brgemm_addr(  # noqa: E731
-                        a_ptr.data_ptr(), b_ptr.data_ptr(), c_ptr.data_ptr(), jobs, m, n, k, batch, m, k, m, 1.0,
-                        0.0, in_dt, _lib.BRK_F32, comp, sp))
+                else:  # address lists into two registered allocations (brk_brgemm_addr_views)
+                    fn = lambda sp: _lib.check(lib.brk_brgemm_addr_views(  # noqa: E731
+                        a_ptr.data_ptr(), b_ptr.data_ptr(), c_ptr.data_ptr(), a.data_ptr(), a.numel(), b.data_ptr(),
+                        b.numel(), jobs, m, n, k, batch, m, k, m, 1.0, 0.0, in_dt, _lib.BRK_F32, comp, sp))
                 mean, best = timer(fn, iters)
                 rows.append({"m": m, "n": n, "k": k, "batch": batch, "variant": var, "jobs": jobs,
                              "us": mean * 1e6, "tflops": flops / mean / 1e12, "roof_frac": t_roof / mean,
