@@ -783,7 +783,7 @@ __device__ __forceinline__ void engine_body(const EngineParams* P, const GroupSc
           const int s = s_begin + (s0 + rot < n_steps ? s0 + rot : s0 + rot - n_steps);
           if (chunked) {  // before the ring wait: the poll latency overlaps the slot becoming free
             wait_chunk(gs, prob, mb, static_cast<int>(rank), s);
-            if (!published) {
+            if (pid == 0 && !published) {  // only producer 0 publishes: the ordinal must not go back
               publish_deps(deps_seq, ordinal);
               published = true;
             }
