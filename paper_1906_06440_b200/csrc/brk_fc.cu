@@ -18,6 +18,7 @@
 #include <cuda_bf16.h>
 
 #include "brk_engine.h"
+#include "brk_mlp.h"
 #include "brk_internal.h"
 #include "brk_ptx.cuh"
 #include "brk_tma_host.h"
@@ -524,6 +525,60 @@ size_t mlp_counter_bytes(int L) { return (static_cast<size_t>(3 * L) * kCounterS
 size_t mlp_chunk_counters(int L, int N, int C) { return static_cast<size_t>(3 * L) * (N / 256) * 2 * (C / 64); }
 }  // namespace
 
+// The captured engine problems of the step -> the lean MLP kernel's problem table (brk_mlp.h):
+// the same operand maps and schedule, plus TMA maps for the epilogue's stores and side operands.
+static int to_mlp_group(const EngineGroup& G, int N, int C, MlpGroup& M) {
+  std::memset(&M, 0, sizeof(M));
+  M.sched = G.sched;
+  const Map4 act = act_layout(N, C), wl = w_layout(C, C);
+  int rc = 0;
+  for (int q = 0; q < G.sched.n_probs && !rc; ++q) {
+    const EngineParams& e = G.probs[q];
+    MlpProb& m = M.probs[q];
+    m.map_a = e.map_a;
+    m.map_b = e.map_b;
+    m.m_tiles = e.m_tiles;
+    m.n_tiles = e.n_tiles;
+    m.k_steps = e.k_steps;
+    m.a_rc2 = e.ca.rc[2]; m.a_rc3 = e.ca.rc[3]; m.a_kc2 = e.ca.kc[0][2]; m.a_kc3 = e.ca.kc[0][3];
+    m.b_rc2 = e.cb.rc[2]; m.b_rc3 = e.cb.rc[3]; m.b_kc2 = e.cb.kc[0][2]; m.b_kc3 = e.cb.kc[0][3];
+    m.a_mn = e.ca.mn_major;
+    m.b_mn = e.cb.mn_major;
+    m.cols = e.cols;
+    m.b_first = e.b_first;
+    m.bias = e.bias;
+    m.colsum_ws = e.colsum_ws;
+    m.db_partials = e.db_partials;
+    m.db_parts = e.db_parts;
+    m.db_out = e.db_out;
+    m.bias_sgd = e.bias_sgd;
+    m.lr = e.sgd_lr != 0.0f ? e.sgd_lr : e.bias_lr;
+    if (e.out_bf16) {
+      m.kind = e.aux_in != nullptr ? kMlpFwdTop : (e.bias != nullptr ? kMlpFwd : (e.mask != nullptr ? kMlpBwd : kMlpBwdPlain));
+      if ((rc = enc(&m.map_out, e.out, act, 64, 32, 1, 1))) break;
+      const void* in = m.kind == kMlpFwdTop ? e.aux_in : (m.kind == kMlpBwd ? e.mask : nullptr);
+      if (in != nullptr) {
+        m.has_in = 1;
+        if ((rc = enc(&m.map_in, in, act, 64, 32, 1, 1))) break;
+      }
+      if (m.kind == kMlpFwdTop) {
+        m.has_aux = 1;
+        if ((rc = enc(&m.map_aux, e.aux_out, act, 64, 32, 1, 1))) break;
+      }
+    } else {
+      m.kind = kMlpUpd;
+      const uint32_t box[4] = {32, 32, 1, 1};
+      if ((rc = encode_tmap(&m.map_out, e.out, false, 4, wl.dims, wl.strides, box))) break;
+      if (e.sgd_w != nullptr) {
+        m.has_in = m.has_aux = 1;
+        if ((rc = enc(&m.map_in, e.sgd_src != nullptr ? e.sgd_src : e.sgd_w, wl, 64, 32, 1, 1))) break;
+        if ((rc = enc(&m.map_aux, e.sgd_w, wl, 64, 32, 1, 1))) break;
+      }
+    }
+  }
+  return rc;
+}
+
 extern "C" {
 
 BRK_API size_t brk_mlp_step_workspace_bytes(int L, int N, int C) {
@@ -659,7 +714,11 @@ BRK_API int brk_mlp_step(int L, int N, int C, const void* const* y, void* const*
   // the counters are zero: zero-initialised once by the caller, re-zeroed by every launch's
   // last CTA (no memset between back-to-back steps)
   g_launches.fetch_add(1);
-  return launch_engine_group(G, 128, 1, st);
+  const char* lean_env = std::getenv("BRK_MLP_LEAN");  // 0 (diagnostics): the generic grouped engine
+  if (lean_env != nullptr && std::atoi(lean_env) == 0) return launch_engine_group(G, 128, 1, st);
+  static MlpGroup M;
+  if ((rc = to_mlp_group(G, N, C, M))) return rc;
+  return launch_mlp_group(M, st);
 }
 
 }  // extern "C"

@@ -1,0 +1,516 @@
+// brk_mlp.cu — the whole MLP training step (BASELINE config 2: L x FC(C) + bias
+// + ReLU, fwd / bwd-data / weight update + SGD) as ONE lean persistent
+// tcgen05 launch.  See brk_mlp.h.
+//
+// Roles (512 threads, one CTA per SM, CTA pairs = clusters of 2):
+//   warps 0..7   epilogue: warp w drains TMEM lane quarter w % 4 (32 rows) and
+//                column half w / 4 (64 columns = one 64-wide output block) of the
+//                CTA's 128 x 128 accumulator with ONE tcgen05.ld (x64), frees the
+//                accumulator, runs its problem kind's epilogue into a 32 x 128 B
+//                staging tile (128B swizzle, the TMA box layout) and stores it
+//                with one TMA store; side operands (dy, ReLU mask, old weights)
+//                were TMA-loaded into the warp's second staging tile before the
+//                accumulator was ready.
+//   warp 8       MMA issuer (leader CTA): tcgen05.mma cta_group::2, M = 256, N = 128.
+//   warps 9..14  TMA producers, one ring stage each (a TMA-issuing warp keeps about
+//                one box in flight, brk_diag_tma_bw).
+// Scheduling (tile order, dependency counters, 64-column chunk releases) is the
+// grouped engine's (brk_sched.cuh), so the host builds the same GroupSched.
+#include <cstdio>
+
+#include "brk_internal.h"
+#include "brk_mlp.h"
+#include "brk_ptx.cuh"
+#include "brk_sched.cuh"
+
+namespace brk {
+namespace {
+
+constexpr int kEpiWarps = 8;
+constexpr int kMmaWarp = kEpiWarps;
+constexpr int kStages = 6;
+constexpr int kProducers = kStages;
+constexpr int kThreads = 16 * 32;
+constexpr int kABytes = 128 * 128;  // per CTA per k-step: 128 rows x 64 bf16
+constexpr int kBBytes = 64 * 128;   // per CTA per k-step: 64 rows (N / 2) x 64 bf16
+constexpr int kStageBytes = kABytes + kBBytes;
+constexpr uint32_t kTxBytes = 2 * kStageBytes;  // both CTAs' boxes complete on the leader's barrier
+constexpr int kEpiTile = 4096;                  // 32 rows x 128 B
+constexpr int kEpiBytes = kEpiWarps * 2 * kEpiTile;
+constexpr int kBiasBytes = kEpiWarps * 256;
+constexpr int kBarBytes = 256;
+constexpr int kSmem = kStages * kStageBytes + kEpiBytes + kBiasBytes + kBarBytes + 1024;
+constexpr int kBN = 128;
+static_assert(kSmem <= 232448, "shared memory budget");
+
+__device__ __forceinline__ uint32_t relu_pack(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+__device__ __forceinline__ uint32_t bf16_pack(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+__device__ __forceinline__ void sts128(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
+}
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ float4 lds_f4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+// smem operand descriptor of MMA sub-step kk (16 K-elements) — bf16, 128B swizzle
+__device__ __forceinline__ uint64_t op_desc(uint32_t base, int mn_major, int kk) {
+  return mn_major ? make_smem_desc(base + kk * 16 * 128, 64 * 128, 1024, kSwizzle128B)
+                  : make_smem_desc(base + kk * 32, 16, 1024, kSwizzle128B);
+}
+
+__device__ __forceinline__ void locate(const GroupSched* gs, const MlpProb* P, int u, int& prob, int& mb, int& nb) {
+  prob = 0;
+  while (prob + 1 < gs->n_probs && u >= gs->tile_begin[prob + 1]) ++prob;
+  const int rel = u - gs->tile_begin[prob];
+  nb = rel % P[prob].n_tiles;
+  mb = rel / P[prob].n_tiles;
+}
+
+// Column sums over the 32 rows of a staged bf16 tile: lane l sums columns 2l, 2l + 1
+// (32-bit word l % 4 of 16 B chunk l / 4, which sits at chunk (l / 4) ^ (r % 8) of row r).
+__device__ __forceinline__ void tile_colsum(uint32_t tile, int lane, float* dst) {
+  const uint32_t j = static_cast<uint32_t>(lane) >> 2, wd = (static_cast<uint32_t>(lane) & 3u) << 2;
+  float s0 = 0.0f, s1 = 0.0f;
+#pragma unroll 8
+  for (uint32_t r = 0; r < 32; ++r) {
+    const uint32_t x = lds32(tile + r * 128 + (((j ^ (r & 7u)) << 4) | wd));
+    s0 += __uint_as_float(x << 16);
+    s1 += __uint_as_float(x & 0xffff0000u);
+  }
+  *reinterpret_cast<float2*>(dst + 2 * lane) = make_float2(s0, s1);
+}
+
+__global__ void __launch_bounds__(kThreads, 1) mlp_step_kernel(const __grid_constant__ MlpGroup G) {
+  const MlpProb* P = G.probs;
+  const GroupSched* gs = &G.sched;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* epi = smem + kStages * kStageBytes;
+  float* bias_area = reinterpret_cast<float*>(epi + kEpiBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi + kEpiBytes + kBiasBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* tfull = empty + kStages;   // [2]
+  uint64_t* tempty = tfull + 2;        // [2]
+  uint64_t* ebar = tempty + 2;         // [kEpiWarps]: epilogue side-operand loads
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ebar + kEpiWarps);
+  uint32_t* deps_seq = tmem_slot + 1;
+  uint32_t* exit_flag = tmem_slot + 2;
+
+  const int warp = warp_id();
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int unit0 = static_cast<int>(blockIdx.x >> 1);
+  const int n_units = static_cast<int>(gridDim.x >> 1);
+  const int num_work = gs->tile_begin[gs->n_probs];
+
+  if (warp == kMmaWarp + 1 && lane == 0) {
+    for (int q = 0; q < gs->n_probs; ++q) {
+      tma_prefetch_desc(&P[q].map_a);
+      tma_prefetch_desc(&P[q].map_b);
+    }
+    *deps_seq = 0u;
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 2 * kEpiWarps);
+    }
+    for (int w = 0; w < kEpiWarps; ++w) mbar_init(&ebar[w], 1);
+    fence_barrier_init();
+  }
+  if (warp == kMmaWarp) tmem_alloc_pair(tmem_slot, 2 * kBN);
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  pdl_launch_dependents();
+
+  if (warp > kMmaWarp) {
+    // ---------------------------------------------------------------- producers
+    const int pid = warp - kMmaWarp - 1;
+    if (pid < kProducers && elect_one()) {
+      pdl_wait();
+      int g = 0;
+      uint32_t ordinal = 0;
+      for (int u = unit0; u < num_work; u += n_units) {
+        int prob, mb, nb;
+        locate(gs, P, u, prob, mb, nb);
+        const MlpProb& p = P[prob];
+        ++ordinal;
+        const bool chunked = has_dep_mode(gs, prob, true);
+        bool published = !chunked;
+        bool deps_pending = !chunked || has_dep_mode(gs, prob, false);
+        if (pid == 0) {
+          wait_deps(gs, P, prob, mb, 2);
+          if (!chunked) publish_deps(deps_seq, ordinal);
+          deps_pending = false;
+        } else if (deps_pending && !p.b_first) {
+          wait_published(deps_seq, ordinal, true);
+          deps_pending = false;
+        }
+        const int arow = mb * 2 + static_cast<int>(rank);
+        const int brow = nb * 2 + static_cast<int>(rank);
+        const int n_steps = p.k_steps;
+        // rotate the batch-list start per tile (concurrent tiles read different blocks)
+        const int rot = (mb * 7 + nb * 3) % n_steps;
+        const int a2 = p.a_rc2 * arow, a3 = p.a_rc3 * arow, b2 = p.b_rc2 * brow, b3 = p.b_rc3 * brow;
+        for (int s0 = (pid - g % kProducers + kProducers) % kProducers; s0 < n_steps; s0 += kProducers) {
+          const int gg = g + s0;
+          const int stage = gg % kStages;
+          const uint32_t phase = (gg / kStages) & 1;
+          const int s = s0 + rot < n_steps ? s0 + rot : s0 + rot - n_steps;
+          if (chunked) {  // before the ring wait: the poll latency overlaps the slot becoming free
+            wait_chunk(gs, prob, mb, static_cast<int>(rank), s);
+            if (pid == 0 && !published) {
+              publish_deps(deps_seq, ordinal);
+              published = true;
+            }
+          }
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * kStageBytes;
+          if (leader) mbar_arrive_expect_tx(&full[stage], kTxBytes);
+          const int32_t ca[4] = {0, 0, a2 + p.a_kc2 * s, a3 + p.a_kc3 * s};
+          const int32_t cb[4] = {0, 0, b2 + p.b_kc2 * s, b3 + p.b_kc3 * s};
+          if (deps_pending) {  // B (weights) does not wait for the tile's dependencies
+            tma_load_pair<4>(sa + kABytes, &p.map_b, &full[stage], cb);
+            wait_published(deps_seq, ordinal, true);
+            deps_pending = false;
+            tma_load_pair<4>(sa, &p.map_a, &full[stage], ca);
+          } else {
+            tma_load_pair<4>(sa, &p.map_a, &full[stage], ca);
+            tma_load_pair<4>(sa + kABytes, &p.map_b, &full[stage], cb);
+          }
+        }
+        if (!published && pid == 0) {
+          wait_chunk(gs, prob, mb, static_cast<int>(rank), 0);
+          publish_deps(deps_seq, ordinal);
+        }
+        g += n_steps;
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    // ---------------------------------------------------------------- MMA issuer (leader CTA)
+    if (leader) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      for (int u = unit0; u < num_work; u += n_units, ++local) {
+        int prob, mb, nb;
+        locate(gs, P, u, prob, mb, nb);
+        const MlpProb& p = P[prob];
+        const int a_mn = p.a_mn, b_mn = p.b_mn, n_steps = p.k_steps;
+        const uint32_t idesc = make_idesc(kFmtBF16, 256, kBN, a_mn, b_mn);
+        const int acc = local & 1;
+        mbar_wait(&tempty[acc], ((local >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * kBN;
+        for (int s = 0; s < n_steps; ++s) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t sa = smem_u32(smem + stage * kStageBytes);
+            const uint32_t sb = sa + kABytes;
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              mma_ss_pair<false>(d_tmem, op_desc(sa, a_mn, kk), op_desc(sb, b_mn, kk), idesc, (s | kk) ? 1u : 0u);
+            mma_commit_pair(&empty[stage]);
+            if (s == n_steps - 1) mma_commit_pair(&tfull[acc]);
+          }
+          __syncwarp();
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else {
+    // ---------------------------------------------------------------- epilogue (warps 0..7)
+    pdl_wait();
+    const int quarter = warp & 3, half = warp >> 2;
+    const uint32_t st0 = smem_u32(epi + warp * 2 * kEpiTile), st1 = st0 + kEpiTile;
+    const uint32_t lrow = static_cast<uint32_t>(lane) * 128;
+    const uint32_t lsw = static_cast<uint32_t>(lane & 7);
+    const uint32_t bias_s = smem_u32(bias_area + warp * 64);
+    const uint32_t tempty_leader = mapa_shared(smem_u32(&tempty[0]), 0);
+    uint32_t ephase = 0;
+    int local = 0;
+    for (int u = unit0; u < num_work; u += n_units, ++local) {
+      int prob, mb, nb;
+      locate(gs, P, u, prob, mb, nb);
+      const MlpProb& p = P[prob];
+      const int kind = p.kind;
+      const int acc = local & 1;
+      const int row0 = mb * 256 + static_cast<int>(rank) * 128 + quarter * 32;  // this warp's first row
+      const int colblk = nb * 2 + half;                                          // its 64-column output block
+      const bool upd = kind == kMlpUpd;
+      // side operand by TMA, issued before the accumulator wait (dy is an input; the ReLU mask
+      // and the weights may be written earlier in this launch: acquire the tile's dependencies)
+      if (p.has_in) {
+        if (kind != kMlpFwdTop) wait_published(deps_seq, static_cast<uint32_t>(local + 1), true);
+        if (lane == 0) {
+          mbar_arrive_expect_tx(&ebar[warp], kEpiTile);
+          const int32_t c[4] = {0, row0 & 63, upd ? row0 >> 6 : colblk, upd ? colblk : row0 >> 6};
+          tma_load<4>(epi + (warp * 2 + 1) * kEpiTile, &p.map_in, &ebar[warp], c);
+        }
+      } else if (p.db_partials != nullptr) {
+        wait_published(deps_seq, static_cast<uint32_t>(local + 1), false);
+      }
+      if (kind <= kMlpFwdTop) {  // this warp's 64 bias values -> smem (read back as broadcasts)
+        const float b0 = __ldg(p.bias + colblk * 64 + lane), b1 = __ldg(p.bias + colblk * 64 + 32 + lane);
+        asm volatile("st.shared.f32 [%0], %1;" ::"r"(bias_s + lane * 4), "f"(b0) : "memory");
+        asm volatile("st.shared.f32 [%0], %1;" ::"r"(bias_s + 128 + lane * 4), "f"(b1) : "memory");
+      }
+      mbar_wait(&tfull[acc], (local >> 1) & 1);
+      tc_fence_after();
+      uint32_t v[64];
+      tmem_ld64(tmem_base + acc * kBN + (static_cast<uint32_t>(quarter * 32) << 16) + half * 64, v);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster_relaxed(tempty_leader + acc * 8);  // accumulator free
+      if (p.has_in) {
+        mbar_wait(&ebar[warp], ephase);
+        ephase ^= 1;
+      }
+      const int32_t ao[4] = {0, row0 & 63, colblk, row0 >> 6};  // activation-layout box
+      float* colsum_dst = p.colsum_ws != nullptr ? p.colsum_ws + (row0 >> 5) * p.cols + colblk * 64 : nullptr;
+      if (kind <= kMlpFwdTop) {
+        // y = relu(acc + bias) -> st0; top layer: dz = dy * (y > 0) in place in st1
+        const bool top = kind == kMlpFwdTop;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float4 bl = lds_f4(bias_s + j * 32), bh = lds_f4(bias_s + j * 32 + 16);
+          const uint32_t x = relu_pack(__uint_as_float(v[8 * j]) + bl.x, __uint_as_float(v[8 * j + 1]) + bl.y);
+          const uint32_t y = relu_pack(__uint_as_float(v[8 * j + 2]) + bl.z, __uint_as_float(v[8 * j + 3]) + bl.w);
+          const uint32_t z = relu_pack(__uint_as_float(v[8 * j + 4]) + bh.x, __uint_as_float(v[8 * j + 5]) + bh.y);
+          const uint32_t w = relu_pack(__uint_as_float(v[8 * j + 6]) + bh.z, __uint_as_float(v[8 * j + 7]) + bh.w);
+          const uint32_t off = lrow + ((static_cast<uint32_t>(j) ^ lsw) << 4);
+          sts128(st0 + off, x, y, z, w);
+          if (top) {  // relu outputs are >= +0: y > 0 <=> the bf16 bits as int16 > 0
+            const uint4 d = lds128(st1 + off);
+            sts128(st1 + off, d.x & __vcmpgts2(x, 0u), d.y & __vcmpgts2(y, 0u), d.z & __vcmpgts2(z, 0u),
+                   d.w & __vcmpgts2(w, 0u));
+          }
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store4(&p.map_out, st0, ao[0], ao[1], ao[2], ao[3]);
+          if (top) tma_store4(&p.map_aux, st1, ao[0], ao[1], ao[2], ao[3]);
+          bulk_commit();
+        }
+        if (top) tile_colsum(st1, lane, colsum_dst);
+      } else if (kind <= kMlpBwdPlain) {
+        // dz = bf16(acc) * (mask > 0) (mask: the previous layer's ReLU output, >= +0)
+        const bool masked = kind == kMlpBwd;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          uint32_t x = bf16_pack(__uint_as_float(v[8 * j]), __uint_as_float(v[8 * j + 1]));
+          uint32_t y = bf16_pack(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3]));
+          uint32_t z = bf16_pack(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5]));
+          uint32_t w = bf16_pack(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7]));
+          const uint32_t off = lrow + ((static_cast<uint32_t>(j) ^ lsw) << 4);
+          if (masked) {
+            const uint4 m = lds128(st1 + off);
+            x &= __vcmpgts2(m.x, 0u);
+            y &= __vcmpgts2(m.y, 0u);
+            z &= __vcmpgts2(m.z, 0u);
+            w &= __vcmpgts2(m.w, 0u);
+          }
+          sts128(st0 + off, x, y, z, w);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store4(&p.map_out, st0, ao[0], ao[1], ao[2], ao[3]);
+          bulk_commit();
+        }
+        if (colsum_dst != nullptr) tile_colsum(st0, lane, colsum_dst);
+      } else {
+        // weight update: dW (fp32, two 32-column boxes through st0); w_next = w - lr dW (st1)
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          if (hh == 1) {
+            if (lane == 0) bulk_wait_read0();  // st0 free again
+            __syncwarp();
+          }
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            sts128(st0 + lrow + ((static_cast<uint32_t>(c) ^ lsw) << 4), v[32 * hh + 4 * c], v[32 * hh + 4 * c + 1],
+                   v[32 * hh + 4 * c + 2], v[32 * hh + 4 * c + 3]);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store4(&p.map_out, st0, 32 * hh, row0 & 63, row0 >> 6, colblk);
+            bulk_commit();
+          }
+          if (hh == 0 && p.has_aux) {
+            const float lr = p.lr;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const uint32_t off = lrow + ((static_cast<uint32_t>(j) ^ lsw) << 4);
+              const uint4 wq = lds128(st1 + off);
+              const uint32_t wv[4] = {wq.x, wq.y, wq.z, wq.w};
+              uint32_t o[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                o[e] = bf16_pack(__uint_as_float(wv[e] << 16) - lr * __uint_as_float(v[8 * j + 2 * e]),
+                                 __uint_as_float(wv[e] & 0xffff0000u) - lr * __uint_as_float(v[8 * j + 2 * e + 1]));
+              sts128(st1 + off, o[0], o[1], o[2], o[3]);
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store4(&p.map_aux, st1, 0, row0 & 63, row0 >> 6, colblk);
+              bulk_commit();
+            }
+          }
+        }
+      }
+      // outputs complete -> release this warp's 32 rows x 64 columns to dependent tiles
+      if (lane == 0) {
+        bulk_wait0();
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        if (!upd && gs->chunk_counters != nullptr)
+          red_release_add(gs->chunk_counters + ((prob * gs->chunk_mb + mb) * 2 + rank) * gs->chunk_n + colblk, 1u);
+      }
+      // bias gradient of the layer from the column-sum partials (row-block-0 tiles of the update)
+      if (upd && p.db_partials != nullptr && mb == 0 && rank == 0) {
+        const int t = threadIdx.x, c = t & (kBN - 1), grp = t >> 7;  // 2 groups x 128 columns
+        const int col = nb * kBN + c;
+        const int per = (p.db_parts + 1) / 2, q0 = grp * per, q1 = min(p.db_parts, q0 + per);
+        float s = 0.0f;
+        for (int q = q0; q < q1; q += 8) {
+          float x[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) x[e] = q + e < q1 ? __ldcg(p.db_partials + (q + e) * p.cols + col) : 0.0f;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) s += x[e];
+        }
+        const uint32_t red = smem_u32(bias_area) + c * 4;
+        if (grp == 1) asm volatile("st.shared.f32 [%0], %1;" ::"r"(red), "f"(s) : "memory");
+        bar_sync(2, kEpiWarps * 32);
+        if (grp == 0) {
+          float o;
+          asm volatile("ld.shared.f32 %0, [%1];" : "=f"(o) : "r"(red) : "memory");
+          s += o;
+          p.db_out[col] = s;
+          if (p.bias_sgd != nullptr) p.bias_sgd[col] -= p.lr * s;
+        }
+        bar_sync(2, kEpiWarps * 32);  // the bias area is reused by the next tile
+      }
+      // whole-tile release (row-block / whole-problem counters: weight updates, in-place SGD)
+      bar_sync(1, kEpiWarps * 32);
+      if (threadIdx.x == 0) {
+        red_release_add(gs->counters + prob * kCounterStride + mb, 1u);
+        red_release_add(gs->counters + prob * kCounterStride + kCounterStride - 1, 1u);
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == kMmaWarp) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem_base, 2 * kBN);
+  }
+  // every CTA is done with the counters: the last one out re-zeroes them for the next launch
+  unsigned* exit_ctr = gs->counters + gs->n_probs * kCounterStride;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    *exit_flag = atomicAdd(exit_ctr, 1u) == gridDim.x - 1 ? 1u : 0u;
+  }
+  __syncthreads();
+  if (*exit_flag) {
+    __threadfence();
+    for (int i = threadIdx.x; i <= gs->n_probs * kCounterStride; i += blockDim.x) gs->counters[i] = 0u;
+    if (gs->chunk_counters != nullptr) {
+      const int nc = gs->n_probs * gs->chunk_mb * 2 * gs->chunk_n;
+      for (int i = threadIdx.x; i < nc; i += blockDim.x) gs->chunk_counters[i] = 0u;
+    }
+  }
+}
+
+}  // namespace
+
+int engine_sm_count();
+
+int launch_mlp_group(const MlpGroup& G, cudaStream_t stream) {
+  const GroupSched& gs = G.sched;
+  if (gs.n_probs < 1 || gs.n_probs > kMaxProbs || gs.counters == nullptr)
+    return set_error(BRK_ERR_CONTRACT, "mlp group: 1..12 problems and a counter buffer");
+  for (int q = 0; q < gs.n_probs; ++q) {
+    const MlpProb& p = G.probs[q];
+    if (gs.tile_begin[q + 1] - gs.tile_begin[q] != p.m_tiles * p.n_tiles || p.k_steps < 1)
+      return set_error(BRK_ERR_CONTRACT, "mlp group: tile_begin does not match the problem's tiles");
+    if (p.m_tiles > kCounterStride - 1) return set_error(BRK_ERR_CONTRACT, "mlp group: > 64 row blocks");
+    for (int d = 0; d < kMaxDeps; ++d)
+      if (gs.dep_prob[q][d] >= q) return set_error(BRK_ERR_CONTRACT, "mlp group: dependencies must point back");
+  }
+  static int attr_set = 0;
+  cudaError_t err;
+  if (!attr_set) {
+    err = cudaFuncSetAttribute(mlp_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    if (err != cudaSuccess) return set_cuda_error(err, "mlp smem attribute");
+    attr_set = 1;
+  }
+  const int units = engine_sm_count() / 2;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(units * 2);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attrs[2];
+  attrs[0].id = cudaLaunchAttributeClusterDimension;
+  attrs[0].val.clusterDim.x = 2;
+  attrs[0].val.clusterDim.y = 1;
+  attrs[0].val.clusterDim.z = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  // tiles spin on counters of earlier problems: every CTA must be resident at once
+  static int resident = -1;
+  if (resident < 0) {
+    err = cudaOccupancyMaxActiveClusters(&resident, mlp_step_kernel, &cfg);
+    if (err != cudaSuccess) return set_cuda_error(err, "mlp occupancy");
+  }
+  if (resident < units) {
+    char buf[128];
+    std::snprintf(buf, sizeof(buf), "mlp step: %d CTA pairs must be co-resident, the device holds %d", units,
+                  resident);
+    return set_error(BRK_ERR_CONTRACT, buf);
+  }
+  attrs[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.numAttrs = 2;
+  err = cudaLaunchKernelEx(&cfg, mlp_step_kernel, G);
+  if (err != cudaSuccess) return set_cuda_error(err, "mlp step launch");
+  return BRK_OK;
+}
+
+}  // namespace brk

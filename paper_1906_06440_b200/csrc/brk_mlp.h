@@ -1,0 +1,63 @@
+// brk_mlp.h — the fused MLP training step (BASELINE config 2) as one lean
+// persistent tcgen05 launch (brk_mlp.cu).
+//
+// Same schedule as the grouped engine (brk_engine.h: GroupSched, one CTA pair
+// per 256 x 128 output tile, tile-level / 64-column-chunk dependency counters),
+// but every problem is one of five fixed MLP passes, so the kernel carries only
+// their epilogues: each is a short, fully specialised code path (the grouped
+// engine's general epilogue executed ~63 KB of code per step, twice the SM's
+// instruction cache) whose outputs leave through TMA stores from a per-warp
+// staging tile and whose side operands (output gradient, ReLU mask, old
+// weights) arrive by TMA before the accumulator does.
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+
+#include "brk_engine.h"
+
+namespace brk {
+
+enum MlpKind : int32_t {
+  kMlpFwd = 0,      // y = relu(acc + bias)                                  -> out (bf16)
+  kMlpFwdTop = 1,   // y = relu(acc + bias) -> out; dz = dy * (y > 0) -> aux, column sums of dz
+  kMlpBwd = 2,      // dz = acc * (mask > 0) -> out (bf16), column sums of dz
+  kMlpBwdPlain = 3, // dx = acc -> out (bf16)
+  kMlpUpd = 4,      // dW = acc -> out (fp32); w_next = w - lr dW -> aux; db = sum of partials
+};
+
+// One problem of the step.  Operand k-step s of a tile in row block `row`
+// (A: the CTA's 128-row block, B: its 64-row block) is the 4-d TMA box at
+//   (0, 0, rc2 * row + kc2 * s, rc3 * row + kc3 * s)
+// of map_a / map_b (the blocked FC layouts of brk_fc.cu).
+struct MlpProb {
+  CUtensorMap map_a;
+  CUtensorMap map_b;
+  CUtensorMap map_out;  // bf16 activations: box (64, 32, 1, 1); fp32 dW: box (32, 32, 1, 1)
+  CUtensorMap map_in;   // dy (top) / ReLU mask (bwd) / old weights (upd): box (64, 32, 1, 1)
+  CUtensorMap map_aux;  // dz_L (top) / new weights (upd): box (64, 32, 1, 1)
+  int32_t kind;         // MlpKind
+  int32_t m_tiles, n_tiles, k_steps;
+  int32_t a_rc2, a_rc3, a_kc2, a_kc3;
+  int32_t b_rc2, b_rc3, b_kc2, b_kc3;
+  int32_t a_mn, b_mn;   // MN-major operand (UMMA descriptor / idesc)
+  int32_t cols;         // output columns (row length of colsum_ws)
+  int32_t has_in;       // the epilogue loads map_in
+  int32_t has_aux;      // the epilogue stores map_aux
+  int32_t b_first;      // B does not depend on this problem's dependencies
+  const float* bias;
+  float* colsum_ws;     // [rows / 32][cols] column sums of the stored gradient
+  const float* db_partials;  // upd: [db_parts][cols] partials to reduce into db_out
+  int32_t db_parts;
+  float* db_out;
+  float* bias_sgd;      // upd: bias -= lr * db (may be null)
+  float lr;
+};
+
+struct MlpGroup {
+  MlpProb probs[kMaxProbs];
+  GroupSched sched;
+};
+
+int launch_mlp_group(const MlpGroup& G, cudaStream_t stream);
+
+}  // namespace brk
