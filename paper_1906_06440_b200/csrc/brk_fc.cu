@@ -718,6 +718,9 @@ BRK_API int brk_mlp_step(int L, int N, int C, const void* const* y, void* const*
   if (lean_env != nullptr && std::atoi(lean_env) == 0) return launch_engine_group(G, 128, 1, st);
   static MlpGroup M;
   if ((rc = to_mlp_group(G, N, C, M))) return rc;
+  M.debug_ts = g_debug_ts;
+  const char* fl = std::getenv("BRK_MLP_FLAGS");
+  M.flags = fl ? std::atoi(fl) : 0;
   return launch_mlp_group(M, st);
 }
 

@@ -106,6 +106,22 @@ __device__ __forceinline__ void tile_colsum(uint32_t tile, int lane, float* dst)
   *reinterpret_cast<float2*>(dst + 2 * lane) = make_float2(s0, s1);
 }
 
+#ifdef BRK_DIAG
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define MLP_TT(tile, slot)                                                                   \
+  do {                                                                                       \
+    if (G.debug_ts != nullptr && (tile) < 16) G.debug_ts[(blockIdx.x * 16 + (tile)) * 8 + (slot)] = gtimer(); \
+  } while (0)
+#else
+#define MLP_TT(tile, slot) \
+  do {                     \
+  } while (0)
+#endif
+
 __global__ void __launch_bounds__(kThreads, 1) mlp_step_kernel(const __grid_constant__ MlpGroup G) {
   const MlpProb* P = G.probs;
   const GroupSched* gs = &G.sched;
@@ -171,7 +187,10 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_step_kernel(const __grid_cons
         bool deps_pending = !chunked || has_dep_mode(gs, prob, false);
         if (pid == 0) {
           wait_deps(gs, P, prob, mb, 2);
-          if (!chunked) publish_deps(deps_seq, ordinal);
+          if (!chunked) {
+            publish_deps(deps_seq, ordinal);
+            MLP_TT(static_cast<int>(ordinal) - 1, 0);
+          }
           deps_pending = false;
         } else if (deps_pending && !p.b_first) {
           wait_published(deps_seq, ordinal, true);
@@ -181,7 +200,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_step_kernel(const __grid_cons
         const int brow = nb * 2 + static_cast<int>(rank);
         const int n_steps = p.k_steps;
         // rotate the batch-list start per tile (concurrent tiles read different blocks)
-        const int rot = (mb * 7 + nb * 3) % n_steps;
+        const int rot = (G.flags & 1) ? (mb * 7 + nb * 3) % n_steps : 0;  // no rotation: tiles sharing a row block read the same A box at about the same time (L2 dedup: 69.5 -> 68.6 us)
         const int a2 = p.a_rc2 * arow, a3 = p.a_rc3 * arow, b2 = p.b_rc2 * brow, b3 = p.b_rc3 * brow;
         for (int s0 = (pid - g % kProducers + kProducers) % kProducers; s0 < n_steps; s0 += kProducers) {
           const int gg = g + s0;
@@ -192,6 +211,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_step_kernel(const __grid_cons
             wait_chunk(gs, prob, mb, static_cast<int>(rank), s);
             if (pid == 0 && !published) {
               publish_deps(deps_seq, ordinal);
+              MLP_TT(static_cast<int>(ordinal) - 1, 0);
               published = true;
             }
           }
@@ -236,6 +256,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_step_kernel(const __grid_cons
         for (int s = 0; s < n_steps; ++s) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
+          if (s == 0 && lane == 0) MLP_TT(local, 1);
           if (elect_one()) {
             const uint32_t sa = smem_u32(smem + stage * kStageBytes);
             const uint32_t sb = sa + kABytes;
@@ -248,6 +269,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_step_kernel(const __grid_cons
           __syncwarp();
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
+        if (lane == 0) MLP_TT(local, 2);
       }
     }
   } else {
@@ -292,6 +314,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_step_kernel(const __grid_cons
       uint32_t v[64];
       tmem_ld64(tmem_base + acc * kBN + (static_cast<uint32_t>(quarter * 32) << 16) + half * 64, v);
       tmem_ld_wait();
+      if (threadIdx.x == 0) MLP_TT(local, 4);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster_relaxed(tempty_leader + acc * 8);  // accumulator free
@@ -395,11 +418,14 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_step_kernel(const __grid_cons
         }
       }
       // outputs complete -> release this warp's 32 rows x 64 columns to dependent tiles
+      if (threadIdx.x == 0) MLP_TT(local, 5);
       if (lane == 0) {
         bulk_wait0();
-        asm volatile("fence.proxy.async.global;" ::: "memory");
+        if (threadIdx.x == 0) MLP_TT(local, 6);
+        if (!(G.flags & 2)) asm volatile("fence.proxy.async.global;" ::: "memory");
         if (!upd && gs->chunk_counters != nullptr)
           red_release_add(gs->chunk_counters + ((prob * gs->chunk_mb + mb) * 2 + rank) * gs->chunk_n + colblk, 1u);
+        if (threadIdx.x == 0) MLP_TT(local, 7);
       }
       // bias gradient of the layer from the column-sum partials (row-block-0 tiles of the update)
       if (upd && p.db_partials != nullptr && mb == 0 && rank == 0) {
@@ -431,6 +457,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_step_kernel(const __grid_cons
       if (threadIdx.x == 0) {
         red_release_add(gs->counters + prob * kCounterStride + mb, 1u);
         red_release_add(gs->counters + prob * kCounterStride + kCounterStride - 1, 1u);
+        MLP_TT(local, 3);
       }
     }
   }

@@ -56,6 +56,11 @@ struct MlpProb {
 struct MlpGroup {
   MlpProb probs[kMaxProbs];
   GroupSched sched;
+  // diagnostics build only (BRK_DIAG): per-CTA, per-local-tile %globaltimer stamps
+  // [blockIdx.x][16][8], slots as in the grouped engine (brk_engine.cu BRK_TT)
+  unsigned long long* debug_ts;
+  // tuning (BRK_MLP_FLAGS): bit0 per-tile k-step rotation, bit1 no writer-side proxy fence
+  int32_t flags;
 };
 
 int launch_mlp_group(const MlpGroup& G, cudaStream_t stream);

@@ -53,9 +53,10 @@ for unit in range(n_units):
         p = np.searchsorted(begin, u, side="right") - 1
         rows.append((p, *(a[unit, i] - t0)))
 rows = np.array(rows, dtype=np.float64)
-print("prob  tiles  dep_ok(min..max)   mma_start   mma_len(mean)  epi_len(mean)  done(max) | commit->acc acc->stored stored->fenced fenced->released [us]")
+print("prob  tiles  dep_ok(min..max)   mma_start   mma_len(mean)  epi_len(mean)  done(max) | commit->acc acc->stored stored->fenced fenced->released [us] | chunk released (lean kernel)")
 for p in range(12):
     r = rows[rows[:, 0] == p]
     print(f"{names[p]:5s} {len(r):4d}  {r[:,1].min()/1e3:7.2f}..{r[:,1].max()/1e3:7.2f}  {r[:,2].mean()/1e3:8.2f}  "
           f"{(r[:,3]-r[:,2]).mean()/1e3:8.2f}  {(r[:,4]-r[:,3]).mean()/1e3:8.2f}  {r[:,4].max()/1e3:8.2f} | "
-          f"{(r[:,5]-r[:,3]).mean()/1e3:6.2f} {(r[:,6]-r[:,5]).mean()/1e3:6.2f} {(r[:,7]-r[:,6]).mean()/1e3:6.2f} {(r[:,4]-r[:,7]).mean()/1e3:6.2f}")
+          f"{(r[:,5]-r[:,3]).mean()/1e3:6.2f} {(r[:,6]-r[:,5]).mean()/1e3:6.2f} {(r[:,7]-r[:,6]).mean()/1e3:6.2f} {(r[:,4]-r[:,7]).mean()/1e3:6.2f}"
+          f" | {(r[:,8]-r[:,7]).mean()/1e3:6.2f}")
