@@ -197,12 +197,12 @@ def cpu_baseline_sample():
 # GPU arm
 # ---------------------------------------------------------------------------
 def kernel_roofline(mlp, torch, peak_tflops):
-    """Roofline block for the dominant kernel of the timed step: the grouped
-    persistent engine launch that runs the whole MLP step (brk_mlp_step,
-    engine_group_kernel).  Algorithmic FLOPs per launch = 12 * 2NCK (SURVEY
-    8(d)); time per launch from CUDA events around a graph of 10 launches on
-    the launching stream; traffic = ncu dram read + write bytes of one launch
-    (profiles/r01c_mlp_kernel.json).  The standalone per-pass kernels (the
+    """Roofline block for the dominant kernel of the timed step: the lean
+    persistent launch that runs the whole MLP step (brk_mlp_step,
+    mlp_step_kernel in csrc/brk_mlp.cu).  Algorithmic FLOPs per launch = 12 *
+    2NCK; time per launch from CUDA events around a graph of 10
+    launches on the launching stream; traffic = ncu dram read + write bytes of
+    one launch (profiles/r02/mlp_kernel_ncu.json).  The standalone per-pass kernels (the
     13-launch path) are timed the same way and reported alongside."""
     from paper_1906_06440_b200 import _lib
     from paper_1906_06440_b200.mlp import flops_per_step
@@ -246,12 +246,12 @@ def kernel_roofline(mlp, torch, peak_tflops):
     }
     per_pass = {k: graph_time(fn) * 1e6 for k, fn in passes.items()}
     traffic = None
-    tf = ROOT / "profiles" / "r01c_mlp_kernel.json"
+    tf = ROOT / "profiles" / "r02" / "mlp_kernel_ncu.json"
     if tf.exists():
         try:
             for recs in json.loads(tf.read_text()).values():
                 for r in recs:
-                    if "engine_group_kernel" in r["kernel"]:
+                    if "mlp_step_kernel" in r["kernel"]:
                         rd = float(r["dram__bytes_read.sum"].split()[0])
                         wr = float(r["dram__bytes_write.sum"].split()[0])
                         traffic = (rd + wr) * 1e6  # ncu reports Mbyte
@@ -262,7 +262,7 @@ def kernel_roofline(mlp, torch, peak_tflops):
         step_flops = 2.0 * n * c * c
         kernel = "brk engine_kernel (one FC pass)"
     else:
-        kernel = "brk engine_group_kernel<128, pair>: the whole MLP step (12 GEMMs) in one persistent launch"
+        kernel = "brk mlp_step_kernel: the whole MLP step (12 GEMMs, 256x128 CTA-pair tiles) in one persistent launch"
     achieved = step_flops / t_step / 1e12
     return {"bound": "tensor", "achieved": achieved, "peak": peak_tflops, "unit": "TFLOP/s",
             "frac": achieved / peak_tflops, "traffic": traffic, "kernel": kernel,
