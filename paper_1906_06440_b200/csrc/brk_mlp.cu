@@ -16,6 +16,8 @@
 //                one box in flight, brk_diag_tma_bw).
 // Scheduling (tile order, dependency counters, 64-column chunk releases) is the
 // grouped engine's (brk_sched.cuh), so the host builds the same GroupSched.
+#include <algorithm>
+#include <vector>
 #include <cstdio>
 
 #include "brk_internal.h"
@@ -78,23 +80,53 @@ __device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
 }
 __device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
+// dep_mode 2 wait (brk_sched.cuh wait_chunk) with the MLP kernel's polling options (flags):
+// bit 2 relaxed probes and one acquire fence once the count is reached (slower: 75.9 vs
+// 68.4 us per step), bits 4/5 back-off 16 ns / none instead of 64 ns
+__device__ __forceinline__ void mlp_wait_chunk(const GroupSched* gs, int prob, int mb, int rank, int s, int flags) {
+  const bool relaxed = (flags & 4) != 0;
+  const unsigned sleep_ns = (flags & 32) ? 0u : ((flags & 16) ? 16u : 64u);
+  for (int d = 0; d < kMaxDeps; ++d) {
+    const int q = gs->dep_prob[prob][d];
+    if (q < 0 || gs->dep_mode[prob][d] != 2) continue;
+    const unsigned* c = gs->chunk_counters + ((q * gs->chunk_mb + mb) * 2 + rank) * gs->chunk_n + s;
+    unsigned v;
+    long long spins = 0;
+    do {
+      if (relaxed) asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
+      else asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
+      if (++spins > (1ll << 31)) __trap();  // a dependency that never completes is a bug: fail loudly
+      if (v < static_cast<unsigned>(gs->chunk_target) && sleep_ns) __nanosleep(sleep_ns);
+    } while (v < static_cast<unsigned>(gs->chunk_target));
+  }
+  if (relaxed) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  asm volatile("fence.proxy.async.global;" ::: "memory");  // the TMA reads follow
+}
+
 // smem operand descriptor of MMA sub-step kk (16 K-elements) — bf16, 128B swizzle
 __device__ __forceinline__ uint64_t op_desc(uint32_t base, int mn_major, int kk) {
   return mn_major ? make_smem_desc(base + kk * 16 * 128, 64 * 128, 1024, kSwizzle128B)
                   : make_smem_desc(base + kk * 32, 16, 1024, kSwizzle128B);
 }
 
-__device__ __forceinline__ void locate(const GroupSched* gs, const MlpProb* P, int u, int& prob, int& mb, int& nb) {
+// Work unit u -> (problem, row block, column tile).  kPairs CTA pairs per cluster take
+// adjacent column tiles of one row block (they share the A operand by multicast).
+template <int kPairs>
+__device__ __forceinline__ void locate(const GroupSched* gs, const MlpProb* P, int u, int pair, int& prob, int& mb,
+                                       int& nb) {
   prob = 0;
   while (prob + 1 < gs->n_probs && u >= gs->tile_begin[prob + 1]) ++prob;
   const int rel = u - gs->tile_begin[prob];
-  nb = rel % P[prob].n_tiles;
-  mb = rel / P[prob].n_tiles;
+  const int per_row = P[prob].n_tiles / kPairs;
+  nb = (rel % per_row) * kPairs + pair;
+  mb = rel / per_row;
 }
 
 // Column sums over the 32 rows of a staged bf16 tile: lane l sums columns 2l, 2l + 1
-// (32-bit word l % 4 of 16 B chunk l / 4, which sits at chunk (l / 4) ^ (r % 8) of row r).
-__device__ __forceinline__ void tile_colsum(uint32_t tile, int lane, float* dst) {
+// (32-bit word l % 4 of 16 B chunk l / 4, which sits at chunk (l / 4) ^ (r % 8) of row r),
+// into 64 floats of shared memory at `dst`; lane 0 then writes them to global by a bulk copy
+// (async proxy: its completion orders them before the relaxed counter release).
+__device__ __forceinline__ void tile_colsum(uint32_t tile, int lane, uint32_t dst, float* gdst) {
   const uint32_t j = static_cast<uint32_t>(lane) >> 2, wd = (static_cast<uint32_t>(lane) & 3u) << 2;
   float s0 = 0.0f, s1 = 0.0f;
 #pragma unroll 8
@@ -103,7 +135,13 @@ __device__ __forceinline__ void tile_colsum(uint32_t tile, int lane, float* dst)
     s0 += __uint_as_float(x << 16);
     s1 += __uint_as_float(x & 0xffff0000u);
   }
-  *reinterpret_cast<float2*>(dst + 2 * lane) = make_float2(s0, s1);
+  asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(dst + lane * 8), "f"(s0), "f"(s1) : "memory");
+  fence_proxy_async_smem();
+  __syncwarp();
+  if (lane == 0) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 256;" ::"l"(gdst), "r"(dst) : "memory");
+    bulk_commit();
+  }
 }
 
 #ifdef BRK_DIAG
@@ -122,7 +160,12 @@ __device__ __forceinline__ unsigned long long gtimer() {
   } while (0)
 #endif
 
+// kCS = 2: one CTA pair per cluster.  kCS = 4: two pairs per cluster on adjacent column tiles
+// of the same row block; the pair whose index matches the k-step's parity loads the A box and
+// multicasts it into both pairs (L2 reads per k-step 96 -> 64 KB per cluster... per pair 48 -> 32).
+template <int kCS>
 __global__ void __launch_bounds__(kThreads, 1) mlp_step_kernel(const __grid_constant__ MlpGroup G) {
+  constexpr int kPairs = kCS / 2;
   const MlpProb* P = G.probs;
   const GroupSched* gs = &G.sched;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -140,11 +183,18 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_step_kernel(const __grid_cons
 
   const int warp = warp_id();
   const int lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_ctarank();
+  const uint32_t crank = cluster_ctarank();
+  const uint32_t rank = crank & 1u;  // rank within the CTA pair
+  const int pair = static_cast<int>(crank >> 1);
   const bool leader = rank == 0;
-  const int unit0 = static_cast<int>(blockIdx.x >> 1);
-  const int n_units = static_cast<int>(gridDim.x >> 1);
+  const int unit0 = static_cast<int>(blockIdx.x) / kCS;
+  const int n_units = static_cast<int>(gridDim.x) / kCS;
   const int num_work = gs->tile_begin[gs->n_probs];
+  // this cluster's work units: the host's list schedule (G.list) or round robin
+  const bool listed = kCS == 2 && G.list_len > 0;
+  const int it_begin = listed ? G.list_off[unit0] : unit0;
+  const int it_end = listed ? G.list_off[unit0 + 1] : num_work;
+  const int it_step = listed ? 1 : n_units;
 
   if (warp == kMmaWarp + 1 && lane == 0) {
     for (int q = 0; q < gs->n_probs; ++q) {
@@ -154,7 +204,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_step_kernel(const __grid_cons
     *deps_seq = 0u;
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], kPairs);  // a stage is free once every pair of the cluster consumed it
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -177,9 +227,10 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_step_kernel(const __grid_cons
       pdl_wait();
       int g = 0;
       uint32_t ordinal = 0;
-      for (int u = unit0; u < num_work; u += n_units) {
+      for (int it = it_begin; it < it_end; it += it_step) {
+        const int u = listed ? G.list[it] : it;
         int prob, mb, nb;
-        locate(gs, P, u, prob, mb, nb);
+        locate<kPairs>(gs, P, u, pair, prob, mb, nb);
         const MlpProb& p = P[prob];
         ++ordinal;
         const bool chunked = has_dep_mode(gs, prob, true);
@@ -200,7 +251,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_step_kernel(const __grid_cons
         const int brow = nb * 2 + static_cast<int>(rank);
         const int n_steps = p.k_steps;
         // rotate the batch-list start per tile (concurrent tiles read different blocks)
-        const int rot = (G.flags & 1) ? (mb * 7 + nb * 3) % n_steps : 0;  // no rotation: tiles sharing a row block read the same A box at about the same time (L2 dedup: 69.5 -> 68.6 us)
+        const int rot = (G.flags & 1) ? (mb * 7 + (nb - pair) * 3) % n_steps : 0;  // no rotation: tiles sharing a row block read the same A box at about the same time (L2 dedup: 69.5 -> 68.6 us)
         const int a2 = p.a_rc2 * arow, a3 = p.a_rc3 * arow, b2 = p.b_rc2 * brow, b3 = p.b_rc3 * brow;
         for (int s0 = (pid - g % kProducers + kProducers) % kProducers; s0 < n_steps; s0 += kProducers) {
           const int gg = g + s0;
@@ -208,7 +259,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_step_kernel(const __grid_cons
           const uint32_t phase = (gg / kStages) & 1;
           const int s = s0 + rot < n_steps ? s0 + rot : s0 + rot - n_steps;
           if (chunked) {  // before the ring wait: the poll latency overlaps the slot becoming free
-            wait_chunk(gs, prob, mb, static_cast<int>(rank), s);
+            mlp_wait_chunk(gs, prob, mb, static_cast<int>(rank), s, G.flags);
             if (pid == 0 && !published) {
               publish_deps(deps_seq, ordinal);
               MLP_TT(static_cast<int>(ordinal) - 1, 0);
@@ -224,10 +275,13 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_step_kernel(const __grid_cons
             tma_load_pair<4>(sa + kABytes, &p.map_b, &full[stage], cb);
             wait_published(deps_seq, ordinal, true);
             deps_pending = false;
-            tma_load_pair<4>(sa, &p.map_a, &full[stage], ca);
           } else {
-            tma_load_pair<4>(sa, &p.map_a, &full[stage], ca);
             tma_load_pair<4>(sa + kABytes, &p.map_b, &full[stage], cb);
+          }
+          if constexpr (kPairs == 1) {
+            tma_load_pair<4>(sa, &p.map_a, &full[stage], ca);
+          } else if ((s & 1) == pair) {  // A into this CTA and its counterpart in the other pair
+            tma_load_pair_mc4(sa, &p.map_a, &full[stage], ca, static_cast<uint16_t>((1u << rank) | (4u << rank)));
           }
         }
         if (!published && pid == 0) {
@@ -243,9 +297,10 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_step_kernel(const __grid_cons
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
-      for (int u = unit0; u < num_work; u += n_units, ++local) {
+      for (int it = it_begin; it < it_end; it += it_step, ++local) {
+        const int u = listed ? G.list[it] : it;
         int prob, mb, nb;
-        locate(gs, P, u, prob, mb, nb);
+        locate<kPairs>(gs, P, u, pair, prob, mb, nb);
         const MlpProb& p = P[prob];
         const int a_mn = p.a_mn, b_mn = p.b_mn, n_steps = p.k_steps;
         const uint32_t idesc = make_idesc(kFmtBF16, 256, kBN, a_mn, b_mn);
@@ -263,8 +318,13 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_step_kernel(const __grid_cons
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
               mma_ss_pair<false>(d_tmem, op_desc(sa, a_mn, kk), op_desc(sb, b_mn, kk), idesc, (s | kk) ? 1u : 0u);
-            mma_commit_pair(&empty[stage]);
-            if (s == n_steps - 1) mma_commit_pair(&tfull[acc]);
+            if constexpr (kPairs == 1) {
+              mma_commit_pair(&empty[stage]);
+              if (s == n_steps - 1) mma_commit_pair(&tfull[acc]);
+            } else {  // the stage was filled by both pairs' producers: free it in all four CTAs
+              mma_commit_pair_mask(&empty[stage], 0xF);
+              if (s == n_steps - 1) mma_commit_pair_mask(&tfull[acc], static_cast<uint16_t>(3u << (2 * pair)));
+            }
           }
           __syncwarp();
           if (++stage == kStages) { stage = 0; phase ^= 1; }
@@ -280,14 +340,18 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_step_kernel(const __grid_cons
     const uint32_t lrow = static_cast<uint32_t>(lane) * 128;
     const uint32_t lsw = static_cast<uint32_t>(lane & 7);
     const uint32_t bias_s = smem_u32(bias_area + warp * 64);
-    const uint32_t tempty_leader = mapa_shared(smem_u32(&tempty[0]), 0);
+    const uint32_t tempty_leader = mapa_shared(smem_u32(&tempty[0]), static_cast<uint32_t>(2 * pair));
     uint32_t ephase = 0;
     int local = 0;
-    for (int u = unit0; u < num_work; u += n_units, ++local) {
+    for (int it = it_begin; it < it_end; it += it_step, ++local) {
+      const int u = listed ? G.list[it] : it;
       int prob, mb, nb;
-      locate(gs, P, u, prob, mb, nb);
+      locate<kPairs>(gs, P, u, pair, prob, mb, nb);
       const MlpProb& p = P[prob];
       const int kind = p.kind;
+#ifdef BRK_DIAG
+      if (threadIdx.x == 0 && G.debug_ts != nullptr && local < 16) G.debug_ts[gridDim.x * 128 + blockIdx.x * 16 + local] = u;
+#endif
       const int acc = local & 1;
       const int row0 = mb * 256 + static_cast<int>(rank) * 128 + quarter * 32;  // this warp's first row
       const int colblk = nb * 2 + half;                                          // its 64-column output block
@@ -324,6 +388,26 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_step_kernel(const __grid_cons
       }
       const int32_t ao[4] = {0, row0 & 63, colblk, row0 >> 6};  // activation-layout box
       float* colsum_dst = p.colsum_ws != nullptr ? p.colsum_ws + (row0 >> 5) * p.cols + colblk * 64 : nullptr;
+      // lane 0, right after the chunk's TMA stores are committed: wait for their completion and
+      // release the warp's 32 rows x 64 columns to dependent tiles (before the column sums).
+      // The data left through TMA stores whose bulk-group completion means they are performed
+      // in L2, and this thread wrote nothing else the consumers read (they acquire the counter,
+      // fence the async proxy and read by TMA from L2).  A release reduction would add a
+      // gpu-scope MEMBAR per warp and tile on the critical path (65.1 vs 68.4 us per step;
+      // flags bit 3 restores it); determinism under thousands of back-to-back steps is a GPU
+      // test (test_gpu_mlp.py).
+      auto release_chunk_mlp = [&]() {
+        if (threadIdx.x == 0) MLP_TT(local, 5);
+        bulk_wait0();
+        if (threadIdx.x == 0) MLP_TT(local, 6);
+        if (!(G.flags & 2)) asm volatile("fence.proxy.async.global;" ::: "memory");
+        if (gs->chunk_counters != nullptr) {
+          unsigned* cc = gs->chunk_counters + ((prob * gs->chunk_mb + mb) * 2 + rank) * gs->chunk_n + colblk;
+          if (G.flags & 8) red_release_add(cc, 1u);
+          else asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(cc) : "memory");
+        }
+        if (threadIdx.x == 0) MLP_TT(local, 7);
+      };
       if (kind <= kMlpFwdTop) {
         // y = relu(acc + bias) -> st0; top layer: dz = dy * (y > 0) in place in st1
         const bool top = kind == kMlpFwdTop;
@@ -348,8 +432,9 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_step_kernel(const __grid_cons
           tma_store4(&p.map_out, st0, ao[0], ao[1], ao[2], ao[3]);
           if (top) tma_store4(&p.map_aux, st1, ao[0], ao[1], ao[2], ao[3]);
           bulk_commit();
+          release_chunk_mlp();
         }
-        if (top) tile_colsum(st1, lane, colsum_dst);
+        if (top) tile_colsum(st1, lane, bias_s, colsum_dst);  // (the bias values are consumed)
       } else if (kind <= kMlpBwdPlain) {
         // dz = bf16(acc) * (mask > 0) (mask: the previous layer's ReLU output, >= +0)
         const bool masked = kind == kMlpBwd;
@@ -374,8 +459,9 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_step_kernel(const __grid_cons
         if (lane == 0) {
           tma_store4(&p.map_out, st0, ao[0], ao[1], ao[2], ao[3]);
           bulk_commit();
+          release_chunk_mlp();
         }
-        if (colsum_dst != nullptr) tile_colsum(st0, lane, colsum_dst);
+        if (colsum_dst != nullptr) tile_colsum(st0, lane, bias_s, colsum_dst);
       } else {
         // weight update: dW (fp32, two 32-column boxes through st0); w_next = w - lr dW (st1)
 #pragma unroll
@@ -417,16 +503,9 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_step_kernel(const __grid_cons
           }
         }
       }
-      // outputs complete -> release this warp's 32 rows x 64 columns to dependent tiles
-      if (threadIdx.x == 0) MLP_TT(local, 5);
-      if (lane == 0) {
-        bulk_wait0();
-        if (threadIdx.x == 0) MLP_TT(local, 6);
-        if (!(G.flags & 2)) asm volatile("fence.proxy.async.global;" ::: "memory");
-        if (!upd && gs->chunk_counters != nullptr)
-          red_release_add(gs->chunk_counters + ((prob * gs->chunk_mb + mb) * 2 + rank) * gs->chunk_n + colblk, 1u);
-        if (threadIdx.x == 0) MLP_TT(local, 7);
-      }
+      if (upd && threadIdx.x == 0) MLP_TT(local, 5);
+      if (lane == 0) bulk_wait0();  // (update kind: dW / new weights complete)
+      if (upd && threadIdx.x == 0) MLP_TT(local, 6);
       // bias gradient of the layer from the column-sum partials (row-block-0 tiles of the update)
       if (upd && p.db_partials != nullptr && mb == 0 && rank == 0) {
         const int t = threadIdx.x, c = t & (kBN - 1), grp = t >> 7;  // 2 groups x 128 columns
@@ -453,10 +532,18 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_step_kernel(const __grid_cons
         bar_sync(2, kEpiWarps * 32);  // the bias area is reused by the next tile
       }
       // whole-tile release (row-block / whole-problem counters: weight updates, in-place SGD)
+      // (every warp's outputs, column sums included, left through bulk copies that lane 0
+      //  waited on: relaxed increments, as for the chunk counters; flags bit 3: release)
       bar_sync(1, kEpiWarps * 32);
       if (threadIdx.x == 0) {
-        red_release_add(gs->counters + prob * kCounterStride + mb, 1u);
-        red_release_add(gs->counters + prob * kCounterStride + kCounterStride - 1, 1u);
+        unsigned* c0 = gs->counters + prob * kCounterStride;
+        if (G.flags & 8) {
+          red_release_add(c0 + mb, 1u);
+          red_release_add(c0 + kCounterStride - 1, 1u);
+        } else {
+          asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(c0 + mb) : "memory");
+          asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(c0 + kCounterStride - 1) : "memory");
+        }
         MLP_TT(local, 3);
       }
     }
@@ -488,56 +575,140 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_step_kernel(const __grid_cons
 
 int engine_sm_count();
 
-int launch_mlp_group(const MlpGroup& G, cudaStream_t stream) {
-  const GroupSched& gs = G.sched;
-  if (gs.n_probs < 1 || gs.n_probs > kMaxProbs || gs.counters == nullptr)
-    return set_error(BRK_ERR_CONTRACT, "mlp group: 1..12 problems and a counter buffer");
-  for (int q = 0; q < gs.n_probs; ++q) {
-    const MlpProb& p = G.probs[q];
-    if (gs.tile_begin[q + 1] - gs.tile_begin[q] != p.m_tiles * p.n_tiles || p.k_steps < 1)
-      return set_error(BRK_ERR_CONTRACT, "mlp group: tile_begin does not match the problem's tiles");
-    if (p.m_tiles > kCounterStride - 1) return set_error(BRK_ERR_CONTRACT, "mlp group: > 64 row blocks");
-    for (int d = 0; d < kMaxDeps; ++d)
-      if (gs.dep_prob[q][d] >= q) return set_error(BRK_ERR_CONTRACT, "mlp group: dependencies must point back");
-  }
+namespace {
+template <int kCS>
+int launch_mlp_t(MlpGroup& G, cudaStream_t stream) {
+  auto kern = mlp_step_kernel<kCS>;
   static int attr_set = 0;
   cudaError_t err;
   if (!attr_set) {
-    err = cudaFuncSetAttribute(mlp_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
     if (err != cudaSuccess) return set_cuda_error(err, "mlp smem attribute");
+    if (kCS > 2) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     attr_set = 1;
   }
-  const int units = engine_sm_count() / 2;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(units * 2);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = kSmem;
   cfg.stream = stream;
   cudaLaunchAttribute attrs[2];
   attrs[0].id = cudaLaunchAttributeClusterDimension;
-  attrs[0].val.clusterDim.x = 2;
+  attrs[0].val.clusterDim.x = kCS;
   attrs[0].val.clusterDim.y = 1;
   attrs[0].val.clusterDim.z = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = 1;
-  // tiles spin on counters of earlier problems: every CTA must be resident at once
+  // tiles spin on counters of earlier problems: every CTA must be resident at once, so the
+  // grid is as many clusters as the device holds together (a persistent grid of any size works)
   static int resident = -1;
   if (resident < 0) {
-    err = cudaOccupancyMaxActiveClusters(&resident, mlp_step_kernel, &cfg);
+    cfg.gridDim = dim3((engine_sm_count() / kCS) * kCS);
+    err = cudaOccupancyMaxActiveClusters(&resident, kern, &cfg);
     if (err != cudaSuccess) return set_cuda_error(err, "mlp occupancy");
   }
-  if (resident < units) {
-    char buf[128];
-    std::snprintf(buf, sizeof(buf), "mlp step: %d CTA pairs must be co-resident, the device holds %d", units,
-                  resident);
-    return set_error(BRK_ERR_CONTRACT, buf);
-  }
+  const int clusters = std::min(engine_sm_count() / kCS, resident);
+  if (clusters < 1) return set_error(BRK_ERR_CONTRACT, "mlp step: no cluster fits on the device");
+  cfg.gridDim = dim3(clusters * kCS);
+  if (kCS == 2 && G.list_len > 0) mlp_list_schedule(G, clusters);  // for the pairs launched
   attrs[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attrs[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.numAttrs = 2;
-  err = cudaLaunchKernelEx(&cfg, mlp_step_kernel, G);
+  err = cudaLaunchKernelEx(&cfg, kern, G);
   if (err != cudaSuccess) return set_cuda_error(err, "mlp step launch");
   return BRK_OK;
+}
+}  // namespace
+
+// Greedy list schedule of the step's work units over the CTA pairs, from a simple timing model
+// of one B200 (profiles/r02/mlp_lean_timeline.txt): a unit's mainloop takes k_steps x 0.175 us
+// (operand delivery bound), its epilogue ~1.4 us (bwd / top-layer kinds more), and a consumer's
+// mainloop starts ~1.3 us after the release it waits for.  Units are taken in the global order
+// (dependencies point backwards); each goes to the pair where it can start first, so the long
+// weight-update units do not sit in front of the bwd-data chain on the pairs it needs.
+void mlp_list_schedule(MlpGroup& G, int pairs) {
+  const GroupSched& gs = G.sched;
+  const int W = gs.tile_begin[gs.n_probs];
+  G.list_len = 0;
+  if (W > kMaxListUnits || pairs > kMaxListPairs || pairs < 1) return;
+  // the schedule depends only on the problem structure: reuse the last one when it matches
+  std::vector<int32_t> key = {pairs, gs.n_probs};
+  for (int q = 0; q < gs.n_probs; ++q) {
+    key.insert(key.end(), {gs.tile_begin[q + 1], G.probs[q].k_steps, G.probs[q].kind, G.probs[q].n_tiles});
+    for (int d = 0; d < kMaxDeps; ++d) key.insert(key.end(), {gs.dep_prob[q][d], gs.dep_mode[q][d]});
+  }
+  static std::vector<int32_t> last_key;
+  static std::vector<int16_t> last_list, last_off;
+  if (key == last_key) {
+    std::copy(last_off.begin(), last_off.end(), G.list_off);
+    std::copy(last_list.begin(), last_list.end(), G.list);
+    G.list_len = static_cast<int32_t>(last_list.size());
+    return;
+  }
+  constexpr double kStep = 0.175, kHandoff = 1.3;
+  double epi[5] = {1.4, 2.1, 1.7, 1.2, 2.5};  // by MlpKind
+  std::vector<double> row_done(static_cast<size_t>(gs.n_probs) * 64, 0.0), prob_done(gs.n_probs, 0.0);
+  std::vector<double> free_at(pairs, 0.0);
+  std::vector<std::vector<int16_t>> lists(pairs);
+  for (int q = 0; q < gs.n_probs; ++q) {
+    const MlpProb& p = G.probs[q];
+    for (int u = gs.tile_begin[q]; u < gs.tile_begin[q + 1]; ++u) {
+      const int rel = u - gs.tile_begin[q];
+      const int mb = rel / p.n_tiles;
+      double ready = 0.0;
+      for (int d = 0; d < kMaxDeps; ++d) {
+        const int s = gs.dep_prob[q][d];
+        if (s < 0) continue;
+        const double t = gs.dep_mode[q][d] == 1 ? prob_done[s] : row_done[static_cast<size_t>(s) * 64 + mb];
+        ready = std::max(ready, t + kHandoff);
+      }
+      int best = 0;
+      double best_start = 1e30;
+      for (int c = 0; c < pairs; ++c) {
+        const double st = std::max(free_at[c], ready);
+        if (st < best_start - 1e-9) { best_start = st; best = c; }
+      }
+      const double main_end = best_start + p.k_steps * kStep;
+      free_at[best] = main_end;
+      const double done = main_end + epi[p.kind];
+      double& rd = row_done[static_cast<size_t>(q) * 64 + mb];
+      rd = std::max(rd, done);
+      prob_done[q] = std::max(prob_done[q], done);
+      lists[best].push_back(static_cast<int16_t>(u));
+    }
+  }
+  int n = 0;
+  for (int c = 0; c < pairs; ++c) {
+    G.list_off[c] = static_cast<int16_t>(n);
+    for (int16_t u : lists[c]) G.list[n++] = u;
+  }
+  G.list_off[pairs] = static_cast<int16_t>(n);
+  G.list_len = n;
+  last_key = key;
+  last_off.assign(G.list_off, G.list_off + pairs + 1);
+  last_list.assign(G.list, G.list + n);
+}
+
+int launch_mlp_group(const MlpGroup& Gin, cudaStream_t stream) {
+  const GroupSched& gs = Gin.sched;
+  if (gs.n_probs < 1 || gs.n_probs > kMaxProbs || gs.counters == nullptr)
+    return set_error(BRK_ERR_CONTRACT, "mlp group: 1..12 problems and a counter buffer");
+  bool even = true;
+  for (int q = 0; q < gs.n_probs; ++q) {
+    const MlpProb& p = Gin.probs[q];
+    if (gs.tile_begin[q + 1] - gs.tile_begin[q] != p.m_tiles * p.n_tiles || p.k_steps < 1)
+      return set_error(BRK_ERR_CONTRACT, "mlp group: tile_begin does not match the problem's tiles");
+    if (p.m_tiles > kCounterStride - 1) return set_error(BRK_ERR_CONTRACT, "mlp group: > 64 row blocks");
+    for (int d = 0; d < kMaxDeps; ++d)
+      if (gs.dep_prob[q][d] >= q) return set_error(BRK_ERR_CONTRACT, "mlp group: dependencies must point back");
+    even = even && p.n_tiles % 2 == 0;
+  }
+  static MlpGroup G;
+  G = Gin;
+  if (Gin.cluster != 4 || !even) return launch_mlp_t<2>(G, stream);
+  // two pairs per cluster: work units are pairs of adjacent column tiles
+  for (int q = 0; q < gs.n_probs; ++q)
+    G.sched.tile_begin[q + 1] = G.sched.tile_begin[q] + G.probs[q].m_tiles * G.probs[q].n_tiles / 2;
+  return launch_mlp_t<4>(G, stream);
 }
 
 }  // namespace brk

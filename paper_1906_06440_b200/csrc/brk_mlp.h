@@ -53,16 +53,31 @@ struct MlpProb {
   float lr;
 };
 
+constexpr int kMaxListPairs = 80;
+constexpr int kMaxListUnits = 2048;
+
 struct MlpGroup {
   MlpProb probs[kMaxProbs];
   GroupSched sched;
   // diagnostics build only (BRK_DIAG): per-CTA, per-local-tile %globaltimer stamps
   // [blockIdx.x][16][8], slots as in the grouped engine (brk_engine.cu BRK_TT)
   unsigned long long* debug_ts;
-  // tuning (BRK_MLP_FLAGS): bit0 per-tile k-step rotation, bit1 no writer-side proxy fence
+  // tuning (BRK_MLP_FLAGS): bit0 per-tile k-step rotation, bit1 no writer-side proxy fence,
+  // bit2 relaxed dependency polling + one acquire fence, bit3 release (not relaxed) chunk counters
   int32_t flags;
+  // CTAs per cluster: 2 (one pair) or 4 (two pairs sharing the A operand by TMA multicast)
+  int32_t cluster;
+  // list schedule (cluster == 2): CTA pair c runs units list[list_off[c] .. list_off[c+1]) in
+  // that order (each list increasing: every unit waits only on units of lower index, so the
+  // lists cannot deadlock); list_len == 0: round robin (pair c runs c, c + pairs, ...)
+  int32_t list_len;
+  int16_t list_off[kMaxListPairs + 1];
+  int16_t list[kMaxListUnits];
 };
 
 int launch_mlp_group(const MlpGroup& G, cudaStream_t stream);
+// list-schedule the group's work units over `pairs` CTA pairs (fills list / list_off / list_len;
+// leaves list_len = 0 when the units do not fit the table)
+void mlp_list_schedule(MlpGroup& G, int pairs);
 
 }  // namespace brk

@@ -384,6 +384,19 @@ __device__ __forceinline__ void tma_load_pair(void* smem_dst, const CUtensorMap*
   }
 }
 
+// Pair TMA load (completes on the pair leader's barrier, as tma_load_pair) multicast to the
+// CTAs in `mask`: each destination CTA receives the box at the same smem offset and its
+// pair leader's same-offset barrier counts the bytes.
+__device__ __forceinline__ void tma_load_pair_mc4(void* smem_dst, const CUtensorMap* map, uint64_t* bar,
+                                                  const int32_t (&c)[4], uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2], %7;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c[0]), "r"(c[1]), "r"(c[2]),
+      "r"(c[3]), "h"(mask)
+      : "memory");
+}
+
 // TMA im2col load on a 5-d map (C, W, H, D, N): coordinates c[] are the
 // starting pixel's position (already including the lower padding corner),
 // off = filter-tap offsets (w, h, d).  kPair: completes on the leader's barrier.
@@ -470,6 +483,15 @@ __device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
           smem_u32(bar)),
       "h"(static_cast<uint16_t>(3))
+      : "memory");
+}
+
+// commit (pair MMA): arrive on the same-offset barrier of every CTA in `mask`
+__device__ __forceinline__ void mma_commit_pair_mask(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
       : "memory");
 }
 

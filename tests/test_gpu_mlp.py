@@ -192,3 +192,26 @@ def test_fused_step_back_to_back_stress():
     torch.cuda.synchronize()
     assert all(torch.isfinite(w.float()).all() for w in m.w)
     assert torch.isfinite(m.grads).all()
+
+
+def test_fused_step_deterministic_under_back_to_back_replays():
+    """The dependency protocol (64-column chunk releases after TMA-store completion, the
+    per-CTA published tile ordinal, the counter reset under programmatic dependent launch)
+    must hand every consumer complete data: with lr = 0 every step is the same computation,
+    so 4000 back-to-back replays must reproduce the first step bit for bit (a stale or
+    partial read anywhere in the chain would perturb y, dW, db or dx)."""
+    m = MLP(layers=4, width=1024, batch=2048, lr=0.0, seed=0)
+    g = torch.Generator(device="cpu").manual_seed(5)
+    m.load_input(blk((torch.rand(2048, 1024, generator=g) * 2 - 1).bfloat16()).cuda(),
+                 blk((torch.rand(2048, 1024, generator=g) * 2 - 1).bfloat16()).cuda())
+    m.capture()
+    m.replay()
+    torch.cuda.synchronize()
+    first = [t.clone() for t in m.dw + m.db + m.y[1:] + m.dz]
+    for i in range(40):
+        for _ in range(100):
+            m.replay()
+        torch.cuda.synchronize()
+        now = m.dw + m.db + m.y[1:] + m.dz
+        for a, b in zip(first, now):
+            assert torch.equal(a, b), f"step {100 * (i + 1)}: fused step not reproducible"

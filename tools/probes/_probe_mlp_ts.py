@@ -17,18 +17,22 @@ for _ in range(3):
     mlp.step()
 torch.cuda.synchronize()
 lib = _lib.load()
-ts = torch.zeros(148 * 16 * 8, dtype=torch.int64, device="cuda")
+ts = torch.zeros(148 * 16 * 8 + 148 * 16, dtype=torch.int64, device="cuda")
 lib.brk_diag_set_timestamps(ts.data_ptr())
 mlp2 = MLP(layers=4, width=1024, batch=2048, lr=1e-4)  # rebuild params with the diag pointer
 mlp2.load_input(x, dy)
 mlp2.step()
 torch.cuda.synchronize()
 lib.brk_diag_set_timestamps(None)
-a = ts.cpu().numpy().reshape(148, 16, 8).astype(np.int64)
-a = a[0::2]  # leader CTAs
+tsn = ts.cpu().numpy().astype(np.int64)
+a = tsn[:148 * 128].reshape(148, 16, 8)
+uid = tsn[148 * 128:].reshape(148, 16)  # unit of each local tile (lean kernel, diagnostics build)
+CS = int(os.environ.get("BRK_MLP_CS", "2"))
+a = a[0::CS]  # (first) pair leader CTA of each cluster
+uid = uid[0::CS]
 valid = a[:, :, 3] > 0
 t0 = a[:, :, 0][valid & (a[:, :, 0] > 0)].min()
-n_units = 74
+n_units = 148 // CS
 # global order of tiles per pair: u = unit + i * n_units; problems: tile_begin from sizes
 import os
 lag = int(os.environ.get("BRK_MLP_UPD_LAG", "1"))
@@ -42,12 +46,12 @@ else:
             names.append(f"bwd{l}")
         if 1 <= l + lag <= 4:
             names.append(f"upd{l + lag}")
-sizes = [32 if n.startswith("upd") else 64 for n in names]
+sizes = [(32 if n.startswith("upd") else 64) * 2 // CS for n in names]
 begin = np.cumsum([0] + sizes)
 rows = []
 for unit in range(n_units):
     for i in range(16):
-        u = unit + i * n_units
+        u = unit + i * n_units if os.environ.get("BRK_MLP_LIST") == "0" else int(uid[unit, i])
         if u >= begin[-1] or not valid[unit, i]:
             continue
         p = np.searchsorted(begin, u, side="right") - 1
