@@ -34,11 +34,13 @@
 // (barrier init, TMEM alloc, tensor-map prefetch) overlaps the previous
 // kernel; griddepcontrol.wait precedes every global-memory access.
 #include <cstdio>
+#include <cstdlib>
 
 #include "brk_engine.h"
 #include "brk_internal.h"
 #include "brk_ptx.cuh"
 #include "brk_sched.cuh"
+#include "brk_tma_host.h"
 
 namespace brk {
 namespace {
@@ -885,6 +887,11 @@ __device__ __forceinline__ void engine_body(const EngineParams* P, const GroupSc
         int cq = cfirst / static_cast<int>(p.om.cb);
         int cr = cfirst - cq * static_cast<int>(p.om.cb);
         uint32_t v[32];
+        const bool tma_out = !kFullEpi && !kGroup && kCW % 64 == 0 && p.out_bf16 && p.tma_out;
+        if (tma_out && local > 0) {  // the previous tile's last store has read the staging tile
+          if (lane == 0) bulk_wait_read0();
+          __syncwarp();
+        }
         tmem_ld32(tbase + colw(0), v);
         // the full (grouped / fused-feature) epilogue keeps one copy of the chunk body
 #pragma unroll(kFullEpi ? 1 : kCW / 32)
@@ -921,10 +928,26 @@ __device__ __forceinline__ void engine_body(const EngineParams* P, const GroupSc
             } else {
               const bool second = p.out_bf16 && (c & 1);
               if (!second) { seg_coff = coff; seg_col = col0; }
+              if (tma_out && !second && seg > 0) {  // the previous segment's store has read the tile
+                if (lane == 0) bulk_wait_read0();
+                __syncwarp();
+              }
               epilogue_stage(ev, f, pick(bias_r, c), stage + lane * 128, lane, second ? 4 : 0);
               if (!p.out_bf16 || second) {
                 if (threadIdx.x == 0 && c < 2) BRK_TS(9 + 2 * c);
                 if (col0 >= ev.cols) __syncwarp();
+                else if (tma_out && warp_row0 % p.out_rb + 32 <= p.out_rb) {
+                  // the staging tile is the 128B-swizzled TMA box: one store of 32 rows x 64 columns
+                  // (a warp whose rows cross an outer block takes the generic flush below)
+                  fence_proxy_async_smem();
+                  __syncwarp();
+                  if (lane == 0) {
+                    const int img = warp_row0 / p.out_rb, pix = warp_row0 - img * p.out_rb;
+                    tma_store3(&p.map_out, smem + kStages * Cfg::kStageBytes + warp * 4096, 0, pix,
+                               img * (p.cols >> 6) + (seg_col >> 6));
+                    bulk_commit();
+                  }
+                }
                 else if (kFullEpi && !plain_here)
                   epilogue_flush<8, true>(ev, stage, roff, ok_bits, seg_coff, lane, warp_row0, seg_col,
                                           seg == 0 ? pre[0] : (seg == 1 ? pre[1] : nullptr));
@@ -1065,6 +1088,7 @@ __device__ __forceinline__ void engine_body(const EngineParams* P, const GroupSc
       }
       if (threadIdx.x == 0) BRK_TS(6);
     }
+    if (!kFullEpi && !kGroup && lane == 0) bulk_wait0();  // TMA stores done before the CTA exits
   }
   tc_fence_before();
   if constexpr (kPair) cluster_sync_all(); else __syncthreads();
@@ -1179,12 +1203,37 @@ int launch_engine(const EngineParams& p, int bn, int tf32, int pair, int max_uni
                     p.alpha != 1.0f || (p.act != kActNone && p.act != kActRelu) ||
                     p.db_partials != nullptr || (splits > 1 && p.split_ws != nullptr) || (p.debug_flags & 8) ||
                     (p.debug_flags & 64);  // bit6: force the full epilogue (diagnostic)
+  // compact epilogue into a blocked [outer][cols / 64][rb][64] bf16 output (conv activations,
+  // FC activations): TMA stores from the staging tiles (BRK_ENGINE_TMA_OUT=0: generic stores)
+  static EngineParams q;
+  const EngineParams* pp = &p;
+  {
+    const OutMap& om = p.om;
+    static const char* env = std::getenv("BRK_ENGINE_TMA_OUT");
+    const bool layout = om.cl == 1 && om.cb == 64 && om.rl == 64 && om.ch == om.rb * 64 && om.rb >= 32 &&
+                        p.cols % 64 == 0 &&
+                        ((om.rb2 >= 0x7fffffff && om.rh == (p.cols / 64) * om.ch) ||
+                         (om.rb2 == om.rb && om.rh == 0 && om.rh2 == (p.cols / 64) * om.ch));
+    if (!full && !tf32 && p.out_bf16 && p.zf_w == 0 && bn >= 128 && splits == 1 && layout &&
+        !(env != nullptr && std::atoi(env) == 0)) {
+      q = p;
+      const int64_t outer = (static_cast<int64_t>(p.rows) + om.rb - 1) / om.rb;
+      const uint64_t dims[3] = {64, static_cast<uint64_t>(om.rb), static_cast<uint64_t>(outer * (p.cols / 64))};
+      const uint64_t strides[3] = {1, 64, static_cast<uint64_t>(om.rb) * 64};
+      const uint32_t box[3] = {64, 32, 1};
+      if (encode_tmap(&q.map_out, p.out, true, 3, dims, strides, box) == BRK_OK) {
+        q.tma_out = 1;
+        q.out_rb = static_cast<int32_t>(om.rb);
+        pp = &q;
+      }
+    }
+  }
 #define BRK_ENGINE_CASE(BN_, PAIR_)                                                                  \
   if (bn == BN_ && pair == PAIR_) {                                                                  \
-    if (full) return tf32 ? launch_engine_t<BN_, true, PAIR_, true>(p, grid, stream, pdl)            \
-                          : launch_engine_t<BN_, false, PAIR_, true>(p, grid, stream, pdl);          \
-    return tf32 ? launch_engine_t<BN_, true, PAIR_, false>(p, grid, stream, pdl)                     \
-                : launch_engine_t<BN_, false, PAIR_, false>(p, grid, stream, pdl);                   \
+    if (full) return tf32 ? launch_engine_t<BN_, true, PAIR_, true>(*pp, grid, stream, pdl)          \
+                          : launch_engine_t<BN_, false, PAIR_, true>(*pp, grid, stream, pdl);        \
+    return tf32 ? launch_engine_t<BN_, true, PAIR_, false>(*pp, grid, stream, pdl)                   \
+                : launch_engine_t<BN_, false, PAIR_, false>(*pp, grid, stream, pdl);                 \
   }
   BRK_ENGINE_CASE(256, true)
   BRK_ENGINE_CASE(128, true)

@@ -66,6 +66,13 @@ enum EpiAct : int { kActNone = 0, kActRelu = 1, kActSigmoid = 2 };
 struct EngineParams {
   CUtensorMap map_a;  // 64-byte aligned inside the param block
   CUtensorMap map_b;
+  // compact-epilogue TMA stores (set by launch_engine when the output is a blocked
+  // [outer][cols / 64][out_rb][64] bf16 layout): 3-d map (64, out_rb, outer * cols / 64),
+  // box (64, 32, 1); a warp's 32 x 64 staging tile leaves in one store (the generic flush
+  // where its rows cross an outer block)
+  CUtensorMap map_out;
+  int32_t tma_out;
+  int32_t out_rb;
   OperandCoords ca;
   OperandCoords cb;
   int32_t m_tiles, n_tiles, k_steps;

@@ -19,6 +19,7 @@
 //            (R_g^T slice resident), the four partials are summed through
 //            distributed shared memory and each CTA of the cluster finishes
 //            the BPTT element math for a quarter of the minibatch rows.
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -31,9 +32,13 @@
 namespace brk {
 namespace {
 
-constexpr int kStagesS = 4;          // A ring (4 producers, one stage each)
-constexpr int kStageBytesS = 32768;  // 2 M-tiles x 128 rows x 128 B
-constexpr int kThreadsS = 9 * 32;    // 4 epilogue, 1 MMA, 4 producer warps
+// A ring of 4 stages of the streamed operand's N valid rows (rounded to 8-row swizzle atoms, not
+// two full 128-row M tiles).  The second M tile's MMA reads rows 128..255 of a stage, past its
+// end into the next stage / the resident slice: those rows are outside N and their accumulator
+// rows are never read.  (6 stages with 6 producer warps measured slower: forward step 9.6 ->
+// 11.7 us, backward 14.8 -> 15.8 us — the chunk stream is not bound by the bytes in flight.)
+constexpr int kStagesS = 4;
+constexpr int kThreadsS = 9 * 32;    // 4 epilogue, 1 MMA, 4 producer warps (one per stage)
 constexpr int kJf = 8;               // forward: hidden units per CTA
 constexpr int kJb = 32;              // backward: hidden units per cluster
 
@@ -57,6 +62,8 @@ struct SeqParams {
   unsigned* flags;       // per 64-column chunk release counters (zeroed by the host)
   unsigned long long* ts;  // diagnostics: per-step %globaltimer stamps of CTA 0 [T][8] (or null)
   int slice;               // forward: rows of h each cluster CTA loads and multicasts (multiple of 8)
+  int stage_bytes;         // ring stage stride (streamed rows x 128 B, 1 KB aligned)
+  int stages;              // ring stages (<= kStagesS: as many as shared memory holds)
 };
 
 __device__ __forceinline__ unsigned long long gtime() {
@@ -157,9 +164,10 @@ __global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_fwd_kernel(const __grid
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int KC = p.K / 64;
   uint8_t* ring = smem;
-  uint8_t* wsm = smem + kStagesS * kStageBytesS;
+  const int NS = p.stages;
+  uint8_t* wsm = smem + NS * p.stage_bytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(wsm + KC * kGN * 128);
-  uint64_t* empty = full + kStagesS;
+  uint64_t* empty = full + kStagesS;  // (barrier arrays sized for the maximum)
   uint64_t* tfull = empty + kStagesS;
   uint64_t* tempty = tfull + 1;
   uint64_t* wbar = tempty + 1;
@@ -178,7 +186,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_fwd_kernel(const __grid
   const int slice = p.slice;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStagesS; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], cs); }
+    for (int s = 0; s < NS; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], cs); }
     mbar_init(tfull, 1);
     mbar_init(tempty, 4);
     mbar_init(wbar, 1);
@@ -203,9 +211,9 @@ __global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_fwd_kernel(const __grid
           }
       }
       const int total = p.T * KC;
-      for (int gi = pid; gi < total; gi += kStagesS) {
+      for (int gi = pid; pid < NS && gi < total; gi += NS) {
         const int t = gi / KC, kc = gi - t * KC;
-        const uint32_t ph = (gi / kStagesS) & 1;
+        const uint32_t ph = (gi / NS) & 1;
         if (t > 0) {
           while (ld_acquire(&p.flags[kc * kFlagStride]) < static_cast<unsigned>(chunk_owners * t)) poll_backoff();
           fence_proxy_async_global();
@@ -214,7 +222,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_fwd_kernel(const __grid
         if (kc == KC - 1) SEQ_TS(t, 1);  // last chunk released
         mbar_wait(&empty[pid], ph ^ 1);  // every CTA of the cluster consumed this stage
         mbar_arrive_expect_tx(&full[pid], static_cast<uint32_t>(slice * cs * 128));
-        tma_load3_mc(ring + pid * kStageBytesS + crank * slice * 128, &p.map_a, &full[pid], kc * 64, crank * slice,
+        tma_load3_mc(ring + pid * p.stage_bytes + crank * slice * 128, &p.map_a, &full[pid], kc * 64, crank * slice,
                      t, cmask);
       }
     }
@@ -226,13 +234,13 @@ __global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_fwd_kernel(const __grid
       mbar_wait(tempty, (t & 1) ^ 1);
       tc_fence_after();
       for (int kc = 0; kc < KC; ++kc) {
-        const int gi = t * KC + kc, st = gi % kStagesS;
-        mbar_wait(&full[st], (gi / kStagesS) & 1);
+        const int gi = t * KC + kc, st = gi % NS;
+        mbar_wait(&full[st], (gi / NS) & 1);
         tc_fence_after();
         if (lane == 0 && kc == 0) SEQ_TS(t, 2);       // first chunk landed
         if (lane == 0 && kc == KC - 1) SEQ_TS(t, 3);  // last chunk landed
         if (elect_one()) {
-          const uint32_t a0 = smem_u32(ring + st * kStageBytesS);
+          const uint32_t a0 = smem_u32(ring + st * p.stage_bytes);
           const uint32_t b0 = smem_u32(wsm + kc * kGN * 128);
           for (int mt = 0; mt < n_mt; ++mt)
 #pragma unroll
@@ -352,10 +360,11 @@ __global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_bwd_kernel(const __grid
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int KC = p.K / 64;
   uint8_t* ring = smem;
-  uint8_t* wsm = smem + kStagesS * kStageBytesS;           // R_g^T slice: 32 rows x K
+  const int NS = p.stages;
+  uint8_t* wsm = smem + NS * p.stage_bytes;                // R_g^T slice: 32 rows x K
   float* part = reinterpret_cast<float*>(wsm + KC * kJb * 128);  // [256][32] partial dh_rec
   uint64_t* full = reinterpret_cast<uint64_t*>(part + 256 * kJb);
-  uint64_t* empty = full + kStagesS;
+  uint64_t* empty = full + kStagesS;  // (barrier arrays sized for the maximum)
   uint64_t* tfull = empty + kStagesS;
   uint64_t* tempty = tfull + 1;
   uint64_t* wbar = tempty + 1;
@@ -369,7 +378,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_bwd_kernel(const __grid
   const int chunk_owners = 2 * 4;  // 64-column chunk of dpre = 2 clusters x 4 CTAs (row quarters)
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStagesS; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < NS; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     mbar_init(tfull, 1);
     mbar_init(tempty, 4);
     mbar_init(wbar, 1);
@@ -396,7 +405,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_bwd_kernel(const __grid
       // steps t = T-2 .. 0 read dpre(t+1) gate g; step T-1 has no recurrent term
       const int steps = p.T - 1;
       const int total = steps * KC;
-      for (int gi = pid; gi < total; gi += kStagesS) {
+      for (int gi = pid; pid < NS && gi < total; gi += NS) {
         const int it = gi / KC, kc = gi - it * KC;
         const int tsrc = p.T - 1 - it;  // dpre slot read by this iteration
         const int fidx = g * KC + kc;
@@ -404,12 +413,10 @@ __global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_bwd_kernel(const __grid
         fence_proxy_async_global();
         if (kc == 0) SEQ_TS(it, 0);
         if (kc == KC - 1) SEQ_TS(it, 1);
-        const uint32_t ph = (gi / kStagesS) & 1;
+        const uint32_t ph = (gi / NS) & 1;
         mbar_wait(&empty[pid], ph ^ 1);
-        mbar_arrive_expect_tx(&full[pid], n_mt * 16384);
-        for (int mt = 0; mt < n_mt; ++mt)
-          tma_load3(ring + pid * kStageBytesS + mt * 16384, &p.map_a, &full[pid], g * p.K + kc * 64, mt * 128,
-                    tsrc);
+        mbar_arrive_expect_tx(&full[pid], static_cast<uint32_t>(p.stage_bytes));
+        tma_load3(ring + pid * p.stage_bytes, &p.map_a, &full[pid], g * p.K + kc * 64, 0, tsrc);
       }
     }
   } else if (warp == 4) {
@@ -419,13 +426,13 @@ __global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_bwd_kernel(const __grid
       mbar_wait(tempty, (it & 1) ^ 1);
       tc_fence_after();
       for (int kc = 0; kc < KC; ++kc) {
-        const int gi = it * KC + kc, st = gi % kStagesS;
-        mbar_wait(&full[st], (gi / kStagesS) & 1);
+        const int gi = it * KC + kc, st = gi % NS;
+        mbar_wait(&full[st], (gi / NS) & 1);
         tc_fence_after();
         if (lane == 0 && kc == 0) SEQ_TS(it, 2);
         if (lane == 0 && kc == KC - 1) SEQ_TS(it, 3);
         if (elect_one()) {
-          const uint32_t a0 = smem_u32(ring + st * kStageBytesS);
+          const uint32_t a0 = smem_u32(ring + st * p.stage_bytes);
           const uint32_t b0 = smem_u32(wsm + kc * kJb * 128);
           for (int mt = 0; mt < n_mt; ++mt)
 #pragma unroll
@@ -599,16 +606,26 @@ __global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_bwd_kernel(const __grid
 
 unsigned long long* g_seq_ts = nullptr;
 
-int smem_fwd(int K) { return kStagesS * kStageBytesS + (K / 64) * 4 * kJf * 128 + 256 + 1024; }
-int smem_bwd(int K) { return kStagesS * kStageBytesS + (K / 64) * kJb * 128 + 256 * kJb * 4 + 256 + 1024; }
+// streamed rows per stage: N rounded up to whole 8-row swizzle atoms (forward: cs slices of
+// `slice` rows, slice = ceil(N / cs) rounded to 8)
+int rows_pad(int N) { return (N + 7) / 8 * 8; }
+// everything but the ring, and the ring depth that fits beside it (>= 3, else 0)
+int fixed_fwd(int K) { return (K / 64) * 4 * kJf * 128 + 256 + 1024; }
+int fixed_bwd(int K) { return (K / 64) * kJb * 128 + 256 * kJb * 4 + 256 + 1024; }
+int ring_stages(int fixed, int stage_bytes) {
+  const int n = std::min(kStagesS, (232448 - fixed) / stage_bytes);
+  return n >= 3 ? n : 0;
+}
 
 int check_seq(int T, int N, int K) {
   char buf[200];
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (T <= 0 || N <= 0 || N > 256 || K <= 0 || K % 64 || K / kJf > sms || smem_fwd(K) > 232448 ||
-      smem_bwd(K) > 232448) {
+  // (worst case of the forward stage: 8 slices of ceil(N / 8) rows rounded to 8)
+  if (T <= 0 || N <= 0 || N > 256 || K <= 0 || K % 64 || K / kJf > sms ||
+      ring_stages(fixed_fwd(K), 8 * rows_pad((N + 7) / 8) * 128) == 0 ||
+      ring_stages(fixed_bwd(K), rows_pad(N) * 128) == 0) {
     std::snprintf(buf, sizeof(buf),
                   "lstm sequence kernels need 1 <= N <= 256, K %% 64 == 0, K/8 <= %d SMs, K <= 1024 "
                   "(T=%d N=%d K=%d)", sms, T, N, K);
@@ -643,7 +660,7 @@ BRK_API int brk_lstm_seq_fwd(const float* gx, const void* r_cat, const float* s0
   p.flags = flags;
   p.ts = g_seq_ts;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int smem = smem_fwd(K);
+  const int smem = 232448;  // the ring depth is chosen per cluster size below
   cudaError_t err = cudaFuncSetAttribute(lstm_seq_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (err != cudaSuccess) return set_cuda_error(err, "lstm seq fwd smem");
   cudaFuncSetAttribute(lstm_seq_fwd_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -676,6 +693,9 @@ BRK_API int brk_lstm_seq_fwd(const float* gx, const void* r_cat, const float* s0
     const uint64_t strides[3] = {1, (uint64_t)K, (uint64_t)N * K};
     const char* full_env = std::getenv("BRK_LSTM_FULL_TILE");  // diagnostics: stream all 256 rows
     p.slice = (full_env != nullptr && std::atoi(full_env) != 0) ? 256 / cs : ((N + cs - 1) / cs + 7) / 8 * 8;
+    p.stage_bytes = p.slice * cs * 128;
+    p.stages = ring_stages(fixed_fwd(K), p.stage_bytes);
+    if (p.stages == 0) return set_error(BRK_ERR_CONTRACT, "lstm seq fwd: ring does not fit");
     const uint32_t box[3] = {64, static_cast<uint32_t>(p.slice), 1};
     if ((rc = encode_tmap(&p.map_a, h_bf, true, 3, dims, strides, box))) return rc;
   }
@@ -709,7 +729,9 @@ BRK_API int brk_lstm_seq_bwd(const float* dh, const float* gates, const float* s
   {
     const uint64_t dims[3] = {(uint64_t)(4 * K), (uint64_t)N, (uint64_t)T};
     const uint64_t strides[3] = {1, (uint64_t)(4 * K), (uint64_t)N * 4 * K};
-    const uint32_t box[3] = {64, 128, 1};
+    p.stage_bytes = rows_pad(N) * 128;
+    p.stages = ring_stages(fixed_bwd(K), p.stage_bytes);
+    const uint32_t box[3] = {64, static_cast<uint32_t>(rows_pad(N)), 1};
     if ((rc = encode_tmap(&p.map_a, dpre, true, 3, dims, strides, box))) return rc;
   }
   {
@@ -721,7 +743,7 @@ BRK_API int brk_lstm_seq_bwd(const float* dh, const float* gates, const float* s
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaError_t err = cudaMemsetAsync(flags, 0, brk_lstm_seq_flags_bytes(K), st);
   if (err != cudaSuccess) return set_cuda_error(err, "lstm seq flags");
-  const int smem = smem_bwd(K);
+  const int smem = p.stages * p.stage_bytes + fixed_bwd(K);
   err = cudaFuncSetAttribute(lstm_seq_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (err != cudaSuccess) return set_cuda_error(err, "lstm seq bwd smem");
   cudaLaunchConfig_t cfg = {};
