@@ -162,6 +162,7 @@ void init_params(EngineParams& p) {
   p.om.rb2 = int64_t(0x7fffffff);
   const char* dbg = std::getenv("BRK_DEBUG_FLAGS");
   p.debug_flags = dbg ? std::atoi(dbg) : 0;
+  p.debug_ts = g_debug_ts;
 }
 
 void pixel_walk(OperandCoords& oc, int kind, int P, int Q, int stride, int pad_h, int pad_w, int64_t total) {

@@ -180,6 +180,27 @@ __device__ __forceinline__ unsigned long long gtimer() {
   } while (0)
 #endif
 
+// diagnostics (BRK_DIAG, single-problem launches): per-CTA sums of clock64 spent waiting,
+// written after the stamps at debug_ts[gridDim.x * 16 + blockIdx.x * 8 + slot]:
+// 0 MMA waits for a free accumulator, 1 MMA waits for operands, 2 epilogue waits for the
+// accumulator, 3 epilogue busy (accumulator -> tile done), 4 producer 0 waits for a free stage
+#ifdef BRK_DIAG
+#define BRK_CLK(var) const long long var = clock64()
+#define BRK_ACC(slot, t0)                                                                          \
+  do {                                                                                             \
+    if (gs == nullptr && P[0].debug_ts != nullptr)                                                 \
+      atomicAdd(&P[0].debug_ts[gridDim.x * 16 + blockIdx.x * 8 + (slot)],                          \
+                static_cast<unsigned long long>(clock64() - (t0)));                                \
+  } while (0)
+#else
+#define BRK_CLK(var) \
+  do {               \
+  } while (0)
+#define BRK_ACC(slot, t0) \
+  do {                    \
+  } while (0)
+#endif
+
 __device__ __forceinline__ void named_bar_sync(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
@@ -713,7 +734,9 @@ __device__ __forceinline__ void engine_body(const EngineParams* P, const GroupSc
               published = true;
             }
           }
+          BRK_CLK(tp0);
           mbar_wait(&empty[stage], phase ^ 1);
+          if (pid == 0) BRK_ACC(4, tp0);
           uint8_t* sa = smem + stage * Cfg::kStageBytes;
           uint8_t* sb = sa + kTileABytes;
           if (p.debug_flags & 2) {
@@ -755,11 +778,15 @@ __device__ __forceinline__ void engine_body(const EngineParams* P, const GroupSc
         const int s_begin = sp * ks_per;
         const int n_steps = min(p.k_steps, s_begin + ks_per) - s_begin;
         const int acc = local & 1;
+        BRK_CLK(tw0);
         mbar_wait(&tempty[acc], ((local >> 1) & 1) ^ 1);
+        if (lane == 0) BRK_ACC(0, tw0);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int s = 0; s < n_steps; ++s) {
+          BRK_CLK(tf0);
           mbar_wait(&full[stage], phase);
+          if (lane == 0) BRK_ACC(1, tf0);
           tc_fence_after();
           if (local == 0 && s == 0 && lane == 0) BRK_TS(3);
           if (s == 0 && lane == 0) BRK_TT(local, 1);
@@ -865,7 +892,10 @@ __device__ __forceinline__ void engine_body(const EngineParams* P, const GroupSc
           }
         }
       }
+      BRK_CLK(te0);
       mbar_wait(&tfull[acc], (local >> 1) & 1);
+      if (threadIdx.x == 0) BRK_ACC(2, te0);
+      BRK_CLK(te1);
       tc_fence_after();
       if (threadIdx.x == 0) BRK_TS(5);
       if (threadIdx.x == 0) BRK_TT(local, 4);
@@ -877,7 +907,59 @@ __device__ __forceinline__ void engine_body(const EngineParams* P, const GroupSc
         // plain epilogue: staging tile, and the row offsets each lane stores in epilogue_flush
         // diagnostics (debug_flags & 128): run the chunk loop twice (i-cache cold vs warm timing)
         const int reps = (p.debug_flags & 128) ? 2 : 1;
-        for (int rep = 0; rep < reps; ++rep) {
+        // compact epilogue, bf16 output, whole 64-column segments per warp: one x64 TMEM load per
+        // segment (one exposed load latency per 64 columns, not per 32), and the accumulator is
+        // released to the MMA as soon as its last segment is in registers
+        const bool fast = !kFullEpi && !kGroup && kCW % 64 == 0 && p.out_bf16 && reps == 1;
+        if constexpr (!kFullEpi && !kGroup && kCW % 64 == 0) {
+          if (fast) {
+            const bool tma_out = p.tma_out != 0;
+#pragma unroll
+            for (int sg = 0; sg < kCW / 64; ++sg) {
+              uint32_t v[64];
+              tmem_ld64(tbase + cbeg + sg * 64, v);
+              tmem_ld_wait();
+              if (sg == kCW / 64 - 1) {  // the whole accumulator slice is in registers: free it
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                  if constexpr (kPair) mbar_arrive_cluster_relaxed(tempty_leader + acc * 8);
+                  else mbar_arrive_relaxed(&tempty[acc]);
+                }
+              }
+              if (tma_out) {  // an earlier store may still be reading the staging tile
+                if (lane == 0) bulk_wait_read0();
+                __syncwarp();
+              }
+              const int col_seg = nb * BN + cbeg + sg * 64;
+#pragma unroll
+              for (int hh = 0; hh < 2; ++hh) {
+                float f[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[32 * hh + j]);
+                epilogue_stage(ev, f, pick(bias_r, 2 * sg + hh), stage + lane * 128, lane, hh ? 4 : 0);
+              }
+              if (col_seg >= ev.cols || p.out == nullptr) {
+                __syncwarp();
+              } else if (tma_out && warp_row0 % p.out_rb + 32 <= p.out_rb) {
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                  const int img = warp_row0 / p.out_rb, pix = warp_row0 - img * p.out_rb;
+                  tma_store3(&p.map_out, smem + kStages * Cfg::kStageBytes + warp * 4096, 0, pix,
+                             img * (p.cols >> 6) + (col_seg >> 6));
+                  bulk_commit();
+                }
+              } else {  // generic coalesced flush (rows crossing an outer block, non-TMA layouts)
+                const int sq = col_seg / static_cast<int>(p.om.cb), sr = col_seg - sq * static_cast<int>(p.om.cb);
+                epilogue_flush<8, false>(ev, stage, roff, ok_bits,
+                                         static_cast<int64_t>(sq) * p.om.ch + static_cast<int64_t>(sr) * p.om.cl,
+                                         lane);
+              }
+            }
+          }
+        }
+        for (int rep = 0; rep < (fast ? 0 : reps); ++rep) {
         int64_t seg_coff = 0;
         int seg_col = 0;
         int seg = 0;  // staged flush index (the first two use prefetched operands)
@@ -960,12 +1042,14 @@ __device__ __forceinline__ void engine_body(const EngineParams* P, const GroupSc
         tmem_ld_wait();
         if (threadIdx.x == 0) BRK_TS(14 + rep);
         }
-        tc_fence_before();
-        __syncwarp();
-        if (threadIdx.x == 0) BRK_TS(12);
-        if (lane == 0) {
-          if constexpr (kPair) mbar_arrive_cluster_relaxed(tempty_leader + acc * 8);
-          else mbar_arrive_relaxed(&tempty[acc]);
+        if (!fast) {
+          tc_fence_before();
+          __syncwarp();
+          if (threadIdx.x == 0) BRK_TS(12);
+          if (lane == 0) {
+            if constexpr (kPair) mbar_arrive_cluster_relaxed(tempty_leader + acc * 8);
+            else mbar_arrive_relaxed(&tempty[acc]);
+          }
         }
         if (threadIdx.x == 0) BRK_TS(13);
         if constexpr (kGroup && kCW % 64 == 0) {
@@ -1087,6 +1171,7 @@ __device__ __forceinline__ void engine_body(const EngineParams* P, const GroupSc
         }
       }
       if (threadIdx.x == 0) BRK_TS(6);
+      if (threadIdx.x == 0) BRK_ACC(3, te1);
     }
     if (!kFullEpi && !kGroup && lane == 0) bulk_wait0();  // TMA stores done before the CTA exits
   }

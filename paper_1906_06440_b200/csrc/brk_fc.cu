@@ -28,6 +28,7 @@ namespace brk {
 int launch_engine(const EngineParams& p, int bn, int tf32, int pair, int max_units, cudaStream_t stream);
 int engine_sm_count();
 size_t engine_split_ws_bytes(int tiles, int splits, int bn, int pair);
+unsigned long long* g_debug_ts = nullptr;  // set by brk_diag_set_timestamps (diagnostics build stamps)
 
 namespace {
 
@@ -196,7 +197,6 @@ int debug_flags() {
   return dbg ? std::atoi(dbg) : 0;
 }
 
-unsigned long long* g_debug_ts = nullptr;  // set by brk_diag_set_timestamps
 
 int finish(const EngineParams& p, const Plan& pl, void* stream, int tf32 = 0) {
   if (g_capture != nullptr) {

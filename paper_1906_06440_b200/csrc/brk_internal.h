@@ -9,6 +9,10 @@
 
 namespace brk {
 
+// diagnostics: engine launches record %globaltimer stamps / wait sums here when set
+// (brk_diag_set_timestamps; only the BRK_DIAG build writes them)
+extern unsigned long long* g_debug_ts;
+
 enum EntryMode : int { kModeAddr = 0, kModeOffs = 1, kModeStride = 2 };
 
 // Parameters of one generic BRGEMM launch (see brk_brgemm_generic.cu).

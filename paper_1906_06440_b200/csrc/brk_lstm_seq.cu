@@ -32,11 +32,10 @@
 namespace brk {
 namespace {
 
-// A ring of 4 stages of the streamed operand's N valid rows (rounded to 8-row swizzle atoms, not
-// two full 128-row M tiles).  The second M tile's MMA reads rows 128..255 of a stage, past its
-// end into the next stage / the resident slice: those rows are outside N and their accumulator
-// rows are never read.  (6 stages with 6 producer warps measured slower: forward step 9.6 ->
-// 11.7 us, backward 14.8 -> 15.8 us — the chunk stream is not bound by the bytes in flight.)
+// A ring of 4 stages of 32 KB (two 128-row M tiles); each receives only the operand's N valid
+// rows (rounded to 8-row swizzle atoms).  Measured and rejected: 6 stages with 6 producer warps
+// (forward step 9.6 -> 11.7 us, backward 14.8 -> 15.8 us) and stages packed to the valid rows
+// (forward 11.3 us): the chunk stream is not bound by the bytes in flight.
 constexpr int kStagesS = 4;
 constexpr int kThreadsS = 9 * 32;    // 4 epilogue, 1 MMA, 4 producer warps (one per stage)
 constexpr int kJf = 8;               // forward: hidden units per CTA
@@ -62,7 +61,8 @@ struct SeqParams {
   unsigned* flags;       // per 64-column chunk release counters (zeroed by the host)
   unsigned long long* ts;  // diagnostics: per-step %globaltimer stamps of CTA 0 [T][8] (or null)
   int slice;               // forward: rows of h each cluster CTA loads and multicasts (multiple of 8)
-  int stage_bytes;         // ring stage stride (streamed rows x 128 B, 1 KB aligned)
+  int stage_bytes;         // ring stage stride: 32 KB (two 128-row M tiles)
+  int stage_tx;            // bytes one stage receives (the N valid rows, whole 8-row atoms)
   int stages;              // ring stages (<= kStagesS: as many as shared memory holds)
 };
 
@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_fwd_kernel(const __grid
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int KC = p.K / 64;
   uint8_t* ring = smem;
-  const int NS = p.stages;
+  constexpr int NS = kStagesS;  // (p.stages == kStagesS: checked at launch)
   uint8_t* wsm = smem + NS * p.stage_bytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(wsm + KC * kGN * 128);
   uint64_t* empty = full + kStagesS;  // (barrier arrays sized for the maximum)
@@ -360,7 +360,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_bwd_kernel(const __grid
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int KC = p.K / 64;
   uint8_t* ring = smem;
-  const int NS = p.stages;
+  constexpr int NS = kStagesS;  // (p.stages == kStagesS: checked at launch)
   uint8_t* wsm = smem + NS * p.stage_bytes;                // R_g^T slice: 32 rows x K
   float* part = reinterpret_cast<float*>(wsm + KC * kJb * 128);  // [256][32] partial dh_rec
   uint64_t* full = reinterpret_cast<uint64_t*>(part + 256 * kJb);
@@ -415,7 +415,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_bwd_kernel(const __grid
         if (kc == KC - 1) SEQ_TS(it, 1);
         const uint32_t ph = (gi / NS) & 1;
         mbar_wait(&empty[pid], ph ^ 1);
-        mbar_arrive_expect_tx(&full[pid], static_cast<uint32_t>(p.stage_bytes));
+        mbar_arrive_expect_tx(&full[pid], static_cast<uint32_t>(p.stage_tx));
         tma_load3(ring + pid * p.stage_bytes, &p.map_a, &full[pid], g * p.K + kc * 64, 0, tsrc);
       }
     }
@@ -624,8 +624,8 @@ int check_seq(int T, int N, int K) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   // (worst case of the forward stage: 8 slices of ceil(N / 8) rows rounded to 8)
   if (T <= 0 || N <= 0 || N > 256 || K <= 0 || K % 64 || K / kJf > sms ||
-      ring_stages(fixed_fwd(K), 8 * rows_pad((N + 7) / 8) * 128) == 0 ||
-      ring_stages(fixed_bwd(K), rows_pad(N) * 128) == 0) {
+      ring_stages(fixed_fwd(K), std::max(32768, 8 * rows_pad((N + 7) / 8) * 128)) == 0 ||
+      ring_stages(fixed_bwd(K), 32768) == 0) {
     std::snprintf(buf, sizeof(buf),
                   "lstm sequence kernels need 1 <= N <= 256, K %% 64 == 0, K/8 <= %d SMs, K <= 1024 "
                   "(T=%d N=%d K=%d)", sms, T, N, K);
@@ -660,7 +660,8 @@ BRK_API int brk_lstm_seq_fwd(const float* gx, const void* r_cat, const float* s0
   p.flags = flags;
   p.ts = g_seq_ts;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int smem = 232448;  // the ring depth is chosen per cluster size below
+  // stages are 32 KB slots (cs slices of ceil(N / cs) rows rounded to 8 never exceed 256 rows)
+  const int smem = kStagesS * 32768 + fixed_fwd(K);
   cudaError_t err = cudaFuncSetAttribute(lstm_seq_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (err != cudaSuccess) return set_cuda_error(err, "lstm seq fwd smem");
   cudaFuncSetAttribute(lstm_seq_fwd_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -693,9 +694,11 @@ BRK_API int brk_lstm_seq_fwd(const float* gx, const void* r_cat, const float* s0
     const uint64_t strides[3] = {1, (uint64_t)K, (uint64_t)N * K};
     const char* full_env = std::getenv("BRK_LSTM_FULL_TILE");  // diagnostics: stream all 256 rows
     p.slice = (full_env != nullptr && std::atoi(full_env) != 0) ? 256 / cs : ((N + cs - 1) / cs + 7) / 8 * 8;
-    p.stage_bytes = p.slice * cs * 128;
+    p.stage_bytes = std::max(32768, p.slice * cs * 128);
+    p.stage_tx = p.slice * cs * 128;
     p.stages = ring_stages(fixed_fwd(K), p.stage_bytes);
-    if (p.stages == 0) return set_error(BRK_ERR_CONTRACT, "lstm seq fwd: ring does not fit");
+    if (p.stages != kStagesS || p.stage_bytes != 32768)
+      return set_error(BRK_ERR_CONTRACT, "lstm seq fwd: ring does not fit");
     const uint32_t box[3] = {64, static_cast<uint32_t>(p.slice), 1};
     if ((rc = encode_tmap(&p.map_a, h_bf, true, 3, dims, strides, box))) return rc;
   }
@@ -729,8 +732,10 @@ BRK_API int brk_lstm_seq_bwd(const float* dh, const float* gates, const float* s
   {
     const uint64_t dims[3] = {(uint64_t)(4 * K), (uint64_t)N, (uint64_t)T};
     const uint64_t strides[3] = {1, (uint64_t)(4 * K), (uint64_t)N * 4 * K};
-    p.stage_bytes = rows_pad(N) * 128;
+    p.stage_bytes = 32768;
+    p.stage_tx = rows_pad(N) * 128;
     p.stages = ring_stages(fixed_bwd(K), p.stage_bytes);
+    if (p.stages != kStagesS) return set_error(BRK_ERR_CONTRACT, "lstm seq bwd: ring does not fit");
     const uint32_t box[3] = {64, static_cast<uint32_t>(rows_pad(N)), 1};
     if ((rc = encode_tmap(&p.map_a, dpre, true, 3, dims, strides, box))) return rc;
   }
