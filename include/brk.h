@@ -164,6 +164,14 @@ BRK_API size_t brk_fc_upd_workspace(int N, int C, int K);
 BRK_API int brk_mlp_step(int L, int N, int C, const void* const* y, void* const* dz, const void* dy,
                          void* const* w, void* const* w_next, float* const* bias, float* const* dw, float* const* db,
                          float* const* colsum, float lr, void* workspace, size_t ws_bytes, void* stream);
+/* The same step with an explicit storage type: BRK_BF16 (= brk_mlp_step) or BRK_F32 (fp32
+ * activations, weights and gradients in the same blocked layouts, kind::tf32 tensor-core math:
+ * the reference's own fp32 storage, north_star "bf16 and TF32 inputs").  Replaces the
+ * reference FC runner's per-pass fc_forward calls (bench.py:355-360) for the whole step. */
+BRK_API int brk_mlp_step_dt(int L, int N, int C, const void* const* y, void* const* dz, const void* dy,
+                            void* const* w, void* const* w_next, float* const* bias, float* const* dw,
+                            float* const* db, float* const* colsum, float lr, void* workspace, size_t ws_bytes,
+                            int dtype, void* stream);
 BRK_API size_t brk_mlp_step_workspace_bytes(int L, int N, int C);
 /* Bias gradient (north star): dz_out = dy * (y > 0) if y != NULL; db[K] = sum over N of dz;
  * if bias_sgd != NULL also bias_sgd -= lr * db (fused SGD).  Deterministic.

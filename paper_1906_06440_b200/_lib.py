@@ -53,6 +53,8 @@ SIGNATURES: dict[str, tuple] = {
     "brk_fc_upd_workspace": (ctypes.c_size_t, [_c_int, _c_int, _c_int]),
     "brk_mlp_step": (_c_int, [_c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_f, _vp,
                               ctypes.c_size_t, _vp]),
+    "brk_mlp_step_dt": (_c_int, [_c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_f, _vp,
+                                 ctypes.c_size_t, _c_int, _vp]),
     "brk_mlp_step_workspace_bytes": (ctypes.c_size_t, [_c_int, _c_int, _c_int]),
     "brk_diag_set_timestamps": (None, [_vp]),
     "brk_lstm_fwd_step": (_c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp]),

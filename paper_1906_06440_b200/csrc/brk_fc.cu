@@ -527,10 +527,24 @@ size_t mlp_chunk_counters(int L, int N, int C) { return static_cast<size_t>(3 * 
 
 // The captured engine problems of the step -> the lean MLP kernel's problem table (brk_mlp.h):
 // the same operand maps and schedule, plus TMA maps for the epilogue's stores and side operands.
-static int to_mlp_group(const EngineGroup& G, int N, int C, MlpGroup& M) {
+// The captured engine problems of the step -> the lean MLP kernel's problem table (brk_mlp.h):
+// the same operand maps and schedule, plus TMA maps for the epilogue's stores and side operands
+// (bf16: 64-column boxes; fp32 storage / TF32: 32-column boxes).
+static int to_mlp_group(const EngineGroup& G, const int* kinds, int N, int C, int dtype, MlpGroup& M) {
   std::memset(&M, 0, sizeof(M));
   M.sched = G.sched;
+  const bool f32 = dtype == BRK_F32;
+  M.tf32 = f32 ? 1 : 0;
   const Map4 act = act_layout(N, C), wl = w_layout(C, C);
+  const uint32_t bx = f32 ? 32 : 64;  // side / output box width (128 B of elements)
+  auto enc_act = [&](CUtensorMap* m, const void* ptr) {
+    const uint32_t box[4] = {bx, 32, 1, 1};
+    return encode_tmap(m, ptr, !f32, 4, act.dims, act.strides, box);
+  };
+  auto enc_w = [&](CUtensorMap* m, const void* ptr) {
+    const uint32_t box[4] = {bx, 32, 1, 1};
+    return encode_tmap(m, ptr, !f32, 4, wl.dims, wl.strides, box);
+  };
   int rc = 0;
   for (int q = 0; q < G.sched.n_probs && !rc; ++q) {
     const EngineParams& e = G.probs[q];
@@ -540,8 +554,11 @@ static int to_mlp_group(const EngineGroup& G, int N, int C, MlpGroup& M) {
     m.m_tiles = e.m_tiles;
     m.n_tiles = e.n_tiles;
     m.k_steps = e.k_steps;
-    m.a_rc2 = e.ca.rc[2]; m.a_rc3 = e.ca.rc[3]; m.a_kc2 = e.ca.kc[0][2]; m.a_kc3 = e.ca.kc[0][3];
-    m.b_rc2 = e.cb.rc[2]; m.b_rc3 = e.cb.rc[3]; m.b_kc2 = e.cb.kc[0][2]; m.b_kc3 = e.cb.kc[0][3];
+    for (int d = 0; d < 5; ++d) {
+      if (e.ca.base[d] != 0 || e.cb.base[d] != 0) return set_error(BRK_ERR_CONTRACT, "mlp step: operand base offset");
+      m.a_rc[d] = e.ca.rc[d]; m.a_k0[d] = e.ca.kc[0][d]; m.a_k1[d] = e.ca.kc[1][d];
+      m.b_rc[d] = e.cb.rc[d]; m.b_k0[d] = e.cb.kc[0][d]; m.b_k1[d] = e.cb.kc[1][d];
+    }
     m.a_mn = e.ca.mn_major;
     m.b_mn = e.cb.mn_major;
     m.cols = e.cols;
@@ -553,26 +570,25 @@ static int to_mlp_group(const EngineGroup& G, int N, int C, MlpGroup& M) {
     m.db_out = e.db_out;
     m.bias_sgd = e.bias_sgd;
     m.lr = e.sgd_lr != 0.0f ? e.sgd_lr : e.bias_lr;
-    if (e.out_bf16) {
-      m.kind = e.aux_in != nullptr ? kMlpFwdTop : (e.bias != nullptr ? kMlpFwd : (e.mask != nullptr ? kMlpBwd : kMlpBwdPlain));
-      if ((rc = enc(&m.map_out, e.out, act, 64, 32, 1, 1))) break;
+    m.kind = kinds[q];
+    if (m.kind != kMlpUpd) {
+      if ((rc = enc_act(&m.map_out, e.out))) break;
       const void* in = m.kind == kMlpFwdTop ? e.aux_in : (m.kind == kMlpBwd ? e.mask : nullptr);
       if (in != nullptr) {
         m.has_in = 1;
-        if ((rc = enc(&m.map_in, in, act, 64, 32, 1, 1))) break;
+        if ((rc = enc_act(&m.map_in, in))) break;
       }
       if (m.kind == kMlpFwdTop) {
         m.has_aux = 1;
-        if ((rc = enc(&m.map_aux, e.aux_out, act, 64, 32, 1, 1))) break;
+        if ((rc = enc_act(&m.map_aux, e.aux_out))) break;
       }
     } else {
-      m.kind = kMlpUpd;
       const uint32_t box[4] = {32, 32, 1, 1};
-      if ((rc = encode_tmap(&m.map_out, e.out, false, 4, wl.dims, wl.strides, box))) break;
+      if ((rc = encode_tmap(&m.map_out, e.out, false, 4, wl.dims, wl.strides, box))) break;  // dW fp32
       if (e.sgd_w != nullptr) {
         m.has_in = m.has_aux = 1;
-        if ((rc = enc(&m.map_in, e.sgd_src != nullptr ? e.sgd_src : e.sgd_w, wl, 64, 32, 1, 1))) break;
-        if ((rc = enc(&m.map_aux, e.sgd_w, wl, 64, 32, 1, 1))) break;
+        if ((rc = enc_w(&m.map_in, e.sgd_src != nullptr ? e.sgd_src : e.sgd_w))) break;
+        if ((rc = enc_w(&m.map_aux, e.sgd_w))) break;
       }
     }
   }
@@ -589,8 +605,16 @@ BRK_API size_t brk_mlp_step_workspace_bytes(int L, int N, int C) {
 BRK_API int brk_mlp_step(int L, int N, int C, const void* const* y, void* const* dz, const void* dy,
                          void* const* w, void* const* w_next, float* const* bias, float* const* dw, float* const* db,
                          float* const* colsum, float lr, void* workspace, size_t ws_bytes, void* stream) {
+  return brk_mlp_step_dt(L, N, C, y, dz, dy, w, w_next, bias, dw, db, colsum, lr, workspace, ws_bytes, BRK_BF16,
+                         stream);
+}
+
+BRK_API int brk_mlp_step_dt(int L, int N, int C, const void* const* y, void* const* dz, const void* dy,
+                            void* const* w, void* const* w_next, float* const* bias, float* const* dw,
+                            float* const* db, float* const* colsum, float lr, void* workspace, size_t ws_bytes,
+                            int dtype, void* stream) {
   if (L < 1 || 3 * L > kMaxProbs) return set_error(BRK_ERR_CONTRACT, "mlp_step: 1 <= layers <= 4");
-  int rc = check_fc(N, C, C, kB, kB, kB, BRK_BF16);
+  int rc = check_fc(N, C, C, kB, kB, kB, dtype);
   if (rc) return rc;
   if (N % 256 || C % 256 || N / 256 > kCounterStride - 1)
     return set_error(BRK_ERR_CONTRACT, "mlp_step: N, C multiples of 256, N <= 16384");
@@ -620,12 +644,14 @@ BRK_API int brk_mlp_step(int L, int N, int C, const void* const* y, void* const*
     return r;
   };
   int fwd_of[8], bwd_of[8], upd_of[8];
+  int kinds[kMaxProbs];
   for (int i = 0; i < 8; ++i) fwd_of[i] = bwd_of[i] = upd_of[i] = -1;
   for (int l = 0; l < L && !rc; ++l) {  // forward: y[l+1] = relu(W_l y[l] + b_l)
     rc = capture([&] {
-      return brk_fc_fwd(y[l], w[l], bias[l], const_cast<void*>(y[l + 1]), N, C, C, kB, kB, kB, kActRelu, BRK_BF16,
+      return brk_fc_fwd(y[l], w[l], bias[l], const_cast<void*>(y[l + 1]), N, C, C, kB, kB, kB, kActRelu, dtype,
                         stream);
     });
+    kinds[q] = l == L - 1 ? kMlpFwdTop : kMlpFwd;
     if (l > 0) { gs.dep_prob[q][0] = fwd_of[l - 1]; gs.dep_mode[q][0] = chunk_mode; }
     G.probs[q].b_first = b_first;  // B = W_l, not written in this launch before the weight updates
     if (l == L - 1) {  // top layer also emits dz_L = dy * (y_L > 0) and its column sums
@@ -644,8 +670,9 @@ BRK_API int brk_mlp_step(int L, int N, int C, const void* const* y, void* const*
     if (dz_src < 0 || bwd_of[l] >= 0) { rc = set_error(BRK_ERR_CONTRACT, "mlp_step: unit order breaks a dependency"); return; }
     rc = capture([&] {
       return brk_fc_bwd_data(dz[l], w[l - 1], l > 1 ? y[l - 1] : nullptr, dz[l - 1], l > 1 ? colsum[l - 1] : nullptr,
-                             N, C, C, kB, kB, kB, BRK_BF16, stream);
+                             N, C, C, kB, kB, kB, dtype, stream);
     });
+    kinds[q] = l > 1 ? kMlpBwd : kMlpBwdPlain;
     gs.dep_prob[q][0] = dz_src; gs.dep_mode[q][0] = chunk_mode;  // the same rows of dz_l
     // B = W_{l-1}: with in-place SGD it is rewritten only after this pass completes (dependency below)
     G.probs[q].b_first = b_first;
@@ -660,10 +687,18 @@ BRK_API int brk_mlp_step(int L, int N, int C, const void* const* y, void* const*
     // lr == 0: gradients only (data parallel: all-reduce, then SGD outside the step)
     const bool sgd = lr != 0.0f;
     void* w_out = !sgd ? nullptr : (w_next != nullptr ? w_next[l - 1] : w[l - 1]);
+    // (fp32 weights: brk_fc_upd rejects a fused fp32 SGD for its own epilogue; the lean kernel
+    //  does it, so the SGD operands are set on the captured problem)
+    const bool f32 = dtype == BRK_F32;
     rc = capture([&] {
-      return brk_fc_upd(y[l - 1], dz[l], dw[l - 1], w_out, lr, colsum[l], N / 32, db[l - 1],
-                        sgd ? bias[l - 1] : nullptr, lr, nullptr, 0, N, C, C, kB, kB, kB, BRK_BF16, stream);
+      return brk_fc_upd(y[l - 1], dz[l], dw[l - 1], f32 ? nullptr : w_out, lr, colsum[l], N / 32, db[l - 1],
+                        sgd ? bias[l - 1] : nullptr, lr, nullptr, 0, N, C, C, kB, kB, kB, dtype, stream);
     });
+    if (f32 && w_out != nullptr) {
+      G.probs[q].sgd_w = w_out;
+      G.probs[q].sgd_lr = lr;
+    }
+    kinds[q] = kMlpUpd;
     gs.dep_prob[q][0] = dz_src; gs.dep_mode[q][0] = 1;  // all of dz_l (reduction over N)
     if (!sgd) {
       // no weight write: no ordering against the bwd-data pass
@@ -715,9 +750,9 @@ BRK_API int brk_mlp_step(int L, int N, int C, const void* const* y, void* const*
   // last CTA (no memset between back-to-back steps)
   g_launches.fetch_add(1);
   const char* lean_env = std::getenv("BRK_MLP_LEAN");  // 0 (diagnostics): the generic grouped engine
-  if (lean_env != nullptr && std::atoi(lean_env) == 0) return launch_engine_group(G, 128, 1, st);
+  if (lean_env != nullptr && std::atoi(lean_env) == 0 && dtype == BRK_BF16) return launch_engine_group(G, 128, 1, st);
   static MlpGroup M;
-  if ((rc = to_mlp_group(G, N, C, M))) return rc;
+  if ((rc = to_mlp_group(G, kinds, N, C, dtype, M))) return rc;
   M.debug_ts = g_debug_ts;
   const char* fl = std::getenv("BRK_MLP_FLAGS");
   M.flags = fl ? std::atoi(fl) : 0;

@@ -30,20 +30,26 @@ namespace {
 
 constexpr int kEpiWarps = 8;
 constexpr int kMmaWarp = kEpiWarps;
-constexpr int kStages = 6;
-constexpr int kProducers = kStages;
 constexpr int kThreads = 16 * 32;
-constexpr int kABytes = 128 * 128;  // per CTA per k-step: 128 rows x 64 bf16
-constexpr int kBBytes = 64 * 128;   // per CTA per k-step: 64 rows (N / 2) x 64 bf16
+constexpr int kABytes = 128 * 128;  // per CTA per k-step: 128 rows x 128 B (64 bf16 / 32 fp32)
+constexpr int kBBytes = 64 * 128;   // per CTA per k-step: 64 rows (N / 2) x 128 B
 constexpr int kStageBytes = kABytes + kBBytes;
 constexpr uint32_t kTxBytes = 2 * kStageBytes;  // both CTAs' boxes complete on the leader's barrier
 constexpr int kEpiTile = 4096;                  // 32 rows x 128 B
-constexpr int kEpiBytes = kEpiWarps * 2 * kEpiTile;
-constexpr int kBiasBytes = kEpiWarps * 256;
 constexpr int kBarBytes = 256;
-constexpr int kSmem = kStages * kStageBytes + kEpiBytes + kBiasBytes + kBarBytes + 1024;
 constexpr int kBN = 128;
-static_assert(kSmem <= 232448, "shared memory budget");
+// bf16: 6 ring stages, 2 staging tiles per epilogue warp (+ bias broadcast area); TF32 (fp32
+// outputs and side operands are two 32-column boxes each): 4 stages, 4 tiles, bias by shuffles
+template <bool kTF32>
+struct MlpCfg {
+  static constexpr int kStages = kTF32 ? 4 : 6;
+  static constexpr int kProducers = kStages;
+  static constexpr int kTiles = kTF32 ? 4 : 2;
+  static constexpr int kEpiBytes = kEpiWarps * kTiles * kEpiTile;
+  static constexpr int kBiasBytes = kTF32 ? 0 : kEpiWarps * 256;
+  static constexpr int kSmem = kStages * kStageBytes + kEpiBytes + kBiasBytes + kBarBytes + 1024;
+  static_assert(kSmem <= 232448, "shared memory budget");
+};
 
 __device__ __forceinline__ uint32_t relu_pack(float lo, float hi) {
   uint32_t r;
@@ -103,10 +109,41 @@ __device__ __forceinline__ void mlp_wait_chunk(const GroupSched* gs, int prob, i
   asm volatile("fence.proxy.async.global;" ::: "memory");  // the TMA reads follow
 }
 
-// smem operand descriptor of MMA sub-step kk (16 K-elements) — bf16, 128B swizzle
+// smem operand descriptor of MMA sub-step kk (32 bytes of K) — 128B swizzle.  MN-major: bf16
+// atoms of 64 K-rows x 128 B (8-row groups 1024 B apart); TF32 the 32 B-chunk swizzle with
+// atoms of 32 K-rows (4-row groups 512 B apart), 8 K-rows per MMA (as brk_engine.cu)
+template <bool kTF32>
 __device__ __forceinline__ uint64_t op_desc(uint32_t base, int mn_major, int kk) {
-  return mn_major ? make_smem_desc(base + kk * 16 * 128, 64 * 128, 1024, kSwizzle128B)
-                  : make_smem_desc(base + kk * 32, 16, 1024, kSwizzle128B);
+  if (!mn_major) return make_smem_desc(base + kk * 32, 16, 1024, kSwizzle128B);
+  if constexpr (kTF32) return make_smem_desc(base + kk * 8 * 128, 32 * 128, 512, kSwizzle128B32);
+  return make_smem_desc(base + kk * 16 * 128, 64 * 128, 1024, kSwizzle128B);
+}
+
+// k-step s of row block `row` -> box coordinates (see MlpProb)
+template <int kDims>
+__device__ __forceinline__ void op_coords(const int32_t* rc, const int32_t* k0, const int32_t* k1, int row, int d0,
+                                          int d1, int32_t (&c)[kDims]) {
+#pragma unroll
+  for (int d = 0; d < kDims; ++d) c[d] = rc[d] * row + k0[d] * d0 + k1[d] * d1;
+}
+
+// fp32 column sums over the 32 rows of two staged 32-column fp32 boxes (columns 0-31 in ta,
+// 32-63 in tb): lane l sums columns 2l, 2l + 1 and stores them (generic stores; the caller
+// fences them before the whole-tile release)
+__device__ __forceinline__ void tile_colsum_f32(uint32_t ta, uint32_t tb, int lane, float* gdst) {
+  const uint32_t tile = lane < 16 ? ta : tb;
+  const uint32_t c32 = (static_cast<uint32_t>(lane) * 2u) & 31u;
+  const uint32_t j = c32 >> 2, wd = (c32 & 3u) << 2;
+  float s0 = 0.0f, s1 = 0.0f;
+#pragma unroll 8
+  for (uint32_t r = 0; r < 32; ++r) {
+    float2 x;
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(x.x), "=f"(x.y)
+                 : "r"(tile + r * 128 + (((j ^ (r & 7u)) << 4) | wd)) : "memory");
+    s0 += x.x;
+    s1 += x.y;
+  }
+  *reinterpret_cast<float2*>(gdst + 2 * lane) = make_float2(s0, s1);
 }
 
 // Work unit u -> (problem, row block, column tile).  kPairs CTA pairs per cluster take
@@ -163,16 +200,22 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // kCS = 2: one CTA pair per cluster.  kCS = 4: two pairs per cluster on adjacent column tiles
 // of the same row block; the pair whose index matches the k-step's parity loads the A box and
 // multicasts it into both pairs (L2 reads per k-step 96 -> 64 KB per cluster... per pair 48 -> 32).
-template <int kCS>
+template <int kCS, bool kTF32>
 __global__ void __launch_bounds__(kThreads, 1) mlp_step_kernel(const __grid_constant__ MlpGroup G) {
   constexpr int kPairs = kCS / 2;
+  using Cfg = MlpCfg<kTF32>;
+  constexpr int kStages = Cfg::kStages;
+  constexpr int kProducers = Cfg::kProducers;
+  constexpr int kEpiBytes = Cfg::kEpiBytes;
+  constexpr int kBiasBytes = Cfg::kBiasBytes;
+  constexpr int kDims = kTF32 ? 5 : 4;
   const MlpProb* P = G.probs;
   const GroupSched* gs = &G.sched;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* epi = smem + kStages * kStageBytes;
   float* bias_area = reinterpret_cast<float*>(epi + kEpiBytes);
-  uint64_t* full = reinterpret_cast<uint64_t*>(epi + kEpiBytes + kBiasBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi + kEpiBytes + kBiasBytes);  // (bias area: bf16 only)
   uint64_t* empty = full + kStages;
   uint64_t* tfull = empty + kStages;   // [2]
   uint64_t* tempty = tfull + 2;        // [2]
@@ -251,15 +294,19 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_step_kernel(const __grid_cons
         const int brow = nb * 2 + static_cast<int>(rank);
         const int n_steps = p.k_steps;
         // rotate the batch-list start per tile (concurrent tiles read different blocks)
-        const int rot = (G.flags & 1) ? (mb * 7 + (nb - pair) * 3) % n_steps : 0;  // no rotation: tiles sharing a row block read the same A box at about the same time (L2 dedup: 69.5 -> 68.6 us)
-        const int a2 = p.a_rc2 * arow, a3 = p.a_rc3 * arow, b2 = p.b_rc2 * brow, b3 = p.b_rc3 * brow;
+        // k-step order: natural (tiles sharing a row block read the same A box at about the same
+        // time: L2 dedup, 69.5 -> 68.6 us); flags bit 0: the per-pass engine's rotation; bit 6
+        // (affinity lists): a chained tile starts with the chunks its own pair wrote last
+        const int rot = (G.flags & 1) ? (mb * 7 + (nb - pair) * 3) % n_steps
+                                      : ((G.flags & 64) && chunked ? (2 * nb) % n_steps : 0);
         for (int s0 = (pid - g % kProducers + kProducers) % kProducers; s0 < n_steps; s0 += kProducers) {
           const int gg = g + s0;
           const int stage = gg % kStages;
           const uint32_t phase = (gg / kStages) & 1;
           const int s = s0 + rot < n_steps ? s0 + rot : s0 + rot - n_steps;
           if (chunked) {  // before the ring wait: the poll latency overlaps the slot becoming free
-            mlp_wait_chunk(gs, prob, mb, static_cast<int>(rank), s, G.flags);
+            // (a TF32 k-step is 32 columns: half of a 64-column chunk)
+            mlp_wait_chunk(gs, prob, mb, static_cast<int>(rank), kTF32 ? s >> 1 : s, G.flags);
             if (pid == 0 && !published) {
               publish_deps(deps_seq, ordinal);
               MLP_TT(static_cast<int>(ordinal) - 1, 0);
@@ -269,19 +316,22 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_step_kernel(const __grid_cons
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * kStageBytes;
           if (leader) mbar_arrive_expect_tx(&full[stage], kTxBytes);
-          const int32_t ca[4] = {0, 0, a2 + p.a_kc2 * s, a3 + p.a_kc3 * s};
-          const int32_t cb[4] = {0, 0, b2 + p.b_kc2 * s, b3 + p.b_kc3 * s};
+          const int d0 = kTF32 ? (s & 1) : s, d1 = kTF32 ? (s >> 1) : 0;
+          int32_t ca[kDims], cb[kDims];
+          op_coords<kDims>(p.a_rc, p.a_k0, p.a_k1, arow, d0, d1, ca);
+          op_coords<kDims>(p.b_rc, p.b_k0, p.b_k1, brow, d0, d1, cb);
           if (deps_pending) {  // B (weights) does not wait for the tile's dependencies
-            tma_load_pair<4>(sa + kABytes, &p.map_b, &full[stage], cb);
+            tma_load_pair<kDims>(sa + kABytes, &p.map_b, &full[stage], cb);
             wait_published(deps_seq, ordinal, true);
             deps_pending = false;
           } else {
-            tma_load_pair<4>(sa + kABytes, &p.map_b, &full[stage], cb);
+            tma_load_pair<kDims>(sa + kABytes, &p.map_b, &full[stage], cb);
           }
           if constexpr (kPairs == 1) {
-            tma_load_pair<4>(sa, &p.map_a, &full[stage], ca);
+            tma_load_pair<kDims>(sa, &p.map_a, &full[stage], ca);
           } else if ((s & 1) == pair) {  // A into this CTA and its counterpart in the other pair
-            tma_load_pair_mc4(sa, &p.map_a, &full[stage], ca, static_cast<uint16_t>((1u << rank) | (4u << rank)));
+            if constexpr (kDims == 4)
+              tma_load_pair_mc4(sa, &p.map_a, &full[stage], ca, static_cast<uint16_t>((1u << rank) | (4u << rank)));
           }
         }
         if (!published && pid == 0) {
@@ -303,7 +353,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_step_kernel(const __grid_cons
         locate<kPairs>(gs, P, u, pair, prob, mb, nb);
         const MlpProb& p = P[prob];
         const int a_mn = p.a_mn, b_mn = p.b_mn, n_steps = p.k_steps;
-        const uint32_t idesc = make_idesc(kFmtBF16, 256, kBN, a_mn, b_mn);
+        const uint32_t idesc = make_idesc(kTF32 ? kFmtTF32 : kFmtBF16, 256, kBN, a_mn, b_mn);
         const int acc = local & 1;
         mbar_wait(&tempty[acc], ((local >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -317,7 +367,8 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_step_kernel(const __grid_cons
             const uint32_t sb = sa + kABytes;
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
-              mma_ss_pair<false>(d_tmem, op_desc(sa, a_mn, kk), op_desc(sb, b_mn, kk), idesc, (s | kk) ? 1u : 0u);
+              mma_ss_pair<kTF32>(d_tmem, op_desc<kTF32>(sa, a_mn, kk), op_desc<kTF32>(sb, b_mn, kk), idesc,
+                                 (s | kk) ? 1u : 0u);
             if constexpr (kPairs == 1) {
               mma_commit_pair(&empty[stage]);
               if (s == n_steps - 1) mma_commit_pair(&tfull[acc]);
@@ -336,7 +387,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_step_kernel(const __grid_cons
     // ---------------------------------------------------------------- epilogue (warps 0..7)
     pdl_wait();
     const int quarter = warp & 3, half = warp >> 2;
-    const uint32_t st0 = smem_u32(epi + warp * 2 * kEpiTile), st1 = st0 + kEpiTile;
+    const uint32_t st0 = smem_u32(epi + warp * Cfg::kTiles * kEpiTile), st1 = st0 + kEpiTile;
     const uint32_t lrow = static_cast<uint32_t>(lane) * 128;
     const uint32_t lsw = static_cast<uint32_t>(lane & 7);
     const uint32_t bias_s = smem_u32(bias_area + warp * 64);
@@ -361,17 +412,29 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_step_kernel(const __grid_cons
       if (p.has_in) {
         if (kind != kMlpFwdTop) wait_published(deps_seq, static_cast<uint32_t>(local + 1), true);
         if (lane == 0) {
-          mbar_arrive_expect_tx(&ebar[warp], kEpiTile);
-          const int32_t c[4] = {0, row0 & 63, upd ? row0 >> 6 : colblk, upd ? colblk : row0 >> 6};
-          tma_load<4>(epi + (warp * 2 + 1) * kEpiTile, &p.map_in, &ebar[warp], c);
+          // bf16: one 64-column box into the warp's second tile; fp32: two 32-column boxes into
+          // its third and fourth
+          constexpr int kBoxes = kTF32 ? 2 : 1;
+          mbar_arrive_expect_tx(&ebar[warp], kBoxes * kEpiTile);
+#pragma unroll
+          for (int b = 0; b < kBoxes; ++b) {
+            const int32_t c[4] = {32 * b, row0 & 63, upd ? row0 >> 6 : colblk, upd ? colblk : row0 >> 6};
+            tma_load<4>(epi + (warp * Cfg::kTiles + (kTF32 ? 2 + b : 1)) * kEpiTile, &p.map_in, &ebar[warp], c);
+          }
         }
       } else if (p.db_partials != nullptr) {
         wait_published(deps_seq, static_cast<uint32_t>(local + 1), false);
       }
-      if (kind <= kMlpFwdTop) {  // this warp's 64 bias values -> smem (read back as broadcasts)
-        const float b0 = __ldg(p.bias + colblk * 64 + lane), b1 = __ldg(p.bias + colblk * 64 + 32 + lane);
-        asm volatile("st.shared.f32 [%0], %1;" ::"r"(bias_s + lane * 4), "f"(b0) : "memory");
-        asm volatile("st.shared.f32 [%0], %1;" ::"r"(bias_s + 128 + lane * 4), "f"(b1) : "memory");
+      // this warp's 64 bias values: bf16 -> smem (read back as broadcasts), TF32 -> registers
+      // (broadcast by shuffles)
+      float bias0 = 0.0f, bias1 = 0.0f;
+      if (kind <= kMlpFwdTop) {
+        bias0 = __ldg(p.bias + colblk * 64 + lane);
+        bias1 = __ldg(p.bias + colblk * 64 + 32 + lane);
+        if constexpr (!kTF32) {
+          asm volatile("st.shared.f32 [%0], %1;" ::"r"(bias_s + lane * 4), "f"(bias0) : "memory");
+          asm volatile("st.shared.f32 [%0], %1;" ::"r"(bias_s + 128 + lane * 4), "f"(bias1) : "memory");
+        }
       }
       mbar_wait(&tfull[acc], (local >> 1) & 1);
       tc_fence_after();
@@ -408,97 +471,199 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_step_kernel(const __grid_cons
         }
         if (threadIdx.x == 0) MLP_TT(local, 7);
       };
-      if (kind <= kMlpFwdTop) {
-        // y = relu(acc + bias) -> st0; top layer: dz = dy * (y > 0) in place in st1
-        const bool top = kind == kMlpFwdTop;
+      if constexpr (kTF32) {
+        // fp32 storage: a warp's 32 x 64 block is two 32-column boxes.  Tiles: t[0], t[1] the
+        // primary output (y / dx / dW); t[2], t[3] the side operand, overwritten in place by the
+        // second output (dz of the top layer, dz of bwd-data, the new weights)
+        const uint32_t t[4] = {st0, st0 + kEpiTile, st0 + 2 * kEpiTile, st0 + 3 * kEpiTile};
+        const int32_t wr = row0 & 63, wb = row0 >> 6;
+        if (kind <= kMlpFwdTop) {
+          const bool top = kind == kMlpFwdTop;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const float4 bl = lds_f4(bias_s + j * 32), bh = lds_f4(bias_s + j * 32 + 16);
-          const uint32_t x = relu_pack(__uint_as_float(v[8 * j]) + bl.x, __uint_as_float(v[8 * j + 1]) + bl.y);
-          const uint32_t y = relu_pack(__uint_as_float(v[8 * j + 2]) + bl.z, __uint_as_float(v[8 * j + 3]) + bl.w);
-          const uint32_t z = relu_pack(__uint_as_float(v[8 * j + 4]) + bh.x, __uint_as_float(v[8 * j + 5]) + bh.y);
-          const uint32_t w = relu_pack(__uint_as_float(v[8 * j + 6]) + bh.z, __uint_as_float(v[8 * j + 7]) + bh.w);
-          const uint32_t off = lrow + ((static_cast<uint32_t>(j) ^ lsw) << 4);
-          sts128(st0 + off, x, y, z, w);
-          if (top) {  // relu outputs are >= +0: y > 0 <=> the bf16 bits as int16 > 0
-            const uint4 d = lds128(st1 + off);
-            sts128(st1 + off, d.x & __vcmpgts2(x, 0u), d.y & __vcmpgts2(y, 0u), d.z & __vcmpgts2(z, 0u),
-                   d.w & __vcmpgts2(w, 0u));
+          for (int hh = 0; hh < 2; ++hh) {
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              float x[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                x[e] = fmaxf(__uint_as_float(v[32 * hh + 4 * c + e]) +
+                                 __shfl_sync(0xffffffffu, hh ? bias1 : bias0, 4 * c + e), 0.0f);
+              const uint32_t off = lrow + ((static_cast<uint32_t>(c) ^ lsw) << 4);
+              sts128(t[hh] + off, __float_as_uint(x[0]), __float_as_uint(x[1]), __float_as_uint(x[2]),
+                     __float_as_uint(x[3]));
+              if (top) {  // dz = dy * (y > 0)
+                const float4 d = lds_f4(t[2 + hh] + off);
+                sts128(t[2 + hh] + off, x[0] > 0.0f ? __float_as_uint(d.x) : 0u, x[1] > 0.0f ? __float_as_uint(d.y) : 0u,
+                       x[2] > 0.0f ? __float_as_uint(d.z) : 0u, x[3] > 0.0f ? __float_as_uint(d.w) : 0u);
+              }
+            }
           }
-        }
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-          tma_store4(&p.map_out, st0, ao[0], ao[1], ao[2], ao[3]);
-          if (top) tma_store4(&p.map_aux, st1, ao[0], ao[1], ao[2], ao[3]);
-          bulk_commit();
-          release_chunk_mlp();
-        }
-        if (top) tile_colsum(st1, lane, bias_s, colsum_dst);  // (the bias values are consumed)
-      } else if (kind <= kMlpBwdPlain) {
-        // dz = bf16(acc) * (mask > 0) (mask: the previous layer's ReLU output, >= +0)
-        const bool masked = kind == kMlpBwd;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          uint32_t x = bf16_pack(__uint_as_float(v[8 * j]), __uint_as_float(v[8 * j + 1]));
-          uint32_t y = bf16_pack(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3]));
-          uint32_t z = bf16_pack(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5]));
-          uint32_t w = bf16_pack(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7]));
-          const uint32_t off = lrow + ((static_cast<uint32_t>(j) ^ lsw) << 4);
-          if (masked) {
-            const uint4 m = lds128(st1 + off);
-            x &= __vcmpgts2(m.x, 0u);
-            y &= __vcmpgts2(m.y, 0u);
-            z &= __vcmpgts2(m.z, 0u);
-            w &= __vcmpgts2(m.w, 0u);
-          }
-          sts128(st0 + off, x, y, z, w);
-        }
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-          tma_store4(&p.map_out, st0, ao[0], ao[1], ao[2], ao[3]);
-          bulk_commit();
-          release_chunk_mlp();
-        }
-        if (colsum_dst != nullptr) tile_colsum(st0, lane, bias_s, colsum_dst);
-      } else {
-        // weight update: dW (fp32, two 32-column boxes through st0); w_next = w - lr dW (st1)
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          if (hh == 1) {
-            if (lane == 0) bulk_wait_read0();  // st0 free again
-            __syncwarp();
-          }
-#pragma unroll
-          for (int c = 0; c < 8; ++c)
-            sts128(st0 + lrow + ((static_cast<uint32_t>(c) ^ lsw) << 4), v[32 * hh + 4 * c], v[32 * hh + 4 * c + 1],
-                   v[32 * hh + 4 * c + 2], v[32 * hh + 4 * c + 3]);
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            tma_store4(&p.map_out, st0, 32 * hh, row0 & 63, row0 >> 6, colblk);
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+              tma_store4(&p.map_out, t[hh], 32 * hh, wr, colblk, wb);
+              if (top) tma_store4(&p.map_aux, t[2 + hh], 32 * hh, wr, colblk, wb);
+            }
+            bulk_commit();
+            release_chunk_mlp();
+          }
+          if (top) tile_colsum_f32(t[2], t[3], lane, colsum_dst);
+        } else if (kind <= kMlpBwdPlain) {
+          // dz = acc * (mask > 0), in place over the mask (bwd-data of layers > 1); dx = acc
+          const bool masked = kind == kMlpBwd;
+          const int o = masked ? 2 : 0;
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              const uint32_t off = lrow + ((static_cast<uint32_t>(c) ^ lsw) << 4);
+              uint32_t x[4] = {v[32 * hh + 4 * c], v[32 * hh + 4 * c + 1], v[32 * hh + 4 * c + 2],
+                               v[32 * hh + 4 * c + 3]};
+              if (masked) {
+                const float4 m = lds_f4(t[2 + hh] + off);
+                x[0] = m.x > 0.0f ? x[0] : 0u;
+                x[1] = m.y > 0.0f ? x[1] : 0u;
+                x[2] = m.z > 0.0f ? x[2] : 0u;
+                x[3] = m.w > 0.0f ? x[3] : 0u;
+              }
+              sts128(t[o + hh] + off, x[0], x[1], x[2], x[3]);
+            }
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store4(&p.map_out, t[o], 0, wr, colblk, wb);
+            tma_store4(&p.map_out, t[o + 1], 32, wr, colblk, wb);
+            bulk_commit();
+            release_chunk_mlp();
+          }
+          if (colsum_dst != nullptr) tile_colsum_f32(t[2], t[3], lane, colsum_dst);
+        } else {
+          // dW (fp32) from t[0], t[1]; w_next = w - lr dW in place over the old weights (t[2], t[3])
+          const float lr = p.lr;
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              const uint32_t off = lrow + ((static_cast<uint32_t>(c) ^ lsw) << 4);
+              const int b = 32 * hh + 4 * c;
+              sts128(t[hh] + off, v[b], v[b + 1], v[b + 2], v[b + 3]);
+              if (p.has_aux) {
+                const float4 w = lds_f4(t[2 + hh] + off);
+                sts128(t[2 + hh] + off, __float_as_uint(w.x - lr * __uint_as_float(v[b])),
+                       __float_as_uint(w.y - lr * __uint_as_float(v[b + 1])),
+                       __float_as_uint(w.z - lr * __uint_as_float(v[b + 2])),
+                       __float_as_uint(w.w - lr * __uint_as_float(v[b + 3])));
+              }
+            }
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+              tma_store4(&p.map_out, t[hh], 32 * hh, wr, wb, colblk);
+              if (p.has_aux) tma_store4(&p.map_aux, t[2 + hh], 32 * hh, wr, wb, colblk);
+            }
             bulk_commit();
           }
-          if (hh == 0 && p.has_aux) {
-            const float lr = p.lr;
+        }
+        if (colsum_dst != nullptr) __threadfence();  // generic column-sum stores before the tile release
+      } else {
+        if (kind <= kMlpFwdTop) {
+          // y = relu(acc + bias) -> st0; top layer: dz = dy * (y > 0) in place in st1
+          const bool top = kind == kMlpFwdTop;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const uint32_t off = lrow + ((static_cast<uint32_t>(j) ^ lsw) << 4);
-              const uint4 wq = lds128(st1 + off);
-              const uint32_t wv[4] = {wq.x, wq.y, wq.z, wq.w};
-              uint32_t o[4];
-#pragma unroll
-              for (int e = 0; e < 4; ++e)
-                o[e] = bf16_pack(__uint_as_float(wv[e] << 16) - lr * __uint_as_float(v[8 * j + 2 * e]),
-                                 __uint_as_float(wv[e] & 0xffff0000u) - lr * __uint_as_float(v[8 * j + 2 * e + 1]));
-              sts128(st1 + off, o[0], o[1], o[2], o[3]);
+          for (int j = 0; j < 8; ++j) {
+            const float4 bl = lds_f4(bias_s + j * 32), bh = lds_f4(bias_s + j * 32 + 16);
+            const uint32_t x = relu_pack(__uint_as_float(v[8 * j]) + bl.x, __uint_as_float(v[8 * j + 1]) + bl.y);
+            const uint32_t y = relu_pack(__uint_as_float(v[8 * j + 2]) + bl.z, __uint_as_float(v[8 * j + 3]) + bl.w);
+            const uint32_t z = relu_pack(__uint_as_float(v[8 * j + 4]) + bh.x, __uint_as_float(v[8 * j + 5]) + bh.y);
+            const uint32_t w = relu_pack(__uint_as_float(v[8 * j + 6]) + bh.z, __uint_as_float(v[8 * j + 7]) + bh.w);
+            const uint32_t off = lrow + ((static_cast<uint32_t>(j) ^ lsw) << 4);
+            sts128(st0 + off, x, y, z, w);
+            if (top) {  // relu outputs are >= +0: y > 0 <=> the bf16 bits as int16 > 0
+              const uint4 d = lds128(st1 + off);
+              sts128(st1 + off, d.x & __vcmpgts2(x, 0u), d.y & __vcmpgts2(y, 0u), d.z & __vcmpgts2(z, 0u),
+                     d.w & __vcmpgts2(w, 0u));
             }
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store4(&p.map_out, st0, ao[0], ao[1], ao[2], ao[3]);
+            if (top) tma_store4(&p.map_aux, st1, ao[0], ao[1], ao[2], ao[3]);
+            bulk_commit();
+            release_chunk_mlp();
+          }
+          if (top) tile_colsum(st1, lane, bias_s, colsum_dst);  // (the bias values are consumed)
+        } else if (kind <= kMlpBwdPlain) {
+          // dz = bf16(acc) * (mask > 0) (mask: the previous layer's ReLU output, >= +0)
+          const bool masked = kind == kMlpBwd;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            uint32_t x = bf16_pack(__uint_as_float(v[8 * j]), __uint_as_float(v[8 * j + 1]));
+            uint32_t y = bf16_pack(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3]));
+            uint32_t z = bf16_pack(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5]));
+            uint32_t w = bf16_pack(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7]));
+            const uint32_t off = lrow + ((static_cast<uint32_t>(j) ^ lsw) << 4);
+            if (masked) {
+              const uint4 m = lds128(st1 + off);
+              x &= __vcmpgts2(m.x, 0u);
+              y &= __vcmpgts2(m.y, 0u);
+              z &= __vcmpgts2(m.z, 0u);
+              w &= __vcmpgts2(m.w, 0u);
+            }
+            sts128(st0 + off, x, y, z, w);
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store4(&p.map_out, st0, ao[0], ao[1], ao[2], ao[3]);
+            bulk_commit();
+            release_chunk_mlp();
+          }
+          if (colsum_dst != nullptr) tile_colsum(st0, lane, bias_s, colsum_dst);
+        } else {
+          // weight update: dW (fp32, two 32-column boxes through st0); w_next = w - lr dW (st1)
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            if (hh == 1) {
+              if (lane == 0) bulk_wait_read0();  // st0 free again
+              __syncwarp();
+            }
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+              sts128(st0 + lrow + ((static_cast<uint32_t>(c) ^ lsw) << 4), v[32 * hh + 4 * c], v[32 * hh + 4 * c + 1],
+                     v[32 * hh + 4 * c + 2], v[32 * hh + 4 * c + 3]);
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-              tma_store4(&p.map_aux, st1, 0, row0 & 63, row0 >> 6, colblk);
+              tma_store4(&p.map_out, st0, 32 * hh, row0 & 63, row0 >> 6, colblk);
               bulk_commit();
+            }
+            if (hh == 0 && p.has_aux) {
+              const float lr = p.lr;
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const uint32_t off = lrow + ((static_cast<uint32_t>(j) ^ lsw) << 4);
+                const uint4 wq = lds128(st1 + off);
+                const uint32_t wv[4] = {wq.x, wq.y, wq.z, wq.w};
+                uint32_t o[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                  o[e] = bf16_pack(__uint_as_float(wv[e] << 16) - lr * __uint_as_float(v[8 * j + 2 * e]),
+                                   __uint_as_float(wv[e] & 0xffff0000u) - lr * __uint_as_float(v[8 * j + 2 * e + 1]));
+                sts128(st1 + off, o[0], o[1], o[2], o[3]);
+              }
+              fence_proxy_async_smem();
+              __syncwarp();
+              if (lane == 0) {
+                tma_store4(&p.map_aux, st1, 0, row0 & 63, row0 >> 6, colblk);
+                bulk_commit();
+              }
             }
           }
         }
@@ -519,17 +684,21 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_step_kernel(const __grid_cons
 #pragma unroll
           for (int e = 0; e < 8; ++e) s += x[e];
         }
-        const uint32_t red = smem_u32(bias_area) + c * 4;
-        if (grp == 1) asm volatile("st.shared.f32 [%0], %1;" ::"r"(red), "f"(s) : "memory");
+        // group 1 parks its sums in its own warps' first staging tile (their stores have completed:
+        // lane 0 waited above); group 0 reads thread t + 128's slot
+        __syncwarp();
+        const uint32_t red_mine = smem_u32(epi) + (t >> 5) * Cfg::kTiles * kEpiTile + (t & 31) * 4;
+        const uint32_t red_peer = smem_u32(epi) + ((t + 128) >> 5) * Cfg::kTiles * kEpiTile + (t & 31) * 4;
+        if (grp == 1) asm volatile("st.shared.f32 [%0], %1;" ::"r"(red_mine), "f"(s) : "memory");
         bar_sync(2, kEpiWarps * 32);
         if (grp == 0) {
           float o;
-          asm volatile("ld.shared.f32 %0, [%1];" : "=f"(o) : "r"(red) : "memory");
+          asm volatile("ld.shared.f32 %0, [%1];" : "=f"(o) : "r"(red_peer) : "memory");
           s += o;
           p.db_out[col] = s;
           if (p.bias_sgd != nullptr) p.bias_sgd[col] -= p.lr * s;
         }
-        bar_sync(2, kEpiWarps * 32);  // the bias area is reused by the next tile
+        bar_sync(2, kEpiWarps * 32);  // the staging tiles are reused by the next tile
       }
       // whole-tile release (row-block / whole-problem counters: weight updates, in-place SGD)
       // (every warp's outputs, column sums included, left through bulk copies that lane 0
@@ -576,9 +745,10 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_step_kernel(const __grid_cons
 int engine_sm_count();
 
 namespace {
-template <int kCS>
+template <int kCS, bool kTF32>
 int launch_mlp_t(MlpGroup& G, cudaStream_t stream) {
-  auto kern = mlp_step_kernel<kCS>;
+  auto kern = mlp_step_kernel<kCS, kTF32>;
+  constexpr int kSmem = MlpCfg<kTF32>::kSmem;
   static int attr_set = 0;
   cudaError_t err;
   if (!attr_set) {
@@ -631,7 +801,7 @@ void mlp_list_schedule(MlpGroup& G, int pairs) {
   G.list_len = 0;
   if (W > kMaxListUnits || pairs > kMaxListPairs || pairs < 1) return;
   // the schedule depends only on the problem structure: reuse the last one when it matches
-  std::vector<int32_t> key = {pairs, gs.n_probs};
+  std::vector<int32_t> key = {pairs, gs.n_probs, G.flags};
   for (int q = 0; q < gs.n_probs; ++q) {
     key.insert(key.end(), {gs.tile_begin[q + 1], G.probs[q].k_steps, G.probs[q].kind, G.probs[q].n_tiles});
     for (int d = 0; d < kMaxDeps; ++d) key.insert(key.end(), {gs.dep_prob[q][d], gs.dep_mode[q][d]});
@@ -663,9 +833,17 @@ void mlp_list_schedule(MlpGroup& G, int pairs) {
       }
       int best = 0;
       double best_start = 1e30;
-      for (int c = 0; c < pairs; ++c) {
-        const double st = std::max(free_at[c], ready);
-        if (st < best_start - 1e-9) { best_start = st; best = c; }
+      const bool chained = G.probs[q].kind != kMlpUpd;
+      if ((G.flags & 64) && chained && p.m_tiles * p.n_tiles <= pairs) {
+        // affinity: tile t of every chained pass on pair t (its first k-steps read the chunks
+        // that pair wrote in the previous pass)
+        best = rel;
+        best_start = std::max(free_at[best], ready);
+      } else {
+        for (int c = 0; c < pairs; ++c) {
+          const double st = std::max(free_at[c], ready);
+          if (st < best_start - 1e-9) { best_start = st; best = c; }
+        }
       }
       const double main_end = best_start + p.k_steps * kStep;
       free_at[best] = main_end;
@@ -704,11 +882,12 @@ int launch_mlp_group(const MlpGroup& Gin, cudaStream_t stream) {
   }
   static MlpGroup G;
   G = Gin;
-  if (Gin.cluster != 4 || !even) return launch_mlp_t<2>(G, stream);
+  if (Gin.tf32) return launch_mlp_t<2, true>(G, stream);
+  if (Gin.cluster != 4 || !even) return launch_mlp_t<2, false>(G, stream);
   // two pairs per cluster: work units are pairs of adjacent column tiles
   for (int q = 0; q < gs.n_probs; ++q)
     G.sched.tile_begin[q + 1] = G.sched.tile_begin[q] + G.probs[q].m_tiles * G.probs[q].n_tiles / 2;
-  return launch_mlp_t<4>(G, stream);
+  return launch_mlp_t<4, false>(G, stream);
 }
 
 }  // namespace brk

@@ -25,20 +25,22 @@ enum MlpKind : int32_t {
   kMlpUpd = 4,      // dW = acc -> out (fp32); w_next = w - lr dW -> aux; db = sum of partials
 };
 
-// One problem of the step.  Operand k-step s of a tile in row block `row`
-// (A: the CTA's 128-row block, B: its 64-row block) is the 4-d TMA box at
-//   (0, 0, rc2 * row + kc2 * s, rc3 * row + kc3 * s)
-// of map_a / map_b (the blocked FC layouts of brk_fc.cu).
+// One problem of the step (A: the CTA's 128-row block, B: its 64-row block, in the blocked FC
+// layouts of brk_fc.cu).  fp32 storage (TF32 step): every map is fp32 and every side / output
+// box is 32 columns (128 B) wide, two per warp.
 struct MlpProb {
   CUtensorMap map_a;
   CUtensorMap map_b;
-  CUtensorMap map_out;  // bf16 activations: box (64, 32, 1, 1); fp32 dW: box (32, 32, 1, 1)
+  CUtensorMap map_out;  // bf16 activations: box (64, 32, 1, 1); fp32 (dW, TF32 step): box (32, 32, 1, 1)
   CUtensorMap map_in;   // dy (top) / ReLU mask (bwd) / old weights (upd): box (64, 32, 1, 1)
   CUtensorMap map_aux;  // dz_L (top) / new weights (upd): box (64, 32, 1, 1)
   int32_t kind;         // MlpKind
   int32_t m_tiles, n_tiles, k_steps;
-  int32_t a_rc2, a_rc3, a_kc2, a_kc3;
-  int32_t b_rc2, b_rc3, b_kc2, b_kc3;
+  // operand box of k-step s for row block `row`: coordinate d = rc[d] * row + k0[d] * d0 +
+  // k1[d] * d1 with (d0, d1) = (s, 0) for bf16 (4-d maps) and (s % 2, s / 2) for TF32 (5-d
+  // maps of 32-element halves, brk_fc.cu split_layout)
+  int32_t a_rc[5], a_k0[5], a_k1[5];
+  int32_t b_rc[5], b_k0[5], b_k1[5];
   int32_t a_mn, b_mn;   // MN-major operand (UMMA descriptor / idesc)
   int32_t cols;         // output columns (row length of colsum_ws)
   int32_t has_in;       // the epilogue loads map_in
@@ -67,6 +69,7 @@ struct MlpGroup {
   int32_t flags;
   // CTAs per cluster: 2 (one pair) or 4 (two pairs sharing the A operand by TMA multicast)
   int32_t cluster;
+  int32_t tf32;  // fp32 storage, kind::tf32 MMAs (k-steps of 32 elements)
   // list schedule (cluster == 2): CTA pair c runs units list[list_off[c] .. list_off[c+1]) in
   // that order (each list increasing: every unit waits only on units of lower index, so the
   // lists cannot deadlock); list_len == 0: round robin (pair c runs c, c + pairs, ...)

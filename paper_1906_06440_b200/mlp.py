@@ -315,8 +315,11 @@ class MLP:
 class MlpTF32:
     """The same MLP training step with the reference's own fp32 storage and TF32
     tensor-core math (north_star "bf16 and TF32 inputs"): activations, weights
-    and gradients fp32 in HBM, every GEMM on the engine's TF32 path (32-element
-    fp32 atoms, 128B swizzle).  One step = 4L + 1 + L native launches:
+    and gradients fp32 in HBM.  By default the whole step is ONE persistent launch
+    of the fused step kernel in its TF32 variant (``brk_mlp_step_dt`` with
+    BRK_F32: kind::tf32 MMAs on 32-element fp32 atoms, fp32 epilogues in 32-column
+    TMA boxes, double-buffered weights).  ``BRK_MLP_FUSED=0`` runs the per-pass
+    path, every GEMM on the engine's TF32 path, 4L + 1 + L native launches:
 
         fwd   y_l = relu(W_l y_{l-1} + b_l)                 brk_fc_fwd(F32)
         top   dz_L = dy * (y_L > 0), db_L, b_L -= lr db_L    brk_fc_bias_grad_dt(F32)
@@ -353,6 +356,20 @@ class MlpTF32:
         upd_bytes = max(int(lib.brk_fc_upd_workspace(batch, width, width)), 16)
         self.upd_ws = [torch.zeros(upd_bytes, dtype=torch.uint8, device=device) for _ in range(layers)]
         self.launches_per_step = 0
+        import ctypes
+        import os
+
+        self.fused = (os.environ.get("BRK_MLP_FUSED", "1") != "0" and layers <= 4
+                      and width % 256 == 0 and batch % 256 == 0)
+        if self.fused:
+            # double-buffered weights (the step writes W - lr dW to the other buffer)
+            self._wbuf = [self.w, [w.clone() for w in self.w]]
+            self._cur = 0
+            arr = lambda ts: (ctypes.c_void_p * len(ts))(*[t.data_ptr() for t in ts])  # noqa: E731
+            self._tables = [(arr(self.y), arr(self.dz), arr(self._wbuf[c]), arr(self._wbuf[1 - c]), arr(self.bias),
+                             arr(self.dw), arr(self.db), arr(self.colsum)) for c in (0, 1)]
+            self.step_ws = torch.zeros(max(int(lib.brk_mlp_step_workspace_bytes(layers, batch, width)), 16),
+                                       dtype=torch.uint8, device=device)
 
     def load_input(self, x, dy) -> None:
         self.y[0].copy_(x, non_blocking=True)
@@ -362,6 +379,14 @@ class MlpTF32:
         torch, lib, n, c, L, lr = self.torch, self.lib, self.N, self.C, self.L, self.lr
         s = torch.cuda.current_stream().cuda_stream if stream is None else stream
         F = _lib.BRK_F32
+        if self.fused:
+            y, dz, w, w_next, b, dw, db, cs = self._tables[self._cur]
+            _lib.check(lib.brk_mlp_step_dt(L, n, c, y, dz, self.dy.data_ptr(), w, w_next, b, dw, db, cs, lr,
+                                           self.step_ws.data_ptr(), self.step_ws.numel(), F, s), RuntimeError)
+            self._cur ^= 1
+            self.w = self._wbuf[self._cur]
+            self.launches_per_step = 1
+            return 1
         chk = lambda rc: _lib.check(rc, RuntimeError)  # noqa: E731
         for l in range(L):
             chk(lib.brk_fc_fwd(self.y[l].data_ptr(), self.w[l].data_ptr(), self.bias[l].data_ptr(),

@@ -470,7 +470,7 @@ if __name__ == "__main__":
 
 def mlp_tf32_suite(layers=4, width=1024, batch=2048, iters=10):
     """BASELINE config 2 with the reference's fp32 storage and TF32 math (MlpTF32):
-    whole step (4L+1+L native launches) captured in one CUDA graph, L2 flushed
+    whole step (one fused persistent launch, or 4L+1+L with BRK_MLP_FUSED=0) captured in a CUDA graph, L2 flushed
     between steps; TFLOP/s against the TF32 dense peak."""
     import torch
 
