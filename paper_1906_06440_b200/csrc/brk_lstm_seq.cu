@@ -33,9 +33,11 @@ namespace brk {
 namespace {
 
 // A ring of 4 stages of 32 KB (two 128-row M tiles); each receives only the operand's N valid
-// rows (rounded to 8-row swizzle atoms).  Measured and rejected: 6 stages with 6 producer warps
-// (forward step 9.6 -> 11.7 us, backward 14.8 -> 15.8 us) and stages packed to the valid rows
-// (forward 11.3 us): the chunk stream is not bound by the bytes in flight.
+// rows (rounded to 8-row swizzle atoms).  The forward chunk stream (16 chunks, ~5 us per step)
+// is neither bound by bytes (streaming all 256 rows: same time), nor by the ring depth (6
+// stages: 10.4 us per step vs 9.7), nor by the cluster multicast (cluster sizes 1..8 equal,
+// BRK_LSTM_CS), nor by serial release polls (polling a producer's chunks of a step together:
+// 11.3 us, the first chunk waits for the last).
 constexpr int kStagesS = 4;
 constexpr int kThreadsS = 9 * 32;    // 4 epilogue, 1 MMA, 4 producer warps (one per stage)
 constexpr int kJf = 8;               // forward: hidden units per CTA
@@ -678,7 +680,8 @@ BRK_API int brk_lstm_seq_fwd(const float* gx, const void* r_cat, const float* s0
   cfg.numAttrs = 1;
   // largest cluster (<= 8, dividing the grid) whose clusters are all co-resident:
   // the CTAs wait on each other's chunks, so the whole grid must be resident
-  int cs = 8;
+  const char* cs_env = std::getenv("BRK_LSTM_CS");  // tuning: largest cluster size to try
+  int cs = cs_env != nullptr ? std::max(1, std::min(8, std::atoi(cs_env))) : 8;
   for (; cs >= 1; cs /= 2) {
     if ((K / kJf) % cs) continue;
     attr[0].val.clusterDim.x = cs;
