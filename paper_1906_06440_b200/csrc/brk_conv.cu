@@ -184,8 +184,17 @@ __global__ void __launch_bounds__(256) split_reduce_kernel(const float4* __restr
   pdl_wait();
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    // the slices' loads are issued eight at a time (independent), the adds stay in split order
     float4 a = __ldcs(ws + i);
-    for (int s = 1; s < splits; ++s) {
+    int s = 1;
+    for (; s + 8 <= splits; s += 8) {
+      float4 b[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) b[j] = __ldcs(ws + (s + j) * n4 + i);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) { a.x += b[j].x; a.y += b[j].y; a.z += b[j].z; a.w += b[j].w; }
+    }
+    for (; s < splits; ++s) {
       const float4 b = __ldcs(ws + s * n4 + i);
       a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
     }
@@ -390,6 +399,46 @@ BRK_API int brk_conv_upd(const void* in, const void* dout, float* dw, void* w_sg
   const int64_t atoms = static_cast<int64_t>(C / kB) * R * S;
   EngineParams p;
   init_params(p);
+  // 1x1 stride-1 convolutions: tile-mode boxes of 64 pixels x 64 channels per image (k-steps
+  // aligned to images, the tail of an image's last box zero-filled out of bounds) instead of the
+  // im2col pixel walk: im2col-mode boxes streamed at ~28 B/clk per SM (tools/probes/
+  // engine_waits.py), tile-mode boxes at the ~70 B/clk chip limit (brk_diag_tma_lanes)
+  static const char* tile_env = std::getenv("BRK_CONV_UPD_TILE");
+  const bool tile_upd = R == 1 && S == 1 && stride == 1 && pad_h == 0 && pad_w == 0 &&
+                        !(tile_env != nullptr && std::atoi(tile_env) == 0);
+  if (tile_upd) {
+    const int64_t hw = static_cast<int64_t>(H) * W;
+    const int kpi = static_cast<int>((hw + 63) / 64);  // k-steps per image
+    auto map3 = [&](CUtensorMap* m, const void* ptr, int X) {
+      const uint64_t dims[3] = {kB, static_cast<uint64_t>(hw), static_cast<uint64_t>(N) * (X / kB)};
+      const uint64_t strides[3] = {1, kB, static_cast<uint64_t>(hw) * kB};
+      const uint32_t box[3] = {kB, 64, 1};
+      return encode_tmap(m, ptr, true, 3, dims, strides, box);
+    };
+    if ((rc = map3(&p.map_a, in, C)) || (rc = map3(&p.map_b, dout, K))) return rc;
+    // k-step s = (image n = s / kpi, pixel block j = s % kpi): coordinate (0, 64 j, n * X_b + block)
+    for (OperandCoords* oc : {&p.ca, &p.cb}) {
+      oc->kdiv0 = kpi;
+      oc->kdiv1 = 1 << 30;
+      oc->kc[0][1] = 64;
+      oc->lc[2] = 1;
+      oc->load_bytes = 64 * 128;
+      oc->mn_major = 1;
+      oc->ndims = 3;
+      oc->kind = 0;
+    }
+    p.ca.kc[1][2] = C / kB;
+    p.ca.rc[2] = 2;  // the CTA's 128 rows: 2 channel blocks (1 when C = 64: rows 64.. are masked)
+    p.ca.n_loads = std::min(2, C / kB);
+    p.cb.kc[1][2] = K / kB;
+    p.cb.rc[2] = brows / kB;
+    p.cb.n_loads = brows / kB;
+    p.k_steps = N * kpi;
+    if (pl.splits > 1) {  // re-plan the split count for the image-aligned k-steps
+      const int per = (p.k_steps + pl.splits - 1) / pl.splits;
+      pl.splits = (p.k_steps + per - 1) / per;
+    }
+  } else {
   // A: input pixels (K side, 64 per step) as 2 MN-major atoms (c_b, rs) of 64 channels
   if ((rc = im2col_map(&p.map_a, in, N, C, H, W, R, S, stride, pad_h, pad_w, 64))) return rc;
   p.ca.n_loads = 2;
@@ -406,9 +455,10 @@ BRK_API int brk_conv_upd(const void* in, const void* dout, float* dw, void* w_sg
   p.cb.load_bytes = 64 * 128;
   p.cb.mn_major = 1;
   pixel_walk(p.cb, 3, g.P, g.Q, 1, 0, 0, pix);
+  p.k_steps = static_cast<int>((pix + 63) / 64);
+  }
   p.m_tiles = static_cast<int>((atoms * kB + (pl.pair ? 255 : 127)) / (pl.pair ? 256 : 128));
   p.n_tiles = K / pl.bn;
-  p.k_steps = static_cast<int>((pix + 63) / 64);
   p.rows = static_cast<int>(atoms * kB);
   p.cols = K;
   p.out_bf16 = 0;

@@ -49,6 +49,35 @@ __global__ void __launch_bounds__(256, 1) tma_bw_kernel(const __grid_constant__ 
   }
 }
 
+// One producer warp whose first `lanes` lanes each issue one box per round (round r fills
+// slot r % 2 of every lane; a lane re-fills its slot after the slot's previous box landed):
+// does issuing from several lanes of one warp keep several boxes in flight?
+__global__ void __launch_bounds__(32, 1) tma_bw_lanes_kernel(const __grid_constant__ CUtensorMap map, int iters,
+                                                             int lanes, int box_rows, int rows, int cols) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int slot_bytes = box_rows * 128;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * lanes * slot_bytes);
+  const int lane = threadIdx.x;
+  if (lane < 2 * lanes) mbar_init(&bars[lane], 1);
+  fence_barrier_init();
+  __syncwarp();
+  const int row_blocks = rows / box_rows, col_blocks = cols / 64;
+  int k = blockIdx.x * 7919 + lane * 131;
+  if (lane < lanes) {
+    for (int i = 0; i < iters; ++i) {
+      const int s = i & 1;
+      uint64_t* b = &bars[lane * 2 + s];
+      if (i >= 2) mbar_wait(b, ((i >> 1) - 1) & 1);
+      mbar_arrive_expect_tx(b, slot_bytes);
+      const int32_t c[2] = {(k % col_blocks) * 64, ((k / col_blocks) % row_blocks) * box_rows};
+      ++k;
+      tma_load<2>(smem + (lane * 2 + s) * slot_bytes, &map, b, c);
+    }
+    for (int i = iters; i < iters + 2; ++i) mbar_wait(&bars[lane * 2 + (i & 1)], ((i >> 1) - 1) & 1);
+  }
+}
+
 // 4 warps: each times `iters` x (tcgen05.ld 32x32b.x32 + wait) with clock64.
 __global__ void __launch_bounds__(128, 1) tmem_ld_kernel(int iters, long long* cycles, float* sink) {
   __shared__ uint32_t slot;
@@ -79,6 +108,35 @@ __global__ void __launch_bounds__(128, 1) tmem_ld_kernel(int iters, long long* c
 }  // namespace brk
 
 using namespace brk;
+
+extern "C" BRK_API int brk_diag_tma_lanes(const void* buf, int rows, int cols, int box_rows, int lanes, int ctas, int iters,
+                               float* us, double* bytes) {
+  if (lanes < 1 || lanes > 16 || box_rows < 8 || box_rows > 256 || rows % box_rows || cols % 64)
+    return set_error(BRK_ERR_CONTRACT, "diag_tma_lanes: bad shape");
+  CUtensorMap map;
+  const uint64_t dims[2] = {static_cast<uint64_t>(cols), static_cast<uint64_t>(rows)};
+  const uint64_t strides[2] = {1, static_cast<uint64_t>(cols)};
+  const uint32_t box[2] = {64, static_cast<uint32_t>(box_rows)};
+  int rc = encode_tmap(&map, buf, true, 2, dims, strides, box);
+  if (rc) return rc;
+  const int smem = 2 * lanes * box_rows * 128 + 1024 + 256;
+  cudaFuncSetAttribute(tma_bw_lanes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  tma_bw_lanes_kernel<<<ctas, 32, smem>>>(map, iters, lanes, box_rows, rows, cols);
+  cudaEventRecord(e0);
+  tma_bw_lanes_kernel<<<ctas, 32, smem>>>(map, iters, lanes, box_rows, rows, cols);
+  cudaEventRecord(e1);
+  cudaError_t err = cudaEventSynchronize(e1);
+  if (err != cudaSuccess) return set_cuda_error(err, "diag_tma_lanes");
+  cudaEventElapsedTime(us, e0, e1);
+  *us *= 1000.0f;
+  *bytes = static_cast<double>(ctas) * iters * lanes * box_rows * 128;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return BRK_OK;
+}
 
 BRK_API int brk_diag_tmem_ld(int ctas, int iters, long long* cycles_dev, float* sink_dev) {
   tmem_ld_kernel<<<ctas, 128>>>(iters, cycles_dev, sink_dev);
