@@ -128,13 +128,17 @@ def test_fused_step_matches_per_pass_launches(monkeypatch):
 
 
 
+@pytest.mark.parametrize("fused", ["1", "0"])
 @pytest.mark.parametrize("layers,width,batch", [(2, 256, 256), (4, 1024, 2048)])
-def test_mlp_tf32_step_matches_oracle(layers, width, batch):
-    """The fp32-storage TF32 step (MlpTF32) at the north-star TF32 tolerance (1e-3)."""
+def test_mlp_tf32_step_matches_oracle(layers, width, batch, fused, monkeypatch):
+    """The fp32-storage TF32 step (MlpTF32) at the north-star TF32 tolerance (1e-3): the fused
+    persistent launch (brk_mlp_step_dt, BRK_F32) and the per-pass launches."""
     from paper_1906_06440_b200.mlp import MlpTF32
 
+    monkeypatch.setenv("BRK_MLP_FUSED", fused)
     lr = 0.05
     mlp = MlpTF32(layers=layers, width=width, batch=batch, lr=lr, seed=1)
+    assert mlp.fused == (fused == "1")
     g = torch.Generator(device="cpu").manual_seed(2)
     x = torch.rand(batch, width, generator=g) * 2 - 1
     dy = torch.rand(batch, width, generator=g) * 2 - 1
@@ -143,7 +147,7 @@ def test_mlp_tf32_step_matches_oracle(layers, width, batch):
     mlp.load_input(blk(x).cuda(), blk(dy).cuda())
     mlp.step()
     torch.cuda.synchronize()
-    case = f"{layers}x{width} N={batch}"
+    case = f"{layers}x{width} N={batch} {'fused' if fused == '1' else 'per-pass'}"
     fwd = orc.mlp_step_reference(ws, bs, x.numpy(), dy.numpy(), lr=lr)
     gpu_y = [unblk(mlp.y[l]).cpu().numpy() for l in range(1, layers + 1)]
     ins = [x.numpy()] + gpu_y[:-1]
