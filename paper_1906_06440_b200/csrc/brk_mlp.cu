@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <vector>
 #include <cstdio>
+#include <cstdlib>
 
 #include "brk_internal.h"
 #include "brk_mlp.h"
@@ -802,6 +803,8 @@ void mlp_list_schedule(MlpGroup& G, int pairs) {
   if (W > kMaxListUnits || pairs > kMaxListPairs || pairs < 1) return;
   // the schedule depends only on the problem structure: reuse the last one when it matches
   std::vector<int32_t> key = {pairs, gs.n_probs, G.flags};
+  if (const char* env = std::getenv("BRK_MLP_SCHED"))
+    for (const char* c = env; *c; ++c) key.push_back(*c);
   for (int q = 0; q < gs.n_probs; ++q) {
     key.insert(key.end(), {gs.tile_begin[q + 1], G.probs[q].k_steps, G.probs[q].kind, G.probs[q].n_tiles});
     for (int d = 0; d < kMaxDeps; ++d) key.insert(key.end(), {gs.dep_prob[q][d], gs.dep_mode[q][d]});
@@ -814,8 +817,11 @@ void mlp_list_schedule(MlpGroup& G, int pairs) {
     G.list_len = static_cast<int32_t>(last_list.size());
     return;
   }
-  constexpr double kStep = 0.175, kHandoff = 1.3;
+  double kStep = 0.175, kHandoff = 1.3, epi_scale = 1.0;
+  if (const char* env = std::getenv("BRK_MLP_SCHED"))  // tuning: "step_us:handoff_us:epilogue_scale"
+    std::sscanf(env, "%lf:%lf:%lf", &kStep, &kHandoff, &epi_scale);
   double epi[5] = {1.4, 2.1, 1.7, 1.2, 2.5};  // by MlpKind
+  for (double& e : epi) e *= epi_scale;
   std::vector<double> row_done(static_cast<size_t>(gs.n_probs) * 64, 0.0), prob_done(gs.n_probs, 0.0);
   std::vector<double> free_at(pairs, 0.0);
   std::vector<std::vector<int16_t>> lists(pairs);
