@@ -38,6 +38,8 @@ import os
 lag = int(os.environ.get("BRK_MLP_UPD_LAG", "1"))
 names = ["fwd1", "fwd2", "fwd3", "fwd4"]
 order = os.environ.get("BRK_MLP_ORDER")
+if not order and "BRK_MLP_UPD_LAG" not in os.environ:  # the default chain-first order (brk_fc.cu)
+    order = "b4b3b2u4u3u2u1b1"
 if order:
     names += [("bwd" if order[i] == "b" else "upd") + order[i + 1] for i in range(0, len(order), 2)]
 else:
