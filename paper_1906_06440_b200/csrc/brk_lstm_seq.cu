@@ -319,8 +319,8 @@ __global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_fwd_kernel(const __grid
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (threadIdx.x == 0) {
         SEQ_TS(t, 5);  // epilogue done
-        __threadfence();
-        atomicAdd(&p.flags[(j0 / 64) * kFlagStride], 1u);
+        // release (acq_rel fence + relaxed add) rather than an SC fence + atomic
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&p.flags[(j0 / 64) * kFlagStride]) : "memory");
       }
       // off the critical path: fp32 h, s and the activated gates (BPTT inputs)
 #pragma unroll
@@ -583,10 +583,13 @@ __global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_bwd_kernel(const __grid
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (threadIdx.x == 0) {
         if (t < p.T - 1) SEQ_TS(it - 1, 6);
-        __threadfence();
-        // this CTA wrote rows of its quarter for units u0..u0+31 of all four gates
+        // this CTA wrote rows of its quarter for units u0..u0+31 of all four gates: one release
+        // fence, then relaxed adds (rather than an SC fence + atomics)
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
 #pragma unroll
-        for (int gg = 0; gg < 4; ++gg) atomicAdd(&p.flags[((gg * p.K + u0) / 64) * kFlagStride], 1u);
+        for (int gg = 0; gg < 4; ++gg)
+          asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(&p.flags[((gg * p.K + u0) / 64) * kFlagStride])
+                       : "memory");
       }
       if (t < p.T - 1) {
         __syncwarp();
