@@ -193,6 +193,16 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
     fence_barrier_init();
   }
   if (warp == kMmaWarp) tmem_alloc(tmem_slot, 2 * kCols);
+  // Small blocks (one K chunk per entry, k <= 64, bf16 gathers): the gather copies only each
+  // entry's valid rows / chunks.  The ring starts zeroed, the MMA B operand's K-rows past k are
+  // never written (stay zero), so stale A chunks past k multiply zeros; rows / columns past the
+  // block only feed accumulator rows / columns the epilogue does not store.
+  const bool sparse = !kTF32 && !p.tma && p.in_bf16 && n_chunks == 1;
+  if (sparse) {
+    for (int i = tid; i < kRingBytes / 16; i += kThreads)
+      asm volatile("st.shared.v4.b32 [%0], {%1, %1, %1, %1};" ::"r"(smem_u32(smem) + i * 16), "r"(0u) : "memory");
+    fence_proxy_async_smem();
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -368,8 +378,11 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
         const bool fast_a = !kTF32 && bf16_in && a_vec;
         const bool fast_b = !kTF32 && bf16_in && b_vec;
         // A operand (K-major) <- reference b block rows: (row r, 16 B chunk c) along k
-        for (int u = gt; u < n_rows8 * 8; u += kGatherWarps * 32) {
-          const int c = u & 7, r = u >> 3;
+        // (sparse: only the n_here rows x chunks holding k)
+        const int a_cpr = sparse ? (k_here + kE - 1) / kE : 8;
+        const int a_units = sparse ? n_here * a_cpr : n_rows8 * 8;
+        for (int u = gt; u < a_units; u += kGatherWarps * 32) {
+          const int r = sparse ? u / a_cpr : u >> 3, c = sparse ? u - r * a_cpr : u & 7;
           const int kk = c * kE;
           if (fast_a) {
             const int bytes = r < n_here ? max(0, min(16, (k_here - kk) * 2)) : 0;
@@ -400,8 +413,11 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
             *reinterpret_cast<uint4*>(b_op + i * 128 + ((c ^ (i & 7)) << 4)) = v;
           }
         } else {
-          for (int u = gt; u < kKC * col_chunks; u += kGatherWarps * 32) {
-            const int kr = u / col_chunks, c = u - kr * col_chunks;
+          // (sparse: only the k_here K-rows x chunks holding m)
+          const int b_cpr = sparse ? (m_here + kE - 1) / kE : col_chunks;
+          const int b_units = sparse ? k_here * b_cpr : kKC * col_chunks;
+          for (int u = gt; u < b_units; u += kGatherWarps * 32) {
+            const int kr = u / b_cpr, c = u - kr * b_cpr;
             const int col = c * kE;
             const int atom = c / (kAtomCols / kE), cc = c % (kAtomCols / kE);
             if (fast_b) {
