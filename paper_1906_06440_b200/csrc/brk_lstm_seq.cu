@@ -355,6 +355,193 @@ __global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_fwd_kernel(const __grid
   }
 }
 
+// ------------------------------------------------------------------ forward, CTA pairs
+// A CTA pair (cta_group::2, M = 256) owns kUpp = 16 hidden units of all four gates (MMA N = 64
+// gate columns, column n = gate * 16 + unit): CTA rank r keeps the B rows of gates 2r, 2r + 1
+// resident and streams only its half of the batch rows of h_{t-1} (rows_half, rounded to 8).
+// Per chunk and SM that is 11 KB of TMA writes + 16 KB of A and 4 KB of B MMA reads instead of
+// 24 + 32 + 8 KB for a single CTA's two 128-row M tiles — the single-CTA chunk stream is bound
+// by shared-memory bandwidth (computing only the first M tile: 5.0 -> 3.7 us per step).
+constexpr int kUpp = 16;
+__global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_fwd_pair_kernel(const __grid_constant__ SeqParams p) {
+  constexpr int kGN = 4 * kUpp;   // 64 gate columns per pair
+  constexpr int kBRows = kGN / 2; // 32 B rows per CTA
+  constexpr int kStageA = 16384;  // one CTA's A stage: 128 rows x 128 B (rows_half of them loaded)
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int KC = p.K / 64;
+  constexpr int NS = kStagesS;
+  uint8_t* ring = smem;
+  uint8_t* wsm = smem + NS * kStageA;  // resident B: KC chunks x 32 rows x 128 B
+  uint64_t* full = reinterpret_cast<uint64_t*>(wsm + KC * kBRows * 128);
+  uint64_t* empty = full + kStagesS;
+  uint64_t* tfull = empty + kStagesS;
+  uint64_t* tempty = tfull + 1;
+  uint64_t* wbar = tempty + 1;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(wbar + 1);
+  const int warp = warp_id(), lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int j0 = (blockIdx.x >> 1) * kUpp;  // the pair's first hidden unit
+  const int rows_half = p.slice;            // batch rows per CTA (multiple of 8, <= 128)
+  const int row_base = static_cast<int>(rank) * rows_half;
+  const int chunk_owners = 2 * (64 / kUpp);  // CTAs writing one 64-column chunk of h
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 8);  // the 4 epilogue warps of both CTAs (on the leader)
+    mbar_init(wbar, 1);
+    fence_barrier_init();
+  }
+  if (warp == 4) tmem_alloc_pair(tslot, 64);
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp >= 5) {
+    // ---------------------------------------------------------------- producers
+    const int pid = warp - 5;
+    if (elect_one()) {
+      if (pid == 0) {  // resident B rows of gates 2r, 2r + 1: row gg*16 + uu <- R_cat[(2r + gg) K + j0 + uu]
+        // (both CTAs' rows complete on the leader's barrier: its MMAs read both)
+        if (leader) mbar_arrive_expect_tx(wbar, 2 * KC * kBRows * 128);
+        for (int kc = 0; kc < KC; ++kc)
+          for (int gg = 0; gg < 2; ++gg) {
+            const int32_t c[2] = {kc * 64, (2 * static_cast<int>(rank) + gg) * p.K + j0};
+            tma_load_pair<2>(wsm + kc * kBRows * 128 + gg * kUpp * 128, &p.map_w, wbar, c);
+          }
+      }
+      const int total = p.T * KC;
+      for (int gi = pid; gi < total; gi += NS) {
+        const int t = gi / KC, kc = gi - t * KC;
+        const uint32_t ph = (gi / NS) & 1;
+        if (t > 0) {
+          while (ld_acquire(&p.flags[kc * kFlagStride]) < static_cast<unsigned>(chunk_owners * t)) poll_backoff();
+          fence_proxy_async_global();
+        }
+        if (kc == 0) SEQ_TS(t, 0);
+        if (kc == KC - 1) SEQ_TS(t, 1);
+        mbar_wait(&empty[pid], ph ^ 1);  // both CTAs' MMAs of the previous round on this stage done
+        if (leader) mbar_arrive_expect_tx(&full[pid], static_cast<uint32_t>(2 * rows_half * 128));
+        const int32_t c[3] = {kc * 64, row_base, t};
+        tma_load_pair<3>(ring + pid * kStageA, &p.map_a, &full[pid], c);
+      }
+    }
+  } else if (warp == 4) {
+    // ---------------------------------------------------------------- MMA issuer (leader)
+    if (leader) {
+      const uint32_t idesc = make_idesc(kFmtBF16, 256, kGN, 0, 0);
+      mbar_wait(wbar, 0);
+      for (int t = 0; t < p.T; ++t) {
+        mbar_wait(tempty, (t & 1) ^ 1);
+        tc_fence_after();
+        for (int kc = 0; kc < KC; ++kc) {
+          const int gi = t * KC + kc, st = gi % NS;
+          mbar_wait(&full[st], (gi / NS) & 1);
+          tc_fence_after();
+          if (lane == 0 && kc == 0) SEQ_TS(t, 2);
+          if (lane == 0 && kc == KC - 1) SEQ_TS(t, 3);
+          if (elect_one()) {
+            const uint32_t a0 = smem_u32(ring + st * kStageA);
+            const uint32_t b0 = smem_u32(wsm + kc * kBRows * 128);
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              mma_ss_pair<false>(tmem, make_smem_desc(a0 + kk * 32, 16, 1024, kSwizzle128B),
+                                 make_smem_desc(b0 + kk * 32, 16, 1024, kSwizzle128B), idesc, (kc | kk) ? 1u : 0u);
+            mma_commit_pair(&empty[st]);
+            if (kc == KC - 1) mma_commit_pair(tfull);
+          }
+          __syncwarp();
+        }
+      }
+    }
+  } else {
+    // ---------------------------------------------------------------- epilogue (warps 0-3)
+    const int li = warp * 32 + lane;  // TMEM lane = this CTA's A row
+    const int n = row_base + li;
+    const bool ok = li < rows_half && n < p.N;
+    const uint32_t tempty_leader = mapa_shared(smem_u32(tempty), 0);
+    float sreg[kUpp];
+#pragma unroll
+    for (int uu = 0; uu < kUpp; ++uu) sreg[uu] = (p.s0 != nullptr && ok) ? p.s0[static_cast<int64_t>(n) * p.K + j0 + uu] : 0.0f;
+    for (int t = 0; t < p.T; ++t) {
+      float pre[4][kUpp];
+      if (ok) {
+        const float* gxr = p.gx + (static_cast<int64_t>(t) * p.N + n) * 4 * p.K + j0;
+#pragma unroll
+        for (int g = 0; g < 4; ++g)
+#pragma unroll
+          for (int q4 = 0; q4 < kUpp / 4; ++q4) {
+            const float4 a = __ldcs(reinterpret_cast<const float4*>(gxr + g * p.K + 4 * q4));
+            pre[g][4 * q4] = a.x; pre[g][4 * q4 + 1] = a.y; pre[g][4 * q4 + 2] = a.z; pre[g][4 * q4 + 3] = a.w;
+          }
+      }
+      mbar_wait(tfull, t & 1);
+      tc_fence_after();
+      if (threadIdx.x == 0) SEQ_TS(t, 4);
+      uint32_t v[64];
+      tmem_ld64(tmem + (static_cast<uint32_t>(warp * 32) << 16), v);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster_relaxed(tempty_leader);  // accumulator free for step t + 1
+      float hv[kUpp];
+      if (ok) {
+#pragma unroll
+        for (int uu = 0; uu < kUpp; ++uu) {
+          const float gi = sigm_s(pre[0][uu] + __uint_as_float(v[uu]));
+          const float gc = tanh_f(pre[1][uu] + __uint_as_float(v[kUpp + uu]));
+          const float gf = sigm_s(pre[2][uu] + __uint_as_float(v[2 * kUpp + uu]));
+          const float go = sigm_s(pre[3][uu] + __uint_as_float(v[3 * kUpp + uu]));
+          const float sv = gf * sreg[uu] + gi * gc;
+          sreg[uu] = sv;
+          hv[uu] = go * tanh_f(sv);
+          pre[0][uu] = gi; pre[1][uu] = gc; pre[2][uu] = gf; pre[3][uu] = go;
+        }
+        uint4* hb = reinterpret_cast<uint4*>(p.h_bf + (static_cast<int64_t>(t + 1) * p.N + n) * p.K + j0);
+#pragma unroll
+        for (int q8 = 0; q8 < kUpp / 8; ++q8)
+          hb[q8] = make_uint4(pack_bf16x2(hv[8 * q8], hv[8 * q8 + 1]), pack_bf16x2(hv[8 * q8 + 2], hv[8 * q8 + 3]),
+                              pack_bf16x2(hv[8 * q8 + 4], hv[8 * q8 + 5]), pack_bf16x2(hv[8 * q8 + 6], hv[8 * q8 + 7]));
+      }
+      fence_proxy_async_global();  // h_t (bf16) is read by other CTAs' TMA (async proxy)
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (threadIdx.x == 0) {
+        SEQ_TS(t, 5);
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&p.flags[(j0 / 64) * kFlagStride]) : "memory");
+      }
+      // off the critical path: fp32 h, s and the activated gates (BPTT inputs)
+      if (ok) {
+        const int64_t row = static_cast<int64_t>(t) * p.N + n;
+        float* go_ = p.gates_out + row * 4 * p.K + j0;
+#pragma unroll
+        for (int g = 0; g < 4; ++g)
+#pragma unroll
+          for (int q4 = 0; q4 < kUpp / 4; ++q4)
+            __stcs(reinterpret_cast<float4*>(go_ + g * p.K + 4 * q4),
+                   make_float4(pre[g][4 * q4], pre[g][4 * q4 + 1], pre[g][4 * q4 + 2], pre[g][4 * q4 + 3]));
+        float* ho = p.h_out + row * p.K + j0;
+        float* so = p.s_out + row * p.K + j0;
+#pragma unroll
+        for (int q4 = 0; q4 < kUpp / 4; ++q4) {
+          __stcs(reinterpret_cast<float4*>(ho + 4 * q4), make_float4(hv[4 * q4], hv[4 * q4 + 1], hv[4 * q4 + 2], hv[4 * q4 + 3]));
+          __stcs(reinterpret_cast<float4*>(so + 4 * q4),
+                 make_float4(sreg[4 * q4], sreg[4 * q4 + 1], sreg[4 * q4 + 2], sreg[4 * q4 + 3]));
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  if (warp == 4) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem, 64);
+  }
+}
+
 // ------------------------------------------------------------------ backward
 // Cluster of 4 CTAs: rank g = gate.  Units u0 = 32 * cluster .. +31.
 __global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_bwd_kernel(const __grid_constant__ SeqParams p) {
@@ -611,6 +798,59 @@ __global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_bwd_kernel(const __grid
 
 unsigned long long* g_seq_ts = nullptr;
 
+// CTA-pair forward (lstm_seq_fwd_pair_kernel): K a multiple of 64, N <= 256; BRK_LSTM_PAIR=0
+// selects the single-CTA kernel
+bool use_fwd_pair(int N, int K) {
+  const char* env = std::getenv("BRK_LSTM_PAIR");
+  return !(env != nullptr && std::atoi(env) == 0) && K % 64 == 0 && N <= 256 && N >= 1;
+}
+int smem_fwd_pair(int K) { return kStagesS * 16384 + (K / 64) * (2 * kUpp) * 128 + 256 + 1024; }
+
+int launch_fwd_pair(SeqParams& p, void* h_bf, const void* r_cat, cudaStream_t st) {
+  const int N = p.N, K = p.K, T = p.T;
+  int rc;
+  p.slice = ((N + 1) / 2 + 7) / 8 * 8;  // batch rows per CTA of the pair
+  {
+    const uint64_t dims[3] = {(uint64_t)K, (uint64_t)N, (uint64_t)(T + 1)};
+    const uint64_t strides[3] = {1, (uint64_t)K, (uint64_t)N * K};
+    const uint32_t box[3] = {64, static_cast<uint32_t>(p.slice), 1};
+    if ((rc = encode_tmap(&p.map_a, h_bf, true, 3, dims, strides, box))) return rc;
+  }
+  {
+    const uint64_t dims[2] = {(uint64_t)K, (uint64_t)(4 * K)};
+    const uint64_t strides[2] = {1, (uint64_t)K};
+    const uint32_t box[2] = {64, static_cast<uint32_t>(kUpp)};
+    if ((rc = encode_tmap(&p.map_w, r_cat, true, 2, dims, strides, box))) return rc;
+  }
+  const int smem = smem_fwd_pair(K);
+  if (smem > 232448) return set_error(BRK_ERR_CONTRACT, "lstm seq fwd: K too large for the resident slice");
+  cudaError_t err = cudaFuncSetAttribute(lstm_seq_fwd_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (err != cudaSuccess) return set_cuda_error(err, "lstm seq fwd pair smem");
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * (K / kUpp));
+  cfg.blockDim = dim3(kThreadsS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  // the pairs wait on each other's chunks: the whole grid must be co-resident
+  int max_clusters = 0;
+  err = cudaOccupancyMaxActiveClusters(&max_clusters, lstm_seq_fwd_pair_kernel, &cfg);
+  if (err != cudaSuccess) return set_cuda_error(err, "lstm seq fwd pair occupancy");
+  if (max_clusters < K / kUpp) return set_error(BRK_ERR_CONTRACT, "lstm seq fwd pair: grid cannot be co-resident");
+  err = cudaMemsetAsync(p.flags, 0, static_cast<size_t>(4 * (K / 64) + 4) * kFlagStride * sizeof(unsigned), st);
+  if (err != cudaSuccess) return set_cuda_error(err, "lstm seq flags");
+  g_launches.fetch_add(1);
+  err = cudaLaunchKernelEx(&cfg, lstm_seq_fwd_pair_kernel, p);
+  return err == cudaSuccess ? BRK_OK : set_cuda_error(err, "lstm seq fwd pair launch");
+}
+
+
 // streamed rows per stage: N rounded up to whole 8-row swizzle atoms (forward: cs slices of
 // `slice` rows, slice = ceil(N / cs) rounded to 8)
 int rows_pad(int N) { return (N + 7) / 8 * 8; }
@@ -665,6 +905,7 @@ BRK_API int brk_lstm_seq_fwd(const float* gx, const void* r_cat, const float* s0
   p.flags = flags;
   p.ts = g_seq_ts;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (use_fwd_pair(N, K)) return launch_fwd_pair(p, h_bf, r_cat, st);
   // stages are 32 KB slots (cs slices of ceil(N / cs) rows rounded to 8 never exceed 256 rows)
   const int smem = kStagesS * 32768 + fixed_fwd(K);
   cudaError_t err = cudaFuncSetAttribute(lstm_seq_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
