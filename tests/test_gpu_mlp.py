@@ -219,3 +219,25 @@ def test_fused_step_deterministic_under_back_to_back_replays():
         now = m.dw + m.db + m.y[1:] + m.dz
         for a, b in zip(first, now):
             assert torch.equal(a, b), f"step {100 * (i + 1)}: fused step not reproducible"
+
+
+def test_fused_tf32_step_deterministic_under_back_to_back_launches():
+    """The TF32 variant of the fused step under the same protocol: with lr = 0 every step
+    repeats the same computation, so 2000 back-to-back launches must reproduce the first
+    step bit for bit."""
+    from paper_1906_06440_b200.mlp import MlpTF32
+
+    m = MlpTF32(layers=4, width=1024, batch=2048, lr=0.0, seed=0)
+    assert m.fused
+    g = torch.Generator(device="cpu").manual_seed(7)
+    m.load_input(blk(torch.rand(2048, 1024, generator=g) * 2 - 1).cuda(),
+                 blk(torch.rand(2048, 1024, generator=g) * 2 - 1).cuda())
+    m.step()
+    torch.cuda.synchronize()
+    first = [t.clone() for t in m.dw + m.db + m.y[1:] + m.dz]
+    for i in range(20):
+        for _ in range(100):
+            m.step()
+        torch.cuda.synchronize()
+        for a, b in zip(first, m.dw + m.db + m.y[1:] + m.dz):
+            assert torch.equal(a, b), f"step {100 * (i + 1)}: fused TF32 step not reproducible"
