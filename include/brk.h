@@ -338,6 +338,15 @@ BRK_API int brk_diag_tma_bw(const void* buf, int rows, int cols, int box_rows, i
 /* Diagnostic: subsequent engine launches record per-CTA %globaltimer phase
  * stamps into ts[8 * blockIdx.x + phase] (device buffer); NULL disables. */
 BRK_API void brk_diag_set_timestamps(unsigned long long* ts);
+/* Diagnostics: the host list schedule of the chain-first MLP step (brk_mlp_step) for L layers of
+ * width C, batch N over `pairs` CTA pairs: units[offsets[c] .. offsets[c+1]) is pair c's list,
+ * tiles[q] / dep[q] each problem's unit count and dependency; returns the unit count (0: none). */
+BRK_API int brk_diag_mlp_schedule(int L, int N, int C, int pairs, int16_t* units, int16_t* offsets, int* tiles,
+                                  int* dep);
+/* Diagnostic: TMA throughput when the first `lanes` lanes of ONE warp per CTA each keep two boxes
+ * (64 bf16 x box_rows) in flight; synchronous; device microseconds and bytes moved. */
+BRK_API int brk_diag_tma_lanes(const void* buf, int rows, int cols, int box_rows, int lanes, int ctas, int iters,
+                               float* us, double* bytes);
 /* Diagnostic: per-warp clock64 cycles of iters x (tcgen05.ld.32x32b.x32 + wait); synchronous. */
 BRK_API int brk_diag_tmem_ld(int ctas, int iters, long long* cycles_dev, float* sink_dev);
 

@@ -62,6 +62,8 @@ SIGNATURES: dict[str, tuple] = {
                                    _vp]),
     "brk_lstm_recurrent_grad": (_c_int, [_vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp]),
     "brk_diag_tmem_ld": (_c_int, [_c_int, _c_int, _vp, _vp]),
+    "brk_diag_tma_lanes": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _vp]),
+    "brk_diag_mlp_schedule": (_c_int, [_c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp]),
     "brk_diag_tma_bw": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int,
                                  ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_double)]),
     "brk_fc_bias_grad": (_c_int, [_vp, _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _c_f, _vp]),

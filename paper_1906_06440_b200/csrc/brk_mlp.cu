@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <vector>
 #include <cstdio>
+#include <cstring>
 #include <cstdlib>
 
 #include "brk_internal.h"
@@ -897,3 +898,45 @@ int launch_mlp_group(const MlpGroup& Gin, cudaStream_t stream) {
 }
 
 }  // namespace brk
+
+// Diagnostics / host test of the list scheduler (no GPU): the chain-first MLP step structure
+// of brk_mlp_step for L layers of width C and batch N (256 x 128 tiles), scheduled over `pairs`
+// CTA pairs.  Writes the pair lists (units[offsets[c] .. offsets[c+1]) for pair c), the unit
+// count per problem (tiles[q]) and each problem's dependency (dep[q], -1: none) and returns the
+// number of units (0: the schedule was not built).
+extern "C" BRK_API int brk_diag_mlp_schedule(int L, int N, int C, int pairs, int16_t* units, int16_t* offsets,
+                                             int* tiles, int* dep) {
+  using namespace brk;
+  if (L < 1 || 3 * L > kMaxProbs || N % 256 || C % 256 || pairs < 1 || pairs > kMaxListPairs) return 0;
+  static MlpGroup G;
+  std::memset(&G, 0, sizeof(G));
+  GroupSched& gs = G.sched;
+  int q = 0;
+  auto add = [&](int kind, int m_tiles, int n_tiles, int k_steps, int d, int mode) {
+    MlpProb& p = G.probs[q];
+    p.kind = kind;
+    p.m_tiles = m_tiles;
+    p.n_tiles = n_tiles;
+    p.k_steps = k_steps;
+    for (int j = 0; j < kMaxDeps; ++j) gs.dep_prob[q][j] = -1;
+    gs.dep_prob[q][0] = d;
+    gs.dep_mode[q][0] = mode;
+    gs.tile_begin[q + 1] = gs.tile_begin[q] + m_tiles * n_tiles;
+    return q++;
+  };
+  int fwd[8], bwd[8];
+  for (int l = 0; l < L; ++l) fwd[l] = add(l == L - 1 ? kMlpFwdTop : kMlpFwd, N / 256, C / 128, C / 64, l ? fwd[l - 1] : -1, 2);
+  for (int l = L; l >= 2; --l) bwd[l] = add(kMlpBwd, N / 256, C / 128, C / 64, l == L ? fwd[L - 1] : bwd[l + 1], 2);
+  for (int l = L; l >= 1; --l) add(kMlpUpd, C / 256, C / 128, N / 64, l == L ? fwd[L - 1] : bwd[l + 1], 1);
+  add(kMlpBwdPlain, N / 256, C / 128, C / 64, L >= 2 ? bwd[2] : fwd[L - 1], 2);
+  gs.n_probs = q;
+  mlp_list_schedule(G, pairs);
+  if (G.list_len == 0) return 0;
+  for (int i = 0; i <= pairs; ++i) offsets[i] = G.list_off[i];
+  for (int i = 0; i < G.list_len; ++i) units[i] = G.list[i];
+  for (int i = 0; i < q; ++i) {
+    tiles[i] = gs.tile_begin[i + 1] - gs.tile_begin[i];
+    dep[i] = gs.dep_prob[i][0];
+  }
+  return G.list_len;
+}
