@@ -764,16 +764,26 @@ __device__ __forceinline__ void engine_body(const EngineParams* P, const GroupSc
     }
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer (leader CTA)
+    // The operand descriptors are built once per tile for stage 0 and advanced by constants (stage: kStageBytes, sub-step kk: 32 B of K or 16 / 8 MN-major
+    // K-rows, all in the 16-byte units of the start-address field): building them per MMA from
+    // the addresses cost ~100 uniform-datapath instructions per k-step, ~600 cycles of issue
+    // against 128 cycles of tensor work at N = 64 (tensor pipe 22 % on the 3x3 / K = 64 conv).
     if (leader) {
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
+      const uint32_t s0 = smem_u32(smem);
       for (int u = unit0; u < num_work; u += n_units, ++local) {
         int prob, mb, nb, t, sp, nsp;
         locate(P, gs, u, splits, prob, mb, nb, t, sp, nsp);
         const EngineParams& p = P[prob];
         const uint32_t idesc = make_idesc(kTF32 ? kFmtTF32 : kFmtBF16, kPair ? 256 : kEngineBM, BN,
                                           p.ca.mn_major, p.cb.mn_major);
+        const uint64_t a0 = operand_desc<kTF32>(s0, p.ca.mn_major, 0);
+        const uint64_t b0 = operand_desc<kTF32>(s0 + kTileABytes, p.cb.mn_major, 0);
+        constexpr uint32_t kMnInc = (kTF32 ? 8 : 16) * 128 / 16;
+        const uint32_t a_inc = p.ca.mn_major ? kMnInc : 2u, b_inc = p.cb.mn_major ? kMnInc : 2u;
+        const bool skip_mma = (p.debug_flags & 1) != 0;
         const int ks_per = (p.k_steps + nsp - 1) / nsp;
         const int s_begin = sp * ks_per;
         const int n_steps = min(p.k_steps, s_begin + ks_per) - s_begin;
@@ -790,33 +800,31 @@ __device__ __forceinline__ void engine_body(const EngineParams* P, const GroupSc
           tc_fence_after();
           if (local == 0 && s == 0 && lane == 0) BRK_TS(3);
           if (s == 0 && lane == 0) BRK_TT(local, 1);
-          if (elect_one()) {
-            if (p.debug_flags & 1) {
-              if constexpr (kPair) {
-                mma_commit_pair(&empty[stage]);
-                if (s == n_steps - 1) mma_commit_pair(&tfull[acc]);
-              } else {
-                mbar_arrive(&empty[stage]);
-                if (s == n_steps - 1) mbar_arrive(&tfull[acc]);
-              }
+          const bool issuer = elect_one();
+          if (!issuer) {
+          } else if (skip_mma) {
+            if constexpr (kPair) {
+              mma_commit_pair(&empty[stage]);
+              if (s == n_steps - 1) mma_commit_pair(&tfull[acc]);
             } else {
-              const uint32_t sa = smem_u32(smem + stage * Cfg::kStageBytes);
-              const uint32_t sb = sa + kTileABytes;
+              mbar_arrive(&empty[stage]);
+              if (s == n_steps - 1) mbar_arrive(&tfull[acc]);
+            }
+          } else {
+            const uint64_t so = static_cast<uint64_t>(stage * (Cfg::kStageBytes / 16));
 #pragma unroll
-              for (int kk = 0; kk < 4; ++kk) {
-                const uint64_t ad = operand_desc<kTF32>(sa, p.ca.mn_major, kk);
-                const uint64_t bd = operand_desc<kTF32>(sb, p.cb.mn_major, kk);
-                const uint32_t accum = (s > 0 || kk > 0) ? 1u : 0u;
-                if constexpr (kPair) mma_ss_pair<kTF32>(d_tmem, ad, bd, idesc, accum);
-                else mma_ss<kTF32>(d_tmem, ad, bd, idesc, accum);
-              }
-              if constexpr (kPair) {
-                mma_commit_pair(&empty[stage]);
-                if (s == n_steps - 1) mma_commit_pair(&tfull[acc]);
-              } else {
-                mma_commit(&empty[stage]);
-                if (s == n_steps - 1) mma_commit(&tfull[acc]);
-              }
+            for (int kk = 0; kk < 4; ++kk) {
+              const uint32_t accum = (s > 0 || kk > 0) ? 1u : 0u;
+              const uint64_t ad = a0 + so + kk * a_inc, bd = b0 + so + kk * b_inc;
+              if constexpr (kPair) mma_ss_pair<kTF32>(d_tmem, ad, bd, idesc, accum);
+              else mma_ss<kTF32>(d_tmem, ad, bd, idesc, accum);
+            }
+            if constexpr (kPair) {
+              mma_commit_pair(&empty[stage]);
+              if (s == n_steps - 1) mma_commit_pair(&tfull[acc]);
+            } else {
+              mma_commit(&empty[stage]);
+              if (s == n_steps - 1) mma_commit(&tfull[acc]);
             }
           }
           __syncwarp();

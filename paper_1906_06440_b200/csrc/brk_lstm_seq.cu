@@ -231,6 +231,8 @@ __global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_fwd_kernel(const __grid
   } else if (warp == 4) {
     // ---------------------------------------------------------------- MMA issuer
     const uint32_t idesc = make_idesc(kFmtBF16, 128, kGN, 0, 0);
+    const uint64_t ring_desc = make_smem_desc(smem_u32(ring), 16, 1024, kSwizzle128B);
+    const uint64_t w_desc = make_smem_desc(smem_u32(wsm), 16, 1024, kSwizzle128B);
     mbar_wait(wbar, 0);
     for (int t = 0; t < p.T; ++t) {
       mbar_wait(tempty, (t & 1) ^ 1);
@@ -241,14 +243,13 @@ __global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_fwd_kernel(const __grid
         tc_fence_after();
         if (lane == 0 && kc == 0) SEQ_TS(t, 2);       // first chunk landed
         if (lane == 0 && kc == KC - 1) SEQ_TS(t, 3);  // last chunk landed
-        if (elect_one()) {
-          const uint32_t a0 = smem_u32(ring + st * p.stage_bytes);
-          const uint32_t b0 = smem_u32(wsm + kc * kGN * 128);
+        if (elect_one()) {  // descriptors advanced by constants (16-byte units), see brk_engine.cu
+          const uint64_t ad = ring_desc + static_cast<uint32_t>(st * p.stage_bytes) / 16;
+          const uint64_t bd = w_desc + static_cast<uint32_t>(kc * kGN * 128 / 16);
           for (int mt = 0; mt < n_mt; ++mt)
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
-              mma_ss<false>(tmem + mt * kGN, make_smem_desc(a0 + mt * 16384 + kk * 32, 16, 1024, kSwizzle128B),
-                            make_smem_desc(b0 + kk * 32, 16, 1024, kSwizzle128B), idesc, (kc | kk) ? 1u : 0u);
+              mma_ss<false>(tmem + mt * kGN, ad + mt * 1024 + kk * 2, bd + kk * 2, idesc, (kc | kk) ? 1u : 0u);
           mma_commit_mc(&empty[st], cmask);  // the stage is free in the whole cluster once all CTAs arrive
           if (kc == KC - 1) mma_commit(tfull);
         }
@@ -433,6 +434,8 @@ __global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_fwd_pair_kernel(const _
     // ---------------------------------------------------------------- MMA issuer (leader)
     if (leader) {
       const uint32_t idesc = make_idesc(kFmtBF16, 256, kGN, 0, 0);
+      const uint64_t ring_desc = make_smem_desc(smem_u32(ring), 16, 1024, kSwizzle128B);
+      const uint64_t w_desc = make_smem_desc(smem_u32(wsm), 16, 1024, kSwizzle128B);
       mbar_wait(wbar, 0);
       for (int t = 0; t < p.T; ++t) {
         mbar_wait(tempty, (t & 1) ^ 1);
@@ -443,13 +446,12 @@ __global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_fwd_pair_kernel(const _
           tc_fence_after();
           if (lane == 0 && kc == 0) SEQ_TS(t, 2);
           if (lane == 0 && kc == KC - 1) SEQ_TS(t, 3);
-          if (elect_one()) {
-            const uint32_t a0 = smem_u32(ring + st * kStageA);
-            const uint32_t b0 = smem_u32(wsm + kc * kBRows * 128);
+          if (elect_one()) {  // descriptors advanced by constants (16-byte units), see brk_engine.cu
+            const uint64_t ad = ring_desc + static_cast<uint32_t>(st * (kStageA / 16));
+            const uint64_t bd = w_desc + static_cast<uint32_t>(kc * (kBRows * 128 / 16));
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
-              mma_ss_pair<false>(tmem, make_smem_desc(a0 + kk * 32, 16, 1024, kSwizzle128B),
-                                 make_smem_desc(b0 + kk * 32, 16, 1024, kSwizzle128B), idesc, (kc | kk) ? 1u : 0u);
+              mma_ss_pair<false>(tmem, ad + kk * 2, bd + kk * 2, idesc, (kc | kk) ? 1u : 0u);
             mma_commit_pair(&empty[st]);
             if (kc == KC - 1) mma_commit_pair(tfull);
           }
@@ -610,6 +612,8 @@ __global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_bwd_kernel(const __grid
     }
   } else if (warp == 4) {
     const uint32_t idesc = make_idesc(kFmtBF16, 128, kJb, 0, 0);
+    const uint64_t ring_desc = make_smem_desc(smem_u32(ring), 16, 1024, kSwizzle128B);
+    const uint64_t w_desc = make_smem_desc(smem_u32(wsm), 16, 1024, kSwizzle128B);
     mbar_wait(wbar, 0);
     for (int it = 0; it < p.T - 1; ++it) {
       mbar_wait(tempty, (it & 1) ^ 1);
@@ -620,14 +624,13 @@ __global__ void __launch_bounds__(kThreadsS, 1) lstm_seq_bwd_kernel(const __grid
         tc_fence_after();
         if (lane == 0 && kc == 0) SEQ_TS(it, 2);
         if (lane == 0 && kc == KC - 1) SEQ_TS(it, 3);
-        if (elect_one()) {
-          const uint32_t a0 = smem_u32(ring + st * p.stage_bytes);
-          const uint32_t b0 = smem_u32(wsm + kc * kJb * 128);
+        if (elect_one()) {  // descriptors advanced by constants (16-byte units), see brk_engine.cu
+          const uint64_t ad = ring_desc + static_cast<uint32_t>(st * p.stage_bytes) / 16;
+          const uint64_t bd = w_desc + static_cast<uint32_t>(kc * kJb * 128 / 16);
           for (int mt = 0; mt < n_mt; ++mt)
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
-              mma_ss<false>(tmem + mt * kJb, make_smem_desc(a0 + mt * 16384 + kk * 32, 16, 1024, kSwizzle128B),
-                            make_smem_desc(b0 + kk * 32, 16, 1024, kSwizzle128B), idesc, (kc | kk) ? 1u : 0u);
+              mma_ss<false>(tmem + mt * kJb, ad + mt * 1024 + kk * 2, bd + kk * 2, idesc, (kc | kk) ? 1u : 0u);
           mma_commit(&empty[st]);
           if (kc == KC - 1) mma_commit(tfull);
         }

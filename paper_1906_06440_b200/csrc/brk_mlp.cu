@@ -345,10 +345,13 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_step_kernel(const __grid_cons
     }
   } else if (warp == kMmaWarp) {
     // ---------------------------------------------------------------- MMA issuer (leader CTA)
+    // descriptors built once per tile and advanced by constants (brk_engine.cu)
     if (leader) {
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
+      const uint32_t s0 = smem_u32(smem);
+      constexpr uint32_t kMnInc = (kTF32 ? 8 : 16) * 128 / 16;
       for (int it = it_begin; it < it_end; it += it_step, ++local) {
         const int u = listed ? G.list[it] : it;
         int prob, mb, nb;
@@ -356,6 +359,8 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_step_kernel(const __grid_cons
         const MlpProb& p = P[prob];
         const int a_mn = p.a_mn, b_mn = p.b_mn, n_steps = p.k_steps;
         const uint32_t idesc = make_idesc(kTF32 ? kFmtTF32 : kFmtBF16, 256, kBN, a_mn, b_mn);
+        const uint64_t a0 = op_desc<kTF32>(s0, a_mn, 0), b0 = op_desc<kTF32>(s0 + kABytes, b_mn, 0);
+        const uint32_t a_inc = a_mn ? kMnInc : 2u, b_inc = b_mn ? kMnInc : 2u;
         const int acc = local & 1;
         mbar_wait(&tempty[acc], ((local >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -364,13 +369,11 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_step_kernel(const __grid_cons
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           if (s == 0 && lane == 0) MLP_TT(local, 1);
+          const uint64_t so = static_cast<uint64_t>(stage * (kStageBytes / 16));
           if (elect_one()) {
-            const uint32_t sa = smem_u32(smem + stage * kStageBytes);
-            const uint32_t sb = sa + kABytes;
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
-              mma_ss_pair<kTF32>(d_tmem, op_desc<kTF32>(sa, a_mn, kk), op_desc<kTF32>(sb, b_mn, kk), idesc,
-                                 (s | kk) ? 1u : 0u);
+              mma_ss_pair<kTF32>(d_tmem, a0 + so + kk * a_inc, b0 + so + kk * b_inc, idesc, (s | kk) ? 1u : 0u);
             if constexpr (kPairs == 1) {
               mma_commit_pair(&empty[stage]);
               if (s == n_steps - 1) mma_commit_pair(&tfull[acc]);
