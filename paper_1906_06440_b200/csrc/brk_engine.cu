@@ -60,7 +60,10 @@ struct EngineCfg {
   // ring depth: as many stages as fit (<= 7), one producer warp each
   static constexpr int kFit = kAvail / kStageBytes > 7 ? 7 : kAvail / kStageBytes;
   static constexpr int kStages = kFit;
-  static constexpr int kTmemCols = 2 * BN;
+  // accumulator buffers in TMEM: four when they fit the 512 columns (BN <= 128), so the MMA can
+  // run up to three tiles ahead of the epilogue (short tiles: 1x1 convs with one or two k-steps)
+  static constexpr int kAcc = 4 * BN <= 512 ? 4 : 2;
+  static constexpr int kTmemCols = kAcc * BN;
   static constexpr int kSmem = kStages * kStageBytes + kEpiStageBytes + 1024 + 256;
   // 7 producer warps: a TMA-issuing warp keeps about one box in flight (~1 box
   // per ~930 clk of latency, profiles/r01_tma_sweep.txt), so the per-SM operand
@@ -627,15 +630,20 @@ __device__ __forceinline__ void engine_body(const EngineParams* P, const GroupSc
   constexpr int kStages = Cfg::kStages;
   constexpr int kMmaWarp = Cfg::kMmaWarp;
   constexpr int kProducers = Cfg::kProducers;
-  constexpr int kCW = Cfg::kColsPerWarp;
+  // BN = 64 compact epilogues: the two epilogue warp groups take alternate tiles and each warp
+  // drains all 64 columns of its 32 rows (one x64 TMEM load, one TMA store) instead of every
+  // warp draining 32 columns of every tile through 64-byte generic stores
+  constexpr bool kAlt = BN == 64 && !kFullEpi && !kGroup;
+  constexpr int kCW = kAlt ? 64 : Cfg::kColsPerWarp;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * Cfg::kStageBytes + Cfg::kEpiStageBytes);
   uint64_t* empty = full + kStages;
-  uint64_t* tfull = empty + kStages;  // [2]
-  uint64_t* tempty = tfull + 2;       // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  constexpr int kAcc = Cfg::kAcc;
+  uint64_t* tfull = empty + kStages;  // [kAcc]
+  uint64_t* tempty = tfull + kAcc;    // [kAcc]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + kAcc);
   uint32_t* split_flag = tmem_slot + 1;
   uint32_t* deps_seq = tmem_slot + 2;  // grouped launches: tiles whose dependencies producer 0 acquired
 
@@ -661,9 +669,10 @@ __device__ __forceinline__ void engine_body(const EngineParams* P, const GroupSc
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < kAcc; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], kPair ? 2 * kEpiWarps : kEpiWarps);
+      constexpr uint32_t kDrainers = kAlt ? kEpiWarps / 2 : kEpiWarps;  // epilogue warps per tile
+      mbar_init(&tempty[a], kPair ? 2 * kDrainers : kDrainers);
     }
     fence_barrier_init();
   }
@@ -735,7 +744,8 @@ __device__ __forceinline__ void engine_body(const EngineParams* P, const GroupSc
             }
           }
           BRK_CLK(tp0);
-          mbar_wait(&empty[stage], phase ^ 1);
+          if (p.debug_flags & 256) mbar_wait(&empty[stage], phase ^ 1);
+          else mbar_wait_sleep(&empty[stage], phase ^ 1);
           if (pid == 0) BRK_ACC(4, tp0);
           uint8_t* sa = smem + stage * Cfg::kStageBytes;
           uint8_t* sb = sa + kTileABytes;
@@ -787,9 +797,9 @@ __device__ __forceinline__ void engine_body(const EngineParams* P, const GroupSc
         const int ks_per = (p.k_steps + nsp - 1) / nsp;
         const int s_begin = sp * ks_per;
         const int n_steps = min(p.k_steps, s_begin + ks_per) - s_begin;
-        const int acc = local & 1;
+        const int acc = local % kAcc;
         BRK_CLK(tw0);
-        mbar_wait(&tempty[acc], ((local >> 1) & 1) ^ 1);
+        mbar_wait(&tempty[acc], ((local / kAcc) & 1) ^ 1);
         if (lane == 0) BRK_ACC(0, tw0);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -839,7 +849,7 @@ __device__ __forceinline__ void engine_body(const EngineParams* P, const GroupSc
     pdl_wait();  // outputs may be read by the previous kernel (WAR) — wait before writing
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
     const int chalf = warp >> 2;   // column half this warp drains
-    const int cbeg = chalf * kCW;
+    const int cbeg = kAlt ? 0 : chalf * kCW;
     // (draining the first 64-column chunk of a tile with all eight warps before the second —
     //  64 B store segments, two releases per warp — was measured slower: 109.7 vs 102.7 us
     //  per MLP step)
@@ -849,11 +859,12 @@ __device__ __forceinline__ void engine_body(const EngineParams* P, const GroupSc
     const int halves = kPair ? 2 : 1;
     int local = 0;
     for (int u = unit0; u < num_work; u += n_units, ++local) {
+      if (kAlt && (local & 1) != chalf) continue;  // the other warp group's tile
       int prob, mb, nb, t, sp, nsp;
       locate(P, gs, u, splits, prob, mb, nb, t, sp, nsp);
       const EngineParams& p = P[prob];
       const EpiView ev(p);
-      const int acc = local & 1;
+      const int acc = local % kAcc;
       // bias for this warp's columns, one value per lane per 32-column chunk, loaded before
       // the accumulator wait (the staged epilogue broadcasts it with shuffles)
       float bias_r[kCW / 32];
@@ -901,7 +912,8 @@ __device__ __forceinline__ void engine_body(const EngineParams* P, const GroupSc
         }
       }
       BRK_CLK(te0);
-      mbar_wait(&tfull[acc], (local >> 1) & 1);
+      if (p.debug_flags & 256) mbar_wait(&tfull[acc], (local / kAcc) & 1);
+      else mbar_wait_sleep(&tfull[acc], (local / kAcc) & 1);
       if (threadIdx.x == 0) BRK_ACC(2, te0);
       BRK_CLK(te1);
       tc_fence_after();
@@ -935,6 +947,7 @@ __device__ __forceinline__ void engine_body(const EngineParams* P, const GroupSc
                   else mbar_arrive_relaxed(&tempty[acc]);
                 }
               }
+              if (p.debug_flags & 512) continue;  // diagnostics: accumulator drained, nothing stored
               if (tma_out) {  // an earlier store may still be reading the staging tile
                 if (lane == 0) bulk_wait_read0();
                 __syncwarp();
