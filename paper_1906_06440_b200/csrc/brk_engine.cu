@@ -1320,7 +1320,7 @@ int launch_engine(const EngineParams& p, int bn, int tf32, int pair, int max_uni
                         p.cols % 64 == 0 &&
                         ((om.rb2 >= 0x7fffffff && om.rh == (p.cols / 64) * om.ch) ||
                          (om.rb2 == om.rb && om.rh == 0 && om.rh2 == (p.cols / 64) * om.ch));
-    if (!full && !tf32 && p.out_bf16 && p.zf_w == 0 && bn >= 128 && splits == 1 && layout &&
+    if (!full && !tf32 && p.out_bf16 && p.zf_w == 0 && (bn >= 128 || (bn == 64 && !pair)) && splits == 1 && layout &&
         !(env != nullptr && std::atoi(env) == 0)) {
       q = p;
       const int64_t outer = (static_cast<int64_t>(p.rows) + om.rb - 1) / om.rb;
@@ -1334,6 +1334,8 @@ int launch_engine(const EngineParams& p, int bn, int tf32, int pair, int max_uni
       }
     }
   }
+  // (a resident-B variant for BN = 64 single-column-tile launches — the weights loaded once per
+  //  CTA, the ring carrying only A — was measured slower: 3x3 K = 64 fwd 101.8 -> 107.0 us)
 #define BRK_ENGINE_CASE(BN_, PAIR_)                                                                  \
   if (bn == BN_ && pair == PAIR_) {                                                                  \
     if (full) return tf32 ? launch_engine_t<BN_, true, PAIR_, true>(*pp, grid, stream, pdl)          \
