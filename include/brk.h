@@ -349,6 +349,9 @@ BRK_API int brk_diag_tma_lanes(const void* buf, int rows, int cols, int box_rows
                                float* us, double* bytes);
 /* Diagnostic: per-warp clock64 cycles of iters x (tcgen05.ld.32x32b.x32 + wait); synchronous. */
 BRK_API int brk_diag_tmem_ld(int ctas, int iters, long long* cycles_dev, float* sink_dev);
+/* Diagnostic: clock64 cycles per CTA of iters x 4 back-to-back SS-mode MMAs (M = 128, N = n, K = 16
+ * bf16; b_mn: MN-major B) from fixed shared-memory operands; synchronous. */
+BRK_API int brk_diag_mma_rate(int n, int b_mn, int ctas, int iters, long long* cycles_dev);
 
 #ifdef __cplusplus
 }

@@ -62,6 +62,7 @@ SIGNATURES: dict[str, tuple] = {
                                    _vp]),
     "brk_lstm_recurrent_grad": (_c_int, [_vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp]),
     "brk_diag_tmem_ld": (_c_int, [_c_int, _c_int, _vp, _vp]),
+    "brk_diag_mma_rate": (_c_int, [_c_int, _c_int, _c_int, _c_int, _vp]),
     "brk_diag_tma_lanes": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _vp]),
     "brk_diag_mlp_schedule": (_c_int, [_c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp]),
     "brk_diag_tma_bw": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int,

@@ -104,10 +104,63 @@ __global__ void __launch_bounds__(128, 1) tmem_ld_kernel(int iters, long long* c
   if (warp == 0) tmem_dealloc(slot, 256);
 }
 
+// Back-to-back SS-mode tcgen05.mma (M = 128, N = n, K = 16 bf16, 4 per "k-step" of 64) from
+// fixed shared-memory operands into one TMEM accumulator, issued by one thread: cycles per
+// MMA, i.e. the tensor pipe's rate for the shape with no operand delivery, barriers or epilogue.
+__global__ void __launch_bounds__(128, 1) mma_rate_kernel(int n, int iters, int b_mn, long long* cycles) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* done = reinterpret_cast<uint64_t*>(smem + 2 * (16384 + 32768));
+  __shared__ uint32_t slot;
+  for (int i = threadIdx.x; i < 2 * (16384 + 32768) / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(smem)[i] = make_uint4(0x3c003c00u, 0x3c003c00u, 0x3c003c00u, 0x3c003c00u);
+  if (threadIdx.x == 0) {
+    mbar_init(done, 1);
+    fence_barrier_init();
+  }
+  fence_proxy_async_smem();
+  if (threadIdx.x < 32) tmem_alloc(&slot, 256);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (threadIdx.x == 0) {
+    const uint32_t idesc = make_idesc(kFmtBF16, 128, static_cast<uint32_t>(n), 0, static_cast<uint32_t>(b_mn));
+    const uint32_t s0 = smem_u32(smem);
+    const long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+      const uint32_t sa = s0 + (i & 1) * (16384 + 32768), sb = sa + 16384;
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const uint64_t ad = make_smem_desc(sa + kk * 32, 16, 1024, kSwizzle128B);
+        const uint64_t bd = b_mn ? make_smem_desc(sb + kk * 16 * 128, 64 * 128, 1024, kSwizzle128B)
+                                 : make_smem_desc(sb + kk * 32, 16, 1024, kSwizzle128B);
+        mma_ss<false>(slot, ad, bd, idesc, (i | kk) ? 1u : 0u);
+      }
+    }
+    mma_commit(done);
+    mbar_wait(done, 0);
+    const long long t1 = clock64();
+    cycles[blockIdx.x] = t1 - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) tmem_dealloc(slot, 256);
+}
+
 }  // namespace
 }  // namespace brk
 
 using namespace brk;
+
+// cycles_dev[ctas]: clock64 cycles for iters x 4 MMAs of M = 128, N = n (bf16, K = 16 each)
+extern "C" BRK_API int brk_diag_mma_rate(int n, int b_mn, int ctas, int iters, long long* cycles_dev) {
+  if (n < 16 || n > 256 || n % 16) return set_error(BRK_ERR_CONTRACT, "diag_mma_rate: bad N");
+  const int smem = 2 * (16384 + 32768) + 1024 + 64;
+  cudaFuncSetAttribute(mma_rate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  mma_rate_kernel<<<ctas, 128, smem>>>(n, iters, b_mn, cycles_dev);
+  cudaError_t err = cudaDeviceSynchronize();
+  return err == cudaSuccess ? BRK_OK : set_cuda_error(err, "diag_mma_rate");
+}
 
 extern "C" BRK_API int brk_diag_tma_lanes(const void* buf, int rows, int cols, int box_rows, int lanes, int ctas, int iters,
                                float* us, double* bytes) {
