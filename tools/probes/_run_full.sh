@@ -1,9 +1,9 @@
 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" 2>&1 | tail -1
-python bench.py > gpurun_out/bench_full4.json 2> gpurun_out/bench_full4.err; tail -c 300 gpurun_out/bench_full4.err
+python bench.py > gpurun_out/bench_full5.json 2> gpurun_out/bench_full5.err; tail -c 300 gpurun_out/bench_full5.err
 python - <<'PY'
 import json
-d = json.loads(open("gpurun_out/bench_full4.json").read().strip().splitlines()[-1])
+d = json.loads(open("gpurun_out/bench_full5.json").read().strip().splitlines()[-1])
 print({k: d[k] for k in ("value", "ms_per_step")}, d["e2e"]["value"], d["roofline"]["achieved"], d["roofline"]["frac"], d["clocks"])
 w = d["workloads"]
 print("resnet all53", {p: round(v["tflops"], 1) for p, v in w["resnet50_conv_n256"]["summary"].items()})
