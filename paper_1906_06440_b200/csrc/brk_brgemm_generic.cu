@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
   // are — A K-major, B MN-major in 32-element atoms (128B swizzle of 32 B chunks) — and the
   // idle gather warps round each stage to TF32 in place (RNA, like the gather path's
   // cvt.rna) before the MMA reads it; the tensor core alone would truncate the mantissa
-  const bool tf32_tma = kTF32 && p.tma && p.all_tma;
+  const bool tf32_tma = kTF32 && p.tma && (p.all_tma || (p.tma_ok != nullptr && *p.tma_ok != 0));
   const bool b_mn = !kTF32 || tf32_tma;  // B operand MN-major (atoms) vs K-major rows
   // ring geometry: the B operand of the widest tile (MN-major atoms, or K-major rows for gathered TF32)
   const int m_max = min(p.m, kCols);
@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
   };
   auto entry_box = [&](int job, int entry) -> EntryBox {
     EntryBox eb{false, 0, 0, 0, 0};
-    if (!p.tma || (kTF32 && !p.all_tma)) return eb;  // TF32 boxes only when every entry is one
+    if (!p.tma || (kTF32 && !tf32_tma)) return eb;  // TF32 boxes only when every entry is one
     if (p.all_tma) {
       eb.tma = true;
       eb.ra = static_cast<int32_t>(job * p.rj_a + entry * p.rs_a);
@@ -538,6 +538,26 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
   }
 }
 
+// TF32 offset / address-with-views launches: is every (job, entry) one in-view box per operand?
+// One CTA walks the entry table (the same arithmetic as entry_box) and writes the verdict.
+__global__ void __launch_bounds__(1024, 1) tf32_box_check_kernel(const __grid_constant__ GenericParams p,
+                                                                int64_t rows_a, int64_t rows_b, int* ok_out) {
+  bool ok = true;
+  const int64_t entries = static_cast<int64_t>(p.n_jobs) * p.batch;
+  for (int64_t idx = threadIdx.x; idx < entries && ok; idx += blockDim.x) {
+    const int job = static_cast<int>(idx / p.batch), i = static_cast<int>(idx - static_cast<int64_t>(job) * p.batch);
+    int64_t oa, ob;
+    if (!entry_offs(p, job, i, oa, ob) || oa < 0 || ob < 0) { ok = false; break; }
+    const int64_t qa = oa / p.a_sk, qb = ob / p.b_sn;
+    ok = (oa - qa * p.a_sk) + p.m <= p.a_sk && (ob - qb * p.b_sn) + p.k <= p.b_sn &&
+         qa + ((p.k + 31) & ~31) <= rows_a && qb + p.n <= rows_b;
+  }
+  ok = __syncthreads_and(ok) != 0;
+  if (threadIdx.x == 0) *ok_out = ok ? 1 : 0;
+}
+
+__device__ int g_tf32_box_ok[256];  // one verdict slot per launch (round robin)
+
 }  // namespace
 
 int launch_brgemm_generic(const GenericParams& p, int compute_tf32, cudaStream_t stream) {
@@ -612,6 +632,37 @@ int launch_brgemm_generic(const GenericParams& p, int compute_tf32, cudaStream_t
       q.rj_a = p.jstride_a / p.a_sk;
       q.rs_b = p.stride_b / p.b_sn;
       q.rj_b = p.jstride_b / p.b_sn;
+    }
+  }
+  // TF32 offset variant / address variant with views: the same TMA path when a check kernel
+  // finds every entry one in-view box per operand (otherwise the launch gathers, as before)
+  const bool tf32_views = p.mode == kModeOffs || addr_views;
+  if (compute_tf32 && !q.tma && !p.in_bf16 && tf32_views && p.k % 32 == 0 && (p.n <= kRows || p.n % kRows == 0) &&
+      p.m % 32 == 0 && p.a_sm == 1 && p.b_sk == 1 && (p.a_sk * 4) % 16 == 0 && (p.b_sn * 4) % 16 == 0 &&
+      p.a_sk >= p.m && p.b_sn >= p.k && (reinterpret_cast<uintptr_t>(p.a_base) & 15) == 0 &&
+      (reinterpret_cast<uintptr_t>(p.b_base) & 15) == 0 && std::getenv("BRK_GENERIC_NO_TMA") == nullptr) {
+    q.nbox = std::min(p.n, kRows);
+    q.abox = 32;
+    uint64_t rows_b = std::min<uint64_t>(0x7fffffffull, (1ull << 38) / (p.b_sn * 4));
+    uint64_t rows_a = std::min<uint64_t>(0x7fffffffull, (1ull << 38) / (p.a_sk * 4));
+    if (addr_views) {
+      rows_b = std::min<uint64_t>(rows_b, static_cast<uint64_t>((p.b_view + p.b_sn - 1) / p.b_sn));
+      rows_a = std::min<uint64_t>(rows_a, static_cast<uint64_t>((p.a_view + p.a_sk - 1) / p.a_sk));
+    }
+    const uint64_t db[2] = {static_cast<uint64_t>(p.b_sn), rows_b}, sb[2] = {1, static_cast<uint64_t>(p.b_sn)};
+    const uint64_t da[2] = {static_cast<uint64_t>(p.a_sk), rows_a}, sa[2] = {1, static_cast<uint64_t>(p.a_sk)};
+    const uint32_t bb[2] = {32, static_cast<uint32_t>(q.nbox)}, ba[2] = {32, 32};
+    static int* slots = nullptr;
+    static std::atomic<unsigned> next{0};
+    if (slots == nullptr) cudaGetSymbolAddress(reinterpret_cast<void**>(&slots), g_tf32_box_ok);
+    if (slots != nullptr && encode_tmap(&q.map_bop, p.b_base, false, 2, db, sb, bb) == BRK_OK &&
+        encode_tmap(&q.map_aop, p.a_base, false, 2, da, sa, ba, /*atom32=*/true) == BRK_OK) {
+      int* ok = slots + (next.fetch_add(1) & 255u);
+      g_launches.fetch_add(1);
+      tf32_box_check_kernel<<<1, 1024, 0, stream>>>(q, static_cast<int64_t>(rows_a), static_cast<int64_t>(rows_b), ok);
+      q.tma = 1;
+      q.all_tma = 0;
+      q.tma_ok = ok;
     }
   }
   cudaError_t err;

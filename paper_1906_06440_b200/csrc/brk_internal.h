@@ -29,6 +29,9 @@ struct GenericParams {
   // box per operand at view row job * rj + i * rs (no per-entry division, no gather work)
   int all_tma;
   int64_t rs_a, rj_a, rs_b, rj_b;
+  // TF32 offset / address-with-views launches: device flag written by a check kernel just
+  // before (1: every entry is one in-view box per operand, so the launch runs like all_tma)
+  const int* tma_ok;
   int mode;    // EntryMode
   int n_jobs;  // number of independent output blocks C_j
   int m, n, k, batch;

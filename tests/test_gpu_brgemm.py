@@ -104,6 +104,34 @@ def test_strided_offset_address_equivalence():
         assert np.array_equal(addr, offs)
 
 
+@pytest.mark.parametrize("aligned", [True, False])
+def test_offset_variant_tf32_views(aligned):
+    """TF32 offset variant: entries that are whole rows of the packed buffers (every offset a
+    multiple of the block row length) run on the TMA path after the device check; one offset
+    inside a row sends the whole launch to the gather path.  Both within the TF32 bound, and
+    the TMA launch bit-identical to the stride variant over the same blocks."""
+    rng = np.random.default_rng([11, int(aligned)])
+    m, n, k, batch, pool = 64, 64, 64, 16, 24
+    a_buf = rng.uniform(-1, 1, (pool, k, m)).astype(F32)
+    b_buf = rng.uniform(-1, 1, (pool, n, k)).astype(F32)
+    pick = rng.integers(0, pool - 1, batch)  # repeats allowed, any order
+    a_offs = [int(i) * k * m for i in pick]
+    b_offs = [int(i) * n * k for i in pick[::-1]]
+    if not aligned:
+        a_offs[3] += 8  # inside a row: not one box
+    a_blocks = [a_buf.reshape(-1)[o:o + k * m].reshape(k, m) for o in a_offs]
+    b_blocks = [b_buf.reshape(-1)[o:o + n * k].reshape(n, k) for o in b_offs]
+    spec = BrgemmSpec(m=m, n=n, k=k, batch=batch, beta=1.0)
+    c0 = rng.uniform(-1, 1, (n, m)).astype(F32)
+    ref = orc.brgemm_reference(a_blocks, b_blocks, c0, 1.0, 1.0)
+    with precision("tf32"):
+        got = brgemm_offset(a_buf, b_buf, a_offs, b_offs, c0.copy(), spec)
+        assert orc.scale_rel_error(got, ref) <= TOL["tf32"]
+        if aligned:
+            strd = brgemm_strided(np.stack(a_blocks), np.stack(b_blocks), k * m, n * k, c0.copy(), spec)
+            assert np.array_equal(got, strd)
+
+
 def test_edge_cases():
     # empty batch keeps C (tests/test_brgemm.py:45-49)
     c = np.arange(12, dtype=F32).reshape(3, 4)
