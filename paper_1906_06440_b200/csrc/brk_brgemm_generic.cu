@@ -129,12 +129,13 @@ __device__ __forceinline__ bool entry_offs(const GenericParams& p, int job, int 
 }
 
 // Persistent: CTA walks job tiles (job, n-tile, m-tile) with four decoupled roles:
-//  * the TMA warp loads an entry's (reference b block, reference a block) pair as one box
-//    each when the blocks do not wrap a row of their buffer's 2-d view (stride / offset
-//    variants, bf16);
-//  * warps 0-7 gather every other entry (cp.async for aligned contiguous bf16 rows, else
+//  * the TMA warps load each entry's (reference b block, reference a block) pair as one box
+//    each when no block of the launch wraps a row of its buffer's 2-d view (stride variant:
+//    decided on the host; offset / address-with-views: by box_check_kernel just before);
+//  * otherwise warps 0-7 gather every entry (cp.async for aligned contiguous bf16 rows, else
 //    converting loads) — reference b rows -> K-major 128B-swizzled A operand, reference a
-//    rows -> MN-major (bf16) or K-major (TF32) B operand;
+//    rows -> MN-major (bf16) or K-major (TF32) B operand; with TF32 boxes they round the
+//    landed stages to TF32 instead;
 //  * warp 8 issues the tcgen05.mma chain (the whole batch reduces in TMEM), two
 //    accumulators so a tile's MMAs overlap the previous tile's epilogue;
 //  * warps 10-13 drain TMEM and apply alpha / beta / bias / act / mask.
@@ -170,7 +171,13 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
   // are — A K-major, B MN-major in 32-element atoms (128B swizzle of 32 B chunks) — and the
   // idle gather warps round each stage to TF32 in place (RNA, like the gather path's
   // cvt.rna) before the MMA reads it; the tensor core alone would truncate the mantissa
-  const bool tf32_tma = kTF32 && p.tma && (p.all_tma || (p.tma_ok != nullptr && *p.tma_ok != 0));
+  // every entry of the launch is one box per operand: known on the host (stride variant) or
+  // checked on the device just before (offset variant, address variant with views).  A launch
+  // either boxes every entry or gathers every entry: the producer and gather roles never
+  // interleave on the ring (a role that skips the other role's stages could run two phases
+  // ahead on a stage, where the parity waits alias)
+  const bool boxes = p.tma && (p.all_tma || (p.tma_ok != nullptr && *p.tma_ok != 0));
+  const bool tf32_tma = kTF32 && boxes;
   const bool b_mn = !kTF32 || tf32_tma;  // B operand MN-major (atoms) vs K-major rows
   // ring geometry: the B operand of the widest tile (MN-major atoms, or K-major rows for gathered TF32)
   const int m_max = min(p.m, kCols);
@@ -216,7 +223,7 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
   };
   auto entry_box = [&](int job, int entry) -> EntryBox {
     EntryBox eb{false, 0, 0, 0, 0};
-    if (!p.tma || (kTF32 && !tf32_tma)) return eb;  // TF32 boxes only when every entry is one
+    if (!boxes) return eb;
     if (p.all_tma) {
       eb.tma = true;
       eb.ra = static_cast<int32_t>(job * p.rj_a + entry * p.rs_a);
@@ -283,7 +290,7 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
   } else if (warp >= kTmaWarp && warp < kTmaWarp + kTmaWarps) {
     // ------------------------------------------------------------ TMA producers (stage g: warp g % 4)
     const int pid = warp - kTmaWarp;
-    if ((!kTF32 || tf32_tma) && p.tma && elect_one()) {
+    if (boxes && elect_one()) {
       int local = 0;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
         const int mt = t % m_tiles;
@@ -294,7 +301,24 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
         const int atoms = (m_here + kAtomCols - 1) / kAtomCols;
         const uint32_t bytes = static_cast<uint32_t>(p.nbox * 128 + atoms * p.abox * 128);
         int g = local * steps;
+        // offset / address tables: this job's entries are contiguous — pull their lines into L1
+        // once, so the per-entry reads below do not each pay an L2 round trip
+        if (!p.all_tma && steps > 0 && (p.mode == kModeOffs || p.mode == kModeAddr)) {
+          const char* ta = p.mode == kModeOffs ? reinterpret_cast<const char*>(p.a_offs)
+                                               : reinterpret_cast<const char*>(p.a_ptrs);
+          const char* tb = p.mode == kModeOffs ? reinterpret_cast<const char*>(p.b_offs)
+                                               : reinterpret_cast<const char*>(p.b_ptrs);
+          const int64_t first = static_cast<int64_t>(job) * p.batch * 8;
+          for (int64_t o = first & ~int64_t(127); o < first + p.batch * 8; o += 128) {
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(ta + o));
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(tb + o));
+          }
+        }
         for (int entry = 0; entry < p.batch && steps > 0; ++entry) {
+          // entries none of whose chunks this producer issues are skipped without reading them
+          bool mine = n_chunks >= kTmaWarps;
+          for (int ch = 0; ch < n_chunks && !mine; ++ch) mine = (g + ch) % kTmaWarps == pid;
+          if (!mine) { g += n_chunks; continue; }
           const EntryBox eb = entry_box(job, entry);
           if (!eb.tma) { g += n_chunks; continue; }
           for (int ch = 0; ch < n_chunks; ++ch, ++g) {
@@ -347,7 +371,7 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
     const bool a_contig = p.b_sk == 1;   // reference b block: k contiguous
     const bool b_contig = p.a_sm == 1;   // reference a block: m contiguous
     int local = 0;
-    for (int t = p.all_tma && !kTF32 ? tiles : blockIdx.x; t < tiles; t += gridDim.x, ++local) {
+    for (int t = boxes ? tiles : blockIdx.x; t < tiles; t += gridDim.x, ++local) {
       const int mt = t % m_tiles;
       const int nt = (t / m_tiles) % n_tiles;
       const int job = t / (m_tiles * n_tiles);
@@ -538,25 +562,51 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
   }
 }
 
-// TF32 offset / address-with-views launches: is every (job, entry) one in-view box per operand?
-// One CTA walks the entry table (the same arithmetic as entry_box) and writes the verdict.
-__global__ void __launch_bounds__(1024, 1) tf32_box_check_kernel(const __grid_constant__ GenericParams p,
-                                                                int64_t rows_a, int64_t rows_b, int* ok_out) {
-  bool ok = true;
-  const int64_t entries = static_cast<int64_t>(p.n_jobs) * p.batch;
-  for (int64_t idx = threadIdx.x; idx < entries && ok; idx += blockDim.x) {
-    const int job = static_cast<int>(idx / p.batch), i = static_cast<int>(idx - static_cast<int64_t>(job) * p.batch);
-    int64_t oa, ob;
-    if (!entry_offs(p, job, i, oa, ob) || oa < 0 || ob < 0) { ok = false; break; }
-    const int64_t qa = oa / p.a_sk, qb = ob / p.b_sn;
+// Offset / address-with-views launches: is every (job, entry) one in-view box per operand?
+// One thread per entry (the same arithmetic as entry_box); an entry that is not clears the
+// verdict, which the host set non-zero just before (every writer writes 0: no ordering needed).
+__global__ void __launch_bounds__(256) box_check_kernel(const __grid_constant__ GenericParams p, int64_t rows_a,
+                                                        int64_t rows_b, int* ok_out) {
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= static_cast<int64_t>(p.n_jobs) * p.batch) return;
+  const int job = static_cast<int>(idx / p.batch), i = static_cast<int>(idx - static_cast<int64_t>(job) * p.batch);
+  int64_t oa, ob;
+  bool ok = entry_offs(p, job, i, oa, ob) && oa >= 0 && ob >= 0;
+  if (ok) {
+    int64_t qa, qb;
+    if (((oa | ob) >> 32) == 0) {
+      qa = static_cast<uint32_t>(oa) / static_cast<uint32_t>(p.a_sk);
+      qb = static_cast<uint32_t>(ob) / static_cast<uint32_t>(p.b_sn);
+    } else {
+      qa = oa / p.a_sk;
+      qb = ob / p.b_sn;
+    }
     ok = (oa - qa * p.a_sk) + p.m <= p.a_sk && (ob - qb * p.b_sn) + p.k <= p.b_sn &&
          qa + ((p.k + 31) & ~31) <= rows_a && qb + p.n <= rows_b;
   }
-  ok = __syncthreads_and(ok) != 0;
-  if (threadIdx.x == 0) *ok_out = ok ? 1 : 0;
+  if (!ok) *ok_out = 0;
 }
 
-__device__ int g_tf32_box_ok[256];  // one verdict slot per launch (round robin)
+__device__ int g_box_ok[256];  // one verdict slot per launch (round robin)
+
+// Launch the entry check ahead of a box launch whose entries are not known to be boxes on the
+// host; the main kernel reads the verdict (false: the whole launch gathers).
+bool attach_box_check(GenericParams& q, uint64_t rows_a, uint64_t rows_b, cudaStream_t stream) {
+  static int* slots = nullptr;
+  static std::atomic<unsigned> next{0};
+  if (slots == nullptr && cudaGetSymbolAddress(reinterpret_cast<void**>(&slots), g_box_ok) != cudaSuccess) {
+    slots = nullptr;
+    return false;
+  }
+  int* ok = slots + (next.fetch_add(1) & 255u);
+  const int64_t entries = static_cast<int64_t>(q.n_jobs) * q.batch;
+  if (cudaMemsetAsync(ok, 1, sizeof(int), stream) != cudaSuccess) return false;  // 0x01010101: true
+  g_launches.fetch_add(1);
+  box_check_kernel<<<static_cast<unsigned>((entries + 255) / 256), 256, 0, stream>>>(
+      q, static_cast<int64_t>(rows_a), static_cast<int64_t>(rows_b), ok);
+  q.tma_ok = ok;
+  return true;
+}
 
 }  // namespace
 
@@ -596,6 +646,7 @@ int launch_brgemm_generic(const GenericParams& p, int compute_tf32, cudaStream_t
         encode_tmap(&q.map_aop, p.a_base, true, 2, da, sa, ba) == BRK_OK)
       q.tma = 1;
     q.all_tma = 0;
+    if (q.tma && p.mode != kModeStride && !attach_box_check(q, rows_a, rows_b, stream)) q.tma = 0;
     if (q.tma && p.mode == kModeStride && p.stride_a % p.a_sk == 0 && p.jstride_a % p.a_sk == 0 &&
         p.stride_b % p.b_sn == 0 && p.jstride_b % p.b_sn == 0 &&
         static_cast<int64_t>(p.n_jobs) * (p.jstride_a / p.a_sk + p.batch * (p.stride_a / p.a_sk)) < (1ll << 31) &&
@@ -652,17 +703,11 @@ int launch_brgemm_generic(const GenericParams& p, int compute_tf32, cudaStream_t
     const uint64_t db[2] = {static_cast<uint64_t>(p.b_sn), rows_b}, sb[2] = {1, static_cast<uint64_t>(p.b_sn)};
     const uint64_t da[2] = {static_cast<uint64_t>(p.a_sk), rows_a}, sa[2] = {1, static_cast<uint64_t>(p.a_sk)};
     const uint32_t bb[2] = {32, static_cast<uint32_t>(q.nbox)}, ba[2] = {32, 32};
-    static int* slots = nullptr;
-    static std::atomic<unsigned> next{0};
-    if (slots == nullptr) cudaGetSymbolAddress(reinterpret_cast<void**>(&slots), g_tf32_box_ok);
-    if (slots != nullptr && encode_tmap(&q.map_bop, p.b_base, false, 2, db, sb, bb) == BRK_OK &&
-        encode_tmap(&q.map_aop, p.a_base, false, 2, da, sa, ba, /*atom32=*/true) == BRK_OK) {
-      int* ok = slots + (next.fetch_add(1) & 255u);
-      g_launches.fetch_add(1);
-      tf32_box_check_kernel<<<1, 1024, 0, stream>>>(q, static_cast<int64_t>(rows_a), static_cast<int64_t>(rows_b), ok);
+    if (encode_tmap(&q.map_bop, p.b_base, false, 2, db, sb, bb) == BRK_OK &&
+        encode_tmap(&q.map_aop, p.a_base, false, 2, da, sa, ba, /*atom32=*/true) == BRK_OK &&
+        attach_box_check(q, rows_a, rows_b, stream)) {
       q.tma = 1;
       q.all_tma = 0;
-      q.tma_ok = ok;
     }
   }
   cudaError_t err;

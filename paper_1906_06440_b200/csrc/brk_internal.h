@@ -21,7 +21,8 @@ struct GenericParams {
   // reference b buffer ([rows][b_sn], box 64 k x nbox rows) and of the reference a
   // buffer ([rows][a_sk], box abox m x 64 k), 128B swizzle.  An entry whose block
   // start (element offset o) satisfies o % ld + extent <= ld is one box per operand
-  // at (o % ld + k0, o / ld + row0); other entries take the cp.async gather.
+  // at (o % ld + k0, o / ld + row0).  A launch boxes every entry or gathers every entry
+  // (tma_ok: the device check of the offset / address tables).
   alignas(64) CUtensorMap map_bop;
   alignas(64) CUtensorMap map_aop;
   int tma, nbox, abox;
@@ -29,8 +30,8 @@ struct GenericParams {
   // box per operand at view row job * rj + i * rs (no per-entry division, no gather work)
   int all_tma;
   int64_t rs_a, rj_a, rs_b, rj_b;
-  // TF32 offset / address-with-views launches: device flag written by a check kernel just
-  // before (1: every entry is one in-view box per operand, so the launch runs like all_tma)
+  // offset / address-with-views launches: device flag written by a check kernel just before
+  // (1: every entry is one in-view box per operand, so the launch runs like all_tma)
   const int* tma_ok;
   int mode;    // EntryMode
   int n_jobs;  // number of independent output blocks C_j
