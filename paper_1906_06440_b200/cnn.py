@@ -203,13 +203,16 @@ def _pad_device(x, pad_h, pad_w):
 
 def _engine_ok(spec: "ConvSpec", dt, pass_: str, engine: bool | None) -> bool:
     """Whether a pass runs on the implicit-GEMM tcgen05 engine (brk_conv_*):
-    bf16 storage, 64-channel blocks, stride 1 or 1x1 stride 2 (include/brk.h).
-    Everything else (fp32/TF32, other blockings, the 3-channel stem) runs on the
-    grouped BRGEMM path, which follows the reference's batch lists directly."""
+    bf16 storage (and fp32 storage / TF32 for the forward pass and the stride-1
+    backward-data pass), 64-channel blocks, stride 1 or 1x1 stride 2 (include/brk.h).
+    Everything else (the TF32 weight update and 1x1 stride-2 backward-data, other blockings,
+    the 3-channel stem) runs on the grouped BRGEMM path,
+    which follows the reference's batch lists directly."""
     torch = require_cuda()
     if engine is False or os.environ.get("BRK_CONV_ENGINE", "1") == "0":
         return False
-    ok = (dt == torch.bfloat16 and spec.b_c == 64 and spec.b_k == 64 and spec.c % 64 == 0
+    dt_ok = dt == torch.bfloat16 or (dt == torch.float32 and (pass_ == "fwd" or (pass_ == "bwd" and spec.stride == 1)))
+    ok = (dt_ok and spec.b_c == 64 and spec.b_k == 64 and spec.c % 64 == 0
           and spec.k % 64 == 0 and max(spec.pad_h, spec.pad_w) <= 15 and max(spec.r, spec.s) <= 16)
     if ok and spec.stride == 1:
         if pass_ == "bwd":
@@ -342,8 +345,9 @@ def conv2d_forward(spec: ConvSpec, inp: BlockedTensor, wgt: BlockedTensor, strat
     if _engine_ok(spec, dt, "fwd", engine):
         x, w = _stage(inp, dt), _stage(wgt, dt)
         out = torch.empty((spec.n, spec.k_blocks, spec.out_h, spec.out_w, spec.b_k), dtype=dt, device="cuda")
+        code = _lib.BRK_BF16 if dt == torch.bfloat16 else _lib.BRK_F32
         _lib.check(_lib.load().brk_conv_fwd(x.data_ptr(), w.data_ptr(), None, out.data_ptr(), *_geom(spec), 64, 64,
-                                            0, _lib.BRK_BF16, stream_ptr()), LayoutError)
+                                            0, code, stream_ptr()), LayoutError)
         res = BlockedTensor(out, n_outer=4, logical_dims={"n": 0, "k": (1, 4), "p": 2, "q": 3})
         return res.to("cpu") if host else res
     x = _pad_device(_stage(inp, dt), spec.pad_h, spec.pad_w)
@@ -408,8 +412,9 @@ def conv2d_backward_data(spec: ConvSpec, dout: BlockedTensor, wgt: BlockedTensor
         return res.to("cpu") if host else res
     if _engine_ok(spec, dt, "bwd", engine):
         din = torch.empty((spec.n, spec.c_blocks, spec.h, spec.w, spec.b_c), dtype=dt, device="cuda")
+        code = _lib.BRK_BF16 if dt == torch.bfloat16 else _lib.BRK_F32
         _lib.check(_lib.load().brk_conv_bwd_data(do.data_ptr(), w.data_ptr(), din.data_ptr(), *_geom(spec), 64, 64,
-                                                 _lib.BRK_BF16, stream_ptr()), LayoutError)
+                                                 code, stream_ptr()), LayoutError)
         res = BlockedTensor(din, n_outer=4, logical_dims={"n": 0, "c": (1, 4), "h": 2, "w": 3})
         return res.to("cpu") if host else res
     n, kb_n, cb_n, r_n, s_n = spec.n, spec.k_blocks, spec.c_blocks, spec.r, spec.s

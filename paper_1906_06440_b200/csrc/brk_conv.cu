@@ -47,9 +47,11 @@ struct ConvGeom {
   int N, C, K, H, W, R, S, stride, pad_h, pad_w, P, Q;
 };
 
-int check_conv(const ConvGeom& g, int b_c, int b_k, int dtype) {
+int check_conv(const ConvGeom& g, int b_c, int b_k, int dtype, bool f32_ok = false) {
   char buf[256];
-  if (dtype != BRK_BF16) return set_error(BRK_ERR_CONTRACT, "conv engine path: bf16 storage only");
+  if (dtype != BRK_BF16 && !(f32_ok && dtype == BRK_F32))
+    return set_error(BRK_ERR_CONTRACT, f32_ok ? "conv engine path: bf16 or fp32 (TF32) storage"
+                                              : "conv engine path: bf16 storage only");
   if (b_c != kB || b_k != kB) {
     std::snprintf(buf, sizeof(buf), "conv engine path needs b_c=b_k=64, got (%d,%d)", b_c, b_k);
     return set_error(BRK_ERR_CONTRACT, buf);
@@ -144,6 +146,18 @@ int im2col_map(CUtensorMap* map, const void* ptr, int N, int X, int Hh, int Ww, 
   const int upper[3] = {pad_w - (S - 1), pad_h - (R - 1), 2};
   const uint32_t es[5] = {1, (uint32_t)stride, (uint32_t)stride, 1, 1};
   return encode_tmap_im2col(map, ptr, dims, strides, lower, upper, kB, pixels, es);
+}
+
+// fp32 activations for TF32 (same dims; boxes of 32 channels = one 128-byte row per pixel)
+int im2col_map_f32(CUtensorMap* map, const void* ptr, int N, int X, int Hh, int Ww, int R, int S, int stride,
+                   int pad_h, int pad_w, uint32_t pixels) {
+  const uint64_t dims[5] = {kB, (uint64_t)Ww, (uint64_t)Hh, (uint64_t)N, (uint64_t)(X / kB)};
+  const uint64_t hw = (uint64_t)Hh * Ww * kB;
+  const uint64_t strides[5] = {1, kB, (uint64_t)Ww * kB, (uint64_t)(X / kB) * hw, hw};
+  const int lower[3] = {-pad_w, -pad_h, 0};
+  const int upper[3] = {pad_w - (S - 1), pad_h - (R - 1), 2};
+  const uint32_t es[5] = {1, (uint32_t)stride, (uint32_t)stride, 1, 1};
+  return encode_tmap_im2col(map, ptr, dims, strides, lower, upper, 32, pixels, es, /*f32=*/true);
 }
 
 // Weights [K_b][C_b][R][S][64 c][64 k]: dims (64 k, 64 c, RS, C_b, K_b)
@@ -261,10 +275,64 @@ BRK_API int brk_conv_fwd(const void* in, const void* w, const float* bias, void*
                          int W, int R, int S, int stride, int pad_h, int pad_w, int b_c, int b_k, int act, int dtype,
                          void* stream) {
   const ConvGeom g = geom(N, C, K, H, W, R, S, stride, pad_h, pad_w);
-  int rc = check_conv(g, b_c, b_k, dtype);
+  int rc = check_conv(g, b_c, b_k, dtype, /*f32_ok=*/true);
   if (rc) return rc;
   if (act < kActNone || act > kActSigmoid) return set_error(BRK_ERR_CONTRACT, "unknown activation");
   const int64_t rows = static_cast<int64_t>(N) * g.P * g.Q;
+  if (dtype == BRK_F32) {
+    // TF32: k-steps of 32 channels, digits (channel half, s, r, c_b); A = fp32 im2col boxes of
+    // 128 pixels x 32 channels (K-major), B = the weights' MN-major 32-element atoms (the
+    // 32 B-chunk 128B swizzle), two per 64 output channels; one 64-channel K block per CTA row
+    // block (CTA pairs of BN = 128, or single CTAs of BN = 64)
+    const bool pair = K % 128 == 0;
+    const int bn = pair ? 128 : 64;
+    EngineParams p;
+    init_params(p);
+    if ((rc = im2col_map_f32(&p.map_a, in, N, C, H, W, R, S, stride, pad_h, pad_w, 128))) return rc;
+    p.ca.kdiv0 = 2;
+    p.ca.kdiv1 = S;
+    p.ca.kdiv2 = R;
+    p.ca.kc[0][0] = 32;  // channel half
+    p.ca.kc[3][4] = 1;   // channel block c_b = d3
+    p.ca.ok[0][1] = 1;   // w tap = s
+    p.ca.ok[1][2] = 1;   // h tap = r
+    p.ca.n_loads = 1;
+    p.ca.load_bytes = 128 * 128;
+    p.ca.mn_major = 0;
+    pixel_walk(p.ca, 1, g.P, g.Q, stride, pad_h, pad_w, rows);
+    {  // W[kb][c_b][rs][64 c][64 k] fp32 as (32 k_lo, 2 k_hi, 64 c, RS * C_b * K_b)
+      const uint64_t dims[4] = {32, 2, kB, static_cast<uint64_t>(R) * S * (C / kB) * (K / kB)};
+      const uint64_t strides[4] = {1, 32, kB, kB * kB};
+      const uint32_t box[4] = {32, 1, 32, 1};
+      if ((rc = encode_tmap(&p.map_b, w, false, 4, dims, strides, box, /*atom32=*/true))) return rc;
+    }
+    p.cb.kdiv0 = 2;
+    p.cb.kdiv1 = S;
+    p.cb.kdiv2 = R;
+    p.cb.kc[0][2] = 32;               // c rows of the half
+    p.cb.kc[1][3] = 1;                // s
+    p.cb.kc[2][3] = S;                // r
+    p.cb.kc[3][3] = R * S;            // c_b
+    p.cb.rc[3] = R * S * (C / kB);    // k_b = the CTA's row block
+    p.cb.lc[1] = 1;                   // load l = k_hi atom
+    p.cb.n_loads = 2;
+    p.cb.load_bytes = 32 * 128;
+    p.cb.mn_major = 1;
+    p.cb.ndims = 4;
+    p.m_tiles = static_cast<int>((rows + (pair ? 255 : 127)) / (pair ? 256 : 128));
+    p.n_tiles = K / bn;
+    p.k_steps = 2 * (C / kB) * R * S;
+    p.rows = static_cast<int>(rows);
+    p.cols = K;
+    p.out = out;
+    p.out_bf16 = 0;
+    const int64_t pq = static_cast<int64_t>(g.P) * g.Q;
+    p.om = OutMap{pq, 0, kB, kB, pq * kB, 1, pq, (int64_t)(K / kB) * pq * kB};
+    p.bias = bias;
+    p.act = act;
+    g_launches.fetch_add(1);
+    return launch_engine(p, bn, 1, pair ? 1 : 0, 0, static_cast<cudaStream_t>(stream));
+  }
   const int k_steps = (C / kB) * R * S;
   const ConvPlan pl = choose(rows, K, k_steps, false, 2.0 * N * C * H * W, 2.0 * K * C * R * S,
                              2.0 * N * K * g.P * g.Q);
@@ -313,7 +381,7 @@ BRK_API int brk_conv_fwd(const void* in, const void* w, const float* bias, void*
 BRK_API int brk_conv_bwd_data(const void* dout, const void* w, void* din, int N, int C, int K, int H, int W, int R,
                               int S, int stride, int pad_h, int pad_w, int b_c, int b_k, int dtype, void* stream) {
   const ConvGeom g = geom(N, C, K, H, W, R, S, stride, pad_h, pad_w);
-  int rc = check_conv(g, b_c, b_k, dtype);
+  int rc = check_conv(g, b_c, b_k, dtype, /*f32_ok=*/stride == 1);
   if (rc) return rc;
   if (stride == 1 && (g.P != H || g.Q != W))
     return set_error(BRK_ERR_CONTRACT, "conv bwd engine path: stride 1 needs same padding");
@@ -321,6 +389,57 @@ BRK_API int brk_conv_bwd_data(const void* dout, const void* w, void* din, int N,
     return set_error(BRK_ERR_CONTRACT, "conv bwd engine path: 1x1 stride 2 needs even H, W");
   EngineParams p;
   init_params(p);
+  if (dtype == BRK_F32) {
+    // TF32 (stride 1): the dual convolution with k-steps of 32 output channels, digits
+    // (channel half, s', r', k_b); A = fp32 im2col boxes of dO, B = the flipped weights read
+    // K-major (rows c, 32 contiguous k = one 128-byte row), one 64-channel C block per CTA row block
+    const bool pair = C % 128 == 0;
+    const int bn = pair ? 128 : 64;
+    const int64_t rows = static_cast<int64_t>(N) * H * W;
+    const int dph = R - 1 - pad_h, dpw = S - 1 - pad_w;
+    if ((rc = im2col_map_f32(&p.map_a, dout, N, K, g.P, g.Q, R, S, 1, dph, dpw, 128))) return rc;
+    p.ca.kdiv0 = 2;
+    p.ca.kdiv1 = S;
+    p.ca.kdiv2 = R;
+    p.ca.kc[0][0] = 32;  // channel half
+    p.ca.kc[3][4] = 1;   // output-channel block k_b = d3
+    p.ca.ok[0][1] = 1;   // w tap = s'
+    p.ca.ok[1][2] = 1;   // h tap = r'
+    p.ca.n_loads = 1;
+    p.ca.load_bytes = 128 * 128;
+    p.ca.mn_major = 0;
+    pixel_walk(p.ca, 1, H, W, 1, dph, dpw, rows);
+    {  // W[kb][c_b][rs][64 c][64 k] fp32 as (32 k_lo, 2 k_hi, 64 c, RS * C_b * K_b)
+      const uint64_t dims[4] = {32, 2, kB, static_cast<uint64_t>(R) * S * (C / kB) * (K / kB)};
+      const uint64_t strides[4] = {1, 32, kB, kB * kB};
+      const uint32_t box[4] = {32, 1, kB, 1};
+      if ((rc = encode_tmap(&p.map_b, w, false, 4, dims, strides, box))) return rc;
+    }
+    p.cb.kdiv0 = 2;
+    p.cb.kdiv1 = S;
+    p.cb.kdiv2 = R;
+    p.cb.kc[0][1] = 1;                 // k_hi = the channel half
+    p.cb.base[3] = R * S - 1;          // flipped tap (R-1-r')*S + (S-1-s')
+    p.cb.kc[1][3] = -1;
+    p.cb.kc[2][3] = -S;
+    p.cb.rc[3] = R * S;                // c_b = the CTA's row block
+    p.cb.kc[3][3] = R * S * (C / kB);  // k_b
+    p.cb.n_loads = 1;
+    p.cb.load_bytes = kB * 128;
+    p.cb.mn_major = 0;
+    p.cb.ndims = 4;
+    p.m_tiles = static_cast<int>((rows + (pair ? 255 : 127)) / (pair ? 256 : 128));
+    p.n_tiles = C / bn;
+    p.k_steps = 2 * (K / kB) * R * S;
+    p.rows = static_cast<int>(rows);
+    p.cols = C;
+    p.out = din;
+    p.out_bf16 = 0;
+    const int64_t hw = static_cast<int64_t>(H) * W;
+    p.om = OutMap{hw, 0, kB, kB, hw * kB, 1, hw, (int64_t)(C / kB) * hw * kB};
+    g_launches.fetch_add(1);
+    return launch_engine(p, bn, 1, pair ? 1 : 0, 0, static_cast<cudaStream_t>(stream));
+  }
   // rows: input pixels (stride 1) or output pixels scattered to (2p, 2q) (stride 2)
   const int64_t rows = stride == 1 ? static_cast<int64_t>(N) * H * W : static_cast<int64_t>(N) * g.P * g.Q;
   const int k_steps = (K / kB) * R * S;

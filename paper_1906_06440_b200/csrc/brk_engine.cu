@@ -82,10 +82,12 @@ template <bool kPair>
 __device__ __forceinline__ void issue_operand(const CUtensorMap* map, const OperandCoords& oc, int rowblk, int s,
                                               uint8_t* dst, uint64_t* bar) {
   const int d0 = s % oc.kdiv0, t = s / oc.kdiv0;
-  const int d1 = t % oc.kdiv1, d2 = t / oc.kdiv1;
+  const int d1 = t % oc.kdiv1, t2 = t / oc.kdiv1;
+  const int d2 = oc.kdiv2 > 0 ? t2 % oc.kdiv2 : t2, d3 = oc.kdiv2 > 0 ? t2 / oc.kdiv2 : 0;
   int32_t cs[5];
 #pragma unroll
-  for (int d = 0; d < 5; ++d) cs[d] = oc.base[d] + oc.rc[d] * rowblk + oc.kc[0][d] * d0 + oc.kc[1][d] * d1 + oc.kc[2][d] * d2;
+  for (int d = 0; d < 5; ++d)
+    cs[d] = oc.base[d] + oc.rc[d] * rowblk + oc.kc[0][d] * d0 + oc.kc[1][d] * d1 + oc.kc[2][d] * d2 + oc.kc[3][d] * d3;
   uint16_t off[3] = {0, 0, 0};
   if (oc.kind != 0) {
     // implicit-GEMM pixel walk: first pixel of this box -> (n, p, q)

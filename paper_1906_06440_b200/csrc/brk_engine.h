@@ -18,7 +18,8 @@ constexpr int kEngineBM = 128;  // tile rows per CTA = TMEM lanes
 
 // How one operand's k-step box(es) are located.  The k-step s is split into
 // mixed-radix digits d0 = s % kdiv0, d1 = (s / kdiv0) % kdiv1,
-// d2 = s / (kdiv0 * kdiv1) (e.g. conv: (s, r, c_b)); then for load l:
+// d2 = s / (kdiv0 * kdiv1) (e.g. conv: (s, r, c_b)) — or, with kdiv2 set, d2 = that % kdiv2
+// and d3 = that / kdiv2 (TF32 conv: (channel half, s, r, c_b)); then for load l:
 //   coord[d] = base[d] + rc[d]*rowblk + sum_j kc[j][d]*d_j + lc[d]*l
 // and each load writes load_bytes to consecutive smem.
 //
@@ -39,9 +40,10 @@ constexpr int kEngineBM = 128;  // tile rows per CTA = TMEM lanes
 struct OperandCoords {
   int32_t base[5];
   int32_t rc[5];
-  int32_t kc[3][5];
+  int32_t kc[4][5];
   int32_t lc[5];
   int32_t kdiv0, kdiv1;
+  int32_t kdiv2;  // 0: no fourth digit (d2 = s / (kdiv0 * kdiv1)); else d2 = that % kdiv2, d3 = that / kdiv2
   int32_t n_loads;
   uint32_t load_bytes;
   int32_t mn_major;  // 0: K-major rows of 128 B; 1: MN-major 64-wide atoms

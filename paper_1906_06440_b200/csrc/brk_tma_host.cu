@@ -63,7 +63,7 @@ std::once_flag g_once_im2col;
 
 int encode_tmap_im2col(CUtensorMap* out, const void* ptr, const uint64_t* dims, const uint64_t* strides_elems,
                        const int* lower, const int* upper, uint32_t channels, uint32_t pixels,
-                       const uint32_t* estrides) {
+                       const uint32_t* estrides, bool f32) {
   std::call_once(g_once_im2col, [] {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -77,9 +77,9 @@ int encode_tmap_im2col(CUtensorMap* out, const void* ptr, const uint64_t* dims, 
   for (int d = 0; d < 5; ++d) {
     gdim[d] = dims[d];
     es[d] = estrides[d];
-    if (d > 0) gstride[d - 1] = strides_elems[d] * 2;
+    if (d > 0) gstride[d - 1] = strides_elems[d] * (f32 ? 4 : 2);
   }
-  CUresult r = g_encode_im2col(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(ptr), gdim, gstride,
+  CUresult r = g_encode_im2col(out, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(ptr), gdim, gstride,
                                lower, upper, channels, pixels, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);

@@ -12,11 +12,11 @@ namespace brk {
 int encode_tmap(CUtensorMap* out, const void* ptr, bool bf16, int ndims, const uint64_t* dims,
                 const uint64_t* strides_elems, const uint32_t* box, bool atom32 = false);
 
-// im2col-mode map over a 5-d bf16 tensor (C, W, H, D, N): lower/upper are the
+// im2col-mode map over a 5-d bf16 (or fp32) tensor (C, W, H, D, N): lower/upper are the
 // pixel bounding-box corners of the 3 spatial dims, estrides the traversal
 // strides of all 5 dims.  128B swizzle, zero OOB fill.
 int encode_tmap_im2col(CUtensorMap* out, const void* ptr, const uint64_t* dims, const uint64_t* strides_elems,
                        const int* lower, const int* upper, uint32_t channels, uint32_t pixels,
-                       const uint32_t* estrides);
+                       const uint32_t* estrides, bool f32 = false);
 
 }  // namespace brk

@@ -123,3 +123,47 @@ def test_engine_matches_grouped_path():
     a = conv2d_forward(spec, inp, wgt, engine=True).data.float()
     b = conv2d_forward(spec, inp, wgt, engine=False).data.float()
     assert (a - b).abs().max().item() <= 1e-2 * b.abs().max().item()
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_engine_tf32_forward(case):
+    """fp32 storage, TF32 MMAs on the engine (k-steps of 32 channels: fp32 im2col boxes, the
+    weights' MN-major 32-element atoms): integer inputs exact, random inputs within the TF32
+    bound of the north star (1e-3), and the same numbers as the grouped TF32 path's bound."""
+    rng = np.random.default_rng(300 + sum(case))
+    for integer in (True, False):
+        spec, i, w, _ = _tensors(case, rng, integer)
+        if not integer:
+            i = rng.uniform(-1, 1, i.shape).astype(F32)
+            w = rng.uniform(-1, 1, w.shape).astype(F32)
+        inp, wgt = block_conv_tensors(i, w, 64, 64)
+        inp, wgt = inp.to("cuda", torch.float32), wgt.to("cuda", torch.float32)
+        got = unblock_conv_output(conv2d_forward(spec, inp, wgt, engine=True, precision="tf32").to("cpu"))
+        ref = orc.conv2d_forward_reference(i, w, spec.stride)
+        got = np.asarray(got, dtype=np.float64)
+        if integer:
+            assert np.array_equal(got, ref), case
+        else:
+            assert orc.scale_rel_error(got, ref) <= 1e-3, case
+
+
+@pytest.mark.parametrize("case", [c for c in CASES if c[6] == 1])
+def test_engine_tf32_backward_data(case):
+    """fp32 storage, TF32 backward-data on the engine (stride 1; k-steps of 32 output channels,
+    the flipped weights read K-major): integer inputs exact, random inputs within 1e-3."""
+    rng = np.random.default_rng(400 + sum(case))
+    for integer in (True, False):
+        spec, _, w, do = _tensors(case, rng, integer)
+        if not integer:
+            w = rng.uniform(-1, 1, w.shape).astype(F32)
+            do = rng.uniform(-1, 1, do.shape).astype(F32)
+        _, wgt = block_conv_tensors(np.zeros((spec.n, spec.c, spec.h, spec.w), F32), w, 64, 64)
+        dob = BlockedTensor(block_conv_input(do, 64).data, 4, {"n": 0, "k": (1, 4), "p": 2, "q": 3})
+        wgt, dob = wgt.to("cuda", torch.float32), dob.to("cuda", torch.float32)
+        got = unblock_conv_input(conv2d_backward_data(spec, dob, wgt, engine=True, precision="tf32").to("cpu"))
+        ref = orc.conv2d_backward_data_reference(do, w, (spec.h, spec.w), spec.stride)
+        got = np.asarray(got, dtype=np.float64)
+        if integer:
+            assert np.array_equal(got, ref), case
+        else:
+            assert orc.scale_rel_error(got, ref) <= 1e-3, case
