@@ -203,15 +203,13 @@ def _pad_device(x, pad_h, pad_w):
 
 def _engine_ok(spec: "ConvSpec", dt, pass_: str, engine: bool | None) -> bool:
     """Whether a pass runs on the implicit-GEMM tcgen05 engine (brk_conv_*):
-    bf16 storage (and fp32 storage / TF32 for the forward pass and the stride-1
-    backward-data pass), 64-channel blocks, stride 1 or 1x1 stride 2 (include/brk.h).
-    Everything else (the TF32 weight update and 1x1 stride-2 backward-data, other blockings,
-    the 3-channel stem) runs on the grouped BRGEMM path,
+    bf16 or fp32 (TF32) storage, 64-channel blocks, stride 1 or 1x1 stride 2 (include/brk.h).
+    Everything else (other blockings, the 3-channel stem) runs on the grouped BRGEMM path,
     which follows the reference's batch lists directly."""
     torch = require_cuda()
     if engine is False or os.environ.get("BRK_CONV_ENGINE", "1") == "0":
         return False
-    dt_ok = dt == torch.bfloat16 or (dt == torch.float32 and (pass_ == "fwd" or (pass_ == "bwd" and spec.stride == 1)))
+    dt_ok = dt in (torch.bfloat16, torch.float32)
     ok = (dt_ok and spec.b_c == 64 and spec.b_k == 64 and spec.c % 64 == 0
           and spec.k % 64 == 0 and max(spec.pad_h, spec.pad_w) <= 15 and max(spec.r, spec.s) <= 16)
     if ok and spec.stride == 1:
@@ -511,7 +509,8 @@ def conv2d_weight_update(spec: ConvSpec, inp: BlockedTensor, dout: BlockedTensor
         ws = _workspace(nbytes)
         _lib.check(lib.brk_conv_upd(x.data_ptr(), do.data_ptr(), dw.data_ptr(), None, 0.0,
                                     ws.data_ptr() if nbytes else None, nbytes, *_geom(spec), 64, 64,
-                                    _lib.BRK_BF16, stream_ptr()), LayoutError)
+                                    _lib.BRK_BF16 if dt == torch.bfloat16 else _lib.BRK_F32, stream_ptr()),
+                   LayoutError)
         res = BlockedTensor(dw, n_outer=4, logical_dims={"k": (0, 5), "c": (1, 4), "r": 2, "s": 3})
         return res.to("cpu") if host else res
     x = _pad_device(_stage(inp, dt), spec.pad_h, spec.pad_w)

@@ -381,7 +381,7 @@ BRK_API int brk_conv_fwd(const void* in, const void* w, const float* bias, void*
 BRK_API int brk_conv_bwd_data(const void* dout, const void* w, void* din, int N, int C, int K, int H, int W, int R,
                               int S, int stride, int pad_h, int pad_w, int b_c, int b_k, int dtype, void* stream) {
   const ConvGeom g = geom(N, C, K, H, W, R, S, stride, pad_h, pad_w);
-  int rc = check_conv(g, b_c, b_k, dtype, /*f32_ok=*/stride == 1);
+  int rc = check_conv(g, b_c, b_k, dtype, /*f32_ok=*/true);
   if (rc) return rc;
   if (stride == 1 && (g.P != H || g.Q != W))
     return set_error(BRK_ERR_CONTRACT, "conv bwd engine path: stride 1 needs same padding");
@@ -390,13 +390,14 @@ BRK_API int brk_conv_bwd_data(const void* dout, const void* w, void* din, int N,
   EngineParams p;
   init_params(p);
   if (dtype == BRK_F32) {
-    // TF32 (stride 1): the dual convolution with k-steps of 32 output channels, digits
-    // (channel half, s', r', k_b); A = fp32 im2col boxes of dO, B = the flipped weights read
-    // K-major (rows c, 32 contiguous k = one 128-byte row), one 64-channel C block per CTA row block
+    // TF32: the dual convolution with k-steps of 32 output channels, digits (channel half, s',
+    // r', k_b); A = fp32 im2col boxes of dO, B = the flipped weights read K-major (rows c, 32
+    // contiguous k = one 128-byte row), one 64-channel C block per CTA row block.  1x1 stride 2:
+    // rows are output pixels scattered to (2p, 2q), the other input pixels zeroed first.
     const bool pair = C % 128 == 0;
     const int bn = pair ? 128 : 64;
-    const int64_t rows = static_cast<int64_t>(N) * H * W;
-    const int dph = R - 1 - pad_h, dpw = S - 1 - pad_w;
+    const int64_t rows = stride == 1 ? static_cast<int64_t>(N) * H * W : static_cast<int64_t>(N) * g.P * g.Q;
+    const int dph = stride == 1 ? R - 1 - pad_h : 0, dpw = stride == 1 ? S - 1 - pad_w : 0;
     if ((rc = im2col_map_f32(&p.map_a, dout, N, K, g.P, g.Q, R, S, 1, dph, dpw, 128))) return rc;
     p.ca.kdiv0 = 2;
     p.ca.kdiv1 = S;
@@ -408,7 +409,8 @@ BRK_API int brk_conv_bwd_data(const void* dout, const void* w, void* din, int N,
     p.ca.n_loads = 1;
     p.ca.load_bytes = 128 * 128;
     p.ca.mn_major = 0;
-    pixel_walk(p.ca, 1, H, W, 1, dph, dpw, rows);
+    if (stride == 1) pixel_walk(p.ca, 1, H, W, 1, dph, dpw, rows);
+    else pixel_walk(p.ca, 1, g.P, g.Q, 1, 0, 0, rows);
     {  // W[kb][c_b][rs][64 c][64 k] fp32 as (32 k_lo, 2 k_hi, 64 c, RS * C_b * K_b)
       const uint64_t dims[4] = {32, 2, kB, static_cast<uint64_t>(R) * S * (C / kB) * (K / kB)};
       const uint64_t strides[4] = {1, 32, kB, kB * kB};
@@ -436,7 +438,15 @@ BRK_API int brk_conv_bwd_data(const void* dout, const void* w, void* din, int N,
     p.out = din;
     p.out_bf16 = 0;
     const int64_t hw = static_cast<int64_t>(H) * W;
-    p.om = OutMap{hw, 0, kB, kB, hw * kB, 1, hw, (int64_t)(C / kB) * hw * kB};
+    if (stride == 1) {
+      p.om = OutMap{hw, 0, kB, kB, hw * kB, 1, hw, (int64_t)(C / kB) * hw * kB};
+    } else {
+      const int64_t pq = static_cast<int64_t>(g.P) * g.Q;
+      p.om = OutMap{g.Q, 2 * (int64_t)W * kB, 2 * kB, kB, hw * kB, 1, pq, (int64_t)(C / kB) * hw * kB};
+      const cudaError_t err =
+          cudaMemsetAsync(din, 0, static_cast<size_t>(N) * C * H * W * sizeof(float), static_cast<cudaStream_t>(stream));
+      if (err != cudaSuccess) return set_cuda_error(err, "conv bwd: zeroing dX");
+    }
     g_launches.fetch_add(1);
     return launch_engine(p, bn, 1, pair ? 1 : 0, 0, static_cast<cudaStream_t>(stream));
   }
@@ -506,7 +516,7 @@ BRK_API int brk_conv_upd(const void* in, const void* dout, float* dw, void* w_sg
                          size_t ws_bytes, int N, int C, int K, int H, int W, int R, int S, int stride, int pad_h,
                          int pad_w, int b_c, int b_k, int dtype, void* stream) {
   const ConvGeom g = geom(N, C, K, H, W, R, S, stride, pad_h, pad_w);
-  int rc = check_conv(g, b_c, b_k, dtype);
+  int rc = check_conv(g, b_c, b_k, dtype, /*f32_ok=*/true);
   if (rc) return rc;
   ConvPlan pl = upd_plan(g);
   if (pl.bn == 0) return set_error(BRK_ERR_CONTRACT, "conv upd: no engine tile fits K");
@@ -518,6 +528,78 @@ BRK_API int brk_conv_upd(const void* in, const void* dout, float* dw, void* w_sg
   const int64_t atoms = static_cast<int64_t>(C / kB) * R * S;
   EngineParams p;
   init_params(p);
+  if (dtype == BRK_F32) {
+    // TF32, tile mode: a k-step is a block of 32 output pixels (bw x bh, bw >= Q when Q <= 32,
+    // else row pieces of 32) of one image; A = 32-channel atoms of the input block shifted by each
+    // atom's tap (padding and slots past Q / P read as out-of-bounds zeros; the latter meet dO
+    // zeros) — for 1x1 stride 2 every other input pixel (TMA traversal strides of 2), B = dO's
+    // block as two 32-channel atoms of the CTA's 64 output channels; both MN-major TF32 atoms
+    // (32 B-chunk swizzle).  CTA pairs of BN = 128 or single CTAs of BN = 64.
+    if (w_sgd != nullptr) return set_error(BRK_ERR_CONTRACT, "conv upd: fused SGD needs bf16 weights");
+    const bool pair = K % 128 == 0;
+    const int bn = pair ? 128 : 64;
+    int bw = 1;
+    while (bw < g.Q && bw < 32) bw *= 2;
+    const int bh = 32 / bw, qb = (g.Q + bw - 1) / bw, pg = (g.P + bh - 1) / bh;
+    auto map4 = [&](CUtensorMap* m, const void* ptr, int X, int hh, int ww, uint32_t st) {
+      const uint64_t dims[4] = {kB, static_cast<uint64_t>(ww), static_cast<uint64_t>(hh),
+                                static_cast<uint64_t>(N) * (X / kB)};
+      const uint64_t strides[4] = {1, kB, static_cast<uint64_t>(ww) * kB, static_cast<uint64_t>(hh) * ww * kB};
+      const uint32_t box[4] = {32, static_cast<uint32_t>(bw) * st, static_cast<uint32_t>(bh) * st, 1};
+      const uint32_t es[4] = {1, st, st, 1};
+      return encode_tmap(m, ptr, false, 4, dims, strides, box, /*atom32=*/true, es);
+    };
+    if ((rc = map4(&p.map_a, in, C, H, W, static_cast<uint32_t>(stride))) ||
+        (rc = map4(&p.map_b, dout, K, g.P, g.Q, 1)))
+      return rc;
+    for (OperandCoords* oc : {&p.ca, &p.cb}) {  // k-step s = ((n * pg + row group) * qb + column block)
+      oc->kdiv0 = qb;
+      oc->kdiv1 = pg;
+      oc->kc[0][1] = bw;
+      oc->kc[1][2] = bh;
+      oc->load_bytes = 32 * 128;
+      oc->mn_major = 1;
+      oc->ndims = 4;
+    }
+    p.ca.base[1] = -pad_w;
+    p.ca.base[2] = -pad_h;
+    p.ca.kc[0][1] = bw * stride;
+    p.ca.kc[1][2] = bh * stride;
+    p.ca.kc[2][3] = C / kB;
+    p.ca.n_loads = 4;
+    p.ca.atom_cb = C / kB;
+    p.ca.atom_s = S;
+    p.ca.kind = 5;
+    p.cb.kc[2][3] = K / kB;
+    p.cb.rc[3] = 1;   // k_b = the CTA's row block
+    p.cb.lc[0] = 32;  // load l = channel half
+    p.cb.n_loads = 2;
+    p.k_steps = N * pg * qb;
+    if (pl.splits > 1) {  // the workspace holds upd_plan's splits; re-plan them for these k-steps
+      const int per = (p.k_steps + pl.splits - 1) / pl.splits;
+      pl.splits = (p.k_steps + per - 1) / per;
+    }
+    p.m_tiles = static_cast<int>((atoms * kB + (pair ? 255 : 127)) / (pair ? 256 : 128));
+    p.n_tiles = K / bn;
+    p.rows = static_cast<int>(atoms * kB);
+    p.cols = K;
+    p.out_bf16 = 0;
+    const int64_t rs_n = static_cast<int64_t>(R) * S;
+    p.om = OutMap{kB, rs_n * kB * kB, kB, kB, (int64_t)(C / kB) * rs_n * kB * kB, 1, (int64_t)(C / kB) * kB,
+                  kB * kB};
+    if (pl.splits > 1) {
+      p.k_splits = pl.splits;
+      p.split_slice = dw_elems;
+      p.out = workspace;
+    } else {
+      p.out = dw;
+    }
+    g_launches.fetch_add(1);
+    rc = launch_engine(p, bn, 1, pair ? 1 : 0, 0, static_cast<cudaStream_t>(stream));
+    if (rc || pl.splits <= 1) return rc;
+    return split_reduce(static_cast<const float*>(workspace), pl.splits, dw_elems, dw, nullptr, 0.0f,
+                        static_cast<cudaStream_t>(stream));
+  }
   // 1x1 stride-1 convolutions: tile-mode boxes of 64 pixels x 64 channels per image (k-steps
   // aligned to images, the tail of an image's last box zero-filled out of bounds) instead of the
   // im2col pixel walk: im2col-mode boxes streamed at ~28 B/clk per SM (tools/probes/

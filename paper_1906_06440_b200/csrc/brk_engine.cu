@@ -89,7 +89,7 @@ __device__ __forceinline__ void issue_operand(const CUtensorMap* map, const Oper
   for (int d = 0; d < 5; ++d)
     cs[d] = oc.base[d] + oc.rc[d] * rowblk + oc.kc[0][d] * d0 + oc.kc[1][d] * d1 + oc.kc[2][d] * d2 + oc.kc[3][d] * d3;
   uint16_t off[3] = {0, 0, 0};
-  if (oc.kind != 0) {
+  if (oc.kind != 0 && oc.kind != 5) {
     // implicit-GEMM pixel walk: first pixel of this box -> (n, p, q)
     int pix = oc.kind == 1 ? rowblk * kEngineBM : s * 64;
     if (pix >= oc.total_pix) pix = oc.total_pix - 1;  // rows-side only (masked rows)
@@ -109,7 +109,17 @@ __device__ __forceinline__ void issue_operand(const CUtensorMap* map, const Oper
 #pragma unroll
     for (int d = 0; d < 5; ++d) c[d] = cs[d] + oc.lc[d] * l;
     uint8_t* p = dst + l * oc.load_bytes;
-    if (oc.kind != 0) {
+    if (oc.kind == 5) {
+      // TF32 weight update in tile mode: load l of the row block is the 32-channel atom
+      // a = ((rs * atom_cb + c_b) * 2 + half); its box is the k-step's pixel block shifted by the
+      // tap (r, s), in plane n * C_b + c_b, at channel offset 32 * half
+      const int a = rowblk * oc.n_loads + l, a2 = a >> 1;
+      const int rs = a2 / oc.atom_cb, r = rs / oc.atom_s;
+      c[0] += (a & 1) * 32;
+      c[1] += rs - r * oc.atom_s;
+      c[2] += r;
+      c[3] += a2 - rs * oc.atom_cb;
+    } else if (oc.kind != 0) {
       if (oc.kind == 2) {
         const int atom = rowblk * oc.n_loads + l;
         const int rs = atom / oc.atom_cb;

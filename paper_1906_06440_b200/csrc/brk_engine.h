@@ -34,6 +34,9 @@ constexpr int kEngineBM = 128;  // tile rows per CTA = TMEM lanes
 //           tap (rs % atom_s, rs / atom_s)  (conv weight update, input side)
 //   kind 3: the reduction runs over pixels, pix = s * 64, no tap offsets
 //           (conv weight update, output-gradient side)
+//   kind 5: tile mode (not im2col), TF32 weight update: atom a = rowblk * n_loads + l is
+//           ((rs * atom_cb + c_b) * 2 + half) and adds (32 half, rs % atom_s, rs / atom_s, c_b)
+//           to coords 0..3
 // pixel -> (n, p, q) adds (q*cstride - pad_w, p*cstride - pad_h, n) to coords
 // 1..3.  The maps' bounding boxes extend two images past N (zero fill), so a
 // pixel walk that runs off the end reads zeros (K-side kinds rely on it).

@@ -18,7 +18,7 @@ std::once_flag g_once;
 }  // namespace
 
 int encode_tmap(CUtensorMap* out, const void* ptr, bool bf16, int ndims, const uint64_t* dims,
-                const uint64_t* strides_elems, const uint32_t* box, bool atom32) {
+                const uint64_t* strides_elems, const uint32_t* box, bool atom32, const uint32_t* estrides) {
   std::call_once(g_once, [] {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -33,7 +33,7 @@ int encode_tmap(CUtensorMap* out, const void* ptr, bool bf16, int ndims, const u
   for (int d = 0; d < ndims; ++d) {
     gdim[d] = dims[d];
     bdim[d] = box[d];
-    estride[d] = 1;
+    estride[d] = estrides != nullptr ? estrides[d] : 1;
     if (d > 0) gstride[d - 1] = strides_elems[d] * esz;
   }
   CUresult r = g_encode(out, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,

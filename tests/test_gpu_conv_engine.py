@@ -147,9 +147,9 @@ def test_engine_tf32_forward(case):
             assert orc.scale_rel_error(got, ref) <= 1e-3, case
 
 
-@pytest.mark.parametrize("case", [c for c in CASES if c[6] == 1])
+@pytest.mark.parametrize("case", CASES)
 def test_engine_tf32_backward_data(case):
-    """fp32 storage, TF32 backward-data on the engine (stride 1; k-steps of 32 output channels,
+    """fp32 storage, TF32 backward-data on the engine (k-steps of 32 output channels,
     the flipped weights read K-major): integer inputs exact, random inputs within 1e-3."""
     rng = np.random.default_rng(400 + sum(case))
     for integer in (True, False):
@@ -162,6 +162,29 @@ def test_engine_tf32_backward_data(case):
         wgt, dob = wgt.to("cuda", torch.float32), dob.to("cuda", torch.float32)
         got = unblock_conv_input(conv2d_backward_data(spec, dob, wgt, engine=True, precision="tf32").to("cpu"))
         ref = orc.conv2d_backward_data_reference(do, w, (spec.h, spec.w), spec.stride)
+        got = np.asarray(got, dtype=np.float64)
+        if integer:
+            assert np.array_equal(got, ref), case
+        else:
+            assert orc.scale_rel_error(got, ref) <= 1e-3, case
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_engine_tf32_weight_update(case):
+    """fp32 storage, TF32 weight update on the engine (tile-mode blocks of 32 output
+    pixels, the taps as coordinate shifts, 32-channel atoms): integer inputs exact, random inputs
+    within 1e-3."""
+    rng = np.random.default_rng(500 + sum(case))
+    for integer in (True, False):
+        spec, i, _, do = _tensors(case, rng, integer)
+        if not integer:
+            i = rng.uniform(-1, 1, i.shape).astype(F32)
+            do = rng.uniform(-1, 1, do.shape).astype(F32)
+        inp, _ = block_conv_tensors(i, np.zeros((spec.k, spec.c, spec.r, spec.s), F32), 64, 64)
+        dob = BlockedTensor(block_conv_input(do, 64).data, 4, {"n": 0, "k": (1, 4), "p": 2, "q": 3})
+        inp, dob = inp.to("cuda", torch.float32), dob.to("cuda", torch.float32)
+        got = unblock_conv_weight(conv2d_weight_update(spec, inp, dob, engine=True, precision="tf32").to("cpu"))
+        ref = orc.conv2d_weight_update_reference(i, do, spec.r, spec.s, spec.stride)
         got = np.asarray(got, dtype=np.float64)
         if integer:
             assert np.array_equal(got, ref), case
