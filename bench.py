@@ -289,6 +289,16 @@ def other_workloads():
                              for r in res["layers"]}}
     except Exception as exc:  # noqa: BLE001 - informational block must not kill the headline line
         out["resnet50_conv_n256"] = {"error": repr(exc)[:300]}
+    try:  # the reference's fp32 storage with TF32 math, the engine layers (the C=3 stem stays bf16-only)
+        res = resnet_suite(n=256, iters=3, layers=list(range(2, 21)), precision="tf32")
+        out["resnet50_conv_n256_tf32"] = {
+            "summary": res["summary"], "peak_tflops": res["peak_tflops"],
+            "note": "layers 2-20 (52 convs weighted by count), fp32 storage, TF32 tcgen05 MMAs, L2 flushed; "
+                    "roofline against the measured TF32 peak",
+            "per_layer_us": {r["id"]: {p: round(r[p]["us"], 1) for p in ("fwd", "bwd", "upd") if r.get(p)}
+                             for r in res["layers"]}}
+    except Exception as exc:  # noqa: BLE001
+        out["resnet50_conv_n256_tf32"] = {"error": repr(exc)[:300]}
     try:
         out["lstm_t50_n168_c1024"] = lstm_suite(iters=2)
     except Exception as exc:  # noqa: BLE001

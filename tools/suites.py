@@ -78,8 +78,9 @@ class _Timer:
         return statistics.fmean(ts), min(ts)
 
 
-def resnet_suite(n=256, iters=10, layers=None, passes=("fwd", "bwd", "upd"), verbose=False):
-    """Per-layer device time of the conv passes at minibatch n (bf16 storage, 64-channel blocks)."""
+def resnet_suite(n=256, iters=10, layers=None, passes=("fwd", "bwd", "upd"), verbose=False, precision="bf16"):
+    """Per-layer device time of the conv passes at minibatch n (64-channel blocks): bf16 storage,
+    or fp32 storage with TF32 math (precision="tf32", roofline against the TF32 peak)."""
     import torch
 
     from paper_1906_06440_b200 import _lib
@@ -88,6 +89,11 @@ def resnet_suite(n=256, iters=10, layers=None, passes=("fwd", "bwd", "upd"), ver
 
     lib = _lib.load()
     peak, hbm, src = _peaks()
+    tf32 = precision == "tf32"
+    if tf32:
+        peak = _tf32_peak(peak)
+    dt = torch.float32 if tf32 else torch.bfloat16
+    code = _lib.BRK_F32 if tf32 else _lib.BRK_BF16
     timer = _Timer(torch)
     rows = []
     tot = {p: [0.0, 0.0, 0.0] for p in passes}  # sum n_i F_i, sum n_i t_i, sum n_i t_roof
@@ -101,11 +107,11 @@ def resnet_suite(n=256, iters=10, layers=None, passes=("fwd", "bwd", "upd"), ver
         p_, q_ = spec.out_h, spec.out_w
         bc, bk = spec.b_c, spec.b_k
         geom = (n, c, k, h, w, r, s, st, spec.pad_h, spec.pad_w)
-        x = (torch.rand((n, c // bc, h, w, bc), generator=g, device="cuda") * 2 - 1).bfloat16()
-        wt = ((torch.rand((k // bk, c // bc, r, s, bc, bk), generator=g, device="cuda") * 2 - 1) * 0.05).bfloat16()
-        dout = (torch.rand((n, k // bk, p_, q_, bk), generator=g, device="cuda") * 2 - 1).bfloat16()
+        x = (torch.rand((n, c // bc, h, w, bc), generator=g, device="cuda") * 2 - 1).to(dt)
+        wt = ((torch.rand((k // bk, c // bc, r, s, bc, bk), generator=g, device="cuda") * 2 - 1) * 0.05).to(dt)
+        dout = (torch.rand((n, k // bk, p_, q_, bk), generator=g, device="cuda") * 2 - 1).to(dt)
         flops = 2.0 * n * k * c * r * s * p_ * q_
-        e = 2
+        e = 4 if tf32 else 2
         act_in, act_out, wbytes = n * c * h * w * e, n * k * p_ * q_ * e, k * c * r * s * e
         # a 1x1 strided conv reads only the sampled input pixels (one in stride^2) in fwd / upd;
         # bwd-data writes the whole input gradient (the skipped pixels get zeros)
@@ -115,26 +121,26 @@ def resnet_suite(n=256, iters=10, layers=None, passes=("fwd", "bwd", "upd"), ver
         engine = bc == 64 and bk == 64
         calls = {}
         if engine:
-            out = torch.empty((n, k // 64, p_, q_, 64), dtype=torch.bfloat16, device="cuda")
+            out = torch.empty((n, k // 64, p_, q_, 64), dtype=dt, device="cuda")
             din = torch.empty_like(x)
             dw = torch.empty((k // 64, c // 64, r, s, 64, 64), dtype=torch.float32, device="cuda")
             nbytes = lib.brk_conv_upd_workspace(*geom)
             ws = torch.empty(max(nbytes, 16), dtype=torch.uint8, device="cuda")
             calls["fwd"] = lambda sp: _lib.check(lib.brk_conv_fwd(x.data_ptr(), wt.data_ptr(), None, out.data_ptr(),
-                                                                  *geom, 64, 64, 0, _lib.BRK_BF16, sp))
+                                                                  *geom, 64, 64, 0, code, sp))
             calls["bwd"] = lambda sp: _lib.check(lib.brk_conv_bwd_data(dout.data_ptr(), wt.data_ptr(), din.data_ptr(),
-                                                                       *geom, 64, 64, _lib.BRK_BF16, sp))
+                                                                       *geom, 64, 64, code, sp))
             calls["upd"] = lambda sp: _lib.check(lib.brk_conv_upd(x.data_ptr(), dout.data_ptr(), dw.data_ptr(), None,
                                                                   0.0, ws.data_ptr() if nbytes else None, nbytes,
-                                                                  *geom, 64, 64, _lib.BRK_BF16, sp))
+                                                                  *geom, 64, 64, code, sp))
             path = "engine"
         else:
             xi = BlockedTensor(x, 4, {"n": 0, "c": (1, 4), "h": 2, "w": 3})
             wi = BlockedTensor(wt, 4, {"k": (0, 5), "c": (1, 4), "r": 2, "s": 3})
             do = BlockedTensor(dout, 4, {"n": 0, "k": (1, 4), "p": 2, "q": 3})
-            calls["fwd"] = lambda sp: conv2d_forward(spec, xi, wi)
-            calls["bwd"] = lambda sp: conv2d_backward_data(spec, do, wi)
-            calls["upd"] = lambda sp: conv2d_weight_update(spec, xi, do)
+            calls["fwd"] = lambda sp: conv2d_forward(spec, xi, wi, precision=precision)
+            calls["bwd"] = lambda sp: conv2d_backward_data(spec, do, wi, precision=precision)
+            calls["upd"] = lambda sp: conv2d_weight_update(spec, xi, do, precision=precision)
             path = ("s2d-engine" if st == 2 and c <= 4 else "im2col-gemm") if c < 64 and k == 64 else "grouped"
         row = {"id": lid, "count": cnt, "path": path, "C": c, "K": k, "H": h, "W": w, "R": r, "stride": st,
                "gflop": flops / 1e9}
@@ -175,7 +181,7 @@ def resnet_suite(n=256, iters=10, layers=None, passes=("fwd", "bwd", "upd"), ver
                           "frac_of_roofline": TR / T, "ms": T * 1e3, "gflop": F / 1e9}
         return out
 
-    return {"n": n, "peak_tflops": peak, "hbm_gbs": hbm, "peak_source": src, "layers": rows,
+    return {"n": n, "precision": precision, "peak_tflops": peak, "hbm_gbs": hbm, "peak_source": src, "layers": rows,
             "summary": summarize(tot), "summary_engine_layers": summarize(tot_engine)}
 
 
