@@ -210,7 +210,8 @@ BRK_API int brk_layout_transform(const void* src, void* dst, int ndims, const in
  * tensor.py:160-235), implicit GEMM with TMA im2col operand fetch:
  *   in, din : [N][C/64][H][W][64]     out, dout : [N][K/64][P][Q][64]
  *   w       : [K/64][C/64][R][S][64 c][64 k]   dw : like w, fp32
- * Engine path: bf16 storage, b_c = b_k = 64, C and K multiples of 64; stride
+ * Engine path: bf16 storage (dtype BRK_BF16) or fp32 storage with TF32 math (BRK_F32: k-steps
+ * of 32 channels, fp32 outputs; no fused SGD), b_c = b_k = 64, C and K multiples of 64; stride
  * 1 (pad <= 15, R, S <= 16) or 1x1 stride 2 without padding.
  * ------------------------------------------------------------------------- */
 /* Replaces brkernels.cnn.conv2d_forward (cnn.py:201-334): out = act(conv(in, w) + bias);
