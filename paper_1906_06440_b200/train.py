@@ -179,6 +179,20 @@ class ResNetConvs:
         return launches
 
 
+def _cat_of(parts):
+    """The gate-concatenated buffer that ``parts`` (consecutive row slices) were cut from,
+    or a concatenation when they are not such slices."""
+    base = parts[0]._base
+    if (base is not None and base.is_contiguous() and all(t._base is base for t in parts)
+            and parts[0].data_ptr() == base.data_ptr() and base.numel() == sum(t.numel() for t in parts)
+            and all(parts[i + 1].data_ptr() == parts[i].data_ptr() + parts[i].numel() * parts[i].element_size()
+                    for i in range(len(parts) - 1))):
+        return base.reshape(-1, *parts[0].shape[1:]) if parts[0].dim() > 1 else base.reshape(-1)
+    import torch
+
+    return torch.cat(parts)
+
+
 class LstmDP:
     """LSTM cell training step, data parallel over sequences (weak scaling: N per rank)."""
 
@@ -193,20 +207,53 @@ class LstmDP:
         self.T, self.N, self.C, self.K = t_steps, n_local, c, k
         wt = LstmCellWeights.random(np.random.default_rng([seed, 303]), c, k)
         params = LstmParams.from_dense(wt, t_steps, n_local)
-        for g in GATE_NAMES:  # device-resident master weights (fp32, blocked)
-            setattr(params, f"w_{g}", getattr(params, f"w_{g}").to("cuda", torch.float32))
-            setattr(params, f"r_{g}", getattr(params, f"r_{g}").to("cuda", torch.float32))
-            setattr(params, f"bias_{g}", torch.from_numpy(getattr(params, f"bias_{g}")).cuda())
+        # fp32 master weights, dense and gate-concatenated as the BPTT gradients come out of
+        # lstm_backward (dW_cat [4K][C], dR_cat [4K][K], db_cat [4K]); the params' blocked
+        # W_g [K_b][C_b][b_c][b_k] / R_g and bias_g are strided views into them, so the public
+        # params always hold the current weights and SGD is three contiguous updates
+        self.w32 = torch.from_numpy(np.concatenate([getattr(wt, f"w_{g}") for g in GATE_NAMES])).cuda().float()
+        self.r32 = torch.from_numpy(np.concatenate([getattr(wt, f"r_{g}") for g in GATE_NAMES])).cuda().float()
+        self.b32 = torch.from_numpy(np.concatenate([np.asarray(getattr(wt, f"bias_{g}"), np.float32).reshape(-1)
+                                                    for g in GATE_NAMES])).cuda()
+        if process_group is not None:
+            broadcast_params([self.w32, self.r32, self.b32], process_group)
+        for i, g in enumerate(GATE_NAMES):
+            getattr(params, f"w_{g}").data = self._blocked(self.w32, i, c, params.b_c, params.b_k)
+            getattr(params, f"r_{g}").data = self._blocked(self.r32, i, k, params.b_k, params.b_k)
+            setattr(params, f"bias_{g}", self.b32[i * k:(i + 1) * k])
         self.params = params
         self.gates = GATE_NAMES
-        if process_group is not None:
-            broadcast_params([t for g in GATE_NAMES for t in (getattr(params, f"w_{g}").data,
-                                                                getattr(params, f"r_{g}").data,
-                                                                getattr(params, f"bias_{g}"))], process_group)
         rng = np.random.default_rng([seed, 303, 1 + self.rank])  # data differs per rank
         self.x = torch.from_numpy(rng.uniform(-1, 1, (t_steps, n_local, c)).astype(np.float32)).cuda()
         self.dh = torch.from_numpy(rng.uniform(-1, 1, (t_steps, n_local, k)).astype(np.float32)).cuda()
         self.reducer = GradientReducer(group=process_group) if process_group is not None else None
+
+    def _blocked(self, master, gate, cols, bx, bk):
+        """W_g (K, X) rows gate*K.. of a dense master as the blocked [K_b][X_b][b_x][b_k] view."""
+        k = self.K
+        return master[gate * k:(gate + 1) * k].view(k // bk, bk, cols // bx, bx).permute(0, 2, 3, 1)
+
+    def _refresh_device_copies(self):
+        """Rebuild the kernels' operand copies straight from the updated masters (lstm._DeviceCell /
+        _SeqCell) and key them on the params as they are now, so the next lstm_forward does not
+        rebuild them through the per-gate blocked views: one cast per bf16 operand, one
+        transposing cast for R^T, one copy per blocked fp32 stack (per-step TF32 kernels)."""
+        from .lstm import _DeviceCell, _params_key, _SeqCell
+
+        torch = require_cuda()
+        p, k, c = self.params, self.K, self.C
+        dc = _DeviceCell.__new__(_DeviceCell)
+        dc.W = self.w32.view(4, k // p.b_k, p.b_k, c // p.b_c, p.b_c).permute(0, 1, 3, 4, 2).contiguous()
+        dc.R = self.r32.view(4, k // p.b_k, p.b_k, k // p.b_k, p.b_k).permute(0, 1, 3, 4, 2).contiguous()
+        dc.bias = self.b32
+        sc = _SeqCell.__new__(_SeqCell)
+        sc.w_cat = self.w32.to(torch.bfloat16)
+        sc.r_cat = self.r32.to(torch.bfloat16)
+        sc.rt_cat = torch.empty((4 * k, k), dtype=torch.bfloat16, device="cuda")
+        sc.rt_cat.view(4, k, k).copy_(self.r32.view(4, k, k).transpose(1, 2))
+        sc.bias = self.b32
+        object.__setattr__(p, "_brk_device_cell", (_params_key(p), dc))
+        object.__setattr__(p, "_brk_seq_cell", sc)
 
     def flops_per_step(self) -> float:
         """fwd 2TN(4KC + 4KK), bwd + upd twice that (reference bench.py flops_lstm_fwd)."""
@@ -223,10 +270,8 @@ class LstmDP:
         if self.reducer is not None:
             self.reducer.wait()
         scale = sgd_scale(self.lr, self.world)
-        k, c = self.K, self.C
-        for g in self.gates:  # dense (K, X) gradients -> blocked [K_b][X_b][b_x][b_k] weights
-            for name, grad, cols, bx in (("w", grads.dw[g], c, p.b_c), ("r", grads.dr[g], k, p.b_k)):
-                wb = getattr(p, f"{name}_{g}").data
-                wb.sub_(scale * grad.reshape(k // p.b_k, p.b_k, cols // bx, bx).permute(0, 2, 3, 1))
-            getattr(p, f"bias_{g}").sub_(scale * grads.db[g])
+        torch = require_cuda()
+        dw, dr, db = (_cat_of([getattr(grads, f)[g] for g in self.gates]) for f in ("dw", "dr", "db"))
+        torch._foreach_add_([self.w32, self.r32, self.b32], [dw, dr, db], alpha=-scale)
+        self._refresh_device_copies()
         return grads

@@ -187,3 +187,35 @@ def test_lstm_dp_world2_matches_full_batch():
     for _, rank, same, worst, *_ in _run("lstm"):
         assert same, f"rank {rank}: replicas differ after the step"
         check_parity("dp.lstm.dw", rank, worst, 1e-2)
+
+
+@pytest.mark.gpu
+def test_lstm_dp_sgd_and_refreshed_operands():
+    """One rank: the SGD step lands on the public blocked params (views of the dense masters),
+    and the operand copies LstmDP refreshes after it equal a rebuild from the params (the
+    next forward is bit-identical to one after dropping the caches)."""
+    from paper_1906_06440_b200 import precision
+    from paper_1906_06440_b200.lstm import lstm_forward
+    from paper_1906_06440_b200.train import LstmDP
+
+    torch.cuda.set_device(0)
+    net = LstmDP(t_steps=4, n_local=40, c=128, k=128, lr=0.05, seed=3, precision="bf16")
+    p = net.params
+    dense = lambda bt, cols: bt.data.permute(0, 3, 1, 2).reshape(net.K, cols).clone()  # noqa: E731
+    w0 = {g: dense(getattr(p, f"w_{g}"), net.C) for g in net.gates}
+    r0 = {g: dense(getattr(p, f"r_{g}"), net.K) for g in net.gates}
+    b0 = {g: getattr(p, f"bias_{g}").clone() for g in net.gates}
+    grads = net.step()
+    torch.cuda.synchronize()
+    for g in net.gates:
+        close = lambda a, b: torch.allclose(a, b, rtol=1e-6, atol=1e-7)  # noqa: E731 (fp32 a - lr*g, FMA or not)
+        assert close(dense(getattr(p, f"w_{g}"), net.C), w0[g] - 0.05 * grads.dw[g])
+        assert close(dense(getattr(p, f"r_{g}"), net.K), r0[g] - 0.05 * grads.dr[g])
+        assert close(getattr(p, f"bias_{g}"), b0[g] - 0.05 * grads.db[g])
+        assert not torch.equal(dense(getattr(p, f"w_{g}"), net.C), w0[g])
+    with precision("bf16"):
+        h_fast = lstm_forward(p, net.x).h.clone()
+        object.__setattr__(p, "_brk_device_cell", None)
+        object.__setattr__(p, "_brk_seq_cell", None)
+        h_rebuilt = lstm_forward(p, net.x).h
+    assert torch.equal(h_fast, h_rebuilt)
