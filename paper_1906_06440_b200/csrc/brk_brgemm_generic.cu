@@ -39,11 +39,11 @@ constexpr int kTmaWarps = 4;       // a warp keeps ~one box in flight: four of t
 constexpr int kEpiWarp0 = kTmaWarp + kTmaWarps;  // warps 13-16: epilogue (one per TMEM lane quarter)
 constexpr int kEpiWarps = 4;
 constexpr int kThreads = (kEpiWarp0 + kEpiWarps) * 32;
-constexpr int kMaxStages = 8;
+constexpr int kMaxStages = 16;  // (16 only for the compact small-block ring; other rings hold <= 8)
 constexpr int kRingBytes = 4 * (kRows * 128 + kCols * 128);  // 192 KB of operand ring
 constexpr int kAtomColsBf16 = 64;  // bf16 elements per 128 B swizzle-atom row
 constexpr int kAOpBytes = kRows * 128;    // K-major, 128B swizzle: 128 rows x 128 B of K
-constexpr int kSmemBytes = kRingBytes + 1024 + 256;  // ring + alignment slack + barriers / TMEM slot
+constexpr int kSmemBytes = kRingBytes + 1024 + 512;  // ring + alignment slack + barriers / TMEM slot
 
 struct EntryPtrs {
   const char* a;
@@ -182,10 +182,30 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
   // ring geometry: the B operand of the widest tile (MN-major atoms, or K-major rows for gathered TF32)
   const int m_max = min(p.m, kCols);
   const int b_bytes = b_mn ? (m_max + kAtomCols - 1) / kAtomCols * kAtomBytes : ((m_max + 15) & ~15) * 128;
-  const int stage_bytes = (kAOpBytes + b_bytes + 1023) & ~1023;
+  // Small blocks (one K chunk per entry, k <= 64, bf16 gathers): the gather copies only each
+  // entry's valid rows / chunks.  The ring starts zeroed, the MMA B operand's K-rows past k are
+  // never written (stay zero), so stale A chunks past k multiply zeros; rows / columns past the
+  // block only feed accumulator rows / columns the epilogue does not store.
+  const bool sparse = !kTF32 && !p.tma && p.in_bf16 && n_chunks == 1;
+  // Compact ring (sparse, k <= 32, one B atom): a stage holds only the block's A rows and B
+  // K-rows (m = n = k = 32: 8 KB instead of 24 KB), so 16 stages are in flight instead of 8.
+  // The M = 128 MMA still reads 128 A rows from the stage start: rows past the block come from
+  // the following stages (or unused ring) and only feed accumulator rows the epilogue does not
+  // store; the MMAs stop at K = ceil16(k), so only the stage's own B K-rows are read.
+  const int a_bytes_c = ((((min(p.n, kRows) + 7) & ~7) * 128) + 1023) & ~1023;
+  const int b_bytes_c = (((p.k + 15) & ~15) * 128 + 1023) & ~1023;
+  const bool compact = sparse && m_max <= kAtomCols && p.k <= 32 &&
+                       (kMaxStages - 1) * (a_bytes_c + b_bytes_c) + kAOpBytes <= kRingBytes;
+  const int b_off = compact ? a_bytes_c : kAOpBytes;  // B operand offset inside a stage
+  const int stage_bytes = compact ? a_bytes_c + b_bytes_c : (kAOpBytes + b_bytes + 1023) & ~1023;
   // (a multiple of the TMA producer count: each stage always has the same producer, so the
   // parity waits on its empty barrier cannot alias)
-  const int n_stages = min(kMaxStages, kRingBytes / stage_bytes) / kTmaWarps * kTmaWarps;
+  const int n_stages =
+      compact ? kMaxStages : min(min(kMaxStages, 8), kRingBytes / stage_bytes) / kTmaWarps * kTmaWarps;
+  // (4, 8 or 16: stage slot and phase by mask and shift — the MMA issuer's per-stage work is
+  // on the serial path of every tile)
+  const int st_shift = n_stages >= 16 ? 4 : (n_stages >= 8 ? 3 : 2);
+  const int st_mask = n_stages - 1;
 
   if (tid == 0) {
     for (int s = 0; s < kMaxStages; ++s) {
@@ -200,11 +220,6 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
     fence_barrier_init();
   }
   if (warp == kMmaWarp) tmem_alloc(tmem_slot, 2 * kCols);
-  // Small blocks (one K chunk per entry, k <= 64, bf16 gathers): the gather copies only each
-  // entry's valid rows / chunks.  The ring starts zeroed, the MMA B operand's K-rows past k are
-  // never written (stay zero), so stale A chunks past k multiply zeros; rows / columns past the
-  // block only feed accumulator rows / columns the epilogue does not store.
-  const bool sparse = !kTF32 && !p.tma && p.in_bf16 && n_chunks == 1;
   if (sparse) {
     for (int i = tid; i < kRingBytes / 16; i += kThreads)
       asm volatile("st.shared.v4.b32 [%0], {%1, %1, %1, %1};" ::"r"(smem_u32(smem) + i * 16), "r"(0u) : "memory");
@@ -263,15 +278,16 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
       const uint32_t d_tmem = tmem + acc * kCols;
       const int g0 = local * steps;
       for (int s = 0; s < steps; ++s) {
-        const int g = g0 + s, st = g % n_stages;
-        mbar_wait(tf32_tma ? &rounded[st] : &full[st], (g / n_stages) & 1);
+        const int g = g0 + s, st = g & st_mask;
+        mbar_wait(tf32_tma ? &rounded[st] : &full[st], (g >> st_shift) & 1);
         tc_fence_after();
         fence_proxy_async_smem();  // gathered / rounded stages were written through the generic proxy
         if (elect_one()) {
           const uint32_t a_base = smem_u32(smem + st * stage_bytes);
-          const uint32_t b_base = a_base + kAOpBytes;
+          const uint32_t b_base = a_base + b_off;
 #pragma unroll
           for (int kk = 0; kk < kKC / kMmaK; ++kk) {
+            if (compact && kk * kMmaK >= p.k) break;
             const uint64_t ad = make_smem_desc(a_base + kk * 32, 16, 1024, kSwizzle128B);
             // MN-major B: bf16 atoms of 64 K-rows (8-row swizzle groups, SBO 1024 B); TF32 atoms of
             // 32 K-rows in the 32 B-chunk swizzle (4-row groups, SBO 512 B); K-major TF32 rows
@@ -323,8 +339,8 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
           if (!eb.tma) { g += n_chunks; continue; }
           for (int ch = 0; ch < n_chunks; ++ch, ++g) {
             if (g % kTmaWarps != pid) continue;
-            const int k0 = ch * kKC, st = g % n_stages;
-            if (g >= n_stages) mbar_wait(&empty[st], ((g / n_stages) + 1) & 1);
+            const int k0 = ch * kKC, st = g & st_mask;
+            if (g >= n_stages) mbar_wait(&empty[st], ((g >> st_shift) + 1) & 1);
             uint8_t* a_op = smem + st * stage_bytes;
             mbar_arrive_expect_tx(&full[st], bytes);
             const int32_t cA[2] = {eb.cb + k0, eb.rb + n0};
@@ -348,8 +364,8 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
       const int vecs = (p.nbox * 128 + atoms * kAtomBytes) / 16;  // the stage bytes the boxes wrote
       const int g0 = local * steps;
       for (int s = 0; s < steps; ++s) {
-        const int g = g0 + s, st = g % n_stages;
-        mbar_wait(&full[st], (g / n_stages) & 1);
+        const int g = g0 + s, st = g & st_mask;
+        mbar_wait(&full[st], (g >> st_shift) & 1);
         uint4* v4 = reinterpret_cast<uint4*>(smem + st * stage_bytes);
         const int a_vecs = p.nbox * 8;
         for (int i = gt; i < vecs; i += kGatherWarps * 32) {
@@ -382,17 +398,64 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
       const int n_rows8 = (n_here + 7) & ~7;
       const int col_chunks = n_cols / kE;
       const int g0 = local * steps;
-      bool skip = false;
-      for (int s = 0; s < steps; ++s) {
-        const int entry = s / n_chunks;
-        if (s % n_chunks == 0) skip = entry_box(job, entry).tma;
-        if (skip) continue;
-        const int g = g0 + s, st = g % n_stages;
-        const int k0 = (s % n_chunks) * kKC;
+      // Per-tile unit tables for the all-cp.async case (bf16 in, contiguous rows): this thread's
+      // (row, 16 B chunk) -> (ring offset, element offset) map is the same for every entry and
+      // K chunk of the tile, so a stage costs one add and one clamp per copy.  (The loops below
+      // recompute it per unit and stage with integer divisions: ~300 instructions per gather
+      // warp per stage, which bounded small blocks at ~1.1 us per stage whatever its bytes.)
+      constexpr int kUnits = 4;
+      int ta_dst[kUnits], ta_src[kUnits], ta_kk[kUnits], tb_dst[kUnits], tb_src[kUnits], tb_kr[kUnits],
+          tb_mc[kUnits];
+      const int k1 = min(kKC, p.k);  // k_here of a sparse tile (one K chunk per entry)
+      const int a_cpr_t = sparse ? (k1 + kE - 1) / kE : 8;
+      const int a_units_t = sparse ? n_here * a_cpr_t : n_rows8 * 8;
+      const int b_cpr_t = sparse ? (m_here + kE - 1) / kE : col_chunks;
+      const int b_units_t = sparse ? k1 * b_cpr_t : kKC * col_chunks;
+      // Tiny stages (<= 4 copies per lane of one warp, e.g. 32 x 32 blocks): each stage is
+      // gathered by ONE warp (stage g by warp g % 8, so eight stages are in flight at once and
+      // no cross-warp barrier is paid per stage); with 8 ring stages a slot always has the
+      // same warp, so its parity waits cannot alias.  Otherwise all 8 warps share each stage.
+      const bool tiny = n_stages % kGatherWarps == 0 && a_units_t <= kUnits * 32 && b_units_t <= kUnits * 32;
+      const int ubase = tiny ? lane : gt, ustride = tiny ? 32 : kGatherWarps * 32;
+      const bool tab = !kTF32 && bf16_in && a_contig && b_contig && a_units_t <= kUnits * ustride &&
+                       b_units_t <= kUnits * ustride &&
+                       static_cast<int64_t>(n0 + kRows) * p.b_sn + p.k + kKC < (1ll << 31) &&
+                       static_cast<int64_t>(p.k + kKC) * p.a_sk + m0 + kCols < (1ll << 31);
+      // (tiny: only a warp that owns one of the tile's stages builds them)
+      if (tab && (!tiny || steps >= kGatherWarps || ((warp - g0) & (kGatherWarps - 1)) < steps)) {
+#pragma unroll
+        for (int j = 0; j < kUnits; ++j) {
+          const int u = ubase + j * ustride;
+          ta_dst[j] = -1;
+          tb_dst[j] = -1;
+          if (u < a_units_t) {
+            const int r = sparse ? u / a_cpr_t : u >> 3, c = sparse ? u - r * a_cpr_t : u & 7;
+            ta_dst[j] = r * 128 + ((c ^ (r & 7)) << 4);
+            ta_src[j] = (n0 + r) * p.b_sn + c * kE;
+            ta_kk[j] = r < n_here ? c * kE : (1 << 20);  // rows past the block: zero-filled
+          }
+          if (u < b_units_t) {
+            const int kr = u / b_cpr_t, c = u - kr * b_cpr_t;
+            const int col = c * kE;
+            const int atom = c / (kAtomCols / kE), cc = c % (kAtomCols / kE);
+            tb_dst[j] = b_off + atom * kAtomBytes + kr * 128 + ((cc ^ (kr & 7)) << 4);
+            tb_src[j] = kr * p.a_sk + m0 + col;
+            tb_kr[j] = kr;
+            tb_mc[j] = m_here - col;
+          }
+        }
+      }
+      // (this loop runs only when the launch gathers every entry, see `boxes`; tiny: the warp
+      // visits only its own stages, g = warp mod 8)
+      const int s_first = tiny ? ((warp - g0) & (kGatherWarps - 1)) : 0, s_step = tiny ? kGatherWarps : 1;
+      for (int s = s_first; s < steps; s += s_step) {
+        const int entry = n_chunks == 1 ? s : s / n_chunks;
+        const int g = g0 + s, st = g & st_mask;
+        const int k0 = (s - entry * n_chunks) * kKC;
         const int k_here = min(kKC, p.k - k0);
-        if (g >= n_stages) mbar_wait(&empty[st], ((g / n_stages) + 1) & 1);
+        if (g >= n_stages) mbar_wait(&empty[st], ((g >> st_shift) + 1) & 1);
         uint8_t* a_op = smem + st * stage_bytes;
-        uint8_t* b_op = a_op + kAOpBytes;
+        uint8_t* b_op = a_op + b_off;
         const EntryPtrs e = entry_ptrs(p, job, entry);
         const size_t esz = bf16_in ? 2 : 4;
         const bool a_vec = a_contig && ((reinterpret_cast<uintptr_t>(e.b) & 15) == 0) && ((p.b_sn * esz) % 16 == 0);
@@ -401,11 +464,27 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
         // zero-filled tails), so each gather thread keeps all ring stages' loads in flight
         const bool fast_a = !kTF32 && bf16_in && a_vec;
         const bool fast_b = !kTF32 && bf16_in && b_vec;
+        if (tab && fast_a && fast_b) {
+          const uint32_t ring = smem_u32(a_op);
+          const char* pa = e.b + static_cast<int64_t>(k0) * 2;
+          const char* pb = e.a + static_cast<int64_t>(k0) * p.a_sk * 2;
+#pragma unroll
+          for (int j = 0; j < kUnits; ++j) {
+            if (ta_dst[j] >= 0) {
+              const int bytes = max(0, min(16, (k_here - ta_kk[j]) * 2));
+              cp_async16(ring + ta_dst[j], bytes > 0 ? pa + static_cast<int64_t>(ta_src[j]) * 2 : e.b, bytes);
+            }
+            if (tb_dst[j] >= 0) {
+              const int bytes = tb_kr[j] < k_here ? max(0, min(16, tb_mc[j] * 2)) : 0;
+              cp_async16(ring + tb_dst[j], bytes > 0 ? pb + static_cast<int64_t>(tb_src[j]) * 2 : e.a, bytes);
+            }
+          }
+        } else {
         // A operand (K-major) <- reference b block rows: (row r, 16 B chunk c) along k
         // (sparse: only the n_here rows x chunks holding k)
         const int a_cpr = sparse ? (k_here + kE - 1) / kE : 8;
         const int a_units = sparse ? n_here * a_cpr : n_rows8 * 8;
-        for (int u = gt; u < a_units; u += kGatherWarps * 32) {
+        for (int u = ubase; u < a_units; u += ustride) {
           const int r = sparse ? u / a_cpr : u >> 3, c = sparse ? u - r * a_cpr : u & 7;
           const int kk = c * kE;
           if (fast_a) {
@@ -426,7 +505,7 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
         // B operand <- reference a block.  bf16: MN-major, (k-row kr, 16 B chunk c along m);
         // TF32 (K-major only): row i = m index, 16 B chunk c along k (strided gather)
         if constexpr (kTF32) {
-          for (int u = gt; u < n_cols * 8; u += kGatherWarps * 32) {
+          for (int u = ubase; u < n_cols * 8; u += ustride) {
             const int i = u >> 3, c = u & 7;
             const int kk = c * kE;
             const uint4 v = (i < m_here)
@@ -440,7 +519,7 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
           // (sparse: only the k_here K-rows x chunks holding m)
           const int b_cpr = sparse ? (m_here + kE - 1) / kE : col_chunks;
           const int b_units = sparse ? k_here * b_cpr : kKC * col_chunks;
-          for (int u = gt; u < b_units; u += kGatherWarps * 32) {
+          for (int u = ubase; u < b_units; u += ustride) {
             const int kr = u / b_cpr, c = u - kr * b_cpr;
             const int col = c * kE;
             const int atom = c / (kAtomCols / kE), cc = c % (kAtomCols / kE);
@@ -461,10 +540,16 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
             *reinterpret_cast<uint4*>(b_op + atom * kAtomBytes + kr * 128 + ((cc ^ (kr & 7)) << 4)) = v;
           }
         }
+        }  // per-unit loops
         fence_proxy_async_smem();   // this thread's st.shared -> the MMA's async-proxy reads
         cp_async_arrive(&full[st]);  // pending +1 now, -1 when this thread's copies land
-        asm volatile("bar.sync 1, %0;" ::"r"(kGatherWarps * 32) : "memory");
-        if (gt == 0) mbar_arrive(&full[st]);  // the stage's one expected arrival
+        if (tiny) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&full[st]);  // the stage's one expected arrival
+        } else {
+          asm volatile("bar.sync 1, %0;" ::"r"(kGatherWarps * 32) : "memory");
+          if (gt == 0) mbar_arrive(&full[st]);
+        }
       }
     }
   } else {

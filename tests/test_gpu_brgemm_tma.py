@@ -171,3 +171,30 @@ def test_addr_views_match_gather(m, n, k, batch, jobs):
         ref = orc.brgemm_reference(list(aj.float().cpu().numpy()), list(b[j].float().cpu().numpy()),
                                    np.zeros((n, m), np.float32), 1.0, 0.0)
         assert np.array_equal(c[j].cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("m,n,k,batch,jobs", [(32, 32, 32, 16, 1184), (16, 24, 8, 7, 300), (64, 32, 32, 5, 400),
+                                              (40, 20, 24, 9, 150), (32, 128, 32, 3, 200), (32, 32, 32, 1, 999),
+                                              (8, 8, 16, 64, 333)])
+def test_small_blocks_warp_stages_and_compact_ring(m, n, k, batch, jobs):
+    """Small blocks take the gather path with one warp per stage (and, for k <= 32 and one
+    64-column B atom, the compact 16-stage ring whose M = 128 MMAs read rows of the next
+    stages): stride and address variants bit-identical and equal to the fp64 oracle on
+    integer inputs, every job checked (a stage read from a wrong slot would show)."""
+    lib = _lib.load()
+    g = torch.Generator(device="cpu").manual_seed(7 * m + n + k + batch)
+    a = ints(g, jobs, batch, k, m).cuda().bfloat16()
+    b = ints(g, jobs, batch, n, k).cuda().bfloat16()
+    c = torch.full((jobs, n, m), float("nan"), device="cuda")
+    _lib.check(lib.brk_brgemm_stride(a.data_ptr(), b.data_ptr(), k * m, n * k, c.data_ptr(), jobs, batch * k * m,
+                                     batch * n * k, n * m, m, n, k, batch, m, k, m, 1.0, 0.0, BF16, F32, CBF16, None))
+    torch.cuda.synchronize()
+    c2 = torch.zeros_like(c)
+    run_addr(lib, [a[j, i].data_ptr() for j in range(jobs) for i in range(batch)],
+             [b[j, i].data_ptr() for j in range(jobs) for i in range(batch)], c2, jobs, m, n, k, batch, m, k)
+    assert torch.equal(c, c2)
+    ref = torch.einsum("jikm,jink->jnm", a.double(), b.double())  # exact for these integer inputs
+    assert torch.equal(c.double(), ref)
+    ref0 = orc.brgemm_reference(list(a[0].float().cpu().numpy()), list(b[0].float().cpu().numpy()),
+                                np.zeros((n, m), np.float32), 1.0, 0.0)
+    assert np.array_equal(c[0].cpu().numpy(), ref0)
