@@ -43,7 +43,8 @@ constexpr int kMaxStages = 16;  // (16 only for the compact small-block ring; ot
 constexpr int kRingBytes = 4 * (kRows * 128 + kCols * 128);  // 192 KB of operand ring
 constexpr int kAtomColsBf16 = 64;  // bf16 elements per 128 B swizzle-atom row
 constexpr int kAOpBytes = kRows * 128;    // K-major, 128B swizzle: 128 rows x 128 B of K
-constexpr int kSmemBytes = kRingBytes + 1024 + 512;  // ring + alignment slack + barriers / TMEM slot
+constexpr int kSmemBytes = kRingBytes + 1024 + 1024;
+constexpr int kMaxAcc = 8;  // TMEM accumulators (512 columns / the widest tile's columns)  // ring + alignment slack + barriers / TMEM slot
 
 struct EntryPtrs {
   const char* a;
@@ -153,9 +154,9 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
                                              ~static_cast<uintptr_t>(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRingBytes);
   uint64_t* empty = full + kMaxStages;
-  uint64_t* done = empty + kMaxStages;  // [2] accumulator complete
-  uint64_t* drained = done + 2;         // [2] epilogue finished reading TMEM
-  uint64_t* rounded = drained + 2;      // [kMaxStages] TF32 TMA stages rounded in place (RNA)
+  uint64_t* done = empty + kMaxStages;  // [kMaxAcc] accumulator complete
+  uint64_t* drained = done + kMaxAcc;   // [kMaxAcc] epilogue finished reading TMEM
+  uint64_t* rounded = drained + kMaxAcc;  // [kMaxStages] TF32 TMA stages rounded in place (RNA)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rounded + kMaxStages);
 
   const int tid = threadIdx.x;
@@ -206,6 +207,13 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
   // on the serial path of every tile)
   const int st_shift = n_stages >= 16 ? 4 : (n_stages >= 8 ? 3 : 2);
   const int st_mask = n_stages - 1;
+  // TMEM accumulators: 512 columns split into as many as the widest tile allows (2 of 256
+  // columns, ... 8 of 64), so short tiles (small batch) keep up to 7 tiles of MMAs ahead of
+  // the epilogue instead of one
+  const int n_cols_max = kTF32 ? (m_max + 15) & ~15 : (m_max + kAtomCols - 1) / kAtomCols * kAtomCols;
+  const int acc_cols = n_cols_max <= 64 ? 64 : (n_cols_max <= 128 ? 128 : 256);
+  const int acc_shift = acc_cols == 64 ? 3 : (acc_cols == 128 ? 2 : 1);  // log2(accumulators)
+  const int acc_mask = (1 << acc_shift) - 1;
 
   if (tid == 0) {
     for (int s = 0; s < kMaxStages; ++s) {
@@ -213,7 +221,7 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
       mbar_init(&empty[s], 1);
       mbar_init(&rounded[s], 1);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < kMaxAcc; ++a) {
       mbar_init(&done[a], 1);
       mbar_init(&drained[a], kEpiWarps);
     }
@@ -272,10 +280,10 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
       const int m_here = min(kCols, p.m - mt * kCols);
       const int n_cols = kTF32 ? (m_here + 15) & ~15 : (m_here + kAtomCols - 1) / kAtomCols * kAtomCols;
       const uint32_t idesc = make_idesc(kTF32 ? kFmtTF32 : kFmtBF16, kRows, n_cols, 0, b_mn ? 1 : 0);
-      const int acc = local & 1;
-      mbar_wait(&drained[acc], ((local >> 1) & 1) ^ 1);  // the epilogue read this accumulator two tiles ago
+      const int acc = local & acc_mask;
+      mbar_wait(&drained[acc], ((local >> acc_shift) & 1) ^ 1);  // the epilogue read this accumulator
       tc_fence_after();
-      const uint32_t d_tmem = tmem + acc * kCols;
+      const uint32_t d_tmem = tmem + acc * acc_cols;
       const int g0 = local * steps;
       for (int s = 0; s < steps; ++s) {
         const int g = g0 + s, st = g & st_mask;
@@ -564,9 +572,9 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
       const int n0 = nt * kRows, m0 = mt * kCols;
       const int m_here = min(kCols, p.m - m0);
       const int n_cols = kTF32 ? (m_here + 15) & ~15 : (m_here + kAtomCols - 1) / kAtomCols * kAtomCols;
-      const int acc = local & 1;
+      const int acc = local & acc_mask;
       if (steps > 0) {
-        mbar_wait(&done[acc], (local >> 1) & 1);
+        mbar_wait(&done[acc], (local >> acc_shift) & 1);
         tc_fence_after();
       }
       const int row = n0 + quarter * 32 + lane;
@@ -582,7 +590,7 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
       for (int c0 = 0; c0 < n_cols; c0 += 32) {
         uint32_t accv[32];
         if (steps > 0) {
-          tmem_ld32(tmem + acc * kCols + (static_cast<uint32_t>(quarter * 32) << 16) + c0, accv);
+          tmem_ld32(tmem + acc * acc_cols + (static_cast<uint32_t>(quarter * 32) << 16) + c0, accv);
           tmem_ld_wait();
         } else {
 #pragma unroll
