@@ -273,6 +273,16 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
 
   if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
+    // stage-0 operand descriptors.  MN-major B: bf16 atoms of 64 K-rows (8-row swizzle
+    // groups, SBO 1024 B); TF32 atoms of 32 K-rows in the 32 B-chunk swizzle (4-row groups,
+    // SBO 512 B); K-major TF32 rows.  Per K-step: A +32 B; B +32 B (K-major) or +kMmaK rows.
+    const uint32_t ring0 = smem_u32(smem);
+    const uint64_t a_desc0 = make_smem_desc(ring0, 16, 1024, kSwizzle128B);
+    const uint64_t b_desc0 =
+        !b_mn ? make_smem_desc(ring0 + b_off, 16, 1024, kSwizzle128B)
+              : (kTF32 ? make_smem_desc(ring0 + b_off, kAtomBytes, 512, kSwizzle128B32)
+                       : make_smem_desc(ring0 + b_off, kAtomBytes, 1024, kSwizzle128B));
+    const uint32_t b_kstep = b_mn ? kMmaK * 128 / 16 : 2;
     int local = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
       if (steps == 0) continue;
@@ -291,19 +301,17 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
         tc_fence_after();
         fence_proxy_async_smem();  // gathered / rounded stages were written through the generic proxy
         if (elect_one()) {
-          const uint32_t a_base = smem_u32(smem + st * stage_bytes);
-          const uint32_t b_base = a_base + b_off;
+          // descriptors built once per launch and advanced by constants (16-byte units): the
+          // issuer's per-stage work is on the serial path of every tile (small blocks: ~0.3 us
+          // per stage); start-address field = bits 0-13, the ring sits below 256 KB
+          const uint32_t so = static_cast<uint32_t>(st * stage_bytes) >> 4;
+          const uint64_t ad = a_desc0 + so;
+          const uint64_t bd = b_desc0 + so;
+          const int ksteps = compact ? (p.k + kMmaK - 1) / kMmaK : kKC / kMmaK;
 #pragma unroll
           for (int kk = 0; kk < kKC / kMmaK; ++kk) {
-            if (compact && kk * kMmaK >= p.k) break;
-            const uint64_t ad = make_smem_desc(a_base + kk * 32, 16, 1024, kSwizzle128B);
-            // MN-major B: bf16 atoms of 64 K-rows (8-row swizzle groups, SBO 1024 B); TF32 atoms of
-            // 32 K-rows in the 32 B-chunk swizzle (4-row groups, SBO 512 B); K-major TF32 rows
-            const uint64_t bd =
-                !b_mn ? make_smem_desc(b_base + kk * 32, 16, 1024, kSwizzle128B)
-                      : (kTF32 ? make_smem_desc(b_base + kk * kMmaK * 128, kAtomBytes, 512, kSwizzle128B32)
-                               : make_smem_desc(b_base + kk * kMmaK * 128, kAtomBytes, 1024, kSwizzle128B));
-            mma_ss<kTF32>(d_tmem, ad, bd, idesc, (s > 0 || kk > 0) ? 1u : 0u);
+            if (kk >= ksteps) break;
+            mma_ss<kTF32>(d_tmem, ad + kk * 2, bd + kk * b_kstep, idesc, (s > 0 || kk > 0) ? 1u : 0u);
           }
           mma_commit(&empty[st]);
           if (s == steps - 1) mma_commit(&done[acc]);
