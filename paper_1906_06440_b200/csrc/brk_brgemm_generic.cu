@@ -197,12 +197,18 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
   const int b_bytes_c = (((p.k + 15) & ~15) * 128 + 1023) & ~1023;
   const bool compact = sparse && m_max <= kAtomCols && p.k <= 32 &&
                        (kMaxStages - 1) * (a_bytes_c + b_bytes_c) + kAOpBytes <= kRingBytes;
-  const int b_off = compact ? a_bytes_c : kAOpBytes;  // B operand offset inside a stage
-  const int stage_bytes = compact ? a_bytes_c + b_bytes_c : (kAOpBytes + b_bytes + 1023) & ~1023;
+  // 64B-swizzle boxes (m = k = 32, TMA): A rows of 64 B, B 32 K-rows x 64 B, compact stages
+  // read like the compact ring (the M = 128 MMA reads 8 KB of A rows from the stage start)
+  const bool sw64 = boxes && p.sw64 != 0;
+  const int a_bytes_s = ((p.nbox * 64) + 1023) & ~1023;
+  const int b_off = compact ? a_bytes_c : (sw64 ? a_bytes_s : kAOpBytes);  // B operand offset inside a stage
+  const int stage_bytes = compact ? a_bytes_c + b_bytes_c
+                                  : (sw64 ? a_bytes_s + 2048 : (kAOpBytes + b_bytes + 1023) & ~1023);
   // (a multiple of the TMA producer count: each stage always has the same producer, so the
   // parity waits on its empty barrier cannot alias)
-  const int n_stages =
-      compact ? kMaxStages : min(min(kMaxStages, 8), kRingBytes / stage_bytes) / kTmaWarps * kTmaWarps;
+  const int n_stages = (compact || sw64)
+                           ? kMaxStages
+                           : min(min(kMaxStages, 8), kRingBytes / stage_bytes) / kTmaWarps * kTmaWarps;
   // (4, 8 or 16: stage slot and phase by mask and shift — the MMA issuer's per-stage work is
   // on the serial path of every tile)
   const int st_shift = n_stages >= 16 ? 4 : (n_stages >= 8 ? 3 : 2);
@@ -277,18 +283,22 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
     // groups, SBO 1024 B); TF32 atoms of 32 K-rows in the 32 B-chunk swizzle (4-row groups,
     // SBO 512 B); K-major TF32 rows.  Per K-step: A +32 B; B +32 B (K-major) or +kMmaK rows.
     const uint32_t ring0 = smem_u32(smem);
-    const uint64_t a_desc0 = make_smem_desc(ring0, 16, 1024, kSwizzle128B);
+    // 64B swizzle (sw64): 8-row groups of 512 B for both; B K-step = 16 K-rows of 64 B
+    const uint64_t a_desc0 = sw64 ? make_smem_desc(ring0, 16, 512, kSwizzle64B)
+                                  : make_smem_desc(ring0, 16, 1024, kSwizzle128B);
     const uint64_t b_desc0 =
-        !b_mn ? make_smem_desc(ring0 + b_off, 16, 1024, kSwizzle128B)
-              : (kTF32 ? make_smem_desc(ring0 + b_off, kAtomBytes, 512, kSwizzle128B32)
-                       : make_smem_desc(ring0 + b_off, kAtomBytes, 1024, kSwizzle128B));
-    const uint32_t b_kstep = b_mn ? kMmaK * 128 / 16 : 2;
+        sw64 ? make_smem_desc(ring0 + b_off, 2048, 512, kSwizzle64B)
+             : (!b_mn ? make_smem_desc(ring0 + b_off, 16, 1024, kSwizzle128B)
+                      : (kTF32 ? make_smem_desc(ring0 + b_off, kAtomBytes, 512, kSwizzle128B32)
+                               : make_smem_desc(ring0 + b_off, kAtomBytes, 1024, kSwizzle128B)));
+    const uint32_t b_kstep = sw64 ? kMmaK * 64 / 16 : (b_mn ? kMmaK * 128 / 16 : 2);
     int local = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
       if (steps == 0) continue;
       const int mt = t % m_tiles;
       const int m_here = min(kCols, p.m - mt * kCols);
-      const int n_cols = kTF32 ? (m_here + 15) & ~15 : (m_here + kAtomCols - 1) / kAtomCols * kAtomCols;
+      const int n_cols =
+          sw64 ? 32 : (kTF32 ? (m_here + 15) & ~15 : (m_here + kAtomCols - 1) / kAtomCols * kAtomCols);
       const uint32_t idesc = make_idesc(kTF32 ? kFmtTF32 : kFmtBF16, kRows, n_cols, 0, b_mn ? 1 : 0);
       const int acc = local & acc_mask;
       mbar_wait(&drained[acc], ((local >> acc_shift) & 1) ^ 1);  // the epilogue read this accumulator
@@ -307,7 +317,7 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
           const uint32_t so = static_cast<uint32_t>(st * stage_bytes) >> 4;
           const uint64_t ad = a_desc0 + so;
           const uint64_t bd = b_desc0 + so;
-          const int ksteps = compact ? (p.k + kMmaK - 1) / kMmaK : kKC / kMmaK;
+          const int ksteps = (compact || sw64) ? (p.k + kMmaK - 1) / kMmaK : kKC / kMmaK;
 #pragma unroll
           for (int kk = 0; kk < kKC / kMmaK; ++kk) {
             if (kk >= ksteps) break;
@@ -331,7 +341,8 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
         const int n0 = nt * kRows, m0 = mt * kCols;
         const int m_here = min(kCols, p.m - m0);
         const int atoms = (m_here + kAtomCols - 1) / kAtomCols;
-        const uint32_t bytes = static_cast<uint32_t>(p.nbox * 128 + atoms * p.abox * 128);
+        const uint32_t bytes =
+            sw64 ? static_cast<uint32_t>(p.nbox * 64 + 2048) : static_cast<uint32_t>(p.nbox * 128 + atoms * p.abox * 128);
         int g = local * steps;
         // offset / address tables: this job's entries are contiguous — pull their lines into L1
         // once, so the per-entry reads below do not each pay an L2 round trip
@@ -363,7 +374,7 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
             tma_load<2>(a_op, &p.map_bop, &full[st], cA);
             for (int at = 0; at < atoms; ++at) {
               const int32_t cB[2] = {eb.ca + m0 + at * kAtomCols, eb.ra + k0};
-              tma_load<2>(a_op + kAOpBytes + at * kAtomBytes, &p.map_aop, &full[st], cB);
+              tma_load<2>(a_op + b_off + at * kAtomBytes, &p.map_aop, &full[st], cB);
             }
           }
         }
@@ -722,16 +733,21 @@ int launch_brgemm_generic(const GenericParams& p, int compute_tf32, cudaStream_t
   // 64-deep K chunks, box extents that stay inside each block (no reads past a block)
   GenericParams q = p;
   q.tma = 0;
-  const bool rows_ok = (p.n <= kRows || p.n % kRows == 0) && p.m % kAtomColsBf16 == 0;
+  q.sw64 = 0;
+  // m = k = 32 blocks (64 B rows): 64B-swizzle boxes, one per operand and entry
+  const bool sw64 = p.m == 32 && p.k == 32 && p.n <= kRows;
+  const bool rows_ok = (p.n <= kRows || p.n % kRows == 0) && (p.m % kAtomColsBf16 == 0 || sw64);
   const bool addr_views = p.mode == kModeAddr && p.a_view > 0 && p.b_view > 0 && p.a_base != nullptr &&
                           p.b_base != nullptr;
-  if (!compute_tf32 && p.in_bf16 && (p.mode != kModeAddr || addr_views) && p.k % 64 == 0 && rows_ok && p.a_sm == 1 &&
+  if (!compute_tf32 && p.in_bf16 && (p.mode != kModeAddr || addr_views) && (p.k % 64 == 0 || sw64) && rows_ok &&
+      p.a_sm == 1 &&
       p.b_sk == 1 &&
       (p.a_sk * 2) % 16 == 0 && (p.b_sn * 2) % 16 == 0 && p.a_sk >= p.m && p.b_sn >= p.k &&
       (reinterpret_cast<uintptr_t>(p.a_base) & 15) == 0 && (reinterpret_cast<uintptr_t>(p.b_base) & 15) == 0 &&
       std::getenv("BRK_GENERIC_NO_TMA") == nullptr) {
     q.nbox = std::min(p.n, kRows);
-    q.abox = kAtomColsBf16;
+    q.abox = sw64 ? 32 : kAtomColsBf16;
+    q.sw64 = sw64 ? 1 : 0;
     // the views span every row an in-bounds offset can address (the kernel reads only boxes
     // inside blocks, so the declared extent is never dereferenced beyond them)
     uint64_t rows_b = std::min<uint64_t>(0x7fffffffull, (1ull << 38) / (p.b_sn * 2));
@@ -742,9 +758,10 @@ int launch_brgemm_generic(const GenericParams& p, int compute_tf32, cudaStream_t
     }
     const uint64_t db[2] = {static_cast<uint64_t>(p.b_sn), rows_b}, sb[2] = {1, static_cast<uint64_t>(p.b_sn)};
     const uint64_t da[2] = {static_cast<uint64_t>(p.a_sk), rows_a}, sa[2] = {1, static_cast<uint64_t>(p.a_sk)};
-    const uint32_t bb[2] = {64, static_cast<uint32_t>(q.nbox)}, ba[2] = {static_cast<uint32_t>(q.abox), 64};
-    if (encode_tmap(&q.map_bop, p.b_base, true, 2, db, sb, bb) == BRK_OK &&
-        encode_tmap(&q.map_aop, p.a_base, true, 2, da, sa, ba) == BRK_OK)
+    const uint32_t kb = sw64 ? 32 : 64;
+    const uint32_t bb[2] = {kb, static_cast<uint32_t>(q.nbox)}, ba[2] = {static_cast<uint32_t>(q.abox), kb};
+    if (encode_tmap(&q.map_bop, p.b_base, true, 2, db, sb, bb, false, nullptr, sw64) == BRK_OK &&
+        encode_tmap(&q.map_aop, p.a_base, true, 2, da, sa, ba, false, nullptr, sw64) == BRK_OK)
       q.tma = 1;
     q.all_tma = 0;
     if (q.tma && p.mode != kModeStride && !attach_box_check(q, rows_a, rows_b, stream)) q.tma = 0;

@@ -18,7 +18,8 @@ std::once_flag g_once;
 }  // namespace
 
 int encode_tmap(CUtensorMap* out, const void* ptr, bool bf16, int ndims, const uint64_t* dims,
-                const uint64_t* strides_elems, const uint32_t* box, bool atom32, const uint32_t* estrides) {
+                const uint64_t* strides_elems, const uint32_t* box, bool atom32, const uint32_t* estrides,
+                bool sw64) {
   std::call_once(g_once, [] {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -39,7 +40,8 @@ int encode_tmap(CUtensorMap* out, const void* ptr, bool bf16, int ndims, const u
   CUresult r = g_encode(out, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                         ndims, const_cast<void*>(ptr), gdim, gstride, bdim, estride,
                         CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        atom32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                        sw64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                             : (atom32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B),
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     char buf[256];

@@ -177,10 +177,12 @@ def test_addr_views_match_gather(m, n, k, batch, jobs):
                                               (40, 20, 24, 9, 150), (32, 128, 32, 3, 200), (32, 32, 32, 1, 999),
                                               (8, 8, 16, 64, 333)])
 def test_small_blocks_warp_stages_and_compact_ring(m, n, k, batch, jobs):
-    """Small blocks take the gather path with one warp per stage (and, for k <= 32 and one
-    64-column B atom, the compact 16-stage ring whose M = 128 MMAs read rows of the next
-    stages): stride and address variants bit-identical and equal to the fp64 oracle on
-    integer inputs, every job checked (a stage read from a wrong slot would show)."""
+    """Small blocks: m = k = 32 take 64B-swizzle TMA boxes (stride, offset), other small
+    shapes and the address variant the gather path with one warp per stage (and, for
+    k <= 32 and one 64-column B atom, the compact 16-stage ring); both compact layouts let
+    the M = 128 MMAs read rows of the next stages.  Stride, offset and address variants
+    bit-identical and equal to the fp64 oracle on integer inputs, every job checked (a
+    stage read from a wrong slot would show)."""
     lib = _lib.load()
     g = torch.Generator(device="cpu").manual_seed(7 * m + n + k + batch)
     a = ints(g, jobs, batch, k, m).cuda().bfloat16()
@@ -193,6 +195,17 @@ def test_small_blocks_warp_stages_and_compact_ring(m, n, k, batch, jobs):
     run_addr(lib, [a[j, i].data_ptr() for j in range(jobs) for i in range(batch)],
              [b[j, i].data_ptr() for j in range(jobs) for i in range(batch)], c2, jobs, m, n, k, batch, m, k)
     assert torch.equal(c, c2)
+    # offset variant (m = k = 32: 64B-swizzle boxes after the device box check)
+    ji = torch.arange(jobs, device="cuda")[:, None] * batch + torch.arange(batch, device="cuda")[None, :]
+    a_off = (ji * (k * m)).reshape(-1).contiguous()
+    b_off = (ji * (n * k)).reshape(-1).contiguous()
+    c_ptr = (c.data_ptr() + torch.arange(jobs, device="cuda") * (n * m * 4)).contiguous()
+    c3 = c.clone()
+    c.fill_(float("nan"))
+    _lib.check(lib.brk_brgemm_offs(a.data_ptr(), b.data_ptr(), a_off.data_ptr(), b_off.data_ptr(), c_ptr.data_ptr(),
+                                   jobs, m, n, k, batch, m, k, m, 1.0, 0.0, BF16, F32, CBF16, None))
+    torch.cuda.synchronize()
+    assert torch.equal(c, c3)
     ref = torch.einsum("jikm,jink->jnm", a.double(), b.double())  # exact for these integer inputs
     assert torch.equal(c.double(), ref)
     ref0 = orc.brgemm_reference(list(a[0].float().cpu().numpy()), list(b[0].float().cpu().numpy()),
