@@ -141,6 +141,25 @@ __device__ __forceinline__ bool entry_offs(const GenericParams& p, int job, int 
 //    accumulators so a tile's MMAs overlap the previous tile's epilogue;
 //  * warps 10-13 drain TMEM and apply alpha / beta / bias / act / mask.
 // Ring stages are sized by the tile (16 KB A + the B atoms actually used).
+// diagnostics build: stamps of CTA 0 — stage g < 64: [g*4 + 0] producer / gather issued,
+// [g*4 + 1] MMA saw it full, [g*4 + 2] MMAs issued; tile l < 16: [256 + l*4 + 0] MMA got the
+// accumulator, [+1] epilogue saw it done, [+2] epilogue released it
+#ifdef BRK_DIAG
+__device__ __forceinline__ unsigned long long gen_gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define GEN_TS(cond, idx)                                                     \
+  do {                                                                        \
+    if (p.ts != nullptr && blockIdx.x == 0 && (cond)) p.ts[idx] = gen_gtimer(); \
+  } while (0)
+#else
+#define GEN_TS(cond, idx) \
+  do {                    \
+  } while (0)
+#endif
+
 template <bool kTF32>
 __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __grid_constant__ GenericParams p) {
   constexpr int kE = kTF32 ? 4 : 8;              // elements per 16 B
@@ -302,14 +321,18 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
       const uint32_t idesc = make_idesc(kTF32 ? kFmtTF32 : kFmtBF16, kRows, n_cols, 0, b_mn ? 1 : 0);
       const int acc = local & acc_mask;
       mbar_wait(&drained[acc], ((local >> acc_shift) & 1) ^ 1);  // the epilogue read this accumulator
+      GEN_TS(local < 16 && lane == 0, 256 + local * 4 + 0);
       tc_fence_after();
       const uint32_t d_tmem = tmem + acc * acc_cols;
       const int g0 = local * steps;
       for (int s = 0; s < steps; ++s) {
         const int g = g0 + s, st = g & st_mask;
         mbar_wait(tf32_tma ? &rounded[st] : &full[st], (g >> st_shift) & 1);
+        GEN_TS(g < 64 && lane == 0, g * 4 + 1);
         tc_fence_after();
-        fence_proxy_async_smem();  // gathered / rounded stages were written through the generic proxy
+        // gathered / rounded stages were written through the generic proxy (TMA boxes land
+        // through the async proxy already: the fence cost ~0.1 us per stage on the serial issuer)
+        if (!boxes || tf32_tma) fence_proxy_async_smem();
         if (elect_one()) {
           // descriptors built once per launch and advanced by constants (16-byte units): the
           // issuer's per-stage work is on the serial path of every tile (small blocks: ~0.3 us
@@ -325,6 +348,7 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
           }
           mma_commit(&empty[st]);
           if (s == steps - 1) mma_commit(&done[acc]);
+          GEN_TS(g < 64, g * 4 + 2);
         }
         __syncwarp();
       }
@@ -369,6 +393,7 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
             const int k0 = ch * kKC, st = g & st_mask;
             if (g >= n_stages) mbar_wait(&empty[st], ((g >> st_shift) + 1) & 1);
             uint8_t* a_op = smem + st * stage_bytes;
+            GEN_TS(g < 64, g * 4 + 0);
             mbar_arrive_expect_tx(&full[st], bytes);
             const int32_t cA[2] = {eb.cb + k0, eb.rb + n0};
             tma_load<2>(a_op, &p.map_bop, &full[st], cA);
@@ -594,6 +619,7 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
       const int acc = local & acc_mask;
       if (steps > 0) {
         mbar_wait(&done[acc], (local >> acc_shift) & 1);
+        GEN_TS(local < 16 && threadIdx.x == kEpiWarp0 * 32, 256 + local * 4 + 1);
         tc_fence_after();
       }
       const int row = n0 + quarter * 32 + lane;
@@ -664,6 +690,7 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
       tc_fence_before();
       __syncwarp();
       if (steps > 0 && lane == 0) mbar_arrive(&drained[acc]);
+      GEN_TS(local < 16 && threadIdx.x == kEpiWarp0 * 32, 256 + local * 4 + 2);
     }
   }
   tc_fence_before();
@@ -734,6 +761,11 @@ int launch_brgemm_generic(const GenericParams& p, int compute_tf32, cudaStream_t
   GenericParams q = p;
   q.tma = 0;
   q.sw64 = 0;
+#ifdef BRK_DIAG
+  q.ts = g_debug_ts;
+#else
+  q.ts = nullptr;
+#endif
   // m = k = 32 blocks (64 B rows): 64B-swizzle boxes, one per operand and entry
   const bool sw64 = p.m == 32 && p.k == 32 && p.n <= kRows;
   const bool rows_ok = (p.n <= kRows || p.n % kRows == 0) && (p.m % kAtomColsBf16 == 0 || sw64);

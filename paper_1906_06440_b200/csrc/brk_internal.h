@@ -29,6 +29,8 @@ struct GenericParams {
   // m = k = 32 blocks: 64 B rows, 64B-swizzle boxes of 32 elements (A: 32 k x nbox rows,
   // B: 32 m x 32 k), compact stages, MMA N = 32
   int sw64;
+  // diagnostics build: CTA 0 stamps (%globaltimer) of its first 64 stages / 16 tiles, or null
+  unsigned long long* ts;
   // stride variant whose block starts all sit at column 0 of the views: every entry is one
   // box per operand at view row job * rj + i * rs (no per-entry division, no gather work)
   int all_tma;
