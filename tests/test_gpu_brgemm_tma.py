@@ -211,3 +211,21 @@ def test_small_blocks_warp_stages_and_compact_ring(m, n, k, batch, jobs):
     ref0 = orc.brgemm_reference(list(a[0].float().cpu().numpy()), list(b[0].float().cpu().numpy()),
                                 np.zeros((n, m), np.float32), 1.0, 0.0)
     assert np.array_equal(c[0].cpu().numpy(), ref0)
+
+
+@pytest.mark.parametrize("m,n,k,batch,jobs", [(16, 16, 32, 9, 300), (8, 16, 8, 5, 200), (32, 8, 64, 3, 150),
+                                              (16, 128, 16, 4, 100)])
+def test_small_blocks_tf32_gather(m, n, k, batch, jobs):
+    """fp32 blocks with TF32 MMAs on the gather path (converting loads; one warp per stage when
+    a stage is <= 4 copies per lane): exact on small-integer inputs, every job checked."""
+    lib = _lib.load()
+    g = torch.Generator(device="cpu").manual_seed(11 * m + n + k)
+    a = ints(g, jobs, batch, k, m).cuda()
+    b = ints(g, jobs, batch, n, k).cuda()
+    c = torch.full((jobs, n, m), float("nan"), device="cuda")
+    _lib.check(lib.brk_brgemm_stride(a.data_ptr(), b.data_ptr(), k * m, n * k, c.data_ptr(), jobs, batch * k * m,
+                                     batch * n * k, n * m, m, n, k, batch, m, k, m, 1.0, 0.0, F32, F32,
+                                     _lib.BRK_COMPUTE_TF32, None))
+    torch.cuda.synchronize()
+    ref = torch.einsum("jikm,jink->jnm", a.double(), b.double())
+    assert torch.equal(c.double(), ref)
