@@ -44,7 +44,10 @@ constexpr int kRingBytes = 4 * (kRows * 128 + kCols * 128);  // 192 KB of operan
 constexpr int kAtomColsBf16 = 64;  // bf16 elements per 128 B swizzle-atom row
 constexpr int kAOpBytes = kRows * 128;    // K-major, 128B swizzle: 128 rows x 128 B of K
 constexpr int kSmemBytes = kRingBytes + 1024 + 1024;
-constexpr int kMaxAcc = 8;  // TMEM accumulators (512 columns / the widest tile's columns)  // ring + alignment slack + barriers / TMEM slot
+constexpr int kMaxAcc = 8;
+#ifndef BRK_GATHER_GROUPS
+#define BRK_GATHER_GROUPS 1  // non-tiny gathered stages: two groups of four warps (0: all eight)
+#endif  // TMEM accumulators (512 columns / the widest tile's columns)  // ring + alignment slack + barriers / TMEM slot
 
 struct EntryPtrs {
   const char* a;
@@ -468,13 +471,21 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
       // no cross-warp barrier is paid per stage); with 8 ring stages a slot always has the
       // same warp, so its parity waits cannot alias.  Otherwise all 8 warps share each stage.
       const bool tiny = n_stages % kGatherWarps == 0 && a_units_t <= kUnits * 32 && b_units_t <= kUnits * 32;
-      const int ubase = tiny ? lane : gt, ustride = tiny ? 32 : kGatherWarps * 32;
+      // Mid-size stages: two groups of four warps, stage g by group g % 2 (two stages in flight,
+      // a 128-thread named barrier per group); with an even ring a slot keeps its group.
+      // (only when the group's unit tables hold the stage — m = 128 stages, 8 copies per thread
+      //  through the per-unit loops, measured 2.3 -> 3.5 us per stage as two groups)
+      const bool grouped = BRK_GATHER_GROUPS && !kTF32 && bf16_in && a_contig && b_contig &&
+                           a_units_t <= kUnits * 128 && b_units_t <= kUnits * 128;
+      const int gw = tiny ? 1 : (grouped ? 4 : kGatherWarps);  // warps per stage
+      const int n_groups = kGatherWarps / gw, grp = warp / gw;
+      const int ubase = (warp % gw) * 32 + lane, ustride = gw * 32;
       const bool tab = !kTF32 && bf16_in && a_contig && b_contig && a_units_t <= kUnits * ustride &&
                        b_units_t <= kUnits * ustride &&
                        static_cast<int64_t>(n0 + kRows) * p.b_sn + p.k + kKC < (1ll << 31) &&
                        static_cast<int64_t>(p.k + kKC) * p.a_sk + m0 + kCols < (1ll << 31);
       // (tiny: only a warp that owns one of the tile's stages builds them)
-      if (tab && (!tiny || steps >= kGatherWarps || ((warp - g0) & (kGatherWarps - 1)) < steps)) {
+      if (tab && (steps >= n_groups || ((grp - g0) & (n_groups - 1)) < steps)) {
 #pragma unroll
         for (int j = 0; j < kUnits; ++j) {
           const int u = ubase + j * ustride;
@@ -499,7 +510,7 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
       }
       // (this loop runs only when the launch gathers every entry, see `boxes`; tiny: the warp
       // visits only its own stages, g = warp mod 8)
-      const int s_first = tiny ? ((warp - g0) & (kGatherWarps - 1)) : 0, s_step = tiny ? kGatherWarps : 1;
+      const int s_first = (grp - g0) & (n_groups - 1), s_step = n_groups;
       for (int s = s_first; s < steps; s += s_step) {
         const int entry = n_chunks == 1 ? s : s / n_chunks;
         const int g = g0 + s, st = g & st_mask;
@@ -595,13 +606,12 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_generic_kernel(const __gri
         }  // per-unit loops
         fence_proxy_async_smem();   // this thread's st.shared -> the MMA's async-proxy reads
         cp_async_arrive(&full[st]);  // pending +1 now, -1 when this thread's copies land
-        if (tiny) {
+        if (gw == 1) {
           __syncwarp();
-          if (lane == 0) mbar_arrive(&full[st]);  // the stage's one expected arrival
         } else {
-          asm volatile("bar.sync 1, %0;" ::"r"(kGatherWarps * 32) : "memory");
-          if (gt == 0) mbar_arrive(&full[st]);
+          asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(gw * 32) : "memory");
         }
+        if (ubase == 0) mbar_arrive(&full[st]);  // the stage's one expected arrival
       }
     }
   } else {
